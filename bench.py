@@ -1,0 +1,347 @@
+"""bench.py -- SMC-with-data-annealing hot path on B200.
+
+A "step" is one SMC iteration (smc_step: fresh momenta, S+1 gradient
+evaluations of the annealed-window log target for every particle, leapfrog,
+incremental weights, normalise/ESS, resampling, gather) of BASELINE.json
+configs[1] (C2: MLP 784-200-10 ReLU, J = 1024, 60000 synthetic 28x28 k/255
+images with teacher labels, mini-batch 1000, +1 MB every 5 iterations,
+HMC S = 3, h = 0.002), run at the schedule's iterations k0 .. k0+W+K-1.
+
+metric = particle-sample grad evals/sec = sum_k J (S+1) M_k / time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU (torchrun): each rank runs its own C2 ensemble ("replicas", weak
+scaling) -- the sharded single-ensemble path is DESIGN.md §7.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # BASELINE.json configs[1]
+    "c2": dict(layers=[784, 200, 10], act="relu", n=60000, J=1024, feature_kind=1, mb=1000, period=5, K=300,
+               S=3, h=0.002, k0=150, cfg_id=2,
+               desc="C2: MLP 784-200-10 ReLU, J=1024 particles, n=60000 synthetic 28x28x1 k/255 teacher-labelled, "
+                    "MB=1000 (+1 MB every 5 iterations, 300 iterations), HMC S=3 h=0.002, prior N(0,1)"),
+    # BASELINE.json configs[0] (CPU-runnable case)
+    "c1": dict(layers=[64, 32, 10], act="tanh", n=2000, J=128, feature_kind=0, mb=100, period=1, K=50, S=3,
+               h=0.002, k0=0, cfg_id=1, ctr=(200, 40),
+               desc="C1: MLP 64-32-10 tanh, J=128, n=2000 U[0,1]^64 teacher-labelled, CTR 2 MB -> 20 MB at it 40"),
+}
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def window(w, k):
+    if "ctr" in w:
+        c0, sw = w["ctr"]
+        return c0 if k < sw else w["n"]
+    return min(w["mb"] * (1 + k // w["period"]), w["n"])
+
+
+def algorithmic_flops_per_row(layers):
+    """F_grad = 4 sum_l n_{l-1} n_l + 2 sum_{l>=2} n_{l-1} n_l per datapoint."""
+    pairs = [layers[i - 1] * layers[i] for i in range(1, len(layers))]
+    return 4 * sum(pairs) + 2 * sum(pairs[1:])
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.f = None
+
+    def __enter__(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for nm, v in zip(names, r[2:6]):
+                    if v.strip().lower() in ("active", "1"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    try:
+        return json.load(open(PEAKS_FILE))
+    except Exception:
+        return {}
+
+
+def make_data(w):
+    import paper_2601_21983_b200 as p
+    spec = p.NetSpec(w["layers"], w["act"])
+    X, y = p.make_teacher_data(spec, w["n"], w["feature_kind"], 0, w["cfg_id"], threads=os.cpu_count() or 8)
+    perm = p.shuffle_permutation(0, w["n"])  # runner.hpp:486-489 (seed 0)
+    return spec, np.ascontiguousarray(X[perm]), np.ascontiguousarray(y[perm])
+
+
+def cpu_sample(w, X, y, ks, threads, warm=False):
+    """The CPU oracle (fp64 restatement of the reference, OpenBLAS dgemm, parallel_for
+    over particles) on a bounded sample: one smc_step of `threads` particles per k."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    O.use_blas(True)
+    layers = w["layers"]
+    a = 0 if w["act"] == "relu" else 1
+    Jc = max(2, threads)
+    X64 = X.astype(np.float64)
+    th, lw = O.init_ensemble(layers, a, X64, y, (0, window(w, ks[0]), w["n"]), 0, 1.0, 1.0, 0, Jc, threads=threads)
+    units, secs = 0.0, 0.0
+    for k in ks:
+        M = window(w, k)
+        t0 = time.perf_counter()
+        th, lw, _, _, _ = O.smc_step(layers, a, X64, y, (0, M, w["n"]), 0, 1.0, 1.0, (w["h"], w["S"], 0), 0, 0.5, 1,
+                                     False, th, lw, k, threads=threads, dumps=False)
+        secs += time.perf_counter() - t0
+        units += Jc * (w["S"] + 1) * M
+    return units, secs, Jc
+
+
+def run_reference(args, w):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    spec, X, y = make_data(w)
+    threads = os.cpu_count() or 1
+    k0 = w["k0"]
+    if args.warmup:
+        cpu_sample(w, X, y, [k0 + i for i in range(min(args.warmup, 1))], threads)
+    ks = [k0 + args.warmup + i for i in range(args.steps)]
+    units, secs, Jc = cpu_sample(w, X, y, ks, threads)
+    v = units / secs
+    line = {"impl": "reference", "metric": "particle-sample grad evals/sec", "value": v,
+            "unit": "particle-sample grad evals/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w["desc"], "iterations": [ks[0], ks[-1]],
+                       "window_rows": [window(w, ks[0]), window(w, ks[-1])]},
+            "cpu_baseline": {"value": v, "unit": "particle-sample grad evals/s", "cores": threads, "kind": "port",
+                             "sample": f"one smc_step of {Jc} particles per step at the step's window "
+                                       f"(CPU oracle, fp64, OpenBLAS dgemm 1 thread x {threads} particle threads; "
+                                       "reference not buildable here: Eigen3 absent)"},
+            "e2e": {"value": v, "unit": "particle-sample grad evals/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, w):
+    import torch
+    import paper_2601_21983_b200 as p
+    from paper_2601_21983_b200 import _lib as L
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = p.load()
+    spec, X, y = make_data(w)
+    J, S, N = w["J"], w["S"], w["n"]
+    D = p.param_count(spec)
+    t = p.GpuEnsembleTarget(spec, X, y, J, device=local, precision=args.precision)
+    k0 = w["k0"]
+    ks_warm = [k0 + i for i in range(args.warmup)]
+    ks = [k0 + args.warmup + i for i in range(args.steps)]
+    Ms = [window(w, k) for k in ks]
+    L.check(lib.dasmc_gpu_reserve_rows(t.h, max(window(w, k) for k in ks_warm + ks + [k0])))
+    t.set_target(0, window(w, k0), N, "scaled", 1.0, 1.0)
+    t.init_ensemble(J, 0)
+    th0, lw0, _ = t.get_ensemble(J, dtype=np.float32)
+    t.set_ensemble(th0, lw0, k0)
+    kc = p.KernelConfig.hmc(w["h"], S)
+    rk = args.resample
+    for k in ks_warm:
+        t.set_target(0, window(w, k), N, "scaled", 1.0, 1.0)
+        t.smc_step(kc, 0, rk, 0.5, sync=False)
+    t.sync_records(0)
+    stream = torch.cuda.ExternalStream(lib.dasmc_gpu_stream(t.h))
+    L.check(lib.dasmc_gpu_set_timing(t.h, 1))
+    n_launch0 = lib.dasmc_launch_count()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for k in ks:
+            t.set_target(0, window(w, k), N, "scaled", 1.0, 1.0)
+            t.smc_step(kc, 0, rk, 0.5, sync=False)
+        e1.record(stream)
+        e1.synchronize()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = lib.dasmc_launch_count() - n_launch0
+    recs = t.sync_records(len(ks))
+    kms = np.zeros(3)
+    kcnt = np.zeros(3, dtype=np.int64)
+    L.check(lib.dasmc_gpu_kernel_times(t.h, kms.ctypes.data_as(L._D), kcnt.ctypes.data_as(L._I64)))
+    L.check(lib.dasmc_gpu_set_timing(t.h, 0))
+    units = float(sum(J * (S + 1) * M for M in Ms))
+    ms_max = ms
+    if dist:
+        tt = torch.tensor([ms, units], device="cuda", dtype=torch.float64)
+        mx = tt.clone()
+        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
+        ms_max, units_all = float(mx[0]), float(tt[1])
+    else:
+        units_all = units
+    value = units_all / (ms_max / 1e3)
+
+    # ---- e2e through the C-ABI with host (pinned) buffers, copies inside the timed region
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    th_h = torch.empty((J, D), dtype=torch.float32, pin_memory=True).numpy()
+    lw_h = torch.empty(J, dtype=torch.float64, pin_memory=True).numpy()
+    th_h[:] = th0
+    lw_h[:] = lw0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_units = 0.0
+    for i in range(e2e_steps):
+        k = ks[i]
+        t.set_ensemble(th_h, lw_h, k)  # H2D: theta (fp32, reference layout) + log-weights
+        t.set_target(0, window(w, k), N, "scaled", 1.0, 1.0)
+        t.smc_step(kc, 0, rk, 0.5, sync=True)
+        L.check(lib.dasmc_gpu_get_ensemble_f32(t.h, th_h.ctypes.data_as(L._F), lw_h.ctypes.data_as(L._D), None))
+        e2e_units += J * (S + 1) * window(w, k)
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        tt = torch.tensor([e2e_s, e2e_units], device="cuda", dtype=torch.float64)
+        mx = tt.clone()
+        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
+        e2e_s, e2e_units = float(mx[0]), float(tt[1])
+    e2e_value = e2e_units / e2e_s
+    step_bytes = J * D * 4 + J * 8
+
+    # ---- roofline of the dominant kernel (live CUDA-event timing on the context stream)
+    n0, n1 = w["layers"][0], w["layers"][1]
+    fl_fwd = sum(2.0 * M * n0 * n1 * J * (S + 1) for M in Ms)
+    fl_dw = sum(2.0 * M * n0 * n1 * J * (S + 1) for M in Ms)
+    kinds = [("layer-1 forward GEMM Z1 = X W1^T (+bias, ReLU epilogue)", fl_fwd, kms[0], kcnt[0]),
+             ("layer-1 weight-gradient GEMM dW1 = delta1^T X (+fused leapfrog epilogue)", fl_dw, kms[1], kcnt[1])]
+    name, fl, kt_ms, kc_n = max(kinds, key=lambda x: x[2])
+    peaks = load_peaks()
+    if args.precision == "fp32":
+        peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        peak_src = "nominal fp32 CUDA-core FMA peak (148 SMs x 128 lanes x 2 x 1965 MHz); not in MEASURED_PEAKS.json"
+    else:
+        bf16 = peaks.get("bf16_tflops", 1590.0)
+        peak = bf16 / 2.0
+        peak_src = f"dense tf32 = measured bf16 burst {bf16} TFLOP/s / 2 (MEASURED_PEAKS.json)"
+    achieved = fl / (kt_ms / 1e3) / 1e12 if kt_ms > 0 else None
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.precision)
+        except Exception:
+            traffic = None
+    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic, "kernel": name,
+            "launches": int(kc_n), "kernel_ms_total": float(kt_ms), "peak_source": peak_src,
+            "share_of_step": float(kt_ms / ms) if ms > 0 else None,
+            "eval_ms_total": float(kms[2])}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        cu, cs, Jc = cpu_sample(w, X, y, [ks[0]], threads)
+        cpu = {"value": cu / cs, "unit": "particle-sample grad evals/s", "cores": threads, "kind": "port",
+               "sample": f"one smc_step of {Jc} particles at window M={window(w, ks[0])} (CPU oracle fp64, "
+                         f"OpenBLAS dgemm, {threads} particle threads)"}
+    if rank == 0:
+        line = {"metric": "particle-sample grad evals/sec", "value": value, "unit": "particle-sample grad evals/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else args.precision,
+                "data": "synthetic (teacher-labelled, seeded; BASELINE.json configs[1] shapes)",
+                "config": {"workload": w["desc"], "particles_per_gpu": J, "iterations": [ks[0], ks[-1]],
+                           "window_rows": [Ms[0], Ms[-1]], "precision": args.precision, "resample": rk,
+                           "l2": "inputs larger than L2 (activations >= 24 GB per step)",
+                           "parallelism": f"{world} independent ensemble replica(s), one per GPU"},
+                "iterations_per_sec": args.steps / (ms_max / 1e3),
+                "particle_grad_evals_per_sec": world * J * (S + 1) * args.steps / (ms_max / 1e3),
+                "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof,
+                "e2e": {"value": e2e_value, "unit": "particle-sample grad evals/s",
+                        "h2d_bytes_per_step": step_bytes, "d2h_bytes_per_step": step_bytes + 64,
+                        "steps": e2e_steps},
+                "cpu_baseline": cpu,
+                "records_tail": [{k: r[k] for k in ("k", "ess", "resampled", "n_divergent")} for r in recs[-2:]]}
+        print(json.dumps(line), flush=True)
+    t.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "3xtf32"])
+    ap.add_argument("--resample", default="systematic", choices=["systematic", "multinomial"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    w = WORKLOADS[args.config]
+    if args.impl == "reference":
+        run_reference(args, w)
+    else:
+        run_ours(args, w)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,811 @@
+// C-ABI implementation and host driver of the B200 SMC hot path
+// (include/dasmc_gpu.h).  The driver owns the SMC loop (runner.hpp:581-604),
+// the annealing schedules and the SDA controller (annealing.hpp), and queues
+// every per-iteration kernel on one CUDA stream without host synchronisation
+// except where the reference's control flow needs a device result on the
+// host (SDA moments; a record the caller asked for).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ctx.cuh"
+#include "host.h"
+#include "tc_gemm.cuh"
+
+struct dasmc_ctx {
+  dasmc_b200::Ctx c;
+};
+
+namespace dasmc_b200 {
+
+namespace {
+thread_local std::string g_err;
+}
+void set_last_error(const std::string& m) { g_err = m; }
+
+namespace {
+
+struct InvalidArg : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct Dead : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return DASMC_OK;
+  } catch (const Dead& e) {
+    g_err = e.what();
+    return DASMC_EDEAD;
+  } catch (const CudaError& e) {
+    g_err = e.msg;
+    return DASMC_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DASMC_EINVAL;
+  }
+}
+
+int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+NetDev make_net(const dasmc_net_desc* d) {
+  if (d == nullptr || d->layer_sizes == nullptr) throw InvalidArg("net: null descriptor");
+  if (d->num_layers < 2) throw InvalidArg("NetSpec: need at least input and output layers");
+  if (d->num_layers - 1 > kMaxLayers) throw InvalidArg("NetSpec: too many layers for this build");
+  for (int i = 0; i < d->num_layers; ++i)
+    if (d->layer_sizes[i] < 1) throw InvalidArg("NetSpec: layer sizes must be >= 1");
+  if (d->activation != DASMC_RELU && d->activation != DASMC_TANH) throw InvalidArg("NetSpec: bad activation");
+  NetDev n{};
+  n.L = d->num_layers - 1;
+  n.act = d->activation;
+  for (int i = 0; i < d->num_layers; ++i) n.sizes[i] = d->layer_sizes[i];
+  int64_t ref = 0, off = 0;
+  for (int l = 0; l < n.L; ++l) {
+    LayerDev& ly = n.layer[l];
+    ly.in = n.sizes[l];
+    ly.out = n.sizes[l + 1];
+    ly.ref_off = ref;
+    ref += (int64_t)ly.in * ly.out + ly.out;
+    ly.woff = off;
+    off = align_up(off + (int64_t)ly.in * ly.out, 32);
+    ly.boff = off;
+    off = align_up(off + ly.out, 32);
+    ly.hidden = l + 1 < n.L ? 1 : 0;
+  }
+  n.D = ref;
+  n.Dp = align_up(off, 32);
+  return n;
+}
+
+void free_ctx(Ctx& c) {
+  cudaSetDevice(c.device);
+  if (c.stream) cudaStreamSynchronize(c.stream);
+  void* ptrs[] = {c.X, c.Xt, c.y, c.theta[0], c.theta[1], c.theta[2], c.p, c.grad, c.logw, c.dT, c.ll_part,
+                  c.th_part, c.p_part, c.p0_part, c.flags, c.lt_old, c.lt_new, c.ll_pre, c.ll_blk, c.wts, c.cdf,
+                  c.uni, c.idx, c.records, c.jump_tab, c.stage};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (int l = 0; l <= kMaxLayers; ++l)
+    if (c.act[l]) cudaFree(c.act[l]);
+  if (c.h_records) cudaFreeHost(c.h_records);
+  if (c.h_stage) cudaFreeHost(c.h_stage);
+  if (c.ev0) cudaEventDestroy(c.ev0);
+  if (c.ev1) cudaEventDestroy(c.ev1);
+  if (c.stream) cudaStreamDestroy(c.stream);
+}
+
+template <typename T>
+void dmalloc(T*& p, size_t count) {
+  CK(cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * std::max<size_t>(count, 1)));
+}
+
+void validate_target(const Ctx& c) {  // target.hpp:104-113
+  if (!(c.sigma > 0.0)) throw InvalidArg("PriorSpec: sigma must be > 0");
+  if (c.prefix_end < 0 || c.prefix_end > c.block_end || c.block_end > c.total_n)
+    throw InvalidArg("SubsetWindow: need 0 <= prefix_end <= block_end <= total_n");
+  if (c.block_end < 1) throw InvalidArg("TargetContext: empty subset");
+  if (c.block_end > c.n) throw InvalidArg("TargetContext: window exceeds dataset");
+  if (c.mode == DASMC_SDA && !(c.beta > 0.0 && c.beta <= 1.0))
+    throw InvalidArg("TargetContext: sda mode needs beta in (0, 1]");
+  if (c.mode != DASMC_SCALED && c.mode != DASMC_SDA) throw InvalidArg("TargetContext: bad mode");
+}
+
+void check_J(const Ctx& c, int64_t J) {
+  if (J < 1 || J > c.Jmax) throw InvalidArg("particle count out of range for this context");
+}
+
+// Window rows and their tempering for the current target: scaled mode puts
+// every row in the "prefix" with weight 1; SDA weights block rows by beta.
+void target_rows(const Ctx& c, int64_t& M, int64_t& P, double& beta_rows) {
+  M = c.block_end;
+  if (c.mode == DASMC_SCALED) {
+    P = M;
+    beta_rows = 1.0;
+  } else {
+    P = c.prefix_end;
+    beta_rows = c.beta;
+  }
+}
+
+EpiParams make_epi(Ctx& c, int mode, double h, const float* th_in, float* th_out) {
+  EpiParams e{};
+  e.mode = mode;
+  e.h = (float)h;
+  e.hh = (float)(0.5 * h);
+  e.inv_var = (float)(1.0 / (c.sigma * c.sigma));
+  e.scale = c.mode == DASMC_SCALED ? (float)((double)c.total_n / (double)c.block_end) : 1.0f;
+  e.theta_in = th_in;
+  e.theta_out = th_out;
+  e.p = c.p;
+  e.grad_out = c.grad;
+  e.flags = c.flags;
+  return e;
+}
+
+void upload(Ctx& c, void* dst, const void* src, size_t bytes) {
+  ensure_host_stage(c, bytes);
+  std::memcpy(c.h_stage, src, bytes);
+  CK(cudaMemcpyAsync(dst, c.h_stage, bytes, cudaMemcpyHostToDevice, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+}
+
+void download(Ctx& c, void* dst, const void* src, size_t bytes) {
+  ensure_host_stage(c, bytes);
+  CK(cudaMemcpyAsync(c.h_stage, src, bytes, cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  std::memcpy(dst, c.h_stage, bytes);
+}
+
+// One proposal + reweight + (conditional) resample of the whole ensemble
+// (smc.hpp:109-158).  Asynchronous: the record lands in c.records[slot].
+void smc_step_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind, double fraction, int always,
+                    int slot) {
+  if (!(kc.step_size > 0.0)) throw InvalidArg("KernelConfig: step_size must be > 0");
+  if (kc.leapfrog_steps < 1) throw InvalidArg("KernelConfig: leapfrog_steps must be >= 1");
+  if (kc.kind == DASMC_LANGEVIN && kc.leapfrog_steps != 1)
+    throw InvalidArg("KernelConfig: langevin requires leapfrog_steps == 1");
+  if (rkind != DASMC_MULTINOMIAL && rkind != DASMC_SYSTEMATIC) throw InvalidArg("bad resample kind");
+  if (!c.has_ensemble) throw InvalidArg("smc_step: no ensemble (call init_ensemble or set_ensemble)");
+  validate_target(c);
+  const int64_t J = c.J;
+  const int k = c.iteration;
+  const int S = kc.leapfrog_steps;
+  int64_t M, P;
+  double br;
+  target_rows(c, M, P, br);
+  launch_zero_ints(c, c.flags, J);
+  // fresh momenta p0 ~ N(0, I) from root.fork(kProposal, k, j) (smc.hpp:119-120; kernels.hpp:131)
+  launch_normals(c, seed, tag::kProposal, (uint64_t)k, J, 1.0f, c.p, c.p0_part);
+  const int t0 = c.start, t1 = (c.start + 1) % 3, t2 = (c.start + 2) % 3;
+  float* bufs[3] = {c.theta[t0], c.theta[t1], c.theta[t2]};
+  int in_idx = 0;
+  for (int s = 0; s <= S; ++s) {
+    const int out_idx = (s % 2 == 0) ? 1 : 2;
+    const int mode = s == 0 ? kEpiFirst : (s < S ? kEpiMid : kEpiLast);
+    EpiParams e = make_epi(c, mode, kc.step_size, bufs[in_idx], s < S ? bufs[out_idx] : nullptr);
+    launch_eval(c, bufs[in_idx], J, M, P, br, true, &e);
+    launch_eval_finalize(c, J, s == 0 ? c.lt_old : c.lt_new, nullptr, nullptr, M, true);
+    if (s < S) in_idx = out_idx;
+  }
+  launch_p_sumsq(c, J);
+  // resampling uniforms from root.fork(kResample, k) (smc.hpp:152)
+  launch_uniforms(c, fork_key(seed, tag::kResample, (uint64_t)k, 0), rkind == DASMC_MULTINOMIAL ? J : 1, c.uni);
+  launch_weights_and_resample(c, J, fraction, always, rkind, slot, k, 0.0);
+  const int end_idx = in_idx;                // theta_S
+  const int dst_idx = end_idx == 1 ? 2 : 1;  // the free trajectory buffer
+  launch_gather(c, bufs[0], bufs[end_idx], bufs[dst_idx], J);
+  c.start = dst_idx == 1 ? t1 : t2;
+  c.iteration = k + 1;  // smc.hpp:150, 154
+}
+
+dasmc_iter_record read_record(Ctx& c, int slot) {
+  const double* r = c.h_records + (size_t)slot * 8;
+  dasmc_iter_record o{};
+  o.k = (int)r[0];
+  o.ess = r[1];
+  o.resampled = (int)r[2];
+  o.mean_log_target = r[3];
+  o.n_divergent = (int)r[4];
+  o.beta = 1.0;
+  if (r[5] != 0.0) throw Dead("normalize: all particles dead (every log-weight is -inf)");
+  return o;
+}
+
+void fetch_records(Ctx& c, int first, int count) {
+  CK(cudaMemcpyAsync(c.h_records + (size_t)first * 8, c.records + (size_t)first * 8, sizeof(double) * 8 * count,
+                     cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+}
+
+// Unscaled prefix / block log-likelihoods of particles under window (P, M) (target.hpp:121-129).
+void loglik_parts_dev(Ctx& c, const float* theta, int64_t J, int64_t P, int64_t M) {
+  launch_eval(c, theta, J, M, P, 1.0, false, nullptr);
+  launch_eval_finalize(c, J, nullptr, c.ll_pre, c.ll_blk, M, false);
+}
+
+void sda_moments_dev(Ctx& c, int64_t P, int64_t M, double* out6) {  // annealing.hpp:153-174
+  if (P < 0 || P > M || M > c.n) throw InvalidArg("SubsetWindow: need 0 <= prefix_end <= block_end <= total_n");
+  if (M <= P) throw InvalidArg("sda_moments: window has no new block");
+  const int64_t J = c.J;
+  loglik_parts_dev(c, c.theta[c.start], J, P, M);
+  std::vector<double> pre((size_t)J), blk((size_t)J), lw((size_t)J);
+  download(c, pre.data(), c.ll_pre, sizeof(double) * J);
+  download(c, blk.data(), c.ll_blk, sizeof(double) * J);
+  download(c, lw.data(), c.logw, sizeof(double) * J);
+  for (int64_t j = 0; j < J; ++j) {
+    pre[(size_t)j] = -pre[(size_t)j];
+    blk[(size_t)j] = -blk[(size_t)j];
+  }
+  sda_moments_from(pre.data(), blk.data(), lw.data(), J, out6);
+}
+
+void init_ensemble_dev(Ctx& c, int64_t J, uint64_t seed) {  // smc.hpp:73-89
+  if (J < 2) throw InvalidArg("init_ensemble: need at least 2 particles");
+  check_J(c, J);
+  validate_target(c);
+  float* th = c.theta[c.start];
+  // theta_j = sigma * normal_vector(D) from root.fork(kInit, j) (network.hpp:235-239)
+  launch_normals(c, seed, tag::kInit, 0, J, (float)c.sigma, th, nullptr);
+  int64_t M, P;
+  double br;
+  target_rows(c, M, P, br);
+  loglik_parts_dev(c, th, J, P, M);
+  std::vector<double> pre((size_t)J), blk((size_t)J), lw((size_t)J);
+  download(c, pre.data(), c.ll_pre, sizeof(double) * J);
+  download(c, blk.data(), c.ll_blk, sizeof(double) * J);
+  const double scale = (double)c.total_n / (double)c.block_end;
+  for (int64_t j = 0; j < J; ++j)  // log_target - prior_logpdf (smc.hpp:85)
+    lw[(size_t)j] = c.mode == DASMC_SCALED ? scale * pre[(size_t)j] : pre[(size_t)j] + c.beta * blk[(size_t)j];
+  upload(c, c.logw, lw.data(), sizeof(double) * J);
+  c.J = J;
+  c.iteration = 0;
+  c.has_ensemble = true;
+}
+
+void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t* y, int64_t n, int Jmax,
+                int device, int precision) {
+  c.net = make_net(net);
+  if (n < 1) throw InvalidArg("dataset: n must be >= 1");
+  if (X == nullptr || y == nullptr) throw InvalidArg("dataset: null X or y");
+  if (Jmax < 2) throw InvalidArg("max_particles must be >= 2");
+  if (precision != DASMC_PREC_FP32 && precision != DASMC_PREC_TF32 && precision != DASMC_PREC_3XTF32)
+    throw InvalidArg("bad precision");
+  const int C = c.net.sizes[c.net.L];
+  for (int64_t i = 0; i < n; ++i)
+    if (y[i] < 0 || y[i] >= C) throw InvalidArg("loglik_batch: label out of range");
+  c.device = device;
+  c.precision = precision;
+  c.n = n;
+  c.Jmax = Jmax;
+  c.total_n = n;
+  c.block_end = n;
+  c.prefix_end = 0;
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&c.ev0));
+  CK(cudaEventCreate(&c.ev1));
+  const int n0 = c.net.sizes[0];
+  dmalloc(c.X, (size_t)n * n0);
+  dmalloc(c.y, (size_t)n);
+  CK(cudaMemcpy(c.X, X, sizeof(float) * (size_t)n * n0, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c.y, y, sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice));
+  const size_t pe = (size_t)Jmax * c.net.Dp;
+  for (auto& t : c.theta) {
+    dmalloc(t, pe);
+    CK(cudaMemset(t, 0, sizeof(float) * pe));
+  }
+  dmalloc(c.p, pe);
+  CK(cudaMemset(c.p, 0, sizeof(float) * pe));
+  dmalloc(c.logw, (size_t)Jmax);
+  c.th_slots = (int)((c.net.Dp + 8191) / 8192);
+  const int64_t nch_rng = (c.net.D + kRngChunkNormals - 1) / kRngChunkNormals;
+  c.rng_slots = (int)nch_rng;
+  dmalloc(c.th_part, (size_t)Jmax * c.th_slots);
+  dmalloc(c.p_part, (size_t)Jmax * c.th_slots);
+  dmalloc(c.p0_part, (size_t)Jmax * c.rng_slots);
+  dmalloc(c.flags, (size_t)Jmax);
+  CK(cudaMemset(c.flags, 0, sizeof(int) * Jmax));
+  dmalloc(c.lt_old, (size_t)Jmax);
+  dmalloc(c.lt_new, (size_t)Jmax);
+  dmalloc(c.ll_pre, (size_t)Jmax);
+  dmalloc(c.ll_blk, (size_t)Jmax);
+  dmalloc(c.wts, (size_t)Jmax);
+  dmalloc(c.cdf, (size_t)Jmax);
+  dmalloc(c.uni, (size_t)Jmax);
+  dmalloc(c.idx, (size_t)Jmax);
+  dmalloc(c.records, (size_t)kRecRing * 8);
+  CK(cudaMallocHost(reinterpret_cast<void**>(&c.h_records), sizeof(double) * kRecRing * 8));
+  const int64_t nch_uni = (Jmax + 2 * kRngChunkNormals - 1) / (2 * kRngChunkNormals);
+  c.jump_chunks = std::max(nch_rng, nch_uni) + 1;
+  const auto tab = jump_table(2 * kRngChunkNormals, c.jump_chunks);
+  dmalloc(c.jump_tab, (size_t)c.jump_chunks * 4);
+  CK(cudaMemcpy(c.jump_tab, tab.data(), sizeof(uint64_t) * 4 * tab.size(), cudaMemcpyHostToDevice));
+  if (precision != DASMC_PREC_FP32) {
+    if (!tc_layer1_eligible(c)) throw InvalidArg("tensor-core precision requested but the tcgen05 path is not eligible for this net");
+  }
+}
+
+}  // namespace
+}  // namespace dasmc_b200
+
+using namespace dasmc_b200;
+
+extern "C" {
+
+const char* dasmc_last_error(void) { return g_err.c_str(); }
+
+int dasmc_gpu_create(const dasmc_net_desc* net, const float* X, const int32_t* y, int64_t n, int max_particles,
+                     int device, int precision, dasmc_ctx** out) {
+  if (out == nullptr) {
+    g_err = "null out";
+    return DASMC_EINVAL;
+  }
+  *out = nullptr;
+  auto* h = new dasmc_ctx();
+  const int rc = guarded([&] { create_ctx(h->c, net, X, y, n, max_particles, device, precision); });
+  if (rc != DASMC_OK) {
+    free_ctx(h->c);
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return DASMC_OK;
+}
+
+int dasmc_gpu_destroy(dasmc_ctx* ctx) {
+  if (!ctx) return DASMC_OK;
+  free_ctx(ctx->c);
+  delete ctx;
+  return DASMC_OK;
+}
+
+int dasmc_gpu_param_count(const dasmc_ctx* ctx) { return ctx ? (int)ctx->c.net.D : -1; }
+
+int dasmc_gpu_set_target(dasmc_ctx* ctx, int64_t prefix_end, int64_t block_end, int64_t total_n, int mode,
+                         double beta, double sigma) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg("null ctx");
+    Ctx t = ctx->c;  // validate on a copy (no allocation happens)
+    t.prefix_end = prefix_end;
+    t.block_end = block_end;
+    t.total_n = total_n;
+    t.mode = mode;
+    t.beta = beta;
+    t.sigma = sigma;
+    validate_target(t);
+    Ctx& c = ctx->c;
+    c.prefix_end = prefix_end;
+    c.block_end = block_end;
+    c.total_n = total_n;
+    c.mode = mode;
+    c.beta = beta;
+    c.sigma = sigma;
+  });
+}
+
+int dasmc_gpu_value_and_grad(dasmc_ctx* ctx, const double* theta, int64_t J, double* values, double* grads) {
+  return guarded([&] {
+    if (!ctx || !theta || !values) throw InvalidArg("null argument");
+    Ctx& c = ctx->c;
+    check_J(c, J);
+    validate_target(c);
+    CK(cudaSetDevice(c.device));
+    const int spare = (c.start + 2) % 3;
+    ensure_stage(c, sizeof(double) * (size_t)J * c.net.D);
+    upload(c, c.stage, theta, sizeof(double) * (size_t)J * c.net.D);
+    launch_ref_to_internal_f64(c, (const double*)c.stage, c.theta[spare], J);
+    if (!c.grad) {
+      dmalloc(c.grad, (size_t)c.Jmax * c.net.Dp);
+      CK(cudaMemset(c.grad, 0, sizeof(float) * (size_t)c.Jmax * c.net.Dp));
+    }
+    int64_t M, P;
+    double br;
+    target_rows(c, M, P, br);
+    launch_zero_ints(c, c.flags, J);
+    EpiParams e = make_epi(c, kEpiStoreGrad, 1.0, c.theta[spare], nullptr);
+    launch_eval(c, c.theta[spare], J, M, P, br, grads != nullptr, &e);
+    launch_eval_finalize(c, J, c.lt_new, nullptr, nullptr, M, true);
+    download(c, values, c.lt_new, sizeof(double) * J);
+    if (grads) {
+      launch_internal_to_ref_f64(c, c.grad, (double*)c.stage, J);
+      download(c, grads, c.stage, sizeof(double) * (size_t)J * c.net.D);
+    }
+  });
+}
+
+int dasmc_gpu_loglik_parts(dasmc_ctx* ctx, const double* theta, int64_t J, double* prefix, double* block) {
+  return guarded([&] {
+    if (!ctx || !theta || !prefix || !block) throw InvalidArg("null argument");
+    Ctx& c = ctx->c;
+    check_J(c, J);
+    if (c.prefix_end < 0 || c.prefix_end > c.block_end || c.block_end > c.n)
+      throw InvalidArg("unscaled_loglik_parts: window exceeds dataset");
+    if (c.block_end < 1) throw InvalidArg("loglik_batch: empty batch");
+    CK(cudaSetDevice(c.device));
+    const int spare = (c.start + 2) % 3;
+    ensure_stage(c, sizeof(double) * (size_t)J * c.net.D);
+    upload(c, c.stage, theta, sizeof(double) * (size_t)J * c.net.D);
+    launch_ref_to_internal_f64(c, (const double*)c.stage, c.theta[spare], J);
+    loglik_parts_dev(c, c.theta[spare], J, c.prefix_end, c.block_end);
+    download(c, prefix, c.ll_pre, sizeof(double) * J);
+    download(c, block, c.ll_blk, sizeof(double) * J);
+  });
+}
+
+int dasmc_gpu_momentum(dasmc_ctx* ctx, uint64_t seed, int k, int64_t J, double* p0) {
+  return guarded([&] {
+    if (!ctx || !p0) throw InvalidArg("null argument");
+    Ctx& c = ctx->c;
+    check_J(c, J);
+    CK(cudaSetDevice(c.device));
+    launch_normals(c, seed, tag::kProposal, (uint64_t)k, J, 1.0f, c.p, c.p0_part);
+    ensure_stage(c, sizeof(double) * (size_t)J * c.net.D);
+    launch_internal_to_ref_f64(c, c.p, (double*)c.stage, J);
+    download(c, p0, c.stage, sizeof(double) * (size_t)J * c.net.D);
+  });
+}
+
+int dasmc_gpu_resample_indices(dasmc_ctx* ctx, const double* w, const double* u, int64_t J, int kind,
+                               int32_t* idx) {
+  return guarded([&] {
+    if (!ctx || !w || !u || !idx) throw InvalidArg("null argument");
+    Ctx& c = ctx->c;
+    check_J(c, J);
+    double s = 0.0;  // check_normalized_weights (numeric.hpp:38-47)
+    for (int64_t j = 0; j < J; ++j) {
+      if (!(w[j] >= 0.0)) throw InvalidArg("weights: entries must be >= 0");
+      s += w[j];
+    }
+    if (std::abs(s - 1.0) > 1e-9) throw InvalidArg("weights: must sum to 1");
+    CK(cudaSetDevice(c.device));
+    upload(c, c.wts, w, sizeof(double) * J);
+    upload(c, c.uni, u, sizeof(double) * (kind == DASMC_MULTINOMIAL ? J : 1));
+    launch_resample_hook(c, c.wts, c.uni, J, kind, c.idx);
+    download(c, idx, c.idx, sizeof(int32_t) * J);
+  });
+}
+
+int dasmc_gpu_init_ensemble(dasmc_ctx* ctx, int64_t J, uint64_t seed) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg("null ctx");
+    CK(cudaSetDevice(ctx->c.device));
+    init_ensemble_dev(ctx->c, J, seed);
+  });
+}
+
+int dasmc_gpu_set_ensemble(dasmc_ctx* ctx, const double* theta, const double* log_weights, int64_t J,
+                           int iteration) {
+  return guarded([&] {
+    if (!ctx || !theta || !log_weights) throw InvalidArg("null argument");
+    Ctx& c = ctx->c;
+    check_J(c, J);
+    if (J < 2) throw InvalidArg("ensemble needs at least 2 particles");
+    CK(cudaSetDevice(c.device));
+    ensure_stage(c, sizeof(double) * (size_t)J * c.net.D);
+    CK(cudaMemcpyAsync(c.stage, theta, sizeof(double) * (size_t)J * c.net.D, cudaMemcpyHostToDevice, c.stream));
+    launch_ref_to_internal_f64(c, (const double*)c.stage, c.theta[c.start], J);
+    CK(cudaMemcpyAsync(c.logw, log_weights, sizeof(double) * J, cudaMemcpyHostToDevice, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    c.J = J;
+    c.iteration = iteration;
+    c.has_ensemble = true;
+  });
+}
+
+int dasmc_gpu_set_ensemble_f32(dasmc_ctx* ctx, const float* theta, const double* log_weights, int64_t J,
+                               int iteration) {
+  return guarded([&] {
+    if (!ctx || !theta || !log_weights) throw InvalidArg("null argument");
+    Ctx& c = ctx->c;
+    check_J(c, J);
+    if (J < 2) throw InvalidArg("ensemble needs at least 2 particles");
+    CK(cudaSetDevice(c.device));
+    ensure_stage(c, sizeof(float) * (size_t)J * c.net.D);
+    CK(cudaMemcpyAsync(c.stage, theta, sizeof(float) * (size_t)J * c.net.D, cudaMemcpyHostToDevice, c.stream));
+    launch_ref_to_internal_f32(c, (const float*)c.stage, c.theta[c.start], J);
+    CK(cudaMemcpyAsync(c.logw, log_weights, sizeof(double) * J, cudaMemcpyHostToDevice, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    c.J = J;
+    c.iteration = iteration;
+    c.has_ensemble = true;
+  });
+}
+
+int dasmc_gpu_get_ensemble(dasmc_ctx* ctx, double* theta, double* log_weights, int* iteration) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg("null ctx");
+    Ctx& c = ctx->c;
+    if (!c.has_ensemble) throw InvalidArg("no ensemble");
+    CK(cudaSetDevice(c.device));
+    if (theta) {
+      ensure_stage(c, sizeof(double) * (size_t)c.J * c.net.D);
+      launch_internal_to_ref_f64(c, c.theta[c.start], (double*)c.stage, c.J);
+      CK(cudaMemcpyAsync(theta, c.stage, sizeof(double) * (size_t)c.J * c.net.D, cudaMemcpyDeviceToHost, c.stream));
+    }
+    if (log_weights) CK(cudaMemcpyAsync(log_weights, c.logw, sizeof(double) * c.J, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    if (iteration) *iteration = c.iteration;
+  });
+}
+
+int dasmc_gpu_get_ensemble_f32(dasmc_ctx* ctx, float* theta, double* log_weights, int* iteration) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg("null ctx");
+    Ctx& c = ctx->c;
+    if (!c.has_ensemble) throw InvalidArg("no ensemble");
+    CK(cudaSetDevice(c.device));
+    if (theta) {
+      ensure_stage(c, sizeof(float) * (size_t)c.J * c.net.D);
+      launch_internal_to_ref_f32(c, c.theta[c.start], (float*)c.stage, c.J);
+      CK(cudaMemcpyAsync(theta, c.stage, sizeof(float) * (size_t)c.J * c.net.D, cudaMemcpyDeviceToHost, c.stream));
+    }
+    if (log_weights) CK(cudaMemcpyAsync(log_weights, c.logw, sizeof(double) * c.J, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    if (iteration) *iteration = c.iteration;
+  });
+}
+
+int dasmc_gpu_smc_step(dasmc_ctx* ctx, const dasmc_kernel_cfg* cfg, uint64_t seed, int resample_kind,
+                       double fraction, int resample_always, dasmc_iter_record* record) {
+  return guarded([&] {
+    if (!ctx || !cfg) throw InvalidArg("null argument");
+    Ctx& c = ctx->c;
+    CK(cudaSetDevice(c.device));
+    if (!(fraction >= 0.0 && fraction <= 1.0)) throw InvalidArg("resample_fraction: must be in [0, 1]");
+    const int slot = c.rec_head % kRecRing;
+    CK(cudaEventRecord(c.ev0, c.stream));
+    smc_step_async(c, *cfg, seed, resample_kind, fraction, resample_always, slot);
+    CK(cudaEventRecord(c.ev1, c.stream));
+    ++c.rec_head;
+    if (record) {
+      fetch_records(c, slot, 1);
+      *record = read_record(c, slot);
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+      record->sampler_ms = ms;
+      record->batch = c.block_end;
+      record->beta = c.mode == DASMC_SDA ? c.beta : 1.0;
+    }
+  });
+}
+
+int dasmc_gpu_sync_records(dasmc_ctx* ctx, dasmc_iter_record* records, int count) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg("null ctx");
+    Ctx& c = ctx->c;
+    CK(cudaSetDevice(c.device));
+    if (count < 0 || count > c.rec_head || count > kRecRing) throw InvalidArg("record count out of range");
+    CK(cudaStreamSynchronize(c.stream));
+    if (count == 0 || records == nullptr) return;
+    CK(cudaMemcpy(c.h_records, c.records, sizeof(double) * 8 * kRecRing, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < count; ++i) {
+      const int slot = (c.rec_head - count + i) % kRecRing;
+      records[i] = read_record(c, slot);
+      records[i].batch = c.block_end;
+      records[i].beta = c.mode == DASMC_SDA ? c.beta : 1.0;
+    }
+  });
+}
+
+int dasmc_gpu_last_proposals(dasmc_ctx* ctx, double* p_final, double* log_target_new, double* log_target_old,
+                             int32_t* divergent, double* norm_weights, int32_t* indices) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg("null ctx");
+    Ctx& c = ctx->c;
+    const int64_t J = c.J;
+    CK(cudaSetDevice(c.device));
+    if (p_final) {
+      ensure_stage(c, sizeof(double) * (size_t)J * c.net.D);
+      launch_internal_to_ref_f64(c, c.p, (double*)c.stage, J);
+      download(c, p_final, c.stage, sizeof(double) * (size_t)J * c.net.D);
+    }
+    if (log_target_new) download(c, log_target_new, c.lt_new, sizeof(double) * J);
+    if (log_target_old) download(c, log_target_old, c.lt_old, sizeof(double) * J);
+    if (divergent) download(c, divergent, c.flags, sizeof(int32_t) * J);
+    if (norm_weights) download(c, norm_weights, c.wts, sizeof(double) * J);
+    if (indices) download(c, indices, c.idx, sizeof(int32_t) * J);
+  });
+}
+
+int dasmc_gpu_sda_moments(dasmc_ctx* ctx, int64_t prefix_end, int64_t block_end, double* out6) {
+  return guarded([&] {
+    if (!ctx || !out6) throw InvalidArg("null argument");
+    if (!ctx->c.has_ensemble) throw InvalidArg("no ensemble");
+    CK(cudaSetDevice(ctx->c.device));
+    sda_moments_dev(ctx->c, prefix_end, block_end, out6);
+  });
+}
+
+int64_t dasmc_batch_size(const dasmc_schedule* cfg, int k) {
+  int64_t out = -1;
+  const int rc = guarded([&] {
+    if (!cfg) throw InvalidArg("null schedule");
+    out = batch_size(*cfg, k);
+  });
+  return rc == DASMC_OK ? out : -1;
+}
+
+int dasmc_sda_init(const dasmc_schedule* cfg, double beta0, double entropy_step, dasmc_sda_state* out) {
+  return guarded([&] {
+    if (!cfg || !out) throw InvalidArg("null argument");
+    *out = sda_init(*cfg, beta0, entropy_step);
+  });
+}
+
+double dasmc_sda_beta_step(double beta, double* entropy_step, double denom) {
+  return sda_beta_step(beta, *entropy_step, denom);
+}
+
+int dasmc_sda_advance_with(const dasmc_schedule* cfg, dasmc_sda_state* state, const double* moments6) {
+  return guarded([&] {
+    if (!cfg || !state || !moments6) throw InvalidArg("null argument");
+    validate_schedule(*cfg);
+    *state = sda_advance_with(*cfg, *state, moments6);
+  });
+}
+
+int dasmc_sda_moments_from(const double* prefix_nll, const double* block_nll, const double* log_weights, int64_t J,
+                           double* out6) {
+  return guarded([&] {
+    if (!prefix_nll || !block_nll || !log_weights || !out6 || J < 1) throw InvalidArg("bad argument");
+    sda_moments_from(prefix_nll, block_nll, log_weights, J, out6);
+  });
+}
+
+int dasmc_make_teacher_data(const dasmc_net_desc* net, int64_t n, int feature_kind, uint64_t seed, uint64_t cfg_id,
+                            int threads, float* X, int32_t* y) {
+  return guarded([&] {
+    const NetDev nd = make_net(net);
+    if (n < 1 || !X || !y) throw InvalidArg("bad argument");
+    std::vector<int> layers(net->layer_sizes, net->layer_sizes + net->num_layers);
+    make_teacher_data(layers, nd.act, n, feature_kind, seed, cfg_id, threads, X, y);
+  });
+}
+
+int dasmc_shuffle_permutation(uint64_t seed, int64_t n, int64_t* perm) {
+  return guarded([&] {
+    if (n < 1 || !perm) throw InvalidArg("bad argument");
+    const auto p = shuffle_permutation(seed, n);
+    std::memcpy(perm, p.data(), sizeof(int64_t) * (size_t)n);
+  });
+}
+
+int dasmc_gpu_reserve_rows(dasmc_ctx* ctx, int64_t M) {
+  return guarded([&] {
+    if (!ctx || M < 1 || M > ctx->c.n) throw InvalidArg("reserve_rows: M out of range");
+    CK(cudaSetDevice(ctx->c.device));
+    ensure_activation_capacity(ctx->c, M);
+  });
+}
+
+void* dasmc_gpu_stream(dasmc_ctx* ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
+
+int64_t dasmc_launch_count(void) { return (int64_t)g_launch_count.load(); }
+
+int dasmc_gpu_set_timing(dasmc_ctx* ctx, int enable) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg("null ctx");
+    Ctx& c = ctx->c;
+    CK(cudaSetDevice(c.device));
+    harvest_timers(c);
+    for (int k = 0; k < kTimerKinds; ++k) {
+      c.kms[k] = 0.0;
+      c.kcount[k] = 0;
+    }
+    c.ktime = enable != 0;
+  });
+}
+
+int dasmc_gpu_kernel_times(dasmc_ctx* ctx, double* ms3, int64_t* count3) {
+  return guarded([&] {
+    if (!ctx || !ms3 || !count3) throw InvalidArg("null argument");
+    Ctx& c = ctx->c;
+    CK(cudaSetDevice(c.device));
+    harvest_timers(c);
+    for (int k = 0; k < kTimerKinds; ++k) {
+      ms3[k] = c.kms[k];
+      count3[k] = c.kcount[k];
+      c.kms[k] = 0.0;
+      c.kcount[k] = 0;
+    }
+  });
+}
+
+int dasmc_rng_skip(uint64_t key, uint64_t skip, int64_t count, uint64_t* out) {
+  return guarded([&] {
+    if (count < 0 || (count > 0 && !out)) throw InvalidArg("bad argument");
+    Xoshiro x;
+    x.seed(key);
+    if (skip > 0) {
+      const auto tab = jump_table(skip, 2);
+      x.jump(tab[1].data());
+    }
+    for (int64_t i = 0; i < count; ++i) out[i] = x.next();
+  });
+}
+
+int dasmc_gpu_run(const dasmc_net_desc* net, const float* X, const int32_t* y, int64_t n, const dasmc_run_cfg* cfg,
+                  int device, int precision, dasmc_iter_record* records, dasmc_sda_state* sda_trace,
+                  double* final_theta, double* final_log_weights) {
+  dasmc_ctx* ctx = nullptr;
+  int rc = guarded([&] {
+    if (!net || !X || !y || !cfg || !records) throw InvalidArg("null argument");
+    // shuffle once with root.fork(kPermutation) (runner.hpp:486-489)
+    const auto perm = shuffle_permutation(cfg->seed, n);
+    const int d = net->layer_sizes[0];
+    std::vector<float> Xs((size_t)n * d);
+    std::vector<int32_t> ys((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+      std::memcpy(Xs.data() + (size_t)i * d, X + (size_t)perm[(size_t)i] * d, sizeof(float) * d);
+      ys[(size_t)i] = y[perm[(size_t)i]];
+    }
+    const int rc2 = dasmc_gpu_create(net, Xs.data(), ys.data(), n, cfg->particles, device, precision, &ctx);
+    if (rc2 != DASMC_OK) throw std::runtime_error(g_err);
+    Ctx& c = ctx->c;
+    dasmc_schedule sched = cfg->schedule;  // runner.hpp:512-521
+    sched.iterations = cfg->iterations;
+    sched.dataset_size = n;
+    if (sched.initial_batch <= 0) sched.initial_batch = n;
+    sched.initial_batch = std::min<int64_t>(sched.initial_batch, n);
+    sched.increment = sched.increment > 0 ? std::min<int64_t>(sched.increment, n) : sched.initial_batch;
+    if (sched.period < 1) sched.period = 1;
+    validate_schedule(sched);
+    const bool sda = sched.kind == DASMC_SCHED_SDA;
+    dasmc_sda_state st{};
+    if (sda) st = sda_init(sched, cfg->beta0, cfg->entropy_step);
+    auto context_for = [&](int k) {  // runner.hpp:544-564
+      c.sigma = cfg->sigma;
+      c.total_n = n;
+      if (sda) {
+        c.mode = DASMC_SDA;
+        c.prefix_end = st.prefix_end;
+        c.block_end = st.block_end;
+        c.beta = st.beta;
+      } else {
+        c.mode = DASMC_SCALED;
+        c.prefix_end = 0;
+        c.block_end = batch_size(sched, k);
+        c.beta = 1.0;
+      }
+    };
+    context_for(0);
+    init_ensemble_dev(c, cfg->particles, cfg->seed);
+    for (int k = 0; k < cfg->iterations; ++k) {
+      const auto t0 = std::chrono::steady_clock::now();
+      context_for(k);
+      const int slot = c.rec_head % kRecRing;
+      smc_step_async(c, cfg->kernel, cfg->seed, cfg->resample_kind, cfg->resample_fraction, cfg->resample_always,
+                     slot);
+      ++c.rec_head;
+      fetch_records(c, slot, 1);
+      dasmc_iter_record r = read_record(c, slot);
+      r.batch = c.block_end;
+      r.beta = sda ? c.beta : 1.0;
+      if (sda && !st.terminal) {  // sda_advance on the post-step ensemble (runner.hpp:592)
+        double m6[6];
+        sda_moments_dev(c, st.prefix_end, st.block_end, m6);
+        st = sda_advance_with(sched, st, m6);
+      }
+      r.sampler_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      records[k] = r;
+      if (sda_trace) sda_trace[k] = st;
+    }
+    if (final_theta || final_log_weights) {
+      const int rc3 = dasmc_gpu_get_ensemble(ctx, final_theta, final_log_weights, nullptr);
+      if (rc3 != DASMC_OK) throw std::runtime_error(g_err);
+    }
+  });
+  if (ctx) dasmc_gpu_destroy(ctx);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,201 @@
+// Device context of the B200 SMC hot path: HBM layout, buffers, launch helpers.
+//
+// HBM layout:
+//  * X   [n x n0]            fp32 row-major, the run's shuffled order; window = rows [0, M)
+//  * Xt  [(n0+1) x n_pad]    fp32, X transposed plus an all-ones row (tensor-core dW1 operand)
+//  * y   [n]                 int32
+//  * theta[3] [Jmax x Dp]    fp32 particle-major; per layer W_l row-major [out][in]
+//                            (K-major for the forward GEMM) then b_l, each segment
+//                            16-byte aligned; the reference layout (W column-major)
+//                            is converted at the C-ABI boundary only.
+//                            Buffers rotate: start / trajectory / spare.
+//  * p   [Jmax x Dp]         fp32 momenta
+//  * act[l] [Jmax x Mcap x n_l] fp32 hidden activations, overwritten in place by
+//                            the backward deltas; act[L] holds logits -> delta_L
+//  * per-particle fp64 partial-sum slots, reduced in a fixed order (deterministic)
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/dasmc_gpu.h"
+
+namespace dasmc_b200 {
+
+struct CudaError {
+  std::string msg;
+};
+void cuda_check(cudaError_t e, const char* what);
+#define CK(x) ::dasmc_b200::cuda_check((x), #x)
+
+// Every kernel launch of the library is counted (bench.py's gpu_launches claim).
+extern std::atomic<long long> g_launch_count;
+#define LAUNCHED()                             \
+  do {                                         \
+    CK(cudaGetLastError());                    \
+    ::dasmc_b200::g_launch_count.fetch_add(1); \
+  } while (0)
+
+// Optional CUDA-event timing of kernel ranges on the context stream
+// (bench.py's live roofline): kind 0 = layer-1 forward GEMM, 1 = layer-1
+// weight-gradient GEMM (+ fused leapfrog), 2 = whole gradient evaluation.
+constexpr int kTimerKinds = 3;
+
+constexpr int kMaxLayers = 8;
+
+struct LayerDev {
+  int in, out;
+  int64_t woff, boff;  // internal offsets (floats) of W_l [out][in] and b_l
+  int64_t ref_off;     // reference offset of layer l's block (W column-major, then b)
+  int hidden;          // 1 if the activation applies after this layer
+};
+
+struct NetDev {
+  int L;  // number of weight layers
+  int act;
+  int sizes[kMaxLayers + 1];
+  LayerDev layer[kMaxLayers];
+  int64_t D;   // reference parameter count
+  int64_t Dp;  // internal padded particle stride (floats)
+};
+
+// Phases of the leapfrog epilogue fused into the gradient kernels
+// (kernels.hpp:85-96).
+enum EpiMode : int {
+  kEpiStoreGrad = 0,  // write the log-target gradient (parity hook)
+  kEpiFirst = 1,      // s = 0: p += h/2 g ; theta_out = theta + h p
+  kEpiMid = 2,        // 0 < s < S: p += h/2 g ; p += h/2 g ; theta_out = theta + h p
+  kEpiLast = 3,       // s = S: p += h/2 g
+  kEpiFirstLast = 4,  // S = 0 never happens; reserved
+};
+
+struct EpiParams {
+  int mode;
+  float h, hh;     // step size, half step
+  float inv_var;   // 1 / sigma^2
+  float scale;     // N/M (scaled) or 1 (sda)
+  const float* theta_in;
+  float* theta_out;
+  float* p;
+  float* grad_out;       // kEpiStoreGrad
+  double* th_part;       // [J][slots] sum theta_in^2
+  double* p_part;        // [J][slots] sum p_final^2 (kEpiLast only)
+  int* flags;            // [J] divergence flags
+  int slots;             // slots per particle
+};
+
+struct Ctx {
+  NetDev net;
+  int device = 0;
+  int precision = DASMC_PREC_FP32;
+  int64_t n = 0;
+  int Jmax = 0;
+  int64_t n_pad = 0;
+  cudaStream_t stream = nullptr;
+
+  // target
+  int64_t prefix_end = 0, block_end = 0, total_n = 0;
+  int mode = DASMC_SCALED;
+  double beta = 1.0, sigma = 1.0;
+
+  // data
+  float* X = nullptr;
+  float* Xt = nullptr;
+  int32_t* y = nullptr;
+
+  // ensemble
+  float* theta[3] = {nullptr, nullptr, nullptr};
+  int start = 0;  // index of the ensemble's current positions
+  float* p = nullptr;
+  float* grad = nullptr;  // parity hook only (lazy)
+  double* logw = nullptr;
+  int64_t J = 0;
+  int iteration = 0;
+  bool has_ensemble = false;
+
+  // activations
+  int64_t Mcap = 0;
+  float* act[kMaxLayers + 1] = {};
+  float* dT = nullptr;  // delta_1 transposed [J][n1][Mcap] (tensor-core dW1 operand)
+
+  // per-particle scratch
+  int ll_slots = 0, th_slots = 0, rng_slots = 0;
+  double* ll_part = nullptr;   // [J][ll_slots][2]
+  double* th_part = nullptr;   // [J][th_slots]
+  double* p_part = nullptr;    // [J][th_slots]
+  double* p0_part = nullptr;   // [J][rng_slots]
+  int* flags = nullptr;        // [J]
+  double* lt_old = nullptr;    // [J]
+  double* lt_new = nullptr;    // [J]
+  double* ll_pre = nullptr;    // [J] (forward-only passes)
+  double* ll_blk = nullptr;    // [J]
+  double* wts = nullptr;       // [J] normalised weights of the last step
+  double* cdf = nullptr;       // [J]
+  double* uni = nullptr;       // [J] resample uniforms
+  int32_t* idx = nullptr;      // [J]
+  double* records = nullptr;   // [kRecRing][8] device-side iteration records
+  double* h_records = nullptr; // pinned mirror
+  int rec_head = 0;            // number of queued records
+  uint64_t* jump_tab = nullptr;  // [nchunks][4]
+  int64_t jump_chunks = 0;
+
+  // staging
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  void* h_stage = nullptr;  // pinned
+  size_t h_stage_bytes = 0;
+
+  // events for sampler_ms
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  // kernel-range timers
+  bool ktime = false;
+  std::vector<cudaEvent_t> kev[kTimerKinds];
+  int kev_used[kTimerKinds] = {};
+  double kms[kTimerKinds] = {};
+  long long kcount[kTimerKinds] = {};
+};
+
+// Brackets a range of launches with an event pair when c.ktime is set.
+struct KTimer {
+  Ctx& c;
+  int kind;
+  KTimer(Ctx& cc, int k);
+  ~KTimer();
+};
+void harvest_timers(Ctx& c);
+
+constexpr int kRecRing = 4096;
+constexpr int kRngChunkNormals = 1024;  // normals per RNG thread (2048 xoshiro draws)
+
+// ---- launchers (kernels.cu) --------------------------------------------------------------
+void ensure_activation_capacity(Ctx& c, int64_t M);
+void ensure_stage(Ctx& c, size_t bytes);
+void ensure_host_stage(Ctx& c, size_t bytes);
+
+// One forward pass (+ optional backward with the fused epilogue) over window
+// rows [0, M), P = prefix_end, for particles [0, J) read from theta_in.
+void launch_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, double beta_rows,
+                 bool need_grad, const EpiParams* epi);
+// Reduce the per-particle slots of the last eval: values (fp64 log target),
+// optionally the unscaled prefix/block log-likelihoods.
+void launch_eval_finalize(Ctx& c, int64_t J, double* values_out, double* pre_out, double* blk_out, int64_t M,
+                          bool with_theta_norm);
+void launch_normals(Ctx& c, uint64_t key_root, uint64_t tag_a, uint64_t a2, int64_t J, float scale, float* dst,
+                    double* sq_part);
+void launch_ref_to_internal_f64(Ctx& c, const double* src, float* dst, int64_t J);
+void launch_ref_to_internal_f32(Ctx& c, const float* src, float* dst, int64_t J);
+void launch_internal_to_ref_f64(Ctx& c, const float* src, double* dst, int64_t J);
+void launch_internal_to_ref_f32(Ctx& c, const float* src, float* dst, int64_t J);
+void launch_zero_ints(Ctx& c, int* p, int64_t n);
+void launch_uniforms(Ctx& c, uint64_t key, int64_t count, double* dst);
+void launch_weights_and_resample(Ctx& c, int64_t J, double fraction, int always, int kind, int rec_slot,
+                                 int k, double log_target_const);
+void launch_gather(Ctx& c, const float* start, const float* end, float* dst, int64_t J);
+void launch_resample_hook(Ctx& c, const double* w, const double* u, int64_t J, int kind, int32_t* idx);
+
+}  // namespace dasmc_b200

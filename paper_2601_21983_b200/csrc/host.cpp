@@ -1,0 +1,322 @@
+// Host-side pieces of the B200 driver (see host.h).
+#include "host.h"
+
+#include <algorithm>
+#include <cmath>
+#include <stdexcept>
+#include <thread>
+
+namespace dasmc_b200 {
+
+uint64_t HostRng::uniform_below(uint64_t n) {  // rng.hpp:66-73
+  if (n == 0) throw std::invalid_argument("uniform_below: n must be positive");
+  const uint64_t limit = ~uint64_t{0} - (~uint64_t{0} % n);
+  uint64_t v = next_u64();
+  while (v >= limit) v = next_u64();
+  return v % n;
+}
+
+double HostRng::normal() {  // rng.hpp:76-81
+  const double u1 = 1.0 - uniform();
+  const double u2 = uniform();
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+}
+
+// ---- GF(2)[x] arithmetic for the jump-ahead ----------------------------------------------
+namespace {
+
+using Poly = std::array<uint64_t, 9>;  // up to 576 bits
+
+int poly_deg(const Poly& p) {
+  for (int w = 8; w >= 0; --w)
+    if (p[(size_t)w]) return w * 64 + 63 - __builtin_clzll(p[(size_t)w]);
+  return -1;
+}
+bool poly_bit(const Poly& p, int i) { return (p[(size_t)(i >> 6)] >> (i & 63)) & 1ULL; }
+void poly_flip(Poly& p, int i) { p[(size_t)(i >> 6)] ^= 1ULL << (i & 63); }
+
+Poly poly_mulmod(const Poly& a, const Poly& b, const Poly& m, int dm) {
+  Poly r{};
+  const int da = poly_deg(a);
+  for (int i = 0; i <= da; ++i) {
+    if (!poly_bit(a, i)) continue;
+    // r ^= b << i
+    const int ws = i >> 6, bs = i & 63;
+    for (int w = 8; w >= 0; --w) {
+      if (w - ws < 0) break;
+      uint64_t v = b[(size_t)(w - ws)] << bs;
+      if (bs && w - ws - 1 >= 0) v |= b[(size_t)(w - ws - 1)] >> (64 - bs);
+      r[(size_t)w] ^= v;
+    }
+  }
+  for (int d = poly_deg(r); d >= dm; d = poly_deg(r)) {
+    const int sh = d - dm;
+    const int ws = sh >> 6, bs = sh & 63;
+    for (int w = 8; w >= 0; --w) {
+      if (w - ws < 0) break;
+      uint64_t v = m[(size_t)(w - ws)] << bs;
+      if (bs && w - ws - 1 >= 0) v |= m[(size_t)(w - ws - 1)] >> (64 - bs);
+      r[(size_t)w] ^= v;
+    }
+  }
+  return r;
+}
+
+struct CharPoly {
+  Poly p{};
+  int deg = 0;
+};
+
+// Berlekamp-Massey on bit 0 of state word 0 gives the minimal polynomial of
+// the F2-linear state transition (degree 256: xoshiro256 has full period).
+const CharPoly& char_poly() {
+  static const CharPoly cp = [] {
+    Xoshiro x;
+    x.seed(0x1234567ULL);
+    const int N = 1024;
+    std::vector<int> s((size_t)N);
+    for (int t = 0; t < N; ++t) {
+      s[(size_t)t] = (int)(x.s[0] & 1ULL);
+      x.step();
+    }
+    std::vector<int> C((size_t)N + 1, 0), B((size_t)N + 1, 0), T;
+    C[0] = B[0] = 1;
+    int L = 0, m = 1;
+    for (int n = 0; n < N; ++n) {
+      int d = s[(size_t)n];
+      for (int i = 1; i <= L; ++i) d ^= C[(size_t)i] & s[(size_t)(n - i)];
+      if (d == 0) {
+        ++m;
+      } else if (2 * L <= n) {
+        T = C;
+        for (int i = 0; i + m <= N; ++i) C[(size_t)(i + m)] ^= B[(size_t)i];
+        L = n + 1 - L;
+        B = T;
+        m = 1;
+      } else {
+        for (int i = 0; i + m <= N; ++i) C[(size_t)(i + m)] ^= B[(size_t)i];
+        ++m;
+      }
+    }
+    if (L != 256) throw std::runtime_error("xoshiro char poly: unexpected degree");
+    CharPoly out;
+    out.deg = L;
+    // P(x) = x^L C(1/x): coefficient of x^(L-i) is C[i].
+    for (int i = 0; i <= L; ++i)
+      if (C[(size_t)i]) poly_flip(out.p, L - i);
+    return out;
+  }();
+  return cp;
+}
+
+std::array<uint64_t, 4> to4(const Poly& p) { return {p[0], p[1], p[2], p[3]}; }
+
+Poly x_pow_mod(uint64_t n) {  // x^n mod P by square-and-multiply
+  const CharPoly& cp = char_poly();
+  Poly result{};
+  result[0] = 1;
+  Poly base{};
+  base[0] = 2;  // x
+  while (n) {
+    if (n & 1ULL) result = poly_mulmod(result, base, cp.p, cp.deg);
+    base = poly_mulmod(base, base, cp.p, cp.deg);
+    n >>= 1;
+  }
+  return result;
+}
+
+}  // namespace
+
+const std::array<uint64_t, 4>& jump_poly_unit() {
+  static const std::array<uint64_t, 4> u = to4(x_pow_mod(1));
+  return u;
+}
+
+std::vector<std::array<uint64_t, 4>> jump_table(uint64_t chunk_steps, int64_t nchunks) {
+  const CharPoly& cp = char_poly();
+  std::vector<std::array<uint64_t, 4>> out((size_t)nchunks);
+  const Poly step = x_pow_mod(chunk_steps);
+  Poly cur{};
+  cur[0] = 1;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    out[(size_t)c] = to4(cur);
+    cur = poly_mulmod(cur, step, cp.p, cp.deg);
+  }
+  return out;
+}
+
+// ---- schedules (annealing.hpp:23-82) ------------------------------------------------------
+void validate_schedule(const dasmc_schedule& c) {
+  if (c.initial_batch < 1 || c.initial_batch > c.dataset_size)
+    throw std::invalid_argument("ScheduleConfig: need 1 <= initial_batch <= dataset_size");
+  if (c.increment < 1 || c.increment > c.dataset_size)
+    throw std::invalid_argument("ScheduleConfig: need 1 <= increment <= dataset_size");
+  if (c.iterations < 1) throw std::invalid_argument("ScheduleConfig: iterations must be >= 1");
+  if (c.period < 1) throw std::invalid_argument("ScheduleConfig: period must be >= 1");
+}
+
+int64_t batch_size(const dasmc_schedule& c, int k) {
+  validate_schedule(c);
+  if (k < 0 || k >= c.iterations) throw std::invalid_argument("batch_size: k out of range");
+  if (c.kind == DASMC_SCHED_SDA) throw std::invalid_argument("batch_size: the sda schedule is state-driven");
+  const double switch_point = 0.9 * (double)c.iterations;
+  const bool early = c.switch_iteration < 0 ? (double)k < switch_point : k < c.switch_iteration;
+  switch (c.kind) {
+    case DASMC_SCHED_CONSTANT: return c.initial_batch;
+    case DASMC_SCHED_FULL_BATCH: return c.dataset_size;
+    case DASMC_SCHED_CTR: return early ? c.initial_batch : c.dataset_size;
+    case DASMC_SCHED_LINEAR:
+      return early ? std::min(c.increment * (int64_t)(k / c.period) + c.initial_batch, c.dataset_size)
+                   : c.dataset_size;
+    case DASMC_SCHED_AUTOMATED: {
+      if (!early) return c.dataset_size;
+      const auto slope = (int64_t)std::floor((double)(c.dataset_size - c.initial_batch) / switch_point);
+      const int64_t raw = c.initial_batch + slope * k;
+      const int64_t rounded = (int64_t)std::floor((double)raw / (double)c.increment + 0.5) * c.increment;
+      return std::clamp(rounded, c.initial_batch, c.dataset_size);
+    }
+    default: break;
+  }
+  throw std::invalid_argument("batch_size: unknown schedule kind");
+}
+
+double sda_beta_step(double beta, double& step, double denom) {  // annealing.hpp:114-122
+  if (denom == 0.0) return 1.0;
+  double cand = beta - step / denom;
+  if (cand <= beta) {
+    step = -step;
+    cand = beta - step / denom;
+  }
+  return std::min(cand, 1.0);
+}
+
+std::vector<double> normalize(const double* lw, int64_t J) {  // smc.hpp:57-64
+  if (J < 1) throw std::invalid_argument("normalize: empty weights");
+  double m = lw[0];
+  for (int64_t j = 0; j < J; ++j) m = std::max(m, lw[j]);
+  if (m == -INFINITY) throw std::runtime_error("normalize: all particles dead (every log-weight is -inf)");
+  std::vector<double> w((size_t)J);
+  double s = 0.0;
+  for (int64_t j = 0; j < J; ++j) {
+    w[(size_t)j] = std::exp(lw[j] - m);
+    s += w[(size_t)j];
+  }
+  for (auto& v : w) v /= s;
+  return w;
+}
+
+// sda_moments's six estimators (annealing.hpp:166-173; numeric.hpp:49-78).
+void sda_moments_from(const double* pre, const double* blk, const double* lw, int64_t J, double* out6) {
+  const std::vector<double> w = normalize(lw, J);
+  double sum = 0.0;
+  for (double v : w) sum += v;
+  if (std::abs(sum - 1.0) > 1e-9) throw std::invalid_argument("weights: must sum to 1");
+  double mb = 0, mbsq = 0, mp = 0, mprod = 0;
+  for (int64_t j = 0; j < J; ++j) mb += w[(size_t)j] * blk[j];
+  for (int64_t j = 0; j < J; ++j) mbsq += w[(size_t)j] * (blk[j] * blk[j]);
+  const double var = std::max(0.0, mbsq - mb * mb);
+  for (int64_t j = 0; j < J; ++j) mp += w[(size_t)j] * pre[j];
+  for (int64_t j = 0; j < J; ++j) mprod += w[(size_t)j] * (pre[j] * blk[j]);
+  out6[0] = mb;
+  out6[1] = mbsq;
+  out6[2] = var;
+  out6[3] = mp;
+  out6[4] = mprod;
+  out6[5] = mprod - mp * mb;
+}
+
+dasmc_sda_state sda_init(const dasmc_schedule& c, double beta0, double entropy_step) {  // annealing.hpp:98-110
+  validate_schedule(c);
+  if (!(beta0 > 0.0 && beta0 <= 1.0)) throw std::invalid_argument("sda_init: beta0 must be in (0, 1]");
+  dasmc_sda_state s{};
+  s.beta = beta0;
+  s.beta_reset = beta0;
+  s.entropy_step = entropy_step;
+  s.prefix_end = 0;
+  s.block_end = c.initial_batch;
+  s.total_n = c.dataset_size;
+  s.stage = 0;
+  s.terminal = 0;
+  return s;
+}
+
+dasmc_sda_state sda_advance_with(const dasmc_schedule& c, const dasmc_sda_state& s, const double* m) {
+  if (s.terminal) return s;  // annealing.hpp:185
+  dasmc_sda_state n = s;
+  const double denom = s.stage == 0 ? m[2] : m[2] + m[5];
+  const double bnew = sda_beta_step(s.beta, n.entropy_step, denom);
+  if (bnew >= 1.0) {
+    const int64_t absorbed = s.block_end;
+    if (absorbed >= c.dataset_size) {
+      n.beta = 1.0;
+      n.prefix_end = n.block_end = n.total_n = c.dataset_size;
+      n.stage = 1;
+      n.terminal = 1;
+    } else {
+      n.beta = s.beta_reset;
+      n.prefix_end = absorbed;
+      n.block_end = std::min(absorbed + c.increment, c.dataset_size);
+      n.total_n = c.dataset_size;
+      n.stage = 1;
+    }
+  } else {
+    n.beta = bnew;
+  }
+  return n;
+}
+
+// ---- data ----------------------------------------------------------------------------------
+std::vector<int64_t> shuffle_permutation(uint64_t seed, int64_t n) {  // dataset.hpp:294-301
+  std::vector<int64_t> order((size_t)n);
+  for (int64_t i = 0; i < n; ++i) order[(size_t)i] = i;
+  HostRng r(fork_key(seed, tag::kPermutation, 0, 0));
+  for (int64_t i = n - 1; i > 0; --i) {
+    const auto j = (int64_t)r.uniform_below((uint64_t)(i + 1));
+    std::swap(order[(size_t)i], order[(size_t)j]);
+  }
+  return order;
+}
+
+void make_teacher_data(const std::vector<int>& layers, int act, int64_t n, int feature_kind, uint64_t seed,
+                       uint64_t cfg_id, int threads, float* X, int32_t* y) {
+  const int d = layers.front();
+  std::vector<double> F((size_t)n * d);
+  HostRng fx(fork_key(seed, tag::kSynthetic, cfg_id, 1));
+  for (auto& v : F) v = feature_kind == 0 ? fx.uniform() : (double)fx.uniform_below(256) / 255.0;
+  int64_t D = 0;
+  for (size_t l = 1; l < layers.size(); ++l) D += (int64_t)layers[l - 1] * layers[l] + layers[l];
+  HostRng ft(fork_key(seed, tag::kSynthetic, cfg_id, 2));
+  std::vector<double> th((size_t)D);
+  for (auto& v : th) v = ft.normal();
+  auto label_rows = [&](int64_t lo, int64_t hi) {
+    std::vector<double> cur, nxt;
+    for (int64_t i = lo; i < hi; ++i) {
+      cur.assign(F.begin() + i * d, F.begin() + (i + 1) * d);
+      int64_t off = 0;
+      for (size_t l = 1; l < layers.size(); ++l) {
+        const int in = layers[l - 1], out = layers[l];
+        nxt.assign((size_t)out, 0.0);
+        for (int r = 0; r < out; ++r) {
+          double acc = 0.0;
+          for (int c = 0; c < in; ++c) acc += th[(size_t)(off + (int64_t)c * out + r)] * cur[(size_t)c];
+          acc += th[(size_t)(off + (int64_t)in * out + r)];
+          if (l + 1 < layers.size()) acc = act == DASMC_RELU ? (acc > 0.0 ? acc : 0.0) : std::tanh(acc);
+          nxt[(size_t)r] = acc;
+        }
+        off += (int64_t)in * out + out;
+        cur.swap(nxt);
+      }
+      int best = 0;
+      for (int c = 1; c < (int)cur.size(); ++c)
+        if (cur[(size_t)c] > cur[(size_t)best]) best = c;
+      y[i] = best;
+    }
+  };
+  const int T = std::max(1, std::min<int>(threads, (int)std::max<int64_t>(1, n / 64)));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t) pool.emplace_back(label_rows, n * t / T, n * (t + 1) / T);
+  for (auto& p : pool) p.join();
+  for (size_t i = 0; i < F.size(); ++i) X[i] = (float)F[i];
+}
+
+}  // namespace dasmc_b200

@@ -1,0 +1,784 @@
+// CUDA-core (SIMT, fp32) kernels of the SMC hot path for sm_100a: batched
+// per-particle MLP forward / log-softmax / backward with the leapfrog move
+// fused into the weight-gradient epilogue, the parallel xoshiro256++ momentum
+// generator, the log-weight / normalise / ESS / resampling block and the
+// particle gather.  The tcgen05 tensor-core GEMMs (tc_gemm.cu) replace the
+// layer-1 contractions when the context's precision asks for them.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <stdexcept>
+
+#include "ctx.cuh"
+#include "host.h"
+#include "tc_gemm.cuh"
+
+namespace dasmc_b200 {
+
+std::atomic<long long> g_launch_count{0};
+
+KTimer::KTimer(Ctx& cc, int k) : c(cc), kind(k) {
+  if (!c.ktime || kind < 0) return;
+  auto& v = c.kev[kind];
+  while ((int)v.size() < 2 * (c.kev_used[kind] + 1)) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    v.push_back(e);
+  }
+  CK(cudaEventRecord(v[2 * c.kev_used[kind]], c.stream));
+}
+
+KTimer::~KTimer() {
+  if (!c.ktime || kind < 0) return;
+  cudaEventRecord(c.kev[kind][2 * c.kev_used[kind] + 1], c.stream);
+  ++c.kev_used[kind];
+}
+
+void harvest_timers(Ctx& c) {
+  CK(cudaStreamSynchronize(c.stream));
+  for (int k = 0; k < kTimerKinds; ++k) {
+    for (int i = 0; i < c.kev_used[k]; ++i) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c.kev[k][2 * i], c.kev[k][2 * i + 1]));
+      c.kms[k] += ms;
+      ++c.kcount[k];
+    }
+    c.kev_used[k] = 0;
+  }
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError{std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+namespace {
+
+constexpr double kLogTwoPi = 1.8378770664093455;
+
+__device__ __forceinline__ bool finitef(float v) { return isfinite(v); }
+
+// ---- reference <-> internal parameter index ------------------------------------------------
+// Reference layout of layer l (network.hpp:55-62): W(r, c) at ref_off + r + c*out, then b.
+// Internal: W row-major [out][in] at woff, b at boff.
+__device__ __forceinline__ int64_t internal_index(const NetDev& net, int64_t i) {
+  int l = 0;
+#pragma unroll 1
+  for (; l < net.L - 1; ++l)
+    if (i < net.layer[l + 1].ref_off) break;
+  const LayerDev& ly = net.layer[l];
+  const int64_t t = i - ly.ref_off;
+  const int64_t nw = (int64_t)ly.in * ly.out;
+  if (t < nw) {
+    const int64_t r = t % ly.out, c = t / ly.out;
+    return ly.woff + r * ly.in + c;
+  }
+  return ly.boff + (t - nw);
+}
+
+template <typename S, typename T>
+__global__ void ref_to_internal_kernel(NetDev net, const S* __restrict__ src, T* __restrict__ dst, int64_t J) {
+  const int64_t total = J * net.D;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / net.D, i = g - j * net.D;
+    dst[j * net.Dp + internal_index(net, i)] = (T)src[g];
+  }
+}
+
+template <typename S, typename T>
+__global__ void internal_to_ref_kernel(NetDev net, const S* __restrict__ src, T* __restrict__ dst, int64_t J) {
+  const int64_t total = J * net.D;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / net.D, i = g - j * net.D;
+    dst[g] = (T)src[j * net.Dp + internal_index(net, i)];
+  }
+}
+
+// ---- deterministic block reductions -------------------------------------------------------
+template <int NT>
+__device__ double block_sum(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NT / 32; ++i) t += sh[i];
+    sh[NT / 32] = t;
+  }
+  __syncthreads();
+  t = sh[NT / 32];
+  __syncthreads();
+  return t;
+}
+
+template <int NT>
+__device__ double block_max(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) sh[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = sh[0];
+    for (int i = 1; i < NT / 32; ++i) t = fmax(t, sh[i]);
+    sh[NT / 32] = t;
+  }
+  __syncthreads();
+  const double t = sh[NT / 32];
+  __syncthreads();
+  return t;
+}
+
+// ---- batched SIMT SGEMM with fused epilogues --------------------------------------------------
+// C(m, n) = sum_k A(m, k) B(n, k) for batch j = blockIdx.z.
+//   AK: A(m,k) = A[m*lda + k] (K-major) else A[k*lda + m];  same for BK / B.
+//   ones_col >= 0: B(ones_col, k) = 1 (bias-gradient column of the dW GEMM).
+// 64x64 block tile, 16-deep k slices double-buffered through shared memory,
+// 4x4 register micro-tile, two-level fp32 accumulation (partial sums are
+// folded every 256 k) to bound the rounding of long data reductions.
+constexpr int TB = 64, TK = 16;
+
+template <bool AK, bool BK, class Epi>
+__global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const float* __restrict__ A, int64_t lda,
+                                                    int64_t sA, const float* __restrict__ B, int64_t ldb,
+                                                    int64_t sB, int ones_col, Epi epi) {
+  __shared__ __align__(16) float As[2][TK][TB + 4];
+  __shared__ __align__(16) float Bs[2][TK][TB + 4];
+  const int j = blockIdx.z;
+  const int m0 = blockIdx.y * TB, n0 = blockIdx.x * TB;
+  A += (int64_t)j * sA;
+  B += (int64_t)j * sB;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+
+  float ra[4], rb[4];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int m, k;
+      if (AK) {
+        m = tid >> 2;
+        k = ((tid & 3) << 2) + q;
+      } else {
+        k = tid >> 4;
+        m = ((tid & 15) << 2) + q;
+      }
+      const int gm = m0 + m, gk = k0 + k;
+      ra[q] = (gm < M && gk < K) ? (AK ? A[(int64_t)gm * lda + gk] : A[(int64_t)gk * lda + gm]) : 0.f;
+      int n, kb;
+      if (BK) {
+        n = tid >> 2;
+        kb = ((tid & 3) << 2) + q;
+      } else {
+        kb = tid >> 4;
+        n = ((tid & 15) << 2) + q;
+      }
+      const int gn = n0 + n, gkb = k0 + kb;
+      float v = 0.f;
+      if (gkb < K && gn < N) {
+        if (gn == ones_col)
+          v = 1.f;
+        else
+          v = BK ? B[(int64_t)gn * ldb + gkb] : B[(int64_t)gkb * ldb + gn];
+      }
+      rb[q] = v;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (AK)
+        As[buf][((tid & 3) << 2) + q][tid >> 2] = ra[q];
+      else
+        As[buf][tid >> 4][((tid & 15) << 2) + q] = ra[q];
+      if (BK)
+        Bs[buf][((tid & 3) << 2) + q][tid >> 2] = rb[q];
+      else
+        Bs[buf][tid >> 4][((tid & 15) << 2) + q] = rb[q];
+    }
+  };
+
+  float acc[4][4], tot[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q] = tot[i][q] = 0.f;
+
+  const int nk = (K + TK - 1) / TK;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < nk) load((t + 1) * TK);
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] = fmaf(av[i], bv[q], acc[i][q]);
+    }
+    if ((t & 15) == 15) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          tot[i][q] += acc[i][q];
+          acc[i][q] = 0.f;
+        }
+    }
+    if (t + 1 < nk) store(buf ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int m = m0 + ty * 4 + i, n = n0 + tx * 4 + q;
+      if (m < M && n < N) epi(j, m, n, tot[i][q] + acc[i][q]);
+    }
+}
+
+// Forward epilogue: out = act(acc + b) (network.hpp:92-95).
+struct EpiFwd {
+  float* C;
+  int64_t ldc, sC;
+  const float* theta;
+  int64_t Dp, boff;
+  int hidden, act;
+  __device__ void operator()(int j, int m, int n, float v) const {
+    v += theta[(int64_t)j * Dp + boff + n];
+    if (hidden) v = act == DASMC_RELU ? fmaxf(v, 0.f) : tanhf(v);
+    C[(int64_t)j * sC + (int64_t)m * ldc + n] = v;
+  }
+};
+
+// Backward delta epilogue: delta_prev = acc * act'(a_prev), in place over a_prev
+// (network.hpp:209-215; relu' from the post-activation, tanh' = 1 - a^2).
+struct EpiDx {
+  float* D;
+  int64_t ldd, sD;
+  int act;
+  __device__ void operator()(int j, int m, int n, float v) const {
+    float* p = D + (int64_t)j * sD + (int64_t)m * ldd + n;
+    const float a = *p;
+    *p = act == DASMC_RELU ? v * (a > 0.f ? 1.f : 0.f) : v * (1.f - a * a);
+  }
+};
+
+// Weight-gradient epilogue with the leapfrog move fused (kernels.hpp:85-96).
+// (o, i) = (m, n); i == in is the bias column.  g = -theta/sigma^2 + scale*acc.
+struct EpiDw {
+  EpiParams e;
+  int64_t Dp, woff, boff;
+  int in;
+  __device__ void operator()(int j, int o, int i, float acc) const {
+    const int64_t idx = (int64_t)j * Dp + (i < in ? woff + (int64_t)o * in + i : boff + o);
+    const float th = e.theta_in[idx];
+    const float g = fmaf(e.scale, acc, -th * e.inv_var);
+    bool bad = !finitef(g);
+    if (e.mode == kEpiStoreGrad) {
+      e.grad_out[idx] = g;
+      return;
+    }
+    float p = e.p[idx];
+    p = fmaf(e.hh, g, p);
+    if (e.mode == kEpiMid) p = fmaf(e.hh, g, p);
+    bad |= !finitef(p);
+    e.p[idx] = p;
+    if (e.mode != kEpiLast) {
+      const float tn = fmaf(e.h, p, th);
+      bad |= !finitef(tn);
+      e.theta_out[idx] = tn;
+    }
+    if (bad) atomicOr(&e.flags[j], 1);
+  }
+};
+
+template <bool AK, bool BK, class Epi>
+void sgemm(cudaStream_t s, int M, int N, int K, const float* A, int64_t lda, int64_t sA, const float* B,
+           int64_t ldb, int64_t sB, int ones_col, int64_t J, const Epi& epi) {
+  if (M <= 0 || N <= 0 || J <= 0) return;
+  dim3 grid((N + TB - 1) / TB, (M + TB - 1) / TB, (unsigned)J);
+  sgemm_kernel<AK, BK, Epi><<<grid, 256, 0, s>>>(M, N, K, A, lda, sA, B, ldb, sB, ones_col, epi);
+  LAUNCHED();
+}
+
+// ---- log-softmax likelihood and output residual (network.hpp:180-193) --------------------------
+// One thread per window row; per-row arithmetic in fp64; per-block prefix and
+// block partial sums of the unscaled log-likelihood.  delta = w_row*(onehot - softmax)
+// with w_row = 1 on the prefix and beta_rows on the block (SDA tempering).
+constexpr int kRowsPerBlock = 128;
+
+__global__ void __launch_bounds__(kRowsPerBlock) softmax_kernel(float* __restrict__ logits, int64_t sL, int C,
+                                                              const int32_t* __restrict__ y, int64_t M, int64_t P,
+                                                              float beta_rows, int need_grad,
+                                                              double* __restrict__ ll_part, int slots) {
+  __shared__ double sh[kRowsPerBlock / 32 + 1];
+  const int j = blockIdx.y;
+  const int64_t m = (int64_t)blockIdx.x * kRowsPerBlock + threadIdx.x;
+  double pre = 0.0, blk = 0.0;
+  if (m < M) {
+    float* z = logits + (int64_t)j * sL + m * C;
+    const int yi = y[m];
+    double mx = (double)z[0];
+    for (int c = 1; c < C; ++c) mx = fmax(mx, (double)z[c]);
+    double den = 0.0;
+    for (int c = 0; c < C; ++c) den += exp((double)z[c] - mx);
+    const double ll = (double)z[yi] - (mx + log(den));
+    if (m < P)
+      pre = ll;
+    else
+      blk = ll;
+    if (need_grad) {
+      const float wr = m < P ? 1.f : beta_rows;
+      for (int c = 0; c < C; ++c) {
+        const double pr = exp((double)z[c] - mx) / den;
+        z[c] = wr * (float)((c == yi ? 1.0 : 0.0) - pr);
+      }
+    }
+  }
+  pre = block_sum<kRowsPerBlock>(pre, sh);
+  blk = block_sum<kRowsPerBlock>(blk, sh);
+  if (threadIdx.x == 0) {
+    double* o = ll_part + ((int64_t)j * slots + blockIdx.x) * 2;
+    o[0] = pre;
+    o[1] = blk;
+  }
+}
+
+// Sum of squares of a particle-major [J][Dp] fp32 array, per (particle, chunk).
+constexpr int kSqChunk = 8192;
+__global__ void __launch_bounds__(256) sumsq_kernel(const float* __restrict__ v, int64_t Dp, double* part,
+                                                   int slots) {
+  __shared__ double sh[256 / 32 + 1];
+  const int j = blockIdx.y;
+  const int64_t base = (int64_t)j * Dp + (int64_t)blockIdx.x * kSqChunk;
+  const int64_t lim = min((int64_t)kSqChunk, Dp - (int64_t)blockIdx.x * kSqChunk);
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < lim; i += 256) {
+    const double x = (double)v[base + i];
+    s += x * x;
+  }
+  s = block_sum<256>(s, sh);
+  if (threadIdx.x == 0) part[(int64_t)j * slots + blockIdx.x] = s;
+}
+
+// Per-particle log target from the slots (target.hpp:131-173 arithmetic in fp64).
+__global__ void eval_finalize_kernel(int64_t J, const double* __restrict__ ll_part, int ll_slots, int used_ll,
+                                     const double* __restrict__ th_part, int th_slots, int used_th, double D,
+                                     double var, int mode, double scale, double beta, double* values,
+                                     double* pre_out, double* blk_out, int* flags) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= J) return;
+  double llp = 0.0, llb = 0.0;
+  for (int s = 0; s < used_ll; ++s) {
+    llp += ll_part[(j * ll_slots + s) * 2];
+    llb += ll_part[(j * ll_slots + s) * 2 + 1];
+  }
+  if (pre_out) pre_out[j] = llp;
+  if (blk_out) blk_out[j] = llb;
+  if (values) {
+    double th2 = 0.0;
+    for (int s = 0; s < used_th; ++s) th2 += th_part[j * th_slots + s];
+    double v = -0.5 * D * (kLogTwoPi + log(var)) - th2 / (2.0 * var);  // network.hpp:221-227
+    if (mode == DASMC_SCALED)
+      v += scale * llp;
+    else
+      v += llp + beta * llb;
+    values[j] = v;
+    if (flags && !isfinite(v)) atomicOr(&flags[j], 1);
+  }
+}
+
+// ---- parallel xoshiro256++ normals ------------------------------------------------------------
+// Thread (j, c) draws the c-th chunk of kRngChunkNormals normals of stream
+// fork(a, b, c') by jumping c*2*kRngChunkNormals steps ahead (F2-linear jump
+// with host-precomputed polynomials).  Box-Muller in fp64 exactly as
+// rng.hpp:76-81; the value is stored in fp32 at its internal position.
+__global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b, int per_particle_c,
+                               int64_t J, int64_t nchunks, const uint64_t* __restrict__ jump_tab, float scale,
+                               float* __restrict__ dst, double* __restrict__ sq_part) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= J * nchunks) return;
+  const int64_t j = g / nchunks, c = g - j * nchunks;
+  // fork(kProposal, k, j) -> (a, b, j); fork(kInit, j) -> (a, j, 0)
+  const uint64_t key = per_particle_c ? fork_key(root, a, b, (uint64_t)j) : fork_key(root, a, (uint64_t)j, 0);
+  Xoshiro x;
+  x.seed(key);
+  if (c > 0) x.jump(jump_tab + 4 * c);
+  const int64_t lo = c * kRngChunkNormals, hi = min(net.D, lo + kRngChunkNormals);
+  double sq = 0.0;
+  float* out = dst + j * net.Dp;
+  for (int64_t i = lo; i < hi; ++i) {
+    const double u1 = 1.0 - x.uniform();
+    const double u2 = x.uniform();
+    const double nv = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+    const float v = (float)((double)scale * nv);
+    out[internal_index(net, i)] = v;
+    sq += (double)v * (double)v;
+  }
+  if (sq_part) sq_part[j * nchunks + c] = sq;
+}
+
+// `count` uniforms of one stream (resampling), chunked with the same jumps
+// (a chunk of kRngChunkNormals normals = 2*kRngChunkNormals draws).
+__global__ void uniforms_kernel(uint64_t key, int64_t count, const uint64_t* __restrict__ jump_tab,
+                                double* __restrict__ dst) {
+  const int64_t per = 2 * kRngChunkNormals;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c * per >= count) return;
+  Xoshiro x;
+  x.seed(key);
+  if (c > 0) x.jump(jump_tab + 4 * c);
+  const int64_t hi = min(count, (c + 1) * per);
+  for (int64_t i = c * per; i < hi; ++i) dst[i] = x.uniform();
+}
+
+// ---- weights / normalise / ESS / resample (smc.hpp:127-156) ---------------------------------------
+// Single 1024-thread block (J <= 65536).  Deterministic fixed-order reductions.
+constexpr int kWT = 1024;
+__global__ void __launch_bounds__(kWT) weights_kernel(int64_t J, double* __restrict__ logw,
+                                                      const double* __restrict__ lt_old,
+                                                      const double* __restrict__ lt_new,
+                                                      const double* __restrict__ p0_part, int p0_slots,
+                                                      const double* __restrict__ pS_part, int pS_slots,
+                                                      const int* __restrict__ flags, double* __restrict__ w,
+                                                      double* __restrict__ cdf, const double* __restrict__ uni,
+                                                      int32_t* __restrict__ idx, double fraction, int always,
+                                                      int kind, double* __restrict__ rec, int k) {
+  __shared__ double sh[kWT / 32 + 1];
+  __shared__ int s_res;
+  // 1) new log-weights (kernels.hpp:153-163, smc.hpp:127-138)
+  int ndiv = 0;
+  for (int64_t j = threadIdx.x; j < J; j += kWT) {
+    double lw;
+    if (flags[j]) {
+      lw = -CUDART_INF;
+      ++ndiv;
+    } else {
+      double p0 = 0.0, ps = 0.0;
+      for (int s = 0; s < p0_slots; ++s) p0 += p0_part[j * p0_slots + s];
+      for (int s = 0; s < pS_slots; ++s) ps += pS_part[j * pS_slots + s];
+      const double a = lt_new[j], b = lt_old[j];
+      const double inc = (isfinite(a) && isfinite(b) && isfinite(p0) && isfinite(ps))
+                             ? (a - b) + 0.5 * (p0 - ps)
+                             : -CUDART_INF;
+      lw = logw[j] + inc;
+    }
+    logw[j] = lw;
+  }
+  const double nd = block_sum<kWT>((double)ndiv, sh);
+  // 2) normalise (smc.hpp:57-64)
+  double mx = -CUDART_INF;
+  for (int64_t j = threadIdx.x; j < J; j += kWT) mx = fmax(mx, logw[j]);
+  mx = block_max<kWT>(mx, sh);
+  if (mx == -CUDART_INF) {  // all particles dead -> SamplerError
+    if (threadIdx.x == 0) {
+      rec[0] = k;
+      rec[1] = 0.0;
+      rec[2] = 0.0;
+      rec[3] = 0.0;
+      rec[4] = nd;
+      rec[5] = 1.0;
+    }
+    return;
+  }
+  double s = 0.0;
+  for (int64_t j = threadIdx.x; j < J; j += kWT) {
+    const double e = exp(logw[j] - mx);
+    w[j] = e;
+    s += e;
+  }
+  s = block_sum<kWT>(s, sh);
+  double s2 = 0.0, mlt = 0.0;
+  for (int64_t j = threadIdx.x; j < J; j += kWT) {
+    const double v = w[j] / s;
+    w[j] = v;
+    s2 += v * v;
+    if (v > 0.0) mlt += v * lt_new[j];  // smc.hpp:144-148
+  }
+  s2 = block_sum<kWT>(s2, sh);
+  mlt = block_sum<kWT>(mlt, sh);
+  const double ess = 1.0 / s2;  // smc.hpp:67-69
+  if (threadIdx.x == 0) {
+    s_res = (always || ess < fraction * (double)J) ? 1 : 0;  // smc.hpp:151
+    rec[0] = k;
+    rec[1] = ess;
+    rec[2] = s_res;
+    rec[3] = mlt;
+    rec[4] = nd;
+    rec[5] = 0.0;
+  }
+  __syncthreads();
+  if (!s_res) {
+    for (int64_t j = threadIdx.x; j < J; j += kWT) idx[j] = (int32_t)j;
+    return;
+  }
+  // 3) sequential fp64 CDF with last = 1.0 (numeric.hpp:87-94), then upper_bound.
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int64_t j = 0; j < J; ++j) {
+      acc += w[j];
+      cdf[j] = acc;
+    }
+    cdf[J - 1] = 1.0;
+  }
+  __syncthreads();
+  const double lj = -log((double)J);
+  for (int64_t j = threadIdx.x; j < J; j += kWT) {
+    const double u = kind == DASMC_MULTINOMIAL ? uni[j] : (uni[0] + (double)j) / (double)J;
+    int64_t lo = 0, hi = J;  // first index with cdf > u
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (cdf[mid] > u)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    idx[j] = (int32_t)lo;
+    logw[j] = lj;  // smc.hpp:100
+  }
+}
+
+// Bit-exact resampling hook: caller-provided normalised weights and uniforms.
+__global__ void __launch_bounds__(kWT) resample_hook_kernel(int64_t J, const double* __restrict__ w,
+                                                            double* __restrict__ cdf,
+                                                            const double* __restrict__ uni, int kind,
+                                                            int32_t* __restrict__ idx) {
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int64_t j = 0; j < J; ++j) {
+      acc += w[j];
+      cdf[j] = acc;
+    }
+    cdf[J - 1] = 1.0;
+  }
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < J; j += kWT) {
+    const double u = kind == DASMC_MULTINOMIAL ? uni[j] : (uni[0] + (double)j) / (double)J;
+    int64_t lo = 0, hi = J;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (cdf[mid] > u)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    idx[j] = (int32_t)lo;
+  }
+}
+
+// dst[j] = (flags[s] ? start : end)[s], s = idx[j]  (smc.hpp:97-99 + 129-131).
+// Vectorised 16-byte copies; grid (chunks, J).
+__global__ void __launch_bounds__(256) gather_kernel(const float4* __restrict__ start,
+                                                     const float4* __restrict__ end, float4* __restrict__ dst,
+                                                     int64_t Dp4, const int32_t* __restrict__ idx,
+                                                     const int* __restrict__ flags) {
+  const int64_t j = blockIdx.y;
+  const int32_t s = idx[j];
+  const float4* src = (flags[s] ? start : end) + (int64_t)s * Dp4;
+  float4* d = dst + j * Dp4;
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < Dp4; i += (int64_t)gridDim.x * 256) d[i] = src[i];
+}
+
+__global__ void zero_ints_kernel(int* p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0;
+}
+
+int grid_for(int64_t total, int threads = 256) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((total + threads - 1) / threads, 148 * 32));
+}
+
+}  // namespace
+
+// ---- host launchers ----------------------------------------------------------------------------
+void ensure_stage(Ctx& c, size_t bytes) {
+  if (bytes <= c.stage_bytes) return;
+  if (c.stage) CK(cudaFree(c.stage));
+  c.stage = nullptr;
+  CK(cudaMalloc(&c.stage, bytes));
+  c.stage_bytes = bytes;
+}
+
+void ensure_host_stage(Ctx& c, size_t bytes) {
+  if (bytes <= c.h_stage_bytes) return;
+  if (c.h_stage) CK(cudaFreeHost(c.h_stage));
+  c.h_stage = nullptr;
+  CK(cudaMallocHost(&c.h_stage, bytes));
+  c.h_stage_bytes = bytes;
+}
+
+void ensure_activation_capacity(Ctx& c, int64_t M) {
+  if (M <= c.Mcap) return;
+  CK(cudaStreamSynchronize(c.stream));
+  const int64_t Mnew = ((M + 127) / 128) * 128;
+  for (int l = 1; l <= c.net.L; ++l) {
+    if (c.act[l]) CK(cudaFree(c.act[l]));
+    c.act[l] = nullptr;
+    CK(cudaMalloc(&c.act[l], sizeof(float) * (size_t)c.Jmax * Mnew * c.net.sizes[l]));
+  }
+  if (c.dT) CK(cudaFree(c.dT));
+  c.dT = nullptr;
+  if (c.precision != DASMC_PREC_FP32)
+    CK(cudaMalloc(&c.dT, sizeof(float) * (size_t)c.Jmax * Mnew * c.net.sizes[1]));
+  const int slots = (int)((Mnew + kRowsPerBlock - 1) / kRowsPerBlock);
+  if (c.ll_part) CK(cudaFree(c.ll_part));
+  CK(cudaMalloc(&c.ll_part, sizeof(double) * 2 * (size_t)c.Jmax * slots));
+  c.ll_slots = slots;
+  c.Mcap = Mnew;
+}
+
+void launch_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, double beta_rows, bool need_grad,
+                 const EpiParams* epi) {
+  ensure_activation_capacity(c, M);
+  KTimer whole(c, need_grad ? 2 : -1);
+  const NetDev& net = c.net;
+  const int L = net.L;
+  const bool tc = c.precision != DASMC_PREC_FP32 && tc_layer1_eligible(c);
+  // forward (network.hpp:159-178)
+  for (int l = 1; l <= L; ++l) {
+    const LayerDev& ly = net.layer[l - 1];
+    EpiFwd e{c.act[l], ly.out, c.Mcap * ly.out, theta_in, net.Dp, ly.boff, ly.hidden, net.act};
+    KTimer kt(c, l == 1 ? 0 : -1);
+    if (l == 1 && tc) {
+      tc_forward_layer1(c, theta_in, J, M);
+    } else {
+      const float* A = l == 1 ? c.X : c.act[l - 1];
+      const int64_t sA = l == 1 ? 0 : c.Mcap * ly.in;
+      sgemm<true, true>(c.stream, (int)M, ly.out, ly.in, A, ly.in, sA, theta_in + ly.woff, ly.in, net.Dp, -1, J, e);
+    }
+  }
+  // log-softmax and residual
+  {
+    const int C = net.sizes[L];
+    dim3 grid((unsigned)((M + kRowsPerBlock - 1) / kRowsPerBlock), (unsigned)J);
+    softmax_kernel<<<grid, kRowsPerBlock, 0, c.stream>>>(c.act[L], c.Mcap * C, C, c.y, M, P, (float)beta_rows,
+                                                         need_grad ? 1 : 0, c.ll_part, c.ll_slots);
+    LAUNCHED();
+  }
+  // ||theta||^2 for the prior (network.hpp:226)
+  {
+    const int slots = (int)((net.Dp + kSqChunk - 1) / kSqChunk);
+    dim3 grid((unsigned)slots, (unsigned)J);
+    sumsq_kernel<<<grid, 256, 0, c.stream>>>(theta_in, net.Dp, c.th_part, c.th_slots);
+    LAUNCHED();
+  }
+  if (!need_grad) return;
+  // backward (network.hpp:195-217): dW_l first (epilogue reads theta_in, writes
+  // theta_out), then delta_{l-1} in place over a_{l-1}.
+  for (int l = L; l >= 1; --l) {
+    const LayerDev& ly = net.layer[l - 1];
+    EpiDw e{*epi, net.Dp, ly.woff, ly.boff, ly.in};
+    KTimer kt(c, l == 1 ? 1 : -1);
+    if (l == 1 && tc) {
+      tc_dw_layer1(c, J, M, *epi);
+    } else {
+      const float* Bp = l == 1 ? c.X : c.act[l - 1];
+      const int64_t sB = l == 1 ? 0 : c.Mcap * ly.in;
+      sgemm<false, false>(c.stream, ly.out, ly.in + 1, (int)M, c.act[l], ly.out, c.Mcap * ly.out, Bp, ly.in, sB,
+                          ly.in, J, e);
+    }
+    if (l > 1) {
+      const LayerDev& lp = net.layer[l - 2];
+      EpiDx d{c.act[l - 1], lp.out, c.Mcap * lp.out, net.act};
+      if (l == 2 && tc) {
+        tc_delta_layer1(c, theta_in, J, M);  // writes delta_1 in both layouts
+      } else {
+        sgemm<true, false>(c.stream, (int)M, ly.in, ly.out, c.act[l], ly.out, c.Mcap * ly.out, theta_in + ly.woff,
+                           ly.in, net.Dp, -1, J, d);
+      }
+    }
+  }
+}
+
+void launch_eval_finalize(Ctx& c, int64_t J, double* values_out, double* pre_out, double* blk_out, int64_t M,
+                          bool with_theta_norm) {
+  const int used_ll = (int)((M + kRowsPerBlock - 1) / kRowsPerBlock);
+  const int used_th = (int)((c.net.Dp + kSqChunk - 1) / kSqChunk);
+  const double scale = (double)c.total_n / (double)c.block_end;  // target.hpp:136-137
+  eval_finalize_kernel<<<(unsigned)((J + 127) / 128), 128, 0, c.stream>>>(
+      J, c.ll_part, c.ll_slots, used_ll, c.th_part, c.th_slots, with_theta_norm ? used_th : 0, (double)c.net.D,
+      c.sigma * c.sigma, c.mode, scale, c.beta, values_out, pre_out, blk_out, c.flags);
+  LAUNCHED();
+}
+
+void launch_normals(Ctx& c, uint64_t root, uint64_t a, uint64_t b, int64_t J, float scale, float* dst,
+                    double* sq_part) {
+  const int64_t nch = (c.net.D + kRngChunkNormals - 1) / kRngChunkNormals;
+  const int per_particle_c = a == tag::kProposal ? 1 : 0;
+  const int64_t total = J * nch;
+  normals_kernel<<<(unsigned)((total + 127) / 128), 128, 0, c.stream>>>(c.net, root, a, b, per_particle_c, J, nch,
+                                                                        c.jump_tab, scale, dst, sq_part);
+  LAUNCHED();
+}
+
+void launch_uniforms(Ctx& c, uint64_t key, int64_t count, double* dst) {
+  const int64_t per = 2 * kRngChunkNormals;
+  const int64_t nch = (count + per - 1) / per;
+  if (nch > c.jump_chunks) throw std::invalid_argument("uniforms: jump table too small");
+  uniforms_kernel<<<(unsigned)((nch + 63) / 64), 64, 0, c.stream>>>(key, count, c.jump_tab, dst);
+  LAUNCHED();
+}
+
+void launch_ref_to_internal_f64(Ctx& c, const double* src, float* dst, int64_t J) {
+  ref_to_internal_kernel<double, float><<<grid_for(J * c.net.D), 256, 0, c.stream>>>(c.net, src, dst, J);
+  LAUNCHED();
+}
+void launch_ref_to_internal_f32(Ctx& c, const float* src, float* dst, int64_t J) {
+  ref_to_internal_kernel<float, float><<<grid_for(J * c.net.D), 256, 0, c.stream>>>(c.net, src, dst, J);
+  LAUNCHED();
+}
+void launch_internal_to_ref_f64(Ctx& c, const float* src, double* dst, int64_t J) {
+  internal_to_ref_kernel<float, double><<<grid_for(J * c.net.D), 256, 0, c.stream>>>(c.net, src, dst, J);
+  LAUNCHED();
+}
+void launch_internal_to_ref_f32(Ctx& c, const float* src, float* dst, int64_t J) {
+  internal_to_ref_kernel<float, float><<<grid_for(J * c.net.D), 256, 0, c.stream>>>(c.net, src, dst, J);
+  LAUNCHED();
+}
+
+void launch_zero_ints(Ctx& c, int* p, int64_t n) {
+  zero_ints_kernel<<<grid_for(n), 256, 0, c.stream>>>(p, n);
+  LAUNCHED();
+}
+
+void launch_weights_and_resample(Ctx& c, int64_t J, double fraction, int always, int kind, int rec_slot, int k,
+                                 double) {
+  const int p0_slots = c.rng_slots;
+  const int pS_slots = (int)((c.net.Dp + kSqChunk - 1) / kSqChunk);
+  weights_kernel<<<1, kWT, 0, c.stream>>>(J, c.logw, c.lt_old, c.lt_new, c.p0_part, p0_slots, c.p_part, pS_slots,
+                                          c.flags, c.wts, c.cdf, c.uni, c.idx, fraction, always, kind,
+                                          c.records + (size_t)rec_slot * 8, k);
+  LAUNCHED();
+}
+
+void launch_p_sumsq(Ctx& c, int64_t J) {
+  const int slots = (int)((c.net.Dp + kSqChunk - 1) / kSqChunk);
+  dim3 grid((unsigned)slots, (unsigned)J);
+  sumsq_kernel<<<grid, 256, 0, c.stream>>>(c.p, c.net.Dp, c.p_part, slots);
+  LAUNCHED();
+}
+
+void launch_gather(Ctx& c, const float* start, const float* end, float* dst, int64_t J) {
+  const int64_t Dp4 = c.net.Dp / 4;
+  const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>((Dp4 + 255) / 256, 64));
+  dim3 grid((unsigned)chunks, (unsigned)J);
+  gather_kernel<<<grid, 256, 0, c.stream>>>(reinterpret_cast<const float4*>(start),
+                                            reinterpret_cast<const float4*>(end), reinterpret_cast<float4*>(dst),
+                                            Dp4, c.idx, c.flags);
+  LAUNCHED();
+}
+
+void launch_resample_hook(Ctx& c, const double* w, const double* u, int64_t J, int kind, int32_t* idx) {
+  resample_hook_kernel<<<1, kWT, 0, c.stream>>>(J, w, c.cdf, u, kind, idx);
+  LAUNCHED();
+}
+
+}  // namespace dasmc_b200
