@@ -150,8 +150,12 @@ def test_smc_step_matches_oracle(product, oracle, S):
     assert it1 == ito == 4
     assert rel(dump["log_target_old"], d["lt_old"]) < VAL_TOL
     assert rel(dump["log_target_new"], d["lt_new"]) < VAL_TOL
+    # p_S - p0 = (h/2) (g_0 + 2 g_1 + ... + g_S): the gradient content of the final momentum
+    hh = 0.5 * 0.002
     for j in range(32):
-        assert grad_err(dump["p_final"][j], d["pS"][j]) < GRAD_TOL
+        gsum, gsum_o = (dump["p_final"][j] - d["p0"][j]) / hh, (d["pS"][j] - d["p0"][j]) / hh
+        assert grad_err(gsum, gsum_o) < GRAD_TOL
+        assert np.linalg.norm(dump["p_final"][j] - d["pS"][j]) / np.linalg.norm(d["pS"][j]) < 1e-6
     np.testing.assert_allclose(rec["ess"], reco["ess"], rtol=1e-3)
     assert rec["resampled"] == reco["resampled"]
     if not rec["resampled"]:
