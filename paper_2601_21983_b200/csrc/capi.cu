@@ -89,6 +89,7 @@ NetDev make_net(const dasmc_net_desc* d) {
 void free_ctx(Ctx& c) {
   cudaSetDevice(c.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
+  tc_free(c);
   void* ptrs[] = {c.X, c.Xt, c.y, c.theta[0], c.theta[1], c.theta[2], c.p, c.grad, c.logw, c.dT, c.ll_part,
                   c.th_part, c.p_part, c.p0_part, c.flags, c.lt_old, c.lt_new, c.ll_pre, c.ll_blk, c.wts, c.cdf,
                   c.uni, c.idx, c.records, c.jump_tab, c.stage};
@@ -330,7 +331,10 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
   dmalloc(c.jump_tab, (size_t)c.jump_chunks * 4);
   CK(cudaMemcpy(c.jump_tab, tab.data(), sizeof(uint64_t) * 4 * tab.size(), cudaMemcpyHostToDevice));
   if (precision != DASMC_PREC_FP32) {
-    if (!tc_layer1_eligible(c)) throw InvalidArg("tensor-core precision requested but the tcgen05 path is not eligible for this net");
+    if (!tc_layer1_eligible(c))
+      throw InvalidArg("tensor-core precision needs a one-hidden-layer MLP with input % 4 == 0, hidden <= 256, "
+                       "classes <= 16 (use DASMC_PREC_FP32)");
+    tc_init(c);
   }
 }
 

@@ -152,6 +152,9 @@ struct Ctx {
   // events for sampler_ms
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
+  // tensor-core path state (tc_gemm.cu), null on the fp32 CUDA-core path
+  struct TcState* tc = nullptr;
+
   // kernel-range timers
   bool ktime = false;
   std::vector<cudaEvent_t> kev[kTimerKinds];

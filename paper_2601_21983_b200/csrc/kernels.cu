@@ -12,6 +12,7 @@
 #include <stdexcept>
 
 #include "ctx.cuh"
+#include "epi.cuh"
 #include "host.h"
 #include "tc_gemm.cuh"
 
@@ -279,24 +280,7 @@ struct EpiDw {
   int in;
   __device__ void operator()(int j, int o, int i, float acc) const {
     const int64_t idx = (int64_t)j * Dp + (i < in ? woff + (int64_t)o * in + i : boff + o);
-    const float th = e.theta_in[idx];
-    const float g = fmaf(e.scale, acc, -th * e.inv_var);
-    bool bad = !finitef(g);
-    if (e.mode == kEpiStoreGrad) {
-      e.grad_out[idx] = g;
-      return;
-    }
-    float p = e.p[idx];
-    p = fmaf(e.hh, g, p);
-    if (e.mode == kEpiMid) p = fmaf(e.hh, g, p);
-    bad |= !finitef(p);
-    e.p[idx] = p;
-    if (e.mode != kEpiLast) {
-      const float tn = fmaf(e.h, p, th);
-      bad |= !finitef(tn);
-      e.theta_out[idx] = tn;
-    }
-    if (bad) atomicOr(&e.flags[j], 1);
+    leapfrog_update(e, j, idx, acc);
   }
 };
 
@@ -619,15 +603,15 @@ void ensure_activation_capacity(Ctx& c, int64_t M) {
   if (M <= c.Mcap) return;
   CK(cudaStreamSynchronize(c.stream));
   const int64_t Mnew = ((M + 127) / 128) * 128;
-  for (int l = 1; l <= c.net.L; ++l) {
-    if (c.act[l]) CK(cudaFree(c.act[l]));
-    c.act[l] = nullptr;
-    CK(cudaMalloc(&c.act[l], sizeof(float) * (size_t)c.Jmax * Mnew * c.net.sizes[l]));
+  if (c.tc) {
+    tc_ensure_rows(c, Mnew);  // transposed activation / delta buffers of the tensor-core path
+  } else {
+    for (int l = 1; l <= c.net.L; ++l) {
+      if (c.act[l]) CK(cudaFree(c.act[l]));
+      c.act[l] = nullptr;
+      CK(cudaMalloc(&c.act[l], sizeof(float) * (size_t)c.Jmax * Mnew * c.net.sizes[l]));
+    }
   }
-  if (c.dT) CK(cudaFree(c.dT));
-  c.dT = nullptr;
-  if (c.precision != DASMC_PREC_FP32)
-    CK(cudaMalloc(&c.dT, sizeof(float) * (size_t)c.Jmax * Mnew * c.net.sizes[1]));
   const int slots = (int)((Mnew + kRowsPerBlock - 1) / kRowsPerBlock);
   if (c.ll_part) CK(cudaFree(c.ll_part));
   CK(cudaMalloc(&c.ll_part, sizeof(double) * 2 * (size_t)c.Jmax * slots));
@@ -641,19 +625,25 @@ void launch_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P,
   KTimer whole(c, need_grad ? 2 : -1);
   const NetDev& net = c.net;
   const int L = net.L;
-  const bool tc = c.precision != DASMC_PREC_FP32 && tc_layer1_eligible(c);
+  // ||theta||^2 for the prior (network.hpp:226), read before any epilogue writes theta_out
+  {
+    const int slots = (int)((net.Dp + kSqChunk - 1) / kSqChunk);
+    dim3 grid((unsigned)slots, (unsigned)J);
+    sumsq_kernel<<<grid, 256, 0, c.stream>>>(theta_in, net.Dp, c.th_part, c.th_slots);
+    LAUNCHED();
+  }
+  if (c.tc) {
+    tc_eval(c, theta_in, J, M, P, beta_rows, need_grad, epi);
+    return;
+  }
   // forward (network.hpp:159-178)
   for (int l = 1; l <= L; ++l) {
     const LayerDev& ly = net.layer[l - 1];
     EpiFwd e{c.act[l], ly.out, c.Mcap * ly.out, theta_in, net.Dp, ly.boff, ly.hidden, net.act};
-    KTimer kt(c, l == 1 ? 0 : -1);
-    if (l == 1 && tc) {
-      tc_forward_layer1(c, theta_in, J, M);
-    } else {
-      const float* A = l == 1 ? c.X : c.act[l - 1];
-      const int64_t sA = l == 1 ? 0 : c.Mcap * ly.in;
-      sgemm<true, true>(c.stream, (int)M, ly.out, ly.in, A, ly.in, sA, theta_in + ly.woff, ly.in, net.Dp, -1, J, e);
-    }
+    KTimer kt(c, l == 1 && need_grad ? 0 : -1);
+    const float* A = l == 1 ? c.X : c.act[l - 1];
+    const int64_t sA = l == 1 ? 0 : c.Mcap * ly.in;
+    sgemm<true, true>(c.stream, (int)M, ly.out, ly.in, A, ly.in, sA, theta_in + ly.woff, ly.in, net.Dp, -1, J, e);
   }
   // log-softmax and residual
   {
@@ -663,23 +653,14 @@ void launch_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P,
                                                          need_grad ? 1 : 0, c.ll_part, c.ll_slots);
     LAUNCHED();
   }
-  // ||theta||^2 for the prior (network.hpp:226)
-  {
-    const int slots = (int)((net.Dp + kSqChunk - 1) / kSqChunk);
-    dim3 grid((unsigned)slots, (unsigned)J);
-    sumsq_kernel<<<grid, 256, 0, c.stream>>>(theta_in, net.Dp, c.th_part, c.th_slots);
-    LAUNCHED();
-  }
   if (!need_grad) return;
   // backward (network.hpp:195-217): dW_l first (epilogue reads theta_in, writes
   // theta_out), then delta_{l-1} in place over a_{l-1}.
   for (int l = L; l >= 1; --l) {
     const LayerDev& ly = net.layer[l - 1];
-    EpiDw e{*epi, net.Dp, ly.woff, ly.boff, ly.in};
-    KTimer kt(c, l == 1 ? 1 : -1);
-    if (l == 1 && tc) {
-      tc_dw_layer1(c, J, M, *epi);
-    } else {
+    {
+      EpiDw e{*epi, net.Dp, ly.woff, ly.boff, ly.in};
+      KTimer kt(c, l == 1 ? 1 : -1);
       const float* Bp = l == 1 ? c.X : c.act[l - 1];
       const int64_t sB = l == 1 ? 0 : c.Mcap * ly.in;
       sgemm<false, false>(c.stream, ly.out, ly.in + 1, (int)M, c.act[l], ly.out, c.Mcap * ly.out, Bp, ly.in, sB,
@@ -688,12 +669,8 @@ void launch_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P,
     if (l > 1) {
       const LayerDev& lp = net.layer[l - 2];
       EpiDx d{c.act[l - 1], lp.out, c.Mcap * lp.out, net.act};
-      if (l == 2 && tc) {
-        tc_delta_layer1(c, theta_in, J, M);  // writes delta_1 in both layouts
-      } else {
-        sgemm<true, false>(c.stream, (int)M, ly.in, ly.out, c.act[l], ly.out, c.Mcap * ly.out, theta_in + ly.woff,
-                           ly.in, net.Dp, -1, J, d);
-      }
+      sgemm<true, false>(c.stream, (int)M, ly.in, ly.out, c.act[l], ly.out, c.Mcap * ly.out, theta_in + ly.woff,
+                         ly.in, net.Dp, -1, J, d);
     }
   }
 }

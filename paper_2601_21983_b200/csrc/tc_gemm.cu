@@ -1,14 +1,799 @@
-// Placeholder until the tcgen05 kernels land: the tensor-core path is not yet
-// eligible, so contexts created with a tensor-core precision fail loudly.
-#include <stdexcept>
+// tcgen05 / TMA / TMEM tensor-core kernels for sm_100a (see tc_gemm.cuh).
+//
+// One persistent, warp-specialised kernel template runs both GEMM shapes:
+//   warp 0      TMA producer: 128B-swizzled K-major tiles of A (128 x 32 fp32)
+//               and B (N x 32 fp32) into a STAGES-deep shared-memory ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32,
+//               M = 128, N <= 256, K = 8 per instruction), double-buffered
+//               128 x 256 fp32 accumulators in TMEM
+//   warps 2..5  epilogue: tcgen05.ld 32x32b rows -> registers -> fused math
+// mbarriers: full/empty per stage (TMA <-> MMA), tmem_full/tmem_empty per
+// accumulator (MMA <-> epilogue).  tcgen05.commit arrives on the mbarriers.
+#include <cuda.h>
+#include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "ctx.cuh"
+#include "epi.cuh"
 #include "tc_gemm.cuh"
 
 namespace dasmc_b200 {
 
-bool tc_layer1_eligible(const Ctx&) { return false; }
-void tc_forward_layer1(Ctx&, const float*, int64_t, int64_t) { throw std::runtime_error("tcgen05 path not built"); }
-void tc_delta_layer1(Ctx&, const float*, int64_t, int64_t) { throw std::runtime_error("tcgen05 path not built"); }
-void tc_dw_layer1(Ctx&, int64_t, int64_t, const EpiParams&) { throw std::runtime_error("tcgen05 path not built"); }
+struct TcState {
+  int n0 = 0, n1 = 0, C = 0;
+  int64_t n_pad = 0;     // X^T row stride (floats)
+  int64_t mcap = 0;      // row stride of the transposed activation buffers
+  bool split = false;    // split-tf32 (3 MMAs)
+  float* Xt = nullptr;   // [(n0+1) x n_pad], row n0 = 1
+  float* Xlo = nullptr;  // [n x n0]   (split)
+  float* Xtlo = nullptr; // [(n0+1) x n_pad] (split; ones row lo = 0)
+  float* W1hi = nullptr; // [J x n1 x n0] (split)
+  float* W1lo = nullptr;
+  float* a1T = nullptr;  // [J x (n1+1) x mcap], row n1 = 1
+  float* d1T = nullptr;  // [J x n1 x mcap]
+  float* d2T = nullptr;  // [J x C x mcap]
+  float* a1Tlo = nullptr;
+  float* d1Tlo = nullptr;
+  float* d2Tlo = nullptr;
+  int num_sms = 148;
+};
+
+namespace {
+
+constexpr int BM = 128;  // UMMA_M
+constexpr int BK = 32;   // fp32 per 128-byte swizzle row
+constexpr int kThreads = 192;
+constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
+constexpr int kEpiKindFwd = 0, kEpiKindDw = 1;
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.b32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Watchdog: a barrier that never completes (a protocol bug) traps after ~10 s
+// instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try(bar, parity))
+    if (clock64() - t0 > 20000000000LL) __trap();
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// 32 lanes x 32 bit, 16 consecutive columns per thread.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// K-major, 128B-swizzled UMMA shared-memory descriptor: 8-row core groups
+// 1024 B apart (SBO), LBO unused (1), version 1 (sm100), layout SWIZZLE_128B.
+__device__ __forceinline__ uint64_t smem_desc(const void* p) {
+  const uint64_t a = (smem_u32(p) >> 4) & 0x3FFFULL;
+  return a | (1ULL << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ULL << 46) | (2ULL << 61);
+}
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M = 128.
+__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// ---------------------------------------------------------------- parameters
+struct TileParams {
+  int rtiles;  // row tiles (of BM rows) per particle
+  int J;
+  int rg;      // row tiles per scheduling group
+  int nkb;     // k blocks of BK
+  int nmma;    // MMA N (multiple of 16, <= 256)
+  int brows;   // TMA box rows of B (valid rows)
+  int stages;
+  uint32_t stage_bytes_tx;
+};
+
+struct FwdParams {
+  const float* theta;  // theta_in
+  int64_t Dp, boff1, woff2, boff2;
+  int n1, C, act;
+  const int32_t* y;
+  int64_t M, P;
+  float beta_rows;
+  int need_grad;
+  int64_t ldm;  // row stride (floats) of the transposed buffers
+  float *a1T, *d1T, *d2T, *a1Tlo, *d1Tlo, *d2Tlo;
+  double* ll_part;
+  int ll_slots;
+};
+
+struct DwParams {
+  EpiParams e;
+  int64_t Dp, woff, boff;
+  int in;        // layer fan-in (row index `in` is the bias row)
+  int n_out;     // valid output columns
+};
+
+__device__ __forceinline__ void tile_coords(const TileParams& tp, int t, int& rt, int& j) {
+  const int gsz = tp.rg * tp.J;
+  const int g = t / gsz;
+  const int loc = t - g * gsz;
+  const int size_g = min(tp.rg, tp.rtiles - g * tp.rg);
+  j = loc / size_g;
+  rt = g * tp.rg + loc % size_g;
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int EPI, bool SPLIT, bool A3D>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
+              const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo, TileParams tp,
+              FwdParams fp, DwParams dp) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t a_bytes = BM * BK * 4;
+  const uint32_t b_bytes = (uint32_t)tp.nmma * BK * 4;
+  const uint32_t sub = SPLIT ? 2 : 1;
+  const uint32_t stage_bytes = sub * (a_bytes + b_bytes);
+  uint8_t* stages = smem;
+  uint64_t* bars = (uint64_t*)(smem + (size_t)tp.stages * stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + tp.stages;
+  uint64_t* tfull = bars + 2 * tp.stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = (uint32_t*)(tempty + 2);
+  float* epi_smem = (float*)(tmem_holder + 4);  // fused-forward parameters
+
+  auto A_of = [&](int s, int lo) { return stages + (size_t)s * stage_bytes + (lo ? a_bytes : 0); };
+  auto B_of = [&](int s, int lo) { return stages + (size_t)s * stage_bytes + sub * a_bytes + (lo ? b_bytes : 0); };
+
+  // zero the stage ring once: rows of B beyond the TMA box stay zero
+  for (uint32_t i = threadIdx.x; i < tp.stages * stage_bytes / 16; i += kThreads)
+    reinterpret_cast<uint4*>(stages)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&mapA);
+    prefetch_map(&mapB);
+    if (SPLIT) {
+      prefetch_map(&mapAlo);
+      prefetch_map(&mapBlo);
+    }
+    for (int s = 0; s < tp.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int ntiles = tp.rtiles * tp.J;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int rt, j;
+        tile_coords(tp, t, rt, j);
+        for (int kb = 0; kb < tp.nkb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], tp.stage_bytes_tx);
+          const int k0 = kb * BK;
+          if (A3D) {
+            tma_3d(A_of(s, 0), &mapA, &full[s], k0, rt * BM, j);
+            if (SPLIT) tma_3d(A_of(s, 1), &mapAlo, &full[s], k0, rt * BM, j);
+          } else {
+            tma_2d(A_of(s, 0), &mapA, &full[s], k0, rt * BM);
+            if (SPLIT) tma_2d(A_of(s, 1), &mapAlo, &full[s], k0, rt * BM);
+          }
+          tma_3d(B_of(s, 0), &mapB, &full[s], k0, 0, j);
+          if (SPLIT) tma_3d(B_of(s, 1), &mapBlo, &full[s], k0, 0, j);
+          if (++s == tp.stages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (one thread) =====================
+    if (lane == 0) {
+      const uint32_t idesc = idesc_tf32(tp.nmma);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * 256);
+        for (int kb = 0; kb < tp.nkb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t ad = smem_desc(A_of(s, 0)), bd = smem_desc(B_of(s, 0));
+          const uint64_t adl = smem_desc(A_of(s, 1)), bdl = smem_desc(B_of(s, 1));
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint64_t off = (uint64_t)(k * 32) >> 4;  // 32 bytes per K=8 step inside the swizzle row
+            tc_mma(d, ad + off, bd + off, idesc, (kb | k) != 0);
+            if (SPLIT) {
+              tc_mma(d, ad + off, bdl + off, idesc, 1);
+              tc_mma(d, adl + off, bd + off, idesc, 1);
+            }
+          }
+          tc_commit(&empty[s]);
+          if (++s == tp.stages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+      }
+    }
+  } else {
+    // ===================== epilogue warps 2..5 =====================
+    const int et = threadIdx.x - 64;              // 0..127
+    const int lane_base = (warp & 3) * 32;        // TMEM lanes this warp may access
+    const int row_in_tile = lane_base + lane;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int rt, j;
+      tile_coords(tp, t, rt, j);
+      if (EPI == kEpiKindFwd) {
+        // per-particle layer-2 parameters -> shared memory
+        const int n1 = fp.n1, C = fp.C;
+        float* W2s = epi_smem;        // [C][n1]
+        float* b1s = W2s + C * n1;    // [n1]
+        float* b2s = b1s + n1;        // [C]
+        double* red = (double*)(((uintptr_t)(b2s + C) + 15) & ~(uintptr_t)15);  // [2][4]
+        named_bar(1, 128);
+        const float* th = fp.theta + (int64_t)j * fp.Dp;
+        for (int i = et; i < C * n1; i += 128) W2s[i] = th[fp.woff2 + i];
+        for (int i = et; i < n1; i += 128) b1s[i] = th[fp.boff1 + i];
+        for (int i = et; i < C; i += 128) b2s[i] = th[fp.boff2 + i];
+        named_bar(1, 128);
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)lane_base << 16);
+        const int64_t m = (int64_t)rt * BM + row_in_tile;
+        const bool valid = m < fp.M;
+        const bool relu = fp.act == DASMC_RELU;
+        float z2[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) z2[c] = 0.f;
+        const int64_t ldm = fp.ldm;
+        float* a1T = fp.a1T + (int64_t)j * (n1 + 1) * ldm + m;
+        for (int o0 = 0; o0 < n1; o0 += 16) {
+          float v[16];
+          tmem_ld16(taddr + o0, v);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int o = o0 + q;
+            if (o < n1) {
+              float a = v[q] + b1s[o];
+              a = relu ? fmaxf(a, 0.f) : tanhf(a);
+#pragma unroll
+              for (int c = 0; c < 16; ++c)
+                if (c < C) z2[c] = fmaf(a, W2s[c * n1 + o], z2[c]);
+              if (valid && fp.need_grad) {
+                if (SPLIT) {
+                  const float hi = tf32_hi(a);
+                  a1T[(int64_t)o * ldm] = hi;
+                  fp.a1Tlo[(int64_t)j * (n1 + 1) * ldm + (int64_t)o * ldm + m] = a - hi;
+                } else {
+                  a1T[(int64_t)o * ldm] = a;
+                }
+              }
+            }
+          }
+        }
+        // log-softmax likelihood of the row in fp64 (network.hpp:183-193)
+        double ll = 0.0;
+        float d2[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) d2[c] = 0.f;
+        if (valid) {
+          const int yi = fp.y[m];
+          double mx = -1e300;
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (c < C) {
+              z2[c] += b2s[c];
+              mx = fmax(mx, (double)z2[c]);
+            }
+          double den = 0.0;
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (c < C) den += exp((double)z2[c] - mx);
+          double zy = 0.0;
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (c == yi) zy = (double)z2[c];
+          ll = zy - (mx + log(den));
+          if (fp.need_grad) {
+            const float wr = m < fp.P ? 1.f : fp.beta_rows;
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+              if (c < C) {
+                const double pr = exp((double)z2[c] - mx) / den;
+                d2[c] = wr * (float)((c == yi ? 1.0 : 0.0) - pr);
+                float* dst = fp.d2T + ((int64_t)j * C + c) * ldm + m;
+                if (SPLIT) {
+                  const float hi = tf32_hi(d2[c]);
+                  *dst = hi;
+                  fp.d2Tlo[((int64_t)j * C + c) * ldm + m] = d2[c] - hi;
+                } else {
+                  *dst = d2[c];
+                }
+              }
+          }
+        }
+        if (fp.need_grad) {
+          // delta1 = (W2^T delta2) . act'(a1)  (network.hpp:209-215)
+          float* d1T = fp.d1T + (int64_t)j * n1 * ldm + m;
+          for (int o0 = 0; o0 < n1; o0 += 16) {
+            float v[16];
+            tmem_ld16(taddr + o0, v);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const int o = o0 + q;
+              if (o < n1 && valid) {
+                float a = v[q] + b1s[o];
+                a = relu ? fmaxf(a, 0.f) : tanhf(a);
+                float dz = 0.f;
+#pragma unroll
+                for (int c = 0; c < 16; ++c)
+                  if (c < C) dz = fmaf(d2[c], W2s[c * n1 + o], dz);
+                const float d1 = relu ? dz * (a > 0.f ? 1.f : 0.f) : dz * (1.f - a * a);
+                if (SPLIT) {
+                  const float hi = tf32_hi(d1);
+                  d1T[(int64_t)o * ldm] = hi;
+                  fp.d1Tlo[(int64_t)j * n1 * ldm + (int64_t)o * ldm + m] = d1 - hi;
+                } else {
+                  d1T[(int64_t)o * ldm] = d1;
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        // per-tile prefix / block log-likelihood partials (deterministic order)
+        double pre = (valid && m < fp.P) ? ll : 0.0, blk = (valid && m >= fp.P) ? ll : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          pre += __shfl_xor_sync(0xffffffffu, pre, o);
+          blk += __shfl_xor_sync(0xffffffffu, blk, o);
+        }
+        if (lane == 0) {
+          red[(warp & 3) * 2] = pre;
+          red[(warp & 3) * 2 + 1] = blk;
+        }
+        named_bar(1, 128);
+        if (et == 0) {
+          double* o = fp.ll_part + ((int64_t)j * fp.ll_slots + rt) * 2;
+          o[0] = red[0] + red[2] + red[4] + red[6];
+          o[1] = red[1] + red[3] + red[5] + red[7];
+        }
+      } else {
+        // weight-gradient tile: row i of A (input index, `in` = bias row), columns o
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)lane_base << 16);
+        const int i = rt * BM + row_in_tile;
+        const bool valid = i <= dp.in;
+        const int64_t base = (int64_t)j * dp.Dp;
+        for (int o0 = 0; o0 < dp.n_out; o0 += 16) {
+          float v[16];
+          tmem_ld16(taddr + o0, v);
+          if (valid) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const int o = o0 + q;
+              if (o < dp.n_out) {
+                const int64_t idx = base + (i < dp.in ? dp.woff + (int64_t)o * dp.in + i : dp.boff + o);
+                leapfrog_update(dp.e, j, idx, v[q]);
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+      }
+      acc ^= 1;
+      if (acc == 0) aph ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- helper kernels
+// X^T with a ones row (and tf32 hi/lo splits): Xt[i][m] = X[m][i], Xt[n0][m] = 1.
+__global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n0, int64_t n_pad, float* Xt, float* Xtlo,
+                                   float* Xlo, int split) {
+  __shared__ float tile[32][33];
+  const int64_t m0 = (int64_t)blockIdx.x * 32;
+  const int i0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t m = m0 + r;
+    const int i = i0 + threadIdx.x;
+    float v = 0.f;
+    if (m < n && i < n0) v = X[m * n0 + i];
+    if (m < n && i == n0) v = 1.f;
+    if (split && m < n && i < n0) Xlo[m * n0 + i] = v - tf32_hi(v);
+    tile[r][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int i = i0 + r;
+    const int64_t m = m0 + threadIdx.x;
+    if (i <= n0 && m < n_pad) {
+      const float v = m < n ? tile[threadIdx.x][r] : 0.f;
+      if (split) {
+        const float hi = tf32_hi(v);
+        Xt[(int64_t)i * n_pad + m] = hi;
+        Xtlo[(int64_t)i * n_pad + m] = v - hi;
+      } else {
+        Xt[(int64_t)i * n_pad + m] = v;
+      }
+    }
+  }
+}
+
+__global__ void split_w1_kernel(const float* __restrict__ theta, int64_t Dp, int64_t woff, int64_t cnt, int64_t J,
+                                float* hi, float* lo) {
+  const int64_t total = J * cnt;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / cnt, r = g - j * cnt;
+    const float v = theta[j * Dp + woff + r];
+    const float h = tf32_hi(v);
+    hi[g] = h;
+    lo[g] = v - h;
+  }
+}
+
+__global__ void fill_ones_row_kernel(float* buf, int64_t J, int64_t rows, int64_t row, int64_t ldm, float v) {
+  const int64_t total = J * ldm;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / ldm, m = g - j * ldm;
+    buf[(j * rows + row) * ldm + m] = v;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// Driver entry point through the runtime (no -lcuda link dependency).
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p) throw CudaError{"cuTensorMapEncodeTiled unavailable"};
+    return (EncodeTiledFn)p;
+  }();
+  return fn;
+}
+
+// rank-2/3 fp32 tensor, innermost dim first; strides in bytes for dims >= 1.
+CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides, const uint32_t* box) {
+  CUtensorMap m;
+  uint32_t es[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base),
+                                 dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError{"cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+  return m;
+}
+
+CUtensorMap map2d(const float* base, uint64_t inner, uint64_t rows, uint64_t ld, uint32_t box_rows) {
+  const uint64_t dims[2] = {inner, rows};
+  const uint64_t strides[1] = {ld * 4};
+  const uint32_t box[2] = {BK, box_rows};
+  return make_map(base, 2, dims, strides, box);
+}
+
+CUtensorMap map3d(const float* base, uint64_t inner, uint64_t rows, uint64_t ld, uint64_t J, uint64_t pstride,
+                  uint32_t box_rows) {
+  const uint64_t dims[3] = {inner, rows, J};
+  const uint64_t strides[2] = {ld * 4, pstride * 4};
+  const uint32_t box[3] = {BK, box_rows, 1};
+  return make_map(base, 3, dims, strides, box);
+}
+
+int round16(int v) { return (v + 15) / 16 * 16; }
+
+template <int EPI, bool SPLIT, bool A3D>
+void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUtensorMap& B, const CUtensorMap& Blo,
+               TileParams tp, const FwdParams& fp, const DwParams& dp, size_t epi_smem_bytes) {
+  const uint32_t sub = SPLIT ? 2 : 1;
+  const size_t stage_bytes = sub * ((size_t)BM * BK * 4 + (size_t)tp.nmma * BK * 4);
+  const size_t fixed = 1024 + 64 * 8 + 64 + epi_smem_bytes;
+  const size_t budget = 227 * 1024;
+  int stages = (int)std::min<size_t>(6, (budget - fixed) / stage_bytes);
+  if (stages < 2) throw CudaError{"tensor-core tile does not fit in shared memory"};
+  tp.stages = stages;
+  tp.stage_bytes_tx = (uint32_t)(sub * ((size_t)BM * BK * 4 + (size_t)tp.brows * BK * 4));
+  const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16 + epi_smem_bytes + 64;
+  auto kern = tc_kernel<EPI, SPLIT, A3D>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget));
+    attr_set = true;
+  }
+  const int ntiles = tp.rtiles * tp.J;
+  const int grid = std::max(1, std::min(ntiles, c.tc->num_sms));
+  kern<<<grid, kThreads, smem, c.stream>>>(A, SPLIT ? Alo : A, B, SPLIT ? Blo : B, tp, fp, dp);
+  LAUNCHED();
+}
+
+}  // namespace
+
+bool tc_layer1_eligible(const Ctx& c) {
+  const NetDev& n = c.net;
+  return n.L == 2 && n.sizes[0] % 4 == 0 && n.sizes[0] >= 4 && n.sizes[1] <= 256 && n.sizes[2] <= 16;
+}
+
+void tc_init(Ctx& c) {
+  auto* s = new TcState();
+  c.tc = s;
+  s->n0 = c.net.sizes[0];
+  s->n1 = c.net.sizes[1];
+  s->C = c.net.sizes[2];
+  s->split = c.precision == DASMC_PREC_3XTF32;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, dev));
+  s->n_pad = (c.n + 31) / 32 * 32;
+  const size_t xt = (size_t)(s->n0 + 1) * s->n_pad;
+  CK(cudaMalloc(&s->Xt, sizeof(float) * xt));
+  if (s->split) {
+    CK(cudaMalloc(&s->Xtlo, sizeof(float) * xt));
+    CK(cudaMalloc(&s->Xlo, sizeof(float) * (size_t)c.n * s->n0));
+    const size_t w = (size_t)c.Jmax * s->n1 * s->n0;
+    CK(cudaMalloc(&s->W1hi, sizeof(float) * w));
+    CK(cudaMalloc(&s->W1lo, sizeof(float) * w));
+  }
+  dim3 grid((unsigned)((s->n_pad + 31) / 32), (unsigned)((s->n0 + 1 + 31) / 32));
+  transpose_x_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(c.X, c.n, s->n0, s->n_pad, s->Xt, s->Xtlo, s->Xlo,
+                                                         s->split ? 1 : 0);
+  LAUNCHED();
+  CK(cudaStreamSynchronize(c.stream));
+}
+
+void tc_free(Ctx& c) {
+  TcState* s = c.tc;
+  if (!s) return;
+  float* p[] = {s->Xt, s->Xlo, s->Xtlo, s->W1hi, s->W1lo, s->a1T, s->d1T, s->d2T, s->a1Tlo, s->d1Tlo, s->d2Tlo};
+  for (float* q : p)
+    if (q) cudaFree(q);
+  delete s;
+  c.tc = nullptr;
+}
+
+void tc_ensure_rows(Ctx& c, int64_t Mcap) {
+  TcState* s = c.tc;
+  if (Mcap <= s->mcap) return;
+  float** bufs[] = {&s->a1T, &s->d1T, &s->d2T, &s->a1Tlo, &s->d1Tlo, &s->d2Tlo};
+  for (float** b : bufs)
+    if (*b) {
+      CK(cudaFree(*b));
+      *b = nullptr;
+    }
+  const size_t J = (size_t)c.Jmax;
+  CK(cudaMalloc(&s->a1T, sizeof(float) * J * (s->n1 + 1) * Mcap));
+  CK(cudaMalloc(&s->d1T, sizeof(float) * J * s->n1 * Mcap));
+  CK(cudaMalloc(&s->d2T, sizeof(float) * J * s->C * Mcap));
+  if (s->split) {
+    CK(cudaMalloc(&s->a1Tlo, sizeof(float) * J * (s->n1 + 1) * Mcap));
+    CK(cudaMalloc(&s->d1Tlo, sizeof(float) * J * s->n1 * Mcap));
+    CK(cudaMalloc(&s->d2Tlo, sizeof(float) * J * s->C * Mcap));
+  }
+  s->mcap = Mcap;
+  const int g = (int)std::min<int64_t>((J * Mcap + 255) / 256, 148 * 16);
+  fill_ones_row_kernel<<<g, 256, 0, c.stream>>>(s->a1T, (int64_t)J, s->n1 + 1, s->n1, Mcap, 1.f);
+  LAUNCHED();
+  if (s->split) {
+    fill_ones_row_kernel<<<g, 256, 0, c.stream>>>(s->a1Tlo, (int64_t)J, s->n1 + 1, s->n1, Mcap, 0.f);
+    LAUNCHED();
+  }
+}
+
+void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, double beta_rows, bool need_grad,
+             const EpiParams* epi) {
+  TcState* s = c.tc;
+  const NetDev& net = c.net;
+  const LayerDev& l1 = net.layer[0];
+  const LayerDev& l2 = net.layer[1];
+  const int n0 = s->n0, n1 = s->n1, C = s->C;
+  const int64_t ldm = s->mcap;
+  const int rtiles = (int)((M + BM - 1) / BM);
+
+  // ---- fused forward: Z1 = X W1^T on tensor cores, layer 2 + loss + deltas in the epilogue
+  {
+    KTimer kt(c, need_grad ? 0 : -1);
+    const float* W1 = theta_in + l1.woff;
+    int64_t wstride = net.Dp;
+    if (s->split) {
+      const int64_t cnt = (int64_t)n1 * n0;
+      split_w1_kernel<<<(int)std::min<int64_t>((J * cnt + 255) / 256, 148 * 16), 256, 0, c.stream>>>(
+          theta_in, net.Dp, l1.woff, cnt, J, s->W1hi, s->W1lo);
+      LAUNCHED();
+      W1 = s->W1hi;
+      wstride = cnt;
+    }
+    const CUtensorMap A = map2d(c.X, n0, M, n0, BM);
+    const CUtensorMap Alo = s->split ? map2d(s->Xlo, n0, M, n0, BM) : A;
+    const CUtensorMap B = map3d(W1, n0, n1, n0, J, wstride, n1);
+    const CUtensorMap Blo = s->split ? map3d(s->W1lo, n0, n1, n0, J, wstride, n1) : B;
+    TileParams tp{};
+    tp.rtiles = rtiles;
+    tp.J = (int)J;
+    tp.rg = 32;
+    tp.nkb = (n0 + BK - 1) / BK;
+    tp.nmma = round16(n1);
+    tp.brows = n1;
+    FwdParams fp{};
+    fp.theta = theta_in;
+    fp.Dp = net.Dp;
+    fp.boff1 = l1.boff;
+    fp.woff2 = l2.woff;
+    fp.boff2 = l2.boff;
+    fp.n1 = n1;
+    fp.C = C;
+    fp.act = net.act;
+    fp.y = c.y;
+    fp.M = M;
+    fp.P = P;
+    fp.beta_rows = (float)beta_rows;
+    fp.need_grad = need_grad ? 1 : 0;
+    fp.ldm = ldm;
+    fp.a1T = s->a1T;
+    fp.d1T = s->d1T;
+    fp.d2T = s->d2T;
+    fp.a1Tlo = s->a1Tlo;
+    fp.d1Tlo = s->d1Tlo;
+    fp.d2Tlo = s->d2Tlo;
+    fp.ll_part = c.ll_part;
+    fp.ll_slots = c.ll_slots;
+    const size_t epi_bytes = sizeof(float) * ((size_t)C * n1 + n1 + C) + 16 + 8 * sizeof(double);
+    DwParams dp{};
+    if (s->split)
+      launch_tc<kEpiKindFwd, true, false>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+    else
+      launch_tc<kEpiKindFwd, false, false>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+  }
+  if (!need_grad) return;
+  FwdParams fp0{};
+  // ---- layer 2: dW2^T[o, c] = sum_m a1^T[o, m] delta2^T[c, m]  (ones row o = n1 -> db2)
+  {
+    const CUtensorMap A = map3d(s->a1T, M, n1 + 1, ldm, J, (uint64_t)(n1 + 1) * ldm, BM);
+    const CUtensorMap Alo = s->split ? map3d(s->a1Tlo, M, n1 + 1, ldm, J, (uint64_t)(n1 + 1) * ldm, BM) : A;
+    const CUtensorMap B = map3d(s->d2T, M, C, ldm, J, (uint64_t)C * ldm, C);
+    const CUtensorMap Blo = s->split ? map3d(s->d2Tlo, M, C, ldm, J, (uint64_t)C * ldm, C) : B;
+    TileParams tp{};
+    tp.rtiles = (n1 + 1 + BM - 1) / BM;
+    tp.J = (int)J;
+    tp.rg = tp.rtiles;
+    tp.nkb = (int)((M + BK - 1) / BK);
+    tp.nmma = round16(C);
+    tp.brows = C;
+    DwParams dp{*epi, net.Dp, l2.woff, l2.boff, n1, C};
+    if (s->split)
+      launch_tc<kEpiKindDw, true, true>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+    else
+      launch_tc<kEpiKindDw, false, true>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+  }
+  // ---- layer 1: dW1^T[i, o] = sum_m X^T[i, m] delta1^T[o, m]  (ones row i = n0 -> db1)
+  {
+    KTimer kt(c, 1);
+    const CUtensorMap A = map2d(s->Xt, M, n0 + 1, s->n_pad, BM);
+    const CUtensorMap Alo = s->split ? map2d(s->Xtlo, M, n0 + 1, s->n_pad, BM) : A;
+    const CUtensorMap B = map3d(s->d1T, M, n1, ldm, J, (uint64_t)n1 * ldm, n1);
+    const CUtensorMap Blo = s->split ? map3d(s->d1Tlo, M, n1, ldm, J, (uint64_t)n1 * ldm, n1) : B;
+    TileParams tp{};
+    tp.rtiles = (n0 + 1 + BM - 1) / BM;
+    tp.J = (int)J;
+    tp.rg = tp.rtiles;
+    tp.nkb = (int)((M + BK - 1) / BK);
+    tp.nmma = round16(n1);
+    tp.brows = n1;
+    DwParams dp{*epi, net.Dp, l1.woff, l1.boff, n0, n1};
+    if (s->split)
+      launch_tc<kEpiKindDw, true, false>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+    else
+      launch_tc<kEpiKindDw, false, false>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+  }
+}
 
 }  // namespace dasmc_b200

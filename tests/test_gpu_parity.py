@@ -138,6 +138,7 @@ def _step_compare(product, oracle, layers, act, n, win, mode, beta, kernel, J, s
                      "multinomial" if rkind == 0 else "systematic", fraction, always)
     dump = t.last_proposals(J)
     th1, lw1, it1 = t.get_ensemble(J)
+    dump["p0"] = t.momentum(seed, 3, J)  # the step's own fp32 draws (iteration 3)
     tho, lwo, ito, reco, d = oracle.smc_step(layers, a, X.astype(np.float64), y, win, mode, beta, sigma, kernel, seed,
                                              fraction, rkind, always, th0, lw0, 3)
     return rec, dump, th1, lw1, it1, reco, d, tho, lwo, ito
@@ -153,7 +154,7 @@ def test_smc_step_matches_oracle(product, oracle, S):
     # p_S - p0 = (h/2) (g_0 + 2 g_1 + ... + g_S): the gradient content of the final momentum
     hh = 0.5 * 0.002
     for j in range(32):
-        gsum, gsum_o = (dump["p_final"][j] - d["p0"][j]) / hh, (d["pS"][j] - d["p0"][j]) / hh
+        gsum, gsum_o = (dump["p_final"][j] - dump["p0"][j]) / hh, (d["pS"][j] - d["p0"][j]) / hh
         assert grad_err(gsum, gsum_o) < GRAD_TOL
         assert np.linalg.norm(dump["p_final"][j] - d["pS"][j]) / np.linalg.norm(d["pS"][j]) < 1e-6
     np.testing.assert_allclose(rec["ess"], reco["ess"], rtol=1e-3)

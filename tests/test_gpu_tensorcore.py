@@ -1,0 +1,94 @@
+"""GPU parity of the tcgen05 tensor-core path (tc_gemm.cu) against the fp64 oracle.
+
+Stated tolerances:
+  * split-tf32 ("3xtf32", 3 MMAs per k-step): the fp32 bar -- gradients
+    max_rel_error < 1e-4 (floor 1e-3 ||ref||_inf), values 1e-5 relative;
+  * plain tf32 (10-bit mantissa operands, fp32 accumulate): gradients
+    normwise ||g - ref|| / ||ref|| < 2e-3 and max_rel_error < 3e-2, values 1e-4.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [([64, 32, 10], "tanh", 200), ([784, 200, 10], "relu", 1000), ([36, 20, 3], "relu", 130),
+          ([8, 256, 16], "tanh", 77), ([784, 200, 10], "relu", 1)]
+
+
+def max_rel_error(a, b, floor):
+    return float(np.max(np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), floor)))
+
+
+def errs(g, ref):
+    return max_rel_error(g, ref, 1e-3 * np.max(np.abs(ref))), float(np.linalg.norm(g - ref) / np.linalg.norm(ref))
+
+
+def problem(product, layers, act, n):
+    spec = product.NetSpec(layers, act)
+    X, y = product.make_teacher_data(spec, n, 1 if layers[0] == 784 else 0, 0, 9, threads=8)
+    return spec, X, y
+
+
+@pytest.mark.parametrize("prec", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("layers,act,M", SHAPES)
+def test_tc_value_and_grad(product, oracle, layers, act, M, prec):
+    n = max(M, 600)
+    spec, X, y = problem(product, layers, act, n)
+    D = product.param_count(spec)
+    J = 5
+    th = (0.5 * np.random.default_rng(5).standard_normal((J, D))).astype(np.float32).astype(np.float64)
+    t = product.GpuEnsembleTarget(spec, X, y, J, precision=prec)
+    a = 0 if act == "relu" else 1
+    for mode, win, beta in (("scaled", (0, M, n), 1.0), ("sda", (M // 3, M, n), 0.4)):
+        t.set_target(*win, mode, beta, 1.0)
+        v, g = t.log_target_with_grad(th)
+        vo, go = oracle.value_and_grad(layers, a, X.astype(np.float64), y, win, 0 if mode == "scaled" else 1, beta,
+                                       1.0, th)
+        vrel = float(np.max(np.abs(v - vo) / np.abs(vo)))
+        worst = max(errs(g[j], go[j]) for j in range(J))
+        print(f"{prec} {layers} M={M} {mode}: value rel {vrel:.2e}  grad max_rel {worst[0]:.2e} norm {worst[1]:.2e}")
+        if prec == "3xtf32":
+            assert vrel < 1e-5
+            for j in range(J):
+                assert errs(g[j], go[j])[0] < 1e-4
+        else:
+            assert vrel < 1e-4
+            for j in range(J):
+                mr, nr = errs(g[j], go[j])
+                assert nr < 2e-3 and mr < 3e-2
+
+
+@pytest.mark.parametrize("prec", ["3xtf32", "tf32"])
+def test_tc_loglik_parts_and_step(product, oracle, prec):
+    layers, act = [64, 32, 10], "tanh"
+    spec, X, y = problem(product, layers, act, 2000)
+    J = 64
+    th0, lw0 = oracle.init_ensemble(layers, 1, X.astype(np.float64), y, (0, 200, 2000), 0, 1.0, 1.0, 13, J)
+    th0 = th0.astype(np.float32).astype(np.float64)
+    t = product.GpuEnsembleTarget(spec, X, y, J, precision=prec)
+    t.set_target(50, 200, 2000, "sda", 0.3, 1.0)
+    a, b = t.unscaled_loglik_parts(th0)
+    ao, bo = oracle.loglik_parts(layers, 1, X.astype(np.float64), y, 50, 200, th0)
+    tol = 1e-5 if prec == "3xtf32" else 1e-3
+    assert np.max(np.abs(a - ao) / np.abs(ao)) < tol and np.max(np.abs(b - bo) / np.abs(bo)) < tol
+    t.set_target(0, 200, 2000, "scaled", 1.0, 1.0)
+    t.set_ensemble(th0, lw0, 5)
+    rec = t.smc_step(product.KernelConfig.hmc(0.002, 3), 13, "multinomial", 0.5)
+    dump = t.last_proposals(J)
+    tho, lwo, ito, reco, d = oracle.smc_step(layers, 1, X.astype(np.float64), y, (0, 200, 2000), 0, 1.0, 1.0,
+                                             (0.002, 3, 0), 13, 0.5, 0, False, th0, lw0, 5)
+    ltol = 1e-5 if prec == "3xtf32" else 1e-4
+    assert np.max(np.abs(dump["log_target_new"] - d["lt_new"]) / np.abs(d["lt_new"])) < ltol
+    np.testing.assert_allclose(rec["ess"], reco["ess"], rtol=1e-2)
+
+
+def test_tc_run_matches_fp32_schedule(product):
+    layers = [64, 32, 10]
+    spec, X, y = problem(product, layers, "tanh", 2000)
+    cfg = product.RunConfig(kernel=product.KernelConfig.hmc(0.002, 3),
+                            schedule=product.ScheduleConfig("ctr", 200, 100, 8, 2000, 1, 5), particles=128,
+                            iterations=8, seed=1, resample="systematic")
+    r32 = product.run_experiment(spec, X, y, cfg, precision="fp32")["records"]
+    r3x = product.run_experiment(spec, X, y, cfg, precision="3xtf32")["records"]
+    assert [r["batch"] for r in r32] == [r["batch"] for r in r3x]
+    np.testing.assert_allclose(r3x[0]["mean_log_target"], r32[0]["mean_log_target"], rtol=1e-5)
