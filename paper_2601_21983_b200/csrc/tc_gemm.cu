@@ -29,9 +29,10 @@ struct TcState {
   int64_t mcap = 0;      // row stride of the transposed activation buffers
   bool split = false;    // split-tf32 (3 MMAs)
   float* Xt = nullptr;   // [(n0+1) x n_pad], row n0 = 1
+  float* Xhi = nullptr;  // [n x n0] X rounded to tf32 (cvt.rna): the MMA truncates raw fp32
   float* Xlo = nullptr;  // [n x n0]   (split)
   float* Xtlo = nullptr; // [(n0+1) x n_pad] (split; ones row lo = 0)
-  float* W1hi = nullptr; // [J x n1 x n0] (split)
+  float* W1hi = nullptr; // [J x n1 x n0] W1 rounded to tf32
   float* W1lo = nullptr;
   float* a1T = nullptr;  // [J x (n1+1) x mcap], row n1 = 1
   float* d1T = nullptr;  // [J x n1 x mcap]
@@ -365,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   a1T[(int64_t)o * ldm] = hi;
                   fp.a1Tlo[(int64_t)j * (n1 + 1) * ldm + (int64_t)o * ldm + m] = a - hi;
                 } else {
-                  a1T[(int64_t)o * ldm] = a;
+                  a1T[(int64_t)o * ldm] = tf32_hi(a);
                 }
               }
             }
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   *dst = hi;
                   fp.d2Tlo[((int64_t)j * C + c) * ldm + m] = d2[c] - hi;
                 } else {
-                  *dst = d2[c];
+                  *dst = tf32_hi(d2[c]);
                 }
               }
           }
@@ -434,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   d1T[(int64_t)o * ldm] = hi;
                   fp.d1Tlo[(int64_t)j * n1 * ldm + (int64_t)o * ldm + m] = d1 - hi;
                 } else {
-                  d1T[(int64_t)o * ldm] = d1;
+                  d1T[(int64_t)o * ldm] = tf32_hi(d1);
                 }
               }
             }
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ---------------------------------------------------------------- helper kernels
 // X^T with a ones row (and tf32 hi/lo splits): Xt[i][m] = X[m][i], Xt[n0][m] = 1.
 __global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n0, int64_t n_pad, float* Xt, float* Xtlo,
-                                   float* Xlo, int split) {
+                                   float* Xhi, float* Xlo, int split) {
   __shared__ float tile[32][33];
   const int64_t m0 = (int64_t)blockIdx.x * 32;
   const int i0 = blockIdx.y * 32;
@@ -508,6 +509,7 @@ __global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n
     float v = 0.f;
     if (m < n && i < n0) v = X[m * n0 + i];
     if (m < n && i == n0) v = 1.f;
+    if (m < n && i < n0) Xhi[m * n0 + i] = tf32_hi(v);
     if (split && m < n && i < n0) Xlo[m * n0 + i] = v - tf32_hi(v);
     tile[r][threadIdx.x] = v;
   }
@@ -517,13 +519,9 @@ __global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n
     const int64_t m = m0 + threadIdx.x;
     if (i <= n0 && m < n_pad) {
       const float v = m < n ? tile[threadIdx.x][r] : 0.f;
-      if (split) {
-        const float hi = tf32_hi(v);
-        Xt[(int64_t)i * n_pad + m] = hi;
-        Xtlo[(int64_t)i * n_pad + m] = v - hi;
-      } else {
-        Xt[(int64_t)i * n_pad + m] = v;
-      }
+      const float hi = tf32_hi(v);
+      Xt[(int64_t)i * n_pad + m] = hi;
+      if (split) Xtlo[(int64_t)i * n_pad + m] = v - hi;
     }
   }
 }
@@ -536,7 +534,7 @@ __global__ void split_w1_kernel(const float* __restrict__ theta, int64_t Dp, int
     const float v = theta[j * Dp + woff + r];
     const float h = tf32_hi(v);
     hi[g] = h;
-    lo[g] = v - h;
+    if (lo) lo[g] = v - h;
   }
 }
 
@@ -637,15 +635,16 @@ void tc_init(Ctx& c) {
   s->n_pad = (c.n + 31) / 32 * 32;
   const size_t xt = (size_t)(s->n0 + 1) * s->n_pad;
   CK(cudaMalloc(&s->Xt, sizeof(float) * xt));
+  const size_t w = (size_t)c.Jmax * s->n1 * s->n0;
+  CK(cudaMalloc(&s->Xhi, sizeof(float) * (size_t)c.n * s->n0));
+  CK(cudaMalloc(&s->W1hi, sizeof(float) * w));
   if (s->split) {
     CK(cudaMalloc(&s->Xtlo, sizeof(float) * xt));
     CK(cudaMalloc(&s->Xlo, sizeof(float) * (size_t)c.n * s->n0));
-    const size_t w = (size_t)c.Jmax * s->n1 * s->n0;
-    CK(cudaMalloc(&s->W1hi, sizeof(float) * w));
     CK(cudaMalloc(&s->W1lo, sizeof(float) * w));
   }
   dim3 grid((unsigned)((s->n_pad + 31) / 32), (unsigned)((s->n0 + 1 + 31) / 32));
-  transpose_x_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(c.X, c.n, s->n0, s->n_pad, s->Xt, s->Xtlo, s->Xlo,
+  transpose_x_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(c.X, c.n, s->n0, s->n_pad, s->Xt, s->Xtlo, s->Xhi, s->Xlo,
                                                          s->split ? 1 : 0);
   LAUNCHED();
   CK(cudaStreamSynchronize(c.stream));
@@ -654,7 +653,7 @@ void tc_init(Ctx& c) {
 void tc_free(Ctx& c) {
   TcState* s = c.tc;
   if (!s) return;
-  float* p[] = {s->Xt, s->Xlo, s->Xtlo, s->W1hi, s->W1lo, s->a1T, s->d1T, s->d2T, s->a1Tlo, s->d1Tlo, s->d2Tlo};
+  float* p[] = {s->Xt, s->Xhi, s->Xlo, s->Xtlo, s->W1hi, s->W1lo, s->a1T, s->d1T, s->d2T, s->a1Tlo, s->d1Tlo, s->d2Tlo};
   for (float* q : p)
     if (q) cudaFree(q);
   delete s;
@@ -704,15 +703,15 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     KTimer kt(c, need_grad ? 0 : -1);
     const float* W1 = theta_in + l1.woff;
     int64_t wstride = net.Dp;
-    if (s->split) {
+    {  // W1 -> tf32 (rna) hi [+ lo]: the MMA would otherwise truncate the low mantissa bits
       const int64_t cnt = (int64_t)n1 * n0;
       split_w1_kernel<<<(int)std::min<int64_t>((J * cnt + 255) / 256, 148 * 16), 256, 0, c.stream>>>(
-          theta_in, net.Dp, l1.woff, cnt, J, s->W1hi, s->W1lo);
+          theta_in, net.Dp, l1.woff, cnt, J, s->W1hi, s->split ? s->W1lo : nullptr);
       LAUNCHED();
       W1 = s->W1hi;
       wstride = cnt;
     }
-    const CUtensorMap A = map2d(c.X, n0, M, n0, BM);
+    const CUtensorMap A = map2d(s->Xhi, n0, M, n0, BM);
     const CUtensorMap Alo = s->split ? map2d(s->Xlo, n0, M, n0, BM) : A;
     const CUtensorMap B = map3d(W1, n0, n1, n0, J, wstride, n1);
     const CUtensorMap Blo = s->split ? map3d(s->W1lo, n0, n1, n0, J, wstride, n1) : B;
