@@ -6,7 +6,8 @@
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32,
 //               M = 128, N <= 256, K = 8 per instruction), double-buffered
 //               128 x 256 fp32 accumulators in TMEM
-//   warps 2..5  epilogue: tcgen05.ld 32x32b rows -> registers -> fused math
+//   warps 2..9  epilogue: tcgen05.ld 32x32b rows -> registers -> fused math
+//               (two warps per TMEM lane group, each taking half the columns)
 // mbarriers: full/empty per stage (TMA <-> MMA), tmem_full/tmem_empty per
 // accumulator (MMA <-> epilogue).  tcgen05.commit arrives on the mbarriers.
 #include <cuda.h>
@@ -16,6 +17,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 #include "ctx.cuh"
 #include "epi.cuh"
@@ -47,7 +49,9 @@ namespace {
 
 constexpr int BM = 128;  // UMMA_M
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kThreads = 64 + kEpiThreads;  // TMA warp + MMA warp + epilogue warps
 constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
 constexpr int kEpiKindFwd = 0, kEpiKindDw = 1;
 
@@ -192,7 +196,7 @@ __device__ __forceinline__ void tile_coords(const TileParams& tp, int t, int& rt
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int EPI, bool SPLIT, bool A3D>
+template <int EPI, bool SPLIT, bool A3D, int CP>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
               const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo, TileParams tp,
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = bars + 2 * tp.stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = (uint32_t*)(tempty + 2);
-  float* epi_smem = (float*)(tmem_holder + 4);  // fused-forward parameters
+  float* epi_smem = (float*)(tmem_holder + 4);  // 16-byte aligned
 
   auto A_of = [&](int s, int lo) { return stages + (size_t)s * stage_bytes + (lo ? a_bytes : 0); };
   auto B_of = [&](int s, int lo) { return stages + (size_t)s * stage_bytes + sub * a_bytes + (lo ? b_bytes : 0); };
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], kEpiThreads);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -315,40 +319,53 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ===================== epilogue warps 2..5 =====================
-    const int et = threadIdx.x - 64;              // 0..127
-    const int lane_base = (warp & 3) * 32;        // TMEM lanes this warp may access
-    const int row_in_tile = lane_base + lane;
+    // ===================== epilogue warps 2..9 =====================
+    // Two warps share each TMEM lane group (warp % 4); `half` splits the
+    // accumulator columns between them.
+    const int et = threadIdx.x - 64;  // 0..255
+    const int lg = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int row_in_tile = lg * 32 + lane;
     int acc = 0;
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int rt, j;
       tile_coords(tp, t, rt, j);
       if (EPI == kEpiKindFwd) {
-        // per-particle layer-2 parameters -> shared memory
         const int n1 = fp.n1, C = fp.C;
-        float* W2s = epi_smem;        // [C][n1]
-        float* b1s = W2s + C * n1;    // [n1]
-        float* b2s = b1s + n1;        // [C]
-        double* red = (double*)(((uintptr_t)(b2s + C) + 15) & ~(uintptr_t)15);  // [2][4]
-        named_bar(1, 128);
+        float* W2T = epi_smem;                  // [n1][CP]  W2 transposed, zero-padded
+        float* b1s = W2T + (size_t)n1 * CP;     // [n1]
+        float* b2s = b1s + ((n1 + 3) & ~3);     // [CP]
+        float* z2x = b2s + CP;                  // [2][128][CP] partial layer-2 logits
+        double* red = (double*)(z2x + 2 * 128 * CP);  // [4][2]
+        named_bar(1, kEpiThreads);
         const float* th = fp.theta + (int64_t)j * fp.Dp;
-        for (int i = et; i < C * n1; i += 128) W2s[i] = th[fp.woff2 + i];
-        for (int i = et; i < n1; i += 128) b1s[i] = th[fp.boff1 + i];
-        for (int i = et; i < C; i += 128) b2s[i] = th[fp.boff2 + i];
-        named_bar(1, 128);
+        for (int i = et; i < n1 * CP; i += kEpiThreads) {
+          const int o = i / CP, c = i - o * CP;
+          W2T[i] = c < C ? th[fp.woff2 + (int64_t)c * n1 + o] : 0.f;
+        }
+        for (int i = et; i < n1; i += kEpiThreads) b1s[i] = th[fp.boff1 + i];
+        for (int i = et; i < CP; i += kEpiThreads) b2s[i] = i < C ? th[fp.boff2 + i] : 0.f;
+        named_bar(1, kEpiThreads);
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
-        const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)lane_base << 16);
+        const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(lg * 32) << 16);
         const int64_t m = (int64_t)rt * BM + row_in_tile;
         const bool valid = m < fp.M;
         const bool relu = fp.act == DASMC_RELU;
-        float z2[16];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) z2[c] = 0.f;
+        const bool wr_out = valid && fp.need_grad;
+        const int nch = (n1 + 15) >> 4, hch = (nch + 1) >> 1;
+        const int c_lo = half ? hch : 0, c_hi = half ? nch : hch;
         const int64_t ldm = fp.ldm;
+        const float4* W2T4 = reinterpret_cast<const float4*>(W2T);
+        float z2[CP];
+#pragma unroll
+        for (int c = 0; c < CP; ++c) z2[c] = 0.f;
         float* a1T = fp.a1T + (int64_t)j * (n1 + 1) * ldm + m;
-        for (int o0 = 0; o0 < n1; o0 += 16) {
+        float* a1Tlo = SPLIT ? fp.a1Tlo + (int64_t)j * (n1 + 1) * ldm + m : nullptr;
+        // pass 1: a1 = act(z1 + b1); partial z2 = W2 a1 over this warp's columns
+        for (int ch = c_lo; ch < c_hi; ++ch) {
+          const int o0 = ch * 16;
           float v[16];
           tmem_ld16(taddr + o0, v);
 #pragma unroll
@@ -358,65 +375,70 @@ __global__ void __launch_bounds__(kThreads, 1)
               float a = v[q] + b1s[o];
               a = relu ? fmaxf(a, 0.f) : tanhf(a);
 #pragma unroll
-              for (int c = 0; c < 16; ++c)
-                if (c < C) z2[c] = fmaf(a, W2s[c * n1 + o], z2[c]);
-              if (valid && fp.need_grad) {
-                if (SPLIT) {
-                  const float hi = tf32_hi(a);
-                  a1T[(int64_t)o * ldm] = hi;
-                  fp.a1Tlo[(int64_t)j * (n1 + 1) * ldm + (int64_t)o * ldm + m] = a - hi;
-                } else {
-                  a1T[(int64_t)o * ldm] = tf32_hi(a);
-                }
+              for (int u = 0; u < CP / 4; ++u) {
+                const float4 w = W2T4[o * (CP / 4) + u];
+                z2[4 * u] = fmaf(a, w.x, z2[4 * u]);
+                z2[4 * u + 1] = fmaf(a, w.y, z2[4 * u + 1]);
+                z2[4 * u + 2] = fmaf(a, w.z, z2[4 * u + 2]);
+                z2[4 * u + 3] = fmaf(a, w.w, z2[4 * u + 3]);
+              }
+              if (wr_out) {
+                const float hi = tf32_hi(a);
+                a1T[(int64_t)o * ldm] = hi;
+                if (SPLIT) a1Tlo[(int64_t)o * ldm] = a - hi;
               }
             }
           }
         }
+        // combine the two column halves in a fixed order
+        float* zx = z2x + ((size_t)half * 128 + row_in_tile) * CP;
+#pragma unroll
+        for (int c = 0; c < CP; ++c) zx[c] = z2[c];
+        named_bar(1, kEpiThreads);
+        const float* z0 = z2x + (size_t)row_in_tile * CP;
+        const float* z1p = z2x + ((size_t)128 + row_in_tile) * CP;
+#pragma unroll
+        for (int c = 0; c < CP; ++c) z2[c] = (z0[c] + z1p[c]) + b2s[c];
         // log-softmax likelihood of the row in fp64 (network.hpp:183-193)
         double ll = 0.0;
-        float d2[16];
+        float d2[CP];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) d2[c] = 0.f;
+        for (int c = 0; c < CP; ++c) d2[c] = 0.f;
         if (valid) {
           const int yi = fp.y[m];
-          double mx = -1e300;
+          double mx = (double)z2[0];
 #pragma unroll
-          for (int c = 0; c < 16; ++c)
+          for (int c = 1; c < CP; ++c)
+            if (c < C) mx = fmax(mx, (double)z2[c]);
+          double den = 0.0, zy = 0.0;
+#pragma unroll
+          for (int c = 0; c < CP; ++c)
             if (c < C) {
-              z2[c] += b2s[c];
-              mx = fmax(mx, (double)z2[c]);
+              den += exp((double)z2[c] - mx);
+              if (c == yi) zy = (double)z2[c];
             }
-          double den = 0.0;
-#pragma unroll
-          for (int c = 0; c < 16; ++c)
-            if (c < C) den += exp((double)z2[c] - mx);
-          double zy = 0.0;
-#pragma unroll
-          for (int c = 0; c < 16; ++c)
-            if (c == yi) zy = (double)z2[c];
           ll = zy - (mx + log(den));
           if (fp.need_grad) {
-            const float wr = m < fp.P ? 1.f : fp.beta_rows;
+            const float wrow = m < fp.P ? 1.f : fp.beta_rows;
 #pragma unroll
-            for (int c = 0; c < 16; ++c)
+            for (int c = 0; c < CP; ++c)
               if (c < C) {
                 const double pr = exp((double)z2[c] - mx) / den;
-                d2[c] = wr * (float)((c == yi ? 1.0 : 0.0) - pr);
-                float* dst = fp.d2T + ((int64_t)j * C + c) * ldm + m;
-                if (SPLIT) {
+                d2[c] = wrow * (float)((c == yi ? 1.0 : 0.0) - pr);
+                if (half == 0) {
                   const float hi = tf32_hi(d2[c]);
-                  *dst = hi;
-                  fp.d2Tlo[((int64_t)j * C + c) * ldm + m] = d2[c] - hi;
-                } else {
-                  *dst = tf32_hi(d2[c]);
+                  fp.d2T[((int64_t)j * C + c) * ldm + m] = hi;
+                  if (SPLIT) fp.d2Tlo[((int64_t)j * C + c) * ldm + m] = d2[c] - hi;
                 }
               }
           }
         }
         if (fp.need_grad) {
-          // delta1 = (W2^T delta2) . act'(a1)  (network.hpp:209-215)
+          // pass 2: delta1 = (W2^T delta2) . act'(a1)  (network.hpp:209-215)
           float* d1T = fp.d1T + (int64_t)j * n1 * ldm + m;
-          for (int o0 = 0; o0 < n1; o0 += 16) {
+          float* d1Tlo = SPLIT ? fp.d1Tlo + (int64_t)j * n1 * ldm + m : nullptr;
+          for (int ch = c_lo; ch < c_hi; ++ch) {
+            const int o0 = ch * 16;
             float v[16];
             tmem_ld16(taddr + o0, v);
 #pragma unroll
@@ -427,16 +449,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 a = relu ? fmaxf(a, 0.f) : tanhf(a);
                 float dz = 0.f;
 #pragma unroll
-                for (int c = 0; c < 16; ++c)
-                  if (c < C) dz = fmaf(d2[c], W2s[c * n1 + o], dz);
-                const float d1 = relu ? dz * (a > 0.f ? 1.f : 0.f) : dz * (1.f - a * a);
-                if (SPLIT) {
-                  const float hi = tf32_hi(d1);
-                  d1T[(int64_t)o * ldm] = hi;
-                  fp.d1Tlo[(int64_t)j * n1 * ldm + (int64_t)o * ldm + m] = d1 - hi;
-                } else {
-                  d1T[(int64_t)o * ldm] = tf32_hi(d1);
+                for (int u = 0; u < CP / 4; ++u) {
+                  const float4 w = W2T4[o * (CP / 4) + u];
+                  dz = fmaf(d2[4 * u], w.x, dz);
+                  dz = fmaf(d2[4 * u + 1], w.y, dz);
+                  dz = fmaf(d2[4 * u + 2], w.z, dz);
+                  dz = fmaf(d2[4 * u + 3], w.w, dz);
                 }
+                const float d1 = relu ? dz * (a > 0.f ? 1.f : 0.f) : dz * (1.f - a * a);
+                const float hi = tf32_hi(d1);
+                d1T[(int64_t)o * ldm] = hi;
+                if (SPLIT) d1Tlo[(int64_t)o * ldm] = d1 - hi;
               }
             }
           }
@@ -450,11 +473,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           pre += __shfl_xor_sync(0xffffffffu, pre, o);
           blk += __shfl_xor_sync(0xffffffffu, blk, o);
         }
-        if (lane == 0) {
-          red[(warp & 3) * 2] = pre;
-          red[(warp & 3) * 2 + 1] = blk;
+        if (lane == 0 && half == 0) {
+          red[lg * 2] = pre;
+          red[lg * 2 + 1] = blk;
         }
-        named_bar(1, 128);
+        named_bar(1, kEpiThreads);
         if (et == 0) {
           double* o = fp.ll_part + ((int64_t)j * fp.ll_slots + rt) * 2;
           o[0] = red[0] + red[2] + red[4] + red[6];
@@ -464,11 +487,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // weight-gradient tile: row i of A (input index, `in` = bias row), columns o
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
-        const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)lane_base << 16);
+        const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(lg * 32) << 16);
         const int i = rt * BM + row_in_tile;
         const bool valid = i <= dp.in;
         const int64_t base = (int64_t)j * dp.Dp;
-        for (int o0 = 0; o0 < dp.n_out; o0 += 16) {
+        const int nch = (dp.n_out + 15) >> 4, hch = (nch + 1) >> 1;
+        const int c_lo = half ? hch : 0, c_hi = half ? nch : hch;
+        for (int ch = c_lo; ch < c_hi; ++ch) {
+          const int o0 = ch * 16;
           float v[16];
           tmem_ld16(taddr + o0, v);
           if (valid) {
@@ -591,7 +617,7 @@ CUtensorMap map3d(const float* base, uint64_t inner, uint64_t rows, uint64_t ld,
 
 int round16(int v) { return (v + 15) / 16 * 16; }
 
-template <int EPI, bool SPLIT, bool A3D>
+template <int EPI, bool SPLIT, bool A3D, int CP = 4>
 void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUtensorMap& B, const CUtensorMap& Blo,
                TileParams tp, const FwdParams& fp, const DwParams& dp, size_t epi_smem_bytes) {
   const uint32_t sub = SPLIT ? 2 : 1;
@@ -603,7 +629,7 @@ void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUten
   tp.stages = stages;
   tp.stage_bytes_tx = (uint32_t)(sub * ((size_t)BM * BK * 4 + (size_t)tp.brows * BK * 4));
   const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16 + epi_smem_bytes + 64;
-  auto kern = tc_kernel<EPI, SPLIT, A3D>;
+  auto kern = tc_kernel<EPI, SPLIT, A3D, CP>;
   static bool attr_set = false;
   if (!attr_set) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget));
@@ -745,12 +771,24 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     fp.d2Tlo = s->d2Tlo;
     fp.ll_part = c.ll_part;
     fp.ll_slots = c.ll_slots;
-    const size_t epi_bytes = sizeof(float) * ((size_t)C * n1 + n1 + C) + 16 + 8 * sizeof(double);
+    // classes padded to a multiple of 4 (float4 rows of W2^T in shared memory)
+    const int CP = (C + 3) / 4 * 4;
+    const size_t epi_bytes =
+        sizeof(float) * ((size_t)n1 * CP + ((n1 + 3) & ~3) + CP + 2 * 128 * CP) + 8 * sizeof(double) + 16;
     DwParams dp{};
-    if (s->split)
-      launch_tc<kEpiKindFwd, true, false>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
-    else
-      launch_tc<kEpiKindFwd, false, false>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+    auto go = [&](auto cp) {
+      constexpr int K = decltype(cp)::value;
+      if (s->split)
+        launch_tc<kEpiKindFwd, true, false, K>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+      else
+        launch_tc<kEpiKindFwd, false, false, K>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+    };
+    switch (CP) {
+      case 4: go(std::integral_constant<int, 4>{}); break;
+      case 8: go(std::integral_constant<int, 8>{}); break;
+      case 12: go(std::integral_constant<int, 12>{}); break;
+      default: go(std::integral_constant<int, 16>{}); break;
+    }
   }
   if (!need_grad) return;
   FwdParams fp0{};
