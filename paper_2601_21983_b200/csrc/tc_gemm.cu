@@ -86,8 +86,10 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try(bar, parity)) return;
   const long long t0 = clock64();
-  while (!mbar_try(bar, parity))
-    if (clock64() - t0 > 20000000000LL) __trap();
+  for (uint32_t i = 1;; ++i) {
+    if (mbar_try(bar, parity)) return;
+    if ((i & 0x3FFFu) == 0 && clock64() - t0 > 20000000000LL) __trap();
+  }
 }
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
@@ -202,7 +204,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo, TileParams tp,
               FwdParams fp, DwParams dp) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-byte alignment for the 128B swizzle atoms; keep the pointer derived
+  // from smem_raw so the compiler emits shared-memory (LDS/STS) accesses.
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t a_bytes = BM * BK * 4;
   const uint32_t b_bytes = (uint32_t)tp.nmma * BK * 4;
@@ -364,30 +368,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* a1T = fp.a1T + (int64_t)j * (n1 + 1) * ldm + m;
         float* a1Tlo = SPLIT ? fp.a1Tlo + (int64_t)j * (n1 + 1) * ldm + m : nullptr;
         // pass 1: a1 = act(z1 + b1); partial z2 = W2 a1 over this warp's columns
+        auto pass1 = [&](const float* v, int q, const float4* w4, float b, float*& pa, float*& pal) {
+          float a = v[q] + b;
+          a = relu ? fmaxf(a, 0.f) : tanhf(a);
+#pragma unroll
+          for (int u = 0; u < CP / 4; ++u) {
+            const float4 w = w4[q * (CP / 4) + u];
+            z2[4 * u] = fmaf(a, w.x, z2[4 * u]);
+            z2[4 * u + 1] = fmaf(a, w.y, z2[4 * u + 1]);
+            z2[4 * u + 2] = fmaf(a, w.z, z2[4 * u + 2]);
+            z2[4 * u + 3] = fmaf(a, w.w, z2[4 * u + 3]);
+          }
+          if (wr_out) {
+            const float hi = tf32_hi(a);
+            *pa = hi;
+            if (SPLIT) *pal = a - hi;
+          }
+          pa += ldm;
+          if (SPLIT) pal += ldm;
+        };
         for (int ch = c_lo; ch < c_hi; ++ch) {
           const int o0 = ch * 16;
           float v[16];
           tmem_ld16(taddr + o0, v);
+          const int nq = min(16, n1 - o0);  // warp-uniform
+          float* pa = a1T + (int64_t)o0 * ldm;
+          float* pal = SPLIT ? a1Tlo + (int64_t)o0 * ldm : nullptr;
+          const float4* w4 = W2T4 + o0 * (CP / 4);
+          if (nq == 16) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int o = o0 + q;
-            if (o < n1) {
-              float a = v[q] + b1s[o];
-              a = relu ? fmaxf(a, 0.f) : tanhf(a);
+            for (int q = 0; q < 16; ++q) pass1(v, q, w4, b1s[o0 + q], pa, pal);
+          } else {  // tail chunk: still unrolled so v[] stays in registers
 #pragma unroll
-              for (int u = 0; u < CP / 4; ++u) {
-                const float4 w = W2T4[o * (CP / 4) + u];
-                z2[4 * u] = fmaf(a, w.x, z2[4 * u]);
-                z2[4 * u + 1] = fmaf(a, w.y, z2[4 * u + 1]);
-                z2[4 * u + 2] = fmaf(a, w.z, z2[4 * u + 2]);
-                z2[4 * u + 3] = fmaf(a, w.w, z2[4 * u + 3]);
-              }
-              if (wr_out) {
-                const float hi = tf32_hi(a);
-                a1T[(int64_t)o * ldm] = hi;
-                if (SPLIT) a1Tlo[(int64_t)o * ldm] = a - hi;
-              }
-            }
+            for (int q = 0; q < 16; ++q)
+              if (q < nq) pass1(v, q, w4, b1s[o0 + q], pa, pal);
           }
         }
         // combine the two column halves in a fixed order
@@ -437,30 +451,42 @@ __global__ void __launch_bounds__(kThreads, 1)
           // pass 2: delta1 = (W2^T delta2) . act'(a1)  (network.hpp:209-215)
           float* d1T = fp.d1T + (int64_t)j * n1 * ldm + m;
           float* d1Tlo = SPLIT ? fp.d1Tlo + (int64_t)j * n1 * ldm + m : nullptr;
+          auto pass2 = [&](const float* v, int q, const float4* w4, float b, float*& pd, float*& pdl) {
+            float a = v[q] + b;
+            a = relu ? fmaxf(a, 0.f) : tanhf(a);
+            float dx = 0.f, dy = 0.f, dzz = 0.f, dw = 0.f;  // 4 independent chains
+#pragma unroll
+            for (int u = 0; u < CP / 4; ++u) {
+              const float4 w = w4[q * (CP / 4) + u];
+              dx = fmaf(d2[4 * u], w.x, dx);
+              dy = fmaf(d2[4 * u + 1], w.y, dy);
+              dzz = fmaf(d2[4 * u + 2], w.z, dzz);
+              dw = fmaf(d2[4 * u + 3], w.w, dw);
+            }
+            const float dz = (dx + dy) + (dzz + dw);
+            const float d1 = relu ? dz * (a > 0.f ? 1.f : 0.f) : dz * (1.f - a * a);
+            const float hi = tf32_hi(d1);
+            *pd = hi;
+            if (SPLIT) *pdl = d1 - hi;
+            pd += ldm;
+            if (SPLIT) pdl += ldm;
+          };
           for (int ch = c_lo; ch < c_hi; ++ch) {
             const int o0 = ch * 16;
             float v[16];
             tmem_ld16(taddr + o0, v);
+            if (!valid) continue;
+            const int nq = min(16, n1 - o0);  // warp-uniform
+            float* pd = d1T + (int64_t)o0 * ldm;
+            float* pdl = SPLIT ? d1Tlo + (int64_t)o0 * ldm : nullptr;
+            const float4* w4 = W2T4 + o0 * (CP / 4);
+            if (nq == 16) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const int o = o0 + q;
-              if (o < n1 && valid) {
-                float a = v[q] + b1s[o];
-                a = relu ? fmaxf(a, 0.f) : tanhf(a);
-                float dz = 0.f;
+              for (int q = 0; q < 16; ++q) pass2(v, q, w4, b1s[o0 + q], pd, pdl);
+            } else {
 #pragma unroll
-                for (int u = 0; u < CP / 4; ++u) {
-                  const float4 w = W2T4[o * (CP / 4) + u];
-                  dz = fmaf(d2[4 * u], w.x, dz);
-                  dz = fmaf(d2[4 * u + 1], w.y, dz);
-                  dz = fmaf(d2[4 * u + 2], w.z, dz);
-                  dz = fmaf(d2[4 * u + 3], w.w, dz);
-                }
-                const float d1 = relu ? dz * (a > 0.f ? 1.f : 0.f) : dz * (1.f - a * a);
-                const float hi = tf32_hi(d1);
-                d1T[(int64_t)o * ldm] = hi;
-                if (SPLIT) d1Tlo[(int64_t)o * ldm] = d1 - hi;
-              }
+              for (int q = 0; q < 16; ++q)
+                if (q < nq) pass2(v, q, w4, b1s[o0 + q], pd, pdl);
             }
           }
         }
