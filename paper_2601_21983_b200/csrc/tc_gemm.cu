@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
@@ -30,6 +31,7 @@ struct TcState {
   int64_t n_pad = 0;     // X^T row stride (floats)
   int64_t mcap = 0;      // row stride of the transposed activation buffers
   bool split = false;    // split-tf32 (3 MMAs)
+  bool tc_layer2 = true; // fused forward runs layer 2 as TMEM-A MMAs (DASMC_TC_LAYER2=0 disables)
   float* Xt = nullptr;   // [(n0+1) x n_pad], row n0 = 1
   float* Xhi = nullptr;  // [n x n0] X rounded to tf32 (cvt.rna): the MMA truncates raw fp32
   float* Xlo = nullptr;  // [n x n0]   (split)
@@ -53,7 +55,7 @@ constexpr int kEpiWarps = 8;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;  // TMA warp + MMA warp + epilogue warps
 constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
-constexpr int kEpiKindFwd = 0, kEpiKindDw = 1;
+constexpr int kEpiKindFwd = 0, kEpiKindDw = 1, kEpiKindFwdTc = 2;
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -124,6 +126,37 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
+// D[tmem] (+)= A[tmem] . B[smem]  (A: 128 lanes x K columns, K-major)
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+      "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
+      "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// Byte offset of element (row r, k) inside a K-major 128B-swizzled tile of
+// 32-element k-blocks (8-row core groups of 1024 B; 16 B chunks XOR row % 8).
+__device__ __forceinline__ uint32_t sw128_offset(int r, int k, int rows) {
+  const int kb = k >> 5, e = k & 31;
+  return (uint32_t)(kb * rows * 128 + r * 128 + ((((e >> 2) ^ (r & 7)) & 7) << 4) + (e & 3) * 4);
+}
+
 // 32 lanes x 32 bit, 16 consecutive columns per thread.
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
@@ -332,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row_in_tile = lg * 32 + lane;
     int acc = 0;
     uint32_t aph = 0;
+    uint32_t sph = 0;  // parity of the small-MMA barrier (fused forward, tensor-core layer 2)
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int rt, j;
       tile_coords(tp, t, rt, j);
@@ -493,6 +527,196 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
         // per-tile prefix / block log-likelihood partials (deterministic order)
+        double pre = (valid && m < fp.P) ? ll : 0.0, blk = (valid && m >= fp.P) ? ll : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          pre += __shfl_xor_sync(0xffffffffu, pre, o);
+          blk += __shfl_xor_sync(0xffffffffu, blk, o);
+        }
+        if (lane == 0 && half == 0) {
+          red[lg * 2] = pre;
+          red[lg * 2 + 1] = blk;
+        }
+        named_bar(1, kEpiThreads);
+        if (et == 0) {
+          double* o = fp.ll_part + ((int64_t)j * fp.ll_slots + rt) * 2;
+          o[0] = red[0] + red[2] + red[4] + red[6];
+          o[1] = red[1] + red[3] + red[5] + red[7];
+        }
+      } else if (EPI == kEpiKindFwdTc) {
+        // Layer 2 on the tensor core: A1 = act(Z1 + b1) is written back into
+        // the accumulator's TMEM columns and becomes the A operand of
+        //   z2 = A1 . W2^T   (N = 16, K = NP)   and   dz = delta2 . W2   (N = NP, K = 16),
+        // issued by one epilogue thread; the CUDA cores only do elementwise work.
+        const int n1 = fp.n1, C = fp.C;
+        const int NP = tp.nmma;                 // padded hidden width (TMEM columns of Z1)
+        const int nkb2 = (NP + 31) >> 5;        // 32-wide k blocks of the z2 GEMM
+        uint8_t* eb = (uint8_t*)epi_smem;
+        eb += (1024u - (smem_u32(eb) & 1023u)) & 1023u;
+        uint8_t* W2B = eb;                       // [nkb2][16 rows c][128 B]   B of z2 (K-major, SW128)
+        uint8_t* W2TB = W2B + nkb2 * 2048;      // [NP rows o][128 B]         B of dz (K = c, padded to 32)
+        float* b1s = (float*)(W2TB + NP * 128);  // [NP]
+        float* b2s = b1s + NP;                  // [16]
+        double* red = (double*)(b2s + 16);      // [4][2]
+        uint64_t* sbar = (uint64_t*)(red + 8);  // small-MMA completion barrier
+        if (et == 0 && t == (int)blockIdx.x) {
+          mbar_init(sbar, 1);
+          asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        named_bar(1, kEpiThreads);
+        const float* th = fp.theta + (int64_t)j * fp.Dp;
+        for (int i = et; i < 16 * NP; i += kEpiThreads) {  // W2 (c, o) into both B tiles
+          const int c = i / NP, o = i - c * NP;
+          const float w = (c < C && o < n1) ? tf32_hi(th[fp.woff2 + (int64_t)c * n1 + o]) : 0.f;
+          *(float*)(W2B + sw128_offset(c, o, 16)) = w;
+          *(float*)(W2TB + sw128_offset(o, c, NP)) = w;
+        }
+        for (int i = et; i < NP * 16; i += kEpiThreads) {  // zero the c in [16, 32) half of W2TB rows
+          const int o = i >> 4, c = 16 + (i & 15);
+          *(float*)(W2TB + sw128_offset(o, c, NP)) = 0.f;
+        }
+        for (int i = et; i < NP; i += kEpiThreads) b1s[i] = i < n1 ? th[fp.boff1 + i] : 0.f;
+        for (int i = et; i < 16; i += kEpiThreads) b2s[i] = i < C ? th[fp.boff2 + i] : 0.f;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> MMA reads
+        named_bar(1, kEpiThreads);
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t tcol = tmem_base + (uint32_t)(acc * 256);
+        const uint32_t lane_off = (uint32_t)(lg * 32) << 16;
+        const int64_t m = (int64_t)rt * BM + row_in_tile;
+        const bool valid = m < fp.M;
+        const bool relu = fp.act == DASMC_RELU;
+        const bool wr_out = valid && fp.need_grad;
+        const int nch = NP >> 4, hch = (nch + 1) >> 1;
+        const int c_lo = half ? hch : 0, c_hi = half ? nch : hch;
+        const int64_t ldm = fp.ldm;
+        float* a1T = fp.a1T + (int64_t)j * (n1 + 1) * ldm + m;
+        float* a1Tlo = SPLIT ? fp.a1Tlo + (int64_t)j * (n1 + 1) * ldm + m : nullptr;
+        // pass 1: A1 = act(Z1 + b1) -> TMEM (in place, tf32-rounded) and a1^T
+        for (int ch = c_lo; ch < c_hi; ++ch) {
+          const int o0 = ch * 16;
+          float v[16];
+          tmem_ld16(tcol + lane_off + o0, v);
+          float* pa = a1T + (int64_t)o0 * ldm;
+          float* pal = SPLIT ? a1Tlo + (int64_t)o0 * ldm : nullptr;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            float a = v[q] + b1s[o0 + q];
+            a = relu ? fmaxf(a, 0.f) : tanhf(a);
+            const float hi = tf32_hi(a);
+            v[q] = hi;
+            if (wr_out && o0 + q < n1) {
+              *pa = hi;
+              if (SPLIT) *pal = a - hi;
+            }
+            pa += ldm;
+            if (SPLIT) pal += ldm;
+          }
+          tmem_st16(tcol + lane_off + o0, v);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        named_bar(1, kEpiThreads);
+        if (et == 0) {  // z2 = A1 . W2^T into columns [NP, NP+16)
+          tc_fence_after();
+          const uint32_t id16 = idesc_tf32(16);
+          for (int s = 0; s < NP / 8; ++s)
+            tc_mma_ts(tcol + NP, tcol + 8 * s, smem_desc(W2B + (s >> 2) * 2048) + (uint64_t)((s & 3) * 2), id16,
+                      s > 0);
+          tc_commit(sbar);
+        }
+        mbar_wait(sbar, sph);
+        sph ^= 1;
+        tc_fence_after();
+        float z2[16];
+        tmem_ld16(tcol + lane_off + NP, z2);
+        double ll = 0.0;
+        float d2[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) d2[c] = 0.f;
+        if (valid) {
+          const int yi = fp.y[m];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) z2[c] += b2s[c];
+          double mx = (double)z2[0];
+#pragma unroll
+          for (int c = 1; c < 16; ++c)
+            if (c < C) mx = fmax(mx, (double)z2[c]);
+          double den = 0.0, zy = 0.0;
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (c < C) {
+              den += exp((double)z2[c] - mx);
+              if (c == yi) zy = (double)z2[c];
+            }
+          ll = zy - (mx + log(den));
+          if (fp.need_grad) {
+            const float wrow = m < fp.P ? 1.f : fp.beta_rows;
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+              if (c < C) {
+                const double pr = exp((double)z2[c] - mx) / den;
+                d2[c] = wrow * (float)((c == yi ? 1.0 : 0.0) - pr);
+                if (half == 0) {
+                  const float hi = tf32_hi(d2[c]);
+                  fp.d2T[((int64_t)j * C + c) * ldm + m] = hi;
+                  if (SPLIT) fp.d2Tlo[((int64_t)j * C + c) * ldm + m] = d2[c] - hi;
+                }
+              }
+          }
+        }
+        if (fp.need_grad) {
+          if (half == 0) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) d2[c] = tf32_hi(d2[c]);
+            tmem_st16(tcol + lane_off + NP + 16, d2);
+            tmem_st_wait();
+          }
+          tc_fence_before();
+          named_bar(1, kEpiThreads);
+          if (et == 0) {  // dz = delta2 . W2 into columns [0, NP) (overwrites A1)
+            tc_fence_after();
+            const uint32_t idn = idesc_tf32(NP);
+            tc_mma_ts(tcol, tcol + NP + 16, smem_desc(W2TB), idn, 0);
+            tc_mma_ts(tcol, tcol + NP + 24, smem_desc(W2TB) + 2, idn, 1);
+            tc_commit(sbar);
+          }
+          mbar_wait(sbar, sph);
+          sph ^= 1;
+          tc_fence_after();
+          // pass 2: delta1 = dz . act'(a1), a1 re-read from the a1^T just written (L2)
+          float* d1T = fp.d1T + (int64_t)j * n1 * ldm + m;
+          float* d1Tlo = SPLIT ? fp.d1Tlo + (int64_t)j * n1 * ldm + m : nullptr;
+          for (int ch = c_lo; ch < c_hi; ++ch) {
+            const int o0 = ch * 16;
+            float v[16];
+            tmem_ld16(tcol + lane_off + o0, v);
+            if (!valid) continue;
+            const float* pa = a1T + (int64_t)o0 * ldm;
+            const float* pal = SPLIT ? a1Tlo + (int64_t)o0 * ldm : nullptr;
+            float* pd = d1T + (int64_t)o0 * ldm;
+            float* pdl = SPLIT ? d1Tlo + (int64_t)o0 * ldm : nullptr;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              if (o0 + q < n1) {
+                float a = *pa;
+                if (SPLIT && !relu) a += *pal;
+                const float d1 = relu ? v[q] * (a > 0.f ? 1.f : 0.f) : v[q] * (1.f - a * a);
+                const float hi = tf32_hi(d1);
+                *pd = hi;
+                if (SPLIT) *pdl = d1 - hi;
+              }
+              pa += ldm;
+              pd += ldm;
+              if (SPLIT) {
+                pal += ldm;
+                pdl += ldm;
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
         double pre = (valid && m < fp.P) ? ll : 0.0, blk = (valid && m >= fp.P) ? ll : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -681,6 +905,7 @@ void tc_init(Ctx& c) {
   s->n1 = c.net.sizes[1];
   s->C = c.net.sizes[2];
   s->split = c.precision == DASMC_PREC_3XTF32;
+  if (const char* e = std::getenv("DASMC_TC_LAYER2")) s->tc_layer2 = e[0] != '0';
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -802,6 +1027,16 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     const size_t epi_bytes =
         sizeof(float) * ((size_t)n1 * CP + ((n1 + 3) & ~3) + CP + 2 * 128 * CP) + 8 * sizeof(double) + 16;
     DwParams dp{};
+    const int NP = tp.nmma;
+    if (s->tc_layer2 && NP + 32 <= 256) {
+      // layer 2 on the tensor core (A1 / delta2 as TMEM A operands)
+      const size_t tc_bytes = 1024 + (size_t)((NP + 31) / 32) * 2048 + (size_t)NP * 128 + (size_t)NP * 4 + 64 +
+                              8 * sizeof(double) + 16;
+      if (s->split)
+        launch_tc<kEpiKindFwdTc, true, false, 4>(c, A, Alo, B, Blo, tp, fp, dp, tc_bytes);
+      else
+        launch_tc<kEpiKindFwdTc, false, false, 4>(c, A, Alo, B, Blo, tp, fp, dp, tc_bytes);
+    } else {
     auto go = [&](auto cp) {
       constexpr int K = decltype(cp)::value;
       if (s->split)
@@ -814,6 +1049,7 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
       case 8: go(std::integral_constant<int, 8>{}); break;
       case 12: go(std::integral_constant<int, 12>{}); break;
       default: go(std::integral_constant<int, 16>{}); break;
+    }
     }
   }
   if (!need_grad) return;
