@@ -31,7 +31,8 @@ struct TcState {
   int64_t n_pad = 0;     // X^T row stride (floats)
   int64_t mcap = 0;      // row stride of the transposed activation buffers
   bool split = false;    // split-tf32 (3 MMAs)
-  bool tc_layer2 = true; // fused forward runs layer 2 as TMEM-A MMAs (DASMC_TC_LAYER2=0 disables)
+  bool tc_layer2 = false; // fused forward runs layer 2 as TMEM-A MMAs (opt-in: DASMC_TC_LAYER2=1;
+                          // measured slower on B200: the small MMAs queue behind the next tile's)
   float* Xt = nullptr;   // [(n0+1) x n_pad], row n0 = 1
   float* Xhi = nullptr;  // [n x n0] X rounded to tf32 (cvt.rna): the MMA truncates raw fp32
   float* Xlo = nullptr;  // [n x n0]   (split)
@@ -168,6 +169,24 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+// Asynchronous variant: issue the load, wait later with tmem_wait16 on the
+// same registers (the "+f" operands order every later use after the wait).
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait16(float* v) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]),
+                 "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]), "+f"(v[14]),
+                 "+f"(v[15])::"memory");
 }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
@@ -421,10 +440,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           pa += ldm;
           if (SPLIT) pal += ldm;
         };
-        for (int ch = c_lo; ch < c_hi; ++ch) {
+        auto chunk1 = [&](int ch, const float* v) {
           const int o0 = ch * 16;
-          float v[16];
-          tmem_ld16(taddr + o0, v);
           const int nq = min(16, n1 - o0);  // warp-uniform
           float* pa = a1T + (int64_t)o0 * ldm;
           float* pal = SPLIT ? a1Tlo + (int64_t)o0 * ldm : nullptr;
@@ -436,6 +453,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int q = 0; q < 16; ++q)
               if (q < nq) pass1(v, q, w4, b1s[o0 + q], pa, pal);
+          }
+        };
+        {  // TMEM loads double-buffered: chunk ch+1 is in flight while ch is processed
+          float va[16] = {}, vb[16] = {};
+          int ch = c_lo;
+          if (ch < c_hi) tmem_ld16_async(taddr + ch * 16, va);
+          tmem_wait16(va);
+          while (ch < c_hi) {
+            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, vb);
+            chunk1(ch, va);
+            tmem_wait16(vb);
+            if (++ch >= c_hi) break;
+            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, va);
+            chunk1(ch, vb);
+            tmem_wait16(va);
+            ++ch;
           }
         }
         // combine the two column halves in a fixed order
@@ -505,11 +538,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             pd += ldm;
             if (SPLIT) pdl += ldm;
           };
-          for (int ch = c_lo; ch < c_hi; ++ch) {
+          auto chunk2 = [&](int ch, const float* v) {
+            if (!valid) return;
             const int o0 = ch * 16;
-            float v[16];
-            tmem_ld16(taddr + o0, v);
-            if (!valid) continue;
             const int nq = min(16, n1 - o0);  // warp-uniform
             float* pd = d1T + (int64_t)o0 * ldm;
             float* pdl = SPLIT ? d1Tlo + (int64_t)o0 * ldm : nullptr;
@@ -522,6 +553,20 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int q = 0; q < 16; ++q)
                 if (q < nq) pass2(v, q, w4, b1s[o0 + q], pd, pdl);
             }
+          };
+          float va[16] = {}, vb[16] = {};
+          int ch = c_lo;
+          if (ch < c_hi) tmem_ld16_async(taddr + ch * 16, va);
+          tmem_wait16(va);
+          while (ch < c_hi) {
+            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, vb);
+            chunk2(ch, va);
+            tmem_wait16(vb);
+            if (++ch >= c_hi) break;
+            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, va);
+            chunk2(ch, vb);
+            tmem_wait16(va);
+            ++ch;
           }
         }
         tc_fence_before();
