@@ -52,7 +52,8 @@ namespace {
 
 constexpr int BM = 128;  // UMMA_M
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 12;            // 3 warps per TMEM lane group
+constexpr int kParts = kEpiWarps / 4;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;  // TMA warp + MMA warp + epilogue warps
 constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
@@ -376,12 +377,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ===================== epilogue warps 2..9 =====================
-    // Two warps share each TMEM lane group (warp % 4); `half` splits the
-    // accumulator columns between them.
-    const int et = threadIdx.x - 64;  // 0..255
+    // kParts warps share each TMEM lane group (warp % 4); `part` selects a
+    // contiguous range of 16-column accumulator chunks.
+    const int et = threadIdx.x - 64;
     const int lg = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int part = (warp - 2) >> 2;
+    const int half = part;  // (kept for the opt-in TMEM-A layer-2 path, which needs kParts == 2)
     const int row_in_tile = lg * 32 + lane;
+    auto chunk_range = [&](int nch, int& lo, int& hi) {
+      lo = nch * part / kParts;
+      hi = nch * (part + 1) / kParts;
+    };
     int acc = 0;
     uint32_t aph = 0;
     uint32_t sph = 0;  // parity of the small-MMA barrier (fused forward, tensor-core layer 2)
@@ -393,16 +399,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* W2T = epi_smem;                  // [n1][CP]  W2 transposed, zero-padded
         float* b1s = W2T + (size_t)n1 * CP;     // [n1]
         float* b2s = b1s + ((n1 + 3) & ~3);     // [CP]
-        float* z2x = b2s + CP;                  // [2][128][CP] partial layer-2 logits
-        double* red = (double*)(z2x + 2 * 128 * CP);  // [4][2]
-        named_bar(1, kEpiThreads);
+        float* z2x = b2s + CP;                  // [kParts][128][CP] partial layer-2 logits
+        double* red = (double*)(z2x + kParts * 128 * CP);  // [4][2]
         const float* th = fp.theta + (int64_t)j * fp.Dp;
-        for (int i = et; i < n1 * CP; i += kEpiThreads) {
+        // per-particle layer-2 parameters: all global loads issued before any
+        // shared-memory store (one L2 round trip per tile, not one per element)
+        constexpr int kPer = (256 * CP + kEpiThreads - 1) / kEpiThreads;
+        float wv[kPer];
+#pragma unroll
+        for (int r = 0; r < kPer; ++r) {
+          const int i = et + r * kEpiThreads;
           const int o = i / CP, c = i - o * CP;
-          W2T[i] = c < C ? th[fp.woff2 + (int64_t)c * n1 + o] : 0.f;
+          wv[r] = (i < n1 * CP && c < C) ? th[fp.woff2 + (int64_t)c * n1 + o] : 0.f;
         }
-        for (int i = et; i < n1; i += kEpiThreads) b1s[i] = th[fp.boff1 + i];
-        for (int i = et; i < CP; i += kEpiThreads) b2s[i] = i < C ? th[fp.boff2 + i] : 0.f;
+        const float bv = et < n1 ? th[fp.boff1 + et] : 0.f;
+        const float b2v = et < C ? th[fp.boff2 + et] : 0.f;
+        named_bar(1, kEpiThreads);  // the previous tile is done with the shared parameters
+#pragma unroll
+        for (int r = 0; r < kPer; ++r) {
+          const int i = et + r * kEpiThreads;
+          if (i < n1 * CP) W2T[i] = wv[r];
+        }
+        if (et < n1) b1s[et] = bv;
+        if (et < CP) b2s[et] = b2v;
         named_bar(1, kEpiThreads);
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
@@ -411,8 +430,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool valid = m < fp.M;
         const bool relu = fp.act == DASMC_RELU;
         const bool wr_out = valid && fp.need_grad;
-        const int nch = (n1 + 15) >> 4, hch = (nch + 1) >> 1;
-        const int c_lo = half ? hch : 0, c_hi = half ? nch : hch;
+        int c_lo, c_hi;
+        chunk_range((n1 + 15) >> 4, c_lo, c_hi);
         const int64_t ldm = fp.ldm;
         const float4* W2T4 = reinterpret_cast<const float4*>(W2T);
         float z2[CP];
@@ -471,15 +490,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++ch;
           }
         }
-        // combine the two column halves in a fixed order
-        float* zx = z2x + ((size_t)half * 128 + row_in_tile) * CP;
+        // combine the column parts in a fixed order
+        float* zx = z2x + ((size_t)part * 128 + row_in_tile) * CP;
 #pragma unroll
         for (int c = 0; c < CP; ++c) zx[c] = z2[c];
         named_bar(1, kEpiThreads);
-        const float* z0 = z2x + (size_t)row_in_tile * CP;
-        const float* z1p = z2x + ((size_t)128 + row_in_tile) * CP;
 #pragma unroll
-        for (int c = 0; c < CP; ++c) z2[c] = (z0[c] + z1p[c]) + b2s[c];
+        for (int c = 0; c < CP; ++c) {
+          float s = z2x[(size_t)row_in_tile * CP + c];
+#pragma unroll
+          for (int p = 1; p < kParts; ++p) s += z2x[((size_t)p * 128 + row_in_tile) * CP + c];
+          z2[c] = s + b2s[c];
+        }
         // log-softmax likelihood of the row in fp64 (network.hpp:183-193)
         double ll = 0.0;
         float d2[CP];
@@ -506,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (c < C) {
                 const double pr = exp((double)z2[c] - mx) / den;
                 d2[c] = wrow * (float)((c == yi ? 1.0 : 0.0) - pr);
-                if (half == 0) {
+                if (part == 0) {
                   const float hi = tf32_hi(d2[c]);
                   fp.d2T[((int64_t)j * C + c) * ldm + m] = hi;
                   if (SPLIT) fp.d2Tlo[((int64_t)j * C + c) * ldm + m] = d2[c] - hi;
@@ -632,8 +654,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool valid = m < fp.M;
         const bool relu = fp.act == DASMC_RELU;
         const bool wr_out = valid && fp.need_grad;
-        const int nch = NP >> 4, hch = (nch + 1) >> 1;
-        const int c_lo = half ? hch : 0, c_hi = half ? nch : hch;
+        int c_lo, c_hi;
+        chunk_range(NP >> 4, c_lo, c_hi);
         const int64_t ldm = fp.ldm;
         float* a1T = fp.a1T + (int64_t)j * (n1 + 1) * ldm + m;
         float* a1Tlo = SPLIT ? fp.a1Tlo + (int64_t)j * (n1 + 1) * ldm + m : nullptr;
@@ -786,8 +808,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int i = rt * BM + row_in_tile;
         const bool valid = i <= dp.in;
         const int64_t base = (int64_t)j * dp.Dp;
-        const int nch = (dp.n_out + 15) >> 4, hch = (nch + 1) >> 1;
-        const int c_lo = half ? hch : 0, c_hi = half ? nch : hch;
+        int c_lo, c_hi;
+        chunk_range((dp.n_out + 15) >> 4, c_lo, c_hi);
         for (int ch = c_lo; ch < c_hi; ++ch) {
           const int o0 = ch * 16;
           float v[16];
@@ -1070,7 +1092,7 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     // classes padded to a multiple of 4 (float4 rows of W2^T in shared memory)
     const int CP = (C + 3) / 4 * 4;
     const size_t epi_bytes =
-        sizeof(float) * ((size_t)n1 * CP + ((n1 + 3) & ~3) + CP + 2 * 128 * CP) + 8 * sizeof(double) + 16;
+        sizeof(float) * ((size_t)n1 * CP + ((n1 + 3) & ~3) + CP + kParts * 128 * CP) + 8 * sizeof(double) + 16;
     DwParams dp{};
     const int NP = tp.nmma;
     if (s->tc_layer2 && NP + 32 <= 256) {
