@@ -232,6 +232,7 @@ struct FwdParams {
   float *a1T, *d1T, *d2T, *a1Tlo, *d1Tlo, *d2Tlo;
   double* ll_part;
   int ll_slots;
+  int dbg;  // DASMC_DEBUG_EPI: 1 = skip global stores, 2 = skip pass 2, 3 = skip the whole epilogue math
 };
 
 struct DwParams {
@@ -429,9 +430,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t m = (int64_t)rt * BM + row_in_tile;
         const bool valid = m < fp.M;
         const bool relu = fp.act == DASMC_RELU;
-        const bool wr_out = valid && fp.need_grad;
+        const bool wr_out = valid && fp.need_grad && fp.dbg != 1;
         int c_lo, c_hi;
         chunk_range((n1 + 15) >> 4, c_lo, c_hi);
+        if (fp.dbg == 3) c_hi = c_lo;
         const int64_t ldm = fp.ldm;
         const float4* W2T4 = reinterpret_cast<const float4*>(W2T);
         float z2[CP];
@@ -495,48 +497,61 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < CP; ++c) zx[c] = z2[c];
         named_bar(1, kEpiThreads);
-#pragma unroll
-        for (int c = 0; c < CP; ++c) {
-          float s = z2x[(size_t)row_in_tile * CP + c];
-#pragma unroll
-          for (int p = 1; p < kParts; ++p) s += z2x[((size_t)p * 128 + row_in_tile) * CP + c];
-          z2[c] = s + b2s[c];
-        }
-        // log-softmax likelihood of the row in fp64 (network.hpp:183-193)
+        // part 0 alone: log-softmax likelihood of the row (network.hpp:183-193) --
+        // fp32 exponentials, fp64 log-normaliser and ll -- and delta2, shared via
+        // its z2x slot with the other parts
         double ll = 0.0;
         float d2[CP];
 #pragma unroll
         for (int c = 0; c < CP; ++c) d2[c] = 0.f;
-        if (valid) {
-          const int yi = fp.y[m];
-          double mx = (double)z2[0];
+        if (part == 0) {
 #pragma unroll
-          for (int c = 1; c < CP; ++c)
-            if (c < C) mx = fmax(mx, (double)z2[c]);
-          double den = 0.0, zy = 0.0;
+          for (int c = 0; c < CP; ++c) {
+            float s = z2x[(size_t)row_in_tile * CP + c];
 #pragma unroll
-          for (int c = 0; c < CP; ++c)
-            if (c < C) {
-              den += exp((double)z2[c] - mx);
-              if (c == yi) zy = (double)z2[c];
+            for (int p = 1; p < kParts; ++p) s += z2x[((size_t)p * 128 + row_in_tile) * CP + c];
+            z2[c] = s + b2s[c];
+          }
+          if (valid) {
+            const int yi = fp.y[m];
+            float mx = z2[0];
+#pragma unroll
+            for (int c = 1; c < CP; ++c)
+              if (c < C) mx = fmaxf(mx, z2[c]);
+            float e[CP];
+            double den = 0.0;
+            float zy = 0.f;
+#pragma unroll
+            for (int c = 0; c < CP; ++c) {
+              e[c] = c < C ? expf(z2[c] - mx) : 0.f;
+              den += (double)e[c];
+              if (c == yi) zy = z2[c];
             }
-          ll = zy - (mx + log(den));
-          if (fp.need_grad) {
-            const float wrow = m < fp.P ? 1.f : fp.beta_rows;
+            ll = (double)zy - ((double)mx + log(den));
+            if (fp.need_grad) {
+              const float wrow = m < fp.P ? 1.f : fp.beta_rows;
+              const float rden = (float)(1.0 / den);
 #pragma unroll
-            for (int c = 0; c < CP; ++c)
-              if (c < C) {
-                const double pr = exp((double)z2[c] - mx) / den;
-                d2[c] = wrow * (float)((c == yi ? 1.0 : 0.0) - pr);
-                if (part == 0) {
+              for (int c = 0; c < CP; ++c)
+                if (c < C) {
+                  d2[c] = wrow * ((c == yi ? 1.f : 0.f) - e[c] * rden);
                   const float hi = tf32_hi(d2[c]);
                   fp.d2T[((int64_t)j * C + c) * ldm + m] = hi;
                   if (SPLIT) fp.d2Tlo[((int64_t)j * C + c) * ldm + m] = d2[c] - hi;
                 }
-              }
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < CP; ++c) zx[c] = d2[c];
+        }
+        if (fp.need_grad && fp.dbg == 0) {
+          named_bar(1, kEpiThreads);
+          if (part != 0) {
+#pragma unroll
+            for (int c = 0; c < CP; ++c) d2[c] = z2x[(size_t)row_in_tile * CP + c];
           }
         }
-        if (fp.need_grad) {
+        if (fp.need_grad && fp.dbg == 0) {
           // pass 2: delta1 = (W2^T delta2) . act'(a1)  (network.hpp:209-215)
           float* d1T = fp.d1T + (int64_t)j * n1 * ldm + m;
           float* d1Tlo = SPLIT ? fp.d1Tlo + (int64_t)j * n1 * ldm + m : nullptr;
@@ -942,7 +957,7 @@ void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUten
   const size_t fixed = 1024 + 64 * 8 + 64 + epi_smem_bytes;
   const size_t budget = 227 * 1024;
   int stages = (int)std::min<size_t>(6, (budget - fixed) / stage_bytes);
-  if (stages < 2) throw CudaError{"tensor-core tile does not fit in shared memory"};
+  if (stages < 1) throw CudaError{"tensor-core tile does not fit in shared memory"};
   tp.stages = stages;
   tp.stage_bytes_tx = (uint32_t)(sub * ((size_t)BM * BK * 4 + (size_t)tp.brows * BK * 4));
   const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16 + epi_smem_bytes + 64;
@@ -1089,6 +1104,7 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     fp.d2Tlo = s->d2Tlo;
     fp.ll_part = c.ll_part;
     fp.ll_slots = c.ll_slots;
+    if (const char* e = std::getenv("DASMC_DEBUG_EPI")) fp.dbg = std::atoi(e);  // profiling only
     // classes padded to a multiple of 4 (float4 rows of W2^T in shared memory)
     const int CP = (C + 3) / 4 * 4;
     const size_t epi_bytes =
