@@ -54,6 +54,10 @@ constexpr int BM = 128;  // UMMA_M
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row
 constexpr int kEpiWarps = 12;            // 3 warps per TMEM lane group
 constexpr int kParts = kEpiWarps / 4;
+// Epilogue a1^T / delta1^T stores through TMA bulk tensor stores instead of
+// st.global.  Correct (tested) but measured slower on B200 at C2 (38.8 vs
+// 36.2 ms per forward: the 48 KB staging costs a pipeline stage), so off.
+constexpr bool kUseTmaStore = false;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;  // TMA warp + MMA warp + epilogue warps
 constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
@@ -109,6 +113,15 @@ __device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, uint64
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// Bulk tensor store smem -> global (bulk async-group of the issuing thread).
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
 }
@@ -221,6 +234,8 @@ struct TileParams {
 };
 
 struct FwdParams {
+  CUtensorMap mapS1;   // a1^T store map  {M, n1, J}, box {32, 16, 1}
+  CUtensorMap mapS2;   // delta1^T store map
   const float* theta;  // theta_in
   int64_t Dp, boff1, woff2, boff2;
   int n1, C, act;
@@ -256,7 +271,10 @@ template <int EPI, bool SPLIT, bool A3D, int CP>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
               const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo, TileParams tp,
-              FwdParams fp, DwParams dp) {
+              const __grid_constant__ FwdParams fp, DwParams dp) {
+  constexpr bool kTmaStore = kUseTmaStore && EPI == kEpiKindFwd && !SPLIT;
+  const CUtensorMap& mapS1 = fp.mapS1;
+  const CUtensorMap& mapS2 = fp.mapS2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128B swizzle atoms; keep the pointer derived
   // from smem_raw so the compiler emits shared-memory (LDS/STS) accesses.
@@ -392,6 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t aph = 0;
     uint32_t sph = 0;  // parity of the small-MMA barrier (fused forward, tensor-core layer 2)
+    int nst = 0;       // TMA-store staging buffer counter (alternates the warp's two buffers)
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int rt, j;
       tile_coords(tp, t, rt, j);
@@ -402,6 +421,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* b2s = b1s + ((n1 + 3) & ~3);     // [CP]
         float* z2x = b2s + CP;                  // [kParts][128][CP] partial layer-2 logits
         double* red = (double*)(z2x + kParts * 128 * CP);  // [4][2]
+        float* stg_all = (float*)((uint8_t*)(red + 8) + ((128u - (smem_u32(red + 8) & 127u)) & 127u));
+        float* stg = stg_all + (warp - 2) * 1024;  // 2 x [16][32] fp32 per warp
         const float* th = fp.theta + (int64_t)j * fp.Dp;
         // per-particle layer-2 parameters: all global loads issued before any
         // shared-memory store (one L2 round trip per tile, not one per element)
@@ -442,7 +463,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* a1T = fp.a1T + (int64_t)j * (n1 + 1) * ldm + m;
         float* a1Tlo = SPLIT ? fp.a1Tlo + (int64_t)j * (n1 + 1) * ldm + m : nullptr;
         // pass 1: a1 = act(z1 + b1); partial z2 = W2 a1 over this warp's columns
-        auto pass1 = [&](const float* v, int q, const float4* w4, float b, float*& pa, float*& pal) {
+        // TMA-store staging (non-split): the warp's 32 rows x 16 columns go to a
+        // [16][32] smem tile, one bulk tensor store per chunk (clipped at m >= M, o >= n1)
+        const bool st_any = kTmaStore && fp.need_grad && fp.dbg != 1;
+        auto stage_begin = [&]() -> float* {
+          float* buf = stg + (nst & 1) * 512;
+          if (lane == 0) bulk_wait_read1();  // the store that last used this buffer has read it
+          __syncwarp();
+          return buf;
+        };
+        auto stage_end = [&](const CUtensorMap* map, float* buf, int o0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(map, buf, rt * BM + lg * 32, o0, j);
+            bulk_commit();
+          }
+          ++nst;
+        };
+        auto pass1 = [&](const float* v, int q, const float4* w4, float b, float*& pa, float*& pal, float* sb) {
           float a = v[q] + b;
           a = relu ? fmaxf(a, 0.f) : tanhf(a);
 #pragma unroll
@@ -453,13 +492,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             z2[4 * u + 2] = fmaf(a, w.z, z2[4 * u + 2]);
             z2[4 * u + 3] = fmaf(a, w.w, z2[4 * u + 3]);
           }
-          if (wr_out) {
-            const float hi = tf32_hi(a);
-            *pa = hi;
-            if (SPLIT) *pal = a - hi;
+          if (kTmaStore) {
+            if (st_any) sb[q * 32 + lane] = tf32_hi(a);
+          } else {
+            if (wr_out) {
+              const float hi = tf32_hi(a);
+              *pa = hi;
+              if (SPLIT) *pal = a - hi;
+            }
+            pa += ldm;
+            if (SPLIT) pal += ldm;
           }
-          pa += ldm;
-          if (SPLIT) pal += ldm;
         };
         auto chunk1 = [&](int ch, const float* v) {
           const int o0 = ch * 16;
@@ -467,14 +510,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           float* pa = a1T + (int64_t)o0 * ldm;
           float* pal = SPLIT ? a1Tlo + (int64_t)o0 * ldm : nullptr;
           const float4* w4 = W2T4 + o0 * (CP / 4);
+          float* sb = st_any ? stage_begin() : nullptr;
           if (nq == 16) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) pass1(v, q, w4, b1s[o0 + q], pa, pal);
+            for (int q = 0; q < 16; ++q) pass1(v, q, w4, b1s[o0 + q], pa, pal, sb);
           } else {  // tail chunk: still unrolled so v[] stays in registers
 #pragma unroll
             for (int q = 0; q < 16; ++q)
-              if (q < nq) pass1(v, q, w4, b1s[o0 + q], pa, pal);
+              if (q < nq) pass1(v, q, w4, b1s[o0 + q], pa, pal, sb);
           }
+          if (st_any) stage_end(&mapS1, sb, o0);
         };
         {  // TMEM loads double-buffered: chunk ch+1 is in flight while ch is processed
           float va[16] = {}, vb[16] = {};
@@ -555,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // pass 2: delta1 = (W2^T delta2) . act'(a1)  (network.hpp:209-215)
           float* d1T = fp.d1T + (int64_t)j * n1 * ldm + m;
           float* d1Tlo = SPLIT ? fp.d1Tlo + (int64_t)j * n1 * ldm + m : nullptr;
-          auto pass2 = [&](const float* v, int q, const float4* w4, float b, float*& pd, float*& pdl) {
+          auto pass2 = [&](const float* v, int q, const float4* w4, float b, float*& pd, float*& pdl, float* sb) {
             float a = v[q] + b;
             a = relu ? fmaxf(a, 0.f) : tanhf(a);
             float dx = 0.f, dy = 0.f, dzz = 0.f, dw = 0.f;  // 4 independent chains
@@ -570,26 +615,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float dz = (dx + dy) + (dzz + dw);
             const float d1 = relu ? dz * (a > 0.f ? 1.f : 0.f) : dz * (1.f - a * a);
             const float hi = tf32_hi(d1);
-            *pd = hi;
-            if (SPLIT) *pdl = d1 - hi;
-            pd += ldm;
-            if (SPLIT) pdl += ldm;
+            if (kTmaStore) {
+              sb[q * 32 + lane] = hi;
+            } else {
+              if (valid) {
+                *pd = hi;
+                if (SPLIT) *pdl = d1 - hi;
+              }
+              pd += ldm;
+              if (SPLIT) pdl += ldm;
+            }
           };
           auto chunk2 = [&](int ch, const float* v) {
-            if (!valid) return;
             const int o0 = ch * 16;
             const int nq = min(16, n1 - o0);  // warp-uniform
             float* pd = d1T + (int64_t)o0 * ldm;
             float* pdl = SPLIT ? d1Tlo + (int64_t)o0 * ldm : nullptr;
             const float4* w4 = W2T4 + o0 * (CP / 4);
+            float* sb = kTmaStore ? stage_begin() : nullptr;
             if (nq == 16) {
 #pragma unroll
-              for (int q = 0; q < 16; ++q) pass2(v, q, w4, b1s[o0 + q], pd, pdl);
+              for (int q = 0; q < 16; ++q) pass2(v, q, w4, b1s[o0 + q], pd, pdl, sb);
             } else {
 #pragma unroll
               for (int q = 0; q < 16; ++q)
-                if (q < nq) pass2(v, q, w4, b1s[o0 + q], pd, pdl);
+                if (q < nq) pass2(v, q, w4, b1s[o0 + q], pd, pdl, sb);
             }
+            if (kTmaStore) stage_end(&mapS2, sb, o0);
           };
           float va[16] = {}, vb[16] = {};
           int ch = c_lo;
@@ -846,6 +898,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) aph ^= 1;
     }
+    if (kTmaStore && lane == 0) bulk_wait_all();  // outstanding epilogue stores done
   }
   __syncthreads();
   if (warp == 1) {
@@ -922,14 +975,24 @@ EncodeTiledFn encode_fn() {
 }
 
 // rank-2/3 fp32 tensor, innermost dim first; strides in bytes for dims >= 1.
-CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides, const uint32_t* box) {
+CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   uint32_t es[3] = {1, 1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base),
-                                 dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError{"cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
   return m;
+}
+
+// Store map of a transposed activation buffer [J][rows_alloc][ld]: valid extent
+// {M, rows} (stores beyond are clipped), box = one warp's 32 rows x 16 columns.
+CUtensorMap map_store(const float* base, uint64_t M, uint64_t rows, uint64_t ld, uint64_t J, uint64_t pstride) {
+  const uint64_t dims[3] = {M, rows, J};
+  const uint64_t strides[2] = {ld * 4, pstride * 4};
+  const uint32_t box[3] = {32, 16, 1};
+  return make_map(base, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
 CUtensorMap map2d(const float* base, uint64_t inner, uint64_t rows, uint64_t ld, uint32_t box_rows) {
@@ -1108,7 +1171,12 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     // classes padded to a multiple of 4 (float4 rows of W2^T in shared memory)
     const int CP = (C + 3) / 4 * 4;
     const size_t epi_bytes =
-        sizeof(float) * ((size_t)n1 * CP + ((n1 + 3) & ~3) + CP + kParts * 128 * CP) + 8 * sizeof(double) + 16;
+        sizeof(float) * ((size_t)n1 * CP + ((n1 + 3) & ~3) + CP + kParts * 128 * CP) + 8 * sizeof(double) + 16 +
+        (s->split || !kUseTmaStore ? 0 : 128 + (size_t)kEpiWarps * 4096);  // TMA-store staging
+    if (!s->split && kUseTmaStore) {
+      fp.mapS1 = map_store(s->a1T, M, n1, ldm, J, (uint64_t)(n1 + 1) * ldm);
+      fp.mapS2 = map_store(s->d1T, M, n1, ldm, J, (uint64_t)n1 * ldm);
+    }
     DwParams dp{};
     const int NP = tp.nmma;
     if (s->tc_layer2 && NP + 32 <= 256) {
