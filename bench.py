@@ -10,8 +10,9 @@ HMC S = 3, h = 0.002), run at the schedule's iterations k0 .. k0+W+K-1.
 metric = particle-sample grad evals/sec = sum_k J (S+1) M_k / time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-Multi-GPU (torchrun): each rank runs its own C2 ensemble ("replicas", weak
-scaling) -- the sharded single-ensemble path is DESIGN.md §7.
+Multi-GPU (torchrun): one particle-sharded ensemble of J = 1024 x N (weak
+scaling): NCCL all-gather of the log-weights, redundant resampling indices,
+point-to-point particle migration (paper_2601_21983_b200/dist.py).
 """
 from __future__ import annotations
 
@@ -193,33 +194,49 @@ def run_ours(args, w):
     Ms = [window(w, k) for k in ks]
     L.check(lib.dasmc_gpu_reserve_rows(t.h, max(window(w, k) for k in ks_warm + ks + [k0])))
     t.set_target(0, window(w, k0), N, "scaled", 1.0, 1.0)
-    t.init_ensemble(J, 0)
+    # world > 1: one particle-sharded ensemble of J_total = J * world (weak scaling,
+    # paper_2601_21983_b200/dist.py); this rank owns global slots [j0, j0 + J)
+    J_total = J * world
+    j0 = J * rank
+    L.check(lib.dasmc_gpu_init_ensemble_at(t.h, J, 0, j0))
     th0, lw0, _ = t.get_ensemble(J, dtype=np.float32)
     t.set_ensemble(th0, lw0, k0)
     kc = p.KernelConfig.hmc(w["h"], S)
     rk = args.resample
+    sharded_recs = []
+    if world > 1:
+        from paper_2601_21983_b200.dist import GpuShardEngine, TorchComm, sharded_step
+        engine, comm = GpuShardEngine(t), TorchComm(torch.device("cuda", local))
+
+        def step(k, sync=False):
+            t.set_target(0, window(w, k), N, "scaled", 1.0, 1.0)
+            sharded_recs.append(sharded_step(engine, comm, J_total, kc, 0, rk, 0.5, False, torch.device("cuda", local)))
+    else:
+        def step(k, sync=False):
+            t.set_target(0, window(w, k), N, "scaled", 1.0, 1.0)
+            t.smc_step(kc, 0, rk, 0.5, sync=sync)
     for k in ks_warm:
-        t.set_target(0, window(w, k), N, "scaled", 1.0, 1.0)
-        t.smc_step(kc, 0, rk, 0.5, sync=False)
-    t.sync_records(0)
-    stream = torch.cuda.ExternalStream(lib.dasmc_gpu_stream(t.h))
+        step(k)
+    if world == 1:
+        t.sync_records(0)
+    stream = torch.cuda.ExternalStream(lib.dasmc_gpu_stream(t.h)) if world == 1 else torch.cuda.current_stream()
     L.check(lib.dasmc_gpu_set_timing(t.h, 1))
     n_launch0 = lib.dasmc_launch_count()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    sharded_recs.clear()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
         for k in ks:
-            t.set_target(0, window(w, k), N, "scaled", 1.0, 1.0)
-            t.smc_step(kc, 0, rk, 0.5, sync=False)
+            step(k)
         e1.record(stream)
         e1.synchronize()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     launches = lib.dasmc_launch_count() - n_launch0
-    recs = t.sync_records(len(ks))
+    recs = t.sync_records(len(ks)) if world == 1 else sharded_recs
     kms = np.zeros(3)
     kcnt = np.zeros(3, dtype=np.int64)
     L.check(lib.dasmc_gpu_kernel_times(t.h, kms.ctypes.data_as(L._D), kcnt.ctypes.data_as(L._I64)))
@@ -250,8 +267,7 @@ def run_ours(args, w):
     for i in range(e2e_steps):
         k = ks[i]
         t.set_ensemble(th_h, lw_h, k)  # H2D: theta (fp32, reference layout) + log-weights
-        t.set_target(0, window(w, k), N, "scaled", 1.0, 1.0)
-        t.smc_step(kc, 0, rk, 0.5, sync=True)
+        step(k, sync=True)
         L.check(lib.dasmc_gpu_get_ensemble_f32(t.h, th_h.ctypes.data_as(L._F), lw_h.ctypes.data_as(L._D), None))
         e2e_units += J * (S + 1) * window(w, k)
     e2e_s = time.perf_counter() - t0
@@ -308,7 +324,9 @@ def run_ours(args, w):
                 "config": {"workload": w["desc"], "particles_per_gpu": J, "iterations": [ks[0], ks[-1]],
                            "window_rows": [Ms[0], Ms[-1]], "precision": args.precision, "resample": rk,
                            "l2": "inputs larger than L2 (activations >= 24 GB per step)",
-                           "parallelism": f"{world} independent ensemble replica(s), one per GPU"},
+                           "parallelism": (f"one particle-sharded ensemble of J={J * world} over {world} GPUs "
+                                           "(NCCL all-gather of log-weights, P2P particle migration)"
+                                           if world > 1 else "single GPU")},
                 "iterations_per_sec": args.steps / (ms_max / 1e3),
                 "particle_grad_evals_per_sec": world * J * (S + 1) * args.steps / (ms_max / 1e3),
                 "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof,

@@ -215,6 +215,46 @@ int dasmc_shuffle_permutation(uint64_t seed, int64_t n, int64_t* perm);
  * (otherwise they grow on first use, which synchronises the stream). */
 int dasmc_gpu_reserve_rows(dasmc_ctx* ctx, int64_t M);
 
+/* ---- particle sharding across GPUs -------------------------------------
+ * Rank r of G owns global particle slots [lo, hi) = [r*J/G, (r+1)*J/G)
+ * (parallel.hpp:30-31's static partition).  Every RNG stream is keyed by the
+ * GLOBAL slot, so results do not depend on G.  One iteration:
+ *   1. dasmc_gpu_shard_propose   -- local move + incremental weights of own slots
+ *   2. all-gather of the local (log_w, log_target_new) vectors  (torch.distributed / NCCL)
+ *   3. dasmc_gpu_shard_resample  -- normalise / ESS / decision / indices on the FULL
+ *      vectors, computed redundantly (identically) on every rank
+ *   4. dasmc_shard_plan + pack / point-to-point exchange / unpack of theta rows. */
+void dasmc_shard_range(int64_t J, int world, int rank, int64_t* lo, int64_t* hi);
+/* init_ensemble of the shard holding global slots [j_offset, j_offset + J)
+ * (streams fork(kInit, j_offset + j), smc.hpp:82). */
+int dasmc_gpu_init_ensemble_at(dasmc_ctx* ctx, int64_t J, uint64_t seed, int64_t j_offset);
+/* Migration plan for `rank` given the global indices idx[J] (out[j] = in[idx[j]]):
+ *   recv_src[Jr]   owner rank of each local destination slot (local slot order)
+ *   recv_row[Jr]   the source's LOCAL row
+ *   send_cnt[G]    rows this rank sends to each rank (self included)
+ *   send_rows[..]  this rank's local rows, grouped by destination rank, each group
+ *                  in the destination's slot order (size = sum send_cnt <= J). */
+int dasmc_shard_plan(const int32_t* idx, int64_t J, int world, int rank, int32_t* recv_src, int32_t* recv_row,
+                     int64_t* send_cnt, int32_t* send_rows);
+/* Propose + reweight the context's J_local particles, which are global slots
+ * [j_offset, j_offset + J_local).  Writes the new (unnormalised) log-weights and
+ * log_target_new of the local slots into caller DEVICE buffers (synchronous). */
+int dasmc_gpu_shard_propose(dasmc_ctx* ctx, const dasmc_kernel_cfg* cfg, uint64_t seed, int64_t j_offset,
+                            double* log_w_dev, double* log_target_new_dev);
+/* Normalise / ESS / mean_log_target / resample decision and indices over the
+ * gathered FULL vectors (device pointers, J_total entries, reference order);
+ * writes idx_dev[J_total] (identity if not resampled), updates the local
+ * log-weight slice, returns the record.  Positions are finalised locally
+ * (divergent particles keep theta, smc.hpp:129-131). */
+int dasmc_gpu_shard_resample(dasmc_ctx* ctx, const double* log_w_full_dev, const double* log_target_new_full_dev,
+                             int64_t J_total, int64_t j_offset, uint64_t seed, int resample_kind, double fraction,
+                             int resample_always, int32_t* idx_dev, dasmc_iter_record* record);
+/* theta rows (internal device layout, row stride dasmc_gpu_row_floats floats):
+ * pack local rows[n] into dst_dev; unpack src_dev into local slots[n] of the next ensemble. */
+int64_t dasmc_gpu_row_floats(const dasmc_ctx* ctx);
+int dasmc_gpu_pack_rows(dasmc_ctx* ctx, const int32_t* rows, int64_t n, float* dst_dev);
+int dasmc_gpu_unpack_rows(dasmc_ctx* ctx, const float* src_dev, const int32_t* slots, int64_t n);
+
 /* ---- instrumentation (bench.py) ------------------------------------------------------ */
 /* The context's CUDA stream (cudaStream_t) -- every kernel of the context runs on it. */
 void* dasmc_gpu_stream(dasmc_ctx* ctx);

@@ -255,6 +255,46 @@ int oracle_smc_step(const int* layers, int nl, int act, const double* X, const i
   });
 }
 
+// The parallel part of smc_step (smc.hpp:118-138) for a SUBSET of particles
+// whose global slots are gj[n]: propose with fork(kProposal, k, gj) and the
+// incremental weight; divergent particles keep theta and get -inf.
+// thetas (n*D) updated in place; inc[n], lt_new[n] out.
+int oracle_propose_particles(const int* layers, int nl, int act, const double* X, const int* y, int64_t n_data,
+                             int64_t prefix_end, int64_t block_end, int64_t total_n, int mode, double beta,
+                             double sigma, double step_size, int leapfrog_steps, int kernel_kind, uint64_t seed,
+                             int k, const int64_t* gj, int64_t n, int threads, double* thetas, double* inc,
+                             double* lt_new) {
+  return guarded([&] {
+    const NetSpec net = net_of(layers, nl, act);
+    const Dataset d = dataset_of(X, y, n_data, layers[0], layers[nl - 1]);
+    TargetContext c;
+    c.data = &d;
+    c.window = SubsetWindow{prefix_end, block_end, total_n};
+    c.mode = (TargetMode)mode;
+    c.beta = beta;
+    c.prior.sigma = sigma;
+    c.model = net;
+    validate(c);
+    const int64_t D = param_count(net);
+    KernelConfig kc{step_size, leapfrog_steps, (KernelKind)kernel_kind};
+    KernelConfig::validate(kc);
+    const RngStream root(seed);
+    parallel_for(n, threads, [&](int64_t i) {
+      RngStream s = root.fork(tag::kProposal, (std::uint64_t)k, (std::uint64_t)gj[i]);
+      const Vec th(thetas + i * D, thetas + (i + 1) * D);
+      const ProposalResult p = propose(ContextTarget{&c}, th, kc, s);
+      if (p.divergent) {
+        inc[i] = kNegInf;
+        lt_new[i] = p.log_target_new;
+      } else {
+        std::memcpy(thetas + i * D, p.theta_new.data(), sizeof(double) * (size_t)D);
+        inc[i] = incremental_log_weight(p.log_target_new, p.log_target_old, p.p_initial, p.p_final);
+        lt_new[i] = p.log_target_new;
+      }
+    });
+  });
+}
+
 // init_ensemble (smc.hpp:73-89) on a scaled/sda context.
 int oracle_init_ensemble(const int* layers, int nl, int act, const double* X, const int* y, int64_t n,
                          int64_t prefix_end, int64_t block_end, int64_t total_n, int mode, double beta,

@@ -213,6 +213,24 @@ def smc_step(layers, act, X, y, window, mode, beta, sigma, kernel, seed, fractio
     return th, lw, it.value, rec, d
 
 
+def propose_particles(layers, act, X, y, window, mode, beta, sigma, kernel, seed, k, gj, thetas, threads=8):
+    """smc.hpp:118-138 for a subset of particles with global slots gj; returns (thetas, inc, lt_new)."""
+    arr, nl = _net(layers)
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    th = np.array(thetas, dtype=np.float64, copy=True, order="C")
+    gj = np.ascontiguousarray(gj, dtype=np.int64)
+    n = th.shape[0]
+    inc, lt = np.empty(n), np.empty(n)
+    P, M, N = window
+    h, S, kk = kernel
+    _check(lib().oracle_propose_particles(arr, nl, act, _dp(X), _ip(y), C.c_int64(X.shape[0]), C.c_int64(P),
+                                          C.c_int64(M), C.c_int64(N), mode, C.c_double(beta), C.c_double(sigma),
+                                          C.c_double(h), S, kk, C.c_uint64(seed), k, gj.ctypes.data_as(_I64),
+                                          C.c_int64(n), threads, _dp(th), _dp(inc), _dp(lt)))
+    return th, inc, lt
+
+
 def resample_indices(w, u, kind):
     w = np.ascontiguousarray(w, dtype=np.float64)
     u = np.ascontiguousarray(u, dtype=np.float64)

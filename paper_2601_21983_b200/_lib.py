@@ -117,6 +117,15 @@ SIGNATURES = {
     "dasmc_sda_moments_from": (C.c_int, [_D, _D, _D, C.c_int64, _D]),
     "dasmc_make_teacher_data": (C.c_int, [C.POINTER(NetDesc), C.c_int64, C.c_int, C.c_uint64, C.c_uint64, C.c_int, _F, _I32]),
     "dasmc_shuffle_permutation": (C.c_int, [C.c_uint64, C.c_int64, _I64]),
+    "dasmc_shard_range": (None, [C.c_int64, C.c_int, C.c_int, _I64, _I64]),
+    "dasmc_gpu_init_ensemble_at": (C.c_int, [_P, C.c_int64, C.c_uint64, C.c_int64]),
+    "dasmc_shard_plan": (C.c_int, [_I32, C.c_int64, C.c_int, C.c_int, _I32, _I32, _I64, _I32]),
+    "dasmc_gpu_shard_propose": (C.c_int, [_P, C.POINTER(KernelCfg), C.c_uint64, C.c_int64, C.c_void_p, C.c_void_p]),
+    "dasmc_gpu_shard_resample": (C.c_int, [_P, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_uint64, C.c_int,
+                                           C.c_double, C.c_int, C.c_void_p, C.POINTER(IterRecord)]),
+    "dasmc_gpu_row_floats": (C.c_int64, [_P]),
+    "dasmc_gpu_pack_rows": (C.c_int, [_P, _I32, C.c_int64, C.c_void_p]),
+    "dasmc_gpu_unpack_rows": (C.c_int, [_P, C.c_void_p, _I32, C.c_int64]),
     "dasmc_gpu_reserve_rows": (C.c_int, [_P, C.c_int64]),
     "dasmc_gpu_stream": (C.c_void_p, [_P]),
     "dasmc_launch_count": (C.c_int64, []),

@@ -92,7 +92,7 @@ void free_ctx(Ctx& c) {
   tc_free(c);
   void* ptrs[] = {c.X, c.Xt, c.y, c.theta[0], c.theta[1], c.theta[2], c.p, c.grad, c.logw, c.dT, c.ll_part,
                   c.th_part, c.p_part, c.p0_part, c.flags, c.lt_old, c.lt_new, c.ll_pre, c.ll_blk, c.wts, c.cdf,
-                  c.uni, c.idx, c.records, c.jump_tab, c.stage};
+                  c.uni, c.idx, c.records, c.jump_tab, c.stage, c.sh_buf, c.sh_idx, c.sh_rows, c.iota};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int l = 0; l <= kMaxLayers; ++l)
@@ -166,15 +166,19 @@ void download(Ctx& c, void* dst, const void* src, size_t bytes) {
   std::memcpy(dst, c.h_stage, bytes);
 }
 
-// One proposal + reweight + (conditional) resample of the whole ensemble
-// (smc.hpp:109-158).  Asynchronous: the record lands in c.records[slot].
-void smc_step_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind, double fraction, int always,
-                    int slot) {
+void check_kernel_cfg(const dasmc_kernel_cfg& kc) {  // kernels.hpp:42-48
   if (!(kc.step_size > 0.0)) throw InvalidArg("KernelConfig: step_size must be > 0");
   if (kc.leapfrog_steps < 1) throw InvalidArg("KernelConfig: leapfrog_steps must be >= 1");
   if (kc.kind == DASMC_LANGEVIN && kc.leapfrog_steps != 1)
     throw InvalidArg("KernelConfig: langevin requires leapfrog_steps == 1");
-  if (rkind != DASMC_MULTINOMIAL && rkind != DASMC_SYSTEMATIC) throw InvalidArg("bad resample kind");
+}
+
+// Fresh momenta + S-step leapfrog + log targets of the context's particles
+// (smc.hpp:118-122, kernels.hpp:75-99).  Global slot of local particle j is
+// j_offset + j (RNG streams).  Returns the buffer index (relative to c.start)
+// holding theta_S.
+int propose_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int64_t j_offset) {
+  check_kernel_cfg(kc);
   if (!c.has_ensemble) throw InvalidArg("smc_step: no ensemble (call init_ensemble or set_ensemble)");
   validate_target(c);
   const int64_t J = c.J;
@@ -185,7 +189,7 @@ void smc_step_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind
   target_rows(c, M, P, br);
   launch_zero_ints(c, c.flags, J);
   // fresh momenta p0 ~ N(0, I) from root.fork(kProposal, k, j) (smc.hpp:119-120; kernels.hpp:131)
-  launch_normals(c, seed, tag::kProposal, (uint64_t)k, J, 1.0f, c.p, c.p0_part);
+  launch_normals(c, seed, tag::kProposal, (uint64_t)k, J, 1.0f, c.p, c.p0_part, j_offset);
   const int t0 = c.start, t1 = (c.start + 1) % 3, t2 = (c.start + 2) % 3;
   float* bufs[3] = {c.theta[t0], c.theta[t1], c.theta[t2]};
   int in_idx = 0;
@@ -198,10 +202,22 @@ void smc_step_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind
     if (s < S) in_idx = out_idx;
   }
   launch_p_sumsq(c, J);
+  return in_idx;
+}
+
+// One proposal + reweight + (conditional) resample of the whole ensemble
+// (smc.hpp:109-158).  Asynchronous: the record lands in c.records[slot].
+void smc_step_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind, double fraction, int always,
+                    int slot) {
+  if (rkind != DASMC_MULTINOMIAL && rkind != DASMC_SYSTEMATIC) throw InvalidArg("bad resample kind");
+  const int64_t J = c.J;
+  const int k = c.iteration;
+  const int t1 = (c.start + 1) % 3, t2 = (c.start + 2) % 3;
+  float* bufs[3] = {c.theta[c.start], c.theta[t1], c.theta[t2]};
+  const int end_idx = propose_async(c, kc, seed, 0);  // theta_S
   // resampling uniforms from root.fork(kResample, k) (smc.hpp:152)
   launch_uniforms(c, fork_key(seed, tag::kResample, (uint64_t)k, 0), rkind == DASMC_MULTINOMIAL ? J : 1, c.uni);
   launch_weights_and_resample(c, J, fraction, always, rkind, slot, k, 0.0);
-  const int end_idx = in_idx;                // theta_S
   const int dst_idx = end_idx == 1 ? 2 : 1;  // the free trajectory buffer
   launch_gather(c, bufs[0], bufs[end_idx], bufs[dst_idx], J);
   c.start = dst_idx == 1 ? t1 : t2;
@@ -249,13 +265,13 @@ void sda_moments_dev(Ctx& c, int64_t P, int64_t M, double* out6) {  // annealing
   sda_moments_from(pre.data(), blk.data(), lw.data(), J, out6);
 }
 
-void init_ensemble_dev(Ctx& c, int64_t J, uint64_t seed) {  // smc.hpp:73-89
+void init_ensemble_dev(Ctx& c, int64_t J, uint64_t seed, int64_t j_offset = 0) {  // smc.hpp:73-89
   if (J < 2) throw InvalidArg("init_ensemble: need at least 2 particles");
   check_J(c, J);
   validate_target(c);
   float* th = c.theta[c.start];
   // theta_j = sigma * normal_vector(D) from root.fork(kInit, j) (network.hpp:235-239)
-  launch_normals(c, seed, tag::kInit, 0, J, (float)c.sigma, th, nullptr);
+  launch_normals(c, seed, tag::kInit, 0, J, (float)c.sigma, th, nullptr, j_offset);
   int64_t M, P;
   double br;
   target_rows(c, M, P, br);
@@ -324,6 +340,12 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
   dmalloc(c.uni, (size_t)Jmax);
   dmalloc(c.idx, (size_t)Jmax);
   dmalloc(c.records, (size_t)kRecRing * 8);
+  {
+    std::vector<int32_t> io((size_t)Jmax);
+    for (int i = 0; i < Jmax; ++i) io[(size_t)i] = i;
+    dmalloc(c.iota, (size_t)Jmax);
+    CK(cudaMemcpy(c.iota, io.data(), sizeof(int32_t) * Jmax, cudaMemcpyHostToDevice));
+  }
   CK(cudaMallocHost(reinterpret_cast<void**>(&c.h_records), sizeof(double) * kRecRing * 8));
   const int64_t nch_uni = (Jmax + 2 * kRngChunkNormals - 1) / (2 * kRngChunkNormals);
   c.jump_chunks = std::max(nch_rng, nch_uni) + 1;
@@ -680,6 +702,166 @@ int dasmc_shuffle_permutation(uint64_t seed, int64_t n, int64_t* perm) {
     if (n < 1 || !perm) throw InvalidArg("bad argument");
     const auto p = shuffle_permutation(seed, n);
     std::memcpy(perm, p.data(), sizeof(int64_t) * (size_t)n);
+  });
+}
+
+int dasmc_gpu_init_ensemble_at(dasmc_ctx* ctx, int64_t J, uint64_t seed, int64_t j_offset) {
+  return guarded([&] {
+    if (!ctx || j_offset < 0) throw InvalidArg("bad argument");
+    CK(cudaSetDevice(ctx->c.device));
+    init_ensemble_dev(ctx->c, J, seed, j_offset);
+  });
+}
+
+void dasmc_shard_range(int64_t J, int world, int rank, int64_t* lo, int64_t* hi) {
+  // parallel.hpp:30-31 static contiguous partition
+  *lo = J * rank / world;
+  *hi = J * (rank + 1) / world;
+}
+
+int dasmc_shard_plan(const int32_t* idx, int64_t J, int world, int rank, int32_t* recv_src, int32_t* recv_row,
+                     int64_t* send_cnt, int32_t* send_rows) {
+  return guarded([&] {
+    if (!idx || world < 1 || rank < 0 || rank >= world || J < world) throw InvalidArg("shard_plan: bad argument");
+    std::vector<int64_t> lo((size_t)world + 1);
+    for (int r = 0; r <= world; ++r) lo[(size_t)r] = J * r / world;
+    auto owner = [&](int64_t g) {
+      return (int)(std::upper_bound(lo.begin(), lo.end(), g) - lo.begin()) - 1;
+    };
+    for (int64_t j = lo[(size_t)rank]; j < lo[(size_t)rank + 1]; ++j) {
+      const int64_t g = idx[j];
+      if (g < 0 || g >= J) throw InvalidArg("shard_plan: index out of range");
+      const int s = owner(g);
+      recv_src[j - lo[(size_t)rank]] = s;
+      recv_row[j - lo[(size_t)rank]] = (int32_t)(g - lo[(size_t)s]);
+    }
+    int64_t n = 0;
+    for (int d = 0; d < world; ++d) {
+      send_cnt[d] = 0;
+      for (int64_t j = lo[(size_t)d]; j < lo[(size_t)d + 1]; ++j) {
+        const int64_t g = idx[j];
+        if (owner(g) == rank) {
+          send_rows[n++] = (int32_t)(g - lo[(size_t)rank]);
+          ++send_cnt[d];
+        }
+      }
+    }
+  });
+}
+
+int dasmc_gpu_shard_propose(dasmc_ctx* ctx, const dasmc_kernel_cfg* cfg, uint64_t seed, int64_t j_offset,
+                            double* log_w_dev, double* log_target_new_dev) {
+  return guarded([&] {
+    if (!ctx || !cfg || !log_w_dev || !log_target_new_dev) throw InvalidArg("null argument");
+    Ctx& c = ctx->c;
+    CK(cudaSetDevice(c.device));
+    const int t1 = (c.start + 1) % 3, t2 = (c.start + 2) % 3;
+    float* bufs[3] = {c.theta[c.start], c.theta[t1], c.theta[t2]};
+    const int end_idx = propose_async(c, *cfg, seed, j_offset);
+    launch_local_weights(c, c.J, log_w_dev, log_target_new_dev);
+    // finalise positions: divergent particles keep theta (smc.hpp:129-131)
+    const int dst_idx = end_idx == 1 ? 2 : 1;
+    launch_gather(c, bufs[0], bufs[end_idx], bufs[dst_idx], c.J, c.iota);
+    c.start = dst_idx == 1 ? t1 : t2;
+    CK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int dasmc_gpu_shard_resample(dasmc_ctx* ctx, const double* log_w_full_dev, const double* log_target_new_full_dev,
+                             int64_t J_total, int64_t j_offset, uint64_t seed, int resample_kind, double fraction,
+                             int resample_always, int32_t* idx_dev, dasmc_iter_record* record) {
+  return guarded([&] {
+    if (!ctx || !log_w_full_dev || !log_target_new_full_dev || !idx_dev) throw InvalidArg("null argument");
+    Ctx& c = ctx->c;
+    if (j_offset < 0 || j_offset + c.J > J_total) throw InvalidArg("shard_resample: slice out of range");
+    if (resample_kind != DASMC_MULTINOMIAL && resample_kind != DASMC_SYSTEMATIC) throw InvalidArg("bad resample kind");
+    CK(cudaSetDevice(c.device));
+    if (J_total > c.sh_cap) {
+      if (c.sh_buf) CK(cudaFree(c.sh_buf));
+      if (c.sh_idx) CK(cudaFree(c.sh_idx));
+      c.sh_buf = nullptr;
+      c.sh_idx = nullptr;
+      dmalloc(c.sh_buf, (size_t)5 * J_total);
+      dmalloc(c.sh_idx, (size_t)J_total);
+      c.sh_cap = J_total;
+    }
+    const int64_t need = (J_total + 2 * kRngChunkNormals - 1) / (2 * kRngChunkNormals) + 1;
+    if (need > c.jump_chunks) {
+      CK(cudaStreamSynchronize(c.stream));
+      CK(cudaFree(c.jump_tab));
+      c.jump_tab = nullptr;
+      const auto tab = jump_table(2 * kRngChunkNormals, need);
+      dmalloc(c.jump_tab, (size_t)need * 4);
+      CK(cudaMemcpy(c.jump_tab, tab.data(), sizeof(uint64_t) * 4 * tab.size(), cudaMemcpyHostToDevice));
+      c.jump_chunks = need;
+    }
+    double* lw = c.sh_buf;
+    double* lt = lw + c.sh_cap;
+    double* w = lt + c.sh_cap;
+    double* cdf = w + c.sh_cap;
+    double* uni = cdf + c.sh_cap;
+    const int k = c.iteration;
+    CK(cudaMemcpyAsync(lw, log_w_full_dev, sizeof(double) * J_total, cudaMemcpyDeviceToDevice, c.stream));
+    CK(cudaMemcpyAsync(lt, log_target_new_full_dev, sizeof(double) * J_total, cudaMemcpyDeviceToDevice, c.stream));
+    launch_uniforms(c, fork_key(seed, tag::kResample, (uint64_t)k, 0),
+                    resample_kind == DASMC_MULTINOMIAL ? J_total : 1, uni);
+    const int slot = c.rec_head % kRecRing;
+    launch_normalize_resample(c, J_total, lw, lt, w, cdf, uni, c.sh_idx, fraction, resample_always, resample_kind,
+                              slot, k);
+    ++c.rec_head;
+    CK(cudaMemcpyAsync(c.logw, lw + j_offset, sizeof(double) * c.J, cudaMemcpyDeviceToDevice, c.stream));
+    CK(cudaMemcpyAsync(idx_dev, c.sh_idx, sizeof(int32_t) * J_total, cudaMemcpyDeviceToDevice, c.stream));
+    fetch_records(c, slot, 1);
+    dasmc_iter_record r = read_record(c, slot);
+    r.batch = c.block_end;
+    r.beta = c.mode == DASMC_SDA ? c.beta : 1.0;
+    if (record) *record = r;
+    c.iteration = k + 1;
+  });
+}
+
+int64_t dasmc_gpu_row_floats(const dasmc_ctx* ctx) { return ctx ? ctx->c.net.Dp : -1; }
+
+static void upload_rows(Ctx& c, const int32_t* rows, int64_t n) {
+  if (n > c.sh_rows_cap) {
+    if (c.sh_rows) CK(cudaFree(c.sh_rows));
+    c.sh_rows = nullptr;
+    dmalloc(c.sh_rows, (size_t)n);
+    c.sh_rows_cap = n;
+  }
+  CK(cudaMemcpyAsync(c.sh_rows, rows, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c.stream));
+}
+
+int dasmc_gpu_pack_rows(dasmc_ctx* ctx, const int32_t* rows, int64_t n, float* dst_dev) {
+  return guarded([&] {
+    if (!ctx || (n > 0 && (!rows || !dst_dev)) || n < 0) throw InvalidArg("bad argument");
+    Ctx& c = ctx->c;
+    for (int64_t i = 0; i < n; ++i)
+      if (rows[i] < 0 || rows[i] >= c.J) throw InvalidArg("pack_rows: row out of range");
+    CK(cudaSetDevice(c.device));
+    if (n == 0) return;
+    upload_rows(c, rows, n);
+    launch_rows(c, c.theta[c.start], dst_dev, c.sh_rows, n, true);
+    CK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int dasmc_gpu_unpack_rows(dasmc_ctx* ctx, const float* src_dev, const int32_t* slots, int64_t n) {
+  return guarded([&] {
+    if (!ctx || !src_dev || !slots) throw InvalidArg("null argument");
+    Ctx& c = ctx->c;
+    if (n != c.J) throw InvalidArg("unpack_rows: every local slot must be written exactly once");
+    std::vector<char> seen((size_t)c.J, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      if (slots[i] < 0 || slots[i] >= c.J || seen[(size_t)slots[i]]) throw InvalidArg("unpack_rows: bad slot list");
+      seen[(size_t)slots[i]] = 1;
+    }
+    CK(cudaSetDevice(c.device));
+    const int next = (c.start + 1) % 3;
+    upload_rows(c, slots, n);
+    launch_rows(c, src_dev, c.theta[next], c.sh_rows, n, false);
+    c.start = next;
+    CK(cudaStreamSynchronize(c.stream));
   });
 }
 

@@ -152,6 +152,14 @@ struct Ctx {
   // events for sampler_ms
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
+  // sharded-ensemble scratch (full-J vectors + row lists)
+  double* sh_buf = nullptr;  // [5][sh_cap]: log_w, log_target_new, w, cdf, uniforms
+  int32_t* sh_idx = nullptr; // [sh_cap]
+  int64_t sh_cap = 0;
+  int32_t* sh_rows = nullptr;
+  int64_t sh_rows_cap = 0;
+  int32_t* iota = nullptr;   // [Jmax] identity indices
+
   // tensor-core path state (tc_gemm.cu), null on the fp32 CUDA-core path
   struct TcState* tc = nullptr;
 
@@ -189,7 +197,7 @@ void launch_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P,
 void launch_eval_finalize(Ctx& c, int64_t J, double* values_out, double* pre_out, double* blk_out, int64_t M,
                           bool with_theta_norm);
 void launch_normals(Ctx& c, uint64_t key_root, uint64_t tag_a, uint64_t a2, int64_t J, float scale, float* dst,
-                    double* sq_part);
+                    double* sq_part, int64_t j_offset = 0);
 void launch_ref_to_internal_f64(Ctx& c, const double* src, float* dst, int64_t J);
 void launch_ref_to_internal_f32(Ctx& c, const float* src, float* dst, int64_t J);
 void launch_internal_to_ref_f64(Ctx& c, const float* src, double* dst, int64_t J);
@@ -198,7 +206,13 @@ void launch_zero_ints(Ctx& c, int* p, int64_t n);
 void launch_uniforms(Ctx& c, uint64_t key, int64_t count, double* dst);
 void launch_weights_and_resample(Ctx& c, int64_t J, double fraction, int always, int kind, int rec_slot,
                                  int k, double log_target_const);
-void launch_gather(Ctx& c, const float* start, const float* end, float* dst, int64_t J);
+void launch_gather(Ctx& c, const float* start, const float* end, float* dst, int64_t J,
+                   const int32_t* idx = nullptr);
+void launch_local_weights(Ctx& c, int64_t J, double* out_lw, double* out_lt);
+void launch_normalize_resample(Ctx& c, int64_t Jtot, double* lw_full, const double* lt_full, double* w, double* cdf,
+                               const double* uni, int32_t* idx, double fraction, int always, int kind, int rec_slot,
+                               int k);
+void launch_rows(Ctx& c, const float* src, float* dst, const int32_t* rows_dev, int64_t n, bool pack);
 void launch_resample_hook(Ctx& c, const double* w, const double* u, int64_t J, int kind, int32_t* idx);
 
 }  // namespace dasmc_b200

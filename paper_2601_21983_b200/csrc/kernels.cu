@@ -387,12 +387,13 @@ __global__ void eval_finalize_kernel(int64_t J, const double* __restrict__ ll_pa
 // rng.hpp:76-81; the value is stored in fp32 at its internal position.
 __global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b, int per_particle_c,
                                int64_t J, int64_t nchunks, const uint64_t* __restrict__ jump_tab, float scale,
-                               float* __restrict__ dst, double* __restrict__ sq_part) {
+                               float* __restrict__ dst, double* __restrict__ sq_part, int64_t j_offset) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= J * nchunks) return;
   const int64_t j = g / nchunks, c = g - j * nchunks;
-  // fork(kProposal, k, j) -> (a, b, j); fork(kInit, j) -> (a, j, 0)
-  const uint64_t key = per_particle_c ? fork_key(root, a, b, (uint64_t)j) : fork_key(root, a, (uint64_t)j, 0);
+  // fork(kProposal, k, j) -> (a, b, j); fork(kInit, j) -> (a, j, 0); j is the GLOBAL slot
+  const uint64_t jg = (uint64_t)(j + j_offset);
+  const uint64_t key = per_particle_c ? fork_key(root, a, b, jg) : fork_key(root, a, jg, 0);
   Xoshiro x;
   x.seed(key);
   if (c > 0) x.jump(jump_tab + 4 * c);
@@ -435,12 +436,14 @@ __global__ void __launch_bounds__(kWT) weights_kernel(int64_t J, double* __restr
                                                       const int* __restrict__ flags, double* __restrict__ w,
                                                       double* __restrict__ cdf, const double* __restrict__ uni,
                                                       int32_t* __restrict__ idx, double fraction, int always,
-                                                      int kind, double* __restrict__ rec, int k) {
+                                                      int kind, double* __restrict__ rec, int k, int compute_lw) {
   __shared__ double sh[kWT / 32 + 1];
   __shared__ int s_res;
-  // 1) new log-weights (kernels.hpp:153-163, smc.hpp:127-138)
+  // 1) new log-weights (kernels.hpp:153-163, smc.hpp:127-138); with compute_lw = 0
+  //    logw already holds them (the gathered vector of a sharded ensemble)
   int ndiv = 0;
-  for (int64_t j = threadIdx.x; j < J; j += kWT) {
+  for (int64_t j = threadIdx.x; j < J && !compute_lw; j += kWT) ndiv += logw[j] == -CUDART_INF ? 1 : 0;
+  for (int64_t j = threadIdx.x; j < J && compute_lw; j += kWT) {
     double lw;
     if (flags[j]) {
       lw = -CUDART_INF;
@@ -528,6 +531,39 @@ __global__ void __launch_bounds__(kWT) weights_kernel(int64_t J, double* __restr
     idx[j] = (int32_t)lo;
     logw[j] = lj;  // smc.hpp:100
   }
+}
+
+// Sharded ensemble, step 1: new (unnormalised) log-weights of the local slots
+// (kernels.hpp:153-163, smc.hpp:127-138) into out_lw; logw itself is untouched.
+__global__ void local_weights_kernel(int64_t J, const double* __restrict__ logw, const double* __restrict__ lt_old,
+                                     const double* __restrict__ lt_new, const double* __restrict__ p0_part,
+                                     int p0_slots, const double* __restrict__ pS_part, int pS_slots,
+                                     const int* __restrict__ flags, double* __restrict__ out_lw,
+                                     double* __restrict__ out_lt) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= J) return;
+  double lw = -CUDART_INF;
+  if (!flags[j]) {
+    double p0 = 0.0, ps = 0.0;
+    for (int s = 0; s < p0_slots; ++s) p0 += p0_part[j * p0_slots + s];
+    for (int s = 0; s < pS_slots; ++s) ps += pS_part[j * pS_slots + s];
+    const double a = lt_new[j], b = lt_old[j];
+    const double inc =
+        (isfinite(a) && isfinite(b) && isfinite(p0) && isfinite(ps)) ? (a - b) + 0.5 * (p0 - ps) : -CUDART_INF;
+    lw = logw[j] + inc;
+  }
+  out_lw[j] = lw;
+  out_lt[j] = lt_new[j];
+}
+
+// theta rows: dst[i] = src_buf[rows[i]] (pack) or dst_buf[rows[i]] = src[i] (unpack); float4 copies.
+__global__ void __launch_bounds__(256) rows_kernel(const float4* __restrict__ src, float4* __restrict__ dst,
+                                                   int64_t Dp4, const int32_t* __restrict__ rows, int pack) {
+  const int64_t i = blockIdx.y;
+  const int64_t r = rows[i];
+  const float4* s = src + (pack ? r : i) * Dp4;
+  float4* d = dst + (pack ? i : r) * Dp4;
+  for (int64_t q = blockIdx.x * 256 + threadIdx.x; q < Dp4; q += (int64_t)gridDim.x * 256) d[q] = s[q];
 }
 
 // Bit-exact resampling hook: caller-provided normalised weights and uniforms.
@@ -687,12 +723,12 @@ void launch_eval_finalize(Ctx& c, int64_t J, double* values_out, double* pre_out
 }
 
 void launch_normals(Ctx& c, uint64_t root, uint64_t a, uint64_t b, int64_t J, float scale, float* dst,
-                    double* sq_part) {
+                    double* sq_part, int64_t j_offset) {
   const int64_t nch = (c.net.D + kRngChunkNormals - 1) / kRngChunkNormals;
   const int per_particle_c = a == tag::kProposal ? 1 : 0;
   const int64_t total = J * nch;
-  normals_kernel<<<(unsigned)((total + 127) / 128), 128, 0, c.stream>>>(c.net, root, a, b, per_particle_c, J, nch,
-                                                                        c.jump_tab, scale, dst, sq_part);
+  normals_kernel<<<(unsigned)((total + 127) / 128), 128, 0, c.stream>>>(
+      c.net, root, a, b, per_particle_c, J, nch, c.jump_tab, scale, dst, sq_part, j_offset);
   LAUNCHED();
 }
 
@@ -732,7 +768,32 @@ void launch_weights_and_resample(Ctx& c, int64_t J, double fraction, int always,
   const int pS_slots = (int)((c.net.Dp + kSqChunk - 1) / kSqChunk);
   weights_kernel<<<1, kWT, 0, c.stream>>>(J, c.logw, c.lt_old, c.lt_new, c.p0_part, p0_slots, c.p_part, pS_slots,
                                           c.flags, c.wts, c.cdf, c.uni, c.idx, fraction, always, kind,
-                                          c.records + (size_t)rec_slot * 8, k);
+                                          c.records + (size_t)rec_slot * 8, k, 1);
+  LAUNCHED();
+}
+
+void launch_local_weights(Ctx& c, int64_t J, double* out_lw, double* out_lt) {
+  const int pS_slots = (int)((c.net.Dp + kSqChunk - 1) / kSqChunk);
+  local_weights_kernel<<<(unsigned)((J + 255) / 256), 256, 0, c.stream>>>(
+      J, c.logw, c.lt_old, c.lt_new, c.p0_part, c.rng_slots, c.p_part, pS_slots, c.flags, out_lw, out_lt);
+  LAUNCHED();
+}
+
+void launch_normalize_resample(Ctx& c, int64_t Jtot, double* lw_full, const double* lt_full, double* w, double* cdf,
+                               const double* uni, int32_t* idx, double fraction, int always, int kind, int rec_slot,
+                               int k) {
+  weights_kernel<<<1, kWT, 0, c.stream>>>(Jtot, lw_full, nullptr, lt_full, nullptr, 0, nullptr, 0, nullptr, w, cdf,
+                                          uni, idx, fraction, always, kind, c.records + (size_t)rec_slot * 8, k, 0);
+  LAUNCHED();
+}
+
+void launch_rows(Ctx& c, const float* src, float* dst, const int32_t* rows_dev, int64_t n, bool pack) {
+  if (n <= 0) return;
+  const int64_t Dp4 = c.net.Dp / 4;
+  const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>((Dp4 + 255) / 256, 64));
+  dim3 grid((unsigned)chunks, (unsigned)n);
+  rows_kernel<<<grid, 256, 0, c.stream>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), Dp4,
+                                          rows_dev, pack ? 1 : 0);
   LAUNCHED();
 }
 
@@ -743,13 +804,13 @@ void launch_p_sumsq(Ctx& c, int64_t J) {
   LAUNCHED();
 }
 
-void launch_gather(Ctx& c, const float* start, const float* end, float* dst, int64_t J) {
+void launch_gather(Ctx& c, const float* start, const float* end, float* dst, int64_t J, const int32_t* idx) {
   const int64_t Dp4 = c.net.Dp / 4;
   const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>((Dp4 + 255) / 256, 64));
   dim3 grid((unsigned)chunks, (unsigned)J);
   gather_kernel<<<grid, 256, 0, c.stream>>>(reinterpret_cast<const float4*>(start),
                                             reinterpret_cast<const float4*>(end), reinterpret_cast<float4*>(dst),
-                                            Dp4, c.idx, c.flags);
+                                            Dp4, idx ? idx : c.idx, c.flags);
   LAUNCHED();
 }
 
