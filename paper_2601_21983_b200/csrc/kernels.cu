@@ -400,13 +400,33 @@ __global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b
   const int64_t lo = c * kRngChunkNormals, hi = min(net.D, lo + kRngChunkNormals);
   double sq = 0.0;
   float* out = dst + j * net.Dp;
+  // reference index i -> internal offset, walked incrementally (one division per chunk):
+  // layer l, W(r, c) at ref_off + r + c*out -> woff + r*in + c; then the bias block.
+  int l = 0;
+  while (l < net.L - 1 && lo >= net.layer[l + 1].ref_off) ++l;
+  int64_t t = lo - net.layer[l].ref_off;
+  int64_t nw = (int64_t)net.layer[l].in * net.layer[l].out;
+  int64_t r = t < nw ? t % net.layer[l].out : 0, cc = t < nw ? t / net.layer[l].out : 0;
   for (int64_t i = lo; i < hi; ++i) {
     const double u1 = 1.0 - x.uniform();
     const double u2 = x.uniform();
     const double nv = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
     const float v = (float)((double)scale * nv);
-    out[internal_index(net, i)] = v;
+    const LayerDev& ly = net.layer[l];
+    out[t < nw ? ly.woff + r * ly.in + cc : ly.boff + (t - nw)] = v;
     sq += (double)v * (double)v;
+    // advance to i + 1
+    if (++t < nw) {
+      if (++r == ly.out) {
+        r = 0;
+        ++cc;
+      }
+    } else if (t == nw + ly.out && l + 1 < net.L) {
+      ++l;
+      t = 0;
+      r = cc = 0;
+      nw = (int64_t)net.layer[l].in * net.layer[l].out;
+    }
   }
   if (sq_part) sq_part[j * nchunks + c] = sq;
 }
