@@ -31,6 +31,7 @@ struct TcState {
   int64_t n_pad = 0;     // X^T row stride (floats)
   int64_t mcap = 0;      // row stride of the transposed activation buffers
   bool split = false;    // split-tf32 (3 MMAs)
+  bool mma_layer2 = true; // fused forward runs the layer-2 products on mma.sync (DASMC_MMA_LAYER2=0: CUDA-core FFMA)
   bool tc_layer2 = false; // fused forward runs layer 2 as TMEM-A MMAs (opt-in: DASMC_TC_LAYER2=1;
                           // measured slower on B200: the small MMAs queue behind the next tile's)
   float* Xt = nullptr;   // [(n0+1) x n_pad], row n0 = 1
@@ -61,7 +62,7 @@ constexpr bool kUseTmaStore = false;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;  // TMA warp + MMA warp + epilogue warps
 constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
-constexpr int kEpiKindFwd = 0, kEpiKindDw = 1, kEpiKindFwdTc = 2;
+constexpr int kEpiKindFwd = 0, kEpiKindDw = 1, kEpiKindFwdTc = 2, kEpiKindFwdMma = 3;
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -222,6 +223,38 @@ __device__ __forceinline__ float tf32_hi(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
+}
+
+// Warp-level D(16x8) += A(16x8) . B(8x8), tf32 inputs, fp32 accumulate, split
+// into hi/lo parts (hi.hi + hi.lo + lo.hi) for fp32-level products.
+// Fragment layouts (g = lane / 4, t = lane % 4):
+//   A: a0 (g, t), a1 (g+8, t), a2 (g, t+4), a3 (g+8, t+4)
+//   B: b0 (k = t, n = g), b1 (k = t+4, n = g)
+//   D: d0 (g, 2t), d1 (g, 2t+1), d2 (g+8, 2t), d3 (g+8, 2t+1)
+__device__ __forceinline__ void mma_tf32(float* d, const uint32_t* a, const uint32_t* b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ void mma_3xtf32(float* d, const float* a, const float* b) {
+  uint32_t ah[4], al[4], bh[2], bl[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float h = tf32_hi(a[i]);
+    ah[i] = __float_as_uint(h);
+    al[i] = __float_as_uint(tf32_hi(a[i] - h));
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float h = tf32_hi(b[i]);
+    bh[i] = __float_as_uint(h);
+    bl[i] = __float_as_uint(tf32_hi(b[i] - h));
+  }
+  mma_tf32(d, al, bh);
+  mma_tf32(d, ah, bl);
+  mma_tf32(d, ah, bh);
 }
 
 // ---------------------------------------------------------------- parameters
@@ -680,6 +713,289 @@ __global__ void __launch_bounds__(kThreads, 1)
           o[0] = red[0] + red[2] + red[4] + red[6];
           o[1] = red[1] + red[3] + red[5] + red[7];
         }
+      } else if (EPI == kEpiKindFwdMma) {
+        // Fused forward with the layer-2 products on warp-level tensor cores:
+        // per 16-column chunk a warp stages its 32 rows x 16 columns of A1 in
+        // shared memory and runs z2 += A1 . W2^T (M 32, N 16, K 16) and, in
+        // pass 2, dz = delta2 . W2 (M 32, N 16, K 16) as split-tf32 mma.sync.
+        constexpr int WS = 24;  // W2T row stride (floats): conflict-free B loads in pass 1
+        constexpr int ZS = 20;  // row stride of the per-warp staging / exchange tiles
+        const int n1 = fp.n1, C = fp.C;
+        const int NP = tp.nmma;
+        float* W2T = epi_smem;                  // [NP][WS]  W2 transposed, zero-padded (c >= C, o >= n1)
+        float* b1s = W2T + (size_t)NP * WS;     // [NP]
+        float* b2s = b1s + NP;                  // [16]
+        float* z2x = b2s + 16;                  // [kParts][128][ZS] z2 partials, then delta2 in part 0
+        double* red = (double*)(z2x + kParts * 128 * ZS);  // [4][2]
+        float* As = (float*)(red + 8) + (warp - 2) * 32 * ZS;  // per-warp [32][ZS] staging
+        const float* th = fp.theta + (int64_t)j * fp.Dp;
+        constexpr int kPerW = (256 * 16 + kEpiThreads - 1) / kEpiThreads;
+        float wv[kPerW];
+#pragma unroll
+        for (int r = 0; r < kPerW; ++r) {  // element (o, c) -> W2[c][o]
+          const int i = et + r * kEpiThreads;
+          const int o = i >> 4, c = i & 15;
+          wv[r] = (o < n1 && c < C) ? th[fp.woff2 + (int64_t)c * n1 + o] : 0.f;
+        }
+        const float bv = et < n1 ? th[fp.boff1 + et] : 0.f;
+        const float b2v = et < C ? th[fp.boff2 + et] : 0.f;
+        named_bar(1, kEpiThreads);
+#pragma unroll
+        for (int r = 0; r < kPerW; ++r) {
+          const int i = et + r * kEpiThreads;
+          if (i < NP * 16) W2T[(i >> 4) * WS + (i & 15)] = wv[r];
+        }
+        if (et < NP) b1s[et] = bv;
+        if (et < 16) b2s[et] = b2v;
+        named_bar(1, kEpiThreads);
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(lg * 32) << 16);
+        const int64_t m = (int64_t)rt * BM + row_in_tile;
+        const bool valid = m < fp.M;
+        const bool relu = fp.act == DASMC_RELU;
+        const bool wr_out = valid && fp.need_grad && fp.dbg != 1;
+        int c_lo, c_hi;
+        chunk_range(NP >> 4, c_lo, c_hi);
+        if (fp.dbg == 3) c_hi = c_lo;
+        const int64_t ldm = fp.ldm;
+        const int g = lane >> 2, tq = lane & 3;
+        float zacc[2][2][4];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) zacc[a][b][q] = 0.f;
+        float* a1T = fp.a1T + (int64_t)j * (n1 + 1) * ldm + m;
+        float* a1Tlo = SPLIT ? fp.a1Tlo + (int64_t)j * (n1 + 1) * ldm + m : nullptr;
+        // pass 1: a1 = act(z1 + b1) -> a1^T; z2 += A1 . W2^T on mma.sync
+        auto chunk1 = [&](int ch, const float* v) {
+          const int o0 = ch * 16;
+          float* pa = a1T + (int64_t)o0 * ldm;
+          float* pal = SPLIT ? a1Tlo + (int64_t)o0 * ldm : nullptr;
+          float a[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            a[q] = v[q] + b1s[o0 + q];
+            a[q] = relu ? fmaxf(a[q], 0.f) : tanhf(a[q]);
+            if (o0 + q >= n1) a[q] = 0.f;
+            if (wr_out && o0 + q < n1) {
+              const float hi = tf32_hi(a[q]);
+              *pa = hi;
+              if (SPLIT) *pal = a[q] - hi;
+            }
+            pa += ldm;
+            if (SPLIT) pal += ldm;
+          }
+          float4* as4 = reinterpret_cast<float4*>(As + lane * ZS);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) as4[q] = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            float bf[2][2];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              bf[nt][0] = W2T[(o0 + 8 * ks + tq) * WS + 8 * nt + g];
+              bf[nt][1] = W2T[(o0 + 8 * ks + tq + 4) * WS + 8 * nt + g];
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+              const float* r0 = As + (16 * mt + g) * ZS + 8 * ks + tq;
+              const float af[4] = {r0[0], r0[8 * ZS], r0[4], r0[8 * ZS + 4]};
+#pragma unroll
+              for (int nt = 0; nt < 2; ++nt) mma_3xtf32(zacc[mt][nt], af, bf[nt]);
+            }
+          }
+          __syncwarp();
+        };
+        {
+          float va[16] = {}, vb[16] = {};
+          int ch = c_lo;
+          if (ch < c_hi) tmem_ld16_async(taddr + ch * 16, va);
+          tmem_wait16(va);
+          while (ch < c_hi) {
+            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, vb);
+            chunk1(ch, va);
+            tmem_wait16(vb);
+            if (++ch >= c_hi) break;
+            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, va);
+            chunk1(ch, vb);
+            tmem_wait16(va);
+            ++ch;
+          }
+        }
+        // z2 partial fragments -> exchange tile rows of this part
+        {
+          float* zb = z2x + ((size_t)part * 128 + lg * 32) * ZS;
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              float* p0 = zb + (16 * mt + g) * ZS + 8 * nt + 2 * tq;
+              *reinterpret_cast<float2*>(p0) = make_float2(zacc[mt][nt][0], zacc[mt][nt][1]);
+              *reinterpret_cast<float2*>(p0 + 8 * ZS) = make_float2(zacc[mt][nt][2], zacc[mt][nt][3]);
+            }
+        }
+        named_bar(1, kEpiThreads);
+        double ll = 0.0;
+        if (part == 0) {
+          float z2[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            float s = z2x[(size_t)row_in_tile * ZS + c];
+#pragma unroll
+            for (int p = 1; p < kParts; ++p) s += z2x[((size_t)p * 128 + row_in_tile) * ZS + c];
+            z2[c] = s + b2s[c];
+          }
+          float d2[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) d2[c] = 0.f;
+          if (valid) {
+            const int yi = fp.y[m];
+            float mx = z2[0];
+#pragma unroll
+            for (int c = 1; c < 16; ++c)
+              if (c < C) mx = fmaxf(mx, z2[c]);
+            float e[16];
+            double den = 0.0;
+            float zy = 0.f;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              e[c] = c < C ? expf(z2[c] - mx) : 0.f;
+              den += (double)e[c];
+              if (c == yi) zy = z2[c];
+            }
+            ll = (double)zy - ((double)mx + log(den));
+            if (fp.need_grad) {
+              const float wrow = m < fp.P ? 1.f : fp.beta_rows;
+              const float rden = (float)(1.0 / den);
+#pragma unroll
+              for (int c = 0; c < 16; ++c)
+                if (c < C) {
+                  d2[c] = wrow * ((c == yi ? 1.f : 0.f) - e[c] * rden);
+                  const float hi = tf32_hi(d2[c]);
+                  fp.d2T[((int64_t)j * C + c) * ldm + m] = hi;
+                  if (SPLIT) fp.d2Tlo[((int64_t)j * C + c) * ldm + m] = d2[c] - hi;
+                }
+            }
+          }
+          float* zx = z2x + (size_t)row_in_tile * ZS;
+#pragma unroll
+          for (int c = 0; c < 16; ++c) zx[c] = d2[c];
+        }
+        if (fp.need_grad && fp.dbg == 0) {
+          named_bar(1, kEpiThreads);
+          // delta2 A fragments of this warp's 32 rows (K = classes)
+          float df[2][2][4];
+          {
+            const float* db = z2x + (size_t)(lg * 32) * ZS;
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+              for (int ks = 0; ks < 2; ++ks) {
+                const float* r0 = db + (16 * mt + g) * ZS + 8 * ks + tq;
+                df[mt][ks][0] = r0[0];
+                df[mt][ks][1] = r0[8 * ZS];
+                df[mt][ks][2] = r0[4];
+                df[mt][ks][3] = r0[8 * ZS + 4];
+              }
+          }
+          float* d1T = fp.d1T + (int64_t)j * n1 * ldm + m;
+          float* d1Tlo = SPLIT ? fp.d1Tlo + (int64_t)j * n1 * ldm + m : nullptr;
+          auto chunk2 = [&](int ch, const float* v) {
+            const int o0 = ch * 16;
+            float dz[2][2][4];
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+              for (int b = 0; b < 2; ++b)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) dz[a][b][q] = 0.f;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              float bf[2][2];
+#pragma unroll
+              for (int nt = 0; nt < 2; ++nt) {  // B(k = c, n = o) = W2[c][o]
+                bf[nt][0] = W2T[(o0 + 8 * nt + g) * WS + 8 * ks + tq];
+                bf[nt][1] = W2T[(o0 + 8 * nt + g) * WS + 8 * ks + tq + 4];
+              }
+#pragma unroll
+              for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) mma_3xtf32(dz[mt][nt], df[mt][ks], bf[nt]);
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+              for (int nt = 0; nt < 2; ++nt) {
+                float* p0 = As + (16 * mt + g) * ZS + 8 * nt + 2 * tq;
+                *reinterpret_cast<float2*>(p0) = make_float2(dz[mt][nt][0], dz[mt][nt][1]);
+                *reinterpret_cast<float2*>(p0 + 8 * ZS) = make_float2(dz[mt][nt][2], dz[mt][nt][3]);
+              }
+            __syncwarp();
+            float dr[16];
+            const float4* as4 = reinterpret_cast<const float4*>(As + lane * ZS);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 f = as4[q];
+              dr[4 * q] = f.x;
+              dr[4 * q + 1] = f.y;
+              dr[4 * q + 2] = f.z;
+              dr[4 * q + 3] = f.w;
+            }
+            __syncwarp();
+            if (!valid) return;
+            float* pd = d1T + (int64_t)o0 * ldm;
+            float* pdl = SPLIT ? d1Tlo + (int64_t)o0 * ldm : nullptr;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              if (o0 + q < n1) {
+                float a = v[q] + b1s[o0 + q];
+                a = relu ? fmaxf(a, 0.f) : tanhf(a);
+                const float d1 = relu ? dr[q] * (a > 0.f ? 1.f : 0.f) : dr[q] * (1.f - a * a);
+                const float hi = tf32_hi(d1);
+                *pd = hi;
+                if (SPLIT) *pdl = d1 - hi;
+              }
+              pd += ldm;
+              if (SPLIT) pdl += ldm;
+            }
+          };
+          float va[16] = {}, vb[16] = {};
+          int ch = c_lo;
+          if (ch < c_hi) tmem_ld16_async(taddr + ch * 16, va);
+          tmem_wait16(va);
+          while (ch < c_hi) {
+            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, vb);
+            chunk2(ch, va);
+            tmem_wait16(vb);
+            if (++ch >= c_hi) break;
+            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, va);
+            chunk2(ch, vb);
+            tmem_wait16(va);
+            ++ch;
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        double pre = (valid && m < fp.P) ? ll : 0.0, blk = (valid && m >= fp.P) ? ll : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          pre += __shfl_xor_sync(0xffffffffu, pre, o);
+          blk += __shfl_xor_sync(0xffffffffu, blk, o);
+        }
+        if (lane == 0 && part == 0) {
+          red[lg * 2] = pre;
+          red[lg * 2 + 1] = blk;
+        }
+        named_bar(1, kEpiThreads);
+        if (et == 0) {
+          double* o = fp.ll_part + ((int64_t)j * fp.ll_slots + rt) * 2;
+          o[0] = red[0] + red[2] + red[4] + red[6];
+          o[1] = red[1] + red[3] + red[5] + red[7];
+        }
       } else if (EPI == kEpiKindFwdTc) {
         // Layer 2 on the tensor core: A1 = act(Z1 + b1) is written back into
         // the accumulator's TMEM columns and becomes the A operand of
@@ -1054,6 +1370,8 @@ void tc_init(Ctx& c) {
   s->C = c.net.sizes[2];
   s->split = c.precision == DASMC_PREC_3XTF32;
   if (const char* e = std::getenv("DASMC_TC_LAYER2")) s->tc_layer2 = e[0] != '0';
+  if (const char* e = std::getenv("DASMC_MMA_LAYER2")) s->mma_layer2 = e[0] != '0';
+  if (s->tc_layer2) s->mma_layer2 = false;
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1182,7 +1500,16 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     }
     DwParams dp{};
     const int NP = tp.nmma;
-    if (s->tc_layer2 && NP + 32 <= 256) {
+    if (s->mma_layer2) {
+      // layer 2 on warp-level mma.sync (split-tf32) inside the epilogue
+      const size_t mma_bytes = sizeof(float) * ((size_t)NP * 24 + NP + 16 + (size_t)kParts * 128 * 20 +
+                                                (size_t)kEpiWarps * 32 * 20) +
+                               8 * sizeof(double) + 64;
+      if (s->split)
+        launch_tc<kEpiKindFwdMma, true, false, 4>(c, A, Alo, B, Blo, tp, fp, dp, mma_bytes);
+      else
+        launch_tc<kEpiKindFwdMma, false, false, 4>(c, A, Alo, B, Blo, tp, fp, dp, mma_bytes);
+    } else if (s->tc_layer2 && NP + 32 <= 256) {
       // layer 2 on the tensor core (A1 / delta2 as TMEM A operands)
       const size_t tc_bytes = 1024 + (size_t)((NP + 31) / 32) * 2048 + (size_t)NP * 128 + (size_t)NP * 4 + 64 +
                               8 * sizeof(double) + 16;
