@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdasmc_gpu.so")
+# DASMC_GPU_LIB overrides the library path (profiling builds of the same sources)
+LIB_PATH = os.environ.get("DASMC_GPU_LIB") or os.path.join(_HERE, "libdasmc_gpu.so")
 
 DASMC_OK, DASMC_EINVAL, DASMC_EDEAD, DASMC_ECUDA = 0, -1, -2, -3
 RELU, TANH = 0, 1

@@ -31,14 +31,13 @@ struct TcState {
   int64_t n_pad = 0;     // X^T row stride (floats)
   int64_t mcap = 0;      // row stride of the transposed activation buffers
   bool split = false;    // split-tf32 (3 MMAs)
-  bool mma_layer2 = true; // fused forward runs the layer-2 products on mma.sync (DASMC_MMA_LAYER2=0: CUDA-core FFMA)
-  bool tc_layer2 = false; // fused forward runs layer 2 as TMEM-A MMAs (opt-in: DASMC_TC_LAYER2=1;
-                          // measured slower on B200: the small MMAs queue behind the next tile's)
+  int cluster = 1;       // fused-forward cluster shape (ClusterShape CL; 0 = single CTAs); DASMC_TC_CLUSTER
   float* Xt = nullptr;   // [(n0+1) x n_pad], row n0 = 1
-  float* Xhi = nullptr;  // [n x n0] X rounded to tf32 (cvt.rna): the MMA truncates raw fp32
-  float* Xlo = nullptr;  // [n x n0]   (split)
+  int64_t kx = 0;        // row stride of Xhi / W1hi: [x, 1] padded to 16 bytes (bias folded into K)
+  float* Xhi = nullptr;  // [n x kx] [X, 1, 0..] rounded to tf32 (rna): the MMA truncates raw fp32
+  float* Xlo = nullptr;  // [n x kx]   (split)
   float* Xtlo = nullptr; // [(n0+1) x n_pad] (split; ones row lo = 0)
-  float* W1hi = nullptr; // [J x n1 x n0] W1 rounded to tf32
+  float* W1hi = nullptr; // [J x n1 x kx] [W1, b1, 0..] rounded to tf32
   float* W1lo = nullptr;
   float* a1T = nullptr;  // [J x (n1+1) x mcap], row n1 = 1
   float* d1T = nullptr;  // [J x n1 x mcap]
@@ -55,14 +54,10 @@ constexpr int BM = 128;  // UMMA_M
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row
 constexpr int kEpiWarps = 12;            // 3 warps per TMEM lane group
 constexpr int kParts = kEpiWarps / 4;
-// Epilogue a1^T / delta1^T stores through TMA bulk tensor stores instead of
-// st.global.  Correct (tested) but measured slower on B200 at C2 (38.8 vs
-// 36.2 ms per forward: the 48 KB staging costs a pipeline stage), so off.
-constexpr bool kUseTmaStore = false;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;  // TMA warp + MMA warp + epilogue warps
 constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
-constexpr int kEpiKindFwd = 0, kEpiKindDw = 1, kEpiKindFwdTc = 2, kEpiKindFwdMma = 3;
+constexpr int kEpiKindFwd = 0, kEpiKindDw = 1;
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -73,9 +68,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // try_wait with a suspend-time hint: the waiting warp is parked by the
 // hardware (up to ~0.5 ms) instead of spinning and stealing issue slots from
@@ -103,6 +95,78 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if ((i & 0x3FFFu) == 0 && clock64() - t0 > 20000000000LL) __trap();
   }
 }
+
+// ---- CTA-pair (cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same shared-memory object in CTA `rank`
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on an mbarrier of the peer (or own) CTA given its shared::cluster address.
+// Default .release.cta semantics: the epilogue only has to order its completed
+// tcgen05.ld (wait::ld + fence::before_thread_sync) before the MMA reuses TMEM, and a
+// cluster-scope release would add a GPU-wide membar behind the warp's global stores.
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA loads for CTA pairs.  The bytes complete on the mbarrier of the pair
+// leader (`bar`: the leader's barrier as a shared::cluster address, peer bit 0).
+// The multicast forms write the same CTA-relative offset in every CTA of `mask`
+// and signal, for each destination, the barrier at `bar`'s offset in that
+// destination's pair leader.
+__device__ __forceinline__ void tma2_2d(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                        uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_3d(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2,
+                                        uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+// L2 eviction-priority policies for TMA loads (0 normal, 1 evict_last, 2 evict_first)
+__device__ __forceinline__ uint64_t l2_policy(int kind) {
+  uint64_t p;
+  if (kind == 1)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else if (kind == 2)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma2_2d_mc(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                           uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_3d_mc(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2,
+                                           uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6, %7;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "h"(mask), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -117,15 +181,14 @@ __device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, uint64
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
-// Bulk tensor store smem -> global (bulk async-group of the issuing thread).
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
-               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
+__device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                       int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
 }
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
 }
@@ -145,35 +208,27 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
-// D[tmem] (+)= A[tmem] . B[smem]  (A: 128 lanes x K columns, K-major)
-__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t acc) {
+// Pair MMA (leader CTA only): M = 256 rows, A rows 128r..128r+127 and B rows
+// (N/2)r..(N/2)r+N/2-1 from CTA r's shared memory at the same offsets; D rows
+// of CTA r land in CTA r's TMEM.
+__device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t acc) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0)
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+// commit the pair's outstanding MMAs to the mbarrier at this offset in every CTA of `mask`
+__device__ __forceinline__ void tc_commit2(uint64_t* bar, uint16_t mask) {
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-          taddr),
-      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
-      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
-      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
-      "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
-      "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
       : "memory");
-}
-__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-// Byte offset of element (row r, k) inside a K-major 128B-swizzled tile of
-// 32-element k-blocks (8-row core groups of 1024 B; 16 B chunks XOR row % 8).
-__device__ __forceinline__ uint32_t sw128_offset(int r, int k, int rows) {
-  const int kb = k >> 5, e = k & 31;
-  return (uint32_t)(kb * rows * 128 + r * 128 + ((((e >> 2) ^ (r & 7)) & 7) << 4) + (e & 3) * 4);
 }
 
 // 32 lanes x 32 bit, 16 consecutive columns per thread.
@@ -206,6 +261,23 @@ __device__ __forceinline__ void tmem_wait16(float* v) {
                  "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]), "+f"(v[14]),
                  "+f"(v[15])::"memory");
 }
+// Epilogue activation stores (a1^T, delta1^T: streamed once, re-read by the
+// weight-gradient GEMMs after ~25 GB of other traffic)
+#ifndef DASMC_ST_POLICY
+#define DASMC_ST_POLICY 0
+#endif
+__device__ __forceinline__ void st_act(float* p, float v, uint64_t pol) {
+#if DASMC_ST_POLICY == 1
+  asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+#elif DASMC_ST_POLICY == 2
+  asm volatile("st.global.L1::no_allocate.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+#elif DASMC_ST_POLICY == 3
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+#else
+  (void)pol;
+  *p = v;
+#endif
+}
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // K-major, 128B-swizzled UMMA shared-memory descriptor: 8-row core groups
@@ -214,47 +286,16 @@ __device__ __forceinline__ uint64_t smem_desc(const void* p) {
   const uint64_t a = (smem_u32(p) >> 4) & 0x3FFFULL;
   return a | (1ULL << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ULL << 46) | (2ULL << 61);
 }
-// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M = 128.
-__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M = 128 (256 for a pair).
+__host__ __device__ constexpr uint32_t idesc_tf32(int n, int m) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
+// Round to the nearest tf32 (ties away from zero), low 13 mantissa bits cleared:
+// what cvt.rna.tf32.f32 computes for finite inputs, in two integer ops (ptxas
+// otherwise expands the cvt with an extra non-finite guard).
 __device__ __forceinline__ float tf32_hi(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
-// Warp-level D(16x8) += A(16x8) . B(8x8), tf32 inputs, fp32 accumulate, split
-// into hi/lo parts (hi.hi + hi.lo + lo.hi) for fp32-level products.
-// Fragment layouts (g = lane / 4, t = lane % 4):
-//   A: a0 (g, t), a1 (g+8, t), a2 (g, t+4), a3 (g+8, t+4)
-//   B: b0 (k = t, n = g), b1 (k = t+4, n = g)
-//   D: d0 (g, 2t), d1 (g, 2t+1), d2 (g+8, 2t), d3 (g+8, 2t+1)
-__device__ __forceinline__ void mma_tf32(float* d, const uint32_t* a, const uint32_t* b) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
-}
-__device__ __forceinline__ void mma_3xtf32(float* d, const float* a, const float* b) {
-  uint32_t ah[4], al[4], bh[2], bl[2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float h = tf32_hi(a[i]);
-    ah[i] = __float_as_uint(h);
-    al[i] = __float_as_uint(tf32_hi(a[i] - h));
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const float h = tf32_hi(b[i]);
-    bh[i] = __float_as_uint(h);
-    bl[i] = __float_as_uint(tf32_hi(b[i] - h));
-  }
-  mma_tf32(d, al, bh);
-  mma_tf32(d, ah, bl);
-  mma_tf32(d, ah, bh);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 // ---------------------------------------------------------------- parameters
@@ -267,16 +308,17 @@ struct TileParams {
   int brows;   // TMA box rows of B (valid rows)
   int stages;
   uint32_t stage_bytes_tx;
+  int bbox;    // clusters with QB = 2: B rows per multicast piece (pieces at 0 and half - bbox)
+  int hint_a, hint_b;  // L2 policies of the A / B loads (pairs): 0 normal, 1 evict_last, 2 evict_first
 };
 
 struct FwdParams {
-  CUtensorMap mapS1;   // a1^T store map  {M, n1, J}, box {32, 16, 1}
-  CUtensorMap mapS2;   // delta1^T store map
   const float* theta;  // theta_in
-  int64_t Dp, boff1, woff2, boff2;
+  int64_t Dp, woff2, boff2;
   int n1, C, act;
   const int32_t* y;
   int64_t M, P;
+  int Jn;  // particles (clusters with QA = 2 may carry one padding particle)
   float beta_rows;
   int need_grad;
   int64_t ldm;  // row stride (floats) of the transposed buffers
@@ -303,21 +345,46 @@ __device__ __forceinline__ void tile_coords(const TileParams& tp, int t, int& rt
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int EPI, bool SPLIT, bool A3D, int CP>
+// CL = 0: one CTA per tile.  CL >= 1 (forward only): clusters of CTA pairs.  A
+// pair (CTA ranks 2p, 2p+1 on one TPC) computes two 128-row tiles of one
+// particle: CTA r loads rows of A for its tile and half the B rows, the leader
+// (r = 0) issues cta_group::2 MMAs (M = 256) reading both CTAs' shared memory,
+// and each CTA's epilogue drains its own TMEM.  Per CTA this halves the B
+// (per-particle W1) bytes streamed from L2.  The cluster holds QA x QB pairs:
+// QA = 2 puts two particles on the same rows (the A tile -- X -- is multicast to
+// both pairs, each CTA loading half of it), QB = 2 puts two row pairs on the
+// same particle (B -- W1 -- multicast).  Multicast cuts L2 -> SM traffic, the
+// forward GEMM's bound.
+template <int CL>
+struct ClusterShape {
+  static constexpr bool kPair = CL > 0;
+  static constexpr int QA = (CL == 2 || CL == 4) ? 2 : 1;
+  static constexpr int QB = (CL == 3 || CL == 4) ? 2 : 1;
+  static constexpr int kSize = kPair ? 2 * QA * QB : 1;
+};
+
+template <int EPI, bool SPLIT, bool A3D, int CP, int ACT, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
               const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo, TileParams tp,
               const __grid_constant__ FwdParams fp, DwParams dp) {
-  constexpr bool kTmaStore = kUseTmaStore && EPI == kEpiKindFwd && !SPLIT;
-  const CUtensorMap& mapS1 = fp.mapS1;
-  const CUtensorMap& mapS2 = fp.mapS2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128B swizzle atoms; keep the pointer derived
   // from smem_raw so the compiler emits shared-memory (LDS/STS) accesses.
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  using CS_ = ClusterShape<CL>;
+  constexpr bool PAIR = CS_::kPair;
+  constexpr int QA = CS_::QA, QB = CS_::QB, CSZ = CS_::kSize;
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
+  const uint32_t prank = crank & 1u;              // rank inside the pair
+  const int pr = (int)(crank >> 1);               // pair inside the cluster
+  const int qa = pr / QB, qb = pr % QB;           // particle slot, row slot
+  const int unit0 = (int)blockIdx.x / CSZ;
+  const int ustride = (int)gridDim.x / CSZ;
+  const uint32_t b_rows = PAIR ? (uint32_t)tp.nmma / 2 : (uint32_t)tp.nmma;  // B rows held by this CTA
   const uint32_t a_bytes = BM * BK * 4;
-  const uint32_t b_bytes = (uint32_t)tp.nmma * BK * 4;
+  const uint32_t b_bytes = b_rows * BK * 4;
   const uint32_t sub = SPLIT ? 2 : 1;
   const uint32_t stage_bytes = sub * (a_bytes + b_bytes);
   uint8_t* stages = smem;
@@ -345,47 +412,110 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < tp.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      // a stage is free once every pair of the cluster consumed it (multicast writes
+      // land in other pairs' stages): one commit per pair leader
+      mbar_init(&empty[s], PAIR ? QA * QB : 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], kEpiThreads);
+      // one arrival per epilogue warp (of both CTAs of a pair: the leader's barrier)
+      mbar_init(&tempty[b], (PAIR ? 2 : 1) * kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync_all();  // the peer's barriers are initialised before any remote arrive / complete_tx
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  const int ntiles = tp.rtiles * tp.J;
+  const int ntiles = tp.rtiles * tp.J;  // scheduling units (row-tile pairs x particles when PAIR)
 
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        int rt, j;
-        tile_coords(tp, t, rt, j);
+      // multicast groups: CTAs sharing this CTA's A tile (same row slot and pair rank,
+      // every particle slot) and its B rows (same particle slot and pair rank)
+      uint16_t amask = 0, bmask = 0;
+      for (int a = 0; a < QA; ++a) amask |= (uint16_t)(1u << (prank + 2 * (qb + QB * a)));
+      for (int b = 0; b < QB; ++b) bmask |= (uint16_t)(1u << (prank + 2 * (b + QB * qa)));
+      const int arows = BM / QA;                                   // A rows this CTA issues
+      const int boff = qb == 0 ? 0 : (int)b_rows - tp.bbox;        // B piece this CTA issues
+      const uint64_t pol_a = l2_policy(tp.hint_a), pol_b = l2_policy(tp.hint_b);
+      for (int t = unit0; t < ntiles; t += ustride) {
+        int ru, j;
+        tile_coords(tp, t, ru, j);
+        const int rt = PAIR ? 2 * (QB * ru + qb) + (int)prank : ru;
+        if (PAIR) j = QA * j + qa;
         for (int kb = 0; kb < tp.nkb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], tp.stage_bytes_tx);
           const int k0 = kb * BK;
-          if (A3D) {
-            tma_3d(A_of(s, 0), &mapA, &full[s], k0, rt * BM, j);
-            if (SPLIT) tma_3d(A_of(s, 1), &mapAlo, &full[s], k0, rt * BM, j);
+          if (PAIR) {
+            // the pair's bytes complete on its leader's full barrier (expect_tx covers the pair)
+            const uint32_t fb = mapa_shared(smem_u32(&full[s]), crank & ~1u);
+            if (prank == 0) mbar_expect_tx(&full[s], tp.stage_bytes_tx);
+            if (QA == 1) {
+              tma2_2d(A_of(s, 0), &mapA, fb, k0, rt * BM, pol_a);
+              if (SPLIT) tma2_2d(A_of(s, 1), &mapAlo, fb, k0, rt * BM, pol_a);
+            } else {
+              const int r0 = qa * arows;
+              tma2_2d_mc(A_of(s, 0) + r0 * 128, &mapA, fb, k0, rt * BM + r0, amask, pol_a);
+              if (SPLIT) tma2_2d_mc(A_of(s, 1) + r0 * 128, &mapAlo, fb, k0, rt * BM + r0, amask, pol_a);
+            }
+            const int brow = (int)(prank * b_rows);
+            if (QB == 1) {
+              tma2_3d(B_of(s, 0), &mapB, fb, k0, brow, j, pol_b);
+              if (SPLIT) tma2_3d(B_of(s, 1), &mapBlo, fb, k0, brow, j, pol_b);
+            } else {
+              tma2_3d_mc(B_of(s, 0) + boff * 128, &mapB, fb, k0, brow + boff, j, bmask, pol_b);
+              if (SPLIT) tma2_3d_mc(B_of(s, 1) + boff * 128, &mapBlo, fb, k0, brow + boff, j, bmask, pol_b);
+            }
           } else {
-            tma_2d(A_of(s, 0), &mapA, &full[s], k0, rt * BM);
-            if (SPLIT) tma_2d(A_of(s, 1), &mapAlo, &full[s], k0, rt * BM);
+            mbar_expect_tx(&full[s], tp.stage_bytes_tx);
+            // row-blocked operands [J][blk][rows][128] (K = window rows): 4-D coordinates
+            // (k within block, row, block, particle); a 32-wide k block never straddles blocks
+            if (A3D) {
+              tma_4d(A_of(s, 0), &mapA, &full[s], k0 & 127, rt * BM, k0 >> 7, j);
+              if (SPLIT) tma_4d(A_of(s, 1), &mapAlo, &full[s], k0 & 127, rt * BM, k0 >> 7, j);
+            } else {
+              tma_2d(A_of(s, 0), &mapA, &full[s], k0, rt * BM);
+              if (SPLIT) tma_2d(A_of(s, 1), &mapAlo, &full[s], k0, rt * BM);
+            }
+            if (EPI == kEpiKindDw) {
+              tma_4d(B_of(s, 0), &mapB, &full[s], k0 & 127, 0, k0 >> 7, j);
+              if (SPLIT) tma_4d(B_of(s, 1), &mapBlo, &full[s], k0 & 127, 0, k0 >> 7, j);
+            } else {
+              tma_3d(B_of(s, 0), &mapB, &full[s], k0, 0, j);
+              if (SPLIT) tma_3d(B_of(s, 1), &mapBlo, &full[s], k0, 0, j);
+            }
           }
-          tma_3d(B_of(s, 0), &mapB, &full[s], k0, 0, j);
-          if (SPLIT) tma_3d(B_of(s, 1), &mapBlo, &full[s], k0, 0, j);
+          if (++s == tp.stages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+      if (PAIR) {
+        // drain: every stage this CTA filled has been released by the leader's MMAs
+        // (their multicast commits land in this CTA's shared memory before it exits)
+        for (int i = 0; i < tp.stages; ++i) {
+          mbar_wait(&empty[s], ph ^ 1);
           if (++s == tp.stages) {
             s = 0;
             ph ^= 1;
@@ -394,14 +524,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0) {
-      const uint32_t idesc = idesc_tf32(tp.nmma);
+    // ===================== MMA issuer (one thread; the leader's when PAIR) =====================
+    if (lane == 0 && prank == 0) {
+      const uint32_t idesc = idesc_tf32(tp.nmma, PAIR ? 2 * BM : BM);
+      const uint16_t all_mask = (uint16_t)((1u << CSZ) - 1u);
+      const uint16_t pair_mask = (uint16_t)(3u << (2 * pr));
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = unit0; t < ntiles; t += ustride) {
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * 256);
@@ -413,179 +545,216 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
             const uint64_t off = (uint64_t)(k * 32) >> 4;  // 32 bytes per K=8 step inside the swizzle row
-            tc_mma(d, ad + off, bd + off, idesc, (kb | k) != 0);
-            if (SPLIT) {
-              tc_mma(d, ad + off, bdl + off, idesc, 1);
-              tc_mma(d, adl + off, bd + off, idesc, 1);
+            if (PAIR) {
+              tc_mma2(d, ad + off, bd + off, idesc, (kb | k) != 0);
+              if (SPLIT) {
+                tc_mma2(d, ad + off, bdl + off, idesc, 1);
+                tc_mma2(d, adl + off, bd + off, idesc, 1);
+              }
+            } else {
+              tc_mma(d, ad + off, bd + off, idesc, (kb | k) != 0);
+              if (SPLIT) {
+                tc_mma(d, ad + off, bdl + off, idesc, 1);
+                tc_mma(d, adl + off, bd + off, idesc, 1);
+              }
             }
           }
-          tc_commit(&empty[s]);
+          if (PAIR)
+            tc_commit2(&empty[s], all_mask);
+          else
+            tc_commit(&empty[s]);
           if (++s == tp.stages) {
             s = 0;
             ph ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);
+        if (PAIR)
+          tc_commit2(&tfull[acc], pair_mask);
+        else
+          tc_commit(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) aph ^= 1;
       }
     }
   } else {
-    // ===================== epilogue warps 2..9 =====================
+    // ===================== epilogue warps 2..13 =====================
     // kParts warps share each TMEM lane group (warp % 4); `part` selects a
     // contiguous range of 16-column accumulator chunks.
     const int et = threadIdx.x - 64;
     const int lg = warp & 3;
     const int part = (warp - 2) >> 2;
-    const int half = part;  // (kept for the opt-in TMEM-A layer-2 path, which needs kParts == 2)
     const int row_in_tile = lg * 32 + lane;
     auto chunk_range = [&](int nch, int& lo, int& hi) {
       lo = nch * part / kParts;
       hi = nch * (part + 1) / kParts;
     };
+    // the accumulator buffer is drained: one arrival per warp on the MMA issuer's barrier
+    const uint32_t tempty_addr0 = PAIR ? mapa_shared(smem_u32(&tempty[0]), crank & ~1u) : smem_u32(&tempty[0]);
+    auto release_acc = [&](int a) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_addr0 + (uint32_t)(a * 8));
+    };
     int acc = 0;
     uint32_t aph = 0;
-    uint32_t sph = 0;  // parity of the small-MMA barrier (fused forward, tensor-core layer 2)
-    int nst = 0;       // TMA-store staging buffer counter (alternates the warp's two buffers)
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t st_pol = l2_policy(2);  // activation stores: evict first (DASMC_ST_POLICY 3)
+    int it = 0;                     // forward tiles processed (W2^T buffer parity)
+    double* ll_pending = nullptr;   // forward: ll slot of the previous tile, written by thread 0
+    double* red = (double*)(epi_smem + 2 * ((size_t)fp.n1 * ((CP + 3) & ~3) + ((CP + 3) & ~3)) +
+                            (size_t)kParts * 128 * CP);  // [4][2] lane-group partials
+    auto flush_ll = [&]() {
+      ll_pending[0] = red[0] + red[2] + red[4] + red[6];
+      ll_pending[1] = red[1] + red[3] + red[5] + red[7];
+      ll_pending = nullptr;
+    };
+    for (int t = unit0; t < ntiles; t += ustride) {
       int rt, j;
       tile_coords(tp, t, rt, j);
+      if (PAIR) {
+        rt = 2 * (QB * rt + qb) + (int)prank;
+        j = QA * j + qa;
+      }
+      if (EPI == kEpiKindFwd && PAIR && ((int64_t)rt * BM >= fp.M || j >= fp.Jn)) {
+        // a tile of the cluster wholly past the window (or a padding particle): nothing to store
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        release_acc(acc);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+        continue;
+      }
       if (EPI == kEpiKindFwd) {
+        // Fused forward epilogue.  The accumulator row already holds the full
+        // pre-activation z1 = [x, 1] . [W1, b1]^T (bias folded into the GEMM as
+        // an extra K column), and rows past the window are TMA zero-fill, so
+        // act(z1) = 0 there and every row-blocked store below is unconditional.
         const int n1 = fp.n1, C = fp.C;
-        float* W2T = epi_smem;                  // [n1][CP]  W2 transposed, zero-padded
-        float* b1s = W2T + (size_t)n1 * CP;     // [n1]
-        float* b2s = b1s + ((n1 + 3) & ~3);     // [CP]
-        float* z2x = b2s + CP;                  // [kParts][128][CP] partial layer-2 logits
-        double* red = (double*)(z2x + kParts * 128 * CP);  // [4][2]
-        float* stg_all = (float*)((uint8_t*)(red + 8) + ((128u - (smem_u32(red + 8) & 127u)) & 127u));
-        float* stg = stg_all + (warp - 2) * 1024;  // 2 x [16][32] fp32 per warp
+        constexpr int CS = (CP + 3) & ~3;       // W2^T row stride (float4 aligned)
+        // W2^T / b2 double-buffered by tile parity: the buffer written here was last read
+        // two tiles ago, before every thread passed the previous tile's barriers
+        float* W2T = epi_smem + (size_t)(it & 1) * ((size_t)n1 * CS + CS);  // [n1][CS]  W2 transposed, zero-padded
+        float* b2s = W2T + (size_t)n1 * CS;     // [CS]
+        float* z2x = epi_smem + 2 * ((size_t)n1 * CS + CS);  // [kParts][128][CP] partial layer-2 logits
+        ++it;
         const float* th = fp.theta + (int64_t)j * fp.Dp;
         // per-particle layer-2 parameters: all global loads issued before any
         // shared-memory store (one L2 round trip per tile, not one per element)
-        constexpr int kPer = (256 * CP + kEpiThreads - 1) / kEpiThreads;
+        constexpr int kPer = (256 * CS + kEpiThreads - 1) / kEpiThreads;
         float wv[kPer];
 #pragma unroll
         for (int r = 0; r < kPer; ++r) {
           const int i = et + r * kEpiThreads;
-          const int o = i / CP, c = i - o * CP;
-          wv[r] = (i < n1 * CP && c < C) ? th[fp.woff2 + (int64_t)c * n1 + o] : 0.f;
+          const int o = i / CS, c = i - o * CS;
+          wv[r] = (i < n1 * CS && c < C) ? th[fp.woff2 + (int64_t)c * n1 + o] : 0.f;
         }
-        const float bv = et < n1 ? th[fp.boff1 + et] : 0.f;
         const float b2v = et < C ? th[fp.boff2 + et] : 0.f;
-        named_bar(1, kEpiThreads);  // the previous tile is done with the shared parameters
 #pragma unroll
         for (int r = 0; r < kPer; ++r) {
           const int i = et + r * kEpiThreads;
-          if (i < n1 * CP) W2T[i] = wv[r];
+          if (i < n1 * CS) W2T[i] = wv[r];
         }
-        if (et < n1) b1s[et] = bv;
-        if (et < CP) b2s[et] = b2v;
+        if (et < CS) b2s[et] = b2v;
         named_bar(1, kEpiThreads);
+        if (et == 0 && ll_pending) flush_ll();
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(lg * 32) << 16);
         const int64_t m = (int64_t)rt * BM + row_in_tile;
         const bool valid = m < fp.M;
-        const bool relu = fp.act == DASMC_RELU;
-        const bool wr_out = valid && fp.need_grad && fp.dbg != 1;
+        const bool st_rows = fp.need_grad && fp.dbg != 1;
         int c_lo, c_hi;
         chunk_range((n1 + 15) >> 4, c_lo, c_hi);
         if (fp.dbg == 3) c_hi = c_lo;
-        const int64_t ldm = fp.ldm;
-        const float4* W2T4 = reinterpret_cast<const float4*>(W2T);
+        // transposed buffers are row-blocked [J][nblk][rows][128]: a tile's rows are one
+        // contiguous region; consecutive rows of a block are 128 floats apart
+        const int64_t nblk = fp.ldm;
+        constexpr int64_t kRow = 128;
         float z2[CP];
 #pragma unroll
         for (int c = 0; c < CP; ++c) z2[c] = 0.f;
-        float* a1T = fp.a1T + (int64_t)j * (n1 + 1) * ldm + m;
-        float* a1Tlo = SPLIT ? fp.a1Tlo + (int64_t)j * (n1 + 1) * ldm + m : nullptr;
-        // pass 1: a1 = act(z1 + b1); partial z2 = W2 a1 over this warp's columns
-        // TMA-store staging (non-split): the warp's 32 rows x 16 columns go to a
-        // [16][32] smem tile, one bulk tensor store per chunk (clipped at m >= M, o >= n1)
-        const bool st_any = kTmaStore && fp.need_grad && fp.dbg != 1;
-        auto stage_begin = [&]() -> float* {
-          float* buf = stg + (nst & 1) * 512;
-          if (lane == 0) bulk_wait_read1();  // the store that last used this buffer has read it
-          __syncwarp();
-          return buf;
-        };
-        auto stage_end = [&](const CUtensorMap* map, float* buf, int o0) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(map, buf, rt * BM + lg * 32, o0, j);
-            bulk_commit();
-          }
-          ++nst;
-        };
-        auto pass1 = [&](const float* v, int q, const float4* w4, float b, float*& pa, float*& pal, float* sb) {
-          float a = v[q] + b;
-          a = relu ? fmaxf(a, 0.f) : tanhf(a);
+        // DASMC_DEBUG_EPI=4 (profiling only): every tile stores into one L2-resident block
+        const int64_t sblk = fp.dbg == 4 ? (int64_t)(blockIdx.x & 1) : (int64_t)j * nblk + rt;
+        float* a1T = fp.a1T + sblk * (n1 + 1) * kRow + row_in_tile;
+        float* a1Tlo = SPLIT ? fp.a1Tlo + ((int64_t)j * nblk + rt) * (n1 + 1) * kRow + row_in_tile : nullptr;
+        // row o of W2^T (CP classes) from shared memory: float4 loads (+ one float2)
+        auto w2row = [&](int o, float* w) {
+          const float* p = W2T + o * CS;
 #pragma unroll
           for (int u = 0; u < CP / 4; ++u) {
-            const float4 w = w4[q * (CP / 4) + u];
-            z2[4 * u] = fmaf(a, w.x, z2[4 * u]);
-            z2[4 * u + 1] = fmaf(a, w.y, z2[4 * u + 1]);
-            z2[4 * u + 2] = fmaf(a, w.z, z2[4 * u + 2]);
-            z2[4 * u + 3] = fmaf(a, w.w, z2[4 * u + 3]);
+            const float4 x = *reinterpret_cast<const float4*>(p + 4 * u);
+            w[4 * u] = x.x;
+            w[4 * u + 1] = x.y;
+            w[4 * u + 2] = x.z;
+            w[4 * u + 3] = x.w;
           }
-          if (kTmaStore) {
-            if (st_any) sb[q * 32 + lane] = tf32_hi(a);
-          } else {
-            if (wr_out) {
-              const float hi = tf32_hi(a);
-              *pa = hi;
-              if (SPLIT) *pal = a - hi;
-            }
-            pa += ldm;
-            if (SPLIT) pal += ldm;
+          if (CP % 4) {
+            const float2 x = *reinterpret_cast<const float2*>(p + 4 * (CP / 4));
+            w[CP - 2] = x.x;
+            w[CP - 1] = x.y;
           }
         };
-        auto chunk1 = [&](int ch, const float* v) {
+        auto act = [](float z) { return ACT == DASMC_RELU ? fmaxf(z, 0.f) : tanhf(z); };
+        // pass 1: a1 = act(z1); partial z2 = W2 a1 over this warp's columns
+        auto chunk1 = [&](auto store, int ch, const float* v) {
           const int o0 = ch * 16;
           const int nq = min(16, n1 - o0);  // warp-uniform
-          float* pa = a1T + (int64_t)o0 * ldm;
-          float* pal = SPLIT ? a1Tlo + (int64_t)o0 * ldm : nullptr;
-          const float4* w4 = W2T4 + o0 * (CP / 4);
-          float* sb = st_any ? stage_begin() : nullptr;
+          float* pa = a1T + (int64_t)o0 * kRow;
+          float* pal = SPLIT ? a1Tlo + (int64_t)o0 * kRow : nullptr;
+          auto one = [&](int q) {
+            const float a = act(v[q]);
+            float w[CP];
+            w2row(o0 + q, w);
+#pragma unroll
+            for (int c = 0; c < CP; ++c) z2[c] = fmaf(a, w[c], z2[c]);
+            if (decltype(store)::value) {
+              const float hi = tf32_hi(a);
+              st_act(pa + q * kRow, hi, st_pol);
+              if (SPLIT) st_act(pal + q * kRow, a - hi, st_pol);
+            }
+          };
           if (nq == 16) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) pass1(v, q, w4, b1s[o0 + q], pa, pal, sb);
+            for (int q = 0; q < 16; ++q) one(q);
           } else {  // tail chunk: still unrolled so v[] stays in registers
 #pragma unroll
             for (int q = 0; q < 16; ++q)
-              if (q < nq) pass1(v, q, w4, b1s[o0 + q], pa, pal, sb);
+              if (q < nq) one(q);
           }
-          if (st_any) stage_end(&mapS1, sb, o0);
         };
-        {  // TMEM loads double-buffered: chunk ch+1 is in flight while ch is processed
+        // TMEM loads double-buffered: chunk ch+1 is in flight while ch is processed
+        auto run_chunks = [&](auto body) {
           float va[16] = {}, vb[16] = {};
           int ch = c_lo;
           if (ch < c_hi) tmem_ld16_async(taddr + ch * 16, va);
           tmem_wait16(va);
           while (ch < c_hi) {
             if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, vb);
-            chunk1(ch, va);
+            body(ch, va);
             tmem_wait16(vb);
             if (++ch >= c_hi) break;
             if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, va);
-            chunk1(ch, vb);
+            body(ch, vb);
             tmem_wait16(va);
             ++ch;
           }
-        }
+        };
+        if (st_rows)
+          run_chunks([&](int ch, const float* v) { chunk1(std::true_type{}, ch, v); });
+        else
+          run_chunks([&](int ch, const float* v) { chunk1(std::false_type{}, ch, v); });
         // combine the column parts in a fixed order
         float* zx = z2x + ((size_t)part * 128 + row_in_tile) * CP;
 #pragma unroll
         for (int c = 0; c < CP; ++c) zx[c] = z2[c];
         named_bar(1, kEpiThreads);
-        // part 0 alone: log-softmax likelihood of the row (network.hpp:183-193) --
-        // fp32 exponentials, fp64 log-normaliser and ll -- and delta2, shared via
-        // its z2x slot with the other parts
+        // every part: log-softmax likelihood of the row (network.hpp:183-193) --
+        // fp32 exponentials, fp64 log-normaliser and ll -- and delta2, computed
+        // redundantly per part (no second barrier); part 0 stores delta2^T
         double ll = 0.0;
         float d2[CP];
 #pragma unroll
         for (int c = 0; c < CP; ++c) d2[c] = 0.f;
-        if (part == 0) {
+        {
 #pragma unroll
           for (int c = 0; c < CP; ++c) {
             float s = z2x[(size_t)row_in_tile * CP + c];
@@ -593,6 +762,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int p = 1; p < kParts; ++p) s += z2x[((size_t)p * 128 + row_in_tile) * CP + c];
             z2[c] = s + b2s[c];
           }
+          float* d2T = fp.d2T + ((int64_t)j * nblk + rt) * C * kRow + row_in_tile;
+          float* d2Tlo = SPLIT ? fp.d2Tlo + ((int64_t)j * nblk + rt) * C * kRow + row_in_tile : nullptr;
           if (valid) {
             const int yi = fp.y[m];
             float mx = z2[0];
@@ -616,576 +787,78 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int c = 0; c < CP; ++c)
                 if (c < C) {
                   d2[c] = wrow * ((c == yi ? 1.f : 0.f) - e[c] * rden);
-                  const float hi = tf32_hi(d2[c]);
-                  fp.d2T[((int64_t)j * C + c) * ldm + m] = hi;
-                  if (SPLIT) fp.d2Tlo[((int64_t)j * C + c) * ldm + m] = d2[c] - hi;
+                  if (part == 0) {
+                    const float hi = tf32_hi(d2[c]);
+                    d2T[c * kRow] = hi;
+                    if (SPLIT) d2Tlo[c * kRow] = d2[c] - hi;
+                  }
                 }
             }
-          }
-#pragma unroll
-          for (int c = 0; c < CP; ++c) zx[c] = d2[c];
-        }
-        if (fp.need_grad && fp.dbg == 0) {
-          named_bar(1, kEpiThreads);
-          if (part != 0) {
-#pragma unroll
-            for (int c = 0; c < CP; ++c) d2[c] = z2x[(size_t)row_in_tile * CP + c];
+          } else if (fp.need_grad && part == 0) {  // rows past the window: zeros in the row-blocked delta2^T
+            for (int c = 0; c < C; ++c) {
+              d2T[c * kRow] = 0.f;
+              if (SPLIT) d2Tlo[c * kRow] = 0.f;
+            }
           }
         }
         if (fp.need_grad && fp.dbg == 0) {
-          // pass 2: delta1 = (W2^T delta2) . act'(a1)  (network.hpp:209-215)
-          float* d1T = fp.d1T + (int64_t)j * n1 * ldm + m;
-          float* d1Tlo = SPLIT ? fp.d1Tlo + (int64_t)j * n1 * ldm + m : nullptr;
-          auto pass2 = [&](const float* v, int q, const float4* w4, float b, float*& pd, float*& pdl, float* sb) {
-            float a = v[q] + b;
-            a = relu ? fmaxf(a, 0.f) : tanhf(a);
-            float dx = 0.f, dy = 0.f, dzz = 0.f, dw = 0.f;  // 4 independent chains
-#pragma unroll
-            for (int u = 0; u < CP / 4; ++u) {
-              const float4 w = w4[q * (CP / 4) + u];
-              dx = fmaf(d2[4 * u], w.x, dx);
-              dy = fmaf(d2[4 * u + 1], w.y, dy);
-              dzz = fmaf(d2[4 * u + 2], w.z, dzz);
-              dw = fmaf(d2[4 * u + 3], w.w, dw);
-            }
-            const float dz = (dx + dy) + (dzz + dw);
-            const float d1 = relu ? dz * (a > 0.f ? 1.f : 0.f) : dz * (1.f - a * a);
-            const float hi = tf32_hi(d1);
-            if (kTmaStore) {
-              sb[q * 32 + lane] = hi;
-            } else {
-              if (valid) {
-                *pd = hi;
-                if (SPLIT) *pdl = d1 - hi;
-              }
-              pd += ldm;
-              if (SPLIT) pdl += ldm;
-            }
-          };
+          // pass 2: delta1 = (W2^T delta2) . act'(z1)  (network.hpp:209-215); zero past the window
+          float* d1T = fp.d1T + sblk * n1 * kRow + row_in_tile;
+          float* d1Tlo = SPLIT ? fp.d1Tlo + ((int64_t)j * nblk + rt) * n1 * kRow + row_in_tile : nullptr;
           auto chunk2 = [&](int ch, const float* v) {
             const int o0 = ch * 16;
             const int nq = min(16, n1 - o0);  // warp-uniform
-            float* pd = d1T + (int64_t)o0 * ldm;
-            float* pdl = SPLIT ? d1Tlo + (int64_t)o0 * ldm : nullptr;
-            const float4* w4 = W2T4 + o0 * (CP / 4);
-            float* sb = kTmaStore ? stage_begin() : nullptr;
+            float* pd = d1T + (int64_t)o0 * kRow;
+            float* pdl = SPLIT ? d1Tlo + (int64_t)o0 * kRow : nullptr;
+            auto one = [&](int q) {
+              float w[CP];
+              w2row(o0 + q, w);
+              float dx = 0.f, dy = 0.f;  // two independent chains
+#pragma unroll
+              for (int c = 0; c < CP; c += 2) {
+                dx = fmaf(d2[c], w[c], dx);
+                dy = fmaf(d2[c + 1], w[c + 1], dy);
+              }
+              const float dz = dx + dy;
+              float d1;
+              if (ACT == DASMC_RELU) {
+                d1 = v[q] > 0.f ? dz : 0.f;
+              } else {
+                const float a = tanhf(v[q]);
+                d1 = dz * (1.f - a * a);
+              }
+              const float hi = tf32_hi(d1);
+              st_act(pd + q * kRow, hi, st_pol);
+              if (SPLIT) st_act(pdl + q * kRow, d1 - hi, st_pol);
+            };
             if (nq == 16) {
 #pragma unroll
-              for (int q = 0; q < 16; ++q) pass2(v, q, w4, b1s[o0 + q], pd, pdl, sb);
+              for (int q = 0; q < 16; ++q) one(q);
             } else {
 #pragma unroll
               for (int q = 0; q < 16; ++q)
-                if (q < nq) pass2(v, q, w4, b1s[o0 + q], pd, pdl, sb);
+                if (q < nq) one(q);
             }
-            if (kTmaStore) stage_end(&mapS2, sb, o0);
           };
-          float va[16] = {}, vb[16] = {};
-          int ch = c_lo;
-          if (ch < c_hi) tmem_ld16_async(taddr + ch * 16, va);
-          tmem_wait16(va);
-          while (ch < c_hi) {
-            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, vb);
-            chunk2(ch, va);
-            tmem_wait16(vb);
-            if (++ch >= c_hi) break;
-            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, va);
-            chunk2(ch, vb);
-            tmem_wait16(va);
-            ++ch;
-          }
+          run_chunks(chunk2);
         }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-        // per-tile prefix / block log-likelihood partials (deterministic order)
+        release_acc(acc);
+        // per-tile prefix / block log-likelihood partials (deterministic order): the
+        // four lane groups' sums go to red[]; thread 0 writes the tile's slot after the
+        // next tile's staging barrier (or after the loop), which orders it behind them
         double pre = (valid && m < fp.P) ? ll : 0.0, blk = (valid && m >= fp.P) ? ll : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          pre += __shfl_xor_sync(0xffffffffu, pre, o);
-          blk += __shfl_xor_sync(0xffffffffu, blk, o);
-        }
-        if (lane == 0 && half == 0) {
-          red[lg * 2] = pre;
-          red[lg * 2 + 1] = blk;
-        }
-        named_bar(1, kEpiThreads);
-        if (et == 0) {
-          double* o = fp.ll_part + ((int64_t)j * fp.ll_slots + rt) * 2;
-          o[0] = red[0] + red[2] + red[4] + red[6];
-          o[1] = red[1] + red[3] + red[5] + red[7];
-        }
-      } else if (EPI == kEpiKindFwdMma) {
-        // Fused forward with the layer-2 products on warp-level tensor cores:
-        // per 16-column chunk a warp stages its 32 rows x 16 columns of A1 in
-        // shared memory and runs z2 += A1 . W2^T (M 32, N 16, K 16) and, in
-        // pass 2, dz = delta2 . W2 (M 32, N 16, K 16) as split-tf32 mma.sync.
-        constexpr int WS = 24;  // W2T row stride (floats): conflict-free B loads in pass 1
-        constexpr int ZS = 20;  // row stride of the per-warp staging / exchange tiles
-        const int n1 = fp.n1, C = fp.C;
-        const int NP = tp.nmma;
-        float* W2T = epi_smem;                  // [NP][WS]  W2 transposed, zero-padded (c >= C, o >= n1)
-        float* b1s = W2T + (size_t)NP * WS;     // [NP]
-        float* b2s = b1s + NP;                  // [16]
-        float* z2x = b2s + 16;                  // [kParts][128][ZS] z2 partials, then delta2 in part 0
-        double* red = (double*)(z2x + kParts * 128 * ZS);  // [4][2]
-        float* As = (float*)(red + 8) + (warp - 2) * 32 * ZS;  // per-warp [32][ZS] staging
-        const float* th = fp.theta + (int64_t)j * fp.Dp;
-        constexpr int kPerW = (256 * 16 + kEpiThreads - 1) / kEpiThreads;
-        float wv[kPerW];
-#pragma unroll
-        for (int r = 0; r < kPerW; ++r) {  // element (o, c) -> W2[c][o]
-          const int i = et + r * kEpiThreads;
-          const int o = i >> 4, c = i & 15;
-          wv[r] = (o < n1 && c < C) ? th[fp.woff2 + (int64_t)c * n1 + o] : 0.f;
-        }
-        const float bv = et < n1 ? th[fp.boff1 + et] : 0.f;
-        const float b2v = et < C ? th[fp.boff2 + et] : 0.f;
-        named_bar(1, kEpiThreads);
-#pragma unroll
-        for (int r = 0; r < kPerW; ++r) {
-          const int i = et + r * kEpiThreads;
-          if (i < NP * 16) W2T[(i >> 4) * WS + (i & 15)] = wv[r];
-        }
-        if (et < NP) b1s[et] = bv;
-        if (et < 16) b2s[et] = b2v;
-        named_bar(1, kEpiThreads);
-        mbar_wait(&tfull[acc], aph);
-        tc_fence_after();
-        const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(lg * 32) << 16);
-        const int64_t m = (int64_t)rt * BM + row_in_tile;
-        const bool valid = m < fp.M;
-        const bool relu = fp.act == DASMC_RELU;
-        const bool wr_out = valid && fp.need_grad && fp.dbg != 1;
-        int c_lo, c_hi;
-        chunk_range(NP >> 4, c_lo, c_hi);
-        if (fp.dbg == 3) c_hi = c_lo;
-        const int64_t ldm = fp.ldm;
-        const int g = lane >> 2, tq = lane & 3;
-        float zacc[2][2][4];
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-#pragma unroll
-          for (int b = 0; b < 2; ++b)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) zacc[a][b][q] = 0.f;
-        float* a1T = fp.a1T + (int64_t)j * (n1 + 1) * ldm + m;
-        float* a1Tlo = SPLIT ? fp.a1Tlo + (int64_t)j * (n1 + 1) * ldm + m : nullptr;
-        // pass 1: a1 = act(z1 + b1) -> a1^T; z2 += A1 . W2^T on mma.sync
-        auto chunk1 = [&](int ch, const float* v) {
-          const int o0 = ch * 16;
-          float* pa = a1T + (int64_t)o0 * ldm;
-          float* pal = SPLIT ? a1Tlo + (int64_t)o0 * ldm : nullptr;
-          float a[16];
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            a[q] = v[q] + b1s[o0 + q];
-            a[q] = relu ? fmaxf(a[q], 0.f) : tanhf(a[q]);
-            if (o0 + q >= n1) a[q] = 0.f;
-            if (wr_out && o0 + q < n1) {
-              const float hi = tf32_hi(a[q]);
-              *pa = hi;
-              if (SPLIT) *pal = a[q] - hi;
-            }
-            pa += ldm;
-            if (SPLIT) pal += ldm;
-          }
-          float4* as4 = reinterpret_cast<float4*>(As + lane * ZS);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) as4[q] = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
-          __syncwarp();
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            float bf[2][2];
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-              bf[nt][0] = W2T[(o0 + 8 * ks + tq) * WS + 8 * nt + g];
-              bf[nt][1] = W2T[(o0 + 8 * ks + tq + 4) * WS + 8 * nt + g];
-            }
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-              const float* r0 = As + (16 * mt + g) * ZS + 8 * ks + tq;
-              const float af[4] = {r0[0], r0[8 * ZS], r0[4], r0[8 * ZS + 4]};
-#pragma unroll
-              for (int nt = 0; nt < 2; ++nt) mma_3xtf32(zacc[mt][nt], af, bf[nt]);
-            }
-          }
-          __syncwarp();
-        };
-        {
-          float va[16] = {}, vb[16] = {};
-          int ch = c_lo;
-          if (ch < c_hi) tmem_ld16_async(taddr + ch * 16, va);
-          tmem_wait16(va);
-          while (ch < c_hi) {
-            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, vb);
-            chunk1(ch, va);
-            tmem_wait16(vb);
-            if (++ch >= c_hi) break;
-            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, va);
-            chunk1(ch, vb);
-            tmem_wait16(va);
-            ++ch;
-          }
-        }
-        // z2 partial fragments -> exchange tile rows of this part
-        {
-          float* zb = z2x + ((size_t)part * 128 + lg * 32) * ZS;
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-              float* p0 = zb + (16 * mt + g) * ZS + 8 * nt + 2 * tq;
-              *reinterpret_cast<float2*>(p0) = make_float2(zacc[mt][nt][0], zacc[mt][nt][1]);
-              *reinterpret_cast<float2*>(p0 + 8 * ZS) = make_float2(zacc[mt][nt][2], zacc[mt][nt][3]);
-            }
-        }
-        named_bar(1, kEpiThreads);
-        double ll = 0.0;
         if (part == 0) {
-          float z2[16];
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            float s = z2x[(size_t)row_in_tile * ZS + c];
-#pragma unroll
-            for (int p = 1; p < kParts; ++p) s += z2x[((size_t)p * 128 + row_in_tile) * ZS + c];
-            z2[c] = s + b2s[c];
+          for (int o = 16; o > 0; o >>= 1) {
+            pre += __shfl_xor_sync(0xffffffffu, pre, o);
+            blk += __shfl_xor_sync(0xffffffffu, blk, o);
           }
-          float d2[16];
-#pragma unroll
-          for (int c = 0; c < 16; ++c) d2[c] = 0.f;
-          if (valid) {
-            const int yi = fp.y[m];
-            float mx = z2[0];
-#pragma unroll
-            for (int c = 1; c < 16; ++c)
-              if (c < C) mx = fmaxf(mx, z2[c]);
-            float e[16];
-            double den = 0.0;
-            float zy = 0.f;
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
-              e[c] = c < C ? expf(z2[c] - mx) : 0.f;
-              den += (double)e[c];
-              if (c == yi) zy = z2[c];
-            }
-            ll = (double)zy - ((double)mx + log(den));
-            if (fp.need_grad) {
-              const float wrow = m < fp.P ? 1.f : fp.beta_rows;
-              const float rden = (float)(1.0 / den);
-#pragma unroll
-              for (int c = 0; c < 16; ++c)
-                if (c < C) {
-                  d2[c] = wrow * ((c == yi ? 1.f : 0.f) - e[c] * rden);
-                  const float hi = tf32_hi(d2[c]);
-                  fp.d2T[((int64_t)j * C + c) * ldm + m] = hi;
-                  if (SPLIT) fp.d2Tlo[((int64_t)j * C + c) * ldm + m] = d2[c] - hi;
-                }
-            }
-          }
-          float* zx = z2x + (size_t)row_in_tile * ZS;
-#pragma unroll
-          for (int c = 0; c < 16; ++c) zx[c] = d2[c];
-        }
-        if (fp.need_grad && fp.dbg == 0) {
-          named_bar(1, kEpiThreads);
-          // delta2 A fragments of this warp's 32 rows (K = classes)
-          float df[2][2][4];
-          {
-            const float* db = z2x + (size_t)(lg * 32) * ZS;
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-              for (int ks = 0; ks < 2; ++ks) {
-                const float* r0 = db + (16 * mt + g) * ZS + 8 * ks + tq;
-                df[mt][ks][0] = r0[0];
-                df[mt][ks][1] = r0[8 * ZS];
-                df[mt][ks][2] = r0[4];
-                df[mt][ks][3] = r0[8 * ZS + 4];
-              }
-          }
-          float* d1T = fp.d1T + (int64_t)j * n1 * ldm + m;
-          float* d1Tlo = SPLIT ? fp.d1Tlo + (int64_t)j * n1 * ldm + m : nullptr;
-          auto chunk2 = [&](int ch, const float* v) {
-            const int o0 = ch * 16;
-            float dz[2][2][4];
-#pragma unroll
-            for (int a = 0; a < 2; ++a)
-#pragma unroll
-              for (int b = 0; b < 2; ++b)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) dz[a][b][q] = 0.f;
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-              float bf[2][2];
-#pragma unroll
-              for (int nt = 0; nt < 2; ++nt) {  // B(k = c, n = o) = W2[c][o]
-                bf[nt][0] = W2T[(o0 + 8 * nt + g) * WS + 8 * ks + tq];
-                bf[nt][1] = W2T[(o0 + 8 * nt + g) * WS + 8 * ks + tq + 4];
-              }
-#pragma unroll
-              for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-                for (int nt = 0; nt < 2; ++nt) mma_3xtf32(dz[mt][nt], df[mt][ks], bf[nt]);
-            }
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-              for (int nt = 0; nt < 2; ++nt) {
-                float* p0 = As + (16 * mt + g) * ZS + 8 * nt + 2 * tq;
-                *reinterpret_cast<float2*>(p0) = make_float2(dz[mt][nt][0], dz[mt][nt][1]);
-                *reinterpret_cast<float2*>(p0 + 8 * ZS) = make_float2(dz[mt][nt][2], dz[mt][nt][3]);
-              }
-            __syncwarp();
-            float dr[16];
-            const float4* as4 = reinterpret_cast<const float4*>(As + lane * ZS);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float4 f = as4[q];
-              dr[4 * q] = f.x;
-              dr[4 * q + 1] = f.y;
-              dr[4 * q + 2] = f.z;
-              dr[4 * q + 3] = f.w;
-            }
-            __syncwarp();
-            if (!valid) return;
-            float* pd = d1T + (int64_t)o0 * ldm;
-            float* pdl = SPLIT ? d1Tlo + (int64_t)o0 * ldm : nullptr;
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              if (o0 + q < n1) {
-                float a = v[q] + b1s[o0 + q];
-                a = relu ? fmaxf(a, 0.f) : tanhf(a);
-                const float d1 = relu ? dr[q] * (a > 0.f ? 1.f : 0.f) : dr[q] * (1.f - a * a);
-                const float hi = tf32_hi(d1);
-                *pd = hi;
-                if (SPLIT) *pdl = d1 - hi;
-              }
-              pd += ldm;
-              if (SPLIT) pdl += ldm;
-            }
-          };
-          float va[16] = {}, vb[16] = {};
-          int ch = c_lo;
-          if (ch < c_hi) tmem_ld16_async(taddr + ch * 16, va);
-          tmem_wait16(va);
-          while (ch < c_hi) {
-            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, vb);
-            chunk2(ch, va);
-            tmem_wait16(vb);
-            if (++ch >= c_hi) break;
-            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, va);
-            chunk2(ch, vb);
-            tmem_wait16(va);
-            ++ch;
+          if (lane == 0) {
+            red[lg * 2] = pre;
+            red[lg * 2 + 1] = blk;
           }
         }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-        double pre = (valid && m < fp.P) ? ll : 0.0, blk = (valid && m >= fp.P) ? ll : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          pre += __shfl_xor_sync(0xffffffffu, pre, o);
-          blk += __shfl_xor_sync(0xffffffffu, blk, o);
-        }
-        if (lane == 0 && part == 0) {
-          red[lg * 2] = pre;
-          red[lg * 2 + 1] = blk;
-        }
-        named_bar(1, kEpiThreads);
-        if (et == 0) {
-          double* o = fp.ll_part + ((int64_t)j * fp.ll_slots + rt) * 2;
-          o[0] = red[0] + red[2] + red[4] + red[6];
-          o[1] = red[1] + red[3] + red[5] + red[7];
-        }
-      } else if (EPI == kEpiKindFwdTc) {
-        // Layer 2 on the tensor core: A1 = act(Z1 + b1) is written back into
-        // the accumulator's TMEM columns and becomes the A operand of
-        //   z2 = A1 . W2^T   (N = 16, K = NP)   and   dz = delta2 . W2   (N = NP, K = 16),
-        // issued by one epilogue thread; the CUDA cores only do elementwise work.
-        const int n1 = fp.n1, C = fp.C;
-        const int NP = tp.nmma;                 // padded hidden width (TMEM columns of Z1)
-        const int nkb2 = (NP + 31) >> 5;        // 32-wide k blocks of the z2 GEMM
-        uint8_t* eb = (uint8_t*)epi_smem;
-        eb += (1024u - (smem_u32(eb) & 1023u)) & 1023u;
-        uint8_t* W2B = eb;                       // [nkb2][16 rows c][128 B]   B of z2 (K-major, SW128)
-        uint8_t* W2TB = W2B + nkb2 * 2048;      // [NP rows o][128 B]         B of dz (K = c, padded to 32)
-        float* b1s = (float*)(W2TB + NP * 128);  // [NP]
-        float* b2s = b1s + NP;                  // [16]
-        double* red = (double*)(b2s + 16);      // [4][2]
-        uint64_t* sbar = (uint64_t*)(red + 8);  // small-MMA completion barrier
-        if (et == 0 && t == (int)blockIdx.x) {
-          mbar_init(sbar, 1);
-          asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        named_bar(1, kEpiThreads);
-        const float* th = fp.theta + (int64_t)j * fp.Dp;
-        for (int i = et; i < 16 * NP; i += kEpiThreads) {  // W2 (c, o) into both B tiles
-          const int c = i / NP, o = i - c * NP;
-          const float w = (c < C && o < n1) ? tf32_hi(th[fp.woff2 + (int64_t)c * n1 + o]) : 0.f;
-          *(float*)(W2B + sw128_offset(c, o, 16)) = w;
-          *(float*)(W2TB + sw128_offset(o, c, NP)) = w;
-        }
-        for (int i = et; i < NP * 16; i += kEpiThreads) {  // zero the c in [16, 32) half of W2TB rows
-          const int o = i >> 4, c = 16 + (i & 15);
-          *(float*)(W2TB + sw128_offset(o, c, NP)) = 0.f;
-        }
-        for (int i = et; i < NP; i += kEpiThreads) b1s[i] = i < n1 ? th[fp.boff1 + i] : 0.f;
-        for (int i = et; i < 16; i += kEpiThreads) b2s[i] = i < C ? th[fp.boff2 + i] : 0.f;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> MMA reads
-        named_bar(1, kEpiThreads);
-        mbar_wait(&tfull[acc], aph);
-        tc_fence_after();
-        const uint32_t tcol = tmem_base + (uint32_t)(acc * 256);
-        const uint32_t lane_off = (uint32_t)(lg * 32) << 16;
-        const int64_t m = (int64_t)rt * BM + row_in_tile;
-        const bool valid = m < fp.M;
-        const bool relu = fp.act == DASMC_RELU;
-        const bool wr_out = valid && fp.need_grad;
-        int c_lo, c_hi;
-        chunk_range(NP >> 4, c_lo, c_hi);
-        const int64_t ldm = fp.ldm;
-        float* a1T = fp.a1T + (int64_t)j * (n1 + 1) * ldm + m;
-        float* a1Tlo = SPLIT ? fp.a1Tlo + (int64_t)j * (n1 + 1) * ldm + m : nullptr;
-        // pass 1: A1 = act(Z1 + b1) -> TMEM (in place, tf32-rounded) and a1^T
-        for (int ch = c_lo; ch < c_hi; ++ch) {
-          const int o0 = ch * 16;
-          float v[16];
-          tmem_ld16(tcol + lane_off + o0, v);
-          float* pa = a1T + (int64_t)o0 * ldm;
-          float* pal = SPLIT ? a1Tlo + (int64_t)o0 * ldm : nullptr;
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            float a = v[q] + b1s[o0 + q];
-            a = relu ? fmaxf(a, 0.f) : tanhf(a);
-            const float hi = tf32_hi(a);
-            v[q] = hi;
-            if (wr_out && o0 + q < n1) {
-              *pa = hi;
-              if (SPLIT) *pal = a - hi;
-            }
-            pa += ldm;
-            if (SPLIT) pal += ldm;
-          }
-          tmem_st16(tcol + lane_off + o0, v);
-        }
-        tmem_st_wait();
-        tc_fence_before();
-        named_bar(1, kEpiThreads);
-        if (et == 0) {  // z2 = A1 . W2^T into columns [NP, NP+16)
-          tc_fence_after();
-          const uint32_t id16 = idesc_tf32(16);
-          for (int s = 0; s < NP / 8; ++s)
-            tc_mma_ts(tcol + NP, tcol + 8 * s, smem_desc(W2B + (s >> 2) * 2048) + (uint64_t)((s & 3) * 2), id16,
-                      s > 0);
-          tc_commit(sbar);
-        }
-        mbar_wait(sbar, sph);
-        sph ^= 1;
-        tc_fence_after();
-        float z2[16];
-        tmem_ld16(tcol + lane_off + NP, z2);
-        double ll = 0.0;
-        float d2[16];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) d2[c] = 0.f;
-        if (valid) {
-          const int yi = fp.y[m];
-#pragma unroll
-          for (int c = 0; c < 16; ++c) z2[c] += b2s[c];
-          double mx = (double)z2[0];
-#pragma unroll
-          for (int c = 1; c < 16; ++c)
-            if (c < C) mx = fmax(mx, (double)z2[c]);
-          double den = 0.0, zy = 0.0;
-#pragma unroll
-          for (int c = 0; c < 16; ++c)
-            if (c < C) {
-              den += exp((double)z2[c] - mx);
-              if (c == yi) zy = (double)z2[c];
-            }
-          ll = zy - (mx + log(den));
-          if (fp.need_grad) {
-            const float wrow = m < fp.P ? 1.f : fp.beta_rows;
-#pragma unroll
-            for (int c = 0; c < 16; ++c)
-              if (c < C) {
-                const double pr = exp((double)z2[c] - mx) / den;
-                d2[c] = wrow * (float)((c == yi ? 1.0 : 0.0) - pr);
-                if (half == 0) {
-                  const float hi = tf32_hi(d2[c]);
-                  fp.d2T[((int64_t)j * C + c) * ldm + m] = hi;
-                  if (SPLIT) fp.d2Tlo[((int64_t)j * C + c) * ldm + m] = d2[c] - hi;
-                }
-              }
-          }
-        }
-        if (fp.need_grad) {
-          if (half == 0) {
-#pragma unroll
-            for (int c = 0; c < 16; ++c) d2[c] = tf32_hi(d2[c]);
-            tmem_st16(tcol + lane_off + NP + 16, d2);
-            tmem_st_wait();
-          }
-          tc_fence_before();
-          named_bar(1, kEpiThreads);
-          if (et == 0) {  // dz = delta2 . W2 into columns [0, NP) (overwrites A1)
-            tc_fence_after();
-            const uint32_t idn = idesc_tf32(NP);
-            tc_mma_ts(tcol, tcol + NP + 16, smem_desc(W2TB), idn, 0);
-            tc_mma_ts(tcol, tcol + NP + 24, smem_desc(W2TB) + 2, idn, 1);
-            tc_commit(sbar);
-          }
-          mbar_wait(sbar, sph);
-          sph ^= 1;
-          tc_fence_after();
-          // pass 2: delta1 = dz . act'(a1), a1 re-read from the a1^T just written (L2)
-          float* d1T = fp.d1T + (int64_t)j * n1 * ldm + m;
-          float* d1Tlo = SPLIT ? fp.d1Tlo + (int64_t)j * n1 * ldm + m : nullptr;
-          for (int ch = c_lo; ch < c_hi; ++ch) {
-            const int o0 = ch * 16;
-            float v[16];
-            tmem_ld16(tcol + lane_off + o0, v);
-            if (!valid) continue;
-            const float* pa = a1T + (int64_t)o0 * ldm;
-            const float* pal = SPLIT ? a1Tlo + (int64_t)o0 * ldm : nullptr;
-            float* pd = d1T + (int64_t)o0 * ldm;
-            float* pdl = SPLIT ? d1Tlo + (int64_t)o0 * ldm : nullptr;
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              if (o0 + q < n1) {
-                float a = *pa;
-                if (SPLIT && !relu) a += *pal;
-                const float d1 = relu ? v[q] * (a > 0.f ? 1.f : 0.f) : v[q] * (1.f - a * a);
-                const float hi = tf32_hi(d1);
-                *pd = hi;
-                if (SPLIT) *pdl = d1 - hi;
-              }
-              pa += ldm;
-              pd += ldm;
-              if (SPLIT) {
-                pal += ldm;
-                pdl += ldm;
-              }
-            }
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-        double pre = (valid && m < fp.P) ? ll : 0.0, blk = (valid && m >= fp.P) ? ll : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          pre += __shfl_xor_sync(0xffffffffu, pre, o);
-          blk += __shfl_xor_sync(0xffffffffu, blk, o);
-        }
-        if (lane == 0 && half == 0) {
-          red[lg * 2] = pre;
-          red[lg * 2 + 1] = blk;
-        }
-        named_bar(1, kEpiThreads);
-        if (et == 0) {
-          double* o = fp.ll_part + ((int64_t)j * fp.ll_slots + rt) * 2;
-          o[0] = red[0] + red[2] + red[4] + red[6];
-          o[1] = red[1] + red[3] + red[5] + red[7];
-        }
+        ll_pending = fp.ll_part + ((int64_t)j * fp.ll_slots + rt) * 2;
       } else {
         // weight-gradient tile: row i of A (input index, `in` = bias row), columns o
         mbar_wait(&tfull[acc], aph);
@@ -1211,25 +884,39 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        release_acc(acc);
       }
       acc ^= 1;
       if (acc == 0) aph ^= 1;
     }
-    if (kTmaStore && lane == 0) bulk_wait_all();  // outstanding epilogue stores done
+    if (EPI == kEpiKindFwd) {
+      named_bar(1, kEpiThreads);  // the last tile's lane-group partials are in red[]
+      if (et == 0 && ll_pending) flush_ll();
+    }
   }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols) : "memory");
+  __syncwarp();
+  if (PAIR) {
+    cluster_sync_all();  // no remote arrive / commit targets this CTA any more
+    if (warp == 1) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                   : "memory");
+    }
+  } else {
+    __syncthreads();
+    if (warp == 1) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                   : "memory");
+    }
   }
 }
 
 // ---------------------------------------------------------------- helper kernels
 // X^T with a ones row (and tf32 hi/lo splits): Xt[i][m] = X[m][i], Xt[n0][m] = 1.
-__global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n0, int64_t n_pad, float* Xt, float* Xtlo,
-                                   float* Xhi, float* Xlo, int split) {
+// Also the forward operand Xhi[m] = [X[m], 1, 0 ...] (row stride kx) and its lo part.
+__global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n0, int64_t n_pad, int64_t kx, float* Xt,
+                                   float* Xtlo, float* Xhi, float* Xlo, int split) {
   __shared__ float tile[32][33];
   const int64_t m0 = (int64_t)blockIdx.x * 32;
   const int i0 = blockIdx.y * 32;
@@ -1239,8 +926,8 @@ __global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n
     float v = 0.f;
     if (m < n && i < n0) v = X[m * n0 + i];
     if (m < n && i == n0) v = 1.f;
-    if (m < n && i < n0) Xhi[m * n0 + i] = tf32_hi(v);
-    if (split && m < n && i < n0) Xlo[m * n0 + i] = v - tf32_hi(v);
+    if (m < n && i < kx) Xhi[m * kx + i] = tf32_hi(v);
+    if (split && m < n && i < kx) Xlo[m * kx + i] = v - tf32_hi(v);
     tile[r][threadIdx.x] = v;
   }
   __syncthreads();
@@ -1256,23 +943,29 @@ __global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n
   }
 }
 
-__global__ void split_w1_kernel(const float* __restrict__ theta, int64_t Dp, int64_t woff, int64_t cnt, int64_t J,
-                                float* hi, float* lo) {
-  const int64_t total = J * cnt;
+// W1hi[j][o] = [W1[o], b1[o], 0 ...] (row stride kx) rounded to tf32, + lo part.
+__global__ void split_w1_kernel(const float* __restrict__ theta, int64_t Dp, int64_t woff, int64_t boff, int n0,
+                                int64_t kx, int64_t cnt, int64_t J, float* hi, float* lo) {
+  const int64_t total = J * cnt;  // cnt = n1 * kx
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = g / cnt, r = g - j * cnt;
-    const float v = theta[j * Dp + woff + r];
+    const int64_t o = r / kx, i = r - o * kx;
+    const float* th = theta + j * Dp;
+    const float v = i < n0 ? th[woff + o * n0 + i] : (i == n0 ? th[boff + o] : 0.f);
     const float h = tf32_hi(v);
     hi[g] = h;
     if (lo) lo[g] = v - h;
   }
 }
 
-__global__ void fill_ones_row_kernel(float* buf, int64_t J, int64_t rows, int64_t row, int64_t ldm, float v) {
-  const int64_t total = J * ldm;
+// Row `row` of a row-blocked [J][nblk][rows][128] buffer set to v (a1^T's ones row -> db2).
+__global__ void fill_ones_row_kernel(float* buf, int64_t J, int64_t rows, int64_t row, int64_t mcap, float v) {
+  const int64_t total = J * mcap;
+  const int64_t nblk = mcap / 128;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = g / ldm, m = g - j * ldm;
-    buf[(j * rows + row) * ldm + m] = v;
+    const int64_t jb = g / 128, r = g - jb * 128;  // jb = j * nblk + block
+    buf[(jb * rows + row) * 128 + r] = v;
+    (void)nblk;
   }
 }
 
@@ -1305,14 +998,22 @@ CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uin
   return m;
 }
 
-// Store map of a transposed activation buffer [J][rows_alloc][ld]: valid extent
-// {M, rows} (stores beyond are clipped), box = one warp's 32 rows x 16 columns.
-CUtensorMap map_store(const float* base, uint64_t M, uint64_t rows, uint64_t ld, uint64_t J, uint64_t pstride) {
-  const uint64_t dims[3] = {M, rows, J};
-  const uint64_t strides[2] = {ld * 4, pstride * 4};
-  const uint32_t box[3] = {32, 16, 1};
-  return make_map(base, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+// Row-blocked transposed buffer [J][nblk_alloc][rows][128] as a 4-D operand:
+// dims {128, rows, nblk_used, J}, box {32 (k), box_rows, 1, 1}.
+CUtensorMap map_blk(const float* base, uint64_t rows, uint64_t nblk_used, uint64_t nblk_alloc, uint64_t J,
+                    uint32_t box_rows) {
+  const uint64_t dims[4] = {128, rows, nblk_used, J};
+  const uint64_t strides[3] = {128 * 4, rows * 128 * 4, nblk_alloc * rows * 128 * 4};
+  const uint32_t box[4] = {BK, box_rows, 1, 1};
+  CUtensorMap m;
+  uint32_t es[4] = {1, 1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box,
+                                 es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError{"cuTensorMapEncodeTiled (4d) failed (" + std::to_string((int)r) + ")"};
+  return m;
 }
+
 
 CUtensorMap map2d(const float* base, uint64_t inner, uint64_t rows, uint64_t ld, uint32_t box_rows) {
   const uint64_t dims[2] = {inner, rows};
@@ -1331,27 +1032,63 @@ CUtensorMap map3d(const float* base, uint64_t inner, uint64_t rows, uint64_t ld,
 
 int round16(int v) { return (v + 15) / 16 * 16; }
 
-template <int EPI, bool SPLIT, bool A3D, int CP = 4>
+// CL >= 1: tp.rtiles counts row groups (2 QB tiles) and tp.J particle groups (QA
+// particles); B's TMA box is tp.nmma / 2 rows per CTA (tp.bbox rows per piece
+// when QB = 2; tp.brows is ignored) and the grid is launched as clusters.
+template <int EPI, bool SPLIT, bool A3D, int CP = 4, int ACT = 0, int CL = 0>
 void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUtensorMap& B, const CUtensorMap& Blo,
                TileParams tp, const FwdParams& fp, const DwParams& dp, size_t epi_smem_bytes) {
-  const uint32_t sub = SPLIT ? 2 : 1;
-  const size_t stage_bytes = sub * ((size_t)BM * BK * 4 + (size_t)tp.nmma * BK * 4);
+  using CS_ = ClusterShape<CL>;
+  const size_t sub = SPLIT ? 2 : 1;
+  const size_t b_rows = CS_::kPair ? (size_t)tp.nmma / 2 : (size_t)tp.nmma;
+  const size_t stage_bytes = sub * ((size_t)BM * BK * 4 + b_rows * BK * 4);
   const size_t fixed = 1024 + 64 * 8 + 64 + epi_smem_bytes;
   const size_t budget = 227 * 1024;
-  int stages = (int)std::min<size_t>(6, (budget - fixed) / stage_bytes);
+  int stages = (int)std::min<size_t>(8, (budget - fixed) / stage_bytes);
   if (stages < 1) throw CudaError{"tensor-core tile does not fit in shared memory"};
   tp.stages = stages;
-  tp.stage_bytes_tx = (uint32_t)(sub * ((size_t)BM * BK * 4 + (size_t)tp.brows * BK * 4));
+  if (CS_::kPair) {
+    // bytes landing in the pair per stage (two overlapping B pieces when QB = 2)
+    const size_t b_land = CS_::QB == 2 ? 2 * (size_t)tp.bbox : b_rows;
+    tp.stage_bytes_tx = (uint32_t)(2 * sub * ((size_t)BM * BK * 4 + b_land * BK * 4));
+  } else {
+    tp.stage_bytes_tx = (uint32_t)(sub * ((size_t)BM * BK * 4 + (size_t)tp.brows * BK * 4));
+  }
   const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16 + epi_smem_bytes + 64;
-  auto kern = tc_kernel<EPI, SPLIT, A3D, CP>;
+  auto kern = tc_kernel<EPI, SPLIT, A3D, CP, ACT, CL>;
   static bool attr_set = false;
+  static int max_clusters = 0;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  if (CS_::kPair) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS_::kSize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
   if (!attr_set) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget));
+    if (CS_::kPair) {
+      cfg.gridDim = dim3((unsigned)(CS_::kSize * (c.tc->num_sms / CS_::kSize)));
+      CK(cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg));
+      if (max_clusters < 1) throw CudaError{"tensor-core cluster does not fit on the device"};
+    }
     attr_set = true;
   }
   const int ntiles = tp.rtiles * tp.J;
-  const int grid = std::max(1, std::min(ntiles, c.tc->num_sms));
-  kern<<<grid, kThreads, smem, c.stream>>>(A, SPLIT ? Alo : A, B, SPLIT ? Blo : B, tp, fp, dp);
+  if (CS_::kPair) {
+    const int nclusters = std::max(1, std::min(ntiles, max_clusters));
+    cfg.gridDim = dim3((unsigned)(CS_::kSize * nclusters));
+    CK(cudaLaunchKernelEx(&cfg, kern, A, SPLIT ? Alo : A, B, SPLIT ? Blo : B, tp, fp, dp));
+  } else {
+    const int grid = std::max(1, std::min(ntiles, c.tc->num_sms));
+    kern<<<grid, kThreads, smem, c.stream>>>(A, SPLIT ? Alo : A, B, SPLIT ? Blo : B, tp, fp, dp);
+  }
   LAUNCHED();
 }
 
@@ -1369,26 +1106,25 @@ void tc_init(Ctx& c) {
   s->n1 = c.net.sizes[1];
   s->C = c.net.sizes[2];
   s->split = c.precision == DASMC_PREC_3XTF32;
-  if (const char* e = std::getenv("DASMC_TC_LAYER2")) s->tc_layer2 = e[0] != '0';
-  if (const char* e = std::getenv("DASMC_MMA_LAYER2")) s->mma_layer2 = e[0] != '0';
-  if (s->tc_layer2) s->mma_layer2 = false;
+  if (const char* e = std::getenv("DASMC_TC_CLUSTER")) s->cluster = std::max(0, std::min(4, std::atoi(e)));
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, dev));
   s->n_pad = (c.n + 31) / 32 * 32;
   const size_t xt = (size_t)(s->n0 + 1) * s->n_pad;
   CK(cudaMalloc(&s->Xt, sizeof(float) * xt));
-  const size_t w = (size_t)c.Jmax * s->n1 * s->n0;
-  CK(cudaMalloc(&s->Xhi, sizeof(float) * (size_t)c.n * s->n0));
+  s->kx = (s->n0 + 1 + 3) / 4 * 4;
+  const size_t w = (size_t)c.Jmax * s->n1 * s->kx;
+  CK(cudaMalloc(&s->Xhi, sizeof(float) * (size_t)c.n * s->kx));
   CK(cudaMalloc(&s->W1hi, sizeof(float) * w));
   if (s->split) {
     CK(cudaMalloc(&s->Xtlo, sizeof(float) * xt));
-    CK(cudaMalloc(&s->Xlo, sizeof(float) * (size_t)c.n * s->n0));
+    CK(cudaMalloc(&s->Xlo, sizeof(float) * (size_t)c.n * s->kx));
     CK(cudaMalloc(&s->W1lo, sizeof(float) * w));
   }
   dim3 grid((unsigned)((s->n_pad + 31) / 32), (unsigned)((s->n0 + 1 + 31) / 32));
-  transpose_x_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(c.X, c.n, s->n0, s->n_pad, s->Xt, s->Xtlo, s->Xhi, s->Xlo,
-                                                         s->split ? 1 : 0);
+  transpose_x_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(c.X, c.n, s->n0, s->n_pad, s->kx, s->Xt, s->Xtlo, s->Xhi,
+                                                         s->Xlo, s->split ? 1 : 0);
   LAUNCHED();
   CK(cudaStreamSynchronize(c.stream));
 }
@@ -1444,31 +1180,41 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
   // ---- fused forward: Z1 = X W1^T on tensor cores, layer 2 + loss + deltas in the epilogue
   {
     KTimer kt(c, need_grad ? 0 : -1);
-    const float* W1 = theta_in + l1.woff;
-    int64_t wstride = net.Dp;
-    {  // W1 -> tf32 (rna) hi [+ lo]: the MMA would otherwise truncate the low mantissa bits
-      const int64_t cnt = (int64_t)n1 * n0;
-      split_w1_kernel<<<(int)std::min<int64_t>((J * cnt + 255) / 256, 148 * 16), 256, 0, c.stream>>>(
-          theta_in, net.Dp, l1.woff, cnt, J, s->W1hi, s->split ? s->W1lo : nullptr);
-      LAUNCHED();
-      W1 = s->W1hi;
-      wstride = cnt;
-    }
-    const CUtensorMap A = map2d(s->Xhi, n0, M, n0, BM);
-    const CUtensorMap Alo = s->split ? map2d(s->Xlo, n0, M, n0, BM) : A;
-    const CUtensorMap B = map3d(W1, n0, n1, n0, J, wstride, n1);
-    const CUtensorMap Blo = s->split ? map3d(s->W1lo, n0, n1, n0, J, wstride, n1) : B;
+    // [W1, b1] -> tf32 (rna) hi [+ lo]: the MMA would otherwise truncate the low mantissa
+    // bits; the bias rides along as K column n0 against X's ones column
+    const int64_t kx = s->kx, cnt = (int64_t)n1 * kx;
+    split_w1_kernel<<<(int)std::min<int64_t>((J * cnt + 255) / 256, 148 * 16), 256, 0, c.stream>>>(
+        theta_in, net.Dp, l1.woff, l1.boff, n0, kx, cnt, J, s->W1hi, s->split ? s->W1lo : nullptr);
+    LAUNCHED();
+    // rows >= M of X are TMA zero fill (ones column included): z1 = 0 there
+    // cluster shape (see ClusterShape): CTA pairs stream half of W1's rows each (box
+    // nmma / 2, rows >= n1 zero fill); QA = 2 multicasts X rows (box 64 rows per CTA),
+    // QB = 2 multicasts W1 rows (two pieces of bbox rows, multiples of 8)
+    const int cl = s->split ? std::min(s->cluster, 1) : s->cluster;
+    const bool pair = cl > 0;
+    const int QA = (cl == 2 || cl == 4) ? 2 : 1, QB = (cl == 3 || cl == 4) ? 2 : 1;
+    const int half = round16(n1) / 2;
+    const int bpiece = QB == 2 ? (half / 2 + 7) / 8 * 8 : half;
+    const uint32_t bbox = pair ? (uint32_t)bpiece : (uint32_t)n1;
+    const CUtensorMap A = map2d(s->Xhi, n0 + 1, M, kx, BM / QA);
+    const CUtensorMap Alo = s->split ? map2d(s->Xlo, n0 + 1, M, kx, BM / QA) : A;
+    const CUtensorMap B = map3d(s->W1hi, n0 + 1, n1, kx, J, cnt, bbox);
+    const CUtensorMap Blo = s->split ? map3d(s->W1lo, n0 + 1, n1, kx, J, cnt, bbox) : B;
     TileParams tp{};
-    tp.rtiles = rtiles;
-    tp.J = (int)J;
-    tp.rg = 32;
-    tp.nkb = (n0 + BK - 1) / BK;
+    tp.rtiles = pair ? (rtiles + 2 * QB - 1) / (2 * QB) : rtiles;
+    tp.J = pair ? (int)((J + QA - 1) / QA) : (int)J;
+    tp.rg = pair ? 32 / (2 * QB) : 32;
+    tp.bbox = bpiece;
+    tp.hint_a = 1;  // X (shared by every particle): keep it in L2 against the activation-store stream
+    if (const char* e = std::getenv("DASMC_TC_RG")) tp.rg = std::max(1, std::atoi(e));   // tuning only
+    if (const char* e = std::getenv("DASMC_TC_HINTA")) tp.hint_a = std::atoi(e);        // tuning only
+    if (const char* e = std::getenv("DASMC_TC_HINTB")) tp.hint_b = std::atoi(e);        // tuning only
+    tp.nkb = (n0 + 1 + BK - 1) / BK;
     tp.nmma = round16(n1);
     tp.brows = n1;
     FwdParams fp{};
     fp.theta = theta_in;
     fp.Dp = net.Dp;
-    fp.boff1 = l1.boff;
     fp.woff2 = l2.woff;
     fp.boff2 = l2.boff;
     fp.n1 = n1;
@@ -1477,9 +1223,10 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     fp.y = c.y;
     fp.M = M;
     fp.P = P;
+    fp.Jn = (int)J;
     fp.beta_rows = (float)beta_rows;
     fp.need_grad = need_grad ? 1 : 0;
-    fp.ldm = ldm;
+    fp.ldm = ldm / 128;  // number of 128-row blocks allocated per particle
     fp.a1T = s->a1T;
     fp.d1T = s->d1T;
     fp.d2T = s->d2T;
@@ -1489,58 +1236,49 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     fp.ll_part = c.ll_part;
     fp.ll_slots = c.ll_slots;
     if (const char* e = std::getenv("DASMC_DEBUG_EPI")) fp.dbg = std::atoi(e);  // profiling only
-    // classes padded to a multiple of 4 (float4 rows of W2^T in shared memory)
-    const int CP = (C + 3) / 4 * 4;
-    const size_t epi_bytes =
-        sizeof(float) * ((size_t)n1 * CP + ((n1 + 3) & ~3) + CP + kParts * 128 * CP) + 8 * sizeof(double) + 16 +
-        (s->split || !kUseTmaStore ? 0 : 128 + (size_t)kEpiWarps * 4096);  // TMA-store staging
-    if (!s->split && kUseTmaStore) {
-      fp.mapS1 = map_store(s->a1T, M, n1, ldm, J, (uint64_t)(n1 + 1) * ldm);
-      fp.mapS2 = map_store(s->d1T, M, n1, ldm, J, (uint64_t)n1 * ldm);
-    }
+    // classes padded to 4, 10 or 16 (W2^T rows float4-aligned in shared memory)
+    const int CP = C <= 4 ? 4 : C <= 10 ? 10 : 16;
+    const int CS = (CP + 3) & ~3;
+    const size_t epi_bytes = sizeof(float) * (2 * ((size_t)n1 * CS + CS) + kParts * 128 * CP) + 8 * sizeof(double) + 16;
     DwParams dp{};
-    const int NP = tp.nmma;
-    if (s->mma_layer2) {
-      // layer 2 on warp-level mma.sync (split-tf32) inside the epilogue
-      const size_t mma_bytes = sizeof(float) * ((size_t)NP * 24 + NP + 16 + (size_t)kParts * 128 * 20 +
-                                                (size_t)kEpiWarps * 32 * 20) +
-                               8 * sizeof(double) + 64;
-      if (s->split)
-        launch_tc<kEpiKindFwdMma, true, false, 4>(c, A, Alo, B, Blo, tp, fp, dp, mma_bytes);
+    auto go = [&](auto cp, auto act) {
+      constexpr int K = decltype(cp)::value, A_ = decltype(act)::value;
+      if (s->split) {
+        if (pair)
+          launch_tc<kEpiKindFwd, true, false, K, A_, 1>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+        else
+          launch_tc<kEpiKindFwd, true, false, K, A_, 0>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+      } else {
+        switch (cl) {
+          case 0: launch_tc<kEpiKindFwd, false, false, K, A_, 0>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+          case 1: launch_tc<kEpiKindFwd, false, false, K, A_, 1>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+          case 2: launch_tc<kEpiKindFwd, false, false, K, A_, 2>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+          case 3: launch_tc<kEpiKindFwd, false, false, K, A_, 3>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+          default: launch_tc<kEpiKindFwd, false, false, K, A_, 4>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+        }
+      }
+    };
+    auto go_act = [&](auto cp) {
+      if (net.act == DASMC_RELU)
+        go(cp, std::integral_constant<int, DASMC_RELU>{});
       else
-        launch_tc<kEpiKindFwdMma, false, false, 4>(c, A, Alo, B, Blo, tp, fp, dp, mma_bytes);
-    } else if (s->tc_layer2 && NP + 32 <= 256) {
-      // layer 2 on the tensor core (A1 / delta2 as TMEM A operands)
-      const size_t tc_bytes = 1024 + (size_t)((NP + 31) / 32) * 2048 + (size_t)NP * 128 + (size_t)NP * 4 + 64 +
-                              8 * sizeof(double) + 16;
-      if (s->split)
-        launch_tc<kEpiKindFwdTc, true, false, 4>(c, A, Alo, B, Blo, tp, fp, dp, tc_bytes);
-      else
-        launch_tc<kEpiKindFwdTc, false, false, 4>(c, A, Alo, B, Blo, tp, fp, dp, tc_bytes);
-    } else {
-    auto go = [&](auto cp) {
-      constexpr int K = decltype(cp)::value;
-      if (s->split)
-        launch_tc<kEpiKindFwd, true, false, K>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
-      else
-        launch_tc<kEpiKindFwd, false, false, K>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+        go(cp, std::integral_constant<int, DASMC_TANH>{});
     };
     switch (CP) {
-      case 4: go(std::integral_constant<int, 4>{}); break;
-      case 8: go(std::integral_constant<int, 8>{}); break;
-      case 12: go(std::integral_constant<int, 12>{}); break;
-      default: go(std::integral_constant<int, 16>{}); break;
-    }
+      case 4: go_act(std::integral_constant<int, 4>{}); break;
+      case 10: go_act(std::integral_constant<int, 10>{}); break;
+      default: go_act(std::integral_constant<int, 16>{}); break;
     }
   }
   if (!need_grad) return;
   FwdParams fp0{};
   // ---- layer 2: dW2^T[o, c] = sum_m a1^T[o, m] delta2^T[c, m]  (ones row o = n1 -> db2)
   {
-    const CUtensorMap A = map3d(s->a1T, M, n1 + 1, ldm, J, (uint64_t)(n1 + 1) * ldm, BM);
-    const CUtensorMap Alo = s->split ? map3d(s->a1Tlo, M, n1 + 1, ldm, J, (uint64_t)(n1 + 1) * ldm, BM) : A;
-    const CUtensorMap B = map3d(s->d2T, M, C, ldm, J, (uint64_t)C * ldm, C);
-    const CUtensorMap Blo = s->split ? map3d(s->d2Tlo, M, C, ldm, J, (uint64_t)C * ldm, C) : B;
+    const uint64_t nbu = (uint64_t)(M + 127) / 128, nba = (uint64_t)ldm / 128;
+    const CUtensorMap A = map_blk(s->a1T, n1 + 1, nbu, nba, J, BM);
+    const CUtensorMap Alo = s->split ? map_blk(s->a1Tlo, n1 + 1, nbu, nba, J, BM) : A;
+    const CUtensorMap B = map_blk(s->d2T, C, nbu, nba, J, C);
+    const CUtensorMap Blo = s->split ? map_blk(s->d2Tlo, C, nbu, nba, J, C) : B;
     TileParams tp{};
     tp.rtiles = (n1 + 1 + BM - 1) / BM;
     tp.J = (int)J;
@@ -1559,8 +1297,9 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     KTimer kt(c, 1);
     const CUtensorMap A = map2d(s->Xt, M, n0 + 1, s->n_pad, BM);
     const CUtensorMap Alo = s->split ? map2d(s->Xtlo, M, n0 + 1, s->n_pad, BM) : A;
-    const CUtensorMap B = map3d(s->d1T, M, n1, ldm, J, (uint64_t)n1 * ldm, n1);
-    const CUtensorMap Blo = s->split ? map3d(s->d1Tlo, M, n1, ldm, J, (uint64_t)n1 * ldm, n1) : B;
+    const uint64_t nbu = (uint64_t)(M + 127) / 128, nba = (uint64_t)ldm / 128;
+    const CUtensorMap B = map_blk(s->d1T, n1, nbu, nba, J, n1);
+    const CUtensorMap Blo = s->split ? map_blk(s->d1Tlo, n1, nbu, nba, J, n1) : B;
     TileParams tp{};
     tp.rtiles = (n0 + 1 + BM - 1) / BM;
     tp.J = (int)J;

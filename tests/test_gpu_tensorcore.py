@@ -92,3 +92,23 @@ def test_tc_run_matches_fp32_schedule(product):
     r3x = product.run_experiment(spec, X, y, cfg, precision="3xtf32")["records"]
     assert [r["batch"] for r in r32] == [r["batch"] for r in r3x]
     np.testing.assert_allclose(r3x[0]["mean_log_target"], r32[0]["mean_log_target"], rtol=1e-5)
+
+
+@pytest.mark.parametrize("cluster", [0, 1, 2, 3, 4])
+def test_tc_cluster_shapes(product, oracle, cluster, monkeypatch):
+    """Every fused-forward cluster shape (single CTAs, CTA pairs, pairs with X or W1
+    multicast, both) gives the same gradients; odd J and M leave padding tiles."""
+    monkeypatch.setenv("DASMC_TC_CLUSTER", str(cluster))
+    layers, act = [784, 200, 10], "relu"
+    n, M, J = 1200, 1100, 5
+    spec, X, y = problem(product, layers, act, n)
+    D = product.param_count(spec)
+    th = (0.5 * np.random.default_rng(7).standard_normal((J, D))).astype(np.float32).astype(np.float64)
+    t = product.GpuEnsembleTarget(spec, X, y, J, precision="tf32")
+    t.set_target(0, M, n, "scaled", 1.0, 1.0)
+    v, g = t.log_target_with_grad(th)
+    vo, go = oracle.value_and_grad(layers, 0, X.astype(np.float64), y, (0, M, n), 0, 1.0, 1.0, th)
+    assert float(np.max(np.abs(v - vo) / np.abs(vo))) < 2e-4
+    for j in range(J):
+        mr, nr = errs(g[j], go[j])
+        assert nr < 6e-3 and mr < 0.5, (cluster, j, mr, nr)
