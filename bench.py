@@ -292,9 +292,11 @@ def run_ours(args, w):
         peak = 148 * 128 * 2 * 1.965e9 / 1e12
         peak_src = "nominal fp32 CUDA-core FMA peak (148 SMs x 128 lanes x 2 x 1965 MHz); not in MEASURED_PEAKS.json"
     else:
-        bf16 = peaks.get("bf16_tflops", 1590.0)
+        # the kernel is timed inside a long step: the sustained bf16 figure applies
+        bf16 = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops", 1590.0)
+        kind = "sustained" if peaks.get("bf16_tflops_sustained") else "burst"
         peak = bf16 / 2.0
-        peak_src = f"dense tf32 = measured bf16 burst {bf16} TFLOP/s / 2 (MEASURED_PEAKS.json)"
+        peak_src = f"dense tf32 = measured bf16 {kind} {bf16} TFLOP/s / 2 (MEASURED_PEAKS.json)"
     achieved = fl / (kt_ms / 1e3) / 1e12 if kt_ms > 0 else None
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")

@@ -140,6 +140,14 @@ __device__ __forceinline__ void tma2_3d(void* dst, const CUtensorMap* map, uint3
       "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
       : "memory");
 }
+// L2 prefetch of a TMA box (no shared-memory destination, no completion)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 // L2 eviction-priority policies for TMA loads (0 normal, 1 evict_last, 2 evict_first)
 __device__ __forceinline__ uint64_t l2_policy(int kind) {
   uint64_t p;
@@ -310,6 +318,7 @@ struct TileParams {
   uint32_t stage_bytes_tx;
   int bbox;    // clusters with QB = 2: B rows per multicast piece (pieces at 0 and half - bbox)
   int hint_a, hint_b;  // L2 policies of the A / B loads (pairs): 0 normal, 1 evict_last, 2 evict_first
+  int prefetch;        // pairs: L2-prefetch the next unit's A / B boxes
 };
 
 struct FwdParams {
@@ -463,7 +472,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         tile_coords(tp, t, ru, j);
         const int rt = PAIR ? 2 * (QB * ru + qb) + (int)prank : ru;
         if (PAIR) j = QA * j + qa;
+        // warm L2 with the next unit's operands while this unit streams (pairs, no multicast)
+        int pf_rt = -1, pf_j = 0;
+        if (PAIR && QA == 1 && QB == 1 && tp.prefetch && t + ustride < ntiles) {
+          int pru;
+          tile_coords(tp, t + ustride, pru, pf_j);
+          pf_rt = 2 * pru + (int)prank;
+        }
         for (int kb = 0; kb < tp.nkb; ++kb) {
+          if (pf_rt >= 0) {
+            tma_prefetch_2d(&mapA, kb * BK, pf_rt * BM);
+            tma_prefetch_3d(&mapB, kb * BK, (int)(prank * b_rows), pf_j);
+          }
           mbar_wait(&empty[s], ph ^ 1);
           const int k0 = kb * BK;
           if (PAIR) {
@@ -1209,6 +1229,7 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     if (const char* e = std::getenv("DASMC_TC_RG")) tp.rg = std::max(1, std::atoi(e));   // tuning only
     if (const char* e = std::getenv("DASMC_TC_HINTA")) tp.hint_a = std::atoi(e);        // tuning only
     if (const char* e = std::getenv("DASMC_TC_HINTB")) tp.hint_b = std::atoi(e);        // tuning only
+    if (const char* e = std::getenv("DASMC_TC_PREFETCH")) tp.prefetch = std::atoi(e);   // tuning only
     tp.nkb = (n0 + 1 + BK - 1) / BK;
     tp.nmma = round16(n1);
     tp.brows = n1;
