@@ -324,7 +324,15 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
   CK(cudaMemset(c.p, 0, sizeof(float) * pe));
   dmalloc(c.logw, (size_t)Jmax);
   c.th_slots = (int)((c.net.Dp + 8191) / 8192);
-  const int64_t nch_rng = (c.net.D + kRngChunkNormals - 1) / kRngChunkNormals;
+  // RNG chunk = one column of the widest layer (the reference's column-major W order
+  // walks a column's rows consecutively; internally those are `in` floats apart, so
+  // threads owning consecutive columns store coalesced); small nets keep 1024
+  {
+    int64_t widest = 0;
+    for (int l = 1; l <= c.net.L; ++l) widest = std::max<int64_t>(widest, c.net.sizes[l]);
+    c.rng_chunk = widest >= 128 ? widest : kRngChunkNormals;
+  }
+  const int64_t nch_rng = (c.net.D + c.rng_chunk - 1) / c.rng_chunk;
   c.rng_slots = (int)nch_rng;
   dmalloc(c.th_part, (size_t)Jmax * c.th_slots);
   dmalloc(c.p_part, (size_t)Jmax * c.th_slots);
@@ -347,9 +355,9 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
     CK(cudaMemcpy(c.iota, io.data(), sizeof(int32_t) * Jmax, cudaMemcpyHostToDevice));
   }
   CK(cudaMallocHost(reinterpret_cast<void**>(&c.h_records), sizeof(double) * kRecRing * 8));
-  const int64_t nch_uni = (Jmax + 2 * kRngChunkNormals - 1) / (2 * kRngChunkNormals);
+  const int64_t nch_uni = (Jmax + 2 * c.rng_chunk - 1) / (2 * c.rng_chunk);
   c.jump_chunks = std::max(nch_rng, nch_uni) + 1;
-  const auto tab = jump_table(2 * kRngChunkNormals, c.jump_chunks);
+  const auto tab = jump_table(2 * (uint64_t)c.rng_chunk, c.jump_chunks);
   dmalloc(c.jump_tab, (size_t)c.jump_chunks * 4);
   CK(cudaMemcpy(c.jump_tab, tab.data(), sizeof(uint64_t) * 4 * tab.size(), cudaMemcpyHostToDevice));
   if (precision != DASMC_PREC_FP32) {
@@ -785,12 +793,12 @@ int dasmc_gpu_shard_resample(dasmc_ctx* ctx, const double* log_w_full_dev, const
       dmalloc(c.sh_idx, (size_t)J_total);
       c.sh_cap = J_total;
     }
-    const int64_t need = (J_total + 2 * kRngChunkNormals - 1) / (2 * kRngChunkNormals) + 1;
+    const int64_t need = (J_total + 2 * c.rng_chunk - 1) / (2 * c.rng_chunk) + 1;
     if (need > c.jump_chunks) {
       CK(cudaStreamSynchronize(c.stream));
       CK(cudaFree(c.jump_tab));
       c.jump_tab = nullptr;
-      const auto tab = jump_table(2 * kRngChunkNormals, need);
+      const auto tab = jump_table(2 * (uint64_t)c.rng_chunk, need);
       dmalloc(c.jump_tab, (size_t)need * 4);
       CK(cudaMemcpy(c.jump_tab, tab.data(), sizeof(uint64_t) * 4 * tab.size(), cudaMemcpyHostToDevice));
       c.jump_chunks = need;

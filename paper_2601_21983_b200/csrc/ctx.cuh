@@ -142,6 +142,7 @@ struct Ctx {
   int rec_head = 0;            // number of queued records
   uint64_t* jump_tab = nullptr;  // [nchunks][4]
   int64_t jump_chunks = 0;
+  int64_t rng_chunk = 1024;  // normals per RNG thread (set in create_ctx)
 
   // staging
   void* stage = nullptr;

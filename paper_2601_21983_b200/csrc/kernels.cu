@@ -381,13 +381,14 @@ __global__ void eval_finalize_kernel(int64_t J, const double* __restrict__ ll_pa
 }
 
 // ---- parallel xoshiro256++ normals ------------------------------------------------------------
-// Thread (j, c) draws the c-th chunk of kRngChunkNormals normals of stream
-// fork(a, b, c') by jumping c*2*kRngChunkNormals steps ahead (F2-linear jump
-// with host-precomputed polynomials).  Box-Muller in fp64 exactly as
-// rng.hpp:76-81; the value is stored in fp32 at its internal position.
+// Thread (j, c) draws the c-th chunk of `chunk` normals of stream fork(a, b, c')
+// by jumping c*2*chunk steps ahead (F2-linear jump with host-precomputed
+// polynomials).  Box-Muller in fp64 exactly as rng.hpp:76-81; the value is
+// stored in fp32 at its internal position.  With chunk = a layer's fan-out a
+// chunk is one column of W, so a warp's stores are coalesced.
 __global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b, int per_particle_c,
-                               int64_t J, int64_t nchunks, const uint64_t* __restrict__ jump_tab, float scale,
-                               float* __restrict__ dst, double* __restrict__ sq_part, int64_t j_offset) {
+                               int64_t J, int64_t nchunks, int64_t chunk, const uint64_t* __restrict__ jump_tab,
+                               float scale, float* __restrict__ dst, double* __restrict__ sq_part, int64_t j_offset) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= J * nchunks) return;
   const int64_t j = g / nchunks, c = g - j * nchunks;
@@ -397,7 +398,7 @@ __global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b
   Xoshiro x;
   x.seed(key);
   if (c > 0) x.jump(jump_tab + 4 * c);
-  const int64_t lo = c * kRngChunkNormals, hi = min(net.D, lo + kRngChunkNormals);
+  const int64_t lo = c * chunk, hi = min(net.D, lo + chunk);
   double sq = 0.0;
   float* out = dst + j * net.Dp;
   // reference index i -> internal offset, walked incrementally (one division per chunk):
@@ -432,10 +433,10 @@ __global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b
 }
 
 // `count` uniforms of one stream (resampling), chunked with the same jumps
-// (a chunk of kRngChunkNormals normals = 2*kRngChunkNormals draws).
-__global__ void uniforms_kernel(uint64_t key, int64_t count, const uint64_t* __restrict__ jump_tab,
+// (a chunk of `chunk` normals = 2*chunk draws).
+__global__ void uniforms_kernel(uint64_t key, int64_t count, int64_t chunk, const uint64_t* __restrict__ jump_tab,
                                 double* __restrict__ dst) {
-  const int64_t per = 2 * kRngChunkNormals;
+  const int64_t per = 2 * chunk;
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c * per >= count) return;
   Xoshiro x;
@@ -744,19 +745,19 @@ void launch_eval_finalize(Ctx& c, int64_t J, double* values_out, double* pre_out
 
 void launch_normals(Ctx& c, uint64_t root, uint64_t a, uint64_t b, int64_t J, float scale, float* dst,
                     double* sq_part, int64_t j_offset) {
-  const int64_t nch = (c.net.D + kRngChunkNormals - 1) / kRngChunkNormals;
+  const int64_t nch = (c.net.D + c.rng_chunk - 1) / c.rng_chunk;
   const int per_particle_c = a == tag::kProposal ? 1 : 0;
   const int64_t total = J * nch;
   normals_kernel<<<(unsigned)((total + 127) / 128), 128, 0, c.stream>>>(
-      c.net, root, a, b, per_particle_c, J, nch, c.jump_tab, scale, dst, sq_part, j_offset);
+      c.net, root, a, b, per_particle_c, J, nch, c.rng_chunk, c.jump_tab, scale, dst, sq_part, j_offset);
   LAUNCHED();
 }
 
 void launch_uniforms(Ctx& c, uint64_t key, int64_t count, double* dst) {
-  const int64_t per = 2 * kRngChunkNormals;
+  const int64_t per = 2 * c.rng_chunk;
   const int64_t nch = (count + per - 1) / per;
   if (nch > c.jump_chunks) throw std::invalid_argument("uniforms: jump table too small");
-  uniforms_kernel<<<(unsigned)((nch + 63) / 64), 64, 0, c.stream>>>(key, count, c.jump_tab, dst);
+  uniforms_kernel<<<(unsigned)((nch + 63) / 64), 64, 0, c.stream>>>(key, count, c.rng_chunk, c.jump_tab, dst);
   LAUNCHED();
 }
 
