@@ -64,11 +64,20 @@ extern "C" {
 
 typedef struct dasmc_ctx dasmc_ctx;
 
-/* NetSpec (network.hpp:24-27). */
+/* NetSpec (network.hpp:24-27).
+ * [EXT] conv != NULL describes a CNN front (BASELINE.json configs[2..3]; the
+ * reference is MLP-only): {in_c, in_h, in_w, nconv, (k, cout, pool) x nconv}.
+ * Each stage is a valid stride-1 convolution (theta block W[cout][cin][k][k]
+ * row-major, then b[cout]), the activation, and an optional 2x2/2 max-pool.
+ * The last stage output is flattened in (c, y, x) order into the MLP given by
+ * layer_sizes, whose layer_sizes[0] must be the flatten size.  theta = conv
+ * blocks in order, then the MLP in the reference layout.  X rows are images
+ * [c][h][w]. */
 typedef struct {
   int num_layers;         /* entries in layer_sizes, >= 2 */
   const int* layer_sizes; /* {input, hidden..., classes} */
   int activation;         /* DASMC_RELU | DASMC_TANH */
+  const int* conv;        /* NULL for an MLP */
 } dasmc_net_desc;
 
 /* KernelConfig (kernels.hpp:26-49). */

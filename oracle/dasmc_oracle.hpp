@@ -352,8 +352,10 @@ inline double loglik_batch(const NetSpec& s, const double* theta, const double* 
 
 // loglik_and_grad_batch (network.hpp:145-219).  grad has param_count entries
 // in the reference theta layout; returns the summed log-likelihood.
+// [EXT] dX (optional, [m x n0]): the gradient with respect to the inputs,
+// delta_1 W_1 (no activation derivative), used by the CNN head.
 inline double loglik_and_grad_batch(const NetSpec& s, const double* theta, const double* X,
-                                    const int* y, int64_t m, double* grad) {
+                                    const int* y, int64_t m, double* grad, double* dX = nullptr) {
   if (m < 1) throw std::invalid_argument("loglik_and_grad_batch: empty batch");
   const size_t L = s.layer_sizes.size();
   const int C = s.layer_sizes.back();
@@ -416,6 +418,8 @@ inline double loglik_and_grad_batch(const NetSpec& s, const double* theta, const
         for (size_t i = 0; i < next.size(); ++i) next[i] *= (1.0 - a[i] * a[i]);
       }
       delta = std::move(next);
+    } else if (dX != nullptr) {
+      gemm(false, true, (int)m, in, out, 1.0, delta.data(), out, theta + offs[(size_t)l], out, 0.0, dX, in);
     }
   }
   return total;
@@ -632,15 +636,270 @@ inline Dataset make_teacher_dataset(const NetSpec& teacher, int64_t n, int featu
   return d;
 }
 
+// ---------------------------------------------------------------- [EXT] CNN models
+// BASELINE.json configs[2..3].  The reference is MLP-only
+// (network.hpp:21-27), so these layers are new and parity here is pinned by
+// finite differences / naive loops / torch fp64 autograd (tests/), not by the
+// reference.  Semantics (stated in DESIGN.md):
+//   * a conv stage is a valid 2-D convolution, stride 1, W[cout][cin][k][k]
+//     row-major then b[cout]; the network activation follows every convolution;
+//     an optional 2x2 / stride-2 max-pool follows (floor for odd sizes) whose
+//     backward routes to the FIRST maximum of the window in (dy, dx) order;
+//   * images are [c][h][w] (w fastest); the last stage output is flattened in
+//     that order and fed to a reference MLP (`head`, network.hpp) whose input
+//     size is the flatten size;
+//   * theta = the conv stages in order, then the head in the reference layout.
+struct ConvSpec {
+  int k = 3, cout = 1;
+  bool pool = false;
+};
+struct CnnSpec {
+  int in_c = 1, in_h = 1, in_w = 1;
+  std::vector<ConvSpec> convs;
+  NetSpec head;
+};
+struct ConvDims {
+  int cin, hin, win, k, cout, ho, wo, sh, sw;  // sh x sw = stage output (after the pool)
+  bool pool;
+  int64_t woff, boff;  // offsets in theta
+};
+
+inline std::vector<ConvDims> conv_dims(const CnnSpec& s) {
+  std::vector<ConvDims> out;
+  int c = s.in_c, h = s.in_h, w = s.in_w;
+  int64_t off = 0;
+  for (const ConvSpec& cs : s.convs) {
+    ConvDims d;
+    d.cin = c;
+    d.hin = h;
+    d.win = w;
+    d.k = cs.k;
+    d.cout = cs.cout;
+    d.ho = h - cs.k + 1;
+    d.wo = w - cs.k + 1;
+    d.pool = cs.pool;
+    d.sh = cs.pool ? d.ho / 2 : d.ho;
+    d.sw = cs.pool ? d.wo / 2 : d.wo;
+    if (cs.k < 1 || cs.cout < 1 || d.ho < 1 || d.wo < 1 || d.sh < 1 || d.sw < 1)
+      throw std::invalid_argument("CnnSpec: convolution does not fit its input");
+    d.woff = off;
+    off += (int64_t)cs.cout * c * cs.k * cs.k;
+    d.boff = off;
+    off += cs.cout;
+    out.push_back(d);
+    c = cs.cout;
+    h = d.sh;
+    w = d.sw;
+  }
+  return out;
+}
+inline int64_t cnn_conv_params(const CnnSpec& s) {
+  const auto d = conv_dims(s);
+  return d.back().boff + d.back().cout;
+}
+inline int64_t flatten_size(const CnnSpec& s) {
+  const auto d = conv_dims(s);
+  return (int64_t)d.back().cout * d.back().sh * d.back().sw;
+}
+inline void validate(const CnnSpec& s) {
+  if (s.in_c < 1 || s.in_h < 1 || s.in_w < 1) throw std::invalid_argument("CnnSpec: bad input shape");
+  if (s.convs.empty()) throw std::invalid_argument("CnnSpec: need at least one convolution");
+  validate(s.head);
+  if (s.head.layer_sizes[0] != flatten_size(s))
+    throw std::invalid_argument("CnnSpec: head input size must equal the flatten size");
+}
+inline int cnn_param_count(const CnnSpec& s) {
+  validate(s);
+  return (int)(cnn_conv_params(s) + param_count(s.head));
+}
+
+inline double act_of(double z, Activation a) { return a == Activation::kRelu ? (z > 0.0 ? z : 0.0) : std::tanh(z); }
+inline double act_grad_from_post(double a, Activation act) {  // network.hpp:211-214 convention
+  return act == Activation::kRelu ? (a > 0.0 ? 1.0 : 0.0) : 1.0 - a * a;
+}
+
+// Conv stages of one image; acts[i] = post-activation (pre-pool) [cout][ho][wo],
+// outs[i] = stage output [cout][sh][sw] (== acts[i] without a pool).
+inline void cnn_stages(const CnnSpec& s, const std::vector<ConvDims>& dims, const double* theta, const double* x,
+                       std::vector<Vec>& acts, std::vector<Vec>& outs) {
+  acts.resize(dims.size());
+  outs.resize(dims.size());
+  const double* in = x;
+  for (size_t i = 0; i < dims.size(); ++i) {
+    const ConvDims& d = dims[i];
+    Vec& A = acts[i];
+    A.assign((size_t)d.cout * d.ho * d.wo, 0.0);
+    for (int co = 0; co < d.cout; ++co)
+      for (int y = 0; y < d.ho; ++y)
+        for (int xx = 0; xx < d.wo; ++xx) {
+          double acc = 0.0;
+          for (int ci = 0; ci < d.cin; ++ci)
+            for (int ky = 0; ky < d.k; ++ky)
+              for (int kx = 0; kx < d.k; ++kx)
+                acc += theta[d.woff + (((int64_t)co * d.cin + ci) * d.k + ky) * d.k + kx] *
+                       in[((size_t)ci * d.hin + y + ky) * d.win + xx + kx];
+          acc += theta[d.boff + co];
+          A[((size_t)co * d.ho + y) * d.wo + xx] = act_of(acc, s.head.activation);
+        }
+    if (d.pool) {
+      Vec& P = outs[i];
+      P.assign((size_t)d.cout * d.sh * d.sw, 0.0);
+      for (int co = 0; co < d.cout; ++co)
+        for (int y = 0; y < d.sh; ++y)
+          for (int xx = 0; xx < d.sw; ++xx) {
+            double mx = A[((size_t)co * d.ho + 2 * y) * d.wo + 2 * xx];
+            for (int dy = 0; dy < 2; ++dy)
+              for (int dx = 0; dx < 2; ++dx) mx = std::max(mx, A[((size_t)co * d.ho + 2 * y + dy) * d.wo + 2 * xx + dx]);
+            P[((size_t)co * d.sh + y) * d.sw + xx] = mx;
+          }
+    } else {
+      outs[i] = A;
+    }
+    in = outs[i].data();
+  }
+}
+
+// Backward through the conv stages of one image given dflat = d ll / d(flatten);
+// accumulates into grad (conv block of theta).
+inline void cnn_stages_backward(const CnnSpec& s, const std::vector<ConvDims>& dims, const double* theta,
+                                const double* x, const std::vector<Vec>& acts, const std::vector<Vec>& outs,
+                                const double* dflat, double* grad) {
+  Vec dout(dflat, dflat + outs.back().size());
+  for (int i = (int)dims.size() - 1; i >= 0; --i) {
+    const ConvDims& d = dims[(size_t)i];
+    const Vec& A = acts[(size_t)i];
+    Vec dz(A.size(), 0.0);
+    if (d.pool) {
+      for (int co = 0; co < d.cout; ++co)
+        for (int y = 0; y < d.sh; ++y)
+          for (int xx = 0; xx < d.sw; ++xx) {
+            int by = 0, bx = 0;
+            double mx = A[((size_t)co * d.ho + 2 * y) * d.wo + 2 * xx];
+            for (int dy = 0; dy < 2; ++dy)
+              for (int dx = 0; dx < 2; ++dx) {
+                const double v = A[((size_t)co * d.ho + 2 * y + dy) * d.wo + 2 * xx + dx];
+                if (v > mx) {
+                  mx = v;
+                  by = dy;
+                  bx = dx;
+                }
+              }
+            dz[((size_t)co * d.ho + 2 * y + by) * d.wo + 2 * xx + bx] = dout[((size_t)co * d.sh + y) * d.sw + xx];
+          }
+    } else {
+      dz = dout;
+    }
+    for (size_t t = 0; t < dz.size(); ++t) dz[t] *= act_grad_from_post(A[t], s.head.activation);
+    const double* in = i == 0 ? x : outs[(size_t)i - 1].data();
+    for (int co = 0; co < d.cout; ++co) {
+      double gb = 0.0;
+      for (int y = 0; y < d.ho; ++y)
+        for (int xx = 0; xx < d.wo; ++xx) gb += dz[((size_t)co * d.ho + y) * d.wo + xx];
+      grad[d.boff + co] += gb;
+      for (int ci = 0; ci < d.cin; ++ci)
+        for (int ky = 0; ky < d.k; ++ky)
+          for (int kx = 0; kx < d.k; ++kx) {
+            double g = 0.0;
+            for (int y = 0; y < d.ho; ++y)
+              for (int xx = 0; xx < d.wo; ++xx)
+                g += dz[((size_t)co * d.ho + y) * d.wo + xx] * in[((size_t)ci * d.hin + y + ky) * d.win + xx + kx];
+            grad[d.woff + (((int64_t)co * d.cin + ci) * d.k + ky) * d.k + kx] += g;
+          }
+    }
+    if (i > 0) {
+      Vec din((size_t)d.cin * d.hin * d.win, 0.0);
+      for (int ci = 0; ci < d.cin; ++ci)
+        for (int y = 0; y < d.hin; ++y)
+          for (int xx = 0; xx < d.win; ++xx) {
+            double acc = 0.0;
+            for (int co = 0; co < d.cout; ++co)
+              for (int ky = 0; ky < d.k; ++ky)
+                for (int kx = 0; kx < d.k; ++kx) {
+                  const int oy = y - ky, ox = xx - kx;
+                  if (oy < 0 || ox < 0 || oy >= d.ho || ox >= d.wo) continue;
+                  acc += dz[((size_t)co * d.ho + oy) * d.wo + ox] *
+                         theta[d.woff + (((int64_t)co * d.cin + ci) * d.k + ky) * d.k + kx];
+                }
+            din[((size_t)ci * d.hin + y) * d.win + xx] = acc;
+          }
+      dout.swap(din);
+    }
+  }
+}
+
+inline Vec cnn_flatten_batch(const CnnSpec& s, const double* theta, const double* X, int64_t m) {
+  const auto dims = conv_dims(s);
+  const int64_t in_sz = (int64_t)s.in_c * s.in_h * s.in_w, F = flatten_size(s);
+  Vec flat((size_t)(m * F));
+  std::vector<Vec> acts, outs;
+  for (int64_t i = 0; i < m; ++i) {
+    cnn_stages(s, dims, theta, X + i * in_sz, acts, outs);
+    std::copy(outs.back().begin(), outs.back().end(), flat.begin() + i * F);
+  }
+  return flat;
+}
+
+inline double cnn_loglik_batch(const CnnSpec& s, const double* theta, const double* X, const int* y, int64_t m) {
+  const Vec flat = cnn_flatten_batch(s, theta, X, m);
+  return loglik_batch(s.head, theta + cnn_conv_params(s), flat.data(), y, m);
+}
+
+inline double cnn_loglik_and_grad_batch(const CnnSpec& s, const double* theta, const double* X, const int* y,
+                                        int64_t m, double* grad) {
+  if (m < 1) throw std::invalid_argument("cnn_loglik_and_grad_batch: empty batch");
+  const auto dims = conv_dims(s);
+  const int64_t in_sz = (int64_t)s.in_c * s.in_h * s.in_w, F = flatten_size(s), Pc = cnn_conv_params(s);
+  const Vec flat = cnn_flatten_batch(s, theta, X, m);
+  Vec dflat((size_t)(m * F));
+  const double ll = loglik_and_grad_batch(s.head, theta + Pc, flat.data(), y, m, grad + Pc, dflat.data());
+  for (int64_t t = 0; t < Pc; ++t) grad[t] = 0.0;
+  std::vector<Vec> acts, outs;
+  for (int64_t i = 0; i < m; ++i) {
+    cnn_stages(s, dims, theta, X + i * in_sz, acts, outs);
+    cnn_stages_backward(s, dims, theta, X + i * in_sz, acts, outs, dflat.data() + i * F, grad);
+  }
+  return ll;
+}
+
+inline Dataset make_teacher_dataset(const CnnSpec& teacher, int64_t n, int feature_kind, std::uint64_t seed,
+                                    std::uint64_t cfg_id, int threads = 1) {
+  validate(teacher);
+  Dataset d;
+  d.n = n;
+  d.d = teacher.in_c * teacher.in_h * teacher.in_w;
+  d.num_classes = teacher.head.layer_sizes.back();
+  d.features.resize((size_t)n * d.d);
+  d.labels.resize((size_t)n);
+  RngStream fx = RngStream(seed).fork(tag::kSynthetic, cfg_id, 1);
+  for (auto& v : d.features) v = feature_kind == 0 ? fx.uniform() : (double)fx.uniform_below(256) / 255.0;
+  RngStream ft = RngStream(seed).fork(tag::kSynthetic, cfg_id, 2);
+  const Vec th = ft.normal_vector(cnn_param_count(teacher));
+  const auto dims = conv_dims(teacher);
+  const int64_t Pc = cnn_conv_params(teacher);
+  parallel_for(n, threads, [&](int64_t i) {
+    std::vector<Vec> acts, outs;
+    cnn_stages(teacher, dims, th.data(), d.row(i), acts, outs);
+    const Vec z = teacher_logits_row(teacher.head, th.data() + Pc, outs.back().data());
+    int best = 0;
+    for (int c = 1; c < (int)z.size(); ++c)
+      if (z[(size_t)c] > z[(size_t)best]) best = c;
+    d.labels[(size_t)i] = best;
+  });
+  d.perm.resize((size_t)n);
+  for (int64_t i = 0; i < n; ++i) d.perm[(size_t)i] = i;
+  return d;
+}
+
 // ---------------------------------------------------------------- target.hpp
 struct LinearGaussianSpec {  // target.hpp:19-22
   int dim = 1;
   double noise_std = 1.0;
 };
-using ModelSpec = std::variant<NetSpec, LinearGaussianSpec>;
+using ModelSpec = std::variant<NetSpec, LinearGaussianSpec, CnnSpec>;  // CnnSpec: [EXT]
 
 inline int model_param_count(const ModelSpec& m) {  // target.hpp:26-29
   if (const auto* net = std::get_if<NetSpec>(&m)) return param_count(*net);
+  if (const auto* cnn = std::get_if<CnnSpec>(&m)) return cnn_param_count(*cnn);
   return std::get<LinearGaussianSpec>(m).dim;
 }
 
@@ -675,6 +934,8 @@ inline double segment_loglik(const ModelSpec& model, const Dataset& d, int64_t l
   if (hi <= lo) return 0.0;
   if (const auto* net = std::get_if<NetSpec>(&model))
     return loglik_batch(*net, theta, d.row(lo), d.labels.data() + lo, hi - lo);
+  if (const auto* cnn = std::get_if<CnnSpec>(&model))
+    return cnn_loglik_batch(*cnn, theta, d.row(lo), d.labels.data() + lo, hi - lo);
   return lingauss_loglik(std::get<LinearGaussianSpec>(model), d, lo, hi, theta, nullptr);
 }
 
@@ -687,6 +948,8 @@ inline double segment_loglik_grad(const ModelSpec& model, const Dataset& d, int6
   }
   if (const auto* net = std::get_if<NetSpec>(&model))
     return loglik_and_grad_batch(*net, theta, d.row(lo), d.labels.data() + lo, hi - lo, grad);
+  if (const auto* cnn = std::get_if<CnnSpec>(&model))
+    return cnn_loglik_and_grad_batch(*cnn, theta, d.row(lo), d.labels.data() + lo, hi - lo, grad);
   return lingauss_loglik(std::get<LinearGaussianSpec>(model), d, lo, hi, theta, grad);
 }
 

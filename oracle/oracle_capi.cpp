@@ -37,6 +37,37 @@ NetSpec net_of(const int* layers, int nl, int act) {
   return s;
 }
 
+// Model encoding of the `layers` array: an MLP is its layer sizes; a CNN
+// ([EXT], dasmc_oracle.hpp) is [-1, in_c, in_h, in_w, nconv, (k, cout, pool) x
+// nconv, head layer sizes...] with head[0] = the flatten size.
+ModelSpec model_of(const int* layers, int nl, int act) {
+  if (nl >= 1 && layers[0] == -1) {
+    if (nl < 5) throw std::invalid_argument("cnn descriptor too short");
+    CnnSpec c;
+    c.in_c = layers[1];
+    c.in_h = layers[2];
+    c.in_w = layers[3];
+    const int nconv = layers[4];
+    int p = 5;
+    for (int i = 0; i < nconv; ++i, p += 3) {
+      if (p + 2 >= nl) throw std::invalid_argument("cnn descriptor too short");
+      c.convs.push_back(ConvSpec{layers[p], layers[p + 1], layers[p + 2] != 0});
+    }
+    c.head = net_of(layers + p, nl - p, act);
+    validate(c);
+    return c;
+  }
+  return net_of(layers, nl, act);
+}
+int input_dim(const ModelSpec& m) {
+  if (const auto* c = std::get_if<CnnSpec>(&m)) return c->in_c * c->in_h * c->in_w;
+  return std::get<NetSpec>(m).layer_sizes.front();
+}
+int classes_of(const ModelSpec& m) {
+  if (const auto* c = std::get_if<CnnSpec>(&m)) return c->head.layer_sizes.back();
+  return std::get<NetSpec>(m).layer_sizes.back();
+}
+
 Dataset dataset_of(const double* X, const int* y, int64_t n, int d, int classes) {
   Dataset ds;
   ds.n = n;
@@ -116,7 +147,10 @@ int oracle_rng_uniform_below(uint64_t key, uint64_t bound, int64_t n, uint64_t* 
 int oracle_make_teacher(const int* layers, int nl, int act, int64_t n, int feature_kind, uint64_t seed,
                         uint64_t cfg_id, int threads, double* X, int* y) {
   return guarded([&] {
-    const Dataset d = make_teacher_dataset(net_of(layers, nl, act), n, feature_kind, seed, cfg_id, threads);
+    const ModelSpec m = model_of(layers, nl, act);
+    const Dataset d = std::holds_alternative<CnnSpec>(m)
+                          ? make_teacher_dataset(std::get<CnnSpec>(m), n, feature_kind, seed, cfg_id, threads)
+                          : make_teacher_dataset(std::get<NetSpec>(m), n, feature_kind, seed, cfg_id, threads);
     std::memcpy(X, d.features.data(), sizeof(double) * d.features.size());
     std::memcpy(y, d.labels.data(), sizeof(int) * d.labels.size());
   });
@@ -147,7 +181,7 @@ int oracle_shuffle_perm(uint64_t seed, int64_t n, int64_t* perm) {
 // ---- network / target ----------------------------------------------------------
 int oracle_param_count(const int* layers, int nl) {
   try {
-    return param_count(net_of(layers, nl, 0));
+    return model_param_count(model_of(layers, nl, 0));
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;
@@ -161,8 +195,8 @@ int oracle_value_and_grad(const int* layers, int nl, int act, const double* X, c
                           double sigma, const double* theta, int64_t J, int threads, double* values,
                           double* grads) {
   return guarded([&] {
-    const NetSpec net = net_of(layers, nl, act);
-    const Dataset d = dataset_of(X, y, n, layers[0], layers[nl - 1]);
+    const ModelSpec net = model_of(layers, nl, act);
+    const Dataset d = dataset_of(X, y, n, input_dim(net), classes_of(net));
     TargetContext c;
     c.data = &d;
     c.window = SubsetWindow{prefix_end, block_end, total_n};
@@ -171,7 +205,7 @@ int oracle_value_and_grad(const int* layers, int nl, int act, const double* X, c
     c.prior.sigma = sigma;
     c.model = net;
     validate(c);
-    const int64_t D = param_count(net);
+    const int64_t D = model_param_count(net);
     parallel_for(J, threads, [&](int64_t j) {
       const ValueGrad vg = log_target_with_grad(c, theta + j * D);
       values[j] = vg.value;
@@ -184,10 +218,10 @@ int oracle_loglik_parts(const int* layers, int nl, int act, const double* X, con
                         int64_t prefix_end, int64_t block_end, const double* theta, int64_t J, int threads,
                         double* prefix, double* block) {
   return guarded([&] {
-    const NetSpec net = net_of(layers, nl, act);
-    const Dataset d = dataset_of(X, y, n, layers[0], layers[nl - 1]);
+    const ModelSpec net = model_of(layers, nl, act);
+    const Dataset d = dataset_of(X, y, n, input_dim(net), classes_of(net));
     const SubsetWindow w{prefix_end, block_end, n};
-    const int64_t D = param_count(net);
+    const int64_t D = model_param_count(net);
     parallel_for(J, threads, [&](int64_t j) {
       const LoglikParts p = unscaled_loglik_parts(d, w, net, theta + j * D);
       prefix[j] = p.prefix;
@@ -214,8 +248,8 @@ int oracle_smc_step(const int* layers, int nl, int act, const double* X, const i
                     double* log_w, int* iteration, oracle_step_out* out, double* p0_out, double* ps_out,
                     double* lt_new_out, double* lt_old_out, int* divergent_out, double* w_out, int* idx_out) {
   return guarded([&] {
-    const NetSpec net = net_of(layers, nl, act);
-    const Dataset d = dataset_of(X, y, n, layers[0], layers[nl - 1]);
+    const ModelSpec net = model_of(layers, nl, act);
+    const Dataset d = dataset_of(X, y, n, input_dim(net), classes_of(net));
     TargetContext c;
     c.data = &d;
     c.window = SubsetWindow{prefix_end, block_end, total_n};
@@ -224,7 +258,7 @@ int oracle_smc_step(const int* layers, int nl, int act, const double* X, const i
     c.prior.sigma = sigma;
     c.model = net;
     validate(c);
-    const int64_t D = param_count(net);
+    const int64_t D = model_param_count(net);
     ParticleEnsemble e;
     e.dim = D;
     e.count = J;
@@ -265,8 +299,8 @@ int oracle_propose_particles(const int* layers, int nl, int act, const double* X
                              int k, const int64_t* gj, int64_t n, int threads, double* thetas, double* inc,
                              double* lt_new) {
   return guarded([&] {
-    const NetSpec net = net_of(layers, nl, act);
-    const Dataset d = dataset_of(X, y, n_data, layers[0], layers[nl - 1]);
+    const ModelSpec net = model_of(layers, nl, act);
+    const Dataset d = dataset_of(X, y, n_data, input_dim(net), classes_of(net));
     TargetContext c;
     c.data = &d;
     c.window = SubsetWindow{prefix_end, block_end, total_n};
@@ -275,7 +309,7 @@ int oracle_propose_particles(const int* layers, int nl, int act, const double* X
     c.prior.sigma = sigma;
     c.model = net;
     validate(c);
-    const int64_t D = param_count(net);
+    const int64_t D = model_param_count(net);
     KernelConfig kc{step_size, leapfrog_steps, (KernelKind)kernel_kind};
     KernelConfig::validate(kc);
     const RngStream root(seed);
@@ -300,8 +334,8 @@ int oracle_init_ensemble(const int* layers, int nl, int act, const double* X, co
                          int64_t prefix_end, int64_t block_end, int64_t total_n, int mode, double beta,
                          double sigma, uint64_t seed, int64_t J, int threads, double* thetas, double* log_w) {
   return guarded([&] {
-    const NetSpec net = net_of(layers, nl, act);
-    const Dataset d = dataset_of(X, y, n, layers[0], layers[nl - 1]);
+    const ModelSpec net = model_of(layers, nl, act);
+    const Dataset d = dataset_of(X, y, n, input_dim(net), classes_of(net));
     TargetContext c;
     c.data = &d;
     c.window = SubsetWindow{prefix_end, block_end, total_n};
@@ -403,7 +437,7 @@ int oracle_run(const int* layers, int nl, int act, const double* X, const int* y
                double* final_log_w) {
   return guarded([&] {
     RunConfig cfg;
-    cfg.model = net_of(layers, nl, act);
+    cfg.model = model_of(layers, nl, act);
     cfg.prior.sigma = sigma;
     cfg.kernel = KernelConfig{step_size, leapfrog_steps, (KernelKind)kernel_kind};
     KernelConfig::validate(cfg.kernel);
@@ -419,7 +453,7 @@ int oracle_run(const int* layers, int nl, int act, const double* X, const int* y
     cfg.resample_fraction = fraction;
     cfg.resample_kind = (ResampleKind)resample_kind;
     cfg.resample_always = resample_always != 0;
-    const Dataset d = dataset_of(X, y, n, layers[0], layers[nl - 1]);
+    const Dataset d = dataset_of(X, y, n, input_dim(cfg.model), classes_of(cfg.model));
     const RunResult r = run_loop(cfg, d);
     for (size_t i = 0; i < r.records.size(); ++i) {
       const IterRecord& a = r.records[i];

@@ -81,6 +81,21 @@ def _net(layers):
     return (C.c_int * len(layers))(*layers), len(layers)
 
 
+def cnn_layers(in_shape, convs, head):
+    """[EXT] CNN model encoding accepted wherever `layers` is: in_shape = (c, h, w),
+    convs = [(k, cout, pool), ...], head = MLP layer sizes after the flatten
+    (head[0] is the flatten size)."""
+    c, h, w = in_shape
+    out = [-1, c, h, w, len(convs)]
+    for k, co, pool in convs:
+        out += [k, co, 1 if pool else 0]
+    return out + list(head)
+
+
+def input_dim(layers):
+    return layers[1] * layers[2] * layers[3] if layers[0] == -1 else layers[0]
+
+
 def use_blas(enable=True):
     """Route the oracle's dgemms through numpy's OpenBLAS (1 thread per call)."""
     if not enable:
@@ -122,7 +137,7 @@ def param_count(layers):
 
 def make_teacher(layers, act, n, feature_kind, seed, cfg_id, threads=8):
     arr, nl = _net(layers)
-    X = np.empty((n, layers[0]))
+    X = np.empty((n, input_dim(layers)))
     y = np.empty(n, dtype=np.int32)
     _check(lib().oracle_make_teacher(arr, nl, act, C.c_int64(n), feature_kind, C.c_uint64(seed), C.c_uint64(cfg_id),
                                      threads, _dp(X), _ip(y)))

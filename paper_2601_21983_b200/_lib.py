@@ -24,7 +24,8 @@ SCHED_CONSTANT, SCHED_FULL_BATCH, SCHED_CTR, SCHED_LINEAR, SCHED_AUTOMATED, SCHE
 
 
 class NetDesc(C.Structure):
-    _fields_ = [("num_layers", C.c_int), ("layer_sizes", C.POINTER(C.c_int)), ("activation", C.c_int)]
+    _fields_ = [("num_layers", C.c_int), ("layer_sizes", C.POINTER(C.c_int)), ("activation", C.c_int),
+                ("conv", C.POINTER(C.c_int))]
 
 
 class KernelCfg(C.Structure):

@@ -37,21 +37,66 @@ def _ip(a):
 
 @dataclass
 class NetSpec:  # network.hpp:24-27
+    """layer_sizes: the MLP {input, hidden..., classes}.  [EXT] conv: a CNN front
+    ((c, h, w), [(k, cout, pool), ...]) whose flattened output feeds the MLP, so
+    layer_sizes[0] must be the flatten size (include/dasmc_gpu.h)."""
     layer_sizes: Sequence[int]
     activation: str = "relu"
+    conv: Optional[tuple] = None
+
+    def conv_array(self):
+        if self.conv is None:
+            return None
+        (c, h, w), stages = self.conv
+        v = [c, h, w, len(stages)]
+        for k, co, pool in stages:
+            v += [k, co, 1 if pool else 0]
+        return v
+
+    def input_dim(self) -> int:
+        if self.conv is None:
+            return int(self.layer_sizes[0])
+        c, h, w = self.conv[0]
+        return c * h * w
 
     def desc(self):
         arr = (C.c_int * len(self.layer_sizes))(*self.layer_sizes)
-        d = L.NetDesc(len(self.layer_sizes), arr, L.RELU if self.activation == "relu" else L.TANH)
-        d._keep = arr
+        cv = self.conv_array()
+        carr = (C.c_int * len(cv))(*cv) if cv is not None else None
+        d = L.NetDesc(len(self.layer_sizes), arr, L.RELU if self.activation == "relu" else L.TANH, carr)
+        d._keep = (arr, carr)
         return d
 
+    def oracle_layers(self):
+        """The oracle's model encoding (oracle/pyoracle.py cnn_layers) -- tests only."""
+        if self.conv is None:
+            return list(self.layer_sizes)
+        (c, h, w), stages = self.conv
+        out = [-1, c, h, w, len(stages)]
+        for k, co, pool in stages:
+            out += [k, co, 1 if pool else 0]
+        return out + list(self.layer_sizes)
 
-def param_count(spec: NetSpec) -> int:  # network.hpp:36-42
+
+def conv_param_count(spec: NetSpec) -> int:
+    if spec.conv is None:
+        return 0
+    (c, h, w), stages = spec.conv
+    total = 0
+    for k, co, pool in stages:
+        total += co * c * k * k + co
+        h, w = h - k + 1, w - k + 1
+        if pool:
+            h, w = h // 2, w // 2
+        c = co
+    return total
+
+
+def param_count(spec: NetSpec) -> int:  # network.hpp:36-42 (+ [EXT] conv blocks)
     s = list(spec.layer_sizes)
     if len(s) < 2 or min(s) < 1:
         raise ValueError("NetSpec: invalid layer sizes")
-    return sum(s[i - 1] * s[i] + s[i] for i in range(1, len(s)))
+    return conv_param_count(spec) + sum(s[i - 1] * s[i] + s[i] for i in range(1, len(s)))
 
 
 @dataclass
@@ -126,7 +171,7 @@ def sda_moments_from(prefix_nll, block_nll, log_weights) -> np.ndarray:
 
 def make_teacher_data(spec: NetSpec, n: int, feature_kind: int, seed: int, cfg_id: int, threads: int = 8):
     """[EXT] teacher-labelled synthetic data; X fp32 [n, d], y int32 [n]."""
-    X = np.empty((n, spec.layer_sizes[0]), dtype=np.float32)
+    X = np.empty((n, spec.input_dim()), dtype=np.float32)
     y = np.empty(n, dtype=np.int32)
     d = spec.desc()
     L.check(L.load().dasmc_make_teacher_data(C.byref(d), n, feature_kind, seed, cfg_id, threads, _fp(X), _ip(y)))

@@ -69,10 +69,51 @@ NetDev make_net(const dasmc_net_desc* d) {
   n.act = d->activation;
   for (int i = 0; i < d->num_layers; ++i) n.sizes[i] = d->layer_sizes[i];
   int64_t ref = 0, off = 0;
+  if (d->conv != nullptr) {  // [EXT] CNN front (dasmc_gpu.h)
+    const int* cv = d->conv;
+    n.in_c = cv[0];
+    n.in_h = cv[1];
+    n.in_w = cv[2];
+    n.nconv = cv[3];
+    if (n.in_c < 1 || n.in_h < 1 || n.in_w < 1) throw InvalidArg("CnnSpec: bad input shape");
+    if (n.nconv < 1 || n.nconv > kMaxConv) throw InvalidArg("CnnSpec: 1..6 convolution stages supported");
+    int ch = n.in_c, h = n.in_h, w = n.in_w;
+    for (int i = 0; i < n.nconv; ++i) {
+      ConvDev& c = n.conv[i];
+      c.cin = ch;
+      c.hin = h;
+      c.win = w;
+      c.k = cv[4 + 3 * i];
+      c.cout = cv[5 + 3 * i];
+      c.pool = cv[6 + 3 * i] != 0 ? 1 : 0;
+      c.ho = h - c.k + 1;
+      c.wo = w - c.k + 1;
+      c.sh = c.pool ? c.ho / 2 : c.ho;
+      c.sw = c.pool ? c.wo / 2 : c.wo;
+      if (c.k < 1 || c.cout < 1 || c.ho < 1 || c.wo < 1 || c.sh < 1 || c.sw < 1)
+        throw InvalidArg("CnnSpec: convolution does not fit its input");
+      // reference and internal layouts coincide on a conv block: W[cout][cin][k][k], b[cout]
+      LayerDev& sg = n.seg[n.nseg++];
+      sg.out = 1;
+      sg.in = c.cout * c.cin * c.k * c.k;
+      sg.nb = c.cout;
+      sg.ref_off = ref;
+      ref += (int64_t)sg.in + sg.nb;
+      c.woff = sg.woff = off;
+      off = align_up(off + sg.in, 32);
+      c.boff = sg.boff = off;
+      off = align_up(off + sg.nb, 32);
+      ch = c.cout;
+      h = c.sh;
+      w = c.sw;
+    }
+    if ((int64_t)ch * h * w != n.sizes[0]) throw InvalidArg("CnnSpec: head input size must equal the flatten size");
+  }
   for (int l = 0; l < n.L; ++l) {
     LayerDev& ly = n.layer[l];
     ly.in = n.sizes[l];
     ly.out = n.sizes[l + 1];
+    ly.nb = ly.out;
     ly.ref_off = ref;
     ref += (int64_t)ly.in * ly.out + ly.out;
     ly.woff = off;
@@ -80,11 +121,15 @@ NetDev make_net(const dasmc_net_desc* d) {
     ly.boff = off;
     off = align_up(off + ly.out, 32);
     ly.hidden = l + 1 < n.L ? 1 : 0;
+    n.seg[n.nseg++] = ly;
   }
   n.D = ref;
   n.Dp = align_up(off, 32);
   return n;
 }
+
+// floats per input row: the MLP input or the CNN image
+int64_t input_floats(const NetDev& n) { return n.nconv > 0 ? (int64_t)n.in_c * n.in_h * n.in_w : n.sizes[0]; }
 
 void free_ctx(Ctx& c) {
   cudaSetDevice(c.device);
@@ -97,6 +142,11 @@ void free_ctx(Ctx& c) {
     if (p) cudaFree(p);
   for (int l = 0; l <= kMaxLayers; ++l)
     if (c.act[l]) cudaFree(c.act[l]);
+  for (int i = 0; i < kMaxConv; ++i) {
+    if (c.cact[i]) cudaFree(c.cact[i]);
+    if (c.cpool[i]) cudaFree(c.cpool[i]);
+    if (c.cdel[i]) cudaFree(c.cdel[i]);
+  }
   if (c.h_records) cudaFreeHost(c.h_records);
   if (c.h_stage) cudaFreeHost(c.h_stage);
   if (c.ev0) cudaEventDestroy(c.ev0);
@@ -310,7 +360,7 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
   CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
   CK(cudaEventCreate(&c.ev0));
   CK(cudaEventCreate(&c.ev1));
-  const int n0 = c.net.sizes[0];
+  const int64_t n0 = input_floats(c.net);
   dmalloc(c.X, (size_t)n * n0);
   dmalloc(c.y, (size_t)n);
   CK(cudaMemcpy(c.X, X, sizeof(float) * (size_t)n * n0, cudaMemcpyHostToDevice));
@@ -362,8 +412,8 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
   CK(cudaMemcpy(c.jump_tab, tab.data(), sizeof(uint64_t) * 4 * tab.size(), cudaMemcpyHostToDevice));
   if (precision != DASMC_PREC_FP32) {
     if (!tc_layer1_eligible(c))
-      throw InvalidArg("tensor-core precision needs a one-hidden-layer MLP with input % 4 == 0, hidden <= 256, "
-                       "classes <= 16 (use DASMC_PREC_FP32)");
+      throw InvalidArg("tensor-core precision needs a one-hidden-layer MLP (no conv stages) with input % 4 == 0, "
+                       "hidden <= 256, classes <= 16 (use DASMC_PREC_FP32)");
     tc_init(c);
   }
 }
@@ -701,7 +751,7 @@ int dasmc_make_teacher_data(const dasmc_net_desc* net, int64_t n, int feature_ki
     const NetDev nd = make_net(net);
     if (n < 1 || !X || !y) throw InvalidArg("bad argument");
     std::vector<int> layers(net->layer_sizes, net->layer_sizes + net->num_layers);
-    make_teacher_data(layers, nd.act, n, feature_kind, seed, cfg_id, threads, X, y);
+    make_teacher_data(layers, nd.act, n, feature_kind, seed, cfg_id, threads, X, y, net->conv);
   });
 }
 
@@ -935,7 +985,7 @@ int dasmc_gpu_run(const dasmc_net_desc* net, const float* X, const int32_t* y, i
     if (!net || !X || !y || !cfg || !records) throw InvalidArg("null argument");
     // shuffle once with root.fork(kPermutation) (runner.hpp:486-489)
     const auto perm = shuffle_permutation(cfg->seed, n);
-    const int d = net->layer_sizes[0];
+    const int64_t d = input_floats(make_net(net));
     std::vector<float> Xs((size_t)n * d);
     std::vector<int32_t> ys((size_t)n);
     for (int64_t i = 0; i < n; ++i) {

@@ -46,19 +46,35 @@ extern std::atomic<long long> g_launch_count;
 constexpr int kTimerKinds = 3;
 
 constexpr int kMaxLayers = 8;
+constexpr int kMaxConv = 6;
 
 struct LayerDev {
   int in, out;
   int64_t woff, boff;  // internal offsets (floats) of W_l [out][in] and b_l
   int64_t ref_off;     // reference offset of layer l's block (W column-major, then b)
   int hidden;          // 1 if the activation applies after this layer
+  int nb;              // biases in the block (= out; cout for a conv block)
+};
+
+// [EXT] CNN stage (dasmc_gpu.h): valid stride-1 convolution + activation (+ 2x2 pool).
+struct ConvDev {
+  int cin, hin, win, k, cout, ho, wo, sh, sw, pool;  // sh x sw: stage output (after the pool)
+  int64_t woff, boff;  // W[cout][cin][k][k] (same order as the reference layout), b[cout]
 };
 
 struct NetDev {
-  int L;  // number of weight layers
+  int L;  // number of (fully connected) weight layers
   int act;
   int sizes[kMaxLayers + 1];
   LayerDev layer[kMaxLayers];
+  int nconv;  // CNN front stages (0 for an MLP); sizes[0] = flatten size
+  int in_c, in_h, in_w;
+  ConvDev conv[kMaxConv];
+  // every parameter block in reference order, for the reference <-> internal index
+  // walks: MLP layers map W column-major -> row-major; a conv block is described as
+  // a 1 x (cout*cin*k*k) "layer" so the same walk is the identity on it
+  int nseg;
+  LayerDev seg[kMaxLayers + kMaxConv];
   int64_t D;   // reference parameter count
   int64_t Dp;  // internal padded particle stride (floats)
 };
@@ -120,6 +136,12 @@ struct Ctx {
   // activations
   int64_t Mcap = 0;
   float* act[kMaxLayers + 1] = {};
+  // [EXT] CNN stages: cact = post-activation (pre-pool) [Jmax][Mcap][cout*ho*wo]; cpool =
+  // pooled stage output; cdel = pre-activation delta of a pooled stage.  Backward
+  // deltas of the stage outputs overwrite the outputs in place (as act[] does).
+  float* cact[kMaxConv] = {};
+  float* cpool[kMaxConv] = {};
+  float* cdel[kMaxConv] = {};
   float* dT = nullptr;  // delta_1 transposed [J][n1][Mcap] (tensor-core dW1 operand)
 
   // per-particle scratch

@@ -278,21 +278,78 @@ std::vector<int64_t> shuffle_permutation(uint64_t seed, int64_t n) {  // dataset
 }
 
 void make_teacher_data(const std::vector<int>& layers, int act, int64_t n, int feature_kind, uint64_t seed,
-                       uint64_t cfg_id, int threads, float* X, int32_t* y) {
-  const int d = layers.front();
+                       uint64_t cfg_id, int threads, float* X, int32_t* y, const int* conv) {
+  // [EXT] conv != nullptr: a CNN teacher (dasmc_gpu.h), same loops as the oracle's cnn_stages
+  struct Stage {
+    int cin, hin, win, k, cout, ho, wo, sh, sw, pool;
+    int64_t woff, boff;
+  };
+  std::vector<Stage> st;
+  int64_t D = 0;
+  int d = layers.front();
+  if (conv != nullptr) {
+    int ch = conv[0], h = conv[1], w = conv[2];
+    d = ch * h * w;
+    for (int i = 0; i < conv[3]; ++i) {
+      Stage s{ch, h, w, conv[4 + 3 * i], conv[5 + 3 * i], 0, 0, 0, 0, conv[6 + 3 * i] != 0 ? 1 : 0, 0, 0};
+      s.ho = h - s.k + 1;
+      s.wo = w - s.k + 1;
+      s.sh = s.pool ? s.ho / 2 : s.ho;
+      s.sw = s.pool ? s.wo / 2 : s.wo;
+      s.woff = D;
+      D += (int64_t)s.cout * s.cin * s.k * s.k;
+      s.boff = D;
+      D += s.cout;
+      st.push_back(s);
+      ch = s.cout;
+      h = s.sh;
+      w = s.sw;
+    }
+  }
+  const int64_t Dconv = D;
   std::vector<double> F((size_t)n * d);
   HostRng fx(fork_key(seed, tag::kSynthetic, cfg_id, 1));
   for (auto& v : F) v = feature_kind == 0 ? fx.uniform() : (double)fx.uniform_below(256) / 255.0;
-  int64_t D = 0;
   for (size_t l = 1; l < layers.size(); ++l) D += (int64_t)layers[l - 1] * layers[l] + layers[l];
   HostRng ft(fork_key(seed, tag::kSynthetic, cfg_id, 2));
   std::vector<double> th((size_t)D);
   for (auto& v : th) v = ft.normal();
+  auto actf = [&](double z) { return act == DASMC_RELU ? (z > 0.0 ? z : 0.0) : std::tanh(z); };
   auto label_rows = [&](int64_t lo, int64_t hi) {
-    std::vector<double> cur, nxt;
+    std::vector<double> cur, nxt, A;
     for (int64_t i = lo; i < hi; ++i) {
       cur.assign(F.begin() + i * d, F.begin() + (i + 1) * d);
-      int64_t off = 0;
+      for (const Stage& s : st) {
+        A.assign((size_t)s.cout * s.ho * s.wo, 0.0);
+        for (int co = 0; co < s.cout; ++co)
+          for (int yy = 0; yy < s.ho; ++yy)
+            for (int xx = 0; xx < s.wo; ++xx) {
+              double acc = 0.0;
+              for (int ci = 0; ci < s.cin; ++ci)
+                for (int ky = 0; ky < s.k; ++ky)
+                  for (int kx = 0; kx < s.k; ++kx)
+                    acc += th[(size_t)(s.woff + (((int64_t)co * s.cin + ci) * s.k + ky) * s.k + kx)] *
+                           cur[((size_t)ci * s.hin + yy + ky) * s.win + xx + kx];
+              acc += th[(size_t)(s.boff + co)];
+              A[((size_t)co * s.ho + yy) * s.wo + xx] = actf(acc);
+            }
+        if (s.pool) {
+          nxt.assign((size_t)s.cout * s.sh * s.sw, 0.0);
+          for (int co = 0; co < s.cout; ++co)
+            for (int yy = 0; yy < s.sh; ++yy)
+              for (int xx = 0; xx < s.sw; ++xx) {
+                double mx = A[((size_t)co * s.ho + 2 * yy) * s.wo + 2 * xx];
+                for (int dy = 0; dy < 2; ++dy)
+                  for (int dx = 0; dx < 2; ++dx)
+                    mx = std::max(mx, A[((size_t)co * s.ho + 2 * yy + dy) * s.wo + 2 * xx + dx]);
+                nxt[((size_t)co * s.sh + yy) * s.sw + xx] = mx;
+              }
+          cur.swap(nxt);
+        } else {
+          cur.swap(A);
+        }
+      }
+      int64_t off = Dconv;
       for (size_t l = 1; l < layers.size(); ++l) {
         const int in = layers[l - 1], out = layers[l];
         nxt.assign((size_t)out, 0.0);
@@ -300,7 +357,7 @@ void make_teacher_data(const std::vector<int>& layers, int act, int64_t n, int f
           double acc = 0.0;
           for (int c = 0; c < in; ++c) acc += th[(size_t)(off + (int64_t)c * out + r)] * cur[(size_t)c];
           acc += th[(size_t)(off + (int64_t)in * out + r)];
-          if (l + 1 < layers.size()) acc = act == DASMC_RELU ? (acc > 0.0 ? acc : 0.0) : std::tanh(acc);
+          if (l + 1 < layers.size()) acc = actf(acc);
           nxt[(size_t)r] = acc;
         }
         off += (int64_t)in * out + out;

@@ -120,7 +120,7 @@ std::vector<double> normalize(const double* lw, int64_t J);
 // ---- data -------------------------------------------------------------------------------
 std::vector<int64_t> shuffle_permutation(uint64_t seed, int64_t n);
 void make_teacher_data(const std::vector<int>& layers, int act, int64_t n, int feature_kind, uint64_t seed,
-                       uint64_t cfg_id, int threads, float* X, int32_t* y);
+                       uint64_t cfg_id, int threads, float* X, int32_t* y, const int* conv = nullptr);
 
 // ---- errors ------------------------------------------------------------------------------
 struct Error {

@@ -66,9 +66,9 @@ __device__ __forceinline__ bool finitef(float v) { return isfinite(v); }
 __device__ __forceinline__ int64_t internal_index(const NetDev& net, int64_t i) {
   int l = 0;
 #pragma unroll 1
-  for (; l < net.L - 1; ++l)
-    if (i < net.layer[l + 1].ref_off) break;
-  const LayerDev& ly = net.layer[l];
+  for (; l < net.nseg - 1; ++l)
+    if (i < net.seg[l + 1].ref_off) break;
+  const LayerDev& ly = net.seg[l];
   const int64_t t = i - ly.ref_off;
   const int64_t nw = (int64_t)ly.in * ly.out;
   if (t < nw) {
@@ -268,7 +268,8 @@ struct EpiDx {
   __device__ void operator()(int j, int m, int n, float v) const {
     float* p = D + (int64_t)j * sD + (int64_t)m * ldd + n;
     const float a = *p;
-    *p = act == DASMC_RELU ? v * (a > 0.f ? 1.f : 0.f) : v * (1.f - a * a);
+    // act < 0: no activation derivative (a pooled CNN stage output: the pool backward applies it)
+    *p = act < 0 ? v : act == DASMC_RELU ? v * (a > 0.f ? 1.f : 0.f) : v * (1.f - a * a);
   }
 };
 
@@ -404,16 +405,16 @@ __global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b
   // reference index i -> internal offset, walked incrementally (one division per chunk):
   // layer l, W(r, c) at ref_off + r + c*out -> woff + r*in + c; then the bias block.
   int l = 0;
-  while (l < net.L - 1 && lo >= net.layer[l + 1].ref_off) ++l;
-  int64_t t = lo - net.layer[l].ref_off;
-  int64_t nw = (int64_t)net.layer[l].in * net.layer[l].out;
-  int64_t r = t < nw ? t % net.layer[l].out : 0, cc = t < nw ? t / net.layer[l].out : 0;
+  while (l < net.nseg - 1 && lo >= net.seg[l + 1].ref_off) ++l;
+  int64_t t = lo - net.seg[l].ref_off;
+  int64_t nw = (int64_t)net.seg[l].in * net.seg[l].out;
+  int64_t r = t < nw ? t % net.seg[l].out : 0, cc = t < nw ? t / net.seg[l].out : 0;
   for (int64_t i = lo; i < hi; ++i) {
     const double u1 = 1.0 - x.uniform();
     const double u2 = x.uniform();
     const double nv = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
     const float v = (float)((double)scale * nv);
-    const LayerDev& ly = net.layer[l];
+    const LayerDev& ly = net.seg[l];
     out[t < nw ? ly.woff + r * ly.in + cc : ly.boff + (t - nw)] = v;
     sq += (double)v * (double)v;
     // advance to i + 1
@@ -422,11 +423,11 @@ __global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b
         r = 0;
         ++cc;
       }
-    } else if (t == nw + ly.out && l + 1 < net.L) {
+    } else if (t == nw + ly.nb && l + 1 < net.nseg) {
       ++l;
       t = 0;
       r = cc = 0;
-      nw = (int64_t)net.layer[l].in * net.layer[l].out;
+      nw = (int64_t)net.seg[l].in * net.seg[l].out;
     }
   }
   if (sq_part) sq_part[j * nchunks + c] = sq;
@@ -656,6 +657,230 @@ void ensure_host_stage(Ctx& c, size_t bytes) {
   c.h_stage_bytes = bytes;
 }
 
+// ---- [EXT] CNN stages (dasmc_gpu.h conv descriptor; oracle cnn_stages / cnn_stages_backward) ----
+// One thread per output element, grid-stride.  Images are [c][h][w]; stage buffers are
+// [Jmax][Mcap][per-image floats].  Stage 0 reads X (shared by every particle).
+__device__ __forceinline__ float act_apply(float z, int act) { return act == DASMC_RELU ? fmaxf(z, 0.f) : tanhf(z); }
+__device__ __forceinline__ float act_grad_post(float a, int act) {
+  return act == DASMC_RELU ? (a > 0.f ? 1.f : 0.f) : 1.f - a * a;
+}
+
+__global__ void conv_fwd_kernel(ConvDev d, int act, const float* __restrict__ in, int64_t in_ps,
+                                const float* __restrict__ theta, int64_t Dp, float* __restrict__ A, int64_t a_ps,
+                                int64_t M, int64_t J) {
+  const int64_t in_img = (int64_t)d.cin * d.hin * d.win, per = (int64_t)d.cout * d.ho * d.wo;
+  const int64_t total = J * M * per;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / (M * per), r = g - j * M * per, m = r / per, o = r - m * per;
+    const int co = (int)(o / ((int64_t)d.ho * d.wo));
+    const int yx = (int)(o - (int64_t)co * d.ho * d.wo), y = yx / d.wo, x = yx - y * d.wo;
+    const float* w = theta + j * Dp + d.woff + (int64_t)co * d.cin * d.k * d.k;
+    const float* src = in + j * in_ps + m * in_img;
+    float acc = 0.f;
+    for (int ci = 0; ci < d.cin; ++ci)
+      for (int ky = 0; ky < d.k; ++ky) {
+        const float* srow = src + ((int64_t)ci * d.hin + y + ky) * d.win + x;
+        const float* wrow = w + ((int64_t)ci * d.k + ky) * d.k;
+        for (int kx = 0; kx < d.k; ++kx) acc = fmaf(wrow[kx], srow[kx], acc);
+      }
+    acc += theta[j * Dp + d.boff + co];
+    A[j * a_ps + m * per + o] = act_apply(acc, act);
+  }
+}
+
+__global__ void pool_fwd_kernel(ConvDev d, const float* __restrict__ A, int64_t a_ps, float* __restrict__ P,
+                                int64_t p_ps, int64_t M, int64_t J) {
+  const int64_t per_a = (int64_t)d.cout * d.ho * d.wo, per = (int64_t)d.cout * d.sh * d.sw;
+  const int64_t total = J * M * per;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / (M * per), r = g - j * M * per, m = r / per, o = r - m * per;
+    const int co = (int)(o / ((int64_t)d.sh * d.sw));
+    const int yx = (int)(o - (int64_t)co * d.sh * d.sw), y = yx / d.sw, x = yx - y * d.sw;
+    const float* a = A + j * a_ps + m * per_a + ((int64_t)co * d.ho + 2 * y) * d.wo + 2 * x;
+    P[j * p_ps + m * per + o] = fmaxf(fmaxf(a[0], a[1]), fmaxf(a[d.wo], a[d.wo + 1]));
+  }
+}
+
+// dz = (first argmax of the window ? dP : 0) * act'(A); positions outside the pooled region get 0
+__global__ void pool_bwd_kernel(ConvDev d, int act, const float* __restrict__ A, int64_t a_ps,
+                                const float* __restrict__ dP, int64_t p_ps, float* __restrict__ dZ, int64_t M,
+                                int64_t J) {
+  const int64_t per_a = (int64_t)d.cout * d.ho * d.wo, per = (int64_t)d.cout * d.sh * d.sw;
+  const int64_t total = J * M * per_a;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / (M * per_a), r = g - j * M * per_a, m = r / per_a, o = r - m * per_a;
+    const int co = (int)(o / ((int64_t)d.ho * d.wo));
+    const int yx = (int)(o - (int64_t)co * d.ho * d.wo), y = yx / d.wo, x = yx - y * d.wo;
+    const int py = y >> 1, px = x >> 1;
+    float v = 0.f;
+    if (py < d.sh && px < d.sw) {
+      const float* a = A + j * a_ps + m * per_a + ((int64_t)co * d.ho + 2 * py) * d.wo + 2 * px;
+      int best = 0;
+      float mx = a[0];
+      if (a[1] > mx) { mx = a[1]; best = 1; }
+      if (a[d.wo] > mx) { mx = a[d.wo]; best = 2; }
+      if (a[d.wo + 1] > mx) { mx = a[d.wo + 1]; best = 3; }
+      if (((y & 1) << 1 | (x & 1)) == best) {
+        const float dp = dP[j * p_ps + m * per + ((int64_t)co * d.sh + py) * d.sw + px];
+        v = dp * act_grad_post(A[j * a_ps + m * per_a + o], act);
+      }
+    }
+    dZ[j * a_ps + m * per_a + o] = v;
+  }
+}
+
+// Weight gradient of one stage: one thread per (j, parameter); window sum with
+// fp32 per-image partials and an fp64 running total, then the fused leapfrog.
+__global__ void conv_dw_kernel(ConvDev d, const float* __restrict__ dZ, int64_t z_ps, const float* __restrict__ in,
+                               int64_t in_ps, int64_t Dp, int64_t M, int64_t J, EpiParams e) {
+  const int64_t nw = (int64_t)d.cout * d.cin * d.k * d.k, np = nw + d.cout;
+  const int64_t in_img = (int64_t)d.cin * d.hin * d.win, per = (int64_t)d.cout * d.ho * d.wo;
+  const int64_t total = J * np;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / np, q = g - j * np;
+    double acc = 0.0;
+    if (q < nw) {
+      const int kx = (int)(q % d.k), ky = (int)((q / d.k) % d.k), ci = (int)((q / ((int64_t)d.k * d.k)) % d.cin);
+      const int co = (int)(q / ((int64_t)d.k * d.k * d.cin));
+      for (int64_t m = 0; m < M; ++m) {
+        const float* z = dZ + j * z_ps + m * per + (int64_t)co * d.ho * d.wo;
+        const float* src = in + j * in_ps + m * in_img + ((int64_t)ci * d.hin + ky) * d.win + kx;
+        float s = 0.f;
+        for (int y = 0; y < d.ho; ++y)
+          for (int x = 0; x < d.wo; ++x) s = fmaf(z[y * d.wo + x], src[(int64_t)y * d.win + x], s);
+        acc += (double)s;
+      }
+      leapfrog_update(e, (int)j, j * Dp + d.woff + q, (float)acc);
+    } else {
+      const int co = (int)(q - nw);
+      for (int64_t m = 0; m < M; ++m) {
+        const float* z = dZ + j * z_ps + m * per + (int64_t)co * d.ho * d.wo;
+        float s = 0.f;
+        for (int t = 0; t < d.ho * d.wo; ++t) s += z[t];
+        acc += (double)s;
+      }
+      leapfrog_update(e, (int)j, j * Dp + d.boff + co, (float)acc);
+    }
+  }
+}
+
+// Input delta of a stage (transposed convolution), in place over the previous stage
+// output `io` (read for the mask first): delta = sum dz * W, times act'(io) unless the
+// previous stage pools (its pool backward applies act' at the argmax instead).
+__global__ void conv_dx_kernel(ConvDev d, int act, int apply_act, const float* __restrict__ dZ, int64_t z_ps,
+                               const float* __restrict__ theta, int64_t Dp, float* io, int64_t io_ps, int64_t M,
+                               int64_t J) {
+  const int64_t in_img = (int64_t)d.cin * d.hin * d.win, per = (int64_t)d.cout * d.ho * d.wo;
+  const int64_t total = J * M * in_img;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / (M * in_img), r = g - j * M * in_img, m = r / in_img, o = r - m * in_img;
+    const int ci = (int)(o / ((int64_t)d.hin * d.win));
+    const int yx = (int)(o - (int64_t)ci * d.hin * d.win), y = yx / d.win, x = yx - y * d.win;
+    const float* z = dZ + j * z_ps + m * per;
+    const float* w = theta + j * Dp + d.woff + (int64_t)ci * d.k * d.k;
+    float acc = 0.f;
+    for (int co = 0; co < d.cout; ++co)
+      for (int ky = 0; ky < d.k; ++ky) {
+        const int oy = y - ky;
+        if (oy < 0 || oy >= d.ho) continue;
+        for (int kx = 0; kx < d.k; ++kx) {
+          const int ox = x - kx;
+          if (ox < 0 || ox >= d.wo) continue;
+          acc = fmaf(z[((int64_t)co * d.ho + oy) * d.wo + ox], w[(int64_t)co * d.cin * d.k * d.k + ky * d.k + kx], acc);
+        }
+      }
+    float* p = io + j * io_ps + m * in_img + o;
+    *p = apply_act ? acc * act_grad_post(*p, act) : acc;
+  }
+}
+
+int64_t conv_out_floats(const ConvDev& d) { return (int64_t)d.cout * d.sh * d.sw; }
+int64_t conv_act_floats(const ConvDev& d) { return (int64_t)d.cout * d.ho * d.wo; }
+float* stage_out(Ctx& c, int i) { return c.net.conv[i].pool ? c.cpool[i] : c.cact[i]; }
+
+// CNN gradient evaluation: conv stages -> flatten -> the SIMT MLP head (layer 1 reads
+// the last stage output) -> head backward incl. the flatten delta -> conv stages backward.
+void launch_eval_cnn(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, double beta_rows, bool need_grad,
+                     const EpiParams* epi) {
+  const NetDev& net = c.net;
+  const int L = net.L, nc = net.nconv;
+  auto grid_of = [](int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32); };
+  // forward through the stages
+  for (int i = 0; i < nc; ++i) {
+    const ConvDev& d = net.conv[i];
+    const float* in = i == 0 ? c.X : stage_out(c, i - 1);
+    const int64_t in_ps = i == 0 ? 0 : c.Mcap * conv_out_floats(net.conv[i - 1]);
+    conv_fwd_kernel<<<grid_of(J * M * conv_act_floats(d)), 256, 0, c.stream>>>(
+        d, net.act, in, in_ps, theta_in, net.Dp, c.cact[i], c.Mcap * conv_act_floats(d), M, J);
+    LAUNCHED();
+    if (d.pool) {
+      pool_fwd_kernel<<<grid_of(J * M * conv_out_floats(d)), 256, 0, c.stream>>>(
+          d, c.cact[i], c.Mcap * conv_act_floats(d), c.cpool[i], c.Mcap * conv_out_floats(d), M, J);
+      LAUNCHED();
+    }
+  }
+  float* flat = stage_out(c, nc - 1);
+  const int64_t F = net.sizes[0];
+  // MLP head (network.hpp:159-178 with layer 1 reading the flatten)
+  for (int l = 1; l <= L; ++l) {
+    const LayerDev& ly = net.layer[l - 1];
+    EpiFwd e{c.act[l], ly.out, c.Mcap * ly.out, theta_in, net.Dp, ly.boff, ly.hidden, net.act};
+    const float* A = l == 1 ? flat : c.act[l - 1];
+    const int64_t sA = l == 1 ? c.Mcap * F : c.Mcap * ly.in;
+    sgemm<true, true>(c.stream, (int)M, ly.out, ly.in, A, ly.in, sA, theta_in + ly.woff, ly.in, net.Dp, -1, J, e);
+  }
+  {
+    const int C = net.sizes[L];
+    dim3 grid((unsigned)((M + kRowsPerBlock - 1) / kRowsPerBlock), (unsigned)J);
+    softmax_kernel<<<grid, kRowsPerBlock, 0, c.stream>>>(c.act[L], c.Mcap * C, C, c.y, M, P, (float)beta_rows,
+                                                         need_grad ? 1 : 0, c.ll_part, c.ll_slots);
+    LAUNCHED();
+  }
+  if (!need_grad) return;
+  for (int l = L; l >= 1; --l) {
+    const LayerDev& ly = net.layer[l - 1];
+    {
+      EpiDw e{*epi, net.Dp, ly.woff, ly.boff, ly.in};
+      const float* Bp = l == 1 ? flat : c.act[l - 1];
+      const int64_t sB = l == 1 ? c.Mcap * F : c.Mcap * ly.in;
+      sgemm<false, false>(c.stream, ly.out, ly.in + 1, (int)M, c.act[l], ly.out, c.Mcap * ly.out, Bp, ly.in, sB,
+                          ly.in, J, e);
+    }
+    // delta_{l-1} in place over a_{l-1}; for l = 1 over the flatten (act' only if the
+    // last stage does not pool)
+    float* Dst = l > 1 ? c.act[l - 1] : flat;
+    const int64_t ldd = l > 1 ? net.layer[l - 2].out : F;
+    const int act = l > 1 || !net.conv[nc - 1].pool ? net.act : -1;
+    EpiDx d{Dst, ldd, c.Mcap * ldd, act};
+    sgemm<true, false>(c.stream, (int)M, ly.in, ly.out, c.act[l], ly.out, c.Mcap * ly.out, theta_in + ly.woff,
+                       ly.in, net.Dp, -1, J, d);
+  }
+  // conv stages backward
+  for (int i = nc - 1; i >= 0; --i) {
+    const ConvDev& d = net.conv[i];
+    const int64_t a_ps = c.Mcap * conv_act_floats(d);
+    float* dz = c.cact[i];  // no pool: the stage-output delta (act' applied) is already dz
+    if (d.pool) {
+      dz = c.cdel[i];
+      pool_bwd_kernel<<<grid_of(J * M * conv_act_floats(d)), 256, 0, c.stream>>>(
+          d, net.act, c.cact[i], a_ps, c.cpool[i], c.Mcap * conv_out_floats(d), dz, M, J);
+      LAUNCHED();
+    }
+    const float* in = i == 0 ? c.X : stage_out(c, i - 1);
+    const int64_t in_ps = i == 0 ? 0 : c.Mcap * conv_out_floats(net.conv[i - 1]);
+    const int64_t np = (int64_t)d.cout * d.cin * d.k * d.k + d.cout;
+    conv_dw_kernel<<<grid_of(J * np), 256, 0, c.stream>>>(d, dz, a_ps, in, in_ps, net.Dp, M, J, *epi);
+    LAUNCHED();
+    if (i > 0) {
+      const ConvDev& dp = net.conv[i - 1];
+      conv_dx_kernel<<<grid_of(J * M * (int64_t)d.cin * d.hin * d.win), 256, 0, c.stream>>>(
+          d, net.act, dp.pool ? 0 : 1, dz, a_ps, theta_in, net.Dp, stage_out(c, i - 1),
+          c.Mcap * conv_out_floats(dp), M, J);
+      LAUNCHED();
+    }
+  }
+}
+
 void ensure_activation_capacity(Ctx& c, int64_t M) {
   if (M <= c.Mcap) return;
   CK(cudaStreamSynchronize(c.stream));
@@ -667,6 +892,20 @@ void ensure_activation_capacity(Ctx& c, int64_t M) {
       if (c.act[l]) CK(cudaFree(c.act[l]));
       c.act[l] = nullptr;
       CK(cudaMalloc(&c.act[l], sizeof(float) * (size_t)c.Jmax * Mnew * c.net.sizes[l]));
+    }
+    for (int i = 0; i < c.net.nconv; ++i) {
+      float** bufs[] = {&c.cact[i], &c.cpool[i], &c.cdel[i]};
+      for (float** b : bufs)
+        if (*b) {
+          CK(cudaFree(*b));
+          *b = nullptr;
+        }
+      const ConvDev& d = c.net.conv[i];
+      CK(cudaMalloc(&c.cact[i], sizeof(float) * (size_t)c.Jmax * Mnew * conv_act_floats(d)));
+      if (d.pool) {
+        CK(cudaMalloc(&c.cpool[i], sizeof(float) * (size_t)c.Jmax * Mnew * conv_out_floats(d)));
+        CK(cudaMalloc(&c.cdel[i], sizeof(float) * (size_t)c.Jmax * Mnew * conv_act_floats(d)));
+      }
     }
   }
   const int slots = (int)((Mnew + kRowsPerBlock - 1) / kRowsPerBlock);
@@ -691,6 +930,10 @@ void launch_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P,
   }
   if (c.tc) {
     tc_eval(c, theta_in, J, M, P, beta_rows, need_grad, epi);
+    return;
+  }
+  if (net.nconv > 0) {
+    launch_eval_cnn(c, theta_in, J, M, P, beta_rows, need_grad, epi);
     return;
   }
   // forward (network.hpp:159-178)

@@ -1116,7 +1116,7 @@ void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUten
 
 bool tc_layer1_eligible(const Ctx& c) {
   const NetDev& n = c.net;
-  return n.L == 2 && n.sizes[0] % 4 == 0 && n.sizes[0] >= 4 && n.sizes[1] <= 256 && n.sizes[2] <= 16;
+  return n.nconv == 0 && n.L == 2 && n.sizes[0] % 4 == 0 && n.sizes[0] >= 4 && n.sizes[1] <= 256 && n.sizes[2] <= 16;
 }
 
 void tc_init(Ctx& c) {
