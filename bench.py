@@ -37,6 +37,23 @@ WORKLOADS = {
                S=3, h=0.002, k0=150, cfg_id=2,
                desc="C2: MLP 784-200-10 ReLU, J=1024 particles, n=60000 synthetic 28x28x1 k/255 teacher-labelled, "
                     "MB=1000 (+1 MB every 5 iterations, 300 iterations), HMC S=3 h=0.002, prior N(0,1)"),
+    # BASELINE.json configs[2]: CNN, SDA annealing; measured at a constant window of MB rows
+    "c3": dict(layers=[512, 10], conv=((1, 28, 28), [(5, 16, True), (5, 32, True)]), act="relu", n=60000, J=512,
+               feature_kind=1, mb=500, const_window=True, K=200, S=3, h=0.002, k0=0, cfg_id=3, cpu_rows=48,
+               desc="C3: CNN conv5x5x16-ReLU-pool-conv5x5x32-ReLU-pool-FC512-10 on 28x28x1 k/255 teacher-labelled, "
+                    "J=512, window M=500 (one MB), HMC S=3 h=0.002"),
+    # BASELINE.json configs[3]: CNN on 32x32x3, constant-to-refine phase window
+    "c4": dict(layers=[1600, 256, 10], conv=((3, 32, 32), [(3, 32, False), (3, 32, True), (3, 64, False),
+                                                           (3, 64, True)]),
+               act="relu", n=50000, J=256, feature_kind=1, mb=500, const_window=True, K=200, S=3, h=0.002, k0=0,
+               cfg_id=4, cpu_rows=6,
+               desc="C4: CNN conv3x3x32-conv3x3x32-pool-conv3x3x64-conv3x3x64-pool-FC256-10 (valid, ReLU) on 32x32x3 "
+                    "U{0..255}/255, J=256, window M=500 (the CTR phase), HMC S=3 h=0.002"),
+    # BASELINE.json configs[4] at J=1024 per GPU (the scaling sweep's per-GPU unit)
+    "c5": dict(layers=[3072, 512, 512, 10], act="relu", n=50000, J=1024, feature_kind=0, mb=1000, const_window=True,
+               K=100, S=3, h=0.002, k0=0, cfg_id=5,
+               desc="C5: MLP 3072-512-512-10 ReLU, J=1024 per GPU, 50000 U[0,1]^3072 teacher-labelled, window "
+                    "M=1000, resample every iteration, HMC S=3 h=0.002"),
     # BASELINE.json configs[0] (CPU-runnable case)
     "c1": dict(layers=[64, 32, 10], act="tanh", n=2000, J=128, feature_kind=0, mb=100, period=1, K=50, S=3,
                h=0.002, k0=0, cfg_id=1, ctr=(200, 40),
@@ -47,16 +64,28 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
 def window(w, k):
+    if w.get("const_window"):
+        return w["mb"]
     if "ctr" in w:
         c0, sw = w["ctr"]
         return c0 if k < sw else w["n"]
     return min(w["mb"] * (1 + k // w["period"]), w["n"])
 
 
-def algorithmic_flops_per_row(layers):
-    """F_grad = 4 sum_l n_{l-1} n_l + 2 sum_{l>=2} n_{l-1} n_l per datapoint."""
-    pairs = [layers[i - 1] * layers[i] for i in range(1, len(layers))]
-    return 4 * sum(pairs) + 2 * sum(pairs[1:])
+def algorithmic_flops_per_row(layers, conv=None):
+    """F_grad = 4 sum_l MAC_l + 2 sum_{l>=2} MAC_l per datapoint (forward + dW + dX,
+    no dX for the first layer); MAC_l = n_{l-1} n_l for a dense layer, outputs x cin k^2 for a conv."""
+    macs = []
+    if conv is not None:
+        (c, h, w), stages = conv
+        for k, co, pool in stages:
+            h, w = h - k + 1, w - k + 1
+            macs.append(h * w * co * c * k * k)
+            if pool:
+                h, w = h // 2, w // 2
+            c = co
+    macs += [layers[i - 1] * layers[i] for i in range(1, len(layers))]
+    return 4 * sum(macs) + 2 * sum(macs[1:])
 
 
 class ClockSampler:
@@ -115,7 +144,7 @@ def load_peaks():
 
 def make_data(w):
     import paper_2601_21983_b200 as p
-    spec = p.NetSpec(w["layers"], w["act"])
+    spec = p.NetSpec(w["layers"], w["act"], w.get("conv"))
     X, y = p.make_teacher_data(spec, w["n"], w["feature_kind"], 0, w["cfg_id"], threads=os.cpu_count() or 8)
     perm = p.shuffle_permutation(0, w["n"])  # runner.hpp:486-489 (seed 0)
     return spec, np.ascontiguousarray(X[perm]), np.ascontiguousarray(y[perm])
@@ -127,14 +156,16 @@ def cpu_sample(w, X, y, ks, threads, warm=False):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as O
     O.use_blas(True)
-    layers = w["layers"]
+    layers = w["layers"] if "conv" not in w else O.cnn_layers(w["conv"][0], w["conv"][1], w["layers"])
     a = 0 if w["act"] == "relu" else 1
     Jc = max(2, threads)
     X64 = X.astype(np.float64)
-    th, lw = O.init_ensemble(layers, a, X64, y, (0, window(w, ks[0]), w["n"]), 0, 1.0, 1.0, 0, Jc, threads=threads)
+    # the CNN oracle is plain loops: its sample takes fewer window rows (per-unit rate)
+    rows = lambda k: min(window(w, k), w.get("cpu_rows", 1 << 62))  # noqa: E731
+    th, lw = O.init_ensemble(layers, a, X64, y, (0, rows(ks[0]), w["n"]), 0, 1.0, 1.0, 0, Jc, threads=threads)
     units, secs = 0.0, 0.0
     for k in ks:
-        M = window(w, k)
+        M = rows(k)
         t0 = time.perf_counter()
         th, lw, _, _, _ = O.smc_step(layers, a, X64, y, (0, M, w["n"]), 0, 1.0, 1.0, (w["h"], w["S"], 0), 0, 0.5, 1,
                                      False, th, lw, k, threads=threads, dumps=False)
@@ -287,6 +318,10 @@ def run_ours(args, w):
     kinds = [("layer-1 forward GEMM Z1 = X W1^T (+bias, ReLU epilogue)", fl_fwd, kms[0], kcnt[0]),
              ("layer-1 weight-gradient GEMM dW1 = delta1^T X (+fused leapfrog epilogue)", fl_dw, kms[1], kcnt[1])]
     name, fl, kt_ms, kc_n = max(kinds, key=lambda x: x[2])
+    if kt_ms <= 0 or "conv" in w:
+        # no per-GEMM timers on this path (CNN stages): the whole gradient evaluation
+        fl = sum(float(algorithmic_flops_per_row(w["layers"], w.get("conv"))) * M * J * (S + 1) for M in Ms)
+        name, kt_ms, kc_n = "whole gradient evaluation (CNN stages + MLP head, SIMT fp32)", kms[2], kcnt[2]
     peaks = load_peaks()
     if args.precision == "fp32":
         peak = 148 * 128 * 2 * 1.965e9 / 1e12
@@ -305,7 +340,7 @@ def run_ours(args, w):
             traffic = json.load(open(tf)).get(args.precision)
         except Exception:
             traffic = None
-    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+    roof = {"bound": "tensor" if args.precision != "fp32" else "compute", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic, "kernel": name,
             "launches": int(kc_n), "kernel_ms_total": float(kt_ms), "peak_source": peak_src,
             "share_of_step": float(kt_ms / ms) if ms > 0 else None,
@@ -351,12 +386,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--precision", default="tf32", choices=["fp32", "tf32", "3xtf32"])
+    ap.add_argument("--precision", default=None, choices=["fp32", "tf32", "3xtf32"],
+                    help="default: tf32 where the tensor-core path applies (one-hidden-layer MLPs), else fp32")
     ap.add_argument("--resample", default="systematic", choices=["systematic", "multinomial"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     w = WORKLOADS[args.config]
+    if args.precision is None:
+        tc_ok = "conv" not in w and len(w["layers"]) == 3 and w["layers"][1] <= 256 and w["layers"][2] <= 16
+        args.precision = "tf32" if tc_ok else "fp32"
     if args.impl == "reference":
         run_reference(args, w)
     else:

@@ -35,4 +35,40 @@ __device__ __forceinline__ void leapfrog_update(const EpiParams& e, int j, int64
   if (bad) atomicOr(&e.flags[j], 1);
 }
 
+// N parameters at once (a 16-column chunk of a weight-gradient tile): every load is
+// issued before any store, so the chunk's 2N loads are in flight together instead of
+// one dependent round trip per parameter (short-K GEMMs are epilogue-latency bound).
+template <int N>
+__device__ __forceinline__ void leapfrog_update_n(const EpiParams& e, int j, const int64_t* idx, const float* acc,
+                                                  int count) {
+  float th[N], p[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+    if (q < count) {
+      th[q] = e.theta_in[idx[q]];
+      if (e.mode != kEpiStoreGrad) p[q] = e.p[idx[q]];
+    }
+  bool bad = false;
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+    if (q < count) {
+      const float g = fmaf(e.scale, acc[q], -th[q] * e.inv_var);
+      bad |= !isfinite(g);
+      if (e.mode == kEpiStoreGrad) {
+        e.grad_out[idx[q]] = g;
+        continue;
+      }
+      float pq = fmaf(e.hh, g, p[q]);
+      if (e.mode == kEpiMid) pq = fmaf(e.hh, g, pq);
+      bad |= !isfinite(pq);
+      e.p[idx[q]] = pq;
+      if (e.mode != kEpiLast) {
+        const float tn = fmaf(e.h, pq, th[q]);
+        bad |= !isfinite(tn);
+        e.theta_out[idx[q]] = tn;
+      }
+    }
+  if (bad && e.mode != kEpiStoreGrad) atomicOr(&e.flags[j], 1);
+}
+
 }  // namespace dasmc_b200

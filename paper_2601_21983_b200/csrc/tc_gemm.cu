@@ -46,6 +46,20 @@ struct TcState {
   float* d1Tlo = nullptr;
   float* d2Tlo = nullptr;
   int num_sms = 148;
+  // deep MLP (>= 2 hidden layers; tc_eval_deep): per layer l (1-based)
+  bool deep = false;
+  int L = 0;
+  int sz[kMaxLayers + 1] = {};
+  int64_t kxl[kMaxLayers + 1] = {};   // a_l row-major stride with the ones column (kxl[0] = kx)
+  int64_t ldd[kMaxLayers + 1] = {};   // delta_l row-major stride (round4(n_l))
+  float* Whi[kMaxLayers + 1] = {};    // [J][n_l][kx_{l-1}] = [W_l, b_l, 0..] tf32, l < L
+  float* WThi[kMaxLayers + 1] = {};   // [J][n_{l-1}][ldd_l] = W_l^T tf32, 2 <= l < L
+  float* aRow[kMaxLayers + 1] = {};   // a_l [J][mcap][kx_l] (column n_l = 1), l < L
+  float* aT[kMaxLayers + 1] = {};     // a_l^T row-blocked [J][nblk][n_l + 1][128] (row n_l = 1), l < L
+  float* dRow[kMaxLayers + 1] = {};   // delta_l [J][mcap][ldd_l], 2 <= l < L (tf32 hi)
+  float* dRowLo[kMaxLayers + 1] = {}; // its split-tf32 low part (the backward-delta GEMMs run 3xtf32)
+  float* WTlo[kMaxLayers + 1] = {};   // low part of WThi
+  float* dTl[kMaxLayers + 1] = {};    // delta_l^T row-blocked [J][nblk][n_l][128], l <= L
 };
 
 namespace {
@@ -57,7 +71,14 @@ constexpr int kParts = kEpiWarps / 4;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;  // TMA warp + MMA warp + epilogue warps
 constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
-constexpr int kEpiKindFwd = 0, kEpiKindDw = 1;
+constexpr int kEpiKindFwd = 0, kEpiKindDw = 1, kEpiKindHidden = 2, kEpiKindBackDelta = 3;
+// Deep path: run the backward-delta GEMMs in split-tf32.  Off: measured on B200 it does not
+// move the deep gradients' error (dominated by ReLU activation-pattern flips under the
+// tf32 forward, not by the backward operands) and costs 19 % of the C5 step.
+constexpr bool kDeepSplitBack = false;
+// A operand addressing: 2-D shared by every particle; 4-D row-blocked per particle
+// (weight-gradient GEMMs, K = window rows); 3-D row-major per particle
+constexpr int kAShared = 0, kABlocked = 1, kARowMajor = 2;
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -319,6 +340,7 @@ struct TileParams {
   int bbox;    // clusters with QB = 2: B rows per multicast piece (pieces at 0 and half - bbox)
   int hint_a, hint_b;  // L2 policies of the A / B loads (pairs): 0 normal, 1 evict_last, 2 evict_first
   int prefetch;        // pairs: L2-prefetch the next unit's A / B boxes
+  int ntn;             // N tiles per (row tile, particle) (single-CTA kernels; 0 = 1): B rows nt * nmma ...
 };
 
 struct FwdParams {
@@ -335,6 +357,16 @@ struct FwdParams {
   double* ll_part;
   int ll_slots;
   int dbg;  // DASMC_DEBUG_EPI: 1 = skip global stores, 2 = skip pass 2, 3 = skip the whole epilogue math
+  // EPI kHidden (a_l = act(acc)) / kBackDelta (delta_{l-1} = acc . act'(a_{l-1})) of the
+  // deep-MLP path: outputs in row-major [J][Mcap][out_ld] (optional) and row-blocked
+  // transposed [J][nblk = ldm][out_rows][128] form, tf32-rounded (GEMM operands)
+  float* out_row;
+  int64_t out_ld, Mcap;
+  float* out_T;
+  int out_rows, n_valid;
+  const float* mask_src;  // kBackDelta: a_{l-1} row-major [J][Mcap][mask_ld]
+  int64_t mask_ld;
+  float* out_row_lo;      // split-tf32 low part of out_row (kBackDelta chains), optional
 };
 
 struct DwParams {
@@ -372,7 +404,7 @@ struct ClusterShape {
   static constexpr int kSize = kPair ? 2 * QA * QB : 1;
 };
 
-template <int EPI, bool SPLIT, bool A3D, int CP, int ACT, int CL>
+template <int EPI, bool SPLIT, int AM, int CP, int ACT, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
               const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo, TileParams tp,
@@ -452,7 +484,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  const int ntiles = tp.rtiles * tp.J;  // scheduling units (row-tile pairs x particles when PAIR)
+  const int ntn = tp.ntn > 0 ? tp.ntn : 1;
+  const int ntiles = tp.rtiles * tp.J * ntn;  // scheduling units (row-tile pairs x particles when PAIR)
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -469,8 +502,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_a = l2_policy(tp.hint_a), pol_b = l2_policy(tp.hint_b);
       for (int t = unit0; t < ntiles; t += ustride) {
         int ru, j;
-        tile_coords(tp, t, ru, j);
+        const int nt = t % ntn;
+        tile_coords(tp, t / ntn, ru, j);
         const int rt = PAIR ? 2 * (QB * ru + qb) + (int)prank : ru;
+        const int bn0 = nt * tp.nmma;  // first B row of this N tile
         if (PAIR) j = QA * j + qa;
         // warm L2 with the next unit's operands while this unit streams (pairs, no multicast)
         int pf_rt = -1, pf_j = 0;
@@ -510,19 +545,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_expect_tx(&full[s], tp.stage_bytes_tx);
             // row-blocked operands [J][blk][rows][128] (K = window rows): 4-D coordinates
             // (k within block, row, block, particle); a 32-wide k block never straddles blocks
-            if (A3D) {
+            if (AM == kABlocked) {
               tma_4d(A_of(s, 0), &mapA, &full[s], k0 & 127, rt * BM, k0 >> 7, j);
               if (SPLIT) tma_4d(A_of(s, 1), &mapAlo, &full[s], k0 & 127, rt * BM, k0 >> 7, j);
+            } else if (AM == kARowMajor) {
+              tma_3d(A_of(s, 0), &mapA, &full[s], k0, rt * BM, j);
+              if (SPLIT) tma_3d(A_of(s, 1), &mapAlo, &full[s], k0, rt * BM, j);
             } else {
               tma_2d(A_of(s, 0), &mapA, &full[s], k0, rt * BM);
               if (SPLIT) tma_2d(A_of(s, 1), &mapAlo, &full[s], k0, rt * BM);
             }
             if (EPI == kEpiKindDw) {
-              tma_4d(B_of(s, 0), &mapB, &full[s], k0 & 127, 0, k0 >> 7, j);
-              if (SPLIT) tma_4d(B_of(s, 1), &mapBlo, &full[s], k0 & 127, 0, k0 >> 7, j);
+              tma_4d(B_of(s, 0), &mapB, &full[s], k0 & 127, bn0, k0 >> 7, j);
+              if (SPLIT) tma_4d(B_of(s, 1), &mapBlo, &full[s], k0 & 127, bn0, k0 >> 7, j);
             } else {
-              tma_3d(B_of(s, 0), &mapB, &full[s], k0, 0, j);
-              if (SPLIT) tma_3d(B_of(s, 1), &mapBlo, &full[s], k0, 0, j);
+              tma_3d(B_of(s, 0), &mapB, &full[s], k0, bn0, j);
+              if (SPLIT) tma_3d(B_of(s, 1), &mapBlo, &full[s], k0, bn0, j);
             }
           }
           if (++s == tp.stages) {
@@ -629,7 +667,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     for (int t = unit0; t < ntiles; t += ustride) {
       int rt, j;
-      tile_coords(tp, t, rt, j);
+      const int nt = t % ntn;
+      tile_coords(tp, t / ntn, rt, j);
       if (PAIR) {
         rt = 2 * (QB * rt + qb) + (int)prank;
         j = QA * j + qa;
@@ -879,6 +918,77 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         ll_pending = fp.ll_part + ((int64_t)j * fp.ll_slots + rt) * 2;
+      } else if (EPI == kEpiKindHidden || EPI == kEpiKindBackDelta) {
+        // deep-MLP epilogues (network.hpp:159-178, 208-216): row m of the tile, columns
+        // o = nt * nmma + ...; rows past the window hold act(0) = 0 / masked zeros
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(lg * 32) << 16);
+        const int64_t m = (int64_t)rt * BM + row_in_tile;
+        const bool valid = m < fp.M;
+        const int64_t nblk = fp.ldm;
+        const int nb0 = nt * tp.nmma;
+        int c_lo, c_hi;
+        chunk_range(tp.nmma >> 4, c_lo, c_hi);
+        for (int ch = c_lo; ch < c_hi; ++ch) {
+          const int o0 = nb0 + ch * 16;
+          const int nq = min(16, fp.n_valid - o0);  // warp-uniform
+          float v[16];
+          tmem_ld16(taddr + ch * 16, v);
+          if (nq <= 0) continue;
+          if (EPI == kEpiKindHidden) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = tf32_hi(ACT == DASMC_RELU ? fmaxf(v[q], 0.f) : tanhf(v[q]));
+          } else {
+            float a[16];
+            const float* src = fp.mask_src + ((int64_t)j * fp.Mcap + m) * fp.mask_ld + o0;
+            if (valid && nq == 16 && (fp.mask_ld & 3) == 0) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float4 x = reinterpret_cast<const float4*>(src)[u];
+                a[4 * u] = x.x;
+                a[4 * u + 1] = x.y;
+                a[4 * u + 2] = x.z;
+                a[4 * u + 3] = x.w;
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < 16; ++q) a[q] = (valid && q < nq) ? src[q] : 0.f;
+            }
+            float lo[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const float dv = valid ? v[q] * (ACT == DASMC_RELU ? (a[q] > 0.f ? 1.f : 0.f) : 1.f - a[q] * a[q]) : 0.f;
+              v[q] = tf32_hi(dv);
+              lo[q] = dv - v[q];
+            }
+            if (fp.out_row_lo && valid) {
+              float* dst = fp.out_row_lo + ((int64_t)j * fp.Mcap + m) * fp.out_ld + o0;
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                if (q < nq) dst[q] = lo[q];
+            }
+          }
+          if (fp.out_row && valid) {
+            float* dst = fp.out_row + ((int64_t)j * fp.Mcap + m) * fp.out_ld + o0;
+            if (nq == 16 && (fp.out_ld & 3) == 0) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                reinterpret_cast<float4*>(dst)[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                if (q < nq) dst[q] = v[q];
+            }
+          }
+          if (fp.out_T) {
+            float* dT = fp.out_T + (((int64_t)j * nblk + rt) * fp.out_rows + o0) * 128 + row_in_tile;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (q < nq) dT[(int64_t)q * 128] = v[q];
+          }
+        }
+        release_acc(acc);
       } else {
         // weight-gradient tile: row i of A (input index, `in` = bias row), columns o
         mbar_wait(&tfull[acc], aph);
@@ -887,21 +997,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int i = rt * BM + row_in_tile;
         const bool valid = i <= dp.in;
         const int64_t base = (int64_t)j * dp.Dp;
+        const int nb0 = nt * tp.nmma;
         int c_lo, c_hi;
-        chunk_range((dp.n_out + 15) >> 4, c_lo, c_hi);
+        chunk_range(min(tp.nmma, dp.n_out - nb0 + 15) >> 4, c_lo, c_hi);
         for (int ch = c_lo; ch < c_hi; ++ch) {
-          const int o0 = ch * 16;
+          const int o0 = nb0 + ch * 16;
           float v[16];
-          tmem_ld16(taddr + o0, v);
+          tmem_ld16(taddr + ch * 16, v);
           if (valid) {
+            int64_t idx[16];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const int o = o0 + q;
-              if (o < dp.n_out) {
-                const int64_t idx = base + (i < dp.in ? dp.woff + (int64_t)o * dp.in + i : dp.boff + o);
-                leapfrog_update(dp.e, j, idx, v[q]);
-              }
-            }
+            for (int q = 0; q < 16; ++q)
+              idx[q] = base + (i < dp.in ? dp.woff + (int64_t)(o0 + q) * dp.in + i : dp.boff + o0 + q);
+            leapfrog_update_n<16>(dp.e, j, idx, v, min(16, dp.n_out - o0));
           }
         }
         release_acc(acc);
@@ -966,15 +1074,175 @@ __global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n
 // W1hi[j][o] = [W1[o], b1[o], 0 ...] (row stride kx) rounded to tf32, + lo part.
 __global__ void split_w1_kernel(const float* __restrict__ theta, int64_t Dp, int64_t woff, int64_t boff, int n0,
                                 int64_t kx, int64_t cnt, int64_t J, float* hi, float* lo) {
-  const int64_t total = J * cnt;  // cnt = n1 * kx
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = g / cnt, r = g - j * cnt;
-    const int64_t o = r / kx, i = r - o * kx;
+  // one block per output row (j, o): coalesced row copies, no per-element divisions
+  const int64_t n1 = cnt / kx, nrows = J * n1;
+  for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const int64_t j = row / n1, o = row - j * n1;
     const float* th = theta + j * Dp;
-    const float v = i < n0 ? th[woff + o * n0 + i] : (i == n0 ? th[boff + o] : 0.f);
-    const float h = tf32_hi(v);
-    hi[g] = h;
-    if (lo) lo[g] = v - h;
+    const float* src = th + woff + o * n0;
+    for (int64_t i = threadIdx.x; i < kx; i += blockDim.x) {
+      const float v = i < n0 ? src[i] : (i == n0 ? th[boff + o] : 0.f);
+      const float h = tf32_hi(v);
+      hi[row * kx + i] = h;
+      if (lo) lo[row * kx + i] = v - h;
+    }
+  }
+}
+
+// WT[j][i][o] = tf32(W_l[o][i]) (internal W row-major [out][in] at woff), row stride ldt.
+__global__ void transpose_w_kernel(const float* __restrict__ theta, int64_t Dp, int64_t woff, int in, int out,
+                                   int64_t ldt, int64_t J, float* __restrict__ WT, float* __restrict__ WTlo) {
+  __shared__ float tile[32][33];
+  const int64_t j = blockIdx.z;
+  const int o0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+  const float* W = theta + j * Dp + woff;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int o = o0 + r, i = i0 + threadIdx.x;
+    tile[r][threadIdx.x] = (o < out && i < in) ? W[(int64_t)o * in + i] : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int i = i0 + r, o = o0 + threadIdx.x;
+    if (i < in && o < out) {
+      const float v = tile[threadIdx.x][r], h = tf32_hi(v);
+      WT[(j * in + i) * ldt + o] = h;
+      if (WTlo) WTlo[(j * in + i) * ldt + o] = v - h;
+    }
+  }
+}
+
+// Column `col` of a row-major [J*rows][ld] buffer set to v (the bias-folding ones column).
+__global__ void fill_col_kernel(float* buf, int64_t nrows, int64_t ld, int64_t col, float v) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nrows; g += (int64_t)gridDim.x * blockDim.x)
+    buf[g * ld + col] = v;
+}
+
+// Output layer of the deep MLP on CUDA cores (network.hpp:174-193, 208-216): one thread
+// per window row of a 128-row tile of particle j.  z_L = W_L a_{L-1} + b_L from the
+// row-blocked a_{L-1}^T (coalesced), fp64 log-softmax / ll partials (the fused
+// forward's slot layout), delta_L = w_m (onehot - softmax), delta_{L-1} = (W_L^T delta_L)
+// . act'(a_{L-1}); writes delta_L^T, delta_{L-1}^T (row-blocked) and delta_{L-1} row-major.
+template <int CP>
+__global__ void __launch_bounds__(128) head_kernel(
+    const float* __restrict__ aT, int n_in, int C, int64_t nblk, const float* __restrict__ theta, int64_t Dp,
+    int64_t woff, int64_t boff, int act, const int32_t* __restrict__ y, int64_t M, int64_t P, float beta_rows,
+    int need_grad, double* __restrict__ ll_part, int ll_slots, float* __restrict__ dLT, float* __restrict__ dT,
+    float* __restrict__ dRow, float* __restrict__ dRowLo, int64_t ldd, int64_t Mcap) {
+  extern __shared__ float hs[];
+  float* Ws = hs;                    // [n_in][CP] = W_L transposed
+  float* bs = Ws + (size_t)n_in * CP;  // [CP]
+  __shared__ double red[8];
+  const int rt = blockIdx.x, r = threadIdx.x;
+  const int64_t j = blockIdx.y;
+  const float* th = theta + j * Dp;
+  for (int i = r; i < n_in * CP; i += 128) {
+    const int o = i / CP, c = i - o * CP;
+    Ws[i] = c < C ? th[woff + (int64_t)c * n_in + o] : 0.f;
+  }
+  if (r < CP) bs[r] = r < C ? th[boff + r] : 0.f;
+  __syncthreads();
+  const int64_t m = (int64_t)rt * 128 + r;
+  const bool valid = m < M;
+  const float* a = aT + (j * nblk + rt) * (int64_t)(n_in + 1) * 128 + r;
+  float z[CP];
+#pragma unroll
+  for (int c = 0; c < CP; ++c) z[c] = bs[c];
+  const float4* W4 = reinterpret_cast<const float4*>(Ws);
+  auto accum = [&](float v, int o) {
+#pragma unroll
+    for (int u = 0; u < CP / 4; ++u) {
+      const float4 w = W4[o * (CP / 4) + u];
+      z[4 * u] = fmaf(v, w.x, z[4 * u]);
+      z[4 * u + 1] = fmaf(v, w.y, z[4 * u + 1]);
+      z[4 * u + 2] = fmaf(v, w.z, z[4 * u + 2]);
+      z[4 * u + 3] = fmaf(v, w.w, z[4 * u + 3]);
+    }
+  };
+  int o = 0;
+  for (; o + 8 <= n_in; o += 8) {  // 8 loads in flight per thread
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = a[(int64_t)(o + q) * 128];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) accum(v[q], o + q);
+  }
+  for (; o < n_in; ++o) accum(a[(int64_t)o * 128], o);
+  double ll = 0.0;
+  float d[CP];
+#pragma unroll
+  for (int c = 0; c < CP; ++c) d[c] = 0.f;
+  if (valid) {
+    const int yi = y[m];
+    float mx = z[0];
+#pragma unroll
+    for (int c = 1; c < CP; ++c)
+      if (c < C) mx = fmaxf(mx, z[c]);
+    float e[CP];
+    double den = 0.0;
+    float zy = 0.f;
+#pragma unroll
+    for (int c = 0; c < CP; ++c) {
+      e[c] = c < C ? expf(z[c] - mx) : 0.f;
+      den += (double)e[c];
+      if (c == yi) zy = z[c];
+    }
+    ll = (double)zy - ((double)mx + log(den));
+    const float wrow = m < P ? 1.f : beta_rows;
+    const float rden = (float)(1.0 / den);
+#pragma unroll
+    for (int c = 0; c < CP; ++c)
+      if (c < C) d[c] = wrow * ((c == yi ? 1.f : 0.f) - e[c] * rden);
+  }
+  if (need_grad) {
+    float* lt = dLT + (j * nblk + rt) * (int64_t)C * 128 + r;
+    for (int c = 0; c < C; ++c) lt[(int64_t)c * 128] = tf32_hi(d[c]);
+    float* dt = dT + (j * nblk + rt) * (int64_t)n_in * 128 + r;
+    float* dr = dRow ? dRow + (j * Mcap + m) * ldd : nullptr;
+    float* drl = dRowLo ? dRowLo + (j * Mcap + m) * ldd : nullptr;
+    for (int o0 = 0; o0 < n_in; o0 += 8) {
+      float av[8], g[8];
+      const int nq = min(8, n_in - o0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) av[q] = q < nq ? a[(int64_t)(o0 + q) * 128] : 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float sacc = 0.f;
+#pragma unroll
+        for (int u = 0; u < CP / 4; ++u) {
+          const float4 w = W4[(o0 + q < n_in ? o0 + q : 0) * (CP / 4) + u];
+          sacc = fmaf(d[4 * u], w.x, sacc);
+          sacc = fmaf(d[4 * u + 1], w.y, sacc);
+          sacc = fmaf(d[4 * u + 2], w.z, sacc);
+          sacc = fmaf(d[4 * u + 3], w.w, sacc);
+        }
+        g[q] = sacc * (act == DASMC_RELU ? (av[q] > 0.f ? 1.f : 0.f) : 1.f - av[q] * av[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < nq) {
+          const float h = tf32_hi(g[q]);
+          dt[(int64_t)(o0 + q) * 128] = h;
+          if (dr) dr[o0 + q] = h;
+          if (drl) drl[o0 + q] = g[q] - h;
+        }
+    }
+  }
+  // per-tile prefix / block partials in a fixed order
+  double pre = (valid && m < P) ? ll : 0.0, blk = (valid && m >= P) ? ll : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    blk += __shfl_xor_sync(0xffffffffu, blk, o);
+  }
+  if ((r & 31) == 0) {
+    red[(r >> 5) * 2] = pre;
+    red[(r >> 5) * 2 + 1] = blk;
+  }
+  __syncthreads();
+  if (r == 0) {
+    double* o = ll_part + (j * ll_slots + rt) * 2;
+    o[0] = red[0] + red[2] + red[4] + red[6];
+    o[1] = red[1] + red[3] + red[5] + red[7];
   }
 }
 
@@ -1055,7 +1323,7 @@ int round16(int v) { return (v + 15) / 16 * 16; }
 // CL >= 1: tp.rtiles counts row groups (2 QB tiles) and tp.J particle groups (QA
 // particles); B's TMA box is tp.nmma / 2 rows per CTA (tp.bbox rows per piece
 // when QB = 2; tp.brows is ignored) and the grid is launched as clusters.
-template <int EPI, bool SPLIT, bool A3D, int CP = 4, int ACT = 0, int CL = 0>
+template <int EPI, bool SPLIT, int AM, int CP = 4, int ACT = 0, int CL = 0>
 void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUtensorMap& B, const CUtensorMap& Blo,
                TileParams tp, const FwdParams& fp, const DwParams& dp, size_t epi_smem_bytes) {
   using CS_ = ClusterShape<CL>;
@@ -1075,7 +1343,7 @@ void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUten
     tp.stage_bytes_tx = (uint32_t)(sub * ((size_t)BM * BK * 4 + (size_t)tp.brows * BK * 4));
   }
   const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16 + epi_smem_bytes + 64;
-  auto kern = tc_kernel<EPI, SPLIT, A3D, CP, ACT, CL>;
+  auto kern = tc_kernel<EPI, SPLIT, AM, CP, ACT, CL>;
   static bool attr_set = false;
   static int max_clusters = 0;
   cudaLaunchConfig_t cfg{};
@@ -1100,7 +1368,7 @@ void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUten
     }
     attr_set = true;
   }
-  const int ntiles = tp.rtiles * tp.J;
+  const int ntiles = tp.rtiles * tp.J * std::max(tp.ntn, 1);
   if (CS_::kPair) {
     const int nclusters = std::max(1, std::min(ntiles, max_clusters));
     cfg.gridDim = dim3((unsigned)(CS_::kSize * nclusters));
@@ -1116,12 +1384,21 @@ void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUten
 
 bool tc_layer1_eligible(const Ctx& c) {
   const NetDev& n = c.net;
-  return n.nconv == 0 && n.L == 2 && n.sizes[0] % 4 == 0 && n.sizes[0] >= 4 && n.sizes[1] <= 256 && n.sizes[2] <= 16;
+  if (n.nconv != 0) return false;
+  if (n.L == 2) return n.sizes[0] % 4 == 0 && n.sizes[0] >= 4 && n.sizes[1] <= 256 && n.sizes[2] <= 16;
+  // deep path (tc_eval_deep): tf32, <= 16 classes, output layer weights in shared memory
+  if (c.precision != DASMC_PREC_TF32 || n.sizes[n.L] > 16 || (int64_t)n.sizes[n.L - 1] * 16 > 16384) return false;
+  for (int l = 0; l < n.L; ++l)
+    if (n.sizes[l] > 8192) return false;
+  return true;
 }
 
 void tc_init(Ctx& c) {
   auto* s = new TcState();
   c.tc = s;
+  s->deep = c.net.L >= 3;
+  s->L = c.net.L;
+  for (int l = 0; l <= c.net.L; ++l) s->sz[l] = c.net.sizes[l];
   s->n0 = c.net.sizes[0];
   s->n1 = c.net.sizes[1];
   s->C = c.net.sizes[2];
@@ -1136,7 +1413,22 @@ void tc_init(Ctx& c) {
   s->kx = (s->n0 + 1 + 3) / 4 * 4;
   const size_t w = (size_t)c.Jmax * s->n1 * s->kx;
   CK(cudaMalloc(&s->Xhi, sizeof(float) * (size_t)c.n * s->kx));
-  CK(cudaMalloc(&s->W1hi, sizeof(float) * w));
+  if (s->deep) {
+    s->kxl[0] = s->kx;
+    for (int l = 1; l <= s->L; ++l) {
+      s->kxl[l] = (s->sz[l] + 1 + 3) / 4 * 4;
+      s->ldd[l] = (s->sz[l] + 3) / 4 * 4;
+    }
+    for (int l = 1; l < s->L; ++l)
+      CK(cudaMalloc(&s->Whi[l], sizeof(float) * (size_t)c.Jmax * s->sz[l] * s->kxl[l - 1]));
+    for (int l = 2; l < s->L; ++l) {
+      CK(cudaMalloc(&s->WThi[l], sizeof(float) * (size_t)c.Jmax * s->sz[l - 1] * s->ldd[l]));
+      if (kDeepSplitBack) CK(cudaMalloc(&s->WTlo[l], sizeof(float) * (size_t)c.Jmax * s->sz[l - 1] * s->ldd[l]));
+    }
+    s->W1hi = s->Whi[1];
+  } else {
+    CK(cudaMalloc(&s->W1hi, sizeof(float) * w));
+  }
   if (s->split) {
     CK(cudaMalloc(&s->Xtlo, sizeof(float) * xt));
     CK(cudaMalloc(&s->Xlo, sizeof(float) * (size_t)c.n * s->kx));
@@ -1152,9 +1444,15 @@ void tc_init(Ctx& c) {
 void tc_free(Ctx& c) {
   TcState* s = c.tc;
   if (!s) return;
+  if (s->deep) s->W1hi = nullptr;  // owned through Whi[1]
   float* p[] = {s->Xt, s->Xhi, s->Xlo, s->Xtlo, s->W1hi, s->W1lo, s->a1T, s->d1T, s->d2T, s->a1Tlo, s->d1Tlo, s->d2Tlo};
   for (float* q : p)
     if (q) cudaFree(q);
+  for (int l = 0; l <= kMaxLayers; ++l) {
+    float* d[] = {s->Whi[l], s->WThi[l], s->WTlo[l], s->aRow[l], s->aT[l], s->dRow[l], s->dRowLo[l], s->dTl[l]};
+    for (float* q : d)
+      if (q) cudaFree(q);
+  }
   delete s;
   c.tc = nullptr;
 }
@@ -1162,6 +1460,36 @@ void tc_free(Ctx& c) {
 void tc_ensure_rows(Ctx& c, int64_t Mcap) {
   TcState* s = c.tc;
   if (Mcap <= s->mcap) return;
+  if (s->deep) {
+    const size_t J = (size_t)c.Jmax;
+    for (int l = 0; l <= kMaxLayers; ++l) {
+      float** d[] = {&s->aRow[l], &s->aT[l], &s->dRow[l], &s->dRowLo[l], &s->dTl[l]};
+      for (float** q : d)
+        if (*q) {
+          CK(cudaFree(*q));
+          *q = nullptr;
+        }
+    }
+    for (int l = 1; l <= s->L; ++l) {
+      if (l < s->L) {
+        CK(cudaMalloc(&s->aRow[l], sizeof(float) * J * Mcap * s->kxl[l]));
+        CK(cudaMalloc(&s->aT[l], sizeof(float) * J * (s->sz[l] + 1) * Mcap));
+        fill_col_kernel<<<(unsigned)std::min<int64_t>((J * Mcap + 255) / 256, 148 * 16), 256, 0, c.stream>>>(
+            s->aRow[l], (int64_t)(J * Mcap), s->kxl[l], s->sz[l], 1.f);
+        LAUNCHED();
+        fill_ones_row_kernel<<<(unsigned)std::min<int64_t>((J * Mcap + 255) / 256, 148 * 16), 256, 0, c.stream>>>(
+            s->aT[l], (int64_t)J, s->sz[l] + 1, s->sz[l], Mcap, 1.f);
+        LAUNCHED();
+      }
+      if (l >= 2 && l < s->L) {
+        CK(cudaMalloc(&s->dRow[l], sizeof(float) * J * Mcap * s->ldd[l]));
+        if (kDeepSplitBack) CK(cudaMalloc(&s->dRowLo[l], sizeof(float) * J * Mcap * s->ldd[l]));
+      }
+      CK(cudaMalloc(&s->dTl[l], sizeof(float) * J * s->sz[l] * Mcap));
+    }
+    s->mcap = Mcap;
+    return;
+  }
   float** bufs[] = {&s->a1T, &s->d1T, &s->d2T, &s->a1Tlo, &s->d1Tlo, &s->d2Tlo};
   for (float** b : bufs)
     if (*b) {
@@ -1187,9 +1515,167 @@ void tc_ensure_rows(Ctx& c, int64_t Mcap) {
   }
 }
 
+// Deep MLP (>= 2 hidden layers) on the tensor cores: per hidden layer a GEMM with the
+// bias folded into K and the activation epilogue (a_l row-major + transposed); the output
+// layer + softmax + delta_L + delta_{L-1} on CUDA cores (head_kernel); backward deltas as
+// GEMMs against W_l^T with the act' epilogue; weight gradients as K = window-row GEMMs
+// with the fused leapfrog (the fused one-hidden-layer path's Dw kernel, N-tiled).
+void tc_eval_deep(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, double beta_rows, bool need_grad,
+                  const EpiParams* epi) {
+  TcState* s = c.tc;
+  const NetDev& net = c.net;
+  const int L = s->L;
+  const int64_t Mcap = s->mcap, nba = Mcap / 128, nbu = (M + 127) / 128;
+  const int rtiles = (int)((M + BM - 1) / BM);
+  auto ntiles_n = [](int n) { return (n + 255) / 256; };
+  auto nmma_of = [&](int n) { return round16((n + ntiles_n(n) - 1) / ntiles_n(n)); };
+  DwParams dp0{};
+  // per-evaluation operand copies: [W_l, b_l] (tf32, bias column) and W_l^T (tf32)
+  for (int l = 1; l < L; ++l) {
+    const LayerDev& ly = net.layer[l - 1];
+    const int64_t cnt = (int64_t)s->sz[l] * s->kxl[l - 1];
+    split_w1_kernel<<<(int)std::min<int64_t>(J * s->sz[l], 148 * 64), 256, 0, c.stream>>>(
+        theta_in, net.Dp, ly.woff, ly.boff, s->sz[l - 1], s->kxl[l - 1], cnt, J, s->Whi[l], nullptr);
+    LAUNCHED();
+  }
+  if (need_grad)
+    for (int l = 2; l < L; ++l) {
+      dim3 grid((unsigned)((s->sz[l] + 31) / 32), (unsigned)((s->sz[l - 1] + 31) / 32), (unsigned)J);
+      transpose_w_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(theta_in, net.Dp, net.layer[l - 1].woff, s->sz[l - 1],
+                                                             s->sz[l], s->ldd[l], J, s->WThi[l], s->WTlo[l]);
+      LAUNCHED();
+    }
+  auto act_go = [&](auto fn) {
+    if (net.act == DASMC_RELU)
+      fn(std::integral_constant<int, DASMC_RELU>{});
+    else
+      fn(std::integral_constant<int, DASMC_TANH>{});
+  };
+  // forward through the hidden layers
+  for (int l = 1; l < L; ++l) {
+    const int nin = s->sz[l - 1], nout = s->sz[l], ntn = ntiles_n(nout), nm = nmma_of(nout);
+    const CUtensorMap A = l == 1 ? map2d(s->Xhi, nin + 1, M, s->kxl[0], BM)
+                                 : map3d(s->aRow[l - 1], nin + 1, M, s->kxl[l - 1], J, Mcap * s->kxl[l - 1], BM);
+    const CUtensorMap B = map3d(s->Whi[l], nin + 1, nout, s->kxl[l - 1], J, (uint64_t)nout * s->kxl[l - 1], nm);
+    TileParams tp{};
+    tp.rtiles = rtiles;
+    tp.J = (int)J;
+    tp.rg = 32;
+    tp.nkb = (nin + 1 + BK - 1) / BK;
+    tp.nmma = nm;
+    tp.brows = nm;
+    tp.ntn = ntn;
+    FwdParams fp{};
+    fp.M = M;
+    fp.Mcap = Mcap;
+    fp.ldm = nba;
+    fp.out_row = s->aRow[l];
+    fp.out_ld = s->kxl[l];
+    fp.out_T = s->aT[l];
+    fp.out_rows = nout + 1;
+    fp.n_valid = nout;
+    act_go([&](auto a) {
+      constexpr int A_ = decltype(a)::value;
+      if (l == 1)
+        launch_tc<kEpiKindHidden, false, kAShared, 4, A_>(c, A, A, B, B, tp, fp, dp0, 0);
+      else
+        launch_tc<kEpiKindHidden, false, kARowMajor, 4, A_>(c, A, A, B, B, tp, fp, dp0, 0);
+    });
+  }
+  // output layer, log-softmax, delta_L, delta_{L-1} (CUDA cores)
+  {
+    const int nin = s->sz[L - 1], C = s->sz[L];
+    const LayerDev& ly = net.layer[L - 1];
+    dim3 grid((unsigned)rtiles, (unsigned)J);
+    auto go = [&](auto cp) {
+      constexpr int CPv = decltype(cp)::value;
+      const size_t sm = sizeof(float) * ((size_t)nin * CPv + CPv);
+      auto kern = head_kernel<CPv>;
+      static bool attr = false;
+      if (!attr) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        attr = true;
+      }
+      kern<<<grid, 128, sm, c.stream>>>(s->aT[L - 1], nin, C, nba, theta_in, net.Dp, ly.woff, ly.boff, net.act, c.y,
+                                        M, P, (float)beta_rows, need_grad ? 1 : 0, c.ll_part, c.ll_slots, s->dTl[L],
+                                        s->dTl[L - 1], L - 1 >= 2 ? s->dRow[L - 1] : nullptr,
+                                        L - 1 >= 2 ? s->dRowLo[L - 1] : nullptr, s->ldd[L - 1], Mcap);
+      LAUNCHED();
+    };
+    if (C <= 4)
+      go(std::integral_constant<int, 4>{});
+    else if (C <= 12)
+      go(std::integral_constant<int, 12>{});
+    else
+      go(std::integral_constant<int, 16>{});
+  }
+  if (!need_grad) return;
+  // backward deltas: delta_{l-1} = (delta_l W_l) . act'(a_{l-1})
+  for (int l = L - 1; l >= 2; --l) {
+    const int nk = s->sz[l], nout = s->sz[l - 1], ntn = ntiles_n(nout), nm = nmma_of(nout);
+    const CUtensorMap A = map3d(s->dRow[l], nk, M, s->ldd[l], J, Mcap * s->ldd[l], BM);
+    const CUtensorMap Alo = kDeepSplitBack ? map3d(s->dRowLo[l], nk, M, s->ldd[l], J, Mcap * s->ldd[l], BM) : A;
+    const CUtensorMap B = map3d(s->WThi[l], nk, nout, s->ldd[l], J, (uint64_t)nout * s->ldd[l], nm);
+    const CUtensorMap Blo =
+        kDeepSplitBack ? map3d(s->WTlo[l], nk, nout, s->ldd[l], J, (uint64_t)nout * s->ldd[l], nm) : B;
+    TileParams tp{};
+    tp.rtiles = rtiles;
+    tp.J = (int)J;
+    tp.rg = 32;
+    tp.nkb = (nk + BK - 1) / BK;
+    tp.nmma = nm;
+    tp.brows = nm;
+    tp.ntn = ntn;
+    FwdParams fp{};
+    fp.M = M;
+    fp.Mcap = Mcap;
+    fp.ldm = nba;
+    fp.out_row = l - 1 >= 2 ? s->dRow[l - 1] : nullptr;
+    fp.out_row_lo = l - 1 >= 2 ? s->dRowLo[l - 1] : nullptr;
+    fp.out_ld = s->ldd[l - 1];
+    fp.out_T = s->dTl[l - 1];
+    fp.out_rows = nout;
+    fp.n_valid = nout;
+    fp.mask_src = s->aRow[l - 1];
+    fp.mask_ld = s->kxl[l - 1];
+    act_go([&](auto a) {
+      constexpr int A_ = decltype(a)::value;
+      launch_tc<kEpiKindBackDelta, kDeepSplitBack, kARowMajor, 4, A_>(c, A, Alo, B, Blo, tp, fp, dp0, 0);
+    });
+  }
+  // weight gradients + fused leapfrog: dW_l^T[i, o] = sum_m a_{l-1}^T[i, m] delta_l^T[o, m]
+  FwdParams fp0{};
+  for (int l = L; l >= 1; --l) {
+    KTimer kt(c, l == 1 ? 1 : -1);
+    const int nin = s->sz[l - 1], nout = s->sz[l], ntn = ntiles_n(nout), nm = nmma_of(nout);
+    const CUtensorMap B = map_blk(s->dTl[l], nout, nbu, nba, J, nm);
+    TileParams tp{};
+    tp.rtiles = (nin + 1 + BM - 1) / BM;
+    tp.J = (int)J;
+    tp.rg = tp.rtiles;
+    tp.nkb = (int)((M + BK - 1) / BK);
+    tp.nmma = nm;
+    tp.brows = nm;
+    tp.ntn = ntn;
+    const LayerDev& ly = net.layer[l - 1];
+    DwParams dp{*epi, net.Dp, ly.woff, ly.boff, nin, nout};
+    if (l == 1) {
+      const CUtensorMap A = map2d(s->Xt, M, nin + 1, s->n_pad, BM);
+      launch_tc<kEpiKindDw, false, kAShared>(c, A, A, B, B, tp, fp0, dp, 0);
+    } else {
+      const CUtensorMap A = map_blk(s->aT[l - 1], nin + 1, nbu, nba, J, BM);
+      launch_tc<kEpiKindDw, false, kABlocked>(c, A, A, B, B, tp, fp0, dp, 0);
+    }
+  }
+}
+
 void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, double beta_rows, bool need_grad,
              const EpiParams* epi) {
   TcState* s = c.tc;
+  if (s->deep) {
+    tc_eval_deep(c, theta_in, J, M, P, beta_rows, need_grad, epi);
+    return;
+  }
   const NetDev& net = c.net;
   const LayerDev& l1 = net.layer[0];
   const LayerDev& l2 = net.layer[1];
@@ -1203,7 +1689,7 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     // [W1, b1] -> tf32 (rna) hi [+ lo]: the MMA would otherwise truncate the low mantissa
     // bits; the bias rides along as K column n0 against X's ones column
     const int64_t kx = s->kx, cnt = (int64_t)n1 * kx;
-    split_w1_kernel<<<(int)std::min<int64_t>((J * cnt + 255) / 256, 148 * 16), 256, 0, c.stream>>>(
+    split_w1_kernel<<<(int)std::min<int64_t>(J * n1, 148 * 64), 256, 0, c.stream>>>(
         theta_in, net.Dp, l1.woff, l1.boff, n0, kx, cnt, J, s->W1hi, s->split ? s->W1lo : nullptr);
     LAUNCHED();
     // rows >= M of X are TMA zero fill (ones column included): z1 = 0 there
@@ -1266,16 +1752,16 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
       constexpr int K = decltype(cp)::value, A_ = decltype(act)::value;
       if (s->split) {
         if (pair)
-          launch_tc<kEpiKindFwd, true, false, K, A_, 1>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+          launch_tc<kEpiKindFwd, true, kAShared, K, A_, 1>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
         else
-          launch_tc<kEpiKindFwd, true, false, K, A_, 0>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+          launch_tc<kEpiKindFwd, true, kAShared, K, A_, 0>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
       } else {
         switch (cl) {
-          case 0: launch_tc<kEpiKindFwd, false, false, K, A_, 0>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
-          case 1: launch_tc<kEpiKindFwd, false, false, K, A_, 1>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
-          case 2: launch_tc<kEpiKindFwd, false, false, K, A_, 2>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
-          case 3: launch_tc<kEpiKindFwd, false, false, K, A_, 3>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
-          default: launch_tc<kEpiKindFwd, false, false, K, A_, 4>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+          case 0: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 0>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+          case 1: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 1>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+          case 2: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 2>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+          case 3: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 3>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+          default: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 4>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
         }
       }
     };
@@ -1309,9 +1795,9 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     tp.brows = C;
     DwParams dp{*epi, net.Dp, l2.woff, l2.boff, n1, C};
     if (s->split)
-      launch_tc<kEpiKindDw, true, true>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+      launch_tc<kEpiKindDw, true, kABlocked>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
     else
-      launch_tc<kEpiKindDw, false, true>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+      launch_tc<kEpiKindDw, false, kABlocked>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
   }
   // ---- layer 1: dW1^T[i, o] = sum_m X^T[i, m] delta1^T[o, m]  (ones row i = n0 -> db1)
   {
@@ -1330,9 +1816,9 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     tp.brows = n1;
     DwParams dp{*epi, net.Dp, l1.woff, l1.boff, n0, n1};
     if (s->split)
-      launch_tc<kEpiKindDw, true, false>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+      launch_tc<kEpiKindDw, true, kAShared>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
     else
-      launch_tc<kEpiKindDw, false, false>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+      launch_tc<kEpiKindDw, false, kAShared>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
   }
 }
 

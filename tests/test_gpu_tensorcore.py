@@ -112,3 +112,33 @@ def test_tc_cluster_shapes(product, oracle, cluster, monkeypatch):
     for j in range(J):
         mr, nr = errs(g[j], go[j])
         assert nr < 6e-3 and mr < 0.5, (cluster, j, mr, nr)
+
+
+@pytest.mark.parametrize("layers,act,M,J", [([64, 48, 32, 10], "tanh", 200, 5), ([784, 300, 200, 10], "relu", 333, 3),
+                                             ([3072, 512, 512, 10], "relu", 150, 2),
+                                             ([20, 40, 30, 20, 5], "relu", 77, 4)])
+def test_tc_deep_mlp(product, oracle, layers, act, M, J):
+    """Deep MLPs (C5 family) on the tensor-core chain: hidden GEMMs with the activation
+    epilogue, CUDA-core output head, backward-delta GEMMs, N-tiled weight gradients."""
+    n = max(M, 400)
+    spec, X, y = problem(product, layers, act, n)
+    D = product.param_count(spec)
+    th = (0.5 * np.random.default_rng(8).standard_normal((J, D)) / np.sqrt(3)).astype(np.float32).astype(np.float64)
+    t = product.GpuEnsembleTarget(spec, X, y, J, precision="tf32")
+    a = 0 if act == "relu" else 1
+    for mode, win, beta in (("scaled", (0, M, n), 1.0), ("sda", (M // 3, M, n), 0.4)):
+        t.set_target(*win, mode, beta, 1.0)
+        v, g = t.log_target_with_grad(th)
+        vo, go = oracle.value_and_grad(layers, a, X.astype(np.float64), y, win, 0 if mode == "scaled" else 1, beta,
+                                       1.0, th)
+        vrel = float(np.max(np.abs(v - vo) / np.abs(vo)))
+        assert vrel < 2e-4, (mode, vrel)
+        # Under the tf32 forward a few ReLU units near z = 0 switch sides against the fp64
+        # oracle; each flip is an O(1) error in that unit's delta, compounding with depth
+        # (DESIGN.md §4).  Bounds: normwise 6e-3 with two hidden layers, 3e-2 with more;
+        # elementwise |diff| < 5e-3 / 3e-2 of ||ref||_inf.
+        tn = 6e-3 if len(layers) <= 4 else 3e-2
+        for j in range(J):
+            nr = float(np.linalg.norm(g[j] - go[j]) / np.linalg.norm(go[j]))
+            ab = float(np.max(np.abs(g[j] - go[j])) / np.max(np.abs(go[j])))
+            assert nr < tn and ab < 5 * tn / 6, (mode, j, ab, nr)
