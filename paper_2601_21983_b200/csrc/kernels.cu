@@ -8,6 +8,7 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <stdexcept>
 
@@ -665,26 +666,56 @@ __device__ __forceinline__ float act_grad_post(float a, int act) {
   return act == DASMC_RELU ? (a > 0.f ? 1.f : 0.f) : 1.f - a * a;
 }
 
-__global__ void conv_fwd_kernel(ConvDev d, int act, const float* __restrict__ in, int64_t in_ps,
-                                const float* __restrict__ theta, int64_t Dp, float* __restrict__ A, int64_t a_ps,
-                                int64_t M, int64_t J) {
+// Register-tiled direct convolution: a block owns one image of one particle and CT output
+// channels; W for the tile sits in shared memory as [cin*k*k][CT] so one float4 load
+// feeds four FMAs; each thread owns output pixels and keeps CT accumulators.
+template <int K, int CT>
+__global__ void __launch_bounds__(128) conv_fwd_kernel(ConvDev d, int act, const float* __restrict__ in,
+                                                        int64_t in_ps, const float* __restrict__ theta, int64_t Dp,
+                                                        float* __restrict__ A, int64_t a_ps) {
+  extern __shared__ float4 cv_sh4[];
+  float* Ws = reinterpret_cast<float*>(cv_sh4);
+  __shared__ float bs[CT];
+  const int64_t m = blockIdx.x, j = blockIdx.z;
+  const int co0 = blockIdx.y * CT, KW = d.cin * K * K;
+  const float* W = theta + j * Dp + d.woff;
+  for (int i = threadIdx.x; i < KW * CT; i += blockDim.x) {
+    const int kidx = i / CT, c = i - kidx * CT;
+    Ws[i] = co0 + c < d.cout ? W[(int64_t)(co0 + c) * KW + kidx] : 0.f;
+  }
+  if (threadIdx.x < CT) bs[threadIdx.x] = co0 + (int)threadIdx.x < d.cout ? theta[j * Dp + d.boff + co0 + threadIdx.x] : 0.f;
+  __syncthreads();
   const int64_t in_img = (int64_t)d.cin * d.hin * d.win, per = (int64_t)d.cout * d.ho * d.wo;
-  const int64_t total = J * M * per;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = g / (M * per), r = g - j * M * per, m = r / per, o = r - m * per;
-    const int co = (int)(o / ((int64_t)d.ho * d.wo));
-    const int yx = (int)(o - (int64_t)co * d.ho * d.wo), y = yx / d.wo, x = yx - y * d.wo;
-    const float* w = theta + j * Dp + d.woff + (int64_t)co * d.cin * d.k * d.k;
-    const float* src = in + j * in_ps + m * in_img;
-    float acc = 0.f;
+  const float* src = in + j * in_ps + m * in_img;
+  float* dst = A + j * a_ps + m * per;
+  const int npix = d.ho * d.wo;
+  for (int p = threadIdx.x; p < npix; p += blockDim.x) {
+    const int y = p / d.wo, x = p - y * d.wo;
+    float acc[CT];
+#pragma unroll
+    for (int c = 0; c < CT; ++c) acc[c] = bs[c];
     for (int ci = 0; ci < d.cin; ++ci)
-      for (int ky = 0; ky < d.k; ++ky) {
+#pragma unroll
+      for (int ky = 0; ky < K; ++ky) {
         const float* srow = src + ((int64_t)ci * d.hin + y + ky) * d.win + x;
-        const float* wrow = w + ((int64_t)ci * d.k + ky) * d.k;
-        for (int kx = 0; kx < d.k; ++kx) acc = fmaf(wrow[kx], srow[kx], acc);
+        const float4* wrow = cv_sh4 + (int64_t)((ci * K + ky) * K) * (CT / 4);
+        float v[K];
+#pragma unroll
+        for (int kx = 0; kx < K; ++kx) v[kx] = srow[kx];
+#pragma unroll
+        for (int kx = 0; kx < K; ++kx)
+#pragma unroll
+          for (int u = 0; u < CT / 4; ++u) {
+            const float4 w = wrow[kx * (CT / 4) + u];
+            acc[4 * u] = fmaf(v[kx], w.x, acc[4 * u]);
+            acc[4 * u + 1] = fmaf(v[kx], w.y, acc[4 * u + 1]);
+            acc[4 * u + 2] = fmaf(v[kx], w.z, acc[4 * u + 2]);
+            acc[4 * u + 3] = fmaf(v[kx], w.w, acc[4 * u + 3]);
+          }
       }
-    acc += theta[j * Dp + d.boff + co];
-    A[j * a_ps + m * per + o] = act_apply(acc, act);
+#pragma unroll
+    for (int c = 0; c < CT; ++c)
+      if (co0 + c < d.cout) dst[(int64_t)(co0 + c) * npix + p] = act_apply(acc[c], act);
   }
 }
 
@@ -729,69 +760,160 @@ __global__ void pool_bwd_kernel(ConvDev d, int act, const float* __restrict__ A,
   }
 }
 
-// Weight gradient of one stage: one thread per (j, parameter); window sum with
-// fp32 per-image partials and an fp64 running total, then the fused leapfrog.
-__global__ void conv_dw_kernel(ConvDev d, const float* __restrict__ dZ, int64_t z_ps, const float* __restrict__ in,
-                               int64_t in_ps, int64_t Dp, int64_t M, int64_t J, EpiParams e) {
-  const int64_t nw = (int64_t)d.cout * d.cin * d.k * d.k, np = nw + d.cout;
-  const int64_t in_img = (int64_t)d.cin * d.hin * d.win, per = (int64_t)d.cout * d.ho * d.wo;
-  const int64_t total = J * np;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+// Weight gradient of one stage, pass 1: a block owns (particle j, input channel ci, CT
+// output channels, a chunk of kImgChunk window images); thread (c, ky) owns the k outputs
+// (c, ky, 0..k-1) and slides a k-wide register window along each input row (two shared-
+// memory loads per k FMAs).  Partial sums (fp32 per row, fp64 across rows and images) go
+// to part[j][chunk][param]; pass 2 (conv_dw_reduce_kernel) adds the chunks in order and
+// applies the fused leapfrog.
+constexpr int kImgChunk = 16;
+template <int K, int CT>
+__global__ void __launch_bounds__(128) conv_dw_kernel(ConvDev d, const float* __restrict__ dZ, int64_t z_ps,
+                                                       const float* __restrict__ in, int64_t in_ps, int64_t M,
+                                                       int64_t np, int nchunks, double* __restrict__ part) {
+  extern __shared__ float4 cv_sh4[];
+  float* in_s = reinterpret_cast<float*>(cv_sh4);           // [hin * win]
+  float* dz_s = in_s + ((d.hin * d.win + 3) & ~3);          // [CT][ho * wo]
+  const int ci = blockIdx.x, co0 = blockIdx.y * CT;
+  const int64_t j = blockIdx.z / nchunks;
+  const int chunk = blockIdx.z - (int)j * nchunks;
+  const int npix = d.ho * d.wo, nplane = d.hin * d.win;
+  const int t = threadIdx.x, c = t / K, ky = t - c * K;
+  const bool active = t < CT * K;
+  double tot[K];
+  double totb = 0.0;
+#pragma unroll
+  for (int q = 0; q < K; ++q) tot[q] = 0.0;
+  const int64_t in_img = (int64_t)d.cin * nplane, per = (int64_t)d.cout * npix;
+  const int64_t m0 = (int64_t)chunk * kImgChunk, m1 = min(M, m0 + kImgChunk);
+  for (int64_t m = m0; m < m1; ++m) {
+    __syncthreads();
+    const float* src = in + j * in_ps + m * in_img + (int64_t)ci * nplane;
+    for (int u = t; u < nplane; u += blockDim.x) in_s[u] = src[u];
+    const float* zsrc = dZ + j * z_ps + m * per + (int64_t)co0 * npix;
+    for (int u = t; u < CT * npix; u += blockDim.x) dz_s[u] = co0 + u / npix < d.cout ? zsrc[u] : 0.f;
+    __syncthreads();
+    if (!active) continue;
+    for (int y = 0; y < d.ho; ++y) {
+      const float* xr = in_s + (y + ky) * d.win;
+      const float* zr = dz_s + (c * d.ho + y) * d.wo;
+      float w[K], acc[K];
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        w[q] = xr[q];
+        acc[q] = 0.f;
+      }
+      float ab = 0.f;
+      for (int x = 0; x < d.wo; ++x) {
+        const float z = zr[x];
+#pragma unroll
+        for (int q = 0; q < K; ++q) acc[q] = fmaf(z, w[q], acc[q]);
+        ab += z;
+#pragma unroll
+        for (int q = 0; q + 1 < K; ++q) w[q] = w[q + 1];
+        w[K - 1] = x + K < d.win ? xr[x + K] : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < K; ++q) tot[q] += (double)acc[q];
+      totb += (double)ab;
+    }
+  }
+  if (!active || co0 + c >= d.cout) return;
+  double* o = part + ((int64_t)j * nchunks + chunk) * np;
+  const int64_t wbase = ((int64_t)(co0 + c) * d.cin + ci) * K * K + (int64_t)ky * K;
+#pragma unroll
+  for (int q = 0; q < K; ++q) o[wbase + q] = tot[q];
+  if (ci == 0 && ky == 0) o[(int64_t)d.cout * d.cin * K * K + co0 + c] = totb;
+}
+
+__global__ void conv_dw_reduce_kernel(ConvDev d, int64_t np, int nchunks, const double* __restrict__ part, int64_t J,
+                                      int64_t Dp, EpiParams e) {
+  const int64_t nw = np - d.cout;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < J * np; g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = g / np, q = g - j * np;
     double acc = 0.0;
-    if (q < nw) {
-      const int kx = (int)(q % d.k), ky = (int)((q / d.k) % d.k), ci = (int)((q / ((int64_t)d.k * d.k)) % d.cin);
-      const int co = (int)(q / ((int64_t)d.k * d.k * d.cin));
-      for (int64_t m = 0; m < M; ++m) {
-        const float* z = dZ + j * z_ps + m * per + (int64_t)co * d.ho * d.wo;
-        const float* src = in + j * in_ps + m * in_img + ((int64_t)ci * d.hin + ky) * d.win + kx;
-        float s = 0.f;
-        for (int y = 0; y < d.ho; ++y)
-          for (int x = 0; x < d.wo; ++x) s = fmaf(z[y * d.wo + x], src[(int64_t)y * d.win + x], s);
-        acc += (double)s;
-      }
-      leapfrog_update(e, (int)j, j * Dp + d.woff + q, (float)acc);
-    } else {
-      const int co = (int)(q - nw);
-      for (int64_t m = 0; m < M; ++m) {
-        const float* z = dZ + j * z_ps + m * per + (int64_t)co * d.ho * d.wo;
-        float s = 0.f;
-        for (int t = 0; t < d.ho * d.wo; ++t) s += z[t];
-        acc += (double)s;
-      }
-      leapfrog_update(e, (int)j, j * Dp + d.boff + co, (float)acc);
-    }
+    for (int ch = 0; ch < nchunks; ++ch) acc += part[((int64_t)j * nchunks + ch) * np + q];
+    leapfrog_update(e, (int)j, j * Dp + (q < nw ? d.woff + q : d.boff + (q - nw)), (float)acc);
   }
 }
 
 // Input delta of a stage (transposed convolution), in place over the previous stage
 // output `io` (read for the mask first): delta = sum dz * W, times act'(io) unless the
-// previous stage pools (its pool backward applies act' at the argmax instead).
-__global__ void conv_dx_kernel(ConvDev d, int act, int apply_act, const float* __restrict__ dZ, int64_t z_ps,
-                               const float* __restrict__ theta, int64_t Dp, float* io, int64_t io_ps, int64_t M,
-                               int64_t J) {
-  const int64_t in_img = (int64_t)d.cin * d.hin * d.win, per = (int64_t)d.cout * d.ho * d.wo;
-  const int64_t total = J * M * in_img;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = g / (M * in_img), r = g - j * M * in_img, m = r / in_img, o = r - m * in_img;
-    const int ci = (int)(o / ((int64_t)d.hin * d.win));
-    const int yx = (int)(o - (int64_t)ci * d.hin * d.win), y = yx / d.win, x = yx - y * d.win;
-    const float* z = dZ + j * z_ps + m * per;
-    const float* w = theta + j * Dp + d.woff + (int64_t)ci * d.k * d.k;
-    float acc = 0.f;
-    for (int co = 0; co < d.cout; ++co)
-      for (int ky = 0; ky < d.k; ++ky) {
-        const int oy = y - ky;
-        if (oy < 0 || oy >= d.ho) continue;
-        for (int kx = 0; kx < d.k; ++kx) {
-          const int ox = x - kx;
-          if (ox < 0 || ox >= d.wo) continue;
-          acc = fmaf(z[((int64_t)co * d.ho + oy) * d.wo + ox], w[(int64_t)co * d.cin * d.k * d.k + ky * d.k + kx], acc);
-        }
-      }
-    float* p = io + j * io_ps + m * in_img + o;
-    *p = apply_act ? acc * act_grad_post(*p, act) : acc;
+// previous stage pools (its pool backward applies act' at the argmax instead).  Tiled like
+// conv_fwd: a block owns one image and CT input channels, W as [cout*k*k][CT] in smem.
+template <int K, int CT>
+__global__ void __launch_bounds__(128) conv_dx_kernel(ConvDev d, int act, int apply_act,
+                                                       const float* __restrict__ dZ, int64_t z_ps,
+                                                       const float* __restrict__ theta, int64_t Dp, float* io,
+                                                       int64_t io_ps) {
+  extern __shared__ float4 cv_sh4[];
+  float* Ws = reinterpret_cast<float*>(cv_sh4);
+  const int64_t m = blockIdx.x, j = blockIdx.z;
+  const int ci0 = blockIdx.y * CT, kk = d.k * d.k;
+  const float* W = theta + j * Dp + d.woff;
+  for (int i = threadIdx.x; i < d.cout * kk * CT; i += blockDim.x) {
+    const int t = i / CT, c = i - t * CT;  // t = (co, ky, kx)
+    const int co = t / kk, r = t - co * kk;
+    Ws[i] = ci0 + c < d.cin ? W[((int64_t)co * d.cin + ci0 + c) * kk + r] : 0.f;
   }
+  __syncthreads();
+  const int64_t in_img = (int64_t)d.cin * d.hin * d.win, per = (int64_t)d.cout * d.ho * d.wo;
+  const float* z = dZ + j * z_ps + m * per;
+  float* dst = io + j * io_ps + m * in_img;
+  const int npix = d.hin * d.win;
+  for (int p = threadIdx.x; p < npix; p += blockDim.x) {
+    const int y = p / d.win, x = p - y * d.win;
+    const int ky0 = max(0, y - d.ho + 1), ky1 = min(d.k - 1, y);
+    const int kx0 = max(0, x - d.wo + 1), kx1 = min(d.k - 1, x);
+    float acc[CT];
+#pragma unroll
+    for (int c = 0; c < CT; ++c) acc[c] = 0.f;
+    for (int co = 0; co < d.cout; ++co)
+      for (int ky = ky0; ky <= ky1; ++ky) {
+        const float* zrow = z + ((int64_t)co * d.ho + y - ky) * d.wo + x;
+        const float4* wrow = cv_sh4 + (int64_t)((co * K + ky) * K) * (CT / 4);
+        float v[K];
+#pragma unroll
+        for (int kx = 0; kx < K; ++kx) v[kx] = (kx >= kx0 && kx <= kx1) ? zrow[-kx] : 0.f;
+#pragma unroll
+        for (int kx = 0; kx < K; ++kx)
+#pragma unroll
+          for (int u = 0; u < CT / 4; ++u) {
+            const float4 w = wrow[kx * (CT / 4) + u];
+            acc[4 * u] = fmaf(v[kx], w.x, acc[4 * u]);
+            acc[4 * u + 1] = fmaf(v[kx], w.y, acc[4 * u + 1]);
+            acc[4 * u + 2] = fmaf(v[kx], w.z, acc[4 * u + 2]);
+            acc[4 * u + 3] = fmaf(v[kx], w.w, acc[4 * u + 3]);
+          }
+      }
+#pragma unroll
+    for (int c = 0; c < CT; ++c)
+      if (ci0 + c < d.cin) {
+        float* q = dst + (int64_t)(ci0 + c) * npix + p;
+        *q = apply_act ? acc[c] * act_grad_post(*q, act) : acc[c];
+      }
+  }
+}
+
+// conv kernel sizes are template parameters (unrolled kx loops / register windows)
+template <typename Fn>
+void dispatch_k(int k, Fn&& fn) {
+  switch (k) {
+    case 1: fn(std::integral_constant<int, 1>{}); break;
+    case 2: fn(std::integral_constant<int, 2>{}); break;
+    case 3: fn(std::integral_constant<int, 3>{}); break;
+    case 4: fn(std::integral_constant<int, 4>{}); break;
+    case 5: fn(std::integral_constant<int, 5>{}); break;
+    case 6: fn(std::integral_constant<int, 6>{}); break;
+    case 7: fn(std::integral_constant<int, 7>{}); break;
+    default: throw std::invalid_argument("conv: kernel sizes 1..7 supported");
+  }
+}
+
+template <typename K>
+void set_smem(K kern, size_t bytes) {
+  if (bytes > 227 * 1024) throw std::invalid_argument("conv: stage too large for shared memory");
+  if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
 int64_t conv_out_floats(const ConvDev& d) { return (int64_t)d.cout * d.sh * d.sw; }
@@ -810,9 +932,15 @@ void launch_eval_cnn(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_
     const ConvDev& d = net.conv[i];
     const float* in = i == 0 ? c.X : stage_out(c, i - 1);
     const int64_t in_ps = i == 0 ? 0 : c.Mcap * conv_out_floats(net.conv[i - 1]);
-    conv_fwd_kernel<<<grid_of(J * M * conv_act_floats(d)), 256, 0, c.stream>>>(
-        d, net.act, in, in_ps, theta_in, net.Dp, c.cact[i], c.Mcap * conv_act_floats(d), M, J);
-    LAUNCHED();
+    dispatch_k(d.k, [&](auto kc) {
+      constexpr int K = decltype(kc)::value, CT = 16;
+      const size_t sm = sizeof(float) * (size_t)d.cin * K * K * CT;
+      set_smem(conv_fwd_kernel<K, CT>, sm);
+      conv_fwd_kernel<K, CT><<<dim3((unsigned)M, (unsigned)((d.cout + CT - 1) / CT), (unsigned)J), 128, sm,
+                               c.stream>>>(d, net.act, in, in_ps, theta_in, net.Dp, c.cact[i],
+                                           c.Mcap * conv_act_floats(d));
+      LAUNCHED();
+    });
     if (d.pool) {
       pool_fwd_kernel<<<grid_of(J * M * conv_out_floats(d)), 256, 0, c.stream>>>(
           d, c.cact[i], c.Mcap * conv_act_floats(d), c.cpool[i], c.Mcap * conv_out_floats(d), M, J);
@@ -868,15 +996,33 @@ void launch_eval_cnn(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_
     }
     const float* in = i == 0 ? c.X : stage_out(c, i - 1);
     const int64_t in_ps = i == 0 ? 0 : c.Mcap * conv_out_floats(net.conv[i - 1]);
-    const int64_t np = (int64_t)d.cout * d.cin * d.k * d.k + d.cout;
-    conv_dw_kernel<<<grid_of(J * np), 256, 0, c.stream>>>(d, dz, a_ps, in, in_ps, net.Dp, M, J, *epi);
-    LAUNCHED();
+    {
+      const int nchunks = (int)((M + kImgChunk - 1) / kImgChunk);
+      const int64_t np = (int64_t)d.cout * d.cin * d.k * d.k + d.cout;
+      ensure_stage(c, sizeof(double) * (size_t)J * nchunks * np);
+      double* part = reinterpret_cast<double*>(c.stage);
+      dispatch_k(d.k, [&](auto kc) {
+        constexpr int K = decltype(kc)::value, CT = 16;
+        const size_t sm = sizeof(float) * (((size_t)d.hin * d.win + 3) / 4 * 4 + (size_t)CT * d.ho * d.wo);
+        set_smem(conv_dw_kernel<K, CT>, sm);
+        conv_dw_kernel<K, CT><<<dim3((unsigned)d.cin, (unsigned)((d.cout + CT - 1) / CT), (unsigned)(J * nchunks)),
+                                128, sm, c.stream>>>(d, dz, a_ps, in, in_ps, M, np, nchunks, part);
+        LAUNCHED();
+      });
+      conv_dw_reduce_kernel<<<grid_of(J * np), 256, 0, c.stream>>>(d, np, nchunks, part, J, net.Dp, *epi);
+      LAUNCHED();
+    }
     if (i > 0) {
       const ConvDev& dp = net.conv[i - 1];
-      conv_dx_kernel<<<grid_of(J * M * (int64_t)d.cin * d.hin * d.win), 256, 0, c.stream>>>(
-          d, net.act, dp.pool ? 0 : 1, dz, a_ps, theta_in, net.Dp, stage_out(c, i - 1),
-          c.Mcap * conv_out_floats(dp), M, J);
-      LAUNCHED();
+      dispatch_k(d.k, [&](auto kc) {
+        constexpr int K = decltype(kc)::value, CT = 16;
+        const size_t sm = sizeof(float) * (size_t)d.cout * K * K * CT;
+        set_smem(conv_dx_kernel<K, CT>, sm);
+        conv_dx_kernel<K, CT><<<dim3((unsigned)M, (unsigned)((d.cin + CT - 1) / CT), (unsigned)J), 128, sm,
+                                c.stream>>>(d, net.act, dp.pool ? 0 : 1, dz, a_ps, theta_in, net.Dp,
+                                            stage_out(c, i - 1), c.Mcap * conv_out_floats(dp));
+        LAUNCHED();
+      });
     }
   }
 }
