@@ -211,6 +211,22 @@ int dasmc_sda_advance_with(const dasmc_schedule* cfg, dasmc_sda_state* state, co
 int dasmc_sda_moments_from(const double* prefix_nll, const double* block_nll, const double* log_weights,
                            int64_t J, double* out6);
 
+/* ---- evaluate_predictive (runner.hpp:331-364) ------------------------------------------
+ * Ensemble-averaged predictive of the context's current ensemble on a labelled test set
+ * (host buffers: n_test rows in the model's input layout, int32 labels): mean log predictive
+ * probability of the true label (floor 1e-300) and argmax accuracy in percent.  Weights are
+ * normalised from the context's log-weights; particles with w = 0 contribute nothing. */
+int dasmc_gpu_evaluate_predictive(dasmc_ctx* ctx, const float* X_test, const int32_t* y_test, int64_t n_test,
+                                  double* log_pred, double* accuracy);
+/* Sharded form: pred[n_test x classes] += sum over this context's J
+ * particles of w[j] * softmax_j, in ascending j (w: the globally normalised weights of the
+ * local slots; y_test needed for CNN contexts only).  Ranks all-reduce pred, then call
+ * dasmc_predictive_metrics. */
+int dasmc_gpu_predictive_mix(dasmc_ctx* ctx, const float* X_test, const int32_t* y_test, int64_t n_test,
+                             const double* w, int64_t J, double* pred);
+int dasmc_predictive_metrics(const double* pred, const int32_t* y, int64_t n, int classes, double* log_pred,
+                             double* accuracy);
+
 /* ---- data (dataset.hpp) -------------------------------------------------------------- */
 /* [EXT] teacher-labelled synthetic data: features of kind 0
  * (U[0,1)) or 1 (k/255), labels = argmax of a N(0,1) teacher of shape `net`. */

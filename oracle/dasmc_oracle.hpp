@@ -1475,6 +1475,58 @@ inline SdaState sda_advance(const ScheduleConfig& c, const SdaState& s, const Pa
 }
 
 // ---------------------------------------------------------------- runner.hpp (loop only)
+// evaluate_predictive (runner.hpp:331-364): ensemble-averaged predictive over a labelled
+// test set.  Weights normalised from the log-weights; dead particles (w = 0) skipped;
+// predictive[i][c] = sum_j w_j softmax_j[i][c] in ascending j; returns (mean log
+// predictive probability of the true label with a 1e-300 floor, argmax accuracy in %;
+// argmax = first maximum).  The logits come from the model's forward pass.
+inline std::pair<double, double> evaluate_predictive(const ParticleEnsemble& e, const ModelSpec& model,
+                                                     const Dataset& test, int threads = 1) {
+  if (test.n < 1 || test.labels.empty()) throw std::invalid_argument("evaluate_predictive: empty or unlabelled test set");
+  const Vec w = normalize(e.log_weights);
+  const int C = std::holds_alternative<CnnSpec>(model) ? std::get<CnnSpec>(model).head.layer_sizes.back()
+                                                     : std::get<NetSpec>(model).layer_sizes.back();
+  std::vector<Vec> probs((size_t)e.count);
+  parallel_for(e.count, threads, [&](int64_t j) {
+    if (w[(size_t)j] <= 0.0) return;
+    Vec logits;
+    if (const auto* cnn = std::get_if<CnnSpec>(&model)) {
+      const Vec flat = cnn_flatten_batch(*cnn, e.col(j), test.row(0), test.n);
+      logits = forward_batch(cnn->head, e.col(j) + cnn_conv_params(*cnn), flat.data(), test.n);
+    } else {
+      logits = forward_batch(std::get<NetSpec>(model), e.col(j), test.row(0), test.n);
+    }
+    for (int64_t i = 0; i < test.n; ++i) {
+      double* row = logits.data() + (size_t)i * C;
+      double m = row[0];
+      for (int c = 1; c < C; ++c) m = std::max(m, row[c]);
+      double s = 0.0;
+      for (int c = 0; c < C; ++c) {
+        row[c] = std::exp(row[c] - m);
+        s += row[c];
+      }
+      for (int c = 0; c < C; ++c) row[c] /= s;
+    }
+    probs[(size_t)j] = std::move(logits);
+  });
+  Vec pred((size_t)test.n * C, 0.0);
+  for (int64_t j = 0; j < e.count; ++j)
+    if (w[(size_t)j] > 0.0)
+      for (size_t t = 0; t < pred.size(); ++t) pred[t] += w[(size_t)j] * probs[(size_t)j][t];
+  double log_pred = 0.0;
+  int64_t correct = 0;
+  for (int64_t i = 0; i < test.n; ++i) {
+    const int y = test.labels[(size_t)i];
+    const double* row = pred.data() + (size_t)i * C;
+    log_pred += std::log(std::max(row[y], 1e-300));
+    int am = 0;
+    for (int c = 1; c < C; ++c)
+      if (row[c] > row[am]) am = c;
+    if (am == y) ++correct;
+  }
+  return {log_pred / (double)test.n, 100.0 * (double)correct / (double)test.n};
+}
+
 struct RunConfig {  // the in-memory subset of runner.hpp:57-70 the hot loop reads
   ModelSpec model;
   PriorSpec prior;

@@ -349,6 +349,24 @@ int oracle_init_ensemble(const int* layers, int nl, int act, const double* X, co
   });
 }
 
+// evaluate_predictive (runner.hpp:331-364) of the ensemble thetas[J*D], log_w[J] on a test set.
+int oracle_evaluate_predictive(const int* layers, int nl, int act, const double* X, const int* y, int64_t n,
+                               const double* thetas, const double* log_w, int64_t J, int threads, double* log_pred,
+                               double* accuracy) {
+  return guarded([&] {
+    const ModelSpec net = model_of(layers, nl, act);
+    const Dataset d = dataset_of(X, y, n, input_dim(net), classes_of(net));
+    ParticleEnsemble e;
+    e.dim = model_param_count(net);
+    e.count = J;
+    e.thetas.assign(thetas, thetas + e.dim * J);
+    e.log_weights.assign(log_w, log_w + J);
+    const auto r = evaluate_predictive(e, net, d, threads);
+    *log_pred = r.first;
+    *accuracy = r.second;
+  });
+}
+
 // ---- resampling / weights --------------------------------------------------------
 // kind 0: multinomial with J given uniforms u[J]; kind 1: systematic with u[0].
 int oracle_resample_indices(const double* w, const double* u, int64_t J, int kind, int* idx) {

@@ -246,6 +246,19 @@ def propose_particles(layers, act, X, y, window, mode, beta, sigma, kernel, seed
     return th, inc, lt
 
 
+def evaluate_predictive(layers, act, X, y, thetas, log_w, threads=8):
+    """runner.hpp:331-364: (mean log predictive probability, accuracy %)."""
+    arr, nl = _net(layers)
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    th = np.ascontiguousarray(thetas, dtype=np.float64)
+    lw = np.ascontiguousarray(log_w, dtype=np.float64)
+    lp, acc = C.c_double(), C.c_double()
+    _check(lib().oracle_evaluate_predictive(arr, nl, act, _dp(X), _ip(y), C.c_int64(X.shape[0]), _dp(th), _dp(lw),
+                                            C.c_int64(th.shape[0]), threads, C.byref(lp), C.byref(acc)))
+    return lp.value, acc.value
+
+
 def resample_indices(w, u, kind):
     w = np.ascontiguousarray(w, dtype=np.float64)
     u = np.ascontiguousarray(u, dtype=np.float64)

@@ -303,6 +303,33 @@ class GpuEnsembleTarget:
         L.check(self.lib.dasmc_gpu_sda_moments(self.h, prefix_end, block_end, _dp(out)))
         return out
 
+    def evaluate_predictive(self, X_test: np.ndarray, y_test: np.ndarray):  # runner.hpp:331-364
+        """(mean log predictive probability of the true label, accuracy %) of the current ensemble."""
+        X = np.ascontiguousarray(X_test, dtype=np.float32)
+        y = np.ascontiguousarray(y_test, dtype=np.int32)
+        lp, acc = C.c_double(), C.c_double()
+        L.check(self.lib.dasmc_gpu_evaluate_predictive(self.h, _fp(X), _ip(y), X.shape[0], C.byref(lp), C.byref(acc)))
+        return lp.value, acc.value
+
+    def predictive_mix(self, X_test: np.ndarray, w_local: np.ndarray, J: int, pred: np.ndarray,
+                       y_test: Optional[np.ndarray] = None) -> np.ndarray:
+        """pred += sum_j w_j softmax_j over this context's J particles (sharded evaluate_predictive)."""
+        X = np.ascontiguousarray(X_test, dtype=np.float32)
+        w = np.ascontiguousarray(w_local, dtype=np.float64)
+        y = np.ascontiguousarray(y_test, dtype=np.int32) if y_test is not None else None
+        L.check(self.lib.dasmc_gpu_predictive_mix(self.h, _fp(X), _ip(y), X.shape[0], _dp(w), J, _dp(pred)))
+        return pred
+
+
+def predictive_metrics(pred: np.ndarray, y: np.ndarray):
+    """Mean log predictive probability (floor 1e-300) and argmax accuracy % (runner.hpp:351-363)."""
+    pred = np.ascontiguousarray(pred, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    lp, acc = C.c_double(), C.c_double()
+    L.check(L.load().dasmc_predictive_metrics(_dp(pred), _ip(y), pred.shape[0], pred.shape[1], C.byref(lp),
+                                              C.byref(acc)))
+    return lp.value, acc.value
+
 
 @dataclass
 class RunConfig:  # runner.hpp:57-70 (hot-loop subset)

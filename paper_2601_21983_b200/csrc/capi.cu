@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <limits>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -974,6 +975,99 @@ int dasmc_rng_skip(uint64_t key, uint64_t skip, int64_t count, uint64_t* out) {
       x.jump(tab[1].data());
     }
     for (int64_t i = 0; i < count; ++i) out[i] = x.next();
+  });
+}
+
+// ---- evaluate_predictive (runner.hpp:331-364) -------------------------------------------
+int dasmc_gpu_predictive_mix(dasmc_ctx* ctx, const float* X_test, const int32_t* y_test, int64_t n_test,
+                             const double* w, int64_t J, double* pred) {
+  return guarded([&] {
+    if (!ctx || !X_test || !w || !pred || n_test < 1) throw InvalidArg("bad argument");
+    Ctx& c = ctx->c;
+    if (!c.has_ensemble) throw InvalidArg("no ensemble");
+    check_J(c, J);
+    const int C = c.net.sizes[c.net.L];
+    if (C > 16) throw InvalidArg("evaluate_predictive: at most 16 classes");
+    if (c.net.nconv > 0 && !y_test) throw InvalidArg("evaluate_predictive: CNN contexts need the labels");
+    CK(cudaSetDevice(c.device));
+    const int64_t d_in = input_floats(c.net);
+    int64_t widest = 0;
+    for (int l = 1; l <= c.net.L; ++l) widest = std::max<int64_t>(widest, c.net.sizes[l]);
+    // rows per chunk: scratch activations of J x R x widest floats stay below ~4 GB
+    const int64_t R = std::max<int64_t>(1, std::min<int64_t>(n_test, (int64_t)(1 << 30) / std::max<int64_t>(1, J * widest)));
+    float *Xd = nullptr, *logits = nullptr, *s0 = nullptr, *s1 = nullptr;
+    int32_t* yd = nullptr;
+    double *wd = nullptr, *pd = nullptr;
+    dmalloc(Xd, (size_t)R * d_in);
+    dmalloc(logits, (size_t)J * R * C);
+    dmalloc(s0, (size_t)J * R * widest);
+    dmalloc(s1, (size_t)J * R * widest);
+    dmalloc(yd, (size_t)R);
+    dmalloc(wd, (size_t)J);
+    dmalloc(pd, (size_t)R * C);
+    CK(cudaMemcpyAsync(wd, w, sizeof(double) * J, cudaMemcpyHostToDevice, c.stream));
+    const float* th = c.theta[c.start];
+    for (int64_t r0 = 0; r0 < n_test; r0 += R) {
+      const int64_t rows = std::min(R, n_test - r0);
+      CK(cudaMemcpyAsync(Xd, X_test + r0 * d_in, sizeof(float) * rows * d_in, cudaMemcpyHostToDevice, c.stream));
+      if (y_test) CK(cudaMemcpyAsync(yd, y_test + r0, sizeof(int32_t) * rows, cudaMemcpyHostToDevice, c.stream));
+      CK(cudaMemcpyAsync(pd, pred + r0 * C, sizeof(double) * rows * C, cudaMemcpyHostToDevice, c.stream));
+      launch_forward_logits(c, th, J, Xd, yd, rows, logits, s0, s1);
+      launch_predictive_mix(c, logits, rows, J, wd, pd);
+      CK(cudaMemcpyAsync(pred + r0 * C, pd, sizeof(double) * rows * C, cudaMemcpyDeviceToHost, c.stream));
+      CK(cudaStreamSynchronize(c.stream));
+    }
+    void* bufs[] = {Xd, logits, s0, s1, yd, wd, pd};
+    for (void* p : bufs) cudaFree(p);
+  });
+}
+
+int dasmc_predictive_metrics(const double* pred, const int32_t* y, int64_t n, int C, double* log_pred,
+                             double* accuracy) {
+  return guarded([&] {
+    if (!pred || !y || n < 1 || C < 1) throw InvalidArg("bad argument");
+    double lp = 0.0;
+    int64_t correct = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      const double* row = pred + i * C;
+      if (y[i] < 0 || y[i] >= C) throw InvalidArg("label out of range");
+      lp += std::log(std::max(row[y[i]], 1e-300));
+      int am = 0;
+      for (int c = 1; c < C; ++c)
+        if (row[c] > row[am]) am = c;
+      if (am == y[i]) ++correct;
+    }
+    if (log_pred) *log_pred = lp / (double)n;
+    if (accuracy) *accuracy = 100.0 * (double)correct / (double)n;
+  });
+}
+
+int dasmc_gpu_evaluate_predictive(dasmc_ctx* ctx, const float* X_test, const int32_t* y_test, int64_t n_test,
+                                  double* log_pred, double* accuracy) {
+  return guarded([&] {
+    if (!ctx || !y_test) throw InvalidArg("bad argument");
+    Ctx& c = ctx->c;
+    if (!c.has_ensemble) throw InvalidArg("no ensemble");
+    const int64_t J = c.J;
+    std::vector<double> lw((size_t)J), w((size_t)J);
+    CK(cudaSetDevice(c.device));
+    CK(cudaMemcpyAsync(lw.data(), c.logw, sizeof(double) * J, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    double m = lw[0];  // normalize (smc.hpp:57-64)
+    for (double x : lw) m = std::max(m, x);
+    if (m == -std::numeric_limits<double>::infinity()) throw Dead("normalize: all particles dead");
+    double s = 0.0;
+    for (int64_t j = 0; j < J; ++j) {
+      w[(size_t)j] = std::exp(lw[(size_t)j] - m);
+      s += w[(size_t)j];
+    }
+    for (auto& x : w) x /= s;
+    const int C = c.net.sizes[c.net.L];
+    std::vector<double> pred((size_t)n_test * C, 0.0);
+    int rc = dasmc_gpu_predictive_mix(ctx, X_test, y_test, n_test, w.data(), J, pred.data());
+    if (rc != DASMC_OK) throw std::runtime_error(g_err);
+    rc = dasmc_predictive_metrics(pred.data(), y_test, n_test, C, log_pred, accuracy);
+    if (rc != DASMC_OK) throw InvalidArg(g_err);
   });
 }
 

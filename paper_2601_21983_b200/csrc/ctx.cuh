@@ -209,6 +209,9 @@ constexpr int kRngChunkNormals = 1024;  // normals per RNG thread (2048 xoshiro 
 // ---- launchers (kernels.cu) --------------------------------------------------------------
 void ensure_activation_capacity(Ctx& c, int64_t M);
 void ensure_stage(Ctx& c, size_t bytes);
+void launch_forward_logits(Ctx& c, const float* theta, int64_t J, const float* Xd, const int32_t* yd, int64_t R,
+                           float* logits, float* scratch0, float* scratch1);
+void launch_predictive_mix(Ctx& c, const float* logits, int64_t R, int64_t J, const double* w, double* pred);
 void ensure_host_stage(Ctx& c, size_t bytes);
 
 // One forward pass (+ optional backward with the fused epilogue) over window

@@ -1027,6 +1027,77 @@ void launch_eval_cnn(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_
   }
 }
 
+// ---- evaluate_predictive (runner.hpp:331-364) --------------------------------------------
+// One thread per test row: predictive[i][c] += sum_j w_j softmax(logits_j[i])[c] over the
+// particles in ascending j (w_j <= 0 skipped), fp64 softmax as the reference.
+__global__ void predictive_mix_kernel(const float* __restrict__ logits, int64_t ps, int C, int64_t R, int64_t J,
+                                      const double* __restrict__ w, double* __restrict__ pred) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= R) return;
+  double acc[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) acc[c] = c < C ? pred[i * C + c] : 0.0;
+  for (int64_t j = 0; j < J; ++j) {
+    const double wj = w[j];
+    if (!(wj > 0.0)) continue;
+    const float* z = logits + j * ps + i * C;
+    double mx = (double)z[0];
+    for (int c = 1; c < C; ++c) mx = fmax(mx, (double)z[c]);
+    double e[16], s = 0.0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c < C) {
+        e[c] = exp((double)z[c] - mx);
+        s += e[c];
+      }
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c < C) acc[c] += wj * (e[c] / s);
+  }
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    if (c < C) pred[i * C + c] = acc[c];
+}
+
+// Logits of J particles on R rows of Xd (device, the model's input layout) into `logits`
+// ([J][R][C] fp32, particle stride R*C).  MLP: the SIMT forward GEMMs with scratch
+// activations; CNN: the context's stage buffers with X / y swapped for the test rows.
+void launch_forward_logits(Ctx& c, const float* theta, int64_t J, const float* Xd, const int32_t* yd, int64_t R,
+                           float* logits, float* scratch0, float* scratch1) {
+  const NetDev& net = c.net;
+  if (net.nconv > 0) {
+    const float* X0 = c.X;
+    const int32_t* y0 = c.y;
+    c.X = const_cast<float*>(Xd);
+    c.y = const_cast<int32_t*>(yd);
+    ensure_activation_capacity(c, R);
+    launch_eval_cnn(c, theta, J, R, R, 1.0, false, nullptr);
+    c.X = const_cast<float*>(X0);
+    c.y = const_cast<int32_t*>(y0);
+    // act[L] [J][Mcap][C] -> logits [J][R][C]
+    const int C = net.sizes[net.L];
+    CK(cudaMemcpy2DAsync(logits, sizeof(float) * R * C, c.act[net.L], sizeof(float) * c.Mcap * C,
+                         sizeof(float) * R * C, (size_t)J, cudaMemcpyDeviceToDevice, c.stream));
+    return;
+  }
+  const float* A = Xd;
+  int64_t sA = 0;
+  for (int l = 1; l <= net.L; ++l) {
+    const LayerDev& ly = net.layer[l - 1];
+    float* out = l == net.L ? logits : (l & 1 ? scratch0 : scratch1);
+    EpiFwd e{out, ly.out, R * ly.out, theta, net.Dp, ly.boff, ly.hidden, net.act};
+    sgemm<true, true>(c.stream, (int)R, ly.out, ly.in, A, ly.in, sA, theta + ly.woff, ly.in, net.Dp, -1, J, e);
+    A = out;
+    sA = R * ly.out;
+  }
+}
+
+void launch_predictive_mix(Ctx& c, const float* logits, int64_t R, int64_t J, const double* w, double* pred) {
+  const int C = c.net.sizes[c.net.L];
+  predictive_mix_kernel<<<(unsigned)((R + 127) / 128), 128, 0, c.stream>>>(logits, R * C, C, R, J, w, pred);
+  LAUNCHED();
+}
+
 void ensure_activation_capacity(Ctx& c, int64_t M) {
   if (M <= c.Mcap) return;
   CK(cudaStreamSynchronize(c.stream));

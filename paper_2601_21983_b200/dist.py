@@ -127,6 +127,13 @@ class GpuShardEngine:
             L.check(self.lib.dasmc_gpu_pack_rows(self.t.h, rows.ctypes.data_as(L._I32), rows.shape[0], buf.data_ptr()))
         return buf
 
+    def classes(self) -> int:
+        return int(self.t.spec.layer_sizes[-1])
+
+    def predictive_mix(self, X_test, w_local, J, pred, y_test=None):
+        self.torch.cuda.synchronize()
+        return self.t.predictive_mix(X_test, w_local, J, pred, y_test)
+
     def unpack(self, src, slots: np.ndarray):
         slots = np.ascontiguousarray(slots, dtype=np.int32)
         self.torch.cuda.synchronize()
@@ -162,3 +169,27 @@ def sharded_step(engine, comm, J: int, cfg: KernelConfig, seed: int, kind: str =
         engine.unpack(src, slots)
         out["migrated_rows"] = int(sum(recv_counts) - recv_counts[rank])
     return out
+
+
+def sharded_evaluate_predictive(engine, comm, J: int, local_log_w, X_test, y_test):
+    """evaluate_predictive (runner.hpp:331-364) of a particle-sharded ensemble (SURVEY.md §8e
+    item 5): all-gather the log-weights, normalise them identically on every rank, mix this
+    rank's particles into pred[n x C], all-reduce pred (sum), then the metrics."""
+    torch = comm.torch
+    world, rank = comm.world, comm.rank
+    bounds = [shard_range(J, world, r) for r in range(world)]
+    counts = [hi - lo for lo, hi in bounds]
+    j0, j1 = bounds[rank]
+    lw = torch.as_tensor(np.ascontiguousarray(local_log_w, dtype=np.float64), device=comm.device)
+    full = comm.all_gather(lw, counts).cpu().numpy()
+    m = full.max()
+    if m == -np.inf:
+        raise L.SamplerError(L.DASMC_EDEAD, "normalize: all particles dead")
+    w = np.exp(full - m)  # normalize (smc.hpp:57-64), same order on every rank
+    w /= w.sum()
+    pred = np.zeros((np.asarray(X_test).shape[0], engine.classes()), dtype=np.float64)
+    engine.predictive_mix(X_test, w[j0:j1], j1 - j0, pred, y_test)
+    pt = torch.as_tensor(pred, device=comm.device)
+    comm.dist.all_reduce(pt)
+    from .api import predictive_metrics
+    return predictive_metrics(pt.cpu().numpy(), y_test)

@@ -163,3 +163,72 @@ def test_shard_plan_roundtrip(product):
                 lo_s, _ = shard_range(J, G, s)
                 assert np.array_equal(sent, recv_row[recv_src == s])
                 assert np.array_equal(sent + lo_s, idx[lo_d:hi_d][recv_src == s])
+
+
+def _np_probs(th, X):
+    """numpy forward of LAYERS (reference theta layout) -> softmax rows (test-side engine)."""
+    a = X
+    off = 0
+    for l in range(1, len(LAYERS)):
+        i, o = LAYERS[l - 1], LAYERS[l]
+        W = th[off:off + i * o].reshape(i, o)
+        off += i * o
+        a = a @ W + th[off:off + o]
+        off += o
+        if l + 1 < len(LAYERS):
+            a = np.maximum(a, 0.0)
+    e = np.exp(a - a.max(1, keepdims=True))
+    return e / e.sum(1, keepdims=True)
+
+
+class _PredEngine:
+    def __init__(self, th):
+        self.th = th
+
+    def classes(self):
+        return LAYERS[-1]
+
+    def predictive_mix(self, X, w_local, Jr, pred, y=None):
+        for j in range(Jr):
+            if w_local[j] > 0:
+                pred += w_local[j] * _np_probs(self.th[j], X)
+        return pred
+
+
+def _pred_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "oracle")]
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2601_21983_b200.dist import TorchComm, shard_range, sharded_evaluate_predictive
+    X, y, th0, lw0 = problem()
+    lw0 = lw0.copy()
+    lw0[2] = -np.inf
+    lo, hi = shard_range(J, world, rank)
+    res = sharded_evaluate_predictive(_PredEngine(th0[lo:hi]), TorchComm("cpu"), J, lw0[lo:hi], X, y)
+    if rank == 0:
+        out_q.put(res)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_evaluate_predictive_two_ranks(oracle):
+    """evaluate_predictive of a sharded ensemble (all-gathered weights, all-reduced mixture)
+    equals the oracle's single-process runner.hpp:331-364."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pred_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    lp, acc = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    X, y, th0, lw0 = problem()
+    lw0 = lw0.copy()
+    lw0[2] = -np.inf
+    lpo, acco = oracle.evaluate_predictive(LAYERS, ACT, X, y, th0, lw0)
+    assert abs(lp - lpo) < 1e-12 * abs(lpo) and acc == acco
