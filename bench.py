@@ -386,7 +386,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--precision", default=None, choices=["fp32", "tf32", "3xtf32"],
+    ap.add_argument("--precision", default=None, choices=["fp32", "tf32", "3xtf32", "f16"],
                     help="default: tf32 where the tensor-core path applies (one-hidden-layer MLPs), else fp32")
     ap.add_argument("--resample", default="systematic", choices=["systematic", "multinomial"])
     ap.add_argument("--e2e-steps", type=int, default=3)

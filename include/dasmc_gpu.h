@@ -54,6 +54,8 @@ extern "C" {
 #define DASMC_PREC_FP32 0   /* fp32 CUDA-core path: the 1e-4 parity path */
 #define DASMC_PREC_TF32 1   /* tcgen05 kind::tf32 tensor-core path (tolerance stated in DESIGN.md) */
 #define DASMC_PREC_3XTF32 2 /* tcgen05 split-tf32 (3 MMAs) tensor-core path, fp32-level accuracy */
+#define DASMC_PREC_F16 3    /* tcgen05 kind::f16 with fp16 operands (the same 10-bit mantissa as tf32, fp32
+                               accumulation, half the operand bytes); one-hidden-layer MLPs */
 /* ScheduleKind (annealing.hpp:18). */
 #define DASMC_SCHED_CONSTANT 0
 #define DASMC_SCHED_FULL_BATCH 1

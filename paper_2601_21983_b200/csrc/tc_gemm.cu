@@ -11,6 +11,7 @@
 // mbarriers: full/empty per stage (TMA <-> MMA), tmem_full/tmem_empty per
 // accumulator (MMA <-> epilogue).  tcgen05.commit arrives on the mbarriers.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -31,6 +32,8 @@ struct TcState {
   int64_t n_pad = 0;     // X^T row stride (floats)
   int64_t mcap = 0;      // row stride of the transposed activation buffers
   bool split = false;    // split-tf32 (3 MMAs)
+  bool f16 = false;      // fp16 operands, kind::f16 (DASMC_PREC_F16): same 10-bit mantissa as tf32
+  int esz = 4;           // operand element bytes (2 when f16)
   int cluster = 1;       // fused-forward cluster shape (ClusterShape CL; 0 = single CTAs); DASMC_TC_CLUSTER
   float* Xt = nullptr;   // [(n0+1) x n_pad], row n0 = 1
   int64_t kx = 0;        // row stride of Xhi / W1hi: [x, 1] padded to 16 bytes (bias folded into K)
@@ -227,29 +230,53 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+// PREC 0: kind::tf32 (fp32 containers, K = 8 per instruction); PREC 1: kind::f16 with
+// fp16 operands (K = 16).  Both advance 32 bytes of K per instruction.
+template <int PREC>
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
+  if (PREC == 1)
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+  else
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
 }
 // Pair MMA (leader CTA only): M = 256 rows, A rows 128r..128r+127 and B rows
 // (N/2)r..(N/2)r+N/2-1 from CTA r's shared memory at the same offsets; D rows
 // of CTA r land in CTA r's TMEM.
+template <int PREC>
 __device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                         uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
+  if (PREC == 1)
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+  else
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
 }
 // commit the pair's outstanding MMAs to the mbarrier at this offset in every CTA of `mask`
 __device__ __forceinline__ void tc_commit2(uint64_t* bar, uint16_t mask) {
@@ -319,6 +346,19 @@ __device__ __forceinline__ uint64_t smem_desc(const void* p) {
 __host__ __device__ constexpr uint32_t idesc_tf32(int n, int m) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
+// kind::f16 instruction descriptor with fp16 A/B (format 0), f32 D, both K-major.
+__host__ __device__ constexpr uint32_t idesc_f16(int n, int m) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+// Operand element type of a precision mode: tf32 in fp32 containers, or fp16.
+template <int PREC>
+using OpT = typename std::conditional<PREC == 1, __half, float>::type;
+template <int PREC>
+__device__ __forceinline__ OpT<PREC> to_op(float v);
+template <>
+__device__ __forceinline__ float to_op<0>(float v) { return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u); }
+template <>
+__device__ __forceinline__ __half to_op<1>(float v) { return __float2half_rn(v); }
 
 // Round to the nearest tf32 (ties away from zero), low 13 mantissa bits cleared:
 // what cvt.rna.tf32.f32 computes for finite inputs, in two integer ops (ptxas
@@ -404,7 +444,7 @@ struct ClusterShape {
   static constexpr int kSize = kPair ? 2 * QA * QB : 1;
 };
 
-template <int EPI, bool SPLIT, int AM, int CP, int ACT, int CL>
+template <int EPI, bool SPLIT, int AM, int CP, int ACT, int CL, int PREC>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
               const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo, TileParams tp,
@@ -424,8 +464,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int unit0 = (int)blockIdx.x / CSZ;
   const int ustride = (int)gridDim.x / CSZ;
   const uint32_t b_rows = PAIR ? (uint32_t)tp.nmma / 2 : (uint32_t)tp.nmma;  // B rows held by this CTA
-  const uint32_t a_bytes = BM * BK * 4;
-  const uint32_t b_bytes = b_rows * BK * 4;
+  constexpr int BKE = PREC == 1 ? 64 : 32;  // K elements per 128-byte swizzle row (= per k-block)
+  using TS = OpT<PREC>;
+  const uint32_t a_bytes = BM * 128;
+  const uint32_t b_bytes = b_rows * 128;
   const uint32_t sub = SPLIT ? 2 : 1;
   const uint32_t stage_bytes = sub * (a_bytes + b_bytes);
   uint8_t* stages = smem;
@@ -516,11 +558,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int kb = 0; kb < tp.nkb; ++kb) {
           if (pf_rt >= 0) {
-            tma_prefetch_2d(&mapA, kb * BK, pf_rt * BM);
-            tma_prefetch_3d(&mapB, kb * BK, (int)(prank * b_rows), pf_j);
+            tma_prefetch_2d(&mapA, kb * BKE, pf_rt * BM);
+            tma_prefetch_3d(&mapB, kb * BKE, (int)(prank * b_rows), pf_j);
           }
           mbar_wait(&empty[s], ph ^ 1);
-          const int k0 = kb * BK;
+          const int k0 = kb * BKE;
           if (PAIR) {
             // the pair's bytes complete on its leader's full barrier (expect_tx covers the pair)
             const uint32_t fb = mapa_shared(smem_u32(&full[s]), crank & ~1u);
@@ -584,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread; the leader's when PAIR) =====================
     if (lane == 0 && prank == 0) {
-      const uint32_t idesc = idesc_tf32(tp.nmma, PAIR ? 2 * BM : BM);
+      const uint32_t idesc = PREC == 1 ? idesc_f16(tp.nmma, PAIR ? 2 * BM : BM) : idesc_tf32(tp.nmma, PAIR ? 2 * BM : BM);
       const uint16_t all_mask = (uint16_t)((1u << CSZ) - 1u);
       const uint16_t pair_mask = (uint16_t)(3u << (2 * pr));
       int s = 0;
@@ -601,19 +643,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t ad = smem_desc(A_of(s, 0)), bd = smem_desc(B_of(s, 0));
           const uint64_t adl = smem_desc(A_of(s, 1)), bdl = smem_desc(B_of(s, 1));
 #pragma unroll
-          for (int k = 0; k < BK / 8; ++k) {
+          for (int k = 0; k < 4; ++k) {  // 32 bytes of K per instruction
             const uint64_t off = (uint64_t)(k * 32) >> 4;  // 32 bytes per K=8 step inside the swizzle row
             if (PAIR) {
-              tc_mma2(d, ad + off, bd + off, idesc, (kb | k) != 0);
+              tc_mma2<PREC>(d, ad + off, bd + off, idesc, (kb | k) != 0);
               if (SPLIT) {
-                tc_mma2(d, ad + off, bdl + off, idesc, 1);
-                tc_mma2(d, adl + off, bd + off, idesc, 1);
+                tc_mma2<PREC>(d, ad + off, bdl + off, idesc, 1);
+                tc_mma2<PREC>(d, adl + off, bd + off, idesc, 1);
               }
             } else {
-              tc_mma(d, ad + off, bd + off, idesc, (kb | k) != 0);
+              tc_mma<PREC>(d, ad + off, bd + off, idesc, (kb | k) != 0);
               if (SPLIT) {
-                tc_mma(d, ad + off, bdl + off, idesc, 1);
-                tc_mma(d, adl + off, bd + off, idesc, 1);
+                tc_mma<PREC>(d, ad + off, bdl + off, idesc, 1);
+                tc_mma<PREC>(d, adl + off, bd + off, idesc, 1);
               }
             }
           }
@@ -733,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < CP; ++c) z2[c] = 0.f;
         // DASMC_DEBUG_EPI=4 (profiling only): every tile stores into one L2-resident block
         const int64_t sblk = fp.dbg == 4 ? (int64_t)(blockIdx.x & 1) : (int64_t)j * nblk + rt;
-        float* a1T = fp.a1T + sblk * (n1 + 1) * kRow + row_in_tile;
+        TS* a1T = reinterpret_cast<TS*>(fp.a1T) + sblk * (n1 + 1) * kRow + row_in_tile;
         float* a1Tlo = SPLIT ? fp.a1Tlo + ((int64_t)j * nblk + rt) * (n1 + 1) * kRow + row_in_tile : nullptr;
         // row o of W2^T (CP classes) from shared memory: float4 loads (+ one float2)
         auto w2row = [&](int o, float* w) {
@@ -757,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto chunk1 = [&](auto store, int ch, const float* v) {
           const int o0 = ch * 16;
           const int nq = min(16, n1 - o0);  // warp-uniform
-          float* pa = a1T + (int64_t)o0 * kRow;
+          TS* pa = a1T + (int64_t)o0 * kRow;
           float* pal = SPLIT ? a1Tlo + (int64_t)o0 * kRow : nullptr;
           auto one = [&](int q) {
             const float a = act(v[q]);
@@ -766,9 +808,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < CP; ++c) z2[c] = fmaf(a, w[c], z2[c]);
             if (decltype(store)::value) {
-              const float hi = tf32_hi(a);
-              st_act(pa + q * kRow, hi, st_pol);
-              if (SPLIT) st_act(pal + q * kRow, a - hi, st_pol);
+              const TS hi = to_op<PREC>(a);
+              pa[q * kRow] = hi;
+              if (SPLIT) st_act(pal + q * kRow, a - (float)hi, st_pol);
             }
           };
           if (nq == 16) {
@@ -821,7 +863,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int p = 1; p < kParts; ++p) s += z2x[((size_t)p * 128 + row_in_tile) * CP + c];
             z2[c] = s + b2s[c];
           }
-          float* d2T = fp.d2T + ((int64_t)j * nblk + rt) * C * kRow + row_in_tile;
+          TS* d2T = reinterpret_cast<TS*>(fp.d2T) + ((int64_t)j * nblk + rt) * C * kRow + row_in_tile;
           float* d2Tlo = SPLIT ? fp.d2Tlo + ((int64_t)j * nblk + rt) * C * kRow + row_in_tile : nullptr;
           if (valid) {
             const int yi = fp.y[m];
@@ -847,27 +889,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (c < C) {
                   d2[c] = wrow * ((c == yi ? 1.f : 0.f) - e[c] * rden);
                   if (part == 0) {
-                    const float hi = tf32_hi(d2[c]);
+                    const TS hi = to_op<PREC>(d2[c]);
                     d2T[c * kRow] = hi;
-                    if (SPLIT) d2Tlo[c * kRow] = d2[c] - hi;
+                    if (SPLIT) d2Tlo[c * kRow] = d2[c] - (float)hi;
                   }
                 }
             }
           } else if (fp.need_grad && part == 0) {  // rows past the window: zeros in the row-blocked delta2^T
             for (int c = 0; c < C; ++c) {
-              d2T[c * kRow] = 0.f;
+              d2T[c * kRow] = to_op<PREC>(0.f);
               if (SPLIT) d2Tlo[c * kRow] = 0.f;
             }
           }
         }
         if (fp.need_grad && fp.dbg == 0) {
           // pass 2: delta1 = (W2^T delta2) . act'(z1)  (network.hpp:209-215); zero past the window
-          float* d1T = fp.d1T + sblk * n1 * kRow + row_in_tile;
+          TS* d1T = reinterpret_cast<TS*>(fp.d1T) + sblk * n1 * kRow + row_in_tile;
           float* d1Tlo = SPLIT ? fp.d1Tlo + ((int64_t)j * nblk + rt) * n1 * kRow + row_in_tile : nullptr;
           auto chunk2 = [&](int ch, const float* v) {
             const int o0 = ch * 16;
             const int nq = min(16, n1 - o0);  // warp-uniform
-            float* pd = d1T + (int64_t)o0 * kRow;
+            TS* pd = d1T + (int64_t)o0 * kRow;
             float* pdl = SPLIT ? d1Tlo + (int64_t)o0 * kRow : nullptr;
             auto one = [&](int q) {
               float w[CP];
@@ -886,9 +928,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float a = tanhf(v[q]);
                 d1 = dz * (1.f - a * a);
               }
-              const float hi = tf32_hi(d1);
-              st_act(pd + q * kRow, hi, st_pol);
-              if (SPLIT) st_act(pdl + q * kRow, d1 - hi, st_pol);
+              const TS hi = to_op<PREC>(d1);
+              pd[q * kRow] = hi;
+              if (SPLIT) st_act(pdl + q * kRow, d1 - (float)hi, st_pol);
             };
             if (nq == 16) {
 #pragma unroll
@@ -1043,8 +1085,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ---------------------------------------------------------------- helper kernels
 // X^T with a ones row (and tf32 hi/lo splits): Xt[i][m] = X[m][i], Xt[n0][m] = 1.
 // Also the forward operand Xhi[m] = [X[m], 1, 0 ...] (row stride kx) and its lo part.
-__global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n0, int64_t n_pad, int64_t kx, float* Xt,
-                                   float* Xtlo, float* Xhi, float* Xlo, int split) {
+template <int PREC>
+__global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n0, int64_t n_pad, int64_t kx,
+                                   OpT<PREC>* Xt, float* Xtlo, OpT<PREC>* Xhi, float* Xlo, int split) {
   __shared__ float tile[32][33];
   const int64_t m0 = (int64_t)blockIdx.x * 32;
   const int i0 = blockIdx.y * 32;
@@ -1054,7 +1097,7 @@ __global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n
     float v = 0.f;
     if (m < n && i < n0) v = X[m * n0 + i];
     if (m < n && i == n0) v = 1.f;
-    if (m < n && i < kx) Xhi[m * kx + i] = tf32_hi(v);
+    if (m < n && i < kx) Xhi[m * kx + i] = to_op<PREC>(v);
     if (split && m < n && i < kx) Xlo[m * kx + i] = v - tf32_hi(v);
     tile[r][threadIdx.x] = v;
   }
@@ -1064,16 +1107,17 @@ __global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n
     const int64_t m = m0 + threadIdx.x;
     if (i <= n0 && m < n_pad) {
       const float v = m < n ? tile[threadIdx.x][r] : 0.f;
-      const float hi = tf32_hi(v);
+      const OpT<PREC> hi = to_op<PREC>(v);
       Xt[(int64_t)i * n_pad + m] = hi;
-      if (split) Xtlo[(int64_t)i * n_pad + m] = v - hi;
+      if (split) Xtlo[(int64_t)i * n_pad + m] = v - (float)hi;
     }
   }
 }
 
 // W1hi[j][o] = [W1[o], b1[o], 0 ...] (row stride kx) rounded to tf32, + lo part.
+template <int PREC>
 __global__ void split_w1_kernel(const float* __restrict__ theta, int64_t Dp, int64_t woff, int64_t boff, int n0,
-                                int64_t kx, int64_t cnt, int64_t J, float* hi, float* lo) {
+                                int64_t kx, int64_t cnt, int64_t J, OpT<PREC>* hi, float* lo) {
   // one block per output row (j, o): coalesced row copies, no per-element divisions
   const int64_t n1 = cnt / kx, nrows = J * n1;
   for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
@@ -1082,9 +1126,9 @@ __global__ void split_w1_kernel(const float* __restrict__ theta, int64_t Dp, int
     const float* src = th + woff + o * n0;
     for (int64_t i = threadIdx.x; i < kx; i += blockDim.x) {
       const float v = i < n0 ? src[i] : (i == n0 ? th[boff + o] : 0.f);
-      const float h = tf32_hi(v);
+      const OpT<PREC> h = to_op<PREC>(v);
       hi[row * kx + i] = h;
-      if (lo) lo[row * kx + i] = v - h;
+      if (lo) lo[row * kx + i] = v - (float)h;
     }
   }
 }
@@ -1247,12 +1291,13 @@ __global__ void __launch_bounds__(128) head_kernel(
 }
 
 // Row `row` of a row-blocked [J][nblk][rows][128] buffer set to v (a1^T's ones row -> db2).
-__global__ void fill_ones_row_kernel(float* buf, int64_t J, int64_t rows, int64_t row, int64_t mcap, float v) {
+template <typename T>
+__global__ void fill_ones_row_kernel(T* buf, int64_t J, int64_t rows, int64_t row, int64_t mcap, float v) {
   const int64_t total = J * mcap;
   const int64_t nblk = mcap / 128;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t jb = g / 128, r = g - jb * 128;  // jb = j * nblk + block
-    buf[(jb * rows + row) * 128 + r] = v;
+    buf[(jb * rows + row) * 128 + r] = (T)v;
     (void)nblk;
   }
 }
@@ -1275,11 +1320,14 @@ EncodeTiledFn encode_fn() {
 }
 
 // rank-2/3 fp32 tensor, innermost dim first; strides in bytes for dims >= 1.
+// esz: operand element size (4 = fp32 / tf32 containers, 2 = fp16); boxes are one
+// 128-byte swizzle row (128 / esz elements) wide.
 CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
-                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B, int esz = 4) {
   CUtensorMap m;
   uint32_t es[3] = {1, 1, 1};
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base),
+  const CUresult r = encode_fn()(&m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                 (cuuint32_t)rank, const_cast<void*>(base),
                                  dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError{"cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
@@ -1288,14 +1336,15 @@ CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uin
 
 // Row-blocked transposed buffer [J][nblk_alloc][rows][128] as a 4-D operand:
 // dims {128, rows, nblk_used, J}, box {32 (k), box_rows, 1, 1}.
-CUtensorMap map_blk(const float* base, uint64_t rows, uint64_t nblk_used, uint64_t nblk_alloc, uint64_t J,
-                    uint32_t box_rows) {
+CUtensorMap map_blk(const void* base, uint64_t rows, uint64_t nblk_used, uint64_t nblk_alloc, uint64_t J,
+                    uint32_t box_rows, int esz = 4) {
   const uint64_t dims[4] = {128, rows, nblk_used, J};
-  const uint64_t strides[3] = {128 * 4, rows * 128 * 4, nblk_alloc * rows * 128 * 4};
-  const uint32_t box[4] = {BK, box_rows, 1, 1};
+  const uint64_t strides[3] = {128 * (uint64_t)esz, rows * 128 * esz, nblk_alloc * rows * 128 * esz};
+  const uint32_t box[4] = {128u / esz, box_rows, 1, 1};
   CUtensorMap m;
   uint32_t es[4] = {1, 1, 1, 1};
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box,
+  const CUresult r = encode_fn()(&m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                                 const_cast<void*>(base), dims, strides, box,
                                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError{"cuTensorMapEncodeTiled (4d) failed (" + std::to_string((int)r) + ")"};
@@ -1303,19 +1352,19 @@ CUtensorMap map_blk(const float* base, uint64_t rows, uint64_t nblk_used, uint64
 }
 
 
-CUtensorMap map2d(const float* base, uint64_t inner, uint64_t rows, uint64_t ld, uint32_t box_rows) {
+CUtensorMap map2d(const void* base, uint64_t inner, uint64_t rows, uint64_t ld, uint32_t box_rows, int esz = 4) {
   const uint64_t dims[2] = {inner, rows};
-  const uint64_t strides[1] = {ld * 4};
-  const uint32_t box[2] = {BK, box_rows};
-  return make_map(base, 2, dims, strides, box);
+  const uint64_t strides[1] = {ld * esz};
+  const uint32_t box[2] = {128u / esz, box_rows};
+  return make_map(base, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, esz);
 }
 
-CUtensorMap map3d(const float* base, uint64_t inner, uint64_t rows, uint64_t ld, uint64_t J, uint64_t pstride,
-                  uint32_t box_rows) {
+CUtensorMap map3d(const void* base, uint64_t inner, uint64_t rows, uint64_t ld, uint64_t J, uint64_t pstride,
+                  uint32_t box_rows, int esz = 4) {
   const uint64_t dims[3] = {inner, rows, J};
-  const uint64_t strides[2] = {ld * 4, pstride * 4};
-  const uint32_t box[3] = {BK, box_rows, 1};
-  return make_map(base, 3, dims, strides, box);
+  const uint64_t strides[2] = {ld * esz, pstride * esz};
+  const uint32_t box[3] = {128u / esz, box_rows, 1};
+  return make_map(base, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, esz);
 }
 
 int round16(int v) { return (v + 15) / 16 * 16; }
@@ -1323,7 +1372,7 @@ int round16(int v) { return (v + 15) / 16 * 16; }
 // CL >= 1: tp.rtiles counts row groups (2 QB tiles) and tp.J particle groups (QA
 // particles); B's TMA box is tp.nmma / 2 rows per CTA (tp.bbox rows per piece
 // when QB = 2; tp.brows is ignored) and the grid is launched as clusters.
-template <int EPI, bool SPLIT, int AM, int CP = 4, int ACT = 0, int CL = 0>
+template <int EPI, bool SPLIT, int AM, int CP = 4, int ACT = 0, int CL = 0, int PREC = 0>
 void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUtensorMap& B, const CUtensorMap& Blo,
                TileParams tp, const FwdParams& fp, const DwParams& dp, size_t epi_smem_bytes) {
   using CS_ = ClusterShape<CL>;
@@ -1343,7 +1392,7 @@ void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUten
     tp.stage_bytes_tx = (uint32_t)(sub * ((size_t)BM * BK * 4 + (size_t)tp.brows * BK * 4));
   }
   const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16 + epi_smem_bytes + 64;
-  auto kern = tc_kernel<EPI, SPLIT, AM, CP, ACT, CL>;
+  auto kern = tc_kernel<EPI, SPLIT, AM, CP, ACT, CL, PREC>;
   static bool attr_set = false;
   static int max_clusters = 0;
   cudaLaunchConfig_t cfg{};
@@ -1386,6 +1435,7 @@ bool tc_layer1_eligible(const Ctx& c) {
   const NetDev& n = c.net;
   if (n.nconv != 0) return false;
   if (n.L == 2) return n.sizes[0] % 4 == 0 && n.sizes[0] >= 4 && n.sizes[1] <= 256 && n.sizes[2] <= 16;
+  if (c.precision == DASMC_PREC_F16) return false;  // fp16 operands: one-hidden-layer path only
   // deep path (tc_eval_deep): tf32, <= 16 classes, output layer weights in shared memory
   if (c.precision != DASMC_PREC_TF32 || n.sizes[n.L] > 16 || (int64_t)n.sizes[n.L - 1] * 16 > 16384) return false;
   for (int l = 0; l < n.L; ++l)
@@ -1403,16 +1453,19 @@ void tc_init(Ctx& c) {
   s->n1 = c.net.sizes[1];
   s->C = c.net.sizes[2];
   s->split = c.precision == DASMC_PREC_3XTF32;
+  s->f16 = c.precision == DASMC_PREC_F16;
+  s->esz = s->f16 ? 2 : 4;
   if (const char* e = std::getenv("DASMC_TC_CLUSTER")) s->cluster = std::max(0, std::min(4, std::atoi(e)));
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, dev));
   s->n_pad = (c.n + 31) / 32 * 32;
   const size_t xt = (size_t)(s->n0 + 1) * s->n_pad;
-  CK(cudaMalloc(&s->Xt, sizeof(float) * xt));
-  s->kx = (s->n0 + 1 + 3) / 4 * 4;
+  CK(cudaMalloc(&s->Xt, (size_t)s->esz * xt));
+  // [x, 1] padded so the row stride is a multiple of 16 bytes
+  s->kx = s->f16 ? (s->n0 + 1 + 7) / 8 * 8 : (s->n0 + 1 + 3) / 4 * 4;
   const size_t w = (size_t)c.Jmax * s->n1 * s->kx;
-  CK(cudaMalloc(&s->Xhi, sizeof(float) * (size_t)c.n * s->kx));
+  CK(cudaMalloc(&s->Xhi, (size_t)s->esz * c.n * s->kx));
   if (s->deep) {
     s->kxl[0] = s->kx;
     for (int l = 1; l <= s->L; ++l) {
@@ -1427,7 +1480,7 @@ void tc_init(Ctx& c) {
     }
     s->W1hi = s->Whi[1];
   } else {
-    CK(cudaMalloc(&s->W1hi, sizeof(float) * w));
+    CK(cudaMalloc(&s->W1hi, (size_t)s->esz * w));
   }
   if (s->split) {
     CK(cudaMalloc(&s->Xtlo, sizeof(float) * xt));
@@ -1435,8 +1488,13 @@ void tc_init(Ctx& c) {
     CK(cudaMalloc(&s->W1lo, sizeof(float) * w));
   }
   dim3 grid((unsigned)((s->n_pad + 31) / 32), (unsigned)((s->n0 + 1 + 31) / 32));
-  transpose_x_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(c.X, c.n, s->n0, s->n_pad, s->kx, s->Xt, s->Xtlo, s->Xhi,
-                                                         s->Xlo, s->split ? 1 : 0);
+  if (s->f16)
+    transpose_x_kernel<1><<<grid, dim3(32, 8), 0, c.stream>>>(
+        c.X, c.n, s->n0, s->n_pad, s->kx, reinterpret_cast<__half*>(s->Xt), nullptr, reinterpret_cast<__half*>(s->Xhi),
+        nullptr, 0);
+  else
+    transpose_x_kernel<0><<<grid, dim3(32, 8), 0, c.stream>>>(c.X, c.n, s->n0, s->n_pad, s->kx, s->Xt, s->Xtlo,
+                                                              s->Xhi, s->Xlo, s->split ? 1 : 0);
   LAUNCHED();
   CK(cudaStreamSynchronize(c.stream));
 }
@@ -1497,9 +1555,9 @@ void tc_ensure_rows(Ctx& c, int64_t Mcap) {
       *b = nullptr;
     }
   const size_t J = (size_t)c.Jmax;
-  CK(cudaMalloc(&s->a1T, sizeof(float) * J * (s->n1 + 1) * Mcap));
-  CK(cudaMalloc(&s->d1T, sizeof(float) * J * s->n1 * Mcap));
-  CK(cudaMalloc(&s->d2T, sizeof(float) * J * s->C * Mcap));
+  CK(cudaMalloc(&s->a1T, (size_t)s->esz * J * (s->n1 + 1) * Mcap));
+  CK(cudaMalloc(&s->d1T, (size_t)s->esz * J * s->n1 * Mcap));
+  CK(cudaMalloc(&s->d2T, (size_t)s->esz * J * s->C * Mcap));
   if (s->split) {
     CK(cudaMalloc(&s->a1Tlo, sizeof(float) * J * (s->n1 + 1) * Mcap));
     CK(cudaMalloc(&s->d1Tlo, sizeof(float) * J * s->n1 * Mcap));
@@ -1507,7 +1565,11 @@ void tc_ensure_rows(Ctx& c, int64_t Mcap) {
   }
   s->mcap = Mcap;
   const int g = (int)std::min<int64_t>((J * Mcap + 255) / 256, 148 * 16);
-  fill_ones_row_kernel<<<g, 256, 0, c.stream>>>(s->a1T, (int64_t)J, s->n1 + 1, s->n1, Mcap, 1.f);
+  if (s->f16)
+    fill_ones_row_kernel<<<g, 256, 0, c.stream>>>(reinterpret_cast<__half*>(s->a1T), (int64_t)J, s->n1 + 1, s->n1,
+                                                  Mcap, 1.f);
+  else
+    fill_ones_row_kernel<<<g, 256, 0, c.stream>>>(s->a1T, (int64_t)J, s->n1 + 1, s->n1, Mcap, 1.f);
   LAUNCHED();
   if (s->split) {
     fill_ones_row_kernel<<<g, 256, 0, c.stream>>>(s->a1Tlo, (int64_t)J, s->n1 + 1, s->n1, Mcap, 0.f);
@@ -1534,7 +1596,7 @@ void tc_eval_deep(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P
   for (int l = 1; l < L; ++l) {
     const LayerDev& ly = net.layer[l - 1];
     const int64_t cnt = (int64_t)s->sz[l] * s->kxl[l - 1];
-    split_w1_kernel<<<(int)std::min<int64_t>(J * s->sz[l], 148 * 64), 256, 0, c.stream>>>(
+    split_w1_kernel<0><<<(int)std::min<int64_t>(J * s->sz[l], 148 * 64), 256, 0, c.stream>>>(
         theta_in, net.Dp, ly.woff, ly.boff, s->sz[l - 1], s->kxl[l - 1], cnt, J, s->Whi[l], nullptr);
     LAUNCHED();
   }
@@ -1669,13 +1731,14 @@ void tc_eval_deep(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P
   }
 }
 
-void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, double beta_rows, bool need_grad,
-             const EpiParams* epi) {
+// The one-hidden-layer path (fused forward + two weight-gradient GEMMs); PREC 0 = tf32 /
+// split-tf32 operands in fp32 containers, PREC 1 = fp16 operands (kind::f16).
+template <int PREC>
+void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, double beta_rows, bool need_grad,
+                   const EpiParams* epi) {
   TcState* s = c.tc;
-  if (s->deep) {
-    tc_eval_deep(c, theta_in, J, M, P, beta_rows, need_grad, epi);
-    return;
-  }
+  constexpr int BKE = PREC == 1 ? 64 : 32;
+  const int esz = PREC == 1 ? 2 : 4;
   const NetDev& net = c.net;
   const LayerDev& l1 = net.layer[0];
   const LayerDev& l2 = net.layer[1];
@@ -1689,8 +1752,9 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     // [W1, b1] -> tf32 (rna) hi [+ lo]: the MMA would otherwise truncate the low mantissa
     // bits; the bias rides along as K column n0 against X's ones column
     const int64_t kx = s->kx, cnt = (int64_t)n1 * kx;
-    split_w1_kernel<<<(int)std::min<int64_t>(J * n1, 148 * 64), 256, 0, c.stream>>>(
-        theta_in, net.Dp, l1.woff, l1.boff, n0, kx, cnt, J, s->W1hi, s->split ? s->W1lo : nullptr);
+    split_w1_kernel<PREC><<<(int)std::min<int64_t>(J * n1, 148 * 64), 256, 0, c.stream>>>(
+        theta_in, net.Dp, l1.woff, l1.boff, n0, kx, cnt, J, reinterpret_cast<OpT<PREC>*>(s->W1hi),
+        PREC == 0 && s->split ? s->W1lo : nullptr);
     LAUNCHED();
     // rows >= M of X are TMA zero fill (ones column included): z1 = 0 there
     // cluster shape (see ClusterShape): CTA pairs stream half of W1's rows each (box
@@ -1702,9 +1766,9 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     const int half = round16(n1) / 2;
     const int bpiece = QB == 2 ? (half / 2 + 7) / 8 * 8 : half;
     const uint32_t bbox = pair ? (uint32_t)bpiece : (uint32_t)n1;
-    const CUtensorMap A = map2d(s->Xhi, n0 + 1, M, kx, BM / QA);
+    const CUtensorMap A = map2d(s->Xhi, n0 + 1, M, kx, BM / QA, esz);
     const CUtensorMap Alo = s->split ? map2d(s->Xlo, n0 + 1, M, kx, BM / QA) : A;
-    const CUtensorMap B = map3d(s->W1hi, n0 + 1, n1, kx, J, cnt, bbox);
+    const CUtensorMap B = map3d(s->W1hi, n0 + 1, n1, kx, J, cnt, bbox, esz);
     const CUtensorMap Blo = s->split ? map3d(s->W1lo, n0 + 1, n1, kx, J, cnt, bbox) : B;
     TileParams tp{};
     tp.rtiles = pair ? (rtiles + 2 * QB - 1) / (2 * QB) : rtiles;
@@ -1716,7 +1780,7 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     if (const char* e = std::getenv("DASMC_TC_HINTA")) tp.hint_a = std::atoi(e);        // tuning only
     if (const char* e = std::getenv("DASMC_TC_HINTB")) tp.hint_b = std::atoi(e);        // tuning only
     if (const char* e = std::getenv("DASMC_TC_PREFETCH")) tp.prefetch = std::atoi(e);   // tuning only
-    tp.nkb = (n0 + 1 + BK - 1) / BK;
+    tp.nkb = (n0 + 1 + BKE - 1) / BKE;
     tp.nmma = round16(n1);
     tp.brows = n1;
     FwdParams fp{};
@@ -1750,19 +1814,21 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     DwParams dp{};
     auto go = [&](auto cp, auto act) {
       constexpr int K = decltype(cp)::value, A_ = decltype(act)::value;
-      if (s->split) {
-        if (pair)
-          launch_tc<kEpiKindFwd, true, kAShared, K, A_, 1>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
-        else
-          launch_tc<kEpiKindFwd, true, kAShared, K, A_, 0>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
-      } else {
-        switch (cl) {
-          case 0: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 0>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
-          case 1: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 1>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
-          case 2: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 2>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
-          case 3: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 3>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
-          default: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 4>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+      if constexpr (PREC == 0) {
+        if (s->split) {
+          if (pair)
+            launch_tc<kEpiKindFwd, true, kAShared, K, A_, 1>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+          else
+            launch_tc<kEpiKindFwd, true, kAShared, K, A_, 0>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+          return;
         }
+      }
+      switch (cl) {
+        case 0: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 0, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+        case 1: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 1, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+        case 2: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 2, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+        case 3: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 3, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+        default: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 4, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
       }
     };
     auto go_act = [&](auto cp) {
@@ -1782,44 +1848,55 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
   // ---- layer 2: dW2^T[o, c] = sum_m a1^T[o, m] delta2^T[c, m]  (ones row o = n1 -> db2)
   {
     const uint64_t nbu = (uint64_t)(M + 127) / 128, nba = (uint64_t)ldm / 128;
-    const CUtensorMap A = map_blk(s->a1T, n1 + 1, nbu, nba, J, BM);
+    const CUtensorMap A = map_blk(s->a1T, n1 + 1, nbu, nba, J, BM, esz);
     const CUtensorMap Alo = s->split ? map_blk(s->a1Tlo, n1 + 1, nbu, nba, J, BM) : A;
-    const CUtensorMap B = map_blk(s->d2T, C, nbu, nba, J, C);
+    const CUtensorMap B = map_blk(s->d2T, C, nbu, nba, J, C, esz);
     const CUtensorMap Blo = s->split ? map_blk(s->d2Tlo, C, nbu, nba, J, C) : B;
     TileParams tp{};
     tp.rtiles = (n1 + 1 + BM - 1) / BM;
     tp.J = (int)J;
     tp.rg = tp.rtiles;
-    tp.nkb = (int)((M + BK - 1) / BK);
+    tp.nkb = (int)((M + BKE - 1) / BKE);
     tp.nmma = round16(C);
     tp.brows = C;
     DwParams dp{*epi, net.Dp, l2.woff, l2.boff, n1, C};
-    if (s->split)
-      launch_tc<kEpiKindDw, true, kABlocked>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+    if (PREC == 0 && s->split)
+      launch_tc<kEpiKindDw, PREC == 0, kABlocked>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
     else
-      launch_tc<kEpiKindDw, false, kABlocked>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+      launch_tc<kEpiKindDw, false, kABlocked, 4, 0, 0, PREC>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
   }
   // ---- layer 1: dW1^T[i, o] = sum_m X^T[i, m] delta1^T[o, m]  (ones row i = n0 -> db1)
   {
     KTimer kt(c, 1);
-    const CUtensorMap A = map2d(s->Xt, M, n0 + 1, s->n_pad, BM);
+    const CUtensorMap A = map2d(s->Xt, M, n0 + 1, s->n_pad, BM, esz);
     const CUtensorMap Alo = s->split ? map2d(s->Xtlo, M, n0 + 1, s->n_pad, BM) : A;
     const uint64_t nbu = (uint64_t)(M + 127) / 128, nba = (uint64_t)ldm / 128;
-    const CUtensorMap B = map_blk(s->d1T, n1, nbu, nba, J, n1);
+    const CUtensorMap B = map_blk(s->d1T, n1, nbu, nba, J, n1, esz);
     const CUtensorMap Blo = s->split ? map_blk(s->d1Tlo, n1, nbu, nba, J, n1) : B;
     TileParams tp{};
     tp.rtiles = (n0 + 1 + BM - 1) / BM;
     tp.J = (int)J;
     tp.rg = tp.rtiles;
-    tp.nkb = (int)((M + BK - 1) / BK);
+    tp.nkb = (int)((M + BKE - 1) / BKE);
     tp.nmma = round16(n1);
     tp.brows = n1;
     DwParams dp{*epi, net.Dp, l1.woff, l1.boff, n0, n1};
-    if (s->split)
-      launch_tc<kEpiKindDw, true, kAShared>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+    if (PREC == 0 && s->split)
+      launch_tc<kEpiKindDw, PREC == 0, kAShared>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
     else
-      launch_tc<kEpiKindDw, false, kAShared>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+      launch_tc<kEpiKindDw, false, kAShared, 4, 0, 0, PREC>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
   }
+}
+
+void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, double beta_rows, bool need_grad,
+             const EpiParams* epi) {
+  TcState* s = c.tc;
+  if (s->deep)
+    tc_eval_deep(c, theta_in, J, M, P, beta_rows, need_grad, epi);
+  else if (s->f16)
+    tc_eval_fused<1>(c, theta_in, J, M, P, beta_rows, need_grad, epi);
+  else
+    tc_eval_fused<0>(c, theta_in, J, M, P, beta_rows, need_grad, epi);
 }
 
 }  // namespace dasmc_b200

@@ -7,7 +7,9 @@ Stated tolerances, measured on B200:
     tensor core's fp32 accumulation (it grows with the number of k-steps),
     not operand rounding;
   * plain tf32 (rna-rounded operands, 1 MMA): values 2e-4; gradients
-    normwise < 6e-3, max_rel_error < 0.5.
+    normwise < 6e-3, max_rel_error < 0.5;
+  * f16 (fp16 operands, kind::f16: the same 10-bit mantissa as tf32, fp32
+    accumulation): the tf32 bounds.
 The fp32 CUDA-core path (test_gpu_parity.py) is the 1e-4 parity path.
 """
 import numpy as np
@@ -33,7 +35,7 @@ def problem(product, layers, act, n):
     return spec, X, y
 
 
-@pytest.mark.parametrize("prec", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("prec", ["3xtf32", "tf32", "f16"])
 @pytest.mark.parametrize("layers,act,M", SHAPES)
 def test_tc_value_and_grad(product, oracle, layers, act, M, prec):
     n = max(M, 600)
@@ -94,8 +96,9 @@ def test_tc_run_matches_fp32_schedule(product):
     np.testing.assert_allclose(r3x[0]["mean_log_target"], r32[0]["mean_log_target"], rtol=1e-5)
 
 
+@pytest.mark.parametrize("prec", ["tf32", "f16"])
 @pytest.mark.parametrize("cluster", [0, 1, 2, 3, 4])
-def test_tc_cluster_shapes(product, oracle, cluster, monkeypatch):
+def test_tc_cluster_shapes(product, oracle, cluster, prec, monkeypatch):
     """Every fused-forward cluster shape (single CTAs, CTA pairs, pairs with X or W1
     multicast, both) gives the same gradients; odd J and M leave padding tiles."""
     monkeypatch.setenv("DASMC_TC_CLUSTER", str(cluster))
@@ -104,7 +107,7 @@ def test_tc_cluster_shapes(product, oracle, cluster, monkeypatch):
     spec, X, y = problem(product, layers, act, n)
     D = product.param_count(spec)
     th = (0.5 * np.random.default_rng(7).standard_normal((J, D))).astype(np.float32).astype(np.float64)
-    t = product.GpuEnsembleTarget(spec, X, y, J, precision="tf32")
+    t = product.GpuEnsembleTarget(spec, X, y, J, precision=prec)
     t.set_target(0, M, n, "scaled", 1.0, 1.0)
     v, g = t.log_target_with_grad(th)
     vo, go = oracle.value_and_grad(layers, 0, X.astype(np.float64), y, (0, M, n), 0, 1.0, 1.0, th)
