@@ -137,6 +137,8 @@ typedef struct {
   double resample_fraction;
   int resample_kind;
   int resample_always; /* [EXT] Appendix A.7 */
+  int redraw_constant; /* ScheduleConfig::redraw_constant: a fresh batch of initial_batch rows per
+                          iteration (runner.hpp:531-556) */
 } dasmc_run_cfg;
 
 /* Last error message of the calling thread. */
@@ -212,6 +214,24 @@ double dasmc_sda_beta_step(double beta, double* entropy_step, double denom); /* 
 int dasmc_sda_advance_with(const dasmc_schedule* cfg, dasmc_sda_state* state, const double* moments6);
 int dasmc_sda_moments_from(const double* prefix_nll, const double* block_nll, const double* log_weights,
                            int64_t J, double* out6);
+
+/* ---- IDX data files (dataset.hpp:84-196) -----------------------------------------------
+ * parse_idx / load_idx: an IDX image (magic 0x803) + label (0x801) pair -> n rows of
+ * rows*cols pixels / 255 (fp32) and labels; gzip files are decompressed transparently.
+ * Malformed input returns DASMC_EINVAL with the reference's FormatError message.  Call with
+ * X == NULL / y == NULL to query n, d and num_classes first. */
+int dasmc_parse_idx(const uint8_t* image_bytes, int64_t image_len, const uint8_t* label_bytes, int64_t label_len,
+                    int64_t* n, int64_t* d, int* num_classes, float* X, int32_t* y);
+int dasmc_load_idx(const char* image_path, const char* label_path, int64_t* n, int64_t* d, int* num_classes, float* X,
+                   int32_t* y);
+
+/* ---- constant-redraw batches (runner.hpp:531-556) ---------------------------------------
+ * rows = draw_batch_rows(k): the first `count` entries of a partial Fisher-Yates shuffle of
+ * 0..n-1 with root.fork(kRedraw, k) (bit-exact); dasmc_gpu_set_rows makes the target read
+ * train[rows[0..count)] (gathered on the device; rows == NULL restores the resident set).
+ * The window is then {0, count, N} as in context_for. */
+int dasmc_redraw_rows(uint64_t seed, int k, int64_t n, int64_t count, int64_t* rows);
+int dasmc_gpu_set_rows(dasmc_ctx* ctx, const int64_t* rows, int64_t count);
 
 /* ---- evaluate_predictive (runner.hpp:331-364) ------------------------------------------
  * Ensemble-averaged predictive of the context's current ensemble on a labelled test set

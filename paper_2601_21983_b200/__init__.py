@@ -6,5 +6,6 @@ thin Python mirror of the reference's sampler API used by tests and bench.py.
 """
 from .api import (GpuEnsembleTarget, KernelConfig, NetSpec, RunConfig, ScheduleConfig, batch_size,  # noqa: F401
                   make_teacher_data, param_count, run_experiment, sda_advance_with, sda_beta_step, sda_init,
-                  predictive_metrics, sda_moments_from, shuffle_permutation)
+                  load_idx, parse_idx, predictive_metrics, redraw_rows, sda_moments_from,
+                  shuffle_permutation)
 from ._lib import LIB_PATH, SamplerError, load  # noqa: F401

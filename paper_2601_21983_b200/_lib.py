@@ -83,6 +83,7 @@ class RunCfg(C.Structure):
         ("resample_fraction", C.c_double),
         ("resample_kind", C.c_int),
         ("resample_always", C.c_int),
+        ("redraw_constant", C.c_int),
     ]
 
 
@@ -137,6 +138,11 @@ SIGNATURES = {
     "dasmc_gpu_evaluate_predictive": (C.c_int, [_P, _F, _I32, C.c_int64, _D, _D]),
     "dasmc_gpu_predictive_mix": (C.c_int, [_P, _F, _I32, C.c_int64, _D, C.c_int64, _D]),
     "dasmc_predictive_metrics": (C.c_int, [_D, _I32, C.c_int64, C.c_int, _D, _D]),
+    "dasmc_parse_idx": (C.c_int, [C.c_char_p, C.c_int64, C.c_char_p, C.c_int64, _I64, _I64, C.POINTER(C.c_int), _F,
+                                  _I32]),
+    "dasmc_load_idx": (C.c_int, [C.c_char_p, C.c_char_p, _I64, _I64, C.POINTER(C.c_int), _F, _I32]),
+    "dasmc_redraw_rows": (C.c_int, [C.c_uint64, C.c_int, C.c_int64, C.c_int64, _I64]),
+    "dasmc_gpu_set_rows": (C.c_int, [_P, _I64, C.c_int64]),
     "dasmc_gpu_run": (C.c_int, [C.POINTER(NetDesc), _F, _I32, C.c_int64, C.POINTER(RunCfg), C.c_int, C.c_int,
                                 C.POINTER(IterRecord), C.POINTER(SdaState), _D, _D]),
 }

@@ -178,6 +178,32 @@ def make_teacher_data(spec: NetSpec, n: int, feature_kind: int, seed: int, cfg_i
     return X, y
 
 
+def _idx(call):
+    n, d, nc = C.c_int64(), C.c_int64(), C.c_int()
+    L.check(call(C.byref(n), C.byref(d), C.byref(nc), None, None))
+    X = np.empty((n.value, d.value), dtype=np.float32)
+    y = np.empty(n.value, dtype=np.int32)
+    L.check(call(C.byref(n), C.byref(d), C.byref(nc), _fp(X), _ip(y)))
+    return X, y, nc.value
+
+
+def parse_idx(image_bytes: bytes, label_bytes: bytes):  # dataset.hpp:84-131
+    """(X [n, rows*cols] fp32 pixels/255, y int32, num_classes) from IDX byte streams."""
+    return _idx(lambda n, d, nc, X, y: L.load().dasmc_parse_idx(image_bytes, len(image_bytes), label_bytes,
+                                                                len(label_bytes), n, d, nc, X, y))
+
+
+def load_idx(image_path: str, label_path: str):  # dataset.hpp:186-196 (gzip transparent)
+    return _idx(lambda n, d, nc, X, y: L.load().dasmc_load_idx(image_path.encode(), label_path.encode(), n, d, nc,
+                                                               X, y))
+
+
+def redraw_rows(seed: int, k: int, n: int, count: int) -> np.ndarray:  # runner.hpp:531-542
+    r = np.empty(count, dtype=np.int64)
+    L.check(L.load().dasmc_redraw_rows(seed, k, n, count, r.ctypes.data_as(L._I64)))
+    return r
+
+
 def shuffle_permutation(seed: int, n: int) -> np.ndarray:  # runner.hpp:486-489
     p = np.empty(n, dtype=np.int64)
     L.check(L.load().dasmc_shuffle_permutation(seed, n, p.ctypes.data_as(L._I64)))
@@ -303,6 +329,13 @@ class GpuEnsembleTarget:
         L.check(self.lib.dasmc_gpu_sda_moments(self.h, prefix_end, block_end, _dp(out)))
         return out
 
+    def set_rows(self, rows: Optional[np.ndarray]):  # runner.hpp:548-557 redraw batch (None: resident set)
+        if rows is None:
+            L.check(self.lib.dasmc_gpu_set_rows(self.h, None, 0))
+        else:
+            r = np.ascontiguousarray(rows, dtype=np.int64)
+            L.check(self.lib.dasmc_gpu_set_rows(self.h, r.ctypes.data_as(L._I64), r.shape[0]))
+
     def evaluate_predictive(self, X_test: np.ndarray, y_test: np.ndarray):  # runner.hpp:331-364
         """(mean log predictive probability of the true label, accuracy %) of the current ensemble."""
         X = np.ascontiguousarray(X_test, dtype=np.float32)
@@ -344,6 +377,7 @@ class RunConfig:  # runner.hpp:57-70 (hot-loop subset)
     resample_fraction: float = 0.5
     resample: str = "multinomial"
     resample_always: bool = False
+    redraw: bool = False  # ScheduleConfig::redraw_constant (runner.hpp:531-556)
 
 
 def run_experiment(spec: NetSpec, X: np.ndarray, y: np.ndarray, cfg: RunConfig, device: int = 0,
@@ -354,7 +388,7 @@ def run_experiment(spec: NetSpec, X: np.ndarray, y: np.ndarray, cfg: RunConfig, 
     y = np.ascontiguousarray(y, dtype=np.int32)
     rc = L.RunCfg(cfg.kernel.c(), cfg.schedule.c(), cfg.sigma, cfg.beta0, cfg.entropy_step, cfg.particles,
                   cfg.iterations, cfg.seed, cfg.resample_fraction, _RESAMPLE[cfg.resample],
-                  1 if cfg.resample_always else 0)
+                  1 if cfg.resample_always else 0, 1 if cfg.redraw else 0)
     recs = (L.IterRecord * cfg.iterations)()
     sda = (L.SdaState * cfg.iterations)()
     D = param_count(spec)

@@ -136,7 +136,7 @@ void free_ctx(Ctx& c) {
   cudaSetDevice(c.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
   tc_free(c);
-  void* ptrs[] = {c.X, c.Xt, c.y, c.theta[0], c.theta[1], c.theta[2], c.p, c.grad, c.logw, c.dT, c.ll_part,
+  void* ptrs[] = {c.X_full, c.Xt, c.y_full, c.Xg, c.yg, c.rows_dev, c.theta[0], c.theta[1], c.theta[2], c.p, c.grad, c.logw, c.dT, c.ll_part,
                   c.th_part, c.p_part, c.p0_part, c.flags, c.lt_old, c.lt_new, c.ll_pre, c.ll_blk, c.wts, c.cdf,
                   c.uni, c.idx, c.records, c.jump_tab, c.stage, c.sh_buf, c.sh_idx, c.sh_rows, c.iota};
   for (void* p : ptrs)
@@ -165,7 +165,7 @@ void validate_target(const Ctx& c) {  // target.hpp:104-113
   if (c.prefix_end < 0 || c.prefix_end > c.block_end || c.block_end > c.total_n)
     throw InvalidArg("SubsetWindow: need 0 <= prefix_end <= block_end <= total_n");
   if (c.block_end < 1) throw InvalidArg("TargetContext: empty subset");
-  if (c.block_end > c.n) throw InvalidArg("TargetContext: window exceeds dataset");
+  if (c.block_end > c.n_active) throw InvalidArg("TargetContext: window exceeds dataset");
   if (c.mode == DASMC_SDA && !(c.beta > 0.0 && c.beta <= 1.0))
     throw InvalidArg("TargetContext: sda mode needs beta in (0, 1]");
   if (c.mode != DASMC_SCALED && c.mode != DASMC_SDA) throw InvalidArg("TargetContext: bad mode");
@@ -367,6 +367,9 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
   dmalloc(c.y, (size_t)n);
   CK(cudaMemcpy(c.X, X, sizeof(float) * (size_t)n * n0, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c.y, y, sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice));
+  c.X_full = c.X;
+  c.y_full = c.y;
+  c.n_active = n;
   const size_t pe = (size_t)Jmax * c.net.Dp;
   for (auto& t : c.theta) {
     dmalloc(t, pe);
@@ -455,6 +458,33 @@ int dasmc_gpu_destroy(dasmc_ctx* ctx) {
 }
 
 int dasmc_gpu_param_count(const dasmc_ctx* ctx) { return ctx ? (int)ctx->c.net.D : -1; }
+
+// The target's data rows: the resident set (rows == NULL) or train[rows[0..count)] gathered
+// on the device (the constant-redraw batch, runner.hpp:531-556).
+void set_rows_dev(Ctx& c, const int64_t* rows, int64_t count) {
+  if (rows == nullptr || count <= 0) {
+    if (c.X == c.X_full) return;
+    c.X = c.X_full;
+    c.y = c.y_full;
+    c.n_active = c.n;
+  } else {
+    for (int64_t i = 0; i < count; ++i)
+      if (rows[i] < 0 || rows[i] >= c.n) throw InvalidArg("set_rows: row out of range");
+    if (count > c.n) throw InvalidArg("set_rows: more rows than the dataset");
+    const int64_t d = input_floats(c.net);
+    if (!c.Xg) {
+      dmalloc(c.Xg, (size_t)c.n * d);
+      dmalloc(c.yg, (size_t)c.n);
+      dmalloc(c.rows_dev, (size_t)c.n);
+    }
+    CK(cudaMemcpyAsync(c.rows_dev, rows, sizeof(int64_t) * count, cudaMemcpyHostToDevice, c.stream));
+    launch_gather_data(c, c.X_full, c.y_full, c.rows_dev, count, d, c.Xg, c.yg);
+    c.X = c.Xg;
+    c.y = c.yg;
+    c.n_active = count;
+  }
+  if (c.tc) tc_refresh_data(c);
+}
 
 int dasmc_gpu_set_target(dasmc_ctx* ctx, int64_t prefix_end, int64_t block_end, int64_t total_n, int mode,
                          double beta, double sigma) {
@@ -1072,6 +1102,50 @@ int dasmc_gpu_evaluate_predictive(dasmc_ctx* ctx, const float* X_test, const int
   });
 }
 
+int dasmc_gpu_set_rows(dasmc_ctx* ctx, const int64_t* rows, int64_t count) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg("null ctx");
+    Ctx& c = ctx->c;
+    CK(cudaSetDevice(c.device));
+    set_rows_dev(c, rows, count);
+  });
+}
+
+// load_idx / parse_idx (dataset.hpp:84-196).  With X == NULL only the sizes are returned.
+static int idx_out(const IdxData& d, int64_t* n, int64_t* dim, int* classes, float* X, int32_t* y) {
+  if (n) *n = d.n;
+  if (dim) *dim = d.d;
+  if (classes) *classes = d.num_classes;
+  if (X) std::memcpy(X, d.X.data(), sizeof(float) * d.X.size());
+  if (y) std::memcpy(y, d.y.data(), sizeof(int32_t) * d.y.size());
+  return DASMC_OK;
+}
+
+int dasmc_parse_idx(const uint8_t* image_bytes, int64_t image_len, const uint8_t* label_bytes, int64_t label_len,
+                    int64_t* n, int64_t* d, int* num_classes, float* X, int32_t* y) {
+  return guarded([&] {
+    if ((!image_bytes && image_len) || (!label_bytes && label_len)) throw InvalidArg("null buffer");
+    const std::vector<unsigned char> im(image_bytes, image_bytes + image_len), lb(label_bytes, label_bytes + label_len);
+    idx_out(parse_idx(im, lb), n, d, num_classes, X, y);
+  });
+}
+
+int dasmc_load_idx(const char* image_path, const char* label_path, int64_t* n, int64_t* d, int* num_classes, float* X,
+                   int32_t* y) {
+  return guarded([&] {
+    if (!image_path || !label_path) throw InvalidArg("null path");
+    idx_out(parse_idx(read_file_bytes(image_path), read_file_bytes(label_path)), n, d, num_classes, X, y);
+  });
+}
+
+int dasmc_redraw_rows(uint64_t seed, int k, int64_t n, int64_t count, int64_t* rows) {
+  return guarded([&] {
+    if (n < 1 || count < 1 || count > n || !rows) throw InvalidArg("bad argument");
+    const auto r = redraw_rows(seed, k, n, count);
+    std::memcpy(rows, r.data(), sizeof(int64_t) * (size_t)count);
+  });
+}
+
 int dasmc_gpu_run(const dasmc_net_desc* net, const float* X, const int32_t* y, int64_t n, const dasmc_run_cfg* cfg,
                   int device, int precision, dasmc_iter_record* records, dasmc_sda_state* sda_trace,
                   double* final_theta, double* final_log_weights) {
@@ -1109,6 +1183,13 @@ int dasmc_gpu_run(const dasmc_net_desc* net, const float* X, const int32_t* y, i
         c.prefix_end = st.prefix_end;
         c.block_end = st.block_end;
         c.beta = st.beta;
+      } else if (cfg->redraw_constant) {  // runner.hpp:548-557: a fresh batch per iteration
+        const auto rows = redraw_rows(cfg->seed, k, n, sched.initial_batch);
+        set_rows_dev(c, rows.data(), (int64_t)rows.size());
+        c.mode = DASMC_SCALED;
+        c.prefix_end = 0;
+        c.block_end = sched.initial_batch;
+        c.beta = 1.0;
       } else {
         c.mode = DASMC_SCALED;
         c.prefix_end = 0;

@@ -118,10 +118,17 @@ struct Ctx {
   int mode = DASMC_SCALED;
   double beta = 1.0, sigma = 1.0;
 
-  // data
+  // data: X / y are the ACTIVE rows the target reads (the resident set, or a gathered
+  // redraw batch in Xg / yg -- runner.hpp:531-556)
   float* X = nullptr;
   float* Xt = nullptr;
   int32_t* y = nullptr;
+  float* X_full = nullptr;
+  int32_t* y_full = nullptr;
+  float* Xg = nullptr;
+  int32_t* yg = nullptr;
+  int64_t* rows_dev = nullptr;
+  int64_t n_active = 0;  // rows of the active data
 
   // ensemble
   float* theta[3] = {nullptr, nullptr, nullptr};
@@ -239,6 +246,9 @@ void launch_normalize_resample(Ctx& c, int64_t Jtot, double* lw_full, const doub
                                const double* uni, int32_t* idx, double fraction, int always, int kind, int rec_slot,
                                int k);
 void launch_rows(Ctx& c, const float* src, float* dst, const int32_t* rows_dev, int64_t n, bool pack);
+// dst rows i = src rows rows[i] (data rows of d floats + labels): the redraw gather
+void launch_gather_data(Ctx& c, const float* X, const int32_t* y, const int64_t* rows, int64_t count, int64_t d,
+                        float* Xd, int32_t* yd);
 void launch_resample_hook(Ctx& c, const double* w, const double* u, int64_t J, int kind, int32_t* idx);
 
 }  // namespace dasmc_b200

@@ -1,9 +1,15 @@
 // Host-side pieces of the B200 driver (see host.h).
 #include "host.h"
 
+#include <zlib.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <iterator>
 #include <stdexcept>
+#include <string>
 #include <thread>
 
 namespace dasmc_b200 {
@@ -274,6 +280,106 @@ std::vector<int64_t> shuffle_permutation(uint64_t seed, int64_t n) {  // dataset
     const auto j = (int64_t)r.uniform_below((uint64_t)(i + 1));
     std::swap(order[(size_t)i], order[(size_t)j]);
   }
+  return order;
+}
+
+// ---- IDX data files (dataset.hpp:84-196) -------------------------------------------------
+namespace {
+uint32_t read_be32(const std::vector<unsigned char>& b, size_t off, const char* field) {
+  if (off + 4 > b.size())
+    throw FormatError(std::string("IDX: truncated while reading ") + field + " at offset " + std::to_string(off));
+  return (uint32_t(b[off]) << 24) | (uint32_t(b[off + 1]) << 16) | (uint32_t(b[off + 2]) << 8) | uint32_t(b[off + 3]);
+}
+
+std::vector<unsigned char> gunzip(const std::vector<unsigned char>& in) {
+  z_stream zs{};
+  if (inflateInit2(&zs, 15 + 16) != Z_OK) throw FormatError("gzip: inflateInit failed");
+  std::vector<unsigned char> out;
+  out.reserve(in.size() * 4);
+  std::vector<unsigned char> buf(1 << 16);
+  zs.next_in = const_cast<unsigned char*>(in.data());
+  zs.avail_in = (uInt)in.size();
+  int rc = Z_OK;
+  do {
+    zs.next_out = buf.data();
+    zs.avail_out = (uInt)buf.size();
+    rc = inflate(&zs, Z_NO_FLUSH);
+    if (rc != Z_OK && rc != Z_STREAM_END) {
+      inflateEnd(&zs);
+      throw FormatError("gzip: corrupt stream (zlib rc " + std::to_string(rc) + ")");
+    }
+    out.insert(out.end(), buf.data(), buf.data() + (buf.size() - zs.avail_out));
+    if (rc != Z_STREAM_END && zs.avail_in == 0 && zs.avail_out != 0) {
+      inflateEnd(&zs);
+      throw FormatError("gzip: truncated stream");
+    }
+  } while (rc != Z_STREAM_END);
+  inflateEnd(&zs);
+  return out;
+}
+}  // namespace
+
+IdxData parse_idx(const std::vector<unsigned char>& img, const std::vector<unsigned char>& lab) {
+  constexpr uint32_t kImageMagic = 0x00000803, kLabelMagic = 0x00000801;
+  const uint32_t im = read_be32(img, 0, "image magic");
+  if (im != kImageMagic) {
+    char buf[96];
+    std::snprintf(buf, sizeof(buf), "IDX image magic: expected 0x%08x, got 0x%08x at offset 0", kImageMagic, im);
+    throw FormatError(buf);
+  }
+  const uint32_t n = read_be32(img, 4, "image count");
+  const uint32_t rows = read_be32(img, 8, "image rows");
+  const uint32_t cols = read_be32(img, 12, "image cols");
+  const size_t pixels = size_t(n) * rows * cols;
+  if (img.size() != 16 + pixels)
+    throw FormatError("IDX image payload: expected " + std::to_string(16 + pixels) + " bytes, got " +
+                      std::to_string(img.size()));
+  const uint32_t lm = read_be32(lab, 0, "label magic");
+  if (lm != kLabelMagic) {
+    char buf[96];
+    std::snprintf(buf, sizeof(buf), "IDX label magic: expected 0x%08x, got 0x%08x at offset 0", kLabelMagic, lm);
+    throw FormatError(buf);
+  }
+  const uint32_t nl = read_be32(lab, 4, "label count");
+  if (lab.size() != 8 + size_t(nl))
+    throw FormatError("IDX label payload: expected " + std::to_string(8 + size_t(nl)) + " bytes, got " +
+                      std::to_string(lab.size()));
+  if (nl != n)
+    throw FormatError("IDX count mismatch: " + std::to_string(n) + " images vs " + std::to_string(nl) + " labels");
+  IdxData d;
+  d.n = n;
+  d.d = (int64_t)rows * cols;
+  d.X.resize(pixels);
+  d.y.resize(n);
+  int max_label = 0;
+  for (size_t p = 0; p < pixels; ++p) d.X[p] = (float)((double)img[16 + p] / 255.0);
+  for (uint32_t i = 0; i < n; ++i) {
+    d.y[i] = lab[8 + i];
+    max_label = std::max(max_label, (int)d.y[i]);
+  }
+  d.num_classes = max_label + 1;
+  return d;
+}
+
+std::vector<unsigned char> read_file_bytes(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw FormatError("cannot open file: " + path);
+  std::vector<unsigned char> bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  if (bytes.size() >= 2 && bytes[0] == 0x1f && bytes[1] == 0x8b) return gunzip(bytes);
+  return bytes;
+}
+
+// draw_batch_rows (runner.hpp:531-542): partial Fisher-Yates over 0..n-1 with the
+// stream root.fork(kRedraw, k), i = 0..count-1, j = i + uniform_below(n - i).
+std::vector<int64_t> redraw_rows(uint64_t seed, int k, int64_t n, int64_t count) {
+  std::vector<int64_t> order((size_t)n);
+  for (int64_t i = 0; i < n; ++i) order[(size_t)i] = i;
+  HostRng r(fork_key(seed, tag::kRedraw, (uint64_t)k, 0));
+  for (int64_t i = 0; i < count; ++i) {
+    const auto j = i + (int64_t)r.uniform_below((uint64_t)(n - i));
+    std::swap(order[(size_t)i], order[(size_t)j]);
+  }
+  order.resize((size_t)count);
   return order;
 }
 

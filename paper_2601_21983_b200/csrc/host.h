@@ -8,6 +8,7 @@
 #pragma once
 
 #include <array>
+#include <stdexcept>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -119,6 +120,20 @@ std::vector<double> normalize(const double* lw, int64_t J);
 
 // ---- data -------------------------------------------------------------------------------
 std::vector<int64_t> shuffle_permutation(uint64_t seed, int64_t n);
+std::vector<int64_t> redraw_rows(uint64_t seed, int k, int64_t n, int64_t count);  // runner.hpp:531-542
+
+// IDX image/label files (dataset.hpp:84-196): FormatError texts as the reference.
+struct FormatError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct IdxData {
+  int64_t n = 0, d = 0;
+  int num_classes = 0;
+  std::vector<float> X;   // pixels / 255
+  std::vector<int32_t> y;
+};
+IdxData parse_idx(const std::vector<unsigned char>& image_bytes, const std::vector<unsigned char>& label_bytes);
+std::vector<unsigned char> read_file_bytes(const std::string& path);  // gzip decompressed transparently
 void make_teacher_data(const std::vector<int>& layers, int act, int64_t n, int feature_kind, uint64_t seed,
                        uint64_t cfg_id, int threads, float* X, int32_t* y, const int* conv = nullptr);
 

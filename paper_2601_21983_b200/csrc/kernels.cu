@@ -1268,6 +1268,23 @@ void launch_normalize_resample(Ctx& c, int64_t Jtot, double* lw_full, const doub
   LAUNCHED();
 }
 
+__global__ void gather_data_kernel(const float* __restrict__ X, const int32_t* __restrict__ y,
+                                   const int64_t* __restrict__ rows, int64_t count, int64_t d, float* __restrict__ Xd,
+                                   int32_t* __restrict__ yd) {
+  for (int64_t r = blockIdx.x; r < count; r += gridDim.x) {
+    const int64_t src = rows[r];
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) Xd[r * d + i] = X[src * d + i];
+    if (threadIdx.x == 0) yd[r] = y[src];
+  }
+}
+
+void launch_gather_data(Ctx& c, const float* X, const int32_t* y, const int64_t* rows, int64_t count, int64_t d,
+                        float* Xd, int32_t* yd) {
+  gather_data_kernel<<<(unsigned)std::min<int64_t>(count, 148 * 32), 256, 0, c.stream>>>(X, y, rows, count, d, Xd,
+                                                                                         yd);
+  LAUNCHED();
+}
+
 void launch_rows(Ctx& c, const float* src, float* dst, const int32_t* rows_dev, int64_t n, bool pack) {
   if (n <= 0) return;
   const int64_t Dp4 = c.net.Dp / 4;

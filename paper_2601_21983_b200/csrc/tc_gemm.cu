@@ -1515,6 +1515,19 @@ void tc_free(Ctx& c) {
   c.tc = nullptr;
 }
 
+void tc_refresh_data(Ctx& c) {
+  TcState* s = c.tc;
+  dim3 grid((unsigned)((s->n_pad + 31) / 32), (unsigned)((s->n0 + 1 + 31) / 32));
+  if (s->f16)
+    transpose_x_kernel<1><<<grid, dim3(32, 8), 0, c.stream>>>(
+        c.X, c.n_active, s->n0, s->n_pad, s->kx, reinterpret_cast<__half*>(s->Xt), nullptr,
+        reinterpret_cast<__half*>(s->Xhi), nullptr, 0);
+  else
+    transpose_x_kernel<0><<<grid, dim3(32, 8), 0, c.stream>>>(c.X, c.n_active, s->n0, s->n_pad, s->kx, s->Xt,
+                                                              s->Xtlo, s->Xhi, s->Xlo, s->split ? 1 : 0);
+  LAUNCHED();
+}
+
 void tc_ensure_rows(Ctx& c, int64_t Mcap) {
   TcState* s = c.tc;
   if (Mcap <= s->mcap) return;

@@ -19,6 +19,7 @@ namespace dasmc_b200 {
 
 bool tc_layer1_eligible(const Ctx& c);
 void tc_init(Ctx& c);  // allocates X^T (+ splits) once per context
+void tc_refresh_data(Ctx& c);  // re-derive the operand copies of X after the active rows changed
 void tc_free(Ctx& c);
 void tc_ensure_rows(Ctx& c, int64_t Mcap);
 // One gradient evaluation (or forward-only pass) of the whole network on the tensor cores.

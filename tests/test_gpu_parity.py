@@ -234,3 +234,21 @@ def test_sda_moments_and_run(product, oracle):
     assert all(0 < b_ <= 1 for b_ in betas)
     pre = [s[1] for s in out["sda"]]
     assert all(p2 >= p1 for p1, p2 in zip(pre, pre[1:]))
+
+
+def test_constant_redraw_run(product, oracle):
+    """Constant schedule with a fresh batch per iteration (runner.hpp:531-556): the device
+    gathers train[draw_batch_rows(k)] and the window is {0, C, N}; records follow the oracle."""
+    layers = [12, 10, 4]
+    spec, X, y = make_problem(product, layers, "relu", 600)
+    for prec in ("fp32", "tf32"):
+        cfg = product.RunConfig(kernel=product.KernelConfig.hmc(0.01, 2),
+                                schedule=product.ScheduleConfig("constant", 100, 100, 6, 600), particles=32,
+                                iterations=6, seed=3, resample="systematic", redraw=True)
+        a = product.run_experiment(spec, X, y, cfg, precision=prec if layers[0] % 4 == 0 else "fp32")["records"]
+        o = oracle.run(layers, 0, X.astype(np.float64), y, kernel=(0.01, 2, 0), sched=(0, 100, 100, 1, -1),
+                       redraw=True, particles=32, iterations=6, seed=3, resample_kind=1)
+        assert [r["batch"] for r in a] == [r["batch"] for r in o] == [100] * 6
+        for ra, ro in zip(a[:3], o[:3]):
+            np.testing.assert_allclose(ra["ess"], ro["ess"], rtol=2e-3 if prec == "tf32" else 1e-3)
+            np.testing.assert_allclose(ra["mean_log_target"], ro["mean_log_target"], rtol=1e-3 if prec == "tf32" else 1e-5)

@@ -100,3 +100,22 @@ def test_invalid_arguments_raise(product):
     rc = lib.dasmc_gpu_create(C.byref(d), X.ctypes.data_as(C.POINTER(C.c_float)),
                               y.ctypes.data_as(C.POINTER(C.c_int32)), 4, 8, 0, 0, C.byref(h))
     assert rc == -1 and b"layer sizes" in lib.dasmc_last_error()
+
+
+def test_redraw_rows_bit_exact(product, oracle):
+    """draw_batch_rows (runner.hpp:531-542): partial Fisher-Yates with fork(kRedraw, k)."""
+    M64 = (1 << 64) - 1
+    for seed, k, n, count in ((0, 0, 100, 10), (7, 13, 1000, 1000), (3, 2, 57, 1)):
+        u = iter(int(v) for v in oracle.rng_u64(oracle.fork_key(seed, 6, k, 0), 4 * count + 64))
+
+        def below(b):  # rng.hpp:66-73
+            limit = M64 - (M64 % b)
+            while True:
+                x = next(u)
+                if x < limit:
+                    return x % b
+        order = list(range(n))
+        for i in range(count):
+            j = i + below(n - i)
+            order[i], order[j] = order[j], order[i]
+        assert list(product.redraw_rows(seed, k, n, count)) == order[:count]
