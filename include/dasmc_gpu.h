@@ -231,6 +231,9 @@ int dasmc_load_idx(const char* image_path, const char* label_path, int64_t* n, i
  * train[rows[0..count)] (gathered on the device; rows == NULL restores the resident set).
  * The window is then {0, count, N} as in context_for. */
 int dasmc_redraw_rows(uint64_t seed, int k, int64_t n, int64_t count, int64_t* rows);
+/* make_synthetic (dataset.hpp:208-267) for the runner's classification datasets: kind 0 =
+ * gaussian_blobs (3 classes), 1 = two_moons (2 classes); X n x 2 (fp32), y int32. */
+int dasmc_make_synthetic(int kind, int64_t n, double noise, uint64_t seed, float* X, int32_t* y);
 int dasmc_gpu_set_rows(dasmc_ctx* ctx, const int64_t* rows, int64_t count);
 
 /* ---- evaluate_predictive (runner.hpp:331-364) ------------------------------------------

@@ -141,6 +141,7 @@ SIGNATURES = {
     "dasmc_parse_idx": (C.c_int, [C.c_char_p, C.c_int64, C.c_char_p, C.c_int64, _I64, _I64, C.POINTER(C.c_int), _F,
                                   _I32]),
     "dasmc_load_idx": (C.c_int, [C.c_char_p, C.c_char_p, _I64, _I64, C.POINTER(C.c_int), _F, _I32]),
+    "dasmc_make_synthetic": (C.c_int, [C.c_int, C.c_int64, C.c_double, C.c_uint64, _F, _I32]),
     "dasmc_redraw_rows": (C.c_int, [C.c_uint64, C.c_int, C.c_int64, C.c_int64, _I64]),
     "dasmc_gpu_set_rows": (C.c_int, [_P, _I64, C.c_int64]),
     "dasmc_gpu_run": (C.c_int, [C.POINTER(NetDesc), _F, _I32, C.c_int64, C.POINTER(RunCfg), C.c_int, C.c_int,

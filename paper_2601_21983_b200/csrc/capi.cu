@@ -1138,6 +1138,13 @@ int dasmc_load_idx(const char* image_path, const char* label_path, int64_t* n, i
   });
 }
 
+int dasmc_make_synthetic(int kind, int64_t n, double noise, uint64_t seed, float* X, int32_t* y) {
+  return guarded([&] {
+    if (!X || !y) throw InvalidArg("null argument");
+    make_synthetic(kind, n, noise, seed, X, y);
+  });
+}
+
 int dasmc_redraw_rows(uint64_t seed, int k, int64_t n, int64_t count, int64_t* rows) {
   return guarded([&] {
     if (n < 1 || count < 1 || count > n || !rows) throw InvalidArg("bad argument");

@@ -369,6 +369,42 @@ std::vector<unsigned char> read_file_bytes(const std::string& path) {
   return bytes;
 }
 
+// make_synthetic (dataset.hpp:208-267), the classification kinds the runner feeds to an MLP:
+// kind 0 = gaussian_blobs (3 classes), 1 = two_moons (2 classes); 2-D features, stream
+// RngStream(seed).fork(kSynthetic).
+void make_synthetic(int kind, int64_t n, double noise, uint64_t seed, float* X, int32_t* y) {
+  if (n < 2) throw std::invalid_argument("make_synthetic: n must be >= 2");
+  if (kind != 0 && kind != 1) throw std::invalid_argument("make_synthetic: classification kinds only (blobs, moons)");
+  HostRng r(fork_key(seed, tag::kSynthetic, 0, 0));
+  constexpr double kPi = 3.141592653589793;
+  for (int64_t i = 0; i < n; ++i) {
+    double x0, x1;
+    if (kind == 0) {
+      const int c = (int)(i % 3);
+      const double angle = 2.0 * kPi * c / 3;
+      x0 = 3.0 * std::cos(angle) + noise * r.normal();
+      x1 = 3.0 * std::sin(angle) + noise * r.normal();
+      y[i] = c;
+    } else {
+      const int c = (int)(i % 2);
+      const double t = kPi * r.uniform();
+      double a, b;
+      if (c == 0) {
+        a = std::cos(t);
+        b = std::sin(t);
+      } else {
+        a = 1.0 - std::cos(t);
+        b = 0.5 - std::sin(t);
+      }
+      x0 = a + noise * r.normal();
+      x1 = b + noise * r.normal();
+      y[i] = c;
+    }
+    X[2 * i] = (float)x0;
+    X[2 * i + 1] = (float)x1;
+  }
+}
+
 // draw_batch_rows (runner.hpp:531-542): partial Fisher-Yates over 0..n-1 with the
 // stream root.fork(kRedraw, k), i = 0..count-1, j = i + uniform_below(n - i).
 std::vector<int64_t> redraw_rows(uint64_t seed, int k, int64_t n, int64_t count) {

@@ -121,6 +121,7 @@ std::vector<double> normalize(const double* lw, int64_t J);
 // ---- data -------------------------------------------------------------------------------
 std::vector<int64_t> shuffle_permutation(uint64_t seed, int64_t n);
 std::vector<int64_t> redraw_rows(uint64_t seed, int k, int64_t n, int64_t count);  // runner.hpp:531-542
+void make_synthetic(int kind, int64_t n, double noise, uint64_t seed, float* X, int32_t* y);  // dataset.hpp:208-267
 
 // IDX image/label files (dataset.hpp:84-196): FormatError texts as the reference.
 struct FormatError : std::runtime_error {
