@@ -236,6 +236,16 @@ int dasmc_redraw_rows(uint64_t seed, int k, int64_t n, int64_t count, int64_t* r
 int dasmc_make_synthetic(int kind, int64_t n, double noise, uint64_t seed, float* X, int32_t* y);
 int dasmc_gpu_set_rows(dasmc_ctx* ctx, const int64_t* rows, int64_t count);
 
+/* ---- start-gradient cache ---------------------------------
+ * Opt-in.  When the target is unchanged since the previous smc_step (same mode, window,
+ * beta, sigma, data rows and J) and that step had no divergent particle, the step's first
+ * leapfrog evaluation is replaced by the previous step's final log targets and gradients,
+ * gathered through its resampling: the same values (deterministic kernels), S instead of
+ * S+1 evaluations.  Needs the record of each step (sync).  The reference recomputes
+ * (kernels.hpp:85); off by default, and bench.py leaves it off. */
+int dasmc_gpu_set_cache_start(dasmc_ctx* ctx, int enable);
+int dasmc_gpu_last_step_cached(dasmc_ctx* ctx); /* 1 if the last smc_step used the cache */
+
 /* ---- evaluate_predictive (runner.hpp:331-364) ------------------------------------------
  * Ensemble-averaged predictive of the context's current ensemble on a labelled test set
  * (host buffers: n_test rows in the model's input layout, int32 labels): mean log predictive

@@ -144,6 +144,8 @@ SIGNATURES = {
     "dasmc_make_synthetic": (C.c_int, [C.c_int, C.c_int64, C.c_double, C.c_uint64, _F, _I32]),
     "dasmc_redraw_rows": (C.c_int, [C.c_uint64, C.c_int, C.c_int64, C.c_int64, _I64]),
     "dasmc_gpu_set_rows": (C.c_int, [_P, _I64, C.c_int64]),
+    "dasmc_gpu_set_cache_start": (C.c_int, [_P, C.c_int]),
+    "dasmc_gpu_last_step_cached": (C.c_int, [_P]),
     "dasmc_gpu_run": (C.c_int, [C.POINTER(NetDesc), _F, _I32, C.c_int64, C.POINTER(RunCfg), C.c_int, C.c_int,
                                 C.POINTER(IterRecord), C.POINTER(SdaState), _D, _D]),
 }

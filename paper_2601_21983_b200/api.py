@@ -329,6 +329,12 @@ class GpuEnsembleTarget:
         L.check(self.lib.dasmc_gpu_sda_moments(self.h, prefix_end, block_end, _dp(out)))
         return out
 
+    def set_cache_start(self, enable: bool = True):  # SPEC.md:410 start-gradient cache (opt-in)
+        L.check(self.lib.dasmc_gpu_set_cache_start(self.h, 1 if enable else 0))
+
+    def last_step_cached(self) -> bool:
+        return bool(self.lib.dasmc_gpu_last_step_cached(self.h))
+
     def set_rows(self, rows: Optional[np.ndarray]):  # runner.hpp:548-557 redraw batch (None: resident set)
         if rows is None:
             L.check(self.lib.dasmc_gpu_set_rows(self.h, None, 0))

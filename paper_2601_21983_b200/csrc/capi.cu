@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <limits>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -136,8 +137,9 @@ void free_ctx(Ctx& c) {
   cudaSetDevice(c.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
   tc_free(c);
-  void* ptrs[] = {c.X_full, c.Xt, c.y_full, c.Xg, c.yg, c.rows_dev, c.theta[0], c.theta[1], c.theta[2], c.p, c.grad, c.logw, c.dT, c.ll_part,
-                  c.th_part, c.p_part, c.p0_part, c.flags, c.lt_old, c.lt_new, c.ll_pre, c.ll_blk, c.wts, c.cdf,
+  void* ptrs[] = {c.X_full, c.Xt, c.y_full, c.Xg, c.yg, c.rows_dev, c.gcache[0], c.gcache[1], c.lt_cache, c.theta[0], c.theta[1], c.theta[2], c.p, c.grad, c.logw, c.dT, c.ll_part,
+                  c.th_part, c.p_part, c.p0_part, c.flags, c.lt_old, c.lt_new, c.ll_pre, c.ll_blk, c.ll_pre0, c.ll_blk0,
+                  c.sda_pre, c.sda_blk, c.wts, c.cdf,
                   c.uni, c.idx, c.records, c.jump_tab, c.stage, c.sh_buf, c.sh_idx, c.sh_rows, c.iota};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -224,6 +226,23 @@ void check_kernel_cfg(const dasmc_kernel_cfg& kc) {  // kernels.hpp:42-48
     throw InvalidArg("KernelConfig: langevin requires leapfrog_steps == 1");
 }
 
+int64_t cache_sig_of(const Ctx& c, int i) {
+  const int64_t v[4] = {c.mode, c.prefix_end, c.block_end, c.total_n};
+  return v[i];
+}
+bool cache_signature_matches(const Ctx& c) {
+  for (int i = 0; i < 4; ++i)
+    if (c.cache_sig[i] != cache_sig_of(c, i)) return false;
+  return c.cache_sigd[0] == c.beta && c.cache_sigd[1] == c.sigma && c.cache_X == c.X && c.cache_sigd[2] == (double)c.J;
+}
+void cache_signature_store(Ctx& c) {
+  for (int i = 0; i < 4; ++i) c.cache_sig[i] = cache_sig_of(c, i);
+  c.cache_sigd[0] = c.beta;
+  c.cache_sigd[1] = c.sigma;
+  c.cache_sigd[2] = (double)c.J;
+  c.cache_X = c.X;
+}
+
 // Fresh momenta + S-step leapfrog + log targets of the context's particles
 // (smc.hpp:118-122, kernels.hpp:75-99).  Global slot of local particle j is
 // j_offset + j (RNG streams).  Returns the buffer index (relative to c.start)
@@ -244,12 +263,23 @@ int propose_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int64_t j_o
   const int t0 = c.start, t1 = (c.start + 1) % 3, t2 = (c.start + 2) % 3;
   float* bufs[3] = {c.theta[t0], c.theta[t1], c.theta[t2]};
   int in_idx = 0;
+  // start-gradient cache: same target as the step that produced the cached final positions
+  const bool use_cache = c.cache_start && c.cache_valid && j_offset == 0 && cache_signature_matches(c);
+  c.last_step_cached = use_cache;
   for (int s = 0; s <= S; ++s) {
     const int out_idx = (s % 2 == 0) ? 1 : 2;
     const int mode = s == 0 ? kEpiFirst : (s < S ? kEpiMid : kEpiLast);
     EpiParams e = make_epi(c, mode, kc.step_size, bufs[in_idx], s < S ? bufs[out_idx] : nullptr);
+    if (s == 0 && use_cache) {  // p += h/2 g(theta_0), theta_1 = theta_0 + h p; lt_old = cached
+      launch_start_from_cache(c, e, J);
+      in_idx = out_idx;
+      continue;
+    }
+    if (s == S && c.cache_start) e.grad_cache = c.gcache[c.gcur ^ 1];
     launch_eval(c, bufs[in_idx], J, M, P, br, true, &e);
-    launch_eval_finalize(c, J, s == 0 ? c.lt_old : c.lt_new, nullptr, nullptr, M, true);
+    // unscaled (prefix, block) ll of the first and last evaluations feed the fused SDA moments
+    launch_eval_finalize(c, J, s == 0 ? c.lt_old : c.lt_new, s == 0 ? c.ll_pre0 : (s == S ? c.ll_pre : nullptr),
+                         s == 0 ? c.ll_blk0 : (s == S ? c.ll_blk : nullptr), M, true);
     if (s < S) in_idx = out_idx;
   }
   launch_p_sumsq(c, J);
@@ -271,6 +301,15 @@ void smc_step_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind
   launch_weights_and_resample(c, J, fraction, always, rkind, slot, k, 0.0);
   const int dst_idx = end_idx == 1 ? 2 : 1;  // the free trajectory buffer
   launch_gather(c, bufs[0], bufs[end_idx], bufs[dst_idx], J);
+  launch_gather_parts(c, J);  // the post-step ensemble's (prefix, block) ll, for sda_advance
+  if (c.cache_start) {  // next step's start gradients / log targets = this step's final ones, resampled
+    launch_gather_cache(c, c.gcache[c.gcur ^ 1], c.gcache[c.gcur], J);
+    cache_signature_store(c);
+  }
+  c.cache_valid = false;  // confirmed by the host once the record shows no divergence
+  c.step_parts_valid = true;
+  c.step_P = c.mode == DASMC_SDA ? c.prefix_end : c.block_end;
+  c.step_M = c.block_end;
   c.start = dst_idx == 1 ? t1 : t2;
   c.iteration = k + 1;  // smc.hpp:150, 154
 }
@@ -304,10 +343,18 @@ void sda_moments_dev(Ctx& c, int64_t P, int64_t M, double* out6) {  // annealing
   if (P < 0 || P > M || M > c.n) throw InvalidArg("SubsetWindow: need 0 <= prefix_end <= block_end <= total_n");
   if (M <= P) throw InvalidArg("sda_moments: window has no new block");
   const int64_t J = c.J;
-  loglik_parts_dev(c, c.theta[c.start], J, P, M);
   std::vector<double> pre((size_t)J), blk((size_t)J), lw((size_t)J);
-  download(c, pre.data(), c.ll_pre, sizeof(double) * J);
-  download(c, blk.data(), c.ll_blk, sizeof(double) * J);
+  // fused: right after an SDA step on this window, the step's own last
+  // evaluation (first one for divergent particles), gathered through the resample, gives the
+  // post-step ensemble's ll without another forward pass; identical values to the pass
+  if (c.step_parts_valid && c.step_P == P && c.step_M == M && c.X == c.X_full && !c.force_moment_pass) {
+    download(c, pre.data(), c.sda_pre, sizeof(double) * J);
+    download(c, blk.data(), c.sda_blk, sizeof(double) * J);
+  } else {
+    loglik_parts_dev(c, c.theta[c.start], J, P, M);
+    download(c, pre.data(), c.ll_pre, sizeof(double) * J);
+    download(c, blk.data(), c.ll_blk, sizeof(double) * J);
+  }
   download(c, lw.data(), c.logw, sizeof(double) * J);
   for (int64_t j = 0; j < J; ++j) {
     pre[(size_t)j] = -pre[(size_t)j];
@@ -337,11 +384,14 @@ void init_ensemble_dev(Ctx& c, int64_t J, uint64_t seed, int64_t j_offset = 0) {
   c.J = J;
   c.iteration = 0;
   c.has_ensemble = true;
+  c.step_parts_valid = false;
+  c.cache_valid = false;
 }
 
 void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t* y, int64_t n, int Jmax,
                 int device, int precision) {
   c.net = make_net(net);
+  if (const char* e = std::getenv("DASMC_SDA_MOMENT_PASS")) c.force_moment_pass = e[0] == '1';
   if (n < 1) throw InvalidArg("dataset: n must be >= 1");
   if (X == nullptr || y == nullptr) throw InvalidArg("dataset: null X or y");
   if (Jmax < 2) throw InvalidArg("max_particles must be >= 2");
@@ -398,6 +448,10 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
   dmalloc(c.lt_new, (size_t)Jmax);
   dmalloc(c.ll_pre, (size_t)Jmax);
   dmalloc(c.ll_blk, (size_t)Jmax);
+  dmalloc(c.ll_pre0, (size_t)Jmax);
+  dmalloc(c.ll_blk0, (size_t)Jmax);
+  dmalloc(c.sda_pre, (size_t)Jmax);
+  dmalloc(c.sda_blk, (size_t)Jmax);
   dmalloc(c.wts, (size_t)Jmax);
   dmalloc(c.cdf, (size_t)Jmax);
   dmalloc(c.uni, (size_t)Jmax);
@@ -614,6 +668,8 @@ int dasmc_gpu_set_ensemble(dasmc_ctx* ctx, const double* theta, const double* lo
     c.J = J;
     c.iteration = iteration;
     c.has_ensemble = true;
+  c.step_parts_valid = false;
+  c.cache_valid = false;
   });
 }
 
@@ -633,6 +689,8 @@ int dasmc_gpu_set_ensemble_f32(dasmc_ctx* ctx, const float* theta, const double*
     c.J = J;
     c.iteration = iteration;
     c.has_ensemble = true;
+  c.step_parts_valid = false;
+  c.cache_valid = false;
   });
 }
 
@@ -685,6 +743,7 @@ int dasmc_gpu_smc_step(dasmc_ctx* ctx, const dasmc_kernel_cfg* cfg, uint64_t see
     if (record) {
       fetch_records(c, slot, 1);
       *record = read_record(c, slot);
+      c.cache_valid = c.cache_start && record->n_divergent == 0;
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
       record->sampler_ms = ms;
@@ -842,6 +901,7 @@ int dasmc_shard_plan(const int32_t* idx, int64_t J, int world, int rank, int32_t
 int dasmc_gpu_shard_propose(dasmc_ctx* ctx, const dasmc_kernel_cfg* cfg, uint64_t seed, int64_t j_offset,
                             double* log_w_dev, double* log_target_new_dev) {
   return guarded([&] {
+    if (ctx) ctx->c.step_parts_valid = ctx->c.cache_valid = false;
     if (!ctx || !cfg || !log_w_dev || !log_target_new_dev) throw InvalidArg("null argument");
     Ctx& c = ctx->c;
     CK(cudaSetDevice(c.device));
@@ -861,6 +921,7 @@ int dasmc_gpu_shard_resample(dasmc_ctx* ctx, const double* log_w_full_dev, const
                              int64_t J_total, int64_t j_offset, uint64_t seed, int resample_kind, double fraction,
                              int resample_always, int32_t* idx_dev, dasmc_iter_record* record) {
   return guarded([&] {
+    if (ctx) ctx->c.step_parts_valid = ctx->c.cache_valid = false;
     if (!ctx || !log_w_full_dev || !log_target_new_full_dev || !idx_dev) throw InvalidArg("null argument");
     Ctx& c = ctx->c;
     if (j_offset < 0 || j_offset + c.J > J_total) throw InvalidArg("shard_resample: slice out of range");
@@ -938,6 +999,7 @@ int dasmc_gpu_pack_rows(dasmc_ctx* ctx, const int32_t* rows, int64_t n, float* d
 
 int dasmc_gpu_unpack_rows(dasmc_ctx* ctx, const float* src_dev, const int32_t* slots, int64_t n) {
   return guarded([&] {
+    if (ctx) ctx->c.step_parts_valid = ctx->c.cache_valid = false;
     if (!ctx || !src_dev || !slots) throw InvalidArg("null argument");
     Ctx& c = ctx->c;
     if (n != c.J) throw InvalidArg("unpack_rows: every local slot must be written exactly once");
@@ -1101,6 +1163,25 @@ int dasmc_gpu_evaluate_predictive(dasmc_ctx* ctx, const float* X_test, const int
     if (rc != DASMC_OK) throw InvalidArg(g_err);
   });
 }
+
+int dasmc_gpu_set_cache_start(dasmc_ctx* ctx, int enable) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg("null ctx");
+    Ctx& c = ctx->c;
+    CK(cudaSetDevice(c.device));
+    c.cache_start = enable != 0;
+    c.cache_valid = false;
+    if (c.cache_start && !c.gcache[0]) {
+      for (auto& g : c.gcache) {
+        dmalloc(g, (size_t)c.Jmax * c.net.Dp);
+        CK(cudaMemset(g, 0, sizeof(float) * (size_t)c.Jmax * c.net.Dp));
+      }
+      dmalloc(c.lt_cache, (size_t)c.Jmax);
+    }
+  });
+}
+
+int dasmc_gpu_last_step_cached(dasmc_ctx* ctx) { return ctx && ctx->c.last_step_cached ? 1 : 0; }
 
 int dasmc_gpu_set_rows(dasmc_ctx* ctx, const int64_t* rows, int64_t count) {
   return guarded([&] {

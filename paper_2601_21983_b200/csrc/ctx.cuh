@@ -102,6 +102,7 @@ struct EpiParams {
   double* p_part;        // [J][slots] sum p_final^2 (kEpiLast only)
   int* flags;            // [J] divergence flags
   int slots;             // slots per particle
+  float* grad_cache;     // kEpiLast: also store the final-position gradient (start-gradient cache)
 };
 
 struct Ctx {
@@ -160,8 +161,30 @@ struct Ctx {
   int* flags = nullptr;        // [J]
   double* lt_old = nullptr;    // [J]
   double* lt_new = nullptr;    // [J]
-  double* ll_pre = nullptr;    // [J] (forward-only passes)
+  double* ll_pre = nullptr;    // [J] (forward-only passes; the step's last evaluation)
   double* ll_blk = nullptr;    // [J]
+  // SDA moments fused into the step: unscaled (prefix, block) ll of the
+  // step's first evaluation (the kept positions of divergent particles) and of the
+  // post-step, post-resample ensemble, valid for window (step_P, step_M) until the
+  // ensemble changes another way
+  double* ll_pre0 = nullptr;
+  double* ll_blk0 = nullptr;
+  double* sda_pre = nullptr;
+  double* sda_blk = nullptr;
+  bool step_parts_valid = false;
+  bool force_moment_pass = false;  // DASMC_SDA_MOMENT_PASS=1: always recompute (tests / A-B)
+  // start-gradient cache: with an unchanged target the next
+  // step's start positions are this step's (gathered) final positions, whose log target and
+  // gradient the last leapfrog evaluation already produced; opt-in (dasmc_gpu_set_cache_start)
+  bool cache_start = false, cache_valid = false;
+  float* gcache[2] = {nullptr, nullptr};
+  int gcur = 0;
+  double* lt_cache = nullptr;
+  int64_t cache_sig[4] = {0, 0, 0, 0};
+  double cache_sigd[3] = {0, 0, 0};
+  const float* cache_X = nullptr;
+  bool last_step_cached = false;
+  int64_t step_P = -1, step_M = -1;
   double* wts = nullptr;       // [J] normalised weights of the last step
   double* cdf = nullptr;       // [J]
   double* uni = nullptr;       // [J] resample uniforms
@@ -241,6 +264,12 @@ void launch_weights_and_resample(Ctx& c, int64_t J, double fraction, int always,
                                  int k, double log_target_const);
 void launch_gather(Ctx& c, const float* start, const float* end, float* dst, int64_t J,
                    const int32_t* idx = nullptr);
+// post-step (prefix, block) ll: (flags[s] ? first-evaluation : last-evaluation)[s], s = idx[j]
+void launch_gather_parts(Ctx& c, int64_t J);
+// start-gradient cache: p += h/2 g_cached, theta_out = theta + h p (kernels.hpp:89-91), flags
+void launch_start_from_cache(Ctx& c, const EpiParams& e, int64_t J);
+// rows dst[j] = src[idx[j]] of Dp floats, and lt_cache[j] = lt_new[idx[j]]
+void launch_gather_cache(Ctx& c, const float* src, float* dst, int64_t J);
 void launch_local_weights(Ctx& c, int64_t J, double* out_lw, double* out_lt);
 void launch_normalize_resample(Ctx& c, int64_t Jtot, double* lw_full, const double* lt_full, double* w, double* cdf,
                                const double* uni, int32_t* idx, double fraction, int always, int kind, int rec_slot,

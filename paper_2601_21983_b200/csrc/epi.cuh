@@ -25,6 +25,7 @@ __device__ __forceinline__ void leapfrog_update(const EpiParams& e, int j, int64
   float p = e.p[idx];
   p = fmaf(e.hh, g, p);
   if (e.mode == kEpiMid) p = fmaf(e.hh, g, p);
+  if (e.mode == kEpiLast && e.grad_cache) e.grad_cache[idx] = g;
   bad |= !isfinite(p);
   e.p[idx] = p;
   if (e.mode != kEpiLast) {
@@ -60,6 +61,7 @@ __device__ __forceinline__ void leapfrog_update_n(const EpiParams& e, int j, con
       }
       float pq = fmaf(e.hh, g, p[q]);
       if (e.mode == kEpiMid) pq = fmaf(e.hh, g, pq);
+      if (e.mode == kEpiLast && e.grad_cache) e.grad_cache[idx[q]] = g;
       bad |= !isfinite(pq);
       e.p[idx[q]] = pq;
       if (e.mode != kEpiLast) {

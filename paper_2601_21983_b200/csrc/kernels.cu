@@ -630,6 +630,17 @@ __global__ void __launch_bounds__(256) gather_kernel(const float4* __restrict__ 
   for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < Dp4; i += (int64_t)gridDim.x * 256) d[i] = src[i];
 }
 
+__global__ void gather_parts_kernel(int64_t J, const int32_t* __restrict__ idx, const int* __restrict__ flags,
+                                    const double* __restrict__ pre0, const double* __restrict__ blk0,
+                                    const double* __restrict__ pre, const double* __restrict__ blk,
+                                    double* __restrict__ out_pre, double* __restrict__ out_blk) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= J) return;
+  const int32_t s = idx[j];
+  out_pre[j] = flags[s] ? pre0[s] : pre[s];
+  out_blk[j] = flags[s] ? blk0[s] : blk[s];
+}
+
 __global__ void zero_ints_kernel(int* p, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = 0;
@@ -1309,6 +1320,47 @@ void launch_gather(Ctx& c, const float* start, const float* end, float* dst, int
   gather_kernel<<<grid, 256, 0, c.stream>>>(reinterpret_cast<const float4*>(start),
                                             reinterpret_cast<const float4*>(end), reinterpret_cast<float4*>(dst),
                                             Dp4, idx ? idx : c.idx, c.flags);
+  LAUNCHED();
+}
+
+__global__ void start_from_cache_kernel(EpiParams e, const float* __restrict__ g_cache, int64_t Dp, int64_t J) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < J * Dp; t += (int64_t)gridDim.x * blockDim.x) {
+    const float g = g_cache[t];
+    const float th = e.theta_in[t];
+    const float p = fmaf(e.hh, g, e.p[t]);
+    const float tn = fmaf(e.h, p, th);
+    e.p[t] = p;
+    e.theta_out[t] = tn;
+    if (!isfinite(g) || !isfinite(p) || !isfinite(tn)) atomicOr(&e.flags[t / Dp], 1);
+  }
+}
+
+__global__ void gather_cache_kernel(const float4* __restrict__ src, float4* __restrict__ dst, int64_t Dp4,
+                                    const int32_t* __restrict__ idx, const double* __restrict__ lt_new,
+                                    double* __restrict__ lt_cache) {
+  const int64_t j = blockIdx.y;
+  const int32_t s = idx[j];
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < Dp4; i += (int64_t)gridDim.x * 256) dst[j * Dp4 + i] = src[s * Dp4 + i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) lt_cache[j] = lt_new[s];
+}
+
+void launch_start_from_cache(Ctx& c, const EpiParams& e, int64_t J) {
+  start_from_cache_kernel<<<grid_for(J * c.net.Dp), 256, 0, c.stream>>>(e, c.gcache[c.gcur], c.net.Dp, J);
+  LAUNCHED();
+  CK(cudaMemcpyAsync(c.lt_old, c.lt_cache, sizeof(double) * J, cudaMemcpyDeviceToDevice, c.stream));
+}
+
+void launch_gather_cache(Ctx& c, const float* src, float* dst, int64_t J) {
+  const int64_t Dp4 = c.net.Dp / 4;
+  const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>((Dp4 + 255) / 256, 64));
+  gather_cache_kernel<<<dim3((unsigned)chunks, (unsigned)J), 256, 0, c.stream>>>(
+      reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), Dp4, c.idx, c.lt_new, c.lt_cache);
+  LAUNCHED();
+}
+
+void launch_gather_parts(Ctx& c, int64_t J) {
+  gather_parts_kernel<<<(unsigned)((J + 255) / 256), 256, 0, c.stream>>>(J, c.idx, c.flags, c.ll_pre0, c.ll_blk0,
+                                                                        c.ll_pre, c.ll_blk, c.sda_pre, c.sda_blk);
   LAUNCHED();
 }
 

@@ -252,3 +252,56 @@ def test_constant_redraw_run(product, oracle):
         for ra, ro in zip(a[:3], o[:3]):
             np.testing.assert_allclose(ra["ess"], ro["ess"], rtol=2e-3 if prec == "tf32" else 1e-3)
             np.testing.assert_allclose(ra["mean_log_target"], ro["mean_log_target"], rtol=1e-3 if prec == "tf32" else 1e-5)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+def test_sda_moments_fused_into_step(product, oracle, prec, monkeypatch):
+    """after an SDA step the moments come from the step's own evaluations
+    (kept positions for divergent particles, gathered through the resample) -- identical to
+    the explicit forward pass on the post-step ensemble, and to the oracle within 1e-5."""
+    layers = [12, 10, 4]
+    spec, X, y = make_problem(product, layers, "relu", 400)
+    res = {}
+    for force in ("0", "1"):
+        monkeypatch.setenv("DASMC_SDA_MOMENT_PASS", force)
+        t = product.GpuEnsembleTarget(spec, X, y, 32, precision=prec if prec == "fp32" else "tf32")
+        t.set_target(100, 250, 400, "sda", 0.3, 1.0)
+        t.init_ensemble(32, 4)
+        t.smc_step(product.KernelConfig.hmc(0.01, 2), 4, "multinomial", 1.0, True)
+        res[force] = t.sda_moments(100, 250)
+        th, lw, _ = t.get_ensemble(32)
+        t.close()
+    assert np.array_equal(res["0"], res["1"])
+    a, b = oracle.loglik_parts(layers, 0, X.astype(np.float64), y, 100, 250, th)
+    mo = oracle.sda_moments_from(-a, -b, lw)
+    np.testing.assert_allclose(res["0"], mo, rtol=1e-5 if prec == "fp32" else 1e-3,
+                               atol=(1e-6 if prec == "fp32" else 1e-3) * np.max(np.abs(mo)))
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+def test_start_gradient_cache_is_exact(product, prec):
+    """SURVEY.md §8f.1 / SPEC.md:410: with an unchanged target the cached start log targets and
+    gradients equal the recomputed ones, so the chain is bit-identical with S instead of S+1
+    evaluations per step; a target change falls back to recomputing."""
+    layers = [16, 12, 4]
+    spec, X, y = make_problem(product, layers, "tanh", 300)
+    runs = {}
+    for cache in (False, True):
+        t = product.GpuEnsembleTarget(spec, X, y, 24, precision=prec)
+        t.set_target(0, 200, 300, "scaled", 1.0, 1.0)
+        t.init_ensemble(24, 9)
+        if cache:
+            t.set_cache_start(True)
+        recs, used = [], []
+        for k in range(5):
+            if k == 3:
+                t.set_target(0, 250, 300, "scaled", 1.0, 1.0)  # window grows: no cache this step
+            recs.append(t.smc_step(product.KernelConfig.hmc(0.01, 3), 9, "systematic", 0.5))
+            used.append(t.last_step_cached())
+        th, lw, _ = t.get_ensemble(24)
+        runs[cache] = (th, lw, recs, used)
+        t.close()
+    assert runs[True][3] == [False, True, True, False, True]
+    assert np.array_equal(runs[False][0], runs[True][0]) and np.array_equal(runs[False][1], runs[True][1])
+    for a, b in zip(runs[False][2], runs[True][2]):
+        assert a["ess"] == b["ess"] and a["mean_log_target"] == b["mean_log_target"]
