@@ -413,7 +413,9 @@ __global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b
   for (int64_t i = lo; i < hi; ++i) {
     const double u1 = 1.0 - x.uniform();
     const double u2 = x.uniform();
-    const double nv = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+    // cos(2 pi u2) as cospi(2 u2): no Payne-Hanek reduction path; differs from
+    // cos(fl(2 pi) u2) by ~1e-16, far below the fp32 rounding of the stored value
+    const double nv = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
     const float v = (float)((double)scale * nv);
     const LayerDev& ly = net.seg[l];
     out[t < nw ? ly.woff + r * ly.in + cc : ly.boff + (t - nw)] = v;

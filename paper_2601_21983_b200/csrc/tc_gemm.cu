@@ -396,7 +396,8 @@ struct FwdParams {
   float *a1T, *d1T, *d2T, *a1Tlo, *d1Tlo, *d2Tlo;
   double* ll_part;
   int ll_slots;
-  int dbg;  // DASMC_DEBUG_EPI: 1 = skip global stores, 2 = skip pass 2, 3 = skip the whole epilogue math
+  int dbg;  // DASMC_DEBUG_EPI: 1 = skip global stores, 2 = skip pass 2, 3 = skip the whole epilogue math,
+            // 4 = stores into one L2-resident block, 5 = skip the a1^T stores, 6 = skip the delta1^T stores
   // EPI kHidden (a_l = act(acc)) / kBackDelta (delta_{l-1} = acc . act'(a_{l-1})) of the
   // deep-MLP path: outputs in row-major [J][Mcap][out_ld] (optional) and row-blocked
   // transposed [J][nblk = ldm][out_rows][128] form, tf32-rounded (GEMM operands)
@@ -762,7 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(lg * 32) << 16);
         const int64_t m = (int64_t)rt * BM + row_in_tile;
         const bool valid = m < fp.M;
-        const bool st_rows = fp.need_grad && fp.dbg != 1;
+        const bool st_rows = fp.need_grad && fp.dbg != 1 && fp.dbg != 5;  // 5: no a1^T stores
         int c_lo, c_hi;
         chunk_range((n1 + 15) >> 4, c_lo, c_hi);
         if (fp.dbg == 3) c_hi = c_lo;
@@ -902,7 +903,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        if (fp.need_grad && fp.dbg == 0) {
+        if (fp.need_grad && (fp.dbg == 0 || fp.dbg >= 5)) {  // 6: no delta1^T stores
           // pass 2: delta1 = (W2^T delta2) . act'(z1)  (network.hpp:209-215); zero past the window
           TS* d1T = reinterpret_cast<TS*>(fp.d1T) + sblk * n1 * kRow + row_in_tile;
           float* d1Tlo = SPLIT ? fp.d1Tlo + ((int64_t)j * nblk + rt) * n1 * kRow + row_in_tile : nullptr;
@@ -929,7 +930,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 d1 = dz * (1.f - a * a);
               }
               const TS hi = to_op<PREC>(d1);
-              pd[q * kRow] = hi;
+              if (fp.dbg != 6) pd[q * kRow] = hi;
               if (SPLIT) st_act(pdl + q * kRow, d1 - (float)hi, st_pol);
             };
             if (nq == 16) {
@@ -1115,20 +1116,46 @@ __global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n
 }
 
 // W1hi[j][o] = [W1[o], b1[o], 0 ...] (row stride kx) rounded to tf32, + lo part.
+// One thread per 4 consecutive outputs (grid-stride): 16-B loads of the W row when
+// the internal layout is 16-B aligned, 16-B (tf32) / 8-B (fp16) stores.
 template <int PREC>
-__global__ void split_w1_kernel(const float* __restrict__ theta, int64_t Dp, int64_t woff, int64_t boff, int n0,
-                                int64_t kx, int64_t cnt, int64_t J, OpT<PREC>* hi, float* lo) {
-  // one block per output row (j, o): coalesced row copies, no per-element divisions
-  const int64_t n1 = cnt / kx, nrows = J * n1;
-  for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
+__global__ void __launch_bounds__(256) split_w1_kernel(const float* __restrict__ theta, int64_t Dp, int64_t woff,
+                                                       int64_t boff, int n0, int64_t kx, int64_t cnt, int64_t J,
+                                                       OpT<PREC>* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t n1 = cnt / kx;
+  const int kq = (int)(kx >> 2);
+  const int64_t total = J * n1 * kq;
+  const bool vec = ((woff | (int64_t)n0 | Dp) & 3) == 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / kq;
+    const int i0 = 4 * (int)(e - row * kq);
     const int64_t j = row / n1, o = row - j * n1;
     const float* th = theta + j * Dp;
     const float* src = th + woff + o * n0;
-    for (int64_t i = threadIdx.x; i < kx; i += blockDim.x) {
-      const float v = i < n0 ? src[i] : (i == n0 ? th[boff + o] : 0.f);
-      const OpT<PREC> h = to_op<PREC>(v);
-      hi[row * kx + i] = h;
-      if (lo) lo[row * kx + i] = v - (float)h;
+    float v[4];
+    if (vec && i0 + 4 <= n0) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(src + i0));
+      v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u;
+        v[u] = i < n0 ? src[i] : (i == n0 ? th[boff + o] : 0.f);
+      }
+    }
+    OpT<PREC> h[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) h[u] = to_op<PREC>(v[u]);
+    const int64_t off = row * kx + i0;
+    if constexpr (PREC == 1) {
+      __half2 p0 = __halves2half2(h[0], h[1]), p1 = __halves2half2(h[2], h[3]);
+      uint2 w;
+      w.x = *reinterpret_cast<uint32_t*>(&p0);
+      w.y = *reinterpret_cast<uint32_t*>(&p1);
+      *reinterpret_cast<uint2*>(hi + off) = w;
+    } else {
+      *reinterpret_cast<float4*>(hi + off) = make_float4(h[0], h[1], h[2], h[3]);
+      if (lo) *reinterpret_cast<float4*>(lo + off) = make_float4(v[0] - h[0], v[1] - h[1], v[2] - h[2], v[3] - h[3]);
     }
   }
 }
@@ -1609,7 +1636,7 @@ void tc_eval_deep(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P
   for (int l = 1; l < L; ++l) {
     const LayerDev& ly = net.layer[l - 1];
     const int64_t cnt = (int64_t)s->sz[l] * s->kxl[l - 1];
-    split_w1_kernel<0><<<(int)std::min<int64_t>(J * s->sz[l], 148 * 64), 256, 0, c.stream>>>(
+    split_w1_kernel<0><<<148 * 8, 256, 0, c.stream>>>(
         theta_in, net.Dp, ly.woff, ly.boff, s->sz[l - 1], s->kxl[l - 1], cnt, J, s->Whi[l], nullptr);
     LAUNCHED();
   }
@@ -1765,7 +1792,7 @@ void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t 
     // [W1, b1] -> tf32 (rna) hi [+ lo]: the MMA would otherwise truncate the low mantissa
     // bits; the bias rides along as K column n0 against X's ones column
     const int64_t kx = s->kx, cnt = (int64_t)n1 * kx;
-    split_w1_kernel<PREC><<<(int)std::min<int64_t>(J * n1, 148 * 64), 256, 0, c.stream>>>(
+    split_w1_kernel<PREC><<<148 * 8, 256, 0, c.stream>>>(
         theta_in, net.Dp, l1.woff, l1.boff, n0, kx, cnt, J, reinterpret_cast<OpT<PREC>*>(s->W1hi),
         PREC == 0 && s->split ? s->W1lo : nullptr);
     LAUNCHED();
