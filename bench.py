@@ -61,6 +61,9 @@ WORKLOADS = {
 }
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# arithmetic of the dense contractions per --precision
+DTYPES = {"fp32": "f32", "tf32": "tf32", "3xtf32": "3xtf32", "f16": "f16",
+          "tf32h": "tf32 (forward), f16-stored operands in the weight-gradient GEMMs"}
 
 
 def window(w, k):
@@ -356,7 +359,7 @@ def run_ours(args, w):
     if rank == 0:
         line = {"metric": "particle-sample grad evals/sec", "value": value, "unit": "particle-sample grad evals/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else args.precision,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPES.get(args.precision, args.precision),
                 "data": "synthetic (teacher-labelled, seeded; BASELINE.json configs[1] shapes)",
                 "config": {"workload": w["desc"], "particles_per_gpu": J, "iterations": [ks[0], ks[-1]],
                            "window_rows": [Ms[0], Ms[-1]], "precision": args.precision, "resample": rk,
@@ -386,7 +389,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--precision", default=None, choices=["fp32", "tf32", "3xtf32", "f16"],
+    ap.add_argument("--precision", default=None, choices=["fp32", "tf32", "tf32h", "3xtf32", "f16"],
                     help="default: tf32 where the tensor-core path applies (one-hidden-layer MLPs), else fp32")
     ap.add_argument("--resample", default="systematic", choices=["systematic", "multinomial"])
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -394,8 +397,11 @@ def main():
     args = ap.parse_args()
     w = WORKLOADS[args.config]
     if args.precision is None:
-        tc_ok = "conv" not in w and len(w["layers"]) == 3 and w["layers"][1] <= 256 and w["layers"][2] <= 16
-        args.precision = "tf32" if tc_ok else "fp32"
+        # one hidden layer: tf32 forward + fp16-stored weight-gradient operands (tf32h, same
+        # 11-bit significand, tolerance of the tf32 path); deep MLPs: tf32 chain; CNNs: fp32
+        tc1 = "conv" not in w and len(w["layers"]) == 3 and w["layers"][1] <= 256 and w["layers"][2] <= 16
+        deep = "conv" not in w and len(w["layers"]) > 3 and w["layers"][-1] <= 16
+        args.precision = "tf32h" if tc1 else "tf32" if deep else "fp32"
     if args.impl == "reference":
         run_reference(args, w)
     else:

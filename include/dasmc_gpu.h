@@ -56,6 +56,10 @@ extern "C" {
 #define DASMC_PREC_3XTF32 2 /* tcgen05 split-tf32 (3 MMAs) tensor-core path, fp32-level accuracy */
 #define DASMC_PREC_F16 3    /* tcgen05 kind::f16 with fp16 operands (the same 10-bit mantissa as tf32, fp32
                                accumulation, half the operand bytes); one-hidden-layer MLPs */
+#define DASMC_PREC_TF32H 4  /* tf32 forward (kind::tf32 on tf32-rounded X, [W1, b1]); the weight-gradient
+                               GEMM operands (X^T, a1^T, delta1^T, delta2^T: bounded-range activations and
+                               deltas) stored as fp16, which carries the same 11-bit significand as tf32,
+                               and contracted with kind::f16 (fp32 accumulation).  Deep MLPs run as TF32 */
 /* ScheduleKind (annealing.hpp:18). */
 #define DASMC_SCHED_CONSTANT 0
 #define DASMC_SCHED_FULL_BATCH 1

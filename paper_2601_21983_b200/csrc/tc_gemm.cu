@@ -33,7 +33,9 @@ struct TcState {
   int64_t mcap = 0;      // row stride of the transposed activation buffers
   bool split = false;    // split-tf32 (3 MMAs)
   bool f16 = false;      // fp16 operands, kind::f16 (DASMC_PREC_F16): same 10-bit mantissa as tf32
-  int esz = 4;           // operand element bytes (2 when f16)
+  int esz = 4;           // forward operand (Xhi, W1hi) element bytes (2 when f16)
+  bool hstore = false;   // tf32h (DASMC_PREC_TF32H): tf32 forward, weight-gradient GEMM operands in fp16
+  int besz = 4;          // weight-gradient operand (Xt, a1T, d1T, d2T) element bytes
   int cluster = 1;       // fused-forward cluster shape (ClusterShape CL; 0 = single CTAs); DASMC_TC_CLUSTER
   float* Xt = nullptr;   // [(n0+1) x n_pad], row n0 = 1
   int64_t kx = 0;        // row stride of Xhi / W1hi: [x, 1] padded to 16 bytes (bias folded into K)
@@ -465,8 +467,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int unit0 = (int)blockIdx.x / CSZ;
   const int ustride = (int)gridDim.x / CSZ;
   const uint32_t b_rows = PAIR ? (uint32_t)tp.nmma / 2 : (uint32_t)tp.nmma;  // B rows held by this CTA
-  constexpr int BKE = PREC == 1 ? 64 : 32;  // K elements per 128-byte swizzle row (= per k-block)
-  using TS = OpT<PREC>;
+  // PREC 0: tf32 MMA, fp32 containers; 1: fp16 MMA and stores; 2 (forward only): tf32 MMA
+  // with the epilogue's GEMM-operand stores (a1^T, delta1^T, delta2^T) in fp16 (kTf32h)
+  constexpr int KP = PREC == 2 ? 0 : PREC;  // MMA kind / operand loads
+  constexpr int SP = PREC == 2 ? 1 : PREC;  // epilogue store type
+  constexpr int BKE = KP == 1 ? 64 : 32;    // K elements per 128-byte swizzle row (= per k-block)
+  using TS = OpT<SP>;
   const uint32_t a_bytes = BM * 128;
   const uint32_t b_bytes = b_rows * 128;
   const uint32_t sub = SPLIT ? 2 : 1;
@@ -627,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread; the leader's when PAIR) =====================
     if (lane == 0 && prank == 0) {
-      const uint32_t idesc = PREC == 1 ? idesc_f16(tp.nmma, PAIR ? 2 * BM : BM) : idesc_tf32(tp.nmma, PAIR ? 2 * BM : BM);
+      const uint32_t idesc = KP == 1 ? idesc_f16(tp.nmma, PAIR ? 2 * BM : BM) : idesc_tf32(tp.nmma, PAIR ? 2 * BM : BM);
       const uint16_t all_mask = (uint16_t)((1u << CSZ) - 1u);
       const uint16_t pair_mask = (uint16_t)(3u << (2 * pr));
       int s = 0;
@@ -647,16 +653,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < 4; ++k) {  // 32 bytes of K per instruction
             const uint64_t off = (uint64_t)(k * 32) >> 4;  // 32 bytes per K=8 step inside the swizzle row
             if (PAIR) {
-              tc_mma2<PREC>(d, ad + off, bd + off, idesc, (kb | k) != 0);
+              tc_mma2<KP>(d, ad + off, bd + off, idesc, (kb | k) != 0);
               if (SPLIT) {
-                tc_mma2<PREC>(d, ad + off, bdl + off, idesc, 1);
-                tc_mma2<PREC>(d, adl + off, bd + off, idesc, 1);
+                tc_mma2<KP>(d, ad + off, bdl + off, idesc, 1);
+                tc_mma2<KP>(d, adl + off, bd + off, idesc, 1);
               }
             } else {
-              tc_mma<PREC>(d, ad + off, bd + off, idesc, (kb | k) != 0);
+              tc_mma<KP>(d, ad + off, bd + off, idesc, (kb | k) != 0);
               if (SPLIT) {
-                tc_mma<PREC>(d, ad + off, bdl + off, idesc, 1);
-                tc_mma<PREC>(d, adl + off, bd + off, idesc, 1);
+                tc_mma<KP>(d, ad + off, bdl + off, idesc, 1);
+                tc_mma<KP>(d, adl + off, bd + off, idesc, 1);
               }
             }
           }
@@ -809,7 +815,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < CP; ++c) z2[c] = fmaf(a, w[c], z2[c]);
             if (decltype(store)::value) {
-              const TS hi = to_op<PREC>(a);
+              const TS hi = to_op<SP>(a);
               pa[q * kRow] = hi;
               if (SPLIT) st_act(pal + q * kRow, a - (float)hi, st_pol);
             }
@@ -890,7 +896,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (c < C) {
                   d2[c] = wrow * ((c == yi ? 1.f : 0.f) - e[c] * rden);
                   if (part == 0) {
-                    const TS hi = to_op<PREC>(d2[c]);
+                    const TS hi = to_op<SP>(d2[c]);
                     d2T[c * kRow] = hi;
                     if (SPLIT) d2Tlo[c * kRow] = d2[c] - (float)hi;
                   }
@@ -898,7 +904,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           } else if (fp.need_grad && part == 0) {  // rows past the window: zeros in the row-blocked delta2^T
             for (int c = 0; c < C; ++c) {
-              d2T[c * kRow] = to_op<PREC>(0.f);
+              d2T[c * kRow] = to_op<SP>(0.f);
               if (SPLIT) d2Tlo[c * kRow] = 0.f;
             }
           }
@@ -929,7 +935,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float a = tanhf(v[q]);
                 d1 = dz * (1.f - a * a);
               }
-              const TS hi = to_op<PREC>(d1);
+              const TS hi = to_op<SP>(d1);
               if (fp.dbg != 6) pd[q * kRow] = hi;
               if (SPLIT) st_act(pdl + q * kRow, d1 - (float)hi, st_pol);
             };
@@ -1086,9 +1092,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ---------------------------------------------------------------- helper kernels
 // X^T with a ones row (and tf32 hi/lo splits): Xt[i][m] = X[m][i], Xt[n0][m] = 1.
 // Also the forward operand Xhi[m] = [X[m], 1, 0 ...] (row stride kx) and its lo part.
-template <int PREC>
+// PT / PH: operand precision (0 tf32, 1 fp16) of Xt (weight-gradient A) and Xhi (forward A).
+template <int PT, int PH>
 __global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n0, int64_t n_pad, int64_t kx,
-                                   OpT<PREC>* Xt, float* Xtlo, OpT<PREC>* Xhi, float* Xlo, int split) {
+                                   OpT<PT>* Xt, float* Xtlo, OpT<PH>* Xhi, float* Xlo, int split) {
   __shared__ float tile[32][33];
   const int64_t m0 = (int64_t)blockIdx.x * 32;
   const int i0 = blockIdx.y * 32;
@@ -1098,7 +1105,7 @@ __global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n
     float v = 0.f;
     if (m < n && i < n0) v = X[m * n0 + i];
     if (m < n && i == n0) v = 1.f;
-    if (m < n && i < kx) Xhi[m * kx + i] = to_op<PREC>(v);
+    if (m < n && i < kx) Xhi[m * kx + i] = to_op<PH>(v);
     if (split && m < n && i < kx) Xlo[m * kx + i] = v - tf32_hi(v);
     tile[r][threadIdx.x] = v;
   }
@@ -1108,7 +1115,7 @@ __global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n
     const int64_t m = m0 + threadIdx.x;
     if (i <= n0 && m < n_pad) {
       const float v = m < n ? tile[threadIdx.x][r] : 0.f;
-      const OpT<PREC> hi = to_op<PREC>(v);
+      const OpT<PT> hi = to_op<PT>(v);
       Xt[(int64_t)i * n_pad + m] = hi;
       if (split) Xtlo[(int64_t)i * n_pad + m] = v - (float)hi;
     }
@@ -1464,10 +1471,29 @@ bool tc_layer1_eligible(const Ctx& c) {
   if (n.L == 2) return n.sizes[0] % 4 == 0 && n.sizes[0] >= 4 && n.sizes[1] <= 256 && n.sizes[2] <= 16;
   if (c.precision == DASMC_PREC_F16) return false;  // fp16 operands: one-hidden-layer path only
   // deep path (tc_eval_deep): tf32, <= 16 classes, output layer weights in shared memory
-  if (c.precision != DASMC_PREC_TF32 || n.sizes[n.L] > 16 || (int64_t)n.sizes[n.L - 1] * 16 > 16384) return false;
+  if ((c.precision != DASMC_PREC_TF32 && c.precision != DASMC_PREC_TF32H) || n.sizes[n.L] > 16 || (int64_t)n.sizes[n.L - 1] * 16 > 16384) return false;
   for (int l = 0; l < n.L; ++l)
     if (n.sizes[l] > 8192) return false;
   return true;
+}
+
+// Xt (weight-gradient A operand, fp16 in the f16 / tf32h modes) and Xhi (forward A
+// operand, fp16 only in the f16 mode) from the first n rows of X.
+static void transpose_x(Ctx& c, int64_t n) {
+  TcState* s = c.tc;
+  dim3 grid((unsigned)((s->n_pad + 31) / 32), (unsigned)((s->n0 + 1 + 31) / 32));
+  if (s->f16)
+    transpose_x_kernel<1, 1><<<grid, dim3(32, 8), 0, c.stream>>>(
+        c.X, n, s->n0, s->n_pad, s->kx, reinterpret_cast<__half*>(s->Xt), nullptr, reinterpret_cast<__half*>(s->Xhi),
+        nullptr, 0);
+  else if (s->hstore)
+    transpose_x_kernel<1, 0><<<grid, dim3(32, 8), 0, c.stream>>>(c.X, n, s->n0, s->n_pad, s->kx,
+                                                                 reinterpret_cast<__half*>(s->Xt), nullptr, s->Xhi,
+                                                                 nullptr, 0);
+  else
+    transpose_x_kernel<0, 0><<<grid, dim3(32, 8), 0, c.stream>>>(c.X, n, s->n0, s->n_pad, s->kx, s->Xt, s->Xtlo,
+                                                                 s->Xhi, s->Xlo, s->split ? 1 : 0);
+  LAUNCHED();
 }
 
 void tc_init(Ctx& c) {
@@ -1481,14 +1507,16 @@ void tc_init(Ctx& c) {
   s->C = c.net.sizes[2];
   s->split = c.precision == DASMC_PREC_3XTF32;
   s->f16 = c.precision == DASMC_PREC_F16;
+  s->hstore = c.precision == DASMC_PREC_TF32H && !s->deep;  // deep MLPs: plain tf32
   s->esz = s->f16 ? 2 : 4;
+  s->besz = (s->f16 || s->hstore) ? 2 : 4;
   if (const char* e = std::getenv("DASMC_TC_CLUSTER")) s->cluster = std::max(0, std::min(4, std::atoi(e)));
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, dev));
   s->n_pad = (c.n + 31) / 32 * 32;
   const size_t xt = (size_t)(s->n0 + 1) * s->n_pad;
-  CK(cudaMalloc(&s->Xt, (size_t)s->esz * xt));
+  CK(cudaMalloc(&s->Xt, (size_t)s->besz * xt));
   // [x, 1] padded so the row stride is a multiple of 16 bytes
   s->kx = s->f16 ? (s->n0 + 1 + 7) / 8 * 8 : (s->n0 + 1 + 3) / 4 * 4;
   const size_t w = (size_t)c.Jmax * s->n1 * s->kx;
@@ -1514,15 +1542,7 @@ void tc_init(Ctx& c) {
     CK(cudaMalloc(&s->Xlo, sizeof(float) * (size_t)c.n * s->kx));
     CK(cudaMalloc(&s->W1lo, sizeof(float) * w));
   }
-  dim3 grid((unsigned)((s->n_pad + 31) / 32), (unsigned)((s->n0 + 1 + 31) / 32));
-  if (s->f16)
-    transpose_x_kernel<1><<<grid, dim3(32, 8), 0, c.stream>>>(
-        c.X, c.n, s->n0, s->n_pad, s->kx, reinterpret_cast<__half*>(s->Xt), nullptr, reinterpret_cast<__half*>(s->Xhi),
-        nullptr, 0);
-  else
-    transpose_x_kernel<0><<<grid, dim3(32, 8), 0, c.stream>>>(c.X, c.n, s->n0, s->n_pad, s->kx, s->Xt, s->Xtlo,
-                                                              s->Xhi, s->Xlo, s->split ? 1 : 0);
-  LAUNCHED();
+  transpose_x(c, c.n);
   CK(cudaStreamSynchronize(c.stream));
 }
 
@@ -1543,16 +1563,7 @@ void tc_free(Ctx& c) {
 }
 
 void tc_refresh_data(Ctx& c) {
-  TcState* s = c.tc;
-  dim3 grid((unsigned)((s->n_pad + 31) / 32), (unsigned)((s->n0 + 1 + 31) / 32));
-  if (s->f16)
-    transpose_x_kernel<1><<<grid, dim3(32, 8), 0, c.stream>>>(
-        c.X, c.n_active, s->n0, s->n_pad, s->kx, reinterpret_cast<__half*>(s->Xt), nullptr,
-        reinterpret_cast<__half*>(s->Xhi), nullptr, 0);
-  else
-    transpose_x_kernel<0><<<grid, dim3(32, 8), 0, c.stream>>>(c.X, c.n_active, s->n0, s->n_pad, s->kx, s->Xt,
-                                                              s->Xtlo, s->Xhi, s->Xlo, s->split ? 1 : 0);
-  LAUNCHED();
+  transpose_x(c, c.n_active);
 }
 
 void tc_ensure_rows(Ctx& c, int64_t Mcap) {
@@ -1595,9 +1606,9 @@ void tc_ensure_rows(Ctx& c, int64_t Mcap) {
       *b = nullptr;
     }
   const size_t J = (size_t)c.Jmax;
-  CK(cudaMalloc(&s->a1T, (size_t)s->esz * J * (s->n1 + 1) * Mcap));
-  CK(cudaMalloc(&s->d1T, (size_t)s->esz * J * s->n1 * Mcap));
-  CK(cudaMalloc(&s->d2T, (size_t)s->esz * J * s->C * Mcap));
+  CK(cudaMalloc(&s->a1T, (size_t)s->besz * J * (s->n1 + 1) * Mcap));
+  CK(cudaMalloc(&s->d1T, (size_t)s->besz * J * s->n1 * Mcap));
+  CK(cudaMalloc(&s->d2T, (size_t)s->besz * J * s->C * Mcap));
   if (s->split) {
     CK(cudaMalloc(&s->a1Tlo, sizeof(float) * J * (s->n1 + 1) * Mcap));
     CK(cudaMalloc(&s->d1Tlo, sizeof(float) * J * s->n1 * Mcap));
@@ -1605,7 +1616,7 @@ void tc_ensure_rows(Ctx& c, int64_t Mcap) {
   }
   s->mcap = Mcap;
   const int g = (int)std::min<int64_t>((J * Mcap + 255) / 256, 148 * 16);
-  if (s->f16)
+  if (s->besz == 2)
     fill_ones_row_kernel<<<g, 256, 0, c.stream>>>(reinterpret_cast<__half*>(s->a1T), (int64_t)J, s->n1 + 1, s->n1,
                                                   Mcap, 1.f);
   else
@@ -1777,8 +1788,10 @@ template <int PREC>
 void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, double beta_rows, bool need_grad,
                    const EpiParams* epi) {
   TcState* s = c.tc;
-  constexpr int BKE = PREC == 1 ? 64 : 32;
-  const int esz = PREC == 1 ? 2 : 4;
+  // PREC 2 (tf32h): tf32 forward (X, W1 tf32), fp16 weight-gradient operands (kind::f16)
+  constexpr int FP = PREC == 1 ? 1 : 0, BP = PREC >= 1 ? 1 : 0;
+  constexpr int BKE = FP == 1 ? 64 : 32, BKB = BP == 1 ? 64 : 32;
+  const int esz = FP == 1 ? 2 : 4, besz = BP == 1 ? 2 : 4;
   const NetDev& net = c.net;
   const LayerDev& l1 = net.layer[0];
   const LayerDev& l2 = net.layer[1];
@@ -1792,8 +1805,8 @@ void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t 
     // [W1, b1] -> tf32 (rna) hi [+ lo]: the MMA would otherwise truncate the low mantissa
     // bits; the bias rides along as K column n0 against X's ones column
     const int64_t kx = s->kx, cnt = (int64_t)n1 * kx;
-    split_w1_kernel<PREC><<<148 * 8, 256, 0, c.stream>>>(
-        theta_in, net.Dp, l1.woff, l1.boff, n0, kx, cnt, J, reinterpret_cast<OpT<PREC>*>(s->W1hi),
+    split_w1_kernel<FP><<<148 * 8, 256, 0, c.stream>>>(
+        theta_in, net.Dp, l1.woff, l1.boff, n0, kx, cnt, J, reinterpret_cast<OpT<FP>*>(s->W1hi),
         PREC == 0 && s->split ? s->W1lo : nullptr);
     LAUNCHED();
     // rows >= M of X are TMA zero fill (ones column included): z1 = 0 there
@@ -1888,43 +1901,43 @@ void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t 
   // ---- layer 2: dW2^T[o, c] = sum_m a1^T[o, m] delta2^T[c, m]  (ones row o = n1 -> db2)
   {
     const uint64_t nbu = (uint64_t)(M + 127) / 128, nba = (uint64_t)ldm / 128;
-    const CUtensorMap A = map_blk(s->a1T, n1 + 1, nbu, nba, J, BM, esz);
+    const CUtensorMap A = map_blk(s->a1T, n1 + 1, nbu, nba, J, BM, besz);
     const CUtensorMap Alo = s->split ? map_blk(s->a1Tlo, n1 + 1, nbu, nba, J, BM) : A;
-    const CUtensorMap B = map_blk(s->d2T, C, nbu, nba, J, C, esz);
+    const CUtensorMap B = map_blk(s->d2T, C, nbu, nba, J, C, besz);
     const CUtensorMap Blo = s->split ? map_blk(s->d2Tlo, C, nbu, nba, J, C) : B;
     TileParams tp{};
     tp.rtiles = (n1 + 1 + BM - 1) / BM;
     tp.J = (int)J;
     tp.rg = tp.rtiles;
-    tp.nkb = (int)((M + BKE - 1) / BKE);
+    tp.nkb = (int)((M + BKB - 1) / BKB);
     tp.nmma = round16(C);
     tp.brows = C;
     DwParams dp{*epi, net.Dp, l2.woff, l2.boff, n1, C};
     if (PREC == 0 && s->split)
       launch_tc<kEpiKindDw, PREC == 0, kABlocked>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
     else
-      launch_tc<kEpiKindDw, false, kABlocked, 4, 0, 0, PREC>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+      launch_tc<kEpiKindDw, false, kABlocked, 4, 0, 0, BP>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
   }
   // ---- layer 1: dW1^T[i, o] = sum_m X^T[i, m] delta1^T[o, m]  (ones row i = n0 -> db1)
   {
     KTimer kt(c, 1);
-    const CUtensorMap A = map2d(s->Xt, M, n0 + 1, s->n_pad, BM, esz);
+    const CUtensorMap A = map2d(s->Xt, M, n0 + 1, s->n_pad, BM, besz);
     const CUtensorMap Alo = s->split ? map2d(s->Xtlo, M, n0 + 1, s->n_pad, BM) : A;
     const uint64_t nbu = (uint64_t)(M + 127) / 128, nba = (uint64_t)ldm / 128;
-    const CUtensorMap B = map_blk(s->d1T, n1, nbu, nba, J, n1, esz);
+    const CUtensorMap B = map_blk(s->d1T, n1, nbu, nba, J, n1, besz);
     const CUtensorMap Blo = s->split ? map_blk(s->d1Tlo, n1, nbu, nba, J, n1) : B;
     TileParams tp{};
     tp.rtiles = (n0 + 1 + BM - 1) / BM;
     tp.J = (int)J;
     tp.rg = tp.rtiles;
-    tp.nkb = (int)((M + BKE - 1) / BKE);
+    tp.nkb = (int)((M + BKB - 1) / BKB);
     tp.nmma = round16(n1);
     tp.brows = n1;
     DwParams dp{*epi, net.Dp, l1.woff, l1.boff, n0, n1};
     if (PREC == 0 && s->split)
       launch_tc<kEpiKindDw, PREC == 0, kAShared>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
     else
-      launch_tc<kEpiKindDw, false, kAShared, 4, 0, 0, PREC>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
+      launch_tc<kEpiKindDw, false, kAShared, 4, 0, 0, BP>(c, A, Alo, B, Blo, tp, fp0, dp, 0);
   }
 }
 
@@ -1935,6 +1948,8 @@ void tc_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, dou
     tc_eval_deep(c, theta_in, J, M, P, beta_rows, need_grad, epi);
   else if (s->f16)
     tc_eval_fused<1>(c, theta_in, J, M, P, beta_rows, need_grad, epi);
+  else if (s->hstore)
+    tc_eval_fused<2>(c, theta_in, J, M, P, beta_rows, need_grad, epi);
   else
     tc_eval_fused<0>(c, theta_in, J, M, P, beta_rows, need_grad, epi);
 }
