@@ -63,7 +63,8 @@ WORKLOADS = {
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # arithmetic of the dense contractions per --precision
 DTYPES = {"fp32": "f32", "tf32": "tf32", "3xtf32": "3xtf32", "f16": "f16",
-          "tf32h": "tf32 (forward), f16-stored operands in the weight-gradient GEMMs"}
+          "tf32h": "tf32 (forward), f16-stored operands in the weight-gradient GEMMs",
+          "f16x2": "f16 MMAs: X f16 x W1 split f16 hi+lo (forward), f16-stored operands (weight gradients)"}
 
 
 def window(w, k):
@@ -389,7 +390,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--precision", default=None, choices=["fp32", "tf32", "tf32h", "3xtf32", "f16"],
+    ap.add_argument("--precision", default=None, choices=["fp32", "tf32", "tf32h", "f16x2", "3xtf32", "f16"],
                     help="default: tf32 where the tensor-core path applies (one-hidden-layer MLPs), else fp32")
     ap.add_argument("--resample", default="systematic", choices=["systematic", "multinomial"])
     ap.add_argument("--e2e-steps", type=int, default=3)

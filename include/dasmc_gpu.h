@@ -60,6 +60,11 @@ extern "C" {
                                GEMM operands (X^T, a1^T, delta1^T, delta2^T: bounded-range activations and
                                deltas) stored as fp16, which carries the same 11-bit significand as tf32,
                                and contracted with kind::f16 (fp32 accumulation).  Deep MLPs run as TF32 */
+#define DASMC_PREC_F16X2 5  /* kind::f16 throughout; forward = X (fp16: the same 11-bit significand as tf32)
+                               times [W1, b1] split into fp16 hi + lo (two MMAs, ~22 significand bits);
+                               weight-gradient operands fp16 as in TF32H.  At least tf32 accuracy, fp16
+                               exponent range (|theta| >= 65504 overflows -> the particle diverges);
+                               one-hidden-layer MLPs */
 /* ScheduleKind (annealing.hpp:18). */
 #define DASMC_SCHED_CONSTANT 0
 #define DASMC_SCHED_FULL_BATCH 1

@@ -19,7 +19,7 @@ RELU, TANH = 0, 1
 SCALED, SDA = 0, 1
 HMC, LANGEVIN = 0, 1
 MULTINOMIAL, SYSTEMATIC = 0, 1
-PREC_FP32, PREC_TF32, PREC_3XTF32, PREC_F16, PREC_TF32H = 0, 1, 2, 3, 4
+PREC_FP32, PREC_TF32, PREC_3XTF32, PREC_F16, PREC_TF32H, PREC_F16X2 = 0, 1, 2, 3, 4, 5
 SCHED_CONSTANT, SCHED_FULL_BATCH, SCHED_CTR, SCHED_LINEAR, SCHED_AUTOMATED, SCHED_SDA = range(6)
 
 

@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _lib as L
 
-_PREC = {"fp32": L.PREC_FP32, "tf32": L.PREC_TF32, "3xtf32": L.PREC_3XTF32, "f16": L.PREC_F16, "tf32h": L.PREC_TF32H}
+_PREC = {"fp32": L.PREC_FP32, "tf32": L.PREC_TF32, "3xtf32": L.PREC_3XTF32, "f16": L.PREC_F16, "tf32h": L.PREC_TF32H, "f16x2": L.PREC_F16X2}
 _SCHED = {"constant": L.SCHED_CONSTANT, "full_batch": L.SCHED_FULL_BATCH, "ctr": L.SCHED_CTR,
           "linear": L.SCHED_LINEAR, "automated": L.SCHED_AUTOMATED, "sda": L.SCHED_SDA}
 _RESAMPLE = {"multinomial": L.MULTINOMIAL, "systematic": L.SYSTEMATIC}

@@ -396,7 +396,7 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
   if (X == nullptr || y == nullptr) throw InvalidArg("dataset: null X or y");
   if (Jmax < 2) throw InvalidArg("max_particles must be >= 2");
   if (precision != DASMC_PREC_FP32 && precision != DASMC_PREC_TF32 && precision != DASMC_PREC_3XTF32 &&
-      precision != DASMC_PREC_F16 && precision != DASMC_PREC_TF32H)
+      precision != DASMC_PREC_F16 && precision != DASMC_PREC_TF32H && precision != DASMC_PREC_F16X2)
     throw InvalidArg("bad precision");
   const int C = c.net.sizes[c.net.L];
   for (int64_t i = 0; i < n; ++i)

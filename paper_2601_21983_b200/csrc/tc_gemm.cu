@@ -34,6 +34,7 @@ struct TcState {
   bool split = false;    // split-tf32 (3 MMAs)
   bool f16 = false;      // fp16 operands, kind::f16 (DASMC_PREC_F16): same 10-bit mantissa as tf32
   int esz = 4;           // forward operand (Xhi, W1hi) element bytes (2 when f16)
+  bool f16x2 = false;    // f16x2 (DASMC_PREC_F16X2): f16 mode with W1 as fp16 hi + lo (two forward MMAs)
   bool hstore = false;   // tf32h (DASMC_PREC_TF32H): tf32 forward, weight-gradient GEMM operands in fp16
   int besz = 4;          // weight-gradient operand (Xt, a1T, d1T, d2T) element bytes
   int cluster = 1;       // fused-forward cluster shape (ClusterShape CL; 0 = single CTAs); DASMC_TC_CLUSTER
@@ -468,15 +469,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ustride = (int)gridDim.x / CSZ;
   const uint32_t b_rows = PAIR ? (uint32_t)tp.nmma / 2 : (uint32_t)tp.nmma;  // B rows held by this CTA
   // PREC 0: tf32 MMA, fp32 containers; 1: fp16 MMA and stores; 2 (forward only): tf32 MMA
-  // with the epilogue's GEMM-operand stores (a1^T, delta1^T, delta2^T) in fp16 (kTf32h)
-  constexpr int KP = PREC == 2 ? 0 : PREC;  // MMA kind / operand loads
-  constexpr int SP = PREC == 2 ? 1 : PREC;  // epilogue store type
+  // with the epilogue's GEMM-operand stores (a1^T, delta1^T, delta2^T) in fp16 (tf32h);
+  // 3 (forward only, f16x2): fp16 MMAs with B split into fp16 hi + lo parts, two MMAs per
+  // k-step (A . B_hi + A . B_lo), fp16 stores
+  constexpr int KP = PREC == 2 ? 0 : PREC == 3 ? 1 : PREC;  // MMA kind / operand loads
+  constexpr int SP = PREC >= 2 ? 1 : PREC;                  // epilogue store type
+  constexpr bool BSPL = SPLIT || PREC == 3;                 // B carries a lo part
   constexpr int BKE = KP == 1 ? 64 : 32;    // K elements per 128-byte swizzle row (= per k-block)
   using TS = OpT<SP>;
   const uint32_t a_bytes = BM * 128;
   const uint32_t b_bytes = b_rows * 128;
-  const uint32_t sub = SPLIT ? 2 : 1;
-  const uint32_t stage_bytes = sub * (a_bytes + b_bytes);
+  const uint32_t sub = SPLIT ? 2 : 1, subb = BSPL ? 2 : 1;
+  const uint32_t stage_bytes = sub * a_bytes + subb * b_bytes;
   uint8_t* stages = smem;
   uint64_t* bars = (uint64_t*)(smem + (size_t)tp.stages * stage_bytes);
   uint64_t* full = bars;
@@ -496,10 +500,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     prefetch_map(&mapA);
     prefetch_map(&mapB);
-    if (SPLIT) {
-      prefetch_map(&mapAlo);
-      prefetch_map(&mapBlo);
-    }
+    if (SPLIT) prefetch_map(&mapAlo);
+    if (BSPL) prefetch_map(&mapBlo);
     for (int s = 0; s < tp.stages; ++s) {
       mbar_init(&full[s], 1);
       // a stage is free once every pair of the cluster consumed it (multicast writes
@@ -585,10 +587,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int brow = (int)(prank * b_rows);
             if (QB == 1) {
               tma2_3d(B_of(s, 0), &mapB, fb, k0, brow, j, pol_b);
-              if (SPLIT) tma2_3d(B_of(s, 1), &mapBlo, fb, k0, brow, j, pol_b);
+              if (BSPL) tma2_3d(B_of(s, 1), &mapBlo, fb, k0, brow, j, pol_b);
             } else {
               tma2_3d_mc(B_of(s, 0) + boff * 128, &mapB, fb, k0, brow + boff, j, bmask, pol_b);
-              if (SPLIT) tma2_3d_mc(B_of(s, 1) + boff * 128, &mapBlo, fb, k0, brow + boff, j, bmask, pol_b);
+              if (BSPL) tma2_3d_mc(B_of(s, 1) + boff * 128, &mapBlo, fb, k0, brow + boff, j, bmask, pol_b);
             }
           } else {
             mbar_expect_tx(&full[s], tp.stage_bytes_tx);
@@ -606,10 +608,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (EPI == kEpiKindDw) {
               tma_4d(B_of(s, 0), &mapB, &full[s], k0 & 127, bn0, k0 >> 7, j);
-              if (SPLIT) tma_4d(B_of(s, 1), &mapBlo, &full[s], k0 & 127, bn0, k0 >> 7, j);
+              if (BSPL) tma_4d(B_of(s, 1), &mapBlo, &full[s], k0 & 127, bn0, k0 >> 7, j);
             } else {
               tma_3d(B_of(s, 0), &mapB, &full[s], k0, bn0, j);
-              if (SPLIT) tma_3d(B_of(s, 1), &mapBlo, &full[s], k0, bn0, j);
+              if (BSPL) tma_3d(B_of(s, 1), &mapBlo, &full[s], k0, bn0, j);
             }
           }
           if (++s == tp.stages) {
@@ -654,16 +656,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t off = (uint64_t)(k * 32) >> 4;  // 32 bytes per K=8 step inside the swizzle row
             if (PAIR) {
               tc_mma2<KP>(d, ad + off, bd + off, idesc, (kb | k) != 0);
-              if (SPLIT) {
-                tc_mma2<KP>(d, ad + off, bdl + off, idesc, 1);
-                tc_mma2<KP>(d, adl + off, bd + off, idesc, 1);
-              }
+              if (BSPL) tc_mma2<KP>(d, ad + off, bdl + off, idesc, 1);
+              if (SPLIT) tc_mma2<KP>(d, adl + off, bd + off, idesc, 1);
             } else {
               tc_mma<KP>(d, ad + off, bd + off, idesc, (kb | k) != 0);
-              if (SPLIT) {
-                tc_mma<KP>(d, ad + off, bdl + off, idesc, 1);
-                tc_mma<KP>(d, adl + off, bd + off, idesc, 1);
-              }
+              if (BSPL) tc_mma<KP>(d, ad + off, bdl + off, idesc, 1);
+              if (SPLIT) tc_mma<KP>(d, adl + off, bd + off, idesc, 1);
             }
           }
           if (PAIR)
@@ -745,6 +743,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* z2x = epi_smem + 2 * ((size_t)n1 * CS + CS);  // [kParts][128][CP] partial layer-2 logits
         ++it;
         const float* th = fp.theta + (int64_t)j * fp.Dp;
+        // the row's label: load in flight across the accumulator wait and pass 1
+        const int y_row = ((int64_t)rt * BM + row_in_tile < fp.M) ? __ldg(fp.y + (int64_t)rt * BM + row_in_tile) : 0;
         // per-particle layer-2 parameters: all global loads issued before any
         // shared-memory store (one L2 round trip per tile, not one per element)
         constexpr int kPer = (256 * CS + kEpiThreads - 1) / kEpiThreads;
@@ -777,29 +777,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         // contiguous region; consecutive rows of a block are 128 floats apart
         const int64_t nblk = fp.ldm;
         constexpr int64_t kRow = 128;
-        float z2[CP];
+        // class pairs in packed fp32x2 registers: the layer-2 FMAs issue as FFMA2 (two IEEE
+        // fp32 FMAs per instruction, the same per-class accumulation order)
+        static_assert(CP % 2 == 0, "class padding must be even");
+        float2 z2p[CP / 2];
 #pragma unroll
-        for (int c = 0; c < CP; ++c) z2[c] = 0.f;
+        for (int c = 0; c < CP / 2; ++c) z2p[c] = make_float2(0.f, 0.f);
         // DASMC_DEBUG_EPI=4 (profiling only): every tile stores into one L2-resident block
         const int64_t sblk = fp.dbg == 4 ? (int64_t)(blockIdx.x & 1) : (int64_t)j * nblk + rt;
         TS* a1T = reinterpret_cast<TS*>(fp.a1T) + sblk * (n1 + 1) * kRow + row_in_tile;
         float* a1Tlo = SPLIT ? fp.a1Tlo + ((int64_t)j * nblk + rt) * (n1 + 1) * kRow + row_in_tile : nullptr;
-        // row o of W2^T (CP classes) from shared memory: float4 loads (+ one float2)
-        auto w2row = [&](int o, float* w) {
+        // row o of W2^T (CP classes) from shared memory as class pairs: float4 loads (+ one float2)
+        auto w2row2 = [&](int o, float2* w) {
           const float* p = W2T + o * CS;
 #pragma unroll
           for (int u = 0; u < CP / 4; ++u) {
             const float4 x = *reinterpret_cast<const float4*>(p + 4 * u);
-            w[4 * u] = x.x;
-            w[4 * u + 1] = x.y;
-            w[4 * u + 2] = x.z;
-            w[4 * u + 3] = x.w;
+            w[2 * u] = make_float2(x.x, x.y);
+            w[2 * u + 1] = make_float2(x.z, x.w);
           }
-          if (CP % 4) {
-            const float2 x = *reinterpret_cast<const float2*>(p + 4 * (CP / 4));
-            w[CP - 2] = x.x;
-            w[CP - 1] = x.y;
-          }
+          if (CP % 4) w[CP / 2 - 1] = *reinterpret_cast<const float2*>(p + 4 * (CP / 4));
         };
         auto act = [](float z) { return ACT == DASMC_RELU ? fmaxf(z, 0.f) : tanhf(z); };
         // pass 1: a1 = act(z1); partial z2 = W2 a1 over this warp's columns
@@ -810,10 +807,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           float* pal = SPLIT ? a1Tlo + (int64_t)o0 * kRow : nullptr;
           auto one = [&](int q) {
             const float a = act(v[q]);
-            float w[CP];
-            w2row(o0 + q, w);
+            float2 w[CP / 2];
+            w2row2(o0 + q, w);
+            const float2 aa = make_float2(a, a);
 #pragma unroll
-            for (int c = 0; c < CP; ++c) z2[c] = fmaf(a, w[c], z2[c]);
+            for (int c = 0; c < CP / 2; ++c) z2p[c] = __ffma2_rn(aa, w[c], z2p[c]);
             if (decltype(store)::value) {
               const TS hi = to_op<SP>(a);
               pa[q * kRow] = hi;
@@ -853,12 +851,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // combine the column parts in a fixed order
         float* zx = z2x + ((size_t)part * 128 + row_in_tile) * CP;
 #pragma unroll
-        for (int c = 0; c < CP; ++c) zx[c] = z2[c];
+        for (int c = 0; c < CP / 2; ++c) reinterpret_cast<float2*>(zx)[c] = z2p[c];
         named_bar(1, kEpiThreads);
-        // every part: log-softmax likelihood of the row (network.hpp:183-193) --
-        // fp32 exponentials, fp64 log-normaliser and ll -- and delta2, computed
-        // redundantly per part (no second barrier); part 0 stores delta2^T
+        // every part: softmax of the row (fp32 exponentials and normaliser) and delta2,
+        // computed redundantly per part (no second barrier); part 0 alone forms the row's
+        // log-likelihood with an fp64 log-normaliser (network.hpp:183-193) and stores delta2^T
         double ll = 0.0;
+        float z2[CP];
         float d2[CP];
 #pragma unroll
         for (int c = 0; c < CP; ++c) d2[c] = 0.f;
@@ -873,24 +872,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           TS* d2T = reinterpret_cast<TS*>(fp.d2T) + ((int64_t)j * nblk + rt) * C * kRow + row_in_tile;
           float* d2Tlo = SPLIT ? fp.d2Tlo + ((int64_t)j * nblk + rt) * C * kRow + row_in_tile : nullptr;
           if (valid) {
-            const int yi = fp.y[m];
+            const int yi = y_row;
             float mx = z2[0];
 #pragma unroll
             for (int c = 1; c < CP; ++c)
               if (c < C) mx = fmaxf(mx, z2[c]);
             float e[CP];
-            double den = 0.0;
+            float den = 0.f;
             float zy = 0.f;
 #pragma unroll
             for (int c = 0; c < CP; ++c) {
               e[c] = c < C ? expf(z2[c] - mx) : 0.f;
-              den += (double)e[c];
+              den += e[c];
               if (c == yi) zy = z2[c];
             }
-            ll = (double)zy - ((double)mx + log(den));
+            if (part == 0) {
+              // the row's log-likelihood (network.hpp:183-193): fp64 log-normaliser, one part only
+              double den64 = 0.0;
+#pragma unroll
+              for (int c = 0; c < CP; ++c) den64 += (double)e[c];
+              ll = (double)zy - ((double)mx + log(den64));
+            }
             if (fp.need_grad) {
               const float wrow = m < fp.P ? 1.f : fp.beta_rows;
-              const float rden = (float)(1.0 / den);
+              const float rden = 1.f / den;  // every part: the same fp32 normaliser for delta2
 #pragma unroll
               for (int c = 0; c < CP; ++c)
                 if (c < C) {
@@ -913,21 +918,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           // pass 2: delta1 = (W2^T delta2) . act'(z1)  (network.hpp:209-215); zero past the window
           TS* d1T = reinterpret_cast<TS*>(fp.d1T) + sblk * n1 * kRow + row_in_tile;
           float* d1Tlo = SPLIT ? fp.d1Tlo + ((int64_t)j * nblk + rt) * n1 * kRow + row_in_tile : nullptr;
+          float2 d2p[CP / 2];
+#pragma unroll
+          for (int c = 0; c < CP / 2; ++c) d2p[c] = make_float2(d2[2 * c], d2[2 * c + 1]);
           auto chunk2 = [&](int ch, const float* v) {
             const int o0 = ch * 16;
             const int nq = min(16, n1 - o0);  // warp-uniform
             TS* pd = d1T + (int64_t)o0 * kRow;
             float* pdl = SPLIT ? d1Tlo + (int64_t)o0 * kRow : nullptr;
             auto one = [&](int q) {
-              float w[CP];
-              w2row(o0 + q, w);
-              float dx = 0.f, dy = 0.f;  // two independent chains
+              float2 w[CP / 2];
+              w2row2(o0 + q, w);
+              float2 acc = make_float2(0.f, 0.f);  // even / odd classes: two chains in one FFMA2
 #pragma unroll
-              for (int c = 0; c < CP; c += 2) {
-                dx = fmaf(d2[c], w[c], dx);
-                dy = fmaf(d2[c + 1], w[c + 1], dy);
-              }
-              const float dz = dx + dy;
+              for (int c = 0; c < CP / 2; ++c) acc = __ffma2_rn(d2p[c], w[c], acc);
+              const float dz = acc.x + acc.y;
               float d1;
               if (ACT == DASMC_RELU) {
                 d1 = v[q] > 0.f ? dz : 0.f;
@@ -1128,7 +1133,7 @@ __global__ void transpose_x_kernel(const float* __restrict__ X, int64_t n, int n
 template <int PREC>
 __global__ void __launch_bounds__(256) split_w1_kernel(const float* __restrict__ theta, int64_t Dp, int64_t woff,
                                                        int64_t boff, int n0, int64_t kx, int64_t cnt, int64_t J,
-                                                       OpT<PREC>* __restrict__ hi, float* __restrict__ lo) {
+                                                       OpT<PREC>* __restrict__ hi, OpT<PREC>* __restrict__ lo) {
   const int64_t n1 = cnt / kx;
   const int kq = (int)(kx >> 2);
   const int64_t total = J * n1 * kq;
@@ -1160,6 +1165,13 @@ __global__ void __launch_bounds__(256) split_w1_kernel(const float* __restrict__
       w.x = *reinterpret_cast<uint32_t*>(&p0);
       w.y = *reinterpret_cast<uint32_t*>(&p1);
       *reinterpret_cast<uint2*>(hi + off) = w;
+      if (lo) {  // f16x2: fp16 residual, hi + lo carries ~22 significand bits
+        __half2 q0 = __floats2half2_rn(v[0] - __half2float(h[0]), v[1] - __half2float(h[1]));
+        __half2 q1 = __floats2half2_rn(v[2] - __half2float(h[2]), v[3] - __half2float(h[3]));
+        w.x = *reinterpret_cast<uint32_t*>(&q0);
+        w.y = *reinterpret_cast<uint32_t*>(&q1);
+        *reinterpret_cast<uint2*>(lo + off) = w;
+      }
     } else {
       *reinterpret_cast<float4*>(hi + off) = make_float4(h[0], h[1], h[2], h[3]);
       if (lo) *reinterpret_cast<float4*>(lo + off) = make_float4(v[0] - h[0], v[1] - h[1], v[2] - h[2], v[3] - h[3]);
@@ -1410,9 +1422,9 @@ template <int EPI, bool SPLIT, int AM, int CP = 4, int ACT = 0, int CL = 0, int 
 void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUtensorMap& B, const CUtensorMap& Blo,
                TileParams tp, const FwdParams& fp, const DwParams& dp, size_t epi_smem_bytes) {
   using CS_ = ClusterShape<CL>;
-  const size_t sub = SPLIT ? 2 : 1;
+  const size_t sub = SPLIT ? 2 : 1, subb = (SPLIT || PREC == 3) ? 2 : 1;
   const size_t b_rows = CS_::kPair ? (size_t)tp.nmma / 2 : (size_t)tp.nmma;
-  const size_t stage_bytes = sub * ((size_t)BM * BK * 4 + b_rows * BK * 4);
+  const size_t stage_bytes = sub * (size_t)BM * BK * 4 + subb * b_rows * BK * 4;
   const size_t fixed = 1024 + 64 * 8 + 64 + epi_smem_bytes;
   const size_t budget = 227 * 1024;
   int stages = (int)std::min<size_t>(8, (budget - fixed) / stage_bytes);
@@ -1421,9 +1433,9 @@ void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUten
   if (CS_::kPair) {
     // bytes landing in the pair per stage (two overlapping B pieces when QB = 2)
     const size_t b_land = CS_::QB == 2 ? 2 * (size_t)tp.bbox : b_rows;
-    tp.stage_bytes_tx = (uint32_t)(2 * sub * ((size_t)BM * BK * 4 + b_land * BK * 4));
+    tp.stage_bytes_tx = (uint32_t)(2 * (sub * (size_t)BM * BK * 4 + subb * b_land * BK * 4));
   } else {
-    tp.stage_bytes_tx = (uint32_t)(sub * ((size_t)BM * BK * 4 + (size_t)tp.brows * BK * 4));
+    tp.stage_bytes_tx = (uint32_t)(sub * (size_t)BM * BK * 4 + subb * (size_t)tp.brows * BK * 4);
   }
   const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16 + epi_smem_bytes + 64;
   auto kern = tc_kernel<EPI, SPLIT, AM, CP, ACT, CL, PREC>;
@@ -1455,10 +1467,10 @@ void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUten
   if (CS_::kPair) {
     const int nclusters = std::max(1, std::min(ntiles, max_clusters));
     cfg.gridDim = dim3((unsigned)(CS_::kSize * nclusters));
-    CK(cudaLaunchKernelEx(&cfg, kern, A, SPLIT ? Alo : A, B, SPLIT ? Blo : B, tp, fp, dp));
+    CK(cudaLaunchKernelEx(&cfg, kern, A, SPLIT ? Alo : A, B, (SPLIT || PREC == 3) ? Blo : B, tp, fp, dp));
   } else {
     const int grid = std::max(1, std::min(ntiles, c.tc->num_sms));
-    kern<<<grid, kThreads, smem, c.stream>>>(A, SPLIT ? Alo : A, B, SPLIT ? Blo : B, tp, fp, dp);
+    kern<<<grid, kThreads, smem, c.stream>>>(A, SPLIT ? Alo : A, B, (SPLIT || PREC == 3) ? Blo : B, tp, fp, dp);
   }
   LAUNCHED();
 }
@@ -1469,7 +1481,7 @@ bool tc_layer1_eligible(const Ctx& c) {
   const NetDev& n = c.net;
   if (n.nconv != 0) return false;
   if (n.L == 2) return n.sizes[0] % 4 == 0 && n.sizes[0] >= 4 && n.sizes[1] <= 256 && n.sizes[2] <= 16;
-  if (c.precision == DASMC_PREC_F16) return false;  // fp16 operands: one-hidden-layer path only
+  if (c.precision == DASMC_PREC_F16 || c.precision == DASMC_PREC_F16X2) return false;  // one-hidden-layer only
   // deep path (tc_eval_deep): tf32, <= 16 classes, output layer weights in shared memory
   if ((c.precision != DASMC_PREC_TF32 && c.precision != DASMC_PREC_TF32H) || n.sizes[n.L] > 16 || (int64_t)n.sizes[n.L - 1] * 16 > 16384) return false;
   for (int l = 0; l < n.L; ++l)
@@ -1506,7 +1518,8 @@ void tc_init(Ctx& c) {
   s->n1 = c.net.sizes[1];
   s->C = c.net.sizes[2];
   s->split = c.precision == DASMC_PREC_3XTF32;
-  s->f16 = c.precision == DASMC_PREC_F16;
+  s->f16x2 = c.precision == DASMC_PREC_F16X2;
+  s->f16 = c.precision == DASMC_PREC_F16 || s->f16x2;
   s->hstore = c.precision == DASMC_PREC_TF32H && !s->deep;  // deep MLPs: plain tf32
   s->esz = s->f16 ? 2 : 4;
   s->besz = (s->f16 || s->hstore) ? 2 : 4;
@@ -1537,6 +1550,7 @@ void tc_init(Ctx& c) {
   } else {
     CK(cudaMalloc(&s->W1hi, (size_t)s->esz * w));
   }
+  if (s->f16x2) CK(cudaMalloc(&s->W1lo, (size_t)s->esz * w));
   if (s->split) {
     CK(cudaMalloc(&s->Xtlo, sizeof(float) * xt));
     CK(cudaMalloc(&s->Xlo, sizeof(float) * (size_t)c.n * s->kx));
@@ -1807,13 +1821,13 @@ void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t 
     const int64_t kx = s->kx, cnt = (int64_t)n1 * kx;
     split_w1_kernel<FP><<<148 * 8, 256, 0, c.stream>>>(
         theta_in, net.Dp, l1.woff, l1.boff, n0, kx, cnt, J, reinterpret_cast<OpT<FP>*>(s->W1hi),
-        PREC == 0 && s->split ? s->W1lo : nullptr);
+        (PREC == 0 && s->split) || (PREC == 1 && s->f16x2) ? reinterpret_cast<OpT<FP>*>(s->W1lo) : nullptr);
     LAUNCHED();
     // rows >= M of X are TMA zero fill (ones column included): z1 = 0 there
     // cluster shape (see ClusterShape): CTA pairs stream half of W1's rows each (box
     // nmma / 2, rows >= n1 zero fill); QA = 2 multicasts X rows (box 64 rows per CTA),
     // QB = 2 multicasts W1 rows (two pieces of bbox rows, multiples of 8)
-    const int cl = s->split ? std::min(s->cluster, 1) : s->cluster;
+    const int cl = (s->split || s->f16x2) ? std::min(s->cluster, 1) : s->cluster;
     const bool pair = cl > 0;
     const int QA = (cl == 2 || cl == 4) ? 2 : 1, QB = (cl == 3 || cl == 4) ? 2 : 1;
     const int half = round16(n1) / 2;
@@ -1822,7 +1836,9 @@ void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t 
     const CUtensorMap A = map2d(s->Xhi, n0 + 1, M, kx, BM / QA, esz);
     const CUtensorMap Alo = s->split ? map2d(s->Xlo, n0 + 1, M, kx, BM / QA) : A;
     const CUtensorMap B = map3d(s->W1hi, n0 + 1, n1, kx, J, cnt, bbox, esz);
-    const CUtensorMap Blo = s->split ? map3d(s->W1lo, n0 + 1, n1, kx, J, cnt, bbox) : B;
+    const CUtensorMap Blo = s->split    ? map3d(s->W1lo, n0 + 1, n1, kx, J, cnt, bbox)
+                            : s->f16x2 ? map3d(s->W1lo, n0 + 1, n1, kx, J, cnt, bbox, esz)
+                                       : B;
     TileParams tp{};
     tp.rtiles = pair ? (rtiles + 2 * QB - 1) / (2 * QB) : rtiles;
     tp.J = pair ? (int)((J + QA - 1) / QA) : (int)J;
@@ -1867,6 +1883,15 @@ void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t 
     DwParams dp{};
     auto go = [&](auto cp, auto act) {
       constexpr int K = decltype(cp)::value, A_ = decltype(act)::value;
+      if constexpr (PREC == 1) {
+        if (s->f16x2) {
+          if (pair)
+            launch_tc<kEpiKindFwd, false, kAShared, K, A_, 1, 3>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+          else
+            launch_tc<kEpiKindFwd, false, kAShared, K, A_, 0, 3>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+          return;
+        }
+      }
       if constexpr (PREC == 0) {
         if (s->split) {
           if (pair)

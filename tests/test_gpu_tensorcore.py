@@ -35,7 +35,7 @@ def problem(product, layers, act, n):
     return spec, X, y
 
 
-@pytest.mark.parametrize("prec", ["3xtf32", "tf32", "tf32h", "f16"])
+@pytest.mark.parametrize("prec", ["3xtf32", "tf32", "tf32h", "f16x2", "f16"])
 @pytest.mark.parametrize("layers,act,M", SHAPES)
 def test_tc_value_and_grad(product, oracle, layers, act, M, prec):
     n = max(M, 600)
@@ -96,7 +96,7 @@ def test_tc_run_matches_fp32_schedule(product):
     np.testing.assert_allclose(r3x[0]["mean_log_target"], r32[0]["mean_log_target"], rtol=1e-5)
 
 
-@pytest.mark.parametrize("prec", ["tf32", "tf32h", "f16"])
+@pytest.mark.parametrize("prec", ["tf32", "tf32h", "f16x2", "f16"])
 @pytest.mark.parametrize("cluster", [0, 1, 2, 3, 4])
 def test_tc_cluster_shapes(product, oracle, cluster, prec, monkeypatch):
     """Every fused-forward cluster shape (single CTAs, CTA pairs, pairs with X or W1
