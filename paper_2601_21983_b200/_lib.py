@@ -153,11 +153,24 @@ SIGNATURES = {
 _lib = None
 
 
+_alt = {}
+
+
 def load(path: str = LIB_PATH) -> C.CDLL:
-    """Load the product library (raises if it has not been built)."""
+    """Load the product library (raises if it has not been built).  A path other than
+    LIB_PATH loads a second build of the same sources side by side (A/B timing tools)."""
     global _lib
+    if path != LIB_PATH:
+        if path not in _alt:
+            _alt[path] = _bind(path)
+        return _alt[path]
     if _lib is not None:
         return _lib
+    _lib = _bind(path)
+    return _lib
+
+
+def _bind(path: str) -> C.CDLL:
     if not os.path.exists(path):
         raise RuntimeError(
             f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -167,7 +180,6 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    _lib = lib
     return lib
 
 

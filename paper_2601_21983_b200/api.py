@@ -222,8 +222,8 @@ class GpuEnsembleTarget:
     and the ensemble loop of ``smc_step`` (smc.hpp:109-158)."""
 
     def __init__(self, spec: NetSpec, X: np.ndarray, y: np.ndarray, max_particles: int, device: int = 0,
-                 precision: str = "fp32"):
-        self.lib = L.load()
+                 precision: str = "fp32", lib_path: str | None = None):
+        self.lib = L.load(lib_path) if lib_path else L.load()
         self.spec = spec
         self.D = param_count(spec)
         X = np.ascontiguousarray(X, dtype=np.float32)

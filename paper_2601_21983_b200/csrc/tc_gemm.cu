@@ -72,7 +72,10 @@ namespace {
 
 constexpr int BM = 128;  // UMMA_M
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row
-constexpr int kEpiWarps = 12;            // 3 warps per TMEM lane group
+#ifndef DASMC_EPI_WARPS
+#define DASMC_EPI_WARPS 12
+#endif
+constexpr int kEpiWarps = DASMC_EPI_WARPS;  // 3 warps per TMEM lane group (a multiple of 4)
 constexpr int kParts = kEpiWarps / 4;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;  // TMA warp + MMA warp + epilogue warps
@@ -735,6 +738,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // an extra K column), and rows past the window are TMA zero-fill, so
         // act(z1) = 0 there and every row-blocked store below is unconditional.
         const int n1 = fp.n1, C = fp.C;
+        // store / math ablations (DASMC_DEBUG_EPI, profiling only).  Kept as a runtime value:
+        // folding it to a constant measured 5 % slower (B200, in-process A/B, tools/tune_fwd.py):
+        // ptxas schedules the predicated store groups of the column loops better
+        const int dbg = fp.dbg;
         constexpr int CS = (CP + 3) & ~3;       // W2^T row stride (float4 aligned)
         // W2^T / b2 double-buffered by tile parity: the buffer written here was last read
         // two tiles ago, before every thread passed the previous tile's barriers
@@ -769,10 +776,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(lg * 32) << 16);
         const int64_t m = (int64_t)rt * BM + row_in_tile;
         const bool valid = m < fp.M;
-        const bool st_rows = fp.need_grad && fp.dbg != 1 && fp.dbg != 5;  // 5: no a1^T stores
+        const bool st_rows = fp.need_grad && dbg != 1 && dbg != 5;  // 5: no a1^T stores
         int c_lo, c_hi;
         chunk_range((n1 + 15) >> 4, c_lo, c_hi);
-        if (fp.dbg == 3) c_hi = c_lo;
+        if (dbg == 3) c_hi = c_lo;
         // transposed buffers are row-blocked [J][nblk][rows][128]: a tile's rows are one
         // contiguous region; consecutive rows of a block are 128 floats apart
         const int64_t nblk = fp.ldm;
@@ -784,7 +791,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < CP / 2; ++c) z2p[c] = make_float2(0.f, 0.f);
         // DASMC_DEBUG_EPI=4 (profiling only): every tile stores into one L2-resident block
-        const int64_t sblk = fp.dbg == 4 ? (int64_t)(blockIdx.x & 1) : (int64_t)j * nblk + rt;
+        const int64_t sblk = dbg == 4 ? (int64_t)(blockIdx.x & 1) : (int64_t)j * nblk + rt;
         TS* a1T = reinterpret_cast<TS*>(fp.a1T) + sblk * (n1 + 1) * kRow + row_in_tile;
         float* a1Tlo = SPLIT ? fp.a1Tlo + ((int64_t)j * nblk + rt) * (n1 + 1) * kRow + row_in_tile : nullptr;
         // row o of W2^T (CP classes) from shared memory as class pairs: float4 loads (+ one float2)
@@ -882,7 +889,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             float zy = 0.f;
 #pragma unroll
             for (int c = 0; c < CP; ++c) {
+#ifdef DASMC_V_FASTEXP
+              e[c] = c < C ? __expf(z2[c] - mx) : 0.f;
+#else
               e[c] = c < C ? expf(z2[c] - mx) : 0.f;
+#endif
               den += e[c];
               if (c == yi) zy = z2[c];
             }
@@ -914,7 +925,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        if (fp.need_grad && (fp.dbg == 0 || fp.dbg >= 5)) {  // 6: no delta1^T stores
+        if (fp.need_grad && (dbg == 0 || dbg >= 5)) {  // 6: no delta1^T stores
           // pass 2: delta1 = (W2^T delta2) . act'(z1)  (network.hpp:209-215); zero past the window
           TS* d1T = reinterpret_cast<TS*>(fp.d1T) + sblk * n1 * kRow + row_in_tile;
           float* d1Tlo = SPLIT ? fp.d1Tlo + ((int64_t)j * nblk + rt) * n1 * kRow + row_in_tile : nullptr;
@@ -929,10 +940,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             auto one = [&](int q) {
               float2 w[CP / 2];
               w2row2(o0 + q, w);
+#ifndef DASMC_V_ACC2
               float2 acc = make_float2(0.f, 0.f);  // even / odd classes: two chains in one FFMA2
 #pragma unroll
               for (int c = 0; c < CP / 2; ++c) acc = __ffma2_rn(d2p[c], w[c], acc);
               const float dz = acc.x + acc.y;
+#else
+              // class pairs alternate between two packed accumulators (four fp32 chains)
+              float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+              for (int c = 0; c < CP / 2; c += 2) {
+                acc0 = __ffma2_rn(d2p[c], w[c], acc0);
+                if (c + 1 < CP / 2) acc1 = __ffma2_rn(d2p[c + 1], w[c + 1], acc1);
+              }
+              const float dz = (acc0.x + acc1.x) + (acc0.y + acc1.y);
+#endif
               float d1;
               if (ACT == DASMC_RELU) {
                 d1 = v[q] > 0.f ? dz : 0.f;
@@ -941,7 +963,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 d1 = dz * (1.f - a * a);
               }
               const TS hi = to_op<SP>(d1);
-              if (fp.dbg != 6) pd[q * kRow] = hi;
+              if (dbg != 6) pd[q * kRow] = hi;
               if (SPLIT) st_act(pdl + q * kRow, d1 - (float)hi, st_pol);
             };
             if (nq == 16) {
@@ -1827,7 +1849,7 @@ void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t 
     // cluster shape (see ClusterShape): CTA pairs stream half of W1's rows each (box
     // nmma / 2, rows >= n1 zero fill); QA = 2 multicasts X rows (box 64 rows per CTA),
     // QB = 2 multicasts W1 rows (two pieces of bbox rows, multiples of 8)
-    const int cl = (s->split || s->f16x2) ? std::min(s->cluster, 1) : s->cluster;
+    const int cl = (s->split || PREC != 0) ? std::min(s->cluster, 1) : s->cluster;
     const bool pair = cl > 0;
     const int QA = (cl == 2 || cl == 4) ? 2 : 1, QB = (cl == 3 || cl == 4) ? 2 : 1;
     const int half = round16(n1) / 2;
@@ -1901,12 +1923,21 @@ void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t 
           return;
         }
       }
-      switch (cl) {
-        case 0: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 0, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
-        case 1: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 1, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
-        case 2: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 2, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
-        case 3: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 3, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
-        default: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 4, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+      // the multicast cluster shapes (CL 2..4, measured slower than plain pairs) are built for
+      // the tf32 path only; fp16-operand modes run single CTAs or pairs
+      if constexpr (PREC == 0) {
+        switch (cl) {
+          case 0: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 0, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+          case 1: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 1, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+          case 2: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 2, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+          case 3: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 3, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+          default: launch_tc<kEpiKindFwd, false, kAShared, K, A_, 4, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes); break;
+        }
+      } else {
+        if (cl == 0)
+          launch_tc<kEpiKindFwd, false, kAShared, K, A_, 0, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+        else
+          launch_tc<kEpiKindFwd, false, kAShared, K, A_, 1, PREC>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
       }
     };
     auto go_act = [&](auto cp) {

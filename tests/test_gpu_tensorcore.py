@@ -100,7 +100,8 @@ def test_tc_run_matches_fp32_schedule(product):
 @pytest.mark.parametrize("cluster", [0, 1, 2, 3, 4])
 def test_tc_cluster_shapes(product, oracle, cluster, prec, monkeypatch):
     """Every fused-forward cluster shape (single CTAs, CTA pairs, pairs with X or W1
-    multicast, both) gives the same gradients; odd J and M leave padding tiles."""
+    multicast, both; fp16-operand modes clamp to pairs) gives the same gradients; odd J and M
+    leave padding tiles."""
     monkeypatch.setenv("DASMC_TC_CLUSTER", str(cluster))
     layers, act = [784, 200, 10], "relu"
     n, M, J = 1200, 1100, 5

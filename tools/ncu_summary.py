@@ -30,7 +30,12 @@ FULL_METRICS = [
 
 
 def full(rep, out, cmd):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # a .ncu-rep, or the `--page raw --csv` export of one (made on the GPU box when the
+    # report itself is too large to bring back)
+    if rep.endswith(".csv"):
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     head, units = rows[0], rows[1]
     kernels = []

@@ -6,6 +6,7 @@ process so that box-to-box clock differences cancel.  Prints, per setting, the
 median fused-forward ms per launch, weight-gradient ms per launch and step ms.
 
   python tools/tune_fwd.py "DASMC_TC_CLUSTER=1" "DASMC_TC_CLUSTER=1 DASMC_TC_HINTA=1"
+  python tools/tune_fwd.py "PREC=tf32h" "PREC=tf32h LIB=_exp/variant.so"   # code A/B
 """
 from __future__ import annotations
 
@@ -46,10 +47,17 @@ def main():
         for s in args.settings:
             os.environ.clear()
             os.environ.update(base_env)
+            prec, lib_path = args.precision, None
             for kv in s.split():
                 k, v = kv.split("=", 1)
-                os.environ[k] = v
-            t = p.GpuEnsembleTarget(spec, X, y, J, device=0, precision=args.precision)
+                if k == "PREC":  # precision mode of this setting
+                    prec = v
+                elif k == "LIB":  # a second build of the library (A/B of code variants)
+                    lib_path = os.path.abspath(v)
+                else:
+                    os.environ[k] = v
+            t = p.GpuEnsembleTarget(spec, X, y, J, device=0, precision=prec, lib_path=lib_path)
+            lib = t.lib
             L.check(lib.dasmc_gpu_reserve_rows(t.h, M))
             t.set_target(0, M, N, "scaled", 1.0, 1.0)
             L.check(lib.dasmc_gpu_init_ensemble_at(t.h, J, 0, 0))
