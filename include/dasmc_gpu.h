@@ -335,6 +335,15 @@ int64_t dasmc_launch_count(void);
  * milliseconds and range counts since the last reset, then resets. */
 int dasmc_gpu_set_timing(dasmc_ctx* ctx, int enable);
 int dasmc_gpu_kernel_times(dasmc_ctx* ctx, double* ms3, int64_t* count3);
+/* Isolated timing of the step's memory-bound kernels on the context's buffers
+ * (bench / profiling only; tools/membench.py): reps launches each of
+ * 0: resample gather theta_new[j] = theta[idx[j]] (smc.hpp:97-99),
+ * 1: sum of squares of J momentum rows (the kinetic term, kernels.hpp:89-95),
+ * 2: momentum generation p ~ N(0, I) (smc.hpp:118-123, rng.hpp:76-81),
+ * 3: weights / normalise / ESS / CDF / systematic search (smc.hpp:28-99).
+ * idx (host, J entries in [0, J)) drives kernel 0.  ms4 = mean ms per launch,
+ * bytes4 = algorithmic HBM bytes per launch. */
+int dasmc_gpu_bench_memory(dasmc_ctx* ctx, int64_t J, const int32_t* idx, int reps, double* ms4, double* bytes4);
 
 /* xoshiro256++ draws [skip, skip+count) of stream `key`, reached with the
  * F2-linear jump-ahead the device generator uses (host check of rng.hpp:48-58). */

@@ -134,6 +134,7 @@ SIGNATURES = {
     "dasmc_launch_count": (C.c_int64, []),
     "dasmc_gpu_set_timing": (C.c_int, [_P, C.c_int]),
     "dasmc_gpu_kernel_times": (C.c_int, [_P, _D, _I64]),
+    "dasmc_gpu_bench_memory": (C.c_int, [_P, C.c_int64, _I32, C.c_int, _D, _D]),
     "dasmc_rng_skip": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(C.c_uint64)]),
     "dasmc_gpu_evaluate_predictive": (C.c_int, [_P, _F, _I32, C.c_int64, _D, _D]),
     "dasmc_gpu_predictive_mix": (C.c_int, [_P, _F, _I32, C.c_int64, _D, C.c_int64, _D]),

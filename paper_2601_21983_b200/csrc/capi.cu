@@ -138,7 +138,7 @@ void free_ctx(Ctx& c) {
   if (c.stream) cudaStreamSynchronize(c.stream);
   tc_free(c);
   void* ptrs[] = {c.X_full, c.Xt, c.y_full, c.Xg, c.yg, c.rows_dev, c.gcache[0], c.gcache[1], c.lt_cache, c.theta[0], c.theta[1], c.theta[2], c.p, c.grad, c.logw, c.dT, c.ll_part,
-                  c.th_part, c.p_part, c.p0_part, c.flags, c.lt_old, c.lt_new, c.ll_pre, c.ll_blk, c.ll_pre0, c.ll_blk0,
+                  c.th_part, c.p_part, c.p0_part, c.p0_sum, c.pS_sum, c.flags, c.lt_old, c.lt_new, c.ll_pre, c.ll_blk, c.ll_pre0, c.ll_blk0,
                   c.sda_pre, c.sda_blk, c.wts, c.cdf,
                   c.uni, c.idx, c.records, c.jump_tab, c.stage, c.sh_buf, c.sh_idx, c.sh_rows, c.iota};
   for (void* p : ptrs)
@@ -442,6 +442,8 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
   dmalloc(c.th_part, (size_t)Jmax * c.th_slots);
   dmalloc(c.p_part, (size_t)Jmax * c.th_slots);
   dmalloc(c.p0_part, (size_t)Jmax * c.rng_slots);
+  dmalloc(c.p0_sum, (size_t)Jmax);
+  dmalloc(c.pS_sum, (size_t)Jmax);
   dmalloc(c.flags, (size_t)Jmax);
   CK(cudaMemset(c.flags, 0, sizeof(int) * Jmax));
   dmalloc(c.lt_old, (size_t)Jmax);
@@ -1314,6 +1316,47 @@ int dasmc_gpu_run(const dasmc_net_desc* net, const float* X, const int32_t* y, i
   });
   if (ctx) dasmc_gpu_destroy(ctx);
   return rc;
+}
+
+int dasmc_gpu_bench_memory(dasmc_ctx* ctx, int64_t J, const int32_t* idx, int reps, double* ms4, double* bytes4) {
+  return guarded([&] {
+    if (!ctx || !idx || !ms4 || !bytes4 || reps < 1) throw InvalidArg("bad argument");
+    Ctx& c = ctx->c;
+    check_J(c, J);
+    for (int64_t j = 0; j < J; ++j)
+      if (idx[j] < 0 || idx[j] >= J) throw InvalidArg("idx out of range");
+    CK(cudaSetDevice(c.device));
+    upload(c, c.idx, idx, sizeof(int32_t) * J);
+    launch_zero_ints(c, c.flags, J);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const double Dp = (double)c.net.Dp, D = (double)c.net.D;
+    for (int kind = 0; kind < 4; ++kind) {
+      auto once = [&] {
+        switch (kind) {
+          case 0: launch_gather(c, c.theta[0], c.theta[1], c.theta[2], J, c.idx); break;
+          case 1: launch_p_sumsq(c, J); break;
+          case 2: launch_normals(c, 12345u, tag::kProposal, 7u, J, 1.0f, c.p, c.p0_part, 0); break;
+          default: launch_weights_and_resample(c, J, 0.5, 1, DASMC_SYSTEMATIC, 0, 0, 0.0); break;
+        }
+      };
+      once();  // warm-up
+      CK(cudaEventRecord(e0, c.stream));
+      for (int r = 0; r < reps; ++r) once();
+      CK(cudaEventRecord(e1, c.stream));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      ms4[kind] = ms / reps;
+    }
+    CK(cudaEventDestroy(e0));
+    CK(cudaEventDestroy(e1));
+    bytes4[0] = 8.0 * (double)J * Dp;  // read + write one row per particle
+    bytes4[1] = 4.0 * (double)J * Dp;
+    bytes4[2] = 4.0 * (double)J * D;
+    bytes4[3] = 48.0 * (double)J;      // log-weights, targets, weights, cdf (fp64), idx, flags
+  });
 }
 
 }  // extern "C"

@@ -158,6 +158,8 @@ struct Ctx {
   double* th_part = nullptr;   // [J][th_slots]
   double* p_part = nullptr;    // [J][th_slots]
   double* p0_part = nullptr;   // [J][rng_slots]
+  double* p0_sum = nullptr;    // [J] fixed-order sums of p0_part / p_part (slot_sum_kernel)
+  double* pS_sum = nullptr;
   int* flags = nullptr;        // [J]
   double* lt_old = nullptr;    // [J]
   double* lt_new = nullptr;    // [J]
@@ -259,6 +261,7 @@ void launch_ref_to_internal_f32(Ctx& c, const float* src, float* dst, int64_t J)
 void launch_internal_to_ref_f64(Ctx& c, const float* src, double* dst, int64_t J);
 void launch_internal_to_ref_f32(Ctx& c, const float* src, float* dst, int64_t J);
 void launch_zero_ints(Ctx& c, int* p, int64_t n);
+void launch_p_sumsq(Ctx& c, int64_t J);
 void launch_uniforms(Ctx& c, uint64_t key, int64_t count, double* dst);
 void launch_weights_and_resample(Ctx& c, int64_t J, double fraction, int always, int kind, int rec_slot,
                                  int k, double log_target_const);

@@ -450,9 +450,82 @@ __global__ void uniforms_kernel(uint64_t key, int64_t count, int64_t chunk, cons
   for (int64_t i = c * per; i < hi; ++i) dst[i] = x.uniform();
 }
 
+// Fixed-order per-particle sum of `slots` fp64 partials, one warp per particle: lane l
+// adds slots l, l+32, ... in order, then a fixed shuffle tree (lane 0's result).  Coalesced,
+// so the single-block weights kernel reads one value per particle instead of walking
+// every particle's slot row itself (J x 795 strided loads at C2).
+__global__ void slot_sum_kernel(const double* __restrict__ part, int slots, int64_t J, double* __restrict__ out) {
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= J) return;
+  double s = 0.0;
+  for (int i = lane; i < slots; i += 32) s += part[j * slots + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[j] = s;
+}
+
 // ---- weights / normalise / ESS / resample (smc.hpp:127-156) ---------------------------------------
 // Single 1024-thread block (J <= 65536).  Deterministic fixed-order reductions.
 constexpr int kWT = 1024;
+// Largest ensemble whose CDF is built in shared memory (128 KB of fp64).
+constexpr int64_t kCdfSmemMax = 16384;
+
+// Sequential fp64 CDF of the normalised weights with last = 1.0 (numeric.hpp:87-94),
+// then upper_bound per particle (multinomial: sorted-or-not uniforms uni[j];
+// systematic: (uni[0] + j) / J).  The running sum keeps the reference's strict
+// left-to-right order (bit-exact cdf); one thread adds while its operands come
+// from shared memory in batches, so the chain is DADD-latency bound, not a
+// dependent global load per element.  cdf (global) receives the same values.
+__device__ void cdf_and_search(int64_t J, const double* __restrict__ w, double* __restrict__ cdf,
+                               const double* __restrict__ uni, int kind, int32_t* __restrict__ idx,
+                               double* __restrict__ logw_reset, double lw_value) {
+  extern __shared__ double cdf_s[];
+  const bool sm = J <= kCdfSmemMax;
+  double* cd = sm ? cdf_s : cdf;
+  if (sm) {
+    for (int64_t j = threadIdx.x; j < J; j += kWT) cdf_s[j] = w[j];
+  } else {
+    for (int64_t j = threadIdx.x; j < J; j += kWT) cdf[j] = w[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    int64_t j = 0;
+    for (; j + 8 <= J; j += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = cd[j + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc += v[u];
+        cd[j + u] = acc;
+      }
+    }
+    for (; j < J; ++j) {
+      acc += cd[j];
+      cd[j] = acc;
+    }
+    cd[J - 1] = 1.0;
+  }
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < J; j += kWT) {
+    const double u = kind == DASMC_MULTINOMIAL ? uni[j] : (uni[0] + (double)j) / (double)J;
+    int64_t lo = 0, hi = J;  // first index with cdf > u
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (cd[mid] > u)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    idx[j] = (int32_t)lo;
+    if (sm) cdf[j] = cd[j];
+    if (logw_reset) logw_reset[j] = lw_value;  // smc.hpp:100
+  }
+}
+
+size_t cdf_smem_bytes(int64_t J) { return J <= kCdfSmemMax ? (size_t)J * sizeof(double) : 0; }
 __global__ void __launch_bounds__(kWT) weights_kernel(int64_t J, double* __restrict__ logw,
                                                       const double* __restrict__ lt_old,
                                                       const double* __restrict__ lt_new,
@@ -533,29 +606,7 @@ __global__ void __launch_bounds__(kWT) weights_kernel(int64_t J, double* __restr
     return;
   }
   // 3) sequential fp64 CDF with last = 1.0 (numeric.hpp:87-94), then upper_bound.
-  if (threadIdx.x == 0) {
-    double acc = 0.0;
-    for (int64_t j = 0; j < J; ++j) {
-      acc += w[j];
-      cdf[j] = acc;
-    }
-    cdf[J - 1] = 1.0;
-  }
-  __syncthreads();
-  const double lj = -log((double)J);
-  for (int64_t j = threadIdx.x; j < J; j += kWT) {
-    const double u = kind == DASMC_MULTINOMIAL ? uni[j] : (uni[0] + (double)j) / (double)J;
-    int64_t lo = 0, hi = J;  // first index with cdf > u
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (cdf[mid] > u)
-        hi = mid;
-      else
-        lo = mid + 1;
-    }
-    idx[j] = (int32_t)lo;
-    logw[j] = lj;  // smc.hpp:100
-  }
+  cdf_and_search(J, w, cdf, uni, kind, idx, logw, -log((double)J));
 }
 
 // Sharded ensemble, step 1: new (unnormalised) log-weights of the local slots
@@ -596,27 +647,7 @@ __global__ void __launch_bounds__(kWT) resample_hook_kernel(int64_t J, const dou
                                                             double* __restrict__ cdf,
                                                             const double* __restrict__ uni, int kind,
                                                             int32_t* __restrict__ idx) {
-  if (threadIdx.x == 0) {
-    double acc = 0.0;
-    for (int64_t j = 0; j < J; ++j) {
-      acc += w[j];
-      cdf[j] = acc;
-    }
-    cdf[J - 1] = 1.0;
-  }
-  __syncthreads();
-  for (int64_t j = threadIdx.x; j < J; j += kWT) {
-    const double u = kind == DASMC_MULTINOMIAL ? uni[j] : (uni[0] + (double)j) / (double)J;
-    int64_t lo = 0, hi = J;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (cdf[mid] > u)
-        hi = mid;
-      else
-        lo = mid + 1;
-    }
-    idx[j] = (int32_t)lo;
-  }
+  cdf_and_search(J, w, cdf, uni, kind, idx, nullptr, 0.0);
 }
 
 // dst[j] = (flags[s] ? start : end)[s], s = idx[j]  (smc.hpp:97-99 + 129-131).
@@ -650,6 +681,18 @@ __global__ void zero_ints_kernel(int* p, int64_t n) {
 
 int grid_for(int64_t total, int threads = 256) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((total + threads - 1) / threads, 148 * 32));
+}
+
+// dynamic shared memory of the weights / resampling kernels (the opt-in above 48 KB, once)
+size_t cdf_smem(int64_t J) {
+  static bool attr = false;
+  if (!attr) {
+    const int b = (int)(kCdfSmemMax * sizeof(double));
+    CK(cudaFuncSetAttribute(weights_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(resample_hook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    attr = true;
+  }
+  return cdf_smem_bytes(J);
 }
 
 }  // namespace
@@ -1256,11 +1299,20 @@ void launch_zero_ints(Ctx& c, int* p, int64_t n) {
   LAUNCHED();
 }
 
+void launch_slot_sums(Ctx& c, int64_t J, int p0_slots, int pS_slots) {
+  const unsigned blocks = (unsigned)((J * 32 + 255) / 256);
+  slot_sum_kernel<<<blocks, 256, 0, c.stream>>>(c.p0_part, p0_slots, J, c.p0_sum);
+  slot_sum_kernel<<<blocks, 256, 0, c.stream>>>(c.p_part, pS_slots, J, c.pS_sum);
+  LAUNCHED();
+  LAUNCHED();
+}
+
 void launch_weights_and_resample(Ctx& c, int64_t J, double fraction, int always, int kind, int rec_slot, int k,
                                  double) {
   const int p0_slots = c.rng_slots;
   const int pS_slots = (int)((c.net.Dp + kSqChunk - 1) / kSqChunk);
-  weights_kernel<<<1, kWT, 0, c.stream>>>(J, c.logw, c.lt_old, c.lt_new, c.p0_part, p0_slots, c.p_part, pS_slots,
+  launch_slot_sums(c, J, p0_slots, pS_slots);
+  weights_kernel<<<1, kWT, cdf_smem(J), c.stream>>>(J, c.logw, c.lt_old, c.lt_new, c.p0_sum, 1, c.pS_sum, 1,
                                           c.flags, c.wts, c.cdf, c.uni, c.idx, fraction, always, kind,
                                           c.records + (size_t)rec_slot * 8, k, 1);
   LAUNCHED();
@@ -1268,15 +1320,16 @@ void launch_weights_and_resample(Ctx& c, int64_t J, double fraction, int always,
 
 void launch_local_weights(Ctx& c, int64_t J, double* out_lw, double* out_lt) {
   const int pS_slots = (int)((c.net.Dp + kSqChunk - 1) / kSqChunk);
+  launch_slot_sums(c, J, c.rng_slots, pS_slots);
   local_weights_kernel<<<(unsigned)((J + 255) / 256), 256, 0, c.stream>>>(
-      J, c.logw, c.lt_old, c.lt_new, c.p0_part, c.rng_slots, c.p_part, pS_slots, c.flags, out_lw, out_lt);
+      J, c.logw, c.lt_old, c.lt_new, c.p0_sum, 1, c.pS_sum, 1, c.flags, out_lw, out_lt);
   LAUNCHED();
 }
 
 void launch_normalize_resample(Ctx& c, int64_t Jtot, double* lw_full, const double* lt_full, double* w, double* cdf,
                                const double* uni, int32_t* idx, double fraction, int always, int kind, int rec_slot,
                                int k) {
-  weights_kernel<<<1, kWT, 0, c.stream>>>(Jtot, lw_full, nullptr, lt_full, nullptr, 0, nullptr, 0, nullptr, w, cdf,
+  weights_kernel<<<1, kWT, cdf_smem(Jtot), c.stream>>>(Jtot, lw_full, nullptr, lt_full, nullptr, 0, nullptr, 0, nullptr, w, cdf,
                                           uni, idx, fraction, always, kind, c.records + (size_t)rec_slot * 8, k, 0);
   LAUNCHED();
 }
@@ -1367,7 +1420,7 @@ void launch_gather_parts(Ctx& c, int64_t J) {
 }
 
 void launch_resample_hook(Ctx& c, const double* w, const double* u, int64_t J, int kind, int32_t* idx) {
-  resample_hook_kernel<<<1, kWT, 0, c.stream>>>(J, w, c.cdf, u, kind, idx);
+  resample_hook_kernel<<<1, kWT, cdf_smem(J), c.stream>>>(J, w, c.cdf, u, kind, idx);
   LAUNCHED();
 }
 

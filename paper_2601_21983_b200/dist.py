@@ -157,16 +157,28 @@ def sharded_step(engine, comm, J: int, cfg: KernelConfig, seed: int, kind: str =
     if rec.resampled:
         idx_h = idx.cpu().numpy() if hasattr(idx, "cpu") else np.asarray(idx)
         recv_src, recv_row, send_cnt, send_rows = shard_plan(idx_h, world, rank)
+        # each distinct source row crosses the fabric once per destination rank: both
+        # sides derive the same sorted unique row list from the (identical) plan, and
+        # the receiver fans the rows out to its slots on the device.  Resampling
+        # duplicates survivors, so after a weight collapse this is 1 row, not J/G
         sends, off = [], 0
         for d in range(world):
             n = int(send_cnt[d])
-            sends.append(engine.pack(send_rows[off:off + n], device))
+            sends.append(engine.pack(np.unique(send_rows[off:off + n]).astype(np.int32), device))
             off += n
-        recv_counts = [int((recv_src == s).sum()) for s in range(world)]
+        uniq, inv = [], np.empty(len(recv_src), dtype=np.int64)
+        base = 0
+        for s in range(world):
+            sl = np.nonzero(recv_src == s)[0]
+            u, iv = np.unique(recv_row[sl], return_inverse=True)
+            uniq.append(u)
+            inv[sl] = base + iv
+            base += len(u)
+        recv_counts = [len(u) for u in uniq]
         recvs = comm.exchange(sends, recv_counts, engine.row, getattr(engine, "dtype", None))
-        slots = np.concatenate([np.nonzero(recv_src == s)[0] for s in range(world)]).astype(np.int32)
         src = torch.cat([r for r in recvs if r.shape[0]], dim=0)
-        engine.unpack(src, slots)
+        src = src.index_select(0, torch.as_tensor(inv, device=src.device))
+        engine.unpack(src, np.arange(len(recv_src), dtype=np.int32))
         out["migrated_rows"] = int(sum(recv_counts) - recv_counts[rank])
     return out
 
