@@ -197,7 +197,9 @@ class SamplerError(DasmcError):
 def check(rc: int) -> None:
     if rc == DASMC_OK:
         return
-    msg = load().dasmc_last_error().decode()
+    # the message of whichever loaded build failed (A/B tools load a second build)
+    msgs = [lib.dasmc_last_error().decode() for lib in [load(), *_alt.values()]]
+    msg = next((m for m in msgs if m), "")
     if rc == DASMC_EDEAD:
         raise SamplerError(rc, msg)
     if rc == DASMC_EINVAL:

@@ -56,35 +56,43 @@ def main():
                     lib_path = os.path.abspath(v)
                 else:
                     os.environ[k] = v
-            t = p.GpuEnsembleTarget(spec, X, y, J, device=0, precision=prec, lib_path=lib_path)
-            lib = t.lib
-            L.check(lib.dasmc_gpu_reserve_rows(t.h, M))
-            t.set_target(0, M, N, "scaled", 1.0, 1.0)
-            L.check(lib.dasmc_gpu_init_ensemble_at(t.h, J, 0, 0))
-            for _ in range(2):
-                t.smc_step(kc, 0, "systematic", 0.5)
-            t.sync_records(0)
-            stream = torch.cuda.ExternalStream(lib.dasmc_gpu_stream(t.h))
-            torch.cuda.synchronize()
-            L.check(lib.dasmc_gpu_set_timing(t.h, 1))
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(args.steps):
-                t.smc_step(kc, 0, "systematic", 0.5)
-            e1.record(stream)
-            e1.synchronize()
-            kms = np.zeros(3)
-            kcnt = np.zeros(3, dtype=np.int64)
-            L.check(lib.dasmc_gpu_kernel_times(t.h, kms.ctypes.data_as(L._D), kcnt.ctypes.data_as(L._I64)))
-            L.check(lib.dasmc_gpu_set_timing(t.h, 0))
-            t.sync_records(0)
-            res[s].append((kms[0] / max(kcnt[0], 1), kms[1] / max(kcnt[1], 1), e0.elapsed_time(e1) / args.steps))
-            t.close()
-            del t
-            torch.cuda.synchronize()
+            t = None
+            try:
+                t = p.GpuEnsembleTarget(spec, X, y, J, device=0, precision=prec, lib_path=lib_path)
+                lib = t.lib
+                L.check(lib.dasmc_gpu_reserve_rows(t.h, M))
+                t.set_target(0, M, N, "scaled", 1.0, 1.0)
+                L.check(lib.dasmc_gpu_init_ensemble_at(t.h, J, 0, 0))
+                for _ in range(2):
+                    t.smc_step(kc, 0, "systematic", 0.5)
+                t.sync_records(0)
+                stream = torch.cuda.ExternalStream(lib.dasmc_gpu_stream(t.h))
+                torch.cuda.synchronize()
+                L.check(lib.dasmc_gpu_set_timing(t.h, 1))
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(args.steps):
+                    t.smc_step(kc, 0, "systematic", 0.5)
+                e1.record(stream)
+                e1.synchronize()
+                kms = np.zeros(3)
+                kcnt = np.zeros(3, dtype=np.int64)
+                L.check(lib.dasmc_gpu_kernel_times(t.h, kms.ctypes.data_as(L._D), kcnt.ctypes.data_as(L._I64)))
+                L.check(lib.dasmc_gpu_set_timing(t.h, 0))
+                t.sync_records(0)
+                res[s].append((kms[0] / max(kcnt[0], 1), kms[1] / max(kcnt[1], 1), e0.elapsed_time(e1) / args.steps))
+                t.close()
+                del t
+                torch.cuda.synchronize()
+            except Exception as e:  # a variant that cannot run: report and go on
+                print(f"{s}: FAILED {e}", flush=True)
+                if t is not None:
+                    t.close()
     os.environ.clear()
     os.environ.update(base_env)
     for s, v in res.items():
+        if not v:
+            continue
         f = statistics.median(x[0] for x in v)
         d = statistics.median(x[1] for x in v)
         st = statistics.median(x[2] for x in v)
