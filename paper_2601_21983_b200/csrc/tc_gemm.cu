@@ -323,6 +323,40 @@ __device__ __forceinline__ void tmem_wait16(float* v) {
                  "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]), "+f"(v[14]),
                  "+f"(v[15])::"memory");
 }
+__device__ __forceinline__ void tmem_ld8_async(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait8(float* v) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7])::"memory");
+}
+template <int W>
+__device__ __forceinline__ void tmem_ldw_async(uint32_t taddr, float* v) {
+  if constexpr (W == 8)
+    tmem_ld8_async(taddr, v);
+  else
+    tmem_ld16_async(taddr, v);
+}
+template <int W>
+__device__ __forceinline__ void tmem_waitw(float* v) {
+  if constexpr (W == 8)
+    tmem_wait8(v);
+  else
+    tmem_wait16(v);
+}
+// forward epilogue: accumulator columns per TMEM load (8 or 16) and how many columns
+// ahead of their FFMA2s the W2^T rows are loaded from shared memory
+#ifndef DASMC_CW
+#define DASMC_CW 0  // 0: per precision mode (see the forward epilogue)
+#endif
+#ifndef DASMC_W2_AHEAD
+#define DASMC_W2_AHEAD 0
+#endif
 // Epilogue activation stores (a1^T, delta1^T: streamed once, re-read by the
 // weight-gradient GEMMs after ~25 GB of other traffic)
 #ifndef DASMC_ST_POLICY
@@ -778,7 +812,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool valid = m < fp.M;
         const bool st_rows = fp.need_grad && dbg != 1 && dbg != 5;  // 5: no a1^T stores
         int c_lo, c_hi;
-        chunk_range((n1 + 15) >> 4, c_lo, c_hi);
+        // 16-column TMEM loads, except in the fp16 mode whose (epilogue-bound) forward
+        // runs 9 % faster with 8 (B200 in-process A/B; tf32 / tf32h 4 % slower with 8)
+        constexpr int CW = DASMC_CW > 0 ? DASMC_CW : (PREC == 1 ? 8 : 16);
+        chunk_range((n1 + CW - 1) / CW, c_lo, c_hi);
         if (dbg == 3) c_hi = c_lo;
         // transposed buffers are row-blocked [J][nblk][rows][128]: a tile's rows are one
         // contiguous region; consecutive rows of a block are 128 floats apart
@@ -805,17 +842,38 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (CP % 4) w[CP / 2 - 1] = *reinterpret_cast<const float2*>(p + 4 * (CP / 4));
         };
+        // the CW columns of a chunk, each W2^T row loaded DASMC_W2_AHEAD columns before its
+        // FFMA2s (0: loaded at the column, scheduled by ptxas)
+        auto w2_pipeline = [&](int o0, int nq, auto&& body) {
+          if constexpr (DASMC_W2_AHEAD == 0) {
+#pragma unroll
+            for (int q = 0; q < CW; ++q)
+              if (q < nq) {
+                float2 w[CP / 2];
+                w2row2(o0 + q, w);
+                body(q, w);
+              }
+          } else {  // one column ahead: the next row is in flight while this one is used
+            float2 wc[CP / 2], wn[CP / 2];
+            w2row2(o0, wc);
+#pragma unroll
+            for (int q = 0; q < CW; ++q) {
+              if (q + 1 < nq) w2row2(o0 + q + 1, wn);
+              if (q < nq) body(q, wc);
+#pragma unroll
+              for (int c = 0; c < CP / 2; ++c) wc[c] = wn[c];
+            }
+          }
+        };
         auto act = [](float z) { return ACT == DASMC_RELU ? fmaxf(z, 0.f) : tanhf(z); };
         // pass 1: a1 = act(z1); partial z2 = W2 a1 over this warp's columns
         auto chunk1 = [&](auto store, int ch, const float* v) {
-          const int o0 = ch * 16;
-          const int nq = min(16, n1 - o0);  // warp-uniform
+          const int o0 = ch * CW;
+          const int nq = min(CW, n1 - o0);  // warp-uniform
           TS* pa = a1T + (int64_t)o0 * kRow;
           float* pal = SPLIT ? a1Tlo + (int64_t)o0 * kRow : nullptr;
-          auto one = [&](int q) {
+          auto one = [&](int q, const float2* w) {
             const float a = act(v[q]);
-            float2 w[CP / 2];
-            w2row2(o0 + q, w);
             const float2 aa = make_float2(a, a);
 #pragma unroll
             for (int c = 0; c < CP / 2; ++c) z2p[c] = __ffma2_rn(aa, w[c], z2p[c]);
@@ -825,29 +883,25 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (SPLIT) st_act(pal + q * kRow, a - (float)hi, st_pol);
             }
           };
-          if (nq == 16) {
-#pragma unroll
-            for (int q = 0; q < 16; ++q) one(q);
-          } else {  // tail chunk: still unrolled so v[] stays in registers
-#pragma unroll
-            for (int q = 0; q < 16; ++q)
-              if (q < nq) one(q);
-          }
+          if (nq == CW)
+            w2_pipeline(o0, CW, one);
+          else  // tail chunk: still unrolled so v[] stays in registers
+            w2_pipeline(o0, nq, one);
         };
         // TMEM loads double-buffered: chunk ch+1 is in flight while ch is processed
         auto run_chunks = [&](auto body) {
-          float va[16] = {}, vb[16] = {};
+          float va[CW] = {}, vb[CW] = {};
           int ch = c_lo;
-          if (ch < c_hi) tmem_ld16_async(taddr + ch * 16, va);
-          tmem_wait16(va);
+          if (ch < c_hi) tmem_ldw_async<CW>(taddr + ch * CW, va);
+          tmem_waitw<CW>(va);
           while (ch < c_hi) {
-            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, vb);
+            if (ch + 1 < c_hi) tmem_ldw_async<CW>(taddr + (ch + 1) * CW, vb);
             body(ch, va);
-            tmem_wait16(vb);
+            tmem_waitw<CW>(vb);
             if (++ch >= c_hi) break;
-            if (ch + 1 < c_hi) tmem_ld16_async(taddr + (ch + 1) * 16, va);
+            if (ch + 1 < c_hi) tmem_ldw_async<CW>(taddr + (ch + 1) * CW, va);
             body(ch, vb);
-            tmem_wait16(va);
+            tmem_waitw<CW>(va);
             ++ch;
           }
         };
@@ -933,13 +987,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int c = 0; c < CP / 2; ++c) d2p[c] = make_float2(d2[2 * c], d2[2 * c + 1]);
           auto chunk2 = [&](int ch, const float* v) {
-            const int o0 = ch * 16;
-            const int nq = min(16, n1 - o0);  // warp-uniform
+            const int o0 = ch * CW;
+            const int nq = min(CW, n1 - o0);  // warp-uniform
             TS* pd = d1T + (int64_t)o0 * kRow;
             float* pdl = SPLIT ? d1Tlo + (int64_t)o0 * kRow : nullptr;
-            auto one = [&](int q) {
-              float2 w[CP / 2];
-              w2row2(o0 + q, w);
+            auto one = [&](int q, const float2* w) {
 #ifndef DASMC_V_ACC2
               float2 acc = make_float2(0.f, 0.f);  // even / odd classes: two chains in one FFMA2
 #pragma unroll
@@ -966,14 +1018,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (dbg != 6) pd[q * kRow] = hi;
               if (SPLIT) st_act(pdl + q * kRow, d1 - (float)hi, st_pol);
             };
-            if (nq == 16) {
-#pragma unroll
-              for (int q = 0; q < 16; ++q) one(q);
-            } else {
-#pragma unroll
-              for (int q = 0; q < 16; ++q)
-                if (q < nq) one(q);
-            }
+            if (nq == CW)
+              w2_pipeline(o0, CW, one);
+            else
+              w2_pipeline(o0, nq, one);
           };
           run_chunks(chunk2);
         }
