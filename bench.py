@@ -334,8 +334,15 @@ def run_ours(args, w):
         # the kernel is timed inside a long step: the sustained bf16 figure applies
         bf16 = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops", 1590.0)
         kind = "sustained" if peaks.get("bf16_tflops_sustained") else "burst"
-        peak = bf16 / 2.0
-        peak_src = f"dense tf32 = measured bf16 {kind} {bf16} TFLOP/s / 2 (MEASURED_PEAKS.json)"
+        # dense rate of the MMAs this kernel issues per algorithmic MAC: kind::tf32 runs at half
+        # the f16/bf16 rate; split modes issue 2 (f16x2 forward) or 3 (3xtf32) MMAs per MAC
+        fwd = name.startswith("layer-1 forward")
+        div, what = {"tf32": (2.0, "tf32"), "3xtf32": (6.0, "3xtf32 (3 tf32 MMAs per MAC)"),
+                     "f16": (1.0, "f16"),
+                     "f16x2": (2.0 if fwd else 1.0, "f16x2 (2 f16 MMAs per MAC)" if fwd else "f16"),
+                     "tf32h": (2.0 if fwd else 1.0, "tf32" if fwd else "f16")}[args.precision]
+        peak = bf16 / div
+        peak_src = f"dense {what} = measured bf16 {kind} {bf16} TFLOP/s / {div:g} (MEASURED_PEAKS.json)"
     achieved = fl / (kt_ms / 1e3) / 1e12 if kt_ms > 0 else None
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
