@@ -93,9 +93,10 @@ def test_momentum_streams(product, oracle):
 
 def test_resample_indices_bit_exact(product, oracle):
     spec, X, y = make_problem(product, [4, 2], "relu", 10)
-    t = product.GpuEnsembleTarget(spec, X, y, 4096)
+    t = product.GpuEnsembleTarget(spec, X, y, 20000)
     rng = np.random.default_rng(4)
-    for J in (2, 3, 100, 1024, 4096):
+    # 16384: the largest CDF built in shared memory; 20000: the global-memory CDF path
+    for J in (2, 3, 100, 1024, 4096, 16384, 20000):
         for trial in range(3):
             w = rng.random(J) ** 8
             if trial == 1:
@@ -305,3 +306,29 @@ def test_start_gradient_cache_is_exact(product, prec):
     assert np.array_equal(runs[False][0], runs[True][0]) and np.array_equal(runs[False][1], runs[True][1])
     for a, b in zip(runs[False][2], runs[True][2]):
         assert a["ess"] == b["ess"] and a["mean_log_target"] == b["mean_log_target"]
+
+
+def test_bench_memory_hook(product):
+    """dasmc_gpu_bench_memory (tools/membench.py): runs every memory-bound kernel of the
+    step on the context's buffers and reports positive times and the algorithmic bytes."""
+    import ctypes as C
+    from paper_2601_21983_b200 import _lib as L
+    spec, X, y = make_problem(product, [30, 20, 5], "relu", 64)
+    J = 300
+    t = product.GpuEnsembleTarget(spec, X, y, J)
+    t.init_ensemble(J, 1)
+    idx = np.random.default_rng(0).integers(0, J, J).astype(np.int32)
+    ms, by = np.zeros(4), np.zeros(4)
+    L.check(t.lib.dasmc_gpu_bench_memory(t.h, J, idx.ctypes.data_as(C.POINTER(C.c_int32)), 2,
+                                         ms.ctypes.data_as(C.POINTER(C.c_double)),
+                                         by.ctypes.data_as(C.POINTER(C.c_double))))
+    assert np.all(ms > 0) and np.all(np.isfinite(ms)), ms
+    D = product.param_count(spec)
+    assert by[2] == 4.0 * J * D and by[0] >= 8.0 * J * D
+    bad = idx.copy()
+    bad[0] = J
+    with pytest.raises(ValueError):
+        L.check(t.lib.dasmc_gpu_bench_memory(t.h, J, bad.ctypes.data_as(C.POINTER(C.c_int32)), 1,
+                                             ms.ctypes.data_as(C.POINTER(C.c_double)),
+                                             by.ctypes.data_as(C.POINTER(C.c_double))))
+    t.close()
