@@ -152,6 +152,12 @@ void free_ctx(Ctx& c) {
   }
   if (c.h_records) cudaFreeHost(c.h_records);
   if (c.h_stage) cudaFreeHost(c.h_stage);
+  if (c.copy) {
+    cudaStreamSynchronize(c.copy);
+    cudaStreamDestroy(c.copy);
+    for (cudaEvent_t e : c.xfer_ev)
+      if (e) cudaEventDestroy(e);
+  }
   if (c.ev0) cudaEventDestroy(c.ev0);
   if (c.ev1) cudaEventDestroy(c.ev1);
   if (c.stream) cudaStreamDestroy(c.stream);
@@ -675,6 +681,24 @@ int dasmc_gpu_set_ensemble(dasmc_ctx* ctx, const double* theta, const double* lo
   });
 }
 
+}  // extern "C"
+
+namespace {
+constexpr int kXferChunks = 8;
+void ensure_copy_stream(Ctx& c) {
+  if (c.copy) return;
+  CK(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : c.xfer_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+// particle chunk ch of kXferChunks: [j0, j1)
+void xfer_chunk(int64_t J, int ch, int64_t& j0, int64_t& j1) {
+  j0 = J * ch / kXferChunks;
+  j1 = J * (ch + 1) / kXferChunks;
+}
+}  // namespace
+
+extern "C" {
+
 int dasmc_gpu_set_ensemble_f32(dasmc_ctx* ctx, const float* theta, const double* log_weights, int64_t J,
                                int iteration) {
   return guarded([&] {
@@ -684,8 +708,22 @@ int dasmc_gpu_set_ensemble_f32(dasmc_ctx* ctx, const float* theta, const double*
     if (J < 2) throw InvalidArg("ensemble needs at least 2 particles");
     CK(cudaSetDevice(c.device));
     ensure_stage(c, sizeof(float) * (size_t)J * c.net.D);
-    CK(cudaMemcpyAsync(c.stage, theta, sizeof(float) * (size_t)J * c.net.D, cudaMemcpyHostToDevice, c.stream));
-    launch_ref_to_internal_f32(c, (const float*)c.stage, c.theta[c.start], J);
+    ensure_copy_stream(c);
+    // the copy stream starts after everything already queued on the context's stream
+    CK(cudaEventRecord(c.xfer_ev[kXferChunks], c.stream));
+    CK(cudaStreamWaitEvent(c.copy, c.xfer_ev[kXferChunks], 0));
+    const int64_t D = c.net.D;
+    float* stage = (float*)c.stage;
+    for (int ch = 0; ch < kXferChunks; ++ch) {  // H2D of chunk ch+1 overlaps the conversion of ch
+      int64_t j0, j1;
+      xfer_chunk(J, ch, j0, j1);
+      if (j1 == j0) continue;
+      CK(cudaMemcpyAsync(stage + j0 * D, theta + j0 * D, sizeof(float) * (size_t)(j1 - j0) * D,
+                         cudaMemcpyHostToDevice, c.copy));
+      CK(cudaEventRecord(c.xfer_ev[ch], c.copy));
+      CK(cudaStreamWaitEvent(c.stream, c.xfer_ev[ch], 0));
+      launch_ref_to_internal_f32(c, stage + j0 * D, c.theta[c.start] + j0 * c.net.Dp, j1 - j0);
+    }
     CK(cudaMemcpyAsync(c.logw, log_weights, sizeof(double) * J, cudaMemcpyHostToDevice, c.stream));
     CK(cudaStreamSynchronize(c.stream));
     c.J = J;
@@ -721,11 +759,23 @@ int dasmc_gpu_get_ensemble_f32(dasmc_ctx* ctx, float* theta, double* log_weights
     CK(cudaSetDevice(c.device));
     if (theta) {
       ensure_stage(c, sizeof(float) * (size_t)c.J * c.net.D);
-      launch_internal_to_ref_f32(c, c.theta[c.start], (float*)c.stage, c.J);
-      CK(cudaMemcpyAsync(theta, c.stage, sizeof(float) * (size_t)c.J * c.net.D, cudaMemcpyDeviceToHost, c.stream));
+      ensure_copy_stream(c);
+      const int64_t D = c.net.D;
+      float* stage = (float*)c.stage;
+      for (int ch = 0; ch < kXferChunks; ++ch) {  // D2H of chunk ch overlaps the conversion of ch+1
+        int64_t j0, j1;
+        xfer_chunk(c.J, ch, j0, j1);
+        if (j1 == j0) continue;
+        launch_internal_to_ref_f32(c, c.theta[c.start] + j0 * c.net.Dp, stage + j0 * D, j1 - j0);
+        CK(cudaEventRecord(c.xfer_ev[ch], c.stream));
+        CK(cudaStreamWaitEvent(c.copy, c.xfer_ev[ch], 0));
+        CK(cudaMemcpyAsync(theta + j0 * D, stage + j0 * D, sizeof(float) * (size_t)(j1 - j0) * D,
+                           cudaMemcpyDeviceToHost, c.copy));
+      }
     }
     if (log_weights) CK(cudaMemcpyAsync(log_weights, c.logw, sizeof(double) * c.J, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
+    if (c.copy) CK(cudaStreamSynchronize(c.copy));
     if (iteration) *iteration = c.iteration;
   });
 }

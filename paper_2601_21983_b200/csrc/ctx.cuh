@@ -206,6 +206,10 @@ struct Ctx {
 
   // events for sampler_ms
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // host <-> device ensemble transfers: DMA on `copy` in kXferChunks particle chunks,
+  // overlapped with the layout conversion of the neighbouring chunk on `stream`
+  cudaStream_t copy = nullptr;
+  cudaEvent_t xfer_ev[9] = {};  // one per chunk + the start of a transfer
 
   // sharded-ensemble scratch (full-J vectors + row lists)
   double* sh_buf = nullptr;  // [5][sh_cap]: log_w, log_target_new, w, cdf, uniforms
