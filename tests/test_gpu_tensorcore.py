@@ -146,3 +146,32 @@ def test_tc_deep_mlp(product, oracle, layers, act, M, J):
             nr = float(np.linalg.norm(g[j] - go[j]) / np.linalg.norm(go[j]))
             ab = float(np.max(np.abs(g[j] - go[j])) / np.max(np.abs(go[j])))
             assert nr < tn and ab < 5 * tn / 6, (mode, j, ab, nr)
+
+
+def test_c2_full_size_step(product):
+    """BASELINE.json configs[1] at its largest window: J = 1024 particles, M = n = 60000 rows
+    (the last iterations of the 300-iteration schedule), tf32h.  Size-independent
+    properties: the step runs in the 180 GB of HBM, is bit-reproducible from the same
+    ensemble and seed, ESS lies in [1, J], and every position is finite (divergent
+    particles keep theta, kernels.hpp:138-145)."""
+    layers, J, n = [784, 200, 10], 1024, 60000
+    spec = product.NetSpec(layers, "relu")
+    X, y = product.make_teacher_data(spec, n, 1, 0, 2, threads=8)
+    t = product.GpuEnsembleTarget(spec, X, y, J, precision="tf32h")
+    t.set_target(0, n, n, "scaled", 1.0, 1.0)
+    t.init_ensemble(J, 5)
+    th0, lw0, it0 = t.get_ensemble(J, dtype=np.float32)
+    kc = product.KernelConfig.hmc(0.002, 3)
+    outs = []
+    for _ in range(2):
+        t.set_ensemble(th0, lw0, it0)
+        rec = t.smc_step(kc, 11, "systematic", 0.5)
+        th, lw, _ = t.get_ensemble(J, dtype=np.float32)
+        outs.append((rec, th, lw))
+    t.close()
+    (r1, th1, lw1), (r2, th2, lw2) = outs
+    assert r1["ess"] == r2["ess"] and np.array_equal(th1, th2) and np.array_equal(lw1, lw2)
+    assert 1.0 - 1e-9 <= r1["ess"] <= J + 1e-9
+    assert np.all(np.isfinite(th1)) and r1["n_divergent"] < J
+    # divergent particles carry -inf log-weights unless the step resampled
+    assert np.all(np.isfinite(lw1)) if r1["resampled"] else np.isfinite(lw1).any()
