@@ -1289,6 +1289,7 @@ __global__ void __launch_bounds__(128) head_kernel(
     int need_grad, double* __restrict__ ll_part, int ll_slots, float* __restrict__ dLT, float* __restrict__ dT,
     float* __restrict__ dRow, float* __restrict__ dRowLo, int64_t ldd, int64_t Mcap) {
   extern __shared__ float hs[];
+  __shared__ float stg[4][32][9];    // per-warp staging of the row-major delta stores
   float* Ws = hs;                    // [n_in][CP] = W_L transposed
   float* bs = Ws + (size_t)n_in * CP;  // [CP]
   __shared__ double red[8];
@@ -1357,7 +1358,7 @@ __global__ void __launch_bounds__(128) head_kernel(
     float* lt = dLT + (j * nblk + rt) * (int64_t)C * 128 + r;
     for (int c = 0; c < C; ++c) lt[(int64_t)c * 128] = tf32_hi(d[c]);
     float* dt = dT + (j * nblk + rt) * (int64_t)n_in * 128 + r;
-    float* dr = dRow ? dRow + (j * Mcap + m) * ldd : nullptr;
+    const bool dr = dRow != nullptr;
     float* drl = dRowLo ? dRowLo + (j * Mcap + m) * ldd : nullptr;
     for (int o0 = 0; o0 < n_in; o0 += 8) {
       float av[8], g[8];
@@ -1382,9 +1383,23 @@ __global__ void __launch_bounds__(128) head_kernel(
         if (q < nq) {
           const float h = tf32_hi(g[q]);
           dt[(int64_t)(o0 + q) * 128] = h;
-          if (dr) dr[o0 + q] = h;
+          stg[r >> 5][r & 31][q] = h;
           if (drl) drl[o0 + q] = g[q] - h;
         }
+      if (dr) {
+        // row-major delta (the next backward-delta GEMM's A operand): the warp's 32 rows x 8
+        // columns go out through shared memory as 32-byte row segments, 4 rows per store
+        // instruction, instead of one 4-byte store per row and column
+        __syncwarp();
+        const int lane = r & 31;
+        float* drw = dRow + (j * Mcap + (int64_t)rt * 128 + (r & ~31)) * ldd + o0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row = i * 4 + (lane >> 3), col = lane & 7;
+          if (col < nq) drw[(int64_t)row * ldd + col] = stg[r >> 5][row][col];
+        }
+        __syncwarp();
+      }
     }
   }
   // per-tile prefix / block partials in a fixed order
