@@ -29,12 +29,13 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--precision", default="tf32")
+    ap.add_argument("--config", default="c2", help="bench.py workload (MLP configs)")
     args = ap.parse_args()
     import torch
     import paper_2601_21983_b200 as p
     from paper_2601_21983_b200 import _lib as L
 
-    w = bench.WORKLOADS["c2"]
+    w = bench.WORKLOADS[args.config]
     lib = p.load()
     spec, X, y = bench.make_data(w)
     J, S, N = w["J"], w["S"], w["n"]
