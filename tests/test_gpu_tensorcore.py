@@ -60,7 +60,7 @@ def test_tc_value_and_grad(product, oracle, layers, act, M, prec):
             assert nr < tn and mr < tm, (j, mr, nr)
 
 
-@pytest.mark.parametrize("prec", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("prec", ["3xtf32", "tf32", "tf32h", "f16x2", "f16"])
 def test_tc_loglik_parts_and_step(product, oracle, prec):
     layers, act = [64, 32, 10], "tanh"
     spec, X, y = problem(product, layers, act, 2000)
