@@ -823,36 +823,44 @@ __global__ void pool_bwd_kernel(ConvDev d, int act, const float* __restrict__ A,
 // to part[j][chunk][param]; pass 2 (conv_dw_reduce_kernel) adds the chunks in order and
 // applies the fused leapfrog.
 constexpr int kImgChunk = 16;
+#ifndef DASMC_CONV_DW_CI
+#define DASMC_CONV_DW_CI 4
+#endif
 // Weight gradient of one stage for one input channel ci and CT output channels, over a
 // chunk of kImgChunk images: dW[co][ci][ky][kx] = sum_m,y,x dz[co][y][x] in[ci][y+ky][x+kx]
 // (+ the bias sums).  Thread (g, c): output channel co0 + c, rows y = g, g+G, ...; it keeps
 // the full K x K patch in registers and slides a K-wide input window along each of the K
 // rows, so one dz load feeds K*K FMAs.  Per row the float partials go into fp64 totals;
 // the G row groups are combined in a fixed order (deterministic).
-template <int K, int CT>
+template <int K, int CT, int CI>
 __global__ void __launch_bounds__(128) conv_dw_kernel(ConvDev d, const float* __restrict__ dZ, int64_t z_ps,
                                                        const float* __restrict__ in, int64_t in_ps, int64_t M,
                                                        int64_t np, int nchunks, double* __restrict__ part) {
   constexpr int G = 128 / CT;
   extern __shared__ float4 cv_sh4[];
-  float* in_s = reinterpret_cast<float*>(cv_sh4);           // [hin * win]
-  const int npix = d.ho * d.wo, nplane = d.hin * d.win;
+  float* in_s = reinterpret_cast<float*>(cv_sh4);           // [CI][pl]
+  const int npix = d.ho * d.wo, nplane = d.hin * d.win, pl = (nplane + 3) & ~3;
   const int zs = npix | 1;                                   // odd plane stride: conflict-free dz reads
-  float* dz_s = in_s + ((nplane + 3) & ~3);                  // [CT][zs]
-  const int ci = blockIdx.x, co0 = blockIdx.y * CT;
+  float* dz_s = in_s + CI * pl;                              // [CT][zs]
+  const int ci0 = blockIdx.x * CI, co0 = blockIdx.y * CT;
   const int64_t j = blockIdx.z / nchunks;
   const int chunk = blockIdx.z - (int)j * nchunks;
   const int t = threadIdx.x, c = t % CT, g = t / CT;
-  double tot[K * K];
+  double tot[CI][K * K];
   double totb = 0.0;
 #pragma unroll
-  for (int q = 0; q < K * K; ++q) tot[q] = 0.0;
+  for (int i = 0; i < CI; ++i)
+#pragma unroll
+    for (int q = 0; q < K * K; ++q) tot[i][q] = 0.0;
   const int64_t in_img = (int64_t)d.cin * nplane, per = (int64_t)d.cout * npix;
   const int64_t m0 = (int64_t)chunk * kImgChunk, m1 = min(M, m0 + kImgChunk);
   for (int64_t m = m0; m < m1; ++m) {
     __syncthreads();
-    const float* src = in + j * in_ps + m * in_img + (int64_t)ci * nplane;
-    for (int u = t; u < nplane; u += blockDim.x) in_s[u] = src[u];
+    const float* src = in + j * in_ps + m * in_img + (int64_t)ci0 * nplane;
+    for (int u = t; u < CI * nplane; u += blockDim.x) {
+      const int cc = u / nplane;
+      in_s[cc * pl + (u - cc * nplane)] = ci0 + cc < d.cin ? src[u] : 0.f;
+    }
     const float* zsrc = dZ + j * z_ps + m * per + (int64_t)co0 * npix;
     for (int u = t; u < CT * npix; u += blockDim.x) {
       const int cc = u / npix;
@@ -861,40 +869,52 @@ __global__ void __launch_bounds__(128) conv_dw_kernel(ConvDev d, const float* __
     __syncthreads();
     for (int y = g; y < d.ho; y += G) {
       const float* zr = dz_s + c * zs + y * d.wo;
-      float w[K][K], acc[K * K];
+      float w[CI][K][K], acc[CI][K * K];
 #pragma unroll
-      for (int ky = 0; ky < K; ++ky)
+      for (int i = 0; i < CI; ++i)
 #pragma unroll
-        for (int q = 0; q < K; ++q) w[ky][q] = in_s[(y + ky) * d.win + q];
+        for (int ky = 0; ky < K; ++ky)
 #pragma unroll
-      for (int q = 0; q < K * K; ++q) acc[q] = 0.f;
+          for (int q = 0; q < K; ++q) w[i][ky][q] = in_s[i * pl + (y + ky) * d.win + q];
+#pragma unroll
+      for (int i = 0; i < CI; ++i)
+#pragma unroll
+        for (int q = 0; q < K * K; ++q) acc[i][q] = 0.f;
       float ab = 0.f;
       for (int x = 0; x < d.wo; ++x) {
         const float z = zr[x];
 #pragma unroll
-        for (int ky = 0; ky < K; ++ky)
+        for (int i = 0; i < CI; ++i)
 #pragma unroll
-          for (int kx = 0; kx < K; ++kx) acc[ky * K + kx] = fmaf(z, w[ky][kx], acc[ky * K + kx]);
+          for (int ky = 0; ky < K; ++ky)
+#pragma unroll
+            for (int kx = 0; kx < K; ++kx) acc[i][ky * K + kx] = fmaf(z, w[i][ky][kx], acc[i][ky * K + kx]);
         ab += z;
 #pragma unroll
-        for (int ky = 0; ky < K; ++ky) {
+        for (int i = 0; i < CI; ++i)
 #pragma unroll
-          for (int q = 0; q + 1 < K; ++q) w[ky][q] = w[ky][q + 1];
-          w[ky][K - 1] = x + K < d.win ? in_s[(y + ky) * d.win + x + K] : 0.f;
-        }
+          for (int ky = 0; ky < K; ++ky) {
+#pragma unroll
+            for (int q = 0; q + 1 < K; ++q) w[i][ky][q] = w[i][ky][q + 1];
+            w[i][ky][K - 1] = x + K < d.win ? in_s[i * pl + (y + ky) * d.win + x + K] : 0.f;
+          }
       }
 #pragma unroll
-      for (int q = 0; q < K * K; ++q) tot[q] += (double)acc[q];
+      for (int i = 0; i < CI; ++i)
+#pragma unroll
+        for (int q = 0; q < K * K; ++q) tot[i][q] += (double)acc[i][q];
       totb += (double)ab;
     }
   }
   // combine the G row groups in order g = 0 .. G-1 (reusing the staging buffers)
   __syncthreads();
-  double* red = reinterpret_cast<double*>(cv_sh4);  // [G][CT][K*K + 1]
-  constexpr int R = K * K + 1;
+  double* red = reinterpret_cast<double*>(cv_sh4);  // [G][CT][CI*K*K + 1]
+  constexpr int R = CI * K * K + 1;
 #pragma unroll
-  for (int q = 0; q < K * K; ++q) red[((size_t)g * CT + c) * R + q] = tot[q];
-  red[((size_t)g * CT + c) * R + K * K] = totb;
+  for (int i = 0; i < CI; ++i)
+#pragma unroll
+    for (int q = 0; q < K * K; ++q) red[((size_t)g * CT + c) * R + i * K * K + q] = tot[i][q];
+  red[((size_t)g * CT + c) * R + CI * K * K] = totb;
   __syncthreads();
   double* o = part + ((int64_t)j * nchunks + chunk) * np;
   for (int e = t; e < CT * R; e += blockDim.x) {
@@ -902,10 +922,12 @@ __global__ void __launch_bounds__(128) conv_dw_kernel(ConvDev d, const float* __
     if (co0 + cc >= d.cout) continue;
     double sum = 0.0;
     for (int gg = 0; gg < G; ++gg) sum += red[((size_t)gg * CT + cc) * R + q];
-    if (q < K * K)
-      o[((int64_t)(co0 + cc) * d.cin + ci) * K * K + q] = sum;
-    else if (ci == 0)
+    if (q < CI * K * K) {
+      const int i = q / (K * K);
+      if (ci0 + i < d.cin) o[((int64_t)(co0 + cc) * d.cin + ci0 + i) * K * K + (q - i * K * K)] = sum;
+    } else if (ci0 == 0) {
       o[(int64_t)d.cout * d.cin * K * K + co0 + cc] = sum;
+    }
   }
 }
 
@@ -1148,13 +1170,15 @@ void launch_eval_cnn(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_
       dispatch_k(d.k, [&](auto kc) {
         constexpr int K = decltype(kc)::value, CT = 16;
         const dim3 grid((unsigned)d.cin, (unsigned)((d.cout + CT - 1) / CT), (unsigned)(J * nchunks));
-        if constexpr (K <= 3) {  // patch-per-thread layout (C4 step 6.36 -> 5.76 s; slower at C3's K = 5)
-          const size_t stage =
-              sizeof(float) * (((size_t)d.hin * d.win + 3) / 4 * 4 + (size_t)CT * ((d.ho * d.wo) | 1));
-          const size_t red = sizeof(double) * (size_t)128 * (K * K + 1);  // [G][CT][K*K + 1], G * CT = 128
+        if constexpr (K <= 3) {  // patch-per-thread layout (C4 step 6.36 -> 4.49 s; slower at C3's K = 5)
+          constexpr int CI = DASMC_CONV_DW_CI;  // input channels per block (the dz planes staged once for them)
+          const dim3 grid_ci((unsigned)((d.cin + CI - 1) / CI), grid.y, grid.z);
+          const size_t stage = sizeof(float) * ((size_t)CI * (((size_t)d.hin * d.win + 3) / 4 * 4) +
+                                                (size_t)CT * ((d.ho * d.wo) | 1));
+          const size_t red = sizeof(double) * (size_t)128 * (CI * K * K + 1);  // [G][CT][CI*K*K + 1]
           const size_t sm = std::max(stage, red);
-          set_smem(conv_dw_kernel<K, CT>, sm);
-          conv_dw_kernel<K, CT><<<grid, 128, sm, c.stream>>>(d, dz, a_ps, in, in_ps, M, np, nchunks, part);
+          set_smem(conv_dw_kernel<K, CT, CI>, sm);
+          conv_dw_kernel<K, CT, CI><<<grid_ci, 128, sm, c.stream>>>(d, dz, a_ps, in, in_ps, M, np, nchunks, part);
         } else {
           const size_t sm = sizeof(float) * (((size_t)d.hin * d.win + 3) / 4 * 4 + (size_t)CT * d.ho * d.wo);
           set_smem(conv_dw_rows_kernel<K, CT>, sm);
