@@ -789,30 +789,35 @@ __global__ void pool_fwd_kernel(ConvDev d, const float* __restrict__ A, int64_t 
 }
 
 // dz = (first argmax of the window ? dP : 0) * act'(A); positions outside the pooled region get 0
+// 2x2/2 max-pool backward: one thread per pooled output (2 index divisions, 32-bit inside an
+// image) routes dP to the first maximum of its window in (dy, dx) order, times act'(max),
+// and writes the window's four dz values.  Pre-pool rows / columns that no window covers
+// (odd sizes, floor pooling) are zeroed by the caller.
 __global__ void pool_bwd_kernel(ConvDev d, int act, const float* __restrict__ A, int64_t a_ps,
                                 const float* __restrict__ dP, int64_t p_ps, float* __restrict__ dZ, int64_t M,
                                 int64_t J) {
-  const int64_t per_a = (int64_t)d.cout * d.ho * d.wo, per = (int64_t)d.cout * d.sh * d.sw;
-  const int64_t total = J * M * per_a;
+  const int64_t per_a = (int64_t)d.cout * d.ho * d.wo;
+  const int npool = d.cout * d.sh * d.sw, nplane = d.sh * d.sw;
+  const int64_t total = J * M * npool;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = g / (M * per_a), r = g - j * M * per_a, m = r / per_a, o = r - m * per_a;
-    const int co = (int)(o / ((int64_t)d.ho * d.wo));
-    const int yx = (int)(o - (int64_t)co * d.ho * d.wo), y = yx / d.wo, x = yx - y * d.wo;
-    const int py = y >> 1, px = x >> 1;
-    float v = 0.f;
-    if (py < d.sh && px < d.sw) {
-      const float* a = A + j * a_ps + m * per_a + ((int64_t)co * d.ho + 2 * py) * d.wo + 2 * px;
-      int best = 0;
-      float mx = a[0];
-      if (a[1] > mx) { mx = a[1]; best = 1; }
-      if (a[d.wo] > mx) { mx = a[d.wo]; best = 2; }
-      if (a[d.wo + 1] > mx) { mx = a[d.wo + 1]; best = 3; }
-      if (((y & 1) << 1 | (x & 1)) == best) {
-        const float dp = dP[j * p_ps + m * per + ((int64_t)co * d.sh + py) * d.sw + px];
-        v = dp * act_grad_post(A[j * a_ps + m * per_a + o], act);
-      }
-    }
-    dZ[j * a_ps + m * per_a + o] = v;
+    const int64_t img = g / npool;
+    const int q = (int)(g - img * npool);
+    const int64_t j = img / M, m = img - j * M;
+    const int co = q / nplane, pyx = q - co * nplane, py = pyx / d.sw, px = pyx - py * d.sw;
+    const int64_t off = j * a_ps + m * per_a + ((int64_t)co * d.ho + 2 * py) * d.wo + 2 * px;
+    const float* a = A + off;
+    const float a0 = a[0], a1 = a[1], a2 = a[d.wo], a3 = a[d.wo + 1];
+    int best = 0;
+    float mx = a0;
+    if (a1 > mx) { mx = a1; best = 1; }
+    if (a2 > mx) { mx = a2; best = 2; }
+    if (a3 > mx) { mx = a3; best = 3; }
+    const float v = dP[j * p_ps + m * (int64_t)npool + q] * act_grad_post(mx, act);
+    float* z = dZ + off;
+    z[0] = best == 0 ? v : 0.f;
+    z[1] = best == 1 ? v : 0.f;
+    z[d.wo] = best == 2 ? v : 0.f;
+    z[d.wo + 1] = best == 3 ? v : 0.f;
   }
 }
 
@@ -1156,7 +1161,8 @@ void launch_eval_cnn(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_
     float* dz = c.cact[i];  // no pool: the stage-output delta (act' applied) is already dz
     if (d.pool) {
       dz = c.cdel[i];
-      pool_bwd_kernel<<<grid_of(J * M * conv_act_floats(d)), 256, 0, c.stream>>>(
+      if ((d.ho | d.wo) & 1) CK(cudaMemsetAsync(dz, 0, sizeof(float) * (size_t)J * a_ps, c.stream));
+      pool_bwd_kernel<<<grid_of(J * M * (int64_t)d.cout * d.sh * d.sw), 256, 0, c.stream>>>(
           d, net.act, c.cact[i], a_ps, c.cpool[i], c.Mcap * conv_out_floats(d), dz, M, J);
       LAUNCHED();
     }
