@@ -56,10 +56,11 @@ WORKLOADS = {
                     "M=1000, resample every iteration, HMC S=3 h=0.002"),
     # BASELINE.json configs[0] (CPU-runnable case)
     "c1": dict(layers=[64, 32, 10], act="tanh", n=2000, J=128, feature_kind=0, mb=100, period=1, K=50, S=3,
-               h=0.002, k0=0, cfg_id=1, ctr=(200, 40),
+               h=0.002, k0=0, cfg_id=1, ctr=(200, 40), big=False,
                desc="C1: MLP 64-32-10 tanh, J=128, n=2000 U[0,1]^64 teacher-labelled, CTR 2 MB -> 20 MB at it 40"),
 }
 
+DATA_DESC = "synthetic (teacher-labelled, seeded; BASELINE.json config shapes)"
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # arithmetic of the dense contractions per --precision
 DTYPES = {"fp32": "f32", "tf32": "tf32", "3xtf32": "3xtf32", "f16": "f16",
@@ -154,9 +155,44 @@ def make_data(w):
     return spec, np.ascontiguousarray(X[perm]), np.ascontiguousarray(y[perm])
 
 
-def cpu_sample(w, X, y, ks, threads, warm=False):
+def oracle_data(w):
+    """The same teacher data and shuffle from the CPU oracle alone (the reference arm never
+    loads the product library)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    layers = w["layers"] if "conv" not in w else O.cnn_layers(w["conv"][0], w["conv"][1], w["layers"])
+    a = 0 if w["act"] == "relu" else 1
+    X, y = O.make_teacher(layers, a, w["n"], w["feature_kind"], 0, w["cfg_id"], threads=os.cpu_count() or 8)
+    perm = O.shuffle_perm(0, w["n"])
+    return np.ascontiguousarray(X[perm].astype(np.float32)), np.ascontiguousarray(y[perm])
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def config_of(args, w, ks, Ms, world):
+    """The workload description both arms print (same dict: the driver compares them)."""
+    J = w["J"]
+    return {"workload": w["desc"], "particles_per_gpu": J, "iterations": [ks[0], ks[-1]],
+            "window_rows": [Ms[0], Ms[-1]], "precision": args.precision, "resample": args.resample,
+            "l2": "inputs larger than L2 (activations >= 24 GB per step)" if w.get("big", True)
+            else "inputs smaller than L2 (launch-bound config)",
+            "parallelism": (f"one particle-sharded ensemble of J={J * world} over {world} GPUs "
+                            "(NCCL all-gather of log-weights, P2P particle migration)"
+                            if world > 1 else "single GPU")}
+
+
+def cpu_sample(w, X, y, ks, threads, warm=0):
     """The CPU oracle (fp64 restatement of the reference, OpenBLAS dgemm, parallel_for
-    over particles) on a bounded sample: one smc_step of `threads` particles per k."""
+    over particles) on a bounded sample: one smc_step of `threads` particles per k, after
+    `warm` untimed steps."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as O
     O.use_blas(True)
@@ -168,38 +204,47 @@ def cpu_sample(w, X, y, ks, threads, warm=False):
     rows = lambda k: min(window(w, k), w.get("cpu_rows", 1 << 62))  # noqa: E731
     th, lw = O.init_ensemble(layers, a, X64, y, (0, rows(ks[0]), w["n"]), 0, 1.0, 1.0, 0, Jc, threads=threads)
     units, secs = 0.0, 0.0
-    for k in ks:
+    for i, k in enumerate([ks[0]] * warm + list(ks)):
         M = rows(k)
         t0 = time.perf_counter()
         th, lw, _, _, _ = O.smc_step(layers, a, X64, y, (0, M, w["n"]), 0, 1.0, 1.0, (w["h"], w["S"], 0), 0, 0.5, 1,
                                      False, th, lw, k, threads=threads, dumps=False)
-        secs += time.perf_counter() - t0
-        units += Jc * (w["S"] + 1) * M
+        if i >= warm:
+            secs += time.perf_counter() - t0
+            units += Jc * (w["S"] + 1) * M
     return units, secs, Jc
 
 
+def cpu_sample_desc(w, Jc, threads, nsteps):
+    rows = f"min(window, {w['cpu_rows']}) rows" if "cpu_rows" in w else "the step's window"
+    return (f"{nsteps} warm smc_step(s) of {Jc} particles at {rows} (CPU oracle: fp64 restatement of the "
+            f"reference, OpenBLAS dgemm 1 thread x {threads} particle threads, {cpu_model()}); the per-unit rate "
+            "extrapolates linearly in J (per-particle work is independent, parallel.hpp static partition); "
+            "the reference itself is not buildable here (Eigen3 absent)")
+
+
 def run_reference(args, w):
+    """--impl reference: the reference's CPU path (the oracle port; the reference does not
+    build without Eigen3) on this box's host cores, same metric / config as our arm.  Only
+    the oracle is loaded (no product library)."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    spec, X, y = make_data(w)
+    X, y = oracle_data(w)
     threads = os.cpu_count() or 1
     k0 = w["k0"]
-    if args.warmup:
-        cpu_sample(w, X, y, [k0 + i for i in range(min(args.warmup, 1))], threads)
     ks = [k0 + args.warmup + i for i in range(args.steps)]
-    units, secs, Jc = cpu_sample(w, X, y, ks, threads)
+    Ms = [window(w, k) for k in ks]
+    units, secs, Jc = cpu_sample(w, X, y, ks, threads, warm=min(args.warmup, 1))
     v = units / secs
     line = {"impl": "reference", "metric": "particle-sample grad evals/sec", "value": v,
             "unit": "particle-sample grad evals/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w["desc"], "iterations": [ks[0], ks[-1]],
-                       "window_rows": [window(w, ks[0]), window(w, ks[-1])]},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA_DESC,
+            "config": config_of(args, w, ks, Ms, world),
             "cpu_baseline": {"value": v, "unit": "particle-sample grad evals/s", "cores": threads, "kind": "port",
-                             "sample": f"one smc_step of {Jc} particles per step at the step's window "
-                                       f"(CPU oracle, fp64, OpenBLAS dgemm 1 thread x {threads} particle threads; "
-                                       "reference not buildable here: Eigen3 absent)"},
+                             "cpu": cpu_model(), "sample": cpu_sample_desc(w, Jc, threads, args.steps)},
             "e2e": {"value": v, "unit": "particle-sample grad evals/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -360,21 +405,16 @@ def run_ours(args, w):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        cu, cs, Jc = cpu_sample(w, X, y, [ks[0]], threads)
+        ncpu = 2
+        cu, cs, Jc = cpu_sample(w, X, y, ks[:ncpu], threads, warm=1)
         cpu = {"value": cu / cs, "unit": "particle-sample grad evals/s", "cores": threads, "kind": "port",
-               "sample": f"one smc_step of {Jc} particles at window M={window(w, ks[0])} (CPU oracle fp64, "
-                         f"OpenBLAS dgemm, {threads} particle threads)"}
+               "cpu": cpu_model(), "sample": cpu_sample_desc(w, Jc, threads, min(ncpu, len(ks)))}
     if rank == 0:
         line = {"metric": "particle-sample grad evals/sec", "value": value, "unit": "particle-sample grad evals/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPES.get(args.precision, args.precision),
-                "data": "synthetic (teacher-labelled, seeded; BASELINE.json configs[1] shapes)",
-                "config": {"workload": w["desc"], "particles_per_gpu": J, "iterations": [ks[0], ks[-1]],
-                           "window_rows": [Ms[0], Ms[-1]], "precision": args.precision, "resample": rk,
-                           "l2": "inputs larger than L2 (activations >= 24 GB per step)",
-                           "parallelism": (f"one particle-sharded ensemble of J={J * world} over {world} GPUs "
-                                           "(NCCL all-gather of log-weights, P2P particle migration)"
-                                           if world > 1 else "single GPU")},
+                "data": DATA_DESC,
+                "config": config_of(args, w, ks, Ms, world),
                 "iterations_per_sec": args.steps / (ms_max / 1e3),
                 "particle_grad_evals_per_sec": world * J * (S + 1) * args.steps / (ms_max / 1e3),
                 "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof,
@@ -402,14 +442,21 @@ def main():
     ap.add_argument("--resample", default="systematic", choices=["systematic", "multinomial"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--J", type=int, default=None, help="particles per GPU (default: the config's)")
     args = ap.parse_args()
-    w = WORKLOADS[args.config]
+    w = dict(WORKLOADS[args.config])
+    if args.J:
+        w["J"] = args.J
+        w["desc"] = w["desc"].replace(f"J={WORKLOADS[args.config]['J']}", f"J={args.J}")
     if args.precision is None:
         # one hidden layer: tf32 forward + fp16-stored weight-gradient operands (tf32h, same
         # 11-bit significand, tolerance of the tf32 path); deep MLPs: tf32 chain; CNNs: fp32
         tc1 = "conv" not in w and len(w["layers"]) == 3 and w["layers"][1] <= 256 and w["layers"][2] <= 16
         deep = "conv" not in w and len(w["layers"]) > 3 and w["layers"][-1] <= 16
-        args.precision = "tf32h" if tc1 else "tf32" if deep else "fp32"
+        # one hidden layer: f16x2 (fp16 X times [W1, b1] split into fp16 hi + lo; the most accurate
+        # tensor-core mode within ~3 % of the fastest at the benched window:
+        # tests/test_gpu_bench_window.py); deep MLPs: tf32 chain; CNNs: fp32
+        args.precision = "f16x2" if tc1 else "tf32" if deep else "fp32"
     if args.impl == "reference":
         run_reference(args, w)
     else:

@@ -177,6 +177,10 @@ int dasmc_gpu_loglik_parts(dasmc_ctx* ctx, const double* theta, int64_t J, doubl
 /* Momentum draws p0 of propose() (kernels.hpp:131) for iteration k, particles
  * [0, J): stream root.fork(kProposal, k, j) (smc.hpp:119-120), fp64 out. */
 int dasmc_gpu_momentum(dasmc_ctx* ctx, uint64_t seed, int k, int64_t J, double* p0);
+/* Resampling uniforms of iteration k as the step draws them on the device: `count` draws of
+ * root.fork(kResample, k) (smc.hpp:152; numeric.hpp:95-99), chunked with the F2 jump-ahead
+ * (parity hook for rng.hpp:60-64 uniform()). */
+int dasmc_gpu_uniforms(dasmc_ctx* ctx, uint64_t seed, int k, int64_t count, double* u);
 /* Bit-exact resampling hook: indices given normalised weights w[J] and
  * uniforms u (J of them for multinomial, u[0] for systematic)
  * (numeric.hpp:81-101 sample_categorical's CDF + upper_bound). */

@@ -9,3 +9,8 @@ from .api import (GpuEnsembleTarget, KernelConfig, NetSpec, RunConfig, ScheduleC
                   load_idx, parse_idx, predictive_metrics, redraw_rows, sda_moments_from,
                   shuffle_permutation)
 from ._lib import LIB_PATH, SamplerError, load  # noqa: F401
+
+# Arithmetic of the one-hidden-layer MLP configs' headline runs (bench.py, smoke): the most
+# accurate tensor-core mode within a few percent of the fastest at the benched window
+# (tests/test_gpu_bench_window.py).
+DEFAULT_PRECISION = "f16x2"

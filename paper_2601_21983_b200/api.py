@@ -273,6 +273,11 @@ class GpuEnsembleTarget:
         L.check(self.lib.dasmc_gpu_momentum(self.h, seed, k, J, _dp(out)))
         return out
 
+    def uniforms(self, seed: int, k: int, count: int) -> np.ndarray:  # fork(kResample, k) draws (smc.hpp:152)
+        u = np.empty(count)
+        L.check(self.lib.dasmc_gpu_uniforms(self.h, seed, k, count, _dp(u)))
+        return u
+
     def resample_indices(self, w, u, kind: str = "multinomial") -> np.ndarray:
         w = np.ascontiguousarray(w, dtype=np.float64)
         u = np.ascontiguousarray(u, dtype=np.float64)

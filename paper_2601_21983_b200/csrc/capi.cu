@@ -632,6 +632,17 @@ int dasmc_gpu_momentum(dasmc_ctx* ctx, uint64_t seed, int k, int64_t J, double* 
   });
 }
 
+int dasmc_gpu_uniforms(dasmc_ctx* ctx, uint64_t seed, int k, int64_t count, double* u) {
+  return guarded([&] {
+    if (!ctx || !u || count < 1) throw InvalidArg("bad argument");
+    Ctx& c = ctx->c;
+    if (count > c.Jmax) throw InvalidArg("uniforms: count exceeds max_particles");
+    CK(cudaSetDevice(c.device));
+    launch_uniforms(c, fork_key(seed, tag::kResample, (uint64_t)k, 0), count, c.uni);
+    download(c, u, c.uni, sizeof(double) * count);
+  });
+}
+
 int dasmc_gpu_resample_indices(dasmc_ctx* ctx, const double* w, const double* u, int64_t J, int kind,
                                int32_t* idx) {
   return guarded([&] {
