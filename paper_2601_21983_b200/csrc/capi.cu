@@ -19,6 +19,7 @@
 #include "ctx.cuh"
 #include "host.h"
 #include "tc_gemm.cuh"
+#include "conv_tc.cuh"
 
 struct dasmc_ctx {
   dasmc_b200::Ctx c;
@@ -137,6 +138,8 @@ void free_ctx(Ctx& c) {
   cudaSetDevice(c.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
   tc_free(c);
+  cnn_tc_free(c);
+  if (c.gacc) cudaFree(c.gacc);
   void* ptrs[] = {c.X_full, c.Xt, c.y_full, c.Xg, c.yg, c.rows_dev, c.gcache[0], c.gcache[1], c.lt_cache, c.theta[0], c.theta[1], c.theta[2], c.p, c.grad, c.logw, c.dT, c.ll_part,
                   c.th_part, c.p_part, c.p0_part, c.p0_sum, c.pS_sum, c.flags, c.lt_old, c.lt_new, c.ll_pre, c.ll_blk, c.ll_pre0, c.ll_blk0,
                   c.sda_pre, c.sda_blk, c.wts, c.cdf,
@@ -477,7 +480,14 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
   const auto tab = jump_table(2 * (uint64_t)c.rng_chunk, c.jump_chunks);
   dmalloc(c.jump_tab, (size_t)c.jump_chunks * 4);
   CK(cudaMemcpy(c.jump_tab, tab.data(), sizeof(uint64_t) * 4 * tab.size(), cudaMemcpyHostToDevice));
-  if (precision != DASMC_PREC_FP32) {
+  if (precision != DASMC_PREC_FP32 && c.net.nconv > 0) {
+    // [EXT] CNN: convolution stages on tcgen05 (kind::tf32 implicit GEMMs), the MLP head on CUDA cores
+    if (precision != DASMC_PREC_TF32 && precision != DASMC_PREC_TF32H)
+      throw InvalidArg("CNN contexts: precision fp32 (CUDA cores) or tf32 (tensor-core convolutions)");
+    if (!cnn_tc_eligible(c))
+      throw InvalidArg("tensor-core CNN stages need cout % 4 == 0 (and cin % 4 == 0 after stage 0), <= 256 channels");
+    cnn_tc_init(c);
+  } else if (precision != DASMC_PREC_FP32) {
     if (!tc_layer1_eligible(c))
       throw InvalidArg("tensor-core precision needs a one-hidden-layer MLP (no conv stages) with input % 4 == 0, "
                        "hidden <= 256, classes <= 16 (use DASMC_PREC_FP32)");
@@ -546,6 +556,7 @@ void set_rows_dev(Ctx& c, const int64_t* rows, int64_t count) {
     c.n_active = count;
   }
   if (c.tc) tc_refresh_data(c);
+  if (c.ctc) cnn_tc_refresh_data(c, c.X, c.n_active);
 }
 
 int dasmc_gpu_set_target(dasmc_ctx* ctx, int64_t prefix_end, int64_t block_end, int64_t total_n, int mode,

@@ -1,0 +1,851 @@
+// [EXT] CNN stages (BASELINE.json configs[2..3]) on the tcgen05 tensor cores: implicit-GEMM
+// convolutions.  The reference is MLP-only; its contraction sites (network.hpp:171-173 forward,
+// 203-209 dW and delta) are generalised to the convolution stages of dasmc_gpu.h's conv
+// descriptor, with the oracle's semantics (oracle/dasmc_oracle.hpp CnnSpec: valid stride-1
+// convolutions, activation, optional 2x2/2 max-pool with floor, first-max routing).
+//
+// One gather-GEMM kernel serves all three contractions of a stage, per particle j:
+//   forward  Z[r, co]   = sum_q A[r, q] W[co, q]      r = output pixel (image, y, x), q = (ky, kx, ci)
+//   delta    dI[r, ci]  = sum_q dZpad[r, q] W'[ci, q] r = input pixel, q = (ky, kx, co)
+//   weights  dW[i, co]  = sum_r In[i, r] dZ[co, r]    i = (ky, kx, ci) (+ the bias row of ones)
+// Operands are never materialised as im2col matrices in HBM: four producer warps gather each
+// 128 x 32 tf32 k-block straight from the NHWC activation buffers into the 128B-swizzled
+// K-major shared-memory layout the UMMA reads, with cp.async (16-byte chunks when four
+// consecutive k are contiguous channels, else 4-byte elements), element offsets taken from
+// small per-stage row / column tables (row part + column part), and zero fill past the edges.
+// cp.async.mbarrier.arrive completes the stage's full barrier; one thread issues
+// tcgen05.mma kind::tf32 (M = 128, N <= 256, K = 8) into double-buffered TMEM accumulators;
+// four epilogue warps drain them (tcgen05.ld) with the fused epilogue:
+//   forward: bias + activation, tf32-rounded NHWC store (the next stage's operand);
+//   delta:   times act'(mask) (or identity before a max-pool), store into the previous stage's
+//            zero-bordered delta buffer (so the next delta GEMM needs no bounds checks);
+//   weights: the fused leapfrog (epi.cuh), with the chunked-window accumulation.
+// Activations are stored tf32-rounded (round to nearest), so the MMA's operand truncation
+// does not bias the long sums (same rule as tc_gemm.cu).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <stdexcept>
+#include <vector>
+
+#include "conv_tc.cuh"
+#include "epi.cuh"
+#include "tc_ptx.cuh"
+
+namespace dasmc_b200 {
+
+namespace {
+
+constexpr int kCBM = 128;              // UMMA M
+constexpr int kCBK = 32;               // tf32 elements per 128-byte swizzle row (one k-block)
+constexpr int kProdWarps = 4;          // gather producers
+constexpr int kCThreads = 32 * (kProdWarps + 1 + 4);  // + MMA warp + 4 epilogue warps
+constexpr int kOnesRow = -2147483647;  // row table entry: a row of ones (the bias row of dW)
+constexpr int kZeroRow = -2147483647 - 1;
+
+struct GOperand {
+  const float* base;
+  int64_t ps;          // particle stride (floats); 0 = shared by all particles
+  const int* rowoff;   // element offset of row i (nullptr: i * ld)
+  int ld;
+  int nrows;           // rows >= nrows are zero
+  const int* coloff;   // element offset of column q (nullptr: q)
+  int K;               // columns >= K are zero
+  int vec;             // 1: coloff[4c .. 4c+3] are consecutive and 16-byte aligned (16-byte copies)
+};
+
+struct GParams {
+  GOperand a, b;
+  const float* ones;  // 16 bytes of 1.0f (the source of kOnesRow elements)
+  int J, rtiles, nkb, nmma, tcols_half, stages;
+  // epilogue (forward / delta): out[j * out_ps + outoff[r] + n] for r < Rvalid, n < nvalid
+  int Rvalid, nvalid;
+  float* out;
+  int64_t out_ps;
+  const int* outoff;
+  int out_ld;
+  const float* mask;  // delta: act'(mask[j * mask_ps + maskoff[r] + n]) (nullptr: identity)
+  int64_t mask_ps;
+  int mask_ld;
+  const float* theta;  // forward: bias b[n] at theta[j * Dp + boff + n]
+  int64_t Dp, boff;
+  // weights: row i < nrows_w is parameter woff + n * Kw + prow[i] (prow[i] < 0: bias boff + n)
+  EpiParams e;
+  int64_t woff;
+  int Kw, nrows_w;
+  const int* prow;
+};
+
+constexpr int kEpiConvFwd = 0, kEpiConvDx = 1, kEpiConvDw = 2;
+
+// byte offset of element (row, k) of a 128B-swizzled K-major tile (8-row atoms of 1024 B)
+__device__ __forceinline__ uint32_t swz(int row, int k) {
+  return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((((k >> 2) ^ row) & 7) << 4) + ((k & 3) << 2));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const float* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ int row_off(const GOperand& o, int i) {
+  if (i >= o.nrows) return kZeroRow;
+  return o.rowoff ? o.rowoff[i] : i * o.ld;
+}
+__device__ __forceinline__ int col_off(const GOperand& o, int q) { return o.coloff ? o.coloff[q] : q; }
+
+// One operand tile (rows [r0, r0 + nrows_tile), k-block kb) into shared memory at `tile`.
+// Vector path: lane -> (row lane / 8, 16-byte chunk lane % 8), a warp stores 4 full rows.
+// Scalar path: lane -> (row lane / 4, element lane % 4 of a chunk), 8 rows x 16 bytes per
+// instruction; both are bank-conflict free under the 128B swizzle.
+template <int MAXP>
+__device__ __forceinline__ void gather_tile(const GOperand& o, const float* pbase, const float* ones, uint32_t tile,
+                                            const int* roff, int npass, int nrt, int kb, int pt, int lane) {
+  const int q0 = kb * kCBK;
+  if (o.vec) {
+    const int c = lane & 7;
+    const int q = q0 + 4 * c;
+    const bool qv = q < o.K;
+    const int co = qv ? col_off(o, q) : 0;
+#pragma unroll
+    for (int p = 0; p < MAXP; ++p) {
+      if (p >= npass) break;
+      const int rl = (p * kProdWarps + pt) * 4 + (lane >> 3);  // row within the tile
+      if (rl >= nrt) break;
+      const int ro = roff[p];
+      const bool v = qv && ro != kZeroRow;
+      cp_async16(tile + swz(rl, 4 * c), v ? pbase + (int64_t)ro + co : pbase, v);
+    }
+  } else {
+    const int e = lane & 3;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int q = q0 + 4 * c + e;
+      const bool qv = q < o.K;
+      const int co = qv ? col_off(o, q) : 0;
+#pragma unroll
+      for (int p = 0; p < MAXP; ++p) {
+        if (p >= npass) break;
+        const int rl = (p * kProdWarps + pt) * 8 + (lane >> 2);
+        if (rl >= nrt) break;
+        const int ro = roff[p];
+        const bool v = qv && ro != kZeroRow;
+        const float* src = ro == kOnesRow ? ones : (v ? pbase + (int64_t)ro + co : pbase);
+        cp_async4(tile + swz(rl, 4 * c + e), src, v);
+      }
+    }
+  }
+}
+
+template <int EPI, int ACT>
+__global__ void __launch_bounds__(kCThreads, 2) conv_tc_kernel(const __grid_constant__ GParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t a_bytes = kCBM * 128, b_bytes = (uint32_t)p.nmma * 128;
+  const uint32_t stage_bytes = a_bytes + b_bytes;
+  uint64_t* full = (uint64_t*)(smem + (size_t)p.stages * stage_bytes);
+  uint64_t* empty = full + p.stages;
+  uint64_t* tfull = empty + p.stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = (uint32_t*)(tempty + 2);
+  const int units = p.rtiles * p.J;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 32 * kProdWarps);  // one cp.async arrival per producer thread
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kProdWarps) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(2 * p.tcols_half)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp < kProdWarps) {
+    // ===================== gather producers =====================
+    const uint32_t stages0 = smem_u32(smem);
+    const int pa = p.a.vec ? 8 : 4;                                   // A row passes per thread
+    const int pb = p.b.vec ? (p.nmma + 15) / 16 : (p.nmma + 31) / 32;  // B row passes per thread
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < units; t += gridDim.x) {
+      const int rt = t % p.rtiles, j = t / p.rtiles;
+      int ra[8], rb[16];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int rl = p.a.vec ? (q * kProdWarps + warp) * 4 + (lane >> 3) : (q * kProdWarps + warp) * 8 + (lane >> 2);
+        ra[q] = q < pa ? row_off(p.a, rt * kCBM + rl) : kZeroRow;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int rl = p.b.vec ? (q * kProdWarps + warp) * 4 + (lane >> 3) : (q * kProdWarps + warp) * 8 + (lane >> 2);
+        rb[q] = (q < pb && rl < p.nmma) ? row_off(p.b, rl) : kZeroRow;
+      }
+      const float* abase = p.a.base + (int64_t)j * p.a.ps;
+      const float* bbase = p.b.base + (int64_t)j * p.b.ps;
+      for (int kb = 0; kb < p.nkb; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        const uint32_t st = stages0 + (uint32_t)s * stage_bytes;
+        gather_tile<8>(p.a, abase, p.ones, st, ra, pa, kCBM, kb, warp, lane);
+        gather_tile<16>(p.b, bbase, p.ones, st + a_bytes, rb, pb, p.nmma, kb, warp, lane);
+        cp_async_arrive(&full[s]);
+        if (++s == p.stages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    // drain: the CTA may not exit with copies in flight
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp == kProdWarps) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      const uint32_t idesc = idesc_tf32(p.nmma, kCBM);
+      int s = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int t = blockIdx.x; t < units; t += gridDim.x) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * p.tcols_half);
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          mbar_wait(&full[s], ph);
+          // the stage was written through the generic proxy (cp.async); order it before the
+          // tensor core's async-proxy reads
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          tc_fence_after();
+          uint8_t* st = smem + (size_t)s * stage_bytes;
+          const uint64_t ad = smem_desc(st), bd = smem_desc(st + a_bytes);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) tc_mma<0>(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          tc_commit(&empty[s]);
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+      }
+    }
+  } else {
+    // ===================== epilogue (4 warps, one TMEM lane group each) =====================
+    const int lg = warp & 3;
+    const int row_in_tile = lg * 32 + lane;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int t = blockIdx.x; t < units; t += gridDim.x) {
+      const int rt = t % p.rtiles, j = t / p.rtiles;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (uint32_t)(acc * p.tcols_half) + ((uint32_t)(lg * 32) << 16);
+      const int r = rt * kCBM + row_in_tile;
+      for (int ch = 0; ch < p.nmma / 16; ++ch) {
+        float v[16];
+        tmem_ld16(taddr + ch * 16, v);
+        const int n0 = ch * 16;
+        const int nq = min(16, p.nvalid - n0);  // warp-uniform
+        if (nq <= 0) continue;
+        if (EPI == kEpiConvFwd || EPI == kEpiConvDx) {
+          if (r >= p.Rvalid) continue;
+          float* dst = p.out + (int64_t)j * p.out_ps + (p.outoff ? (int64_t)p.outoff[r] : (int64_t)r * p.out_ld) + n0;
+          if (EPI == kEpiConvFwd) {
+            const float* b = p.theta + (int64_t)j * p.Dp + p.boff + n0;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (q < nq) {
+                const float z = v[q] + b[q];
+                v[q] = tf32_hi(ACT == DASMC_RELU ? fmaxf(z, 0.f) : tanhf(z));
+              }
+          } else {
+            if (p.mask) {
+              const float* m = p.mask + (int64_t)j * p.mask_ps + (int64_t)r * p.mask_ld + n0;
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                if (q < nq) {
+                  const float a = m[q];
+                  v[q] *= ACT == DASMC_RELU ? (a > 0.f ? 1.f : 0.f) : 1.f - a * a;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = tf32_hi(v[q]);
+          }
+          if (nq == 16 && (((uintptr_t)dst) & 15) == 0) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              reinterpret_cast<float4*>(dst)[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (q < nq) dst[q] = v[q];
+          }
+        } else {
+          if (r >= p.nrows_w) continue;
+          const int pr = p.prow[r];
+          int64_t idx[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            idx[q] = (int64_t)j * p.Dp + (pr >= 0 ? p.woff + (int64_t)(n0 + q) * p.Kw + pr : p.boff + n0 + q);
+          leapfrog_update_n<16>(p.e, j, idx, v, nq);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[acc]));
+      acc ^= 1;
+      if (acc == 0) aph ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == kProdWarps) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * p.tcols_half)
+                 : "memory");
+  }
+}
+
+// ---- stage helpers -------------------------------------------------------------------------
+// W copies for the forward (Wf[j][n][kk], kk in the stage's k-order) and delta (Wd[j][ci][kk],
+// kk = (ky, kx, co)) GEMMs, tf32-rounded, zero padded to [nrows][Kp].
+__global__ void conv_wcopy_kernel(const float* __restrict__ theta, int64_t Dp, int64_t woff, int cin, int k, int cout,
+                                  int mode, int korder, int nrows, int Kp, int64_t J, float* __restrict__ out) {
+  const int kk2 = k * k;
+  const int64_t per = (int64_t)nrows * Kp, total = J * per;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / per;
+    const int rem = (int)(g - j * per), n = rem / Kp, q = rem - n * Kp;
+    float v = 0.f;
+    if (mode == 0) {  // forward: row co, column q over (ky, kx, ci) [korder 0] or (ci, ky, kx) [korder 1]
+      if (n < cout && q < cin * kk2) {
+        const int src = korder == 0 ? (q % cin) * kk2 + q / cin : q;
+        v = theta[j * Dp + woff + (int64_t)n * cin * kk2 + src];
+      }
+    } else {  // delta: row ci, column q over (ky, kx, co)
+      if (n < cin && q < cout * kk2) {
+        const int kyx = q / cout, co = q - kyx * cout;
+        v = theta[j * Dp + woff + ((int64_t)co * cin + n) * kk2 + kyx];
+      }
+    }
+    out[g] = tf32_hi(v);
+  }
+}
+
+// 2x2/2 max-pool forward of an NHWC stage output; flat != 0 writes the flatten order (c, y, x)
+// of the head input instead of NHWC.
+__global__ void pool_fwd_nhwc_kernel(ConvDev d, const float* __restrict__ A, int64_t a_ps, float* __restrict__ P,
+                                     int64_t p_ps, int64_t M, int64_t J, int flat) {
+  const int C = d.cout;
+  const int64_t per = (int64_t)d.sh * d.sw * C, total = J * M * per;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / (M * per), rem = g - j * M * per, m = rem / per;
+    const int o = (int)(rem - m * per);
+    const int c = o % C, pyx = o / C, py = pyx / d.sw, px = pyx - py * d.sw;
+    const float* a = A + j * a_ps + m * (int64_t)d.ho * d.wo * C + ((int64_t)(2 * py) * d.wo + 2 * px) * C + c;
+    const int64_t rowC = (int64_t)d.wo * C;
+    const float v = fmaxf(fmaxf(a[0], a[C]), fmaxf(a[rowC], a[rowC + C]));
+    P[j * p_ps + m * per + (flat ? (int64_t)c * d.sh * d.sw + pyx : o)] = v;
+  }
+}
+
+// Max-pool backward into the stage's zero-bordered delta buffer: the pooled delta (NHWC, or the
+// head's flatten order) times act'(max) goes to the first maximum of the window in (dy, dx)
+// order, zeros to the other three positions (network activation derivative from the
+// post-activation value, network.hpp:211-214).  Pad = k - 1 on every side.
+__global__ void pool_bwd_nhwc_kernel(ConvDev d, int act, const float* __restrict__ A, int64_t a_ps,
+                                     const float* __restrict__ dP, int64_t dp_ps, int flat, float* __restrict__ dZ,
+                                     int64_t dz_ps, int64_t M, int64_t J) {
+  const int C = d.cout, pad = d.k - 1, W2 = d.wo + 2 * pad, H2 = d.ho + 2 * pad;
+  const int64_t per = (int64_t)d.sh * d.sw * C, total = J * M * per;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / (M * per), rem = g - j * M * per, m = rem / per;
+    const int o = (int)(rem - m * per);
+    const int c = o % C, pyx = o / C, py = pyx / d.sw, px = pyx - py * d.sw;
+    const int64_t rowC = (int64_t)d.wo * C;
+    const float* a = A + j * a_ps + m * (int64_t)d.ho * d.wo * C + ((int64_t)(2 * py) * d.wo + 2 * px) * C + c;
+    const float a0 = a[0], a1 = a[C], a2 = a[rowC], a3 = a[rowC + C];
+    int best = 0;
+    float mx = a0;
+    if (a1 > mx) { mx = a1; best = 1; }
+    if (a2 > mx) { mx = a2; best = 2; }
+    if (a3 > mx) { mx = a3; best = 3; }
+    const float gp = dP[j * dp_ps + m * per + (flat ? (int64_t)c * d.sh * d.sw + pyx : o)];
+    const float v = tf32_hi(gp * (act == DASMC_RELU ? (mx > 0.f ? 1.f : 0.f) : 1.f - mx * mx));
+    float* z = dZ + j * dz_ps + m * (int64_t)H2 * W2 * C + ((int64_t)(2 * py + pad) * W2 + 2 * px + pad) * C + c;
+    const int64_t zrow = (int64_t)W2 * C;
+    z[0] = best == 0 ? v : 0.f;
+    z[C] = best == 1 ? v : 0.f;
+    z[zrow] = best == 2 ? v : 0.f;
+    z[zrow + C] = best == 3 ? v : 0.f;
+  }
+}
+
+// Last stage without a pool: NHWC output <-> the head's flatten order (c, y, x).
+__global__ void nhwc_to_flat_kernel(ConvDev d, const float* __restrict__ A, int64_t a_ps, float* __restrict__ F,
+                                    int64_t f_ps, int64_t M, int64_t J) {
+  const int C = d.cout;
+  const int64_t per = (int64_t)d.ho * d.wo * C, total = J * M * per;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / (M * per), rem = g - j * M * per, m = rem / per;
+    const int o = (int)(rem - m * per), c = o % C, yx = o / C;
+    F[j * f_ps + m * per + (int64_t)c * d.ho * d.wo + yx] = A[j * a_ps + m * per + o];
+  }
+}
+__global__ void flat_to_dzpad_kernel(ConvDev d, const float* __restrict__ F, int64_t f_ps, float* __restrict__ dZ,
+                                     int64_t dz_ps, int64_t M, int64_t J) {
+  const int C = d.cout, pad = d.k - 1, W2 = d.wo + 2 * pad, H2 = d.ho + 2 * pad;
+  const int64_t per = (int64_t)d.ho * d.wo * C, total = J * M * per;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / (M * per), rem = g - j * M * per, m = rem / per;
+    const int o = (int)(rem - m * per), c = o % C, yx = o / C, y = yx / d.wo, x = yx - y * d.wo;
+    dZ[j * dz_ps + m * (int64_t)H2 * W2 * C + ((int64_t)(y + pad) * W2 + x + pad) * C + c] =
+        tf32_hi(F[j * f_ps + m * per + (int64_t)c * d.ho * d.wo + yx]);
+  }
+}
+
+__global__ void round_tf32_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = tf32_hi(src[i]);
+}
+
+unsigned grid_of(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 32)); }
+
+int64_t pad_plane(const ConvDev& d) { return (int64_t)(d.ho + 2 * d.k - 2) * (d.wo + 2 * d.k - 2) * d.cout; }
+int64_t act_plane(const ConvDev& d) { return (int64_t)d.ho * d.wo * d.cout; }
+int64_t pool_plane(const ConvDev& d) { return (int64_t)d.sh * d.sw * d.cout; }
+int round_up(int v, int a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+// ---- per-context state ------------------------------------------------------------------------
+struct ConvTcState {
+  float* Xr = nullptr;  // tf32-rounded copy of the active X rows (stage-0 operand)
+  int64_t Xr_rows = 0;
+  float* ones = nullptr;
+  int64_t mcap = 0;  // images per chunk the buffers hold
+  int korder[kMaxConv] = {};   // 0: k = (ky, kx, ci) over NHWC input; 1: (ci, ky, kx) over X (NCHW)
+  int nmmaF[kMaxConv] = {}, KpF[kMaxConv] = {}, nmmaD[kMaxConv] = {}, KpD[kMaxConv] = {};
+  float* Wf[kMaxConv] = {};
+  float* Wd[kMaxConv] = {};
+  float* dP[kMaxConv] = {};  // delta of a pooled (non-last) stage output, NHWC
+  // tables (device, int32)
+  int* fa_row[kMaxConv] = {};  // output pixel -> input pixel base (forward A rows, weight-gradient A columns)
+  int* fa_col[kMaxConv] = {};  // forward k -> offset
+  int* wa_row[kMaxConv] = {};  // weight-gradient A rows: (ky, kx, ci) offsets + the ones row
+  int* prow[kMaxConv] = {};    // weight-gradient row -> parameter offset within W (-1: bias)
+  int* zpix[kMaxConv] = {};    // output pixel -> zero-bordered delta buffer position
+  int* da_row[kMaxConv] = {};  // delta A rows: input pixel -> dZpad base
+  int* da_col[kMaxConv] = {};  // delta k = (ky, kx, co) -> offset
+  int num_sms = 148;
+};
+
+namespace {
+
+template <typename T>
+T* upload_vec(const std::vector<T>& v) {
+  T* d = nullptr;
+  CK(cudaMalloc(&d, sizeof(T) * std::max<size_t>(v.size(), 1)));
+  CK(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return d;
+}
+
+void free_tables(ConvTcState* s) {
+  int** t[] = {s->fa_row, s->fa_col, s->wa_row, s->prow, s->zpix, s->da_row, s->da_col};
+  for (int** a : t)
+    for (int i = 0; i < kMaxConv; ++i)
+      if (a[i]) {
+        cudaFree(a[i]);
+        a[i] = nullptr;
+      }
+}
+
+// Tables of stage i for chunks of up to `mc` images (host-built, geometry only).
+void build_tables(Ctx& c, int64_t mc) {
+  ConvTcState* s = c.ctc;
+  free_tables(s);
+  const NetDev& net = c.net;
+  for (int i = 0; i < net.nconv; ++i) {
+    const ConvDev& d = net.conv[i];
+    const int k = d.k, kk2 = k * k, pad = k - 1, H2 = d.ho + 2 * pad, W2 = d.wo + 2 * pad;
+    const int64_t npix = (int64_t)d.ho * d.wo, nin = (int64_t)d.hin * d.win;
+    const bool x_nchw = i == 0;  // stage 0 reads X [c][h][w]; later stages NHWC activations
+    const int64_t limit = (int64_t)1 << 31;
+    if (mc * std::max<int64_t>(nin * d.cin, (int64_t)H2 * W2 * d.cout) >= limit)
+      throw std::invalid_argument("conv: chunk too large for 32-bit operand tables");
+    std::vector<int> fa_row((size_t)(mc * npix)), zpix((size_t)(mc * npix));
+    for (int64_t m = 0; m < mc; ++m)
+      for (int y = 0; y < d.ho; ++y)
+        for (int x = 0; x < d.wo; ++x) {
+          const int64_t r = m * npix + (int64_t)y * d.wo + x;
+          fa_row[(size_t)r] = x_nchw ? (int)(m * d.cin * nin + (int64_t)y * d.win + x)
+                                     : (int)(m * nin * d.cin + ((int64_t)y * d.win + x) * d.cin);
+          zpix[(size_t)r] = (int)(m * (int64_t)H2 * W2 * d.cout + ((int64_t)(y + pad) * W2 + x + pad) * d.cout);
+        }
+    const int Kf = d.cin * kk2;
+    std::vector<int> fa_col((size_t)Kf), wa_row((size_t)Kf + 1), prow((size_t)Kf + 1);
+    for (int q = 0; q < Kf; ++q) {
+      int ci, ky, kx;
+      if (s->korder[i] == 0) {
+        ci = q % d.cin;
+        ky = (q / d.cin) / k;
+        kx = (q / d.cin) % k;
+      } else {
+        ci = q / kk2;
+        ky = (q % kk2) / k;
+        kx = q % k;
+      }
+      const int off = x_nchw ? (int)(ci * nin + (int64_t)ky * d.win + kx) : (int)(((int64_t)ky * d.win + kx) * d.cin + ci);
+      fa_col[(size_t)q] = off;
+      wa_row[(size_t)q] = off;
+      prow[(size_t)q] = ci * kk2 + ky * k + kx;
+    }
+    wa_row[(size_t)Kf] = kOnesRow;
+    prow[(size_t)Kf] = -1;
+    s->fa_row[i] = upload_vec(fa_row);
+    s->zpix[i] = upload_vec(zpix);
+    s->fa_col[i] = upload_vec(fa_col);
+    s->wa_row[i] = upload_vec(wa_row);
+    s->prow[i] = upload_vec(prow);
+    if (i > 0) {  // delta GEMM of stage i: rows = input pixels of stage i (= stage i-1 output or pool)
+      std::vector<int> da_row((size_t)(mc * nin)), da_col((size_t)d.cout * kk2);
+      for (int64_t m = 0; m < mc; ++m)
+        for (int y = 0; y < d.hin; ++y)
+          for (int x = 0; x < d.win; ++x)
+            da_row[(size_t)(m * nin + (int64_t)y * d.win + x)] =
+                (int)(m * (int64_t)H2 * W2 * d.cout + ((int64_t)(y + pad) * W2 + x + pad) * d.cout);
+      for (int q = 0; q < d.cout * kk2; ++q) {
+        const int kyx = q / d.cout, co = q % d.cout, ky = kyx / k, kx = kyx % k;
+        da_col[(size_t)q] = -(ky * W2 + kx) * d.cout + co;
+      }
+      s->da_row[i] = upload_vec(da_row);
+      s->da_col[i] = upload_vec(da_col);
+    }
+  }
+}
+
+template <int EPI>
+void launch_gemm(Ctx& c, GParams& p, int act) {
+  const size_t stage_bytes = (size_t)kCBM * 128 + (size_t)p.nmma * 128;
+  // up to 6 stages, two CTAs per SM when they fit (more producer warps in flight per SM)
+  const size_t fixed = 1024 + 64 * 8 + 64;
+  int stages = (int)std::min<size_t>(6, (110 * 1024 - fixed) / stage_bytes);
+  if (stages < 2) stages = (int)std::min<size_t>(4, (227 * 1024 - fixed) / stage_bytes);
+  if (stages < 2) throw std::invalid_argument("conv: GEMM tile does not fit in shared memory");
+  p.stages = stages;
+  const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+  int tc = 32;
+  while (tc < p.nmma) tc <<= 1;
+  p.tcols_half = tc;
+  const int units = p.rtiles * p.J;
+  auto go = [&](auto kern) {
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr = true;
+    }
+    const int per_sm = std::max(1, std::min(2, (int)((228 * 1024) / (smem + 1024))));
+    const int grid = std::max(1, std::min(units, c.ctc->num_sms * per_sm));
+    kern<<<grid, kCThreads, smem, c.stream>>>(p);
+    LAUNCHED();
+  };
+  if (act == DASMC_RELU)
+    go(conv_tc_kernel<EPI, DASMC_RELU>);
+  else
+    go(conv_tc_kernel<EPI, DASMC_TANH>);
+}
+
+}  // namespace
+
+// ---- public entry points (conv_tc.cuh) ----------------------------------------------------------
+bool cnn_tc_eligible(const Ctx& c) {
+  const NetDev& n = c.net;
+  if (n.nconv < 1) return false;
+  for (int i = 0; i < n.nconv; ++i) {
+    const ConvDev& d = n.conv[i];
+    if (d.cout % 4 != 0 || d.cout > 256 || d.cin > 256) return false;
+    if (i > 0 && d.cin % 4 != 0) return false;
+  }
+  return true;
+}
+
+void cnn_tc_init(Ctx& c) {
+  auto* s = new ConvTcState();
+  c.ctc = s;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, dev));
+  const NetDev& net = c.net;
+  for (int i = 0; i < net.nconv; ++i) {
+    const ConvDev& d = net.conv[i];
+    s->korder[i] = (i > 0 && d.cin % 4 == 0) ? 0 : 1;
+    s->nmmaF[i] = round_up(d.cout, 16);
+    s->KpF[i] = round_up(d.cin * d.k * d.k, kCBK);
+    s->nmmaD[i] = round_up(d.cin, 16);
+    s->KpD[i] = round_up(d.cout * d.k * d.k, kCBK);
+    CK(cudaMalloc(&s->Wf[i], sizeof(float) * (size_t)c.Jmax * s->nmmaF[i] * s->KpF[i]));
+    if (i > 0) CK(cudaMalloc(&s->Wd[i], sizeof(float) * (size_t)c.Jmax * s->nmmaD[i] * s->KpD[i]));
+  }
+  const float ones[4] = {1.f, 1.f, 1.f, 1.f};
+  CK(cudaMalloc(&s->ones, sizeof(ones)));
+  CK(cudaMemcpy(s->ones, ones, sizeof(ones), cudaMemcpyHostToDevice));
+  cnn_tc_refresh_data(c, c.X, c.n_active);
+}
+
+void cnn_tc_refresh_data(Ctx& c, const float* X, int64_t rows) {
+  ConvTcState* s = c.ctc;
+  const int64_t d = (int64_t)c.net.in_c * c.net.in_h * c.net.in_w;
+  if (rows > s->Xr_rows) {
+    CK(cudaStreamSynchronize(c.stream));
+    if (s->Xr) CK(cudaFree(s->Xr));
+    s->Xr = nullptr;
+    const int64_t cap = std::max(rows, c.n);
+    CK(cudaMalloc(&s->Xr, sizeof(float) * (size_t)cap * d));
+    s->Xr_rows = cap;
+  }
+  round_tf32_kernel<<<grid_of(rows * d), 256, 0, c.stream>>>(X, s->Xr, rows * d);
+  LAUNCHED();
+}
+
+void cnn_tc_free(Ctx& c) {
+  ConvTcState* s = c.ctc;
+  if (!s) return;
+  free_tables(s);
+  for (int i = 0; i < kMaxConv; ++i) {
+    float* p[] = {s->Wf[i], s->Wd[i], s->dP[i]};
+    for (float* q : p)
+      if (q) cudaFree(q);
+  }
+  if (s->Xr) cudaFree(s->Xr);
+  if (s->ones) cudaFree(s->ones);
+  delete s;
+  c.ctc = nullptr;
+}
+
+int64_t cnn_tc_image_floats(const Ctx& c) {
+  const NetDev& net = c.net;
+  int64_t f = 0;
+  for (int i = 0; i < net.nconv; ++i) {
+    const ConvDev& d = net.conv[i];
+    f += act_plane(d) + pad_plane(d);
+    if (d.pool || i == net.nconv - 1) f += pool_plane(d) > 0 ? std::max(pool_plane(d), act_plane(d)) : 0;
+    if (d.pool && i + 1 < net.nconv) f += pool_plane(d);
+  }
+  return f;
+}
+
+// Stage buffers for chunks of mc images: cact = NHWC stage output, cpool = pooled NHWC (or the
+// head's flatten order for the last stage), cdel = zero-bordered NHWC delta, dP = delta of a
+// pooled non-last stage output.
+void cnn_tc_alloc(Ctx& c, int64_t mc) {
+  ConvTcState* s = c.ctc;
+  const NetDev& net = c.net;
+  const size_t J = (size_t)c.Jmax;
+  for (int i = 0; i < net.nconv; ++i) {
+    float** bufs[] = {&c.cact[i], &c.cpool[i], &c.cdel[i], &s->dP[i]};
+    for (float** b : bufs)
+      if (*b) {
+        CK(cudaFree(*b));
+        *b = nullptr;
+      }
+    const ConvDev& d = net.conv[i];
+    CK(cudaMalloc(&c.cact[i], sizeof(float) * J * mc * act_plane(d)));
+    CK(cudaMalloc(&c.cdel[i], sizeof(float) * J * mc * pad_plane(d)));
+    CK(cudaMemsetAsync(c.cdel[i], 0, sizeof(float) * J * mc * pad_plane(d), c.stream));
+    const bool last = i == net.nconv - 1;
+    if (d.pool || last) CK(cudaMalloc(&c.cpool[i], sizeof(float) * J * mc * (d.pool ? pool_plane(d) : act_plane(d))));
+    if (d.pool && !last) CK(cudaMalloc(&s->dP[i], sizeof(float) * J * mc * pool_plane(d)));
+  }
+  build_tables(c, mc);
+  s->mcap = mc;
+}
+
+// Flatten buffer the head reads (and its delta is written to): [Jmax][mcap][F].
+float* cnn_tc_flat(Ctx& c) { return c.cpool[c.net.nconv - 1]; }
+
+void cnn_tc_weights(Ctx& c, const float* theta, int64_t J, bool need_grad) {
+  ConvTcState* s = c.ctc;
+  const NetDev& net = c.net;
+  for (int i = 0; i < net.nconv; ++i) {
+    const ConvDev& d = net.conv[i];
+    conv_wcopy_kernel<<<grid_of(J * s->nmmaF[i] * s->KpF[i]), 256, 0, c.stream>>>(
+        theta, net.Dp, d.woff, d.cin, d.k, d.cout, 0, s->korder[i], s->nmmaF[i], s->KpF[i], J, s->Wf[i]);
+    LAUNCHED();
+    if (need_grad && i > 0) {
+      conv_wcopy_kernel<<<grid_of(J * s->nmmaD[i] * s->KpD[i]), 256, 0, c.stream>>>(
+          theta, net.Dp, d.woff, d.cin, d.k, d.cout, 1, 0, s->nmmaD[i], s->KpD[i], J, s->Wd[i]);
+      LAUNCHED();
+    }
+  }
+}
+
+void cnn_tc_forward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t mc) {
+  ConvTcState* s = c.ctc;
+  const NetDev& net = c.net;
+  const int64_t img = (int64_t)net.in_c * net.in_h * net.in_w;
+  const int64_t cap = s->mcap;
+  for (int i = 0; i < net.nconv; ++i) {
+    const ConvDev& d = net.conv[i];
+    const int64_t R = mc * d.ho * d.wo;
+    GParams p{};
+    p.a.base = i == 0 ? s->Xr + m0 * img : c.cpool[i - 1] ? c.cpool[i - 1] : c.cact[i - 1];
+    if (i > 0 && !net.conv[i - 1].pool) p.a.base = c.cact[i - 1];
+    p.a.ps = i == 0 ? 0 : cap * (net.conv[i - 1].pool ? pool_plane(net.conv[i - 1]) : act_plane(net.conv[i - 1]));
+    p.a.rowoff = s->fa_row[i];
+    p.a.nrows = (int)R;
+    p.a.coloff = s->fa_col[i];
+    p.a.K = d.cin * d.k * d.k;
+    p.a.vec = s->korder[i] == 0 ? 1 : 0;
+    p.b.base = s->Wf[i];
+    p.b.ps = (int64_t)s->nmmaF[i] * s->KpF[i];
+    p.b.ld = s->KpF[i];
+    p.b.nrows = s->nmmaF[i];
+    p.b.K = s->KpF[i];
+    p.b.vec = 1;
+    p.ones = s->ones;
+    p.J = (int)J;
+    p.rtiles = (int)((R + kCBM - 1) / kCBM);
+    p.nkb = s->KpF[i] / kCBK;
+    p.nmma = s->nmmaF[i];
+    p.Rvalid = (int)R;
+    p.nvalid = d.cout;
+    p.out = c.cact[i];
+    p.out_ps = cap * act_plane(d);
+    p.out_ld = d.cout;
+    p.theta = theta;
+    p.Dp = net.Dp;
+    p.boff = d.boff;
+    launch_gemm<kEpiConvFwd>(c, p, net.act);
+    const bool last = i == net.nconv - 1;
+    if (d.pool) {
+      pool_fwd_nhwc_kernel<<<grid_of(J * mc * pool_plane(d)), 256, 0, c.stream>>>(
+          d, c.cact[i], cap * act_plane(d), c.cpool[i], cap * pool_plane(d), mc, J, last ? 1 : 0);
+      LAUNCHED();
+    } else if (last) {
+      nhwc_to_flat_kernel<<<grid_of(J * mc * act_plane(d)), 256, 0, c.stream>>>(d, c.cact[i], cap * act_plane(d),
+                                                                                 c.cpool[i], cap * act_plane(d), mc, J);
+      LAUNCHED();
+    }
+  }
+}
+
+// Backward through the stages, given the flatten delta (head backward, act' applied unless the
+// last stage pools) in cnn_tc_flat(c); e carries the chunk's accumulation mode.
+void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t mc, const EpiParams& e) {
+  ConvTcState* s = c.ctc;
+  const NetDev& net = c.net;
+  const int64_t img = (int64_t)net.in_c * net.in_h * net.in_w;
+  const int64_t cap = s->mcap;
+  const int L = net.nconv - 1;
+  {
+    const ConvDev& d = net.conv[L];
+    if (d.pool) {
+      pool_bwd_nhwc_kernel<<<grid_of(J * mc * pool_plane(d)), 256, 0, c.stream>>>(
+          d, net.act, c.cact[L], cap * act_plane(d), c.cpool[L], cap * pool_plane(d), 1, c.cdel[L], cap * pad_plane(d),
+          mc, J);
+    } else {
+      flat_to_dzpad_kernel<<<grid_of(J * mc * act_plane(d)), 256, 0, c.stream>>>(d, c.cpool[L], cap * act_plane(d),
+                                                                                   c.cdel[L], cap * pad_plane(d), mc, J);
+    }
+    LAUNCHED();
+  }
+  for (int i = L; i >= 0; --i) {
+    const ConvDev& d = net.conv[i];
+    const int64_t R = mc * d.ho * d.wo;
+    // ---- weight gradient + fused leapfrog: dW[(ky,kx,ci) | bias, co] = sum_r In[., r] dZ[co, r]
+    {
+      GParams p{};
+      const bool x_in = i == 0;
+      p.a.base = x_in ? s->Xr + m0 * img : (net.conv[i - 1].pool ? c.cpool[i - 1] : c.cact[i - 1]);
+      p.a.ps = x_in ? 0 : cap * (net.conv[i - 1].pool ? pool_plane(net.conv[i - 1]) : act_plane(net.conv[i - 1]));
+      p.a.rowoff = s->wa_row[i];
+      p.a.nrows = d.cin * d.k * d.k + 1;
+      p.a.coloff = s->fa_row[i];
+      p.a.K = (int)R;
+      p.a.vec = 0;
+      p.b.base = c.cdel[i];
+      p.b.ps = cap * pad_plane(d);
+      p.b.ld = 1;
+      p.b.nrows = d.cout;
+      p.b.coloff = s->zpix[i];
+      p.b.K = (int)R;
+      p.b.vec = 0;
+      p.ones = s->ones;
+      p.J = (int)J;
+      p.rtiles = (p.a.nrows + kCBM - 1) / kCBM;
+      p.nkb = (int)((R + kCBK - 1) / kCBK);
+      p.nmma = s->nmmaF[i];
+      p.nvalid = d.cout;
+      p.Dp = net.Dp;
+      p.boff = d.boff;
+      p.e = e;
+      p.woff = d.woff;
+      p.Kw = d.cin * d.k * d.k;
+      p.nrows_w = p.a.nrows;
+      p.prow = s->prow[i];
+      launch_gemm<kEpiConvDw>(c, p, net.act);
+    }
+    if (i == 0) break;
+    // ---- delta of the stage input: dI[r_in, ci] = sum_(ky,kx,co) dZpad[.] W[co, ci, ky, kx]
+    const ConvDev& dp = net.conv[i - 1];
+    const int64_t Rin = mc * d.hin * d.win;
+    GParams p{};
+    p.a.base = c.cdel[i];
+    p.a.ps = cap * pad_plane(d);
+    p.a.rowoff = s->da_row[i];
+    p.a.nrows = (int)Rin;
+    p.a.coloff = s->da_col[i];
+    p.a.K = d.cout * d.k * d.k;
+    p.a.vec = 1;
+    p.b.base = s->Wd[i];
+    p.b.ps = (int64_t)s->nmmaD[i] * s->KpD[i];
+    p.b.ld = s->KpD[i];
+    p.b.nrows = s->nmmaD[i];
+    p.b.K = s->KpD[i];
+    p.b.vec = 1;
+    p.ones = s->ones;
+    p.J = (int)J;
+    p.rtiles = (int)((Rin + kCBM - 1) / kCBM);
+    p.nkb = s->KpD[i] / kCBK;
+    p.nmma = s->nmmaD[i];
+    p.Rvalid = (int)Rin;
+    p.nvalid = d.cin;
+    if (dp.pool) {  // delta of the pooled output (NHWC); its max-pool backward follows
+      p.out = s->dP[i - 1];
+      p.out_ps = cap * pool_plane(dp);
+      p.out_ld = dp.cout;
+    } else {  // pre-activation delta of stage i-1: act'(a_{i-1}), into its zero-bordered buffer
+      p.out = c.cdel[i - 1];
+      p.out_ps = cap * pad_plane(dp);
+      p.outoff = s->zpix[i - 1];
+      p.mask = c.cact[i - 1];
+      p.mask_ps = cap * act_plane(dp);
+      p.mask_ld = dp.cout;
+    }
+    launch_gemm<kEpiConvDx>(c, p, net.act);
+    if (dp.pool) {
+      pool_bwd_nhwc_kernel<<<grid_of(J * mc * pool_plane(dp)), 256, 0, c.stream>>>(
+          dp, net.act, c.cact[i - 1], cap * act_plane(dp), s->dP[i - 1], cap * pool_plane(dp), 0, c.cdel[i - 1],
+          cap * pad_plane(dp), mc, J);
+      LAUNCHED();
+    }
+  }
+}
+
+}  // namespace dasmc_b200

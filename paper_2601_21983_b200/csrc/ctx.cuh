@@ -103,6 +103,12 @@ struct EpiParams {
   int* flags;            // [J] divergence flags
   int slots;             // slots per particle
   float* grad_cache;     // kEpiLast: also store the final-position gradient (start-gradient cache)
+  // window evaluated in row chunks (CNN stages, memory independent of M): the data gradient
+  // is summed over the chunks in order in gacc[J][Dp] (fp32) before the move.
+  // acc_mode 0: one chunk (apply directly); 1: first chunk (store); 2: middle (add);
+  // 3: last chunk (add, then apply)
+  int acc_mode;
+  float* gacc;
 };
 
 struct Ctx {
@@ -221,6 +227,10 @@ struct Ctx {
 
   // tensor-core path state (tc_gemm.cu), null on the fp32 CUDA-core path
   struct TcState* tc = nullptr;
+  // [EXT] CNN stages on the tensor cores (conv_tc.cu), null on the fp32 CUDA-core path
+  struct ConvTcState* ctc = nullptr;
+  float* gacc = nullptr;  // [Jmax][Dp] data-gradient sums across window chunks (EpiParams::acc_mode)
+  int64_t cnn_ll_slots = 0;
 
   // kernel-range timers
   bool ktime = false;

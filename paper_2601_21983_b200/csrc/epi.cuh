@@ -14,7 +14,23 @@
 
 namespace dasmc_b200 {
 
+// Chunked windows (EpiParams::acc_mode): true when `acc` now holds the whole window's sum.
+__device__ __forceinline__ bool grad_accumulate(const EpiParams& e, int64_t idx, float& acc) {
+  if (e.acc_mode == 0) return true;
+  if (e.acc_mode == 1) {
+    e.gacc[idx] = acc;
+    return false;
+  }
+  if (e.acc_mode == 2) {
+    e.gacc[idx] += acc;
+    return false;
+  }
+  acc = e.gacc[idx] + acc;
+  return true;
+}
+
 __device__ __forceinline__ void leapfrog_update(const EpiParams& e, int j, int64_t idx, float acc) {
+  if (!grad_accumulate(e, idx, acc)) return;
   const float th = e.theta_in[idx];
   const float g = fmaf(e.scale, acc, -th * e.inv_var);
   bool bad = !isfinite(g);
@@ -40,8 +56,18 @@ __device__ __forceinline__ void leapfrog_update(const EpiParams& e, int j, int64
 // issued before any store, so the chunk's 2N loads are in flight together instead of
 // one dependent round trip per parameter (short-K GEMMs are epilogue-latency bound).
 template <int N>
-__device__ __forceinline__ void leapfrog_update_n(const EpiParams& e, int j, const int64_t* idx, const float* acc,
+__device__ __forceinline__ void leapfrog_update_n(const EpiParams& e, int j, const int64_t* idx, const float* acc_in,
                                                   int count) {
+  float acc[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q) acc[q] = acc_in[q];
+  if (e.acc_mode != 0) {
+    bool apply = true;
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+      if (q < count) apply = grad_accumulate(e, idx[q], acc[q]);
+    if (!apply) return;
+  }
   float th[N], p[N];
 #pragma unroll
   for (int q = 0; q < N; ++q)

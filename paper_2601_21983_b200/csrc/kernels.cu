@@ -8,6 +8,7 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <cstdio>
 #include <stdexcept>
@@ -16,6 +17,7 @@
 #include "epi.cuh"
 #include "host.h"
 #include "tc_gemm.cuh"
+#include "conv_tc.cuh"
 
 namespace dasmc_b200 {
 
@@ -1091,17 +1093,69 @@ int64_t conv_out_floats(const ConvDev& d) { return (int64_t)d.cout * d.sh * d.sw
 int64_t conv_act_floats(const ConvDev& d) { return (int64_t)d.cout * d.ho * d.wo; }
 float* stage_out(Ctx& c, int i) { return c.net.conv[i].pool ? c.cpool[i] : c.cact[i]; }
 
-// CNN gradient evaluation: conv stages -> flatten -> the SIMT MLP head (layer 1 reads
-// the last stage output) -> head backward incl. the flatten delta -> conv stages backward.
-void launch_eval_cnn(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, double beta_rows, bool need_grad,
-                     const EpiParams* epi) {
+// MLP head of a CNN chunk (network.hpp:159-219 with layer 1 reading the flatten `flat`,
+// [J][Mcap][F]): forward, log-softmax / ll partials into the chunk's slots, and, with a
+// gradient, the head's weight gradients (+ the leapfrog / chunk accumulation of e) and the
+// flatten delta in place over `flat` (act' only if the last stage does not pool).  logits_out
+// (optional, [J][R][C]) receives the chunk's logits rows m0 .. m0+mc.
+void cnn_head(Ctx& c, const float* theta_in, int64_t J, int64_t m0, int64_t mc, int64_t P, double beta_rows,
+              bool need_grad, const EpiParams* e, float* flat, float* logits_out, int64_t R_out) {
   const NetDev& net = c.net;
-  const int L = net.L, nc = net.nconv;
+  const int L = net.L;
+  const int64_t F = net.sizes[0];
+  for (int l = 1; l <= L; ++l) {
+    const LayerDev& ly = net.layer[l - 1];
+    EpiFwd ef{c.act[l], ly.out, c.Mcap * ly.out, theta_in, net.Dp, ly.boff, ly.hidden, net.act};
+    const float* A = l == 1 ? flat : c.act[l - 1];
+    const int64_t sA = l == 1 ? c.Mcap * F : c.Mcap * ly.in;
+    sgemm<true, true>(c.stream, (int)mc, ly.out, ly.in, A, ly.in, sA, theta_in + ly.woff, ly.in, net.Dp, -1, J, ef);
+  }
+  const int C = net.sizes[L];
+  if (logits_out)
+    CK(cudaMemcpy2DAsync(logits_out + m0 * C, sizeof(float) * R_out * C, c.act[L], sizeof(float) * c.Mcap * C,
+                         sizeof(float) * mc * C, (size_t)J, cudaMemcpyDeviceToDevice, c.stream));
+  {
+    // the chunk's rows are window rows m0 .. m0+mc (m0 a multiple of 128: slot offset m0 / 128)
+    dim3 grid((unsigned)((mc + kRowsPerBlock - 1) / kRowsPerBlock), (unsigned)J);
+    softmax_kernel<<<grid, kRowsPerBlock, 0, c.stream>>>(c.act[L], c.Mcap * C, C, c.y + m0, mc, P - m0,
+                                                         (float)beta_rows, need_grad ? 1 : 0,
+                                                         c.ll_part + 2 * (m0 / kRowsPerBlock), c.ll_slots);
+    LAUNCHED();
+  }
+  if (!need_grad) return;
+  for (int l = L; l >= 1; --l) {
+    const LayerDev& ly = net.layer[l - 1];
+    {
+      EpiDw ew{*e, net.Dp, ly.woff, ly.boff, ly.in};
+      const float* Bp = l == 1 ? flat : c.act[l - 1];
+      const int64_t sB = l == 1 ? c.Mcap * F : c.Mcap * ly.in;
+      sgemm<false, false>(c.stream, ly.out, ly.in + 1, (int)mc, c.act[l], ly.out, c.Mcap * ly.out, Bp, ly.in, sB,
+                          ly.in, J, ew);
+    }
+    // delta_{l-1} in place over a_{l-1}; for l = 1 over the flatten (act' only if the
+    // last stage does not pool)
+    float* Dst = l > 1 ? c.act[l - 1] : flat;
+    const int64_t ldd = l > 1 ? net.layer[l - 2].out : F;
+    const int act = l > 1 || !net.conv[net.nconv - 1].pool ? net.act : -1;
+    EpiDx ed{Dst, ldd, c.Mcap * ldd, act};
+    sgemm<true, false>(c.stream, (int)mc, ly.in, ly.out, c.act[l], ly.out, c.Mcap * ly.out, theta_in + ly.woff, ly.in,
+                       net.Dp, -1, J, ed);
+  }
+}
+
+// fp32 CUDA-core stages (the 1e-4 parity path) for window rows m0 .. m0+mc; NCHW stage
+// buffers [Jmax][Mcap][per-image floats].
+void cnn_chunk_simt(Ctx& c, const float* theta_in, int64_t J, int64_t m0, int64_t M, int64_t P, double beta_rows,
+                    bool need_grad, const EpiParams* epi, float* logits_out, int64_t R_out) {
+  const NetDev& net = c.net;
+  const int nc = net.nconv;
+  const int64_t img = (int64_t)net.in_c * net.in_h * net.in_w;
+  const float* X0 = c.X + m0 * img;
   auto grid_of = [](int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32); };
   // forward through the stages
   for (int i = 0; i < nc; ++i) {
     const ConvDev& d = net.conv[i];
-    const float* in = i == 0 ? c.X : stage_out(c, i - 1);
+    const float* in = i == 0 ? X0 : stage_out(c, i - 1);
     const int64_t in_ps = i == 0 ? 0 : c.Mcap * conv_out_floats(net.conv[i - 1]);
     dispatch_k(d.k, [&](auto kc) {
       constexpr int K = decltype(kc)::value, CT = 16;
@@ -1119,41 +1173,8 @@ void launch_eval_cnn(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_
     }
   }
   float* flat = stage_out(c, nc - 1);
-  const int64_t F = net.sizes[0];
-  // MLP head (network.hpp:159-178 with layer 1 reading the flatten)
-  for (int l = 1; l <= L; ++l) {
-    const LayerDev& ly = net.layer[l - 1];
-    EpiFwd e{c.act[l], ly.out, c.Mcap * ly.out, theta_in, net.Dp, ly.boff, ly.hidden, net.act};
-    const float* A = l == 1 ? flat : c.act[l - 1];
-    const int64_t sA = l == 1 ? c.Mcap * F : c.Mcap * ly.in;
-    sgemm<true, true>(c.stream, (int)M, ly.out, ly.in, A, ly.in, sA, theta_in + ly.woff, ly.in, net.Dp, -1, J, e);
-  }
-  {
-    const int C = net.sizes[L];
-    dim3 grid((unsigned)((M + kRowsPerBlock - 1) / kRowsPerBlock), (unsigned)J);
-    softmax_kernel<<<grid, kRowsPerBlock, 0, c.stream>>>(c.act[L], c.Mcap * C, C, c.y, M, P, (float)beta_rows,
-                                                         need_grad ? 1 : 0, c.ll_part, c.ll_slots);
-    LAUNCHED();
-  }
+  cnn_head(c, theta_in, J, m0, M, P, beta_rows, need_grad, epi, flat, logits_out, R_out);
   if (!need_grad) return;
-  for (int l = L; l >= 1; --l) {
-    const LayerDev& ly = net.layer[l - 1];
-    {
-      EpiDw e{*epi, net.Dp, ly.woff, ly.boff, ly.in};
-      const float* Bp = l == 1 ? flat : c.act[l - 1];
-      const int64_t sB = l == 1 ? c.Mcap * F : c.Mcap * ly.in;
-      sgemm<false, false>(c.stream, ly.out, ly.in + 1, (int)M, c.act[l], ly.out, c.Mcap * ly.out, Bp, ly.in, sB,
-                          ly.in, J, e);
-    }
-    // delta_{l-1} in place over a_{l-1}; for l = 1 over the flatten (act' only if the
-    // last stage does not pool)
-    float* Dst = l > 1 ? c.act[l - 1] : flat;
-    const int64_t ldd = l > 1 ? net.layer[l - 2].out : F;
-    const int act = l > 1 || !net.conv[nc - 1].pool ? net.act : -1;
-    EpiDx d{Dst, ldd, c.Mcap * ldd, act};
-    sgemm<true, false>(c.stream, (int)M, ly.in, ly.out, c.act[l], ly.out, c.Mcap * ly.out, theta_in + ly.woff,
-                       ly.in, net.Dp, -1, J, d);
-  }
   // conv stages backward
   for (int i = nc - 1; i >= 0; --i) {
     const ConvDev& d = net.conv[i];
@@ -1166,7 +1187,7 @@ void launch_eval_cnn(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_
           d, net.act, c.cact[i], a_ps, c.cpool[i], c.Mcap * conv_out_floats(d), dz, M, J);
       LAUNCHED();
     }
-    const float* in = i == 0 ? c.X : stage_out(c, i - 1);
+    const float* in = i == 0 ? X0 : stage_out(c, i - 1);
     const int64_t in_ps = i == 0 ? 0 : c.Mcap * conv_out_floats(net.conv[i - 1]);
     {
       const int nchunks = (int)((M + kImgChunk - 1) / kImgChunk);
@@ -1206,6 +1227,100 @@ void launch_eval_cnn(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_
                                             stage_out(c, i - 1), c.Mcap * conv_out_floats(dp));
         LAUNCHED();
       });
+    }
+  }
+}
+
+// Window chunk (images) for a window of M rows: M itself when the chunk buffers for J = Jmax
+// fit kCnnBudget, else the largest multiple of 128 that does.  A pure function of (M, net,
+// Jmax, precision): the chunk split -- and with it the fp32 order of the cross-chunk gradient
+// sums -- never depends on earlier calls.  DASMC_CNN_CHUNK (tests) caps it.
+constexpr double kCnnBudget = 48e9;
+int64_t cnn_image_floats(const Ctx& c) {
+  const NetDev& net = c.net;
+  int64_t f = 0;
+  for (int l = 1; l <= net.L; ++l) f += net.sizes[l];
+  if (c.ctc) return f + cnn_tc_image_floats(c);
+  for (int i = 0; i < net.nconv; ++i) {
+    const ConvDev& d = net.conv[i];
+    f += conv_act_floats(d);
+    if (d.pool) f += conv_out_floats(d) + conv_act_floats(d);
+  }
+  return f;
+}
+int64_t cnn_chunk_images(const Ctx& c, int64_t M) {
+  int64_t cap = (int64_t)(kCnnBudget / (4.0 * (double)c.Jmax * (double)cnn_image_floats(c)));
+  if (!c.ctc) cap = std::min<int64_t>(cap, 16 * 65535 / c.Jmax);  // conv_dw grid.z = J * ceil(rows / 16)
+  if (const char* e = std::getenv("DASMC_CNN_CHUNK")) cap = std::min<int64_t>(cap, std::atoll(e));
+  cap = cap / kRowsPerBlock * kRowsPerBlock;
+  if (cap < kRowsPerBlock) throw std::invalid_argument("CNN: max_particles too large for the chunked stage buffers");
+  return M <= cap ? M : cap;
+}
+
+void cnn_ensure(Ctx& c, int64_t M) {
+  const int64_t slots = (M + kRowsPerBlock - 1) / kRowsPerBlock;
+  if (slots > c.ll_slots) {
+    CK(cudaStreamSynchronize(c.stream));
+    if (c.ll_part) CK(cudaFree(c.ll_part));
+    c.ll_part = nullptr;
+    CK(cudaMalloc(&c.ll_part, sizeof(double) * 2 * (size_t)c.Jmax * slots));
+    c.ll_slots = (int)slots;
+  }
+  const int64_t need = (cnn_chunk_images(c, M) + kRowsPerBlock - 1) / kRowsPerBlock * kRowsPerBlock;
+  if (need <= c.Mcap) return;
+  CK(cudaStreamSynchronize(c.stream));
+  for (int l = 1; l <= c.net.L; ++l) {
+    if (c.act[l]) CK(cudaFree(c.act[l]));
+    c.act[l] = nullptr;
+    CK(cudaMalloc(&c.act[l], sizeof(float) * (size_t)c.Jmax * need * c.net.sizes[l]));
+  }
+  if (c.ctc) {
+    cnn_tc_alloc(c, need);
+  } else {
+    for (int i = 0; i < c.net.nconv; ++i) {
+      float** bufs[] = {&c.cact[i], &c.cpool[i], &c.cdel[i]};
+      for (float** b : bufs)
+        if (*b) {
+          CK(cudaFree(*b));
+          *b = nullptr;
+        }
+      const ConvDev& d = c.net.conv[i];
+      CK(cudaMalloc(&c.cact[i], sizeof(float) * (size_t)c.Jmax * need * conv_act_floats(d)));
+      if (d.pool) {
+        CK(cudaMalloc(&c.cpool[i], sizeof(float) * (size_t)c.Jmax * need * conv_out_floats(d)));
+        CK(cudaMalloc(&c.cdel[i], sizeof(float) * (size_t)c.Jmax * need * conv_act_floats(d)));
+      }
+    }
+  }
+  c.Mcap = need;
+}
+
+// CNN gradient evaluation over window rows [0, M) in chunks of cnn_chunk_images(M) images:
+// conv stages -> flatten -> the SIMT MLP head -> head backward -> conv stages backward, per
+// chunk; the weight gradients are summed across chunks in order (EpiParams::acc_mode) before
+// the fused leapfrog.  Stage bodies: tcgen05 implicit GEMMs (conv_tc.cu) when the context's
+// precision is a tensor-core one, else the fp32 CUDA-core kernels.
+void launch_eval_cnn(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P, double beta_rows, bool need_grad,
+                     const EpiParams* epi, float* logits_out = nullptr) {
+  cnn_ensure(c, M);
+  const int64_t Mc = cnn_chunk_images(c, M);
+  const int nch = (int)((M + Mc - 1) / Mc);
+  if (nch > 1 && need_grad && !c.gacc) CK(cudaMalloc(&c.gacc, sizeof(float) * (size_t)c.Jmax * c.net.Dp));
+  if (c.ctc) cnn_tc_weights(c, theta_in, J, need_grad);
+  for (int ch = 0; ch < nch; ++ch) {
+    const int64_t m0 = ch * Mc, mc = std::min(Mc, M - m0);
+    EpiParams e{};
+    if (need_grad) {
+      e = *epi;
+      e.acc_mode = nch == 1 ? 0 : ch == 0 ? 1 : ch + 1 < nch ? 2 : 3;
+      e.gacc = c.gacc;
+    }
+    if (c.ctc) {
+      cnn_tc_forward(c, theta_in, J, m0, mc);
+      cnn_head(c, theta_in, J, m0, mc, P, beta_rows, need_grad, &e, cnn_tc_flat(c), logits_out, M);
+      if (need_grad) cnn_tc_backward(c, theta_in, J, m0, mc, e);
+    } else {
+      cnn_chunk_simt(c, theta_in, J, m0, mc, P, beta_rows, need_grad, &e, logits_out, M);
     }
   }
 }
@@ -1253,14 +1368,11 @@ void launch_forward_logits(Ctx& c, const float* theta, int64_t J, const float* X
     const int32_t* y0 = c.y;
     c.X = const_cast<float*>(Xd);
     c.y = const_cast<int32_t*>(yd);
-    ensure_activation_capacity(c, R);
-    launch_eval_cnn(c, theta, J, R, R, 1.0, false, nullptr);
+    if (c.ctc) cnn_tc_refresh_data(c, Xd, R);  // the stage-0 operand copy of the test rows
+    launch_eval_cnn(c, theta, J, R, R, 1.0, false, nullptr, logits);
     c.X = const_cast<float*>(X0);
     c.y = const_cast<int32_t*>(y0);
-    // act[L] [J][Mcap][C] -> logits [J][R][C]
-    const int C = net.sizes[net.L];
-    CK(cudaMemcpy2DAsync(logits, sizeof(float) * R * C, c.act[net.L], sizeof(float) * c.Mcap * C,
-                         sizeof(float) * R * C, (size_t)J, cudaMemcpyDeviceToDevice, c.stream));
+    if (c.ctc) cnn_tc_refresh_data(c, c.X, c.n_active);
     return;
   }
   const float* A = Xd;
@@ -1282,6 +1394,10 @@ void launch_predictive_mix(Ctx& c, const float* logits, int64_t R, int64_t J, co
 }
 
 void ensure_activation_capacity(Ctx& c, int64_t M) {
+  if (c.net.nconv > 0) {
+    cnn_ensure(c, M);
+    return;
+  }
   if (M <= c.Mcap) return;
   CK(cudaStreamSynchronize(c.stream));
   const int64_t Mnew = ((M + 127) / 128) * 128;
