@@ -39,9 +39,10 @@ WORKLOADS = {
                     "MB=1000 (+1 MB every 5 iterations, 300 iterations), HMC S=3 h=0.002, prior N(0,1)"),
     # BASELINE.json configs[2]: CNN, SDA annealing; measured at a constant window of MB rows
     "c3": dict(layers=[512, 10], conv=((1, 28, 28), [(5, 16, True), (5, 32, True)]), act="relu", n=60000, J=512,
-               feature_kind=1, mb=500, const_window=True, K=200, S=3, h=0.002, k0=0, cfg_id=3, cpu_rows=48,
+               feature_kind=1, mb=500, sda=True, K=200, S=3, h=0.002, k0=0, cfg_id=3, cpu_rows=48,
                desc="C3: CNN conv5x5x16-ReLU-pool-conv5x5x32-ReLU-pool-FC512-10 on 28x28x1 k/255 teacher-labelled, "
-                    "J=512, window M=500 (one MB), HMC S=3 h=0.002"),
+                    "J=512, MB=500, adaptive (SDA) annealing from the first MB (beta0=0.1, entropy step 1), "
+                    "HMC S=3 h=0.002"),
     # BASELINE.json configs[3]: CNN on 32x32x3, constant-to-refine phase window
     "c4": dict(layers=[1600, 256, 10], conv=((3, 32, 32), [(3, 32, False), (3, 32, True), (3, 64, False),
                                                            (3, 64, True)]),
@@ -49,6 +50,13 @@ WORKLOADS = {
                cfg_id=4, cpu_rows=6,
                desc="C4: CNN conv3x3x32-conv3x3x32-pool-conv3x3x64-conv3x3x64-pool-FC256-10 (valid, ReLU) on 32x32x3 "
                     "U{0..255}/255, J=256, window M=500 (the CTR phase), HMC S=3 h=0.002"),
+    # BASELINE.json configs[3]: the full-batch run (window = all 50000 images)
+    "c4fb": dict(layers=[1600, 256, 10], conv=((3, 32, 32), [(3, 32, False), (3, 32, True), (3, 64, False),
+                                                             (3, 64, True)]),
+                 act="relu", n=50000, J=256, feature_kind=1, mb=50000, const_window=True, K=200, S=3, h=0.002, k0=0,
+                 cfg_id=4, cpu_rows=6,
+                 desc="C4: CNN conv3x3x32-conv3x3x32-pool-conv3x3x64-conv3x3x64-pool-FC256-10 (valid, ReLU) on "
+                      "32x32x3 U{0..255}/255, J=256, full-batch window M=50000, HMC S=3 h=0.002"),
     # BASELINE.json configs[4] at J=1024 per GPU (the scaling sweep's per-GPU unit)
     "c5": dict(layers=[3072, 512, 512, 10], act="relu", n=50000, J=1024, feature_kind=0, mb=1000, const_window=True,
                K=100, S=3, h=0.002, k0=0, cfg_id=5,
@@ -271,9 +279,28 @@ def run_ours(args, w):
     k0 = w["k0"]
     ks_warm = [k0 + i for i in range(args.warmup)]
     ks = [k0 + args.warmup + i for i in range(args.steps)]
-    Ms = [window(w, k) for k in ks]
-    L.check(lib.dasmc_gpu_reserve_rows(t.h, max(window(w, k) for k in ks_warm + ks + [k0])))
-    t.set_target(0, window(w, k0), N, "scaled", 1.0, 1.0)
+    sda = bool(w.get("sda"))
+    if sda:  # adaptive annealing (annealing.hpp:84-208): the window grows when the trigger fires
+        sched = p.ScheduleConfig("sda", w["mb"], w["mb"], w["K"], N)
+        st = [p.sda_init(sched, 0.1, 1.0)]
+        # CNN windows are chunked: reserving n rows sizes the log-likelihood slots only
+        L.check(lib.dasmc_gpu_reserve_rows(t.h, N))
+    else:
+        L.check(lib.dasmc_gpu_reserve_rows(t.h, max(window(w, k) for k in ks_warm + ks + [k0])))
+
+    def target_of(k):
+        if sda:
+            s_ = st[0]
+            return s_.prefix_end, s_.block_end, "sda", s_.beta
+        return 0, window(w, k), "scaled", 1.0
+
+    def advance():  # sda_advance on the post-step ensemble (runner.hpp:589-592)
+        if sda and not st[0].terminal:
+            s_ = st[0]
+            st[0] = p.sda_advance_with(sched, s_, t.sda_moments(s_.prefix_end, s_.block_end))
+
+    P0, M0, mode0, beta0 = target_of(k0)
+    t.set_target(P0, M0, N, mode0, beta0, 1.0)
     # world > 1: one particle-sharded ensemble of J_total = J * world (weak scaling,
     # paper_2601_21983_b200/dist.py); this rank owns global slots [j0, j0 + J)
     J_total = J * world
@@ -284,17 +311,23 @@ def run_ours(args, w):
     kc = p.KernelConfig.hmc(w["h"], S)
     rk = args.resample
     sharded_recs = []
+    Ms = []
     if world > 1:
         from paper_2601_21983_b200.dist import GpuShardEngine, TorchComm, sharded_step
         engine, comm = GpuShardEngine(t), TorchComm(torch.device("cuda", local))
 
         def step(k, sync=False):
-            t.set_target(0, window(w, k), N, "scaled", 1.0, 1.0)
+            Pk, Mk, mode, beta = target_of(k)
+            t.set_target(Pk, Mk, N, mode, beta, 1.0)
+            Ms.append(Mk)
             sharded_recs.append(sharded_step(engine, comm, J_total, kc, 0, rk, 0.5, False, torch.device("cuda", local)))
     else:
         def step(k, sync=False):
-            t.set_target(0, window(w, k), N, "scaled", 1.0, 1.0)
+            Pk, Mk, mode, beta = target_of(k)
+            t.set_target(Pk, Mk, N, mode, beta, 1.0)
+            Ms.append(Mk)
             t.smc_step(kc, 0, rk, 0.5, sync=sync)
+            advance()
     for k in ks_warm:
         step(k)
     if world == 1:
@@ -306,6 +339,7 @@ def run_ours(args, w):
         dist.barrier()
     torch.cuda.synchronize()
     sharded_recs.clear()
+    Ms.clear()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
@@ -334,6 +368,7 @@ def run_ours(args, w):
     value = units_all / (ms_max / 1e3)
 
     # ---- e2e through the C-ABI with host (pinned) buffers, copies inside the timed region
+    Ms_timed = list(Ms)
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     th_h = torch.empty((J, D), dtype=torch.float32, pin_memory=True).numpy()
     lw_h = torch.empty(J, dtype=torch.float64, pin_memory=True).numpy()
@@ -349,8 +384,9 @@ def run_ours(args, w):
         t.set_ensemble(th_h, lw_h, k)  # H2D: theta (fp32, reference layout) + log-weights
         step(k, sync=True)
         L.check(lib.dasmc_gpu_get_ensemble_f32(t.h, th_h.ctypes.data_as(L._F), lw_h.ctypes.data_as(L._D), None))
-        e2e_units += J * (S + 1) * window(w, k)
+        e2e_units += J * (S + 1) * Ms[-1]
     e2e_s = time.perf_counter() - t0
+    Ms[:] = Ms_timed
     if dist:
         tt = torch.tensor([e2e_s, e2e_units], device="cuda", dtype=torch.float64)
         mx = tt.clone()
@@ -370,7 +406,9 @@ def run_ours(args, w):
     if kt_ms <= 0 or "conv" in w:
         # no per-GEMM timers on this path (CNN stages): the whole gradient evaluation
         fl = sum(float(algorithmic_flops_per_row(w["layers"], w.get("conv"))) * M * J * (S + 1) for M in Ms)
-        name, kt_ms, kc_n = "whole gradient evaluation (CNN stages + MLP head, SIMT fp32)", kms[2], kcnt[2]
+        name, kt_ms, kc_n = ("whole gradient evaluation (CNN stages on tcgen05 tf32 implicit GEMMs + CUDA-core head)"
+                             if args.precision != "fp32" else
+                             "whole gradient evaluation (CNN stages + MLP head, SIMT fp32)"), kms[2], kcnt[2]
     peaks = load_peaks()
     if args.precision == "fp32":
         peak = 148 * 128 * 2 * 1.965e9 / 1e12
@@ -455,8 +493,8 @@ def main():
         deep = "conv" not in w and len(w["layers"]) > 3 and w["layers"][-1] <= 16
         # one hidden layer: f16x2 (fp16 X times [W1, b1] split into fp16 hi + lo; the most accurate
         # tensor-core mode within ~3 % of the fastest at the benched window:
-        # tests/test_gpu_bench_window.py); deep MLPs: tf32 chain; CNNs: fp32
-        args.precision = "f16x2" if tc1 else "tf32" if deep else "fp32"
+        # tests/test_gpu_bench_window.py)
+        args.precision = "f16x2" if tc1 else "tf32"  # deep MLPs: tf32 chain; CNNs: tf32 conv stages
     if args.impl == "reference":
         run_reference(args, w)
     else:

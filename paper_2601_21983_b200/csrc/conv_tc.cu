@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <stdexcept>
+#include <type_traits>
 #include <vector>
 
 #include "conv_tc.cuh"
@@ -554,8 +555,10 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
   while (tc < p.nmma) tc <<= 1;
   p.tcols_half = tc;
   const int units = p.rtiles * p.J;
-  auto go = [&](auto kern) {
-    static bool attr = false;
+  auto go = [&](auto act_c) {
+    constexpr int A_ = decltype(act_c)::value;
+    auto kern = conv_tc_kernel<EPI, A_>;
+    static bool attr = false;  // one flag per (EPI, ACT) instantiation
     if (!attr) {
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       attr = true;
@@ -566,9 +569,9 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
     LAUNCHED();
   };
   if (act == DASMC_RELU)
-    go(conv_tc_kernel<EPI, DASMC_RELU>);
+    go(std::integral_constant<int, DASMC_RELU>{});
   else
-    go(conv_tc_kernel<EPI, DASMC_TANH>);
+    go(std::integral_constant<int, DASMC_TANH>{});
 }
 
 }  // namespace
