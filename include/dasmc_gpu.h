@@ -328,6 +328,22 @@ int64_t dasmc_gpu_row_floats(const dasmc_ctx* ctx);
 int dasmc_gpu_pack_rows(dasmc_ctx* ctx, const int32_t* rows, int64_t n, float* dst_dev);
 int dasmc_gpu_unpack_rows(dasmc_ctx* ctx, const float* src_dev, const int32_t* slots, int64_t n);
 
+/* ---- single-process multi-GPU group --------------------------------------
+ * One ensemble of up to max_particles particles sharded over ndev shard contexts, shard r on
+ * devices[r] owning global slots [r*J/G, (r+1)*J/G) (parallel.hpp:30-31).  The returned
+ * handle is used with the SAME hot-path entry points as a single context: set_target,
+ * init_ensemble, set/get_ensemble(_f32), smc_step, sync_records, sda_moments, reserve_rows,
+ * stream / timing (lead shard), destroy.  smc_step runs every shard's propose + reweight,
+ * all-gathers the log-weights and log targets into every shard (peer copies over NVLink),
+ * computes the same normalise / ESS / resampling indices redundantly on every shard, and
+ * migrates resampled rows with a gather kernel that reads the owners' memory directly (P2P
+ * loads, no host plan).  RNG streams are keyed by the GLOBAL slot, so results are identical
+ * to one context for any G.  Devices may repeat (shards sharing a GPU: the in-process
+ * emulation used by the single-GPU tests).  Other entry points return DASMC_EINVAL. */
+int dasmc_gpu_create_multi(const dasmc_net_desc* net, const float* X, const int32_t* y, int64_t n,
+                           int max_particles, const int* devices, int ndev, int precision, dasmc_ctx** out);
+int dasmc_gpu_multi_shards(const dasmc_ctx* ctx); /* G (1 for a single context) */
+
 /* ---- instrumentation (bench.py) ------------------------------------------------------ */
 /* The context's CUDA stream (cudaStream_t) -- every kernel of the context runs on it. */
 void* dasmc_gpu_stream(dasmc_ctx* ctx);

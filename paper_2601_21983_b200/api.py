@@ -222,7 +222,9 @@ class GpuEnsembleTarget:
     and the ensemble loop of ``smc_step`` (smc.hpp:109-158)."""
 
     def __init__(self, spec: NetSpec, X: np.ndarray, y: np.ndarray, max_particles: int, device: int = 0,
-                 precision: str = "fp32", lib_path: str | None = None):
+                 precision: str = "fp32", lib_path: str | None = None, devices: Optional[Sequence[int]] = None):
+        """devices: a single-process multi-GPU group (dasmc_gpu_create_multi): the ensemble is
+        sharded over one shard context per listed device (devices may repeat)."""
         self.lib = L.load(lib_path) if lib_path else L.load()
         self.spec = spec
         self.D = param_count(spec)
@@ -231,8 +233,13 @@ class GpuEnsembleTarget:
         self.n = X.shape[0]
         d = spec.desc()
         h = C.c_void_p()
-        L.check(self.lib.dasmc_gpu_create(C.byref(d), _fp(X), _ip(y), self.n, max_particles, device,
-                                          _PREC[precision], C.byref(h)))
+        if devices is not None:
+            dv = (C.c_int * len(devices))(*devices)
+            L.check(self.lib.dasmc_gpu_create_multi(C.byref(d), _fp(X), _ip(y), self.n, max_particles, dv, len(devices),
+                                                    _PREC[precision], C.byref(h)))
+        else:
+            L.check(self.lib.dasmc_gpu_create(C.byref(d), _fp(X), _ip(y), self.n, max_particles, device,
+                                              _PREC[precision], C.byref(h)))
         self.h = h
         self.max_particles = max_particles
 

@@ -21,8 +21,12 @@
 #include "tc_gemm.cuh"
 #include "conv_tc.cuh"
 
+namespace dasmc_b200 {
+struct MultiState;
+}
 struct dasmc_ctx {
   dasmc_b200::Ctx c;
+  dasmc_b200::MultiState* multi = nullptr;  // single-process multi-GPU group (dasmc_gpu_create_multi)
 };
 
 namespace dasmc_b200 {
@@ -498,6 +502,21 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
 }  // namespace
 }  // namespace dasmc_b200
 
+namespace dasmc_b200 {
+struct MultiState;
+void multi_destroy(MultiState* m);
+dasmc_ctx* multi_shard_handle(MultiState* m, int r);
+void multi_set_target_api(MultiState& m, int64_t P, int64_t M, int64_t N, int mode, double beta, double sigma);
+void multi_init_api(MultiState& m, int64_t J, uint64_t seed);
+void multi_set_ensemble_api(MultiState& m, const void* theta, bool f32, const double* lw, int64_t J, int it);
+void multi_get_ensemble_api(MultiState& m, void* theta, bool f32, double* lw, int* it);
+void multi_smc_step_api(MultiState& m, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind, double fraction,
+                        int always, dasmc_iter_record* record);
+void multi_sync_records_api(MultiState& m, dasmc_iter_record* records, int count);
+void multi_sda_moments_api(MultiState& m, int64_t P, int64_t M, double* out6);
+Ctx& multi_lead(MultiState& m);
+}  // namespace dasmc_b200
+
 using namespace dasmc_b200;
 
 extern "C" {
@@ -524,6 +543,11 @@ int dasmc_gpu_create(const dasmc_net_desc* net, const float* X, const int32_t* y
 
 int dasmc_gpu_destroy(dasmc_ctx* ctx) {
   if (!ctx) return DASMC_OK;
+  if (ctx->multi) {
+    multi_destroy(ctx->multi);
+    delete ctx;
+    return DASMC_OK;
+  }
   free_ctx(ctx->c);
   delete ctx;
   return DASMC_OK;
@@ -563,6 +587,10 @@ int dasmc_gpu_set_target(dasmc_ctx* ctx, int64_t prefix_end, int64_t block_end, 
                          double beta, double sigma) {
   return guarded([&] {
     if (!ctx) throw InvalidArg("null ctx");
+    if (ctx->multi) {
+      multi_set_target_api(*ctx->multi, prefix_end, block_end, total_n, mode, beta, sigma);
+      return;
+    }
     Ctx t = ctx->c;  // validate on a copy (no allocation happens)
     t.prefix_end = prefix_end;
     t.block_end = block_end;
@@ -677,6 +705,10 @@ int dasmc_gpu_resample_indices(dasmc_ctx* ctx, const double* w, const double* u,
 int dasmc_gpu_init_ensemble(dasmc_ctx* ctx, int64_t J, uint64_t seed) {
   return guarded([&] {
     if (!ctx) throw InvalidArg("null ctx");
+    if (ctx->multi) {
+      multi_init_api(*ctx->multi, J, seed);
+      return;
+    }
     CK(cudaSetDevice(ctx->c.device));
     init_ensemble_dev(ctx->c, J, seed);
   });
@@ -686,6 +718,10 @@ int dasmc_gpu_set_ensemble(dasmc_ctx* ctx, const double* theta, const double* lo
                            int iteration) {
   return guarded([&] {
     if (!ctx || !theta || !log_weights) throw InvalidArg("null argument");
+    if (ctx->multi) {
+      multi_set_ensemble_api(*ctx->multi, theta, false, log_weights, J, iteration);
+      return;
+    }
     Ctx& c = ctx->c;
     check_J(c, J);
     if (J < 2) throw InvalidArg("ensemble needs at least 2 particles");
@@ -725,6 +761,10 @@ int dasmc_gpu_set_ensemble_f32(dasmc_ctx* ctx, const float* theta, const double*
                                int iteration) {
   return guarded([&] {
     if (!ctx || !theta || !log_weights) throw InvalidArg("null argument");
+    if (ctx->multi) {
+      multi_set_ensemble_api(*ctx->multi, theta, true, log_weights, J, iteration);
+      return;
+    }
     Ctx& c = ctx->c;
     check_J(c, J);
     if (J < 2) throw InvalidArg("ensemble needs at least 2 particles");
@@ -759,6 +799,10 @@ int dasmc_gpu_set_ensemble_f32(dasmc_ctx* ctx, const float* theta, const double*
 int dasmc_gpu_get_ensemble(dasmc_ctx* ctx, double* theta, double* log_weights, int* iteration) {
   return guarded([&] {
     if (!ctx) throw InvalidArg("null ctx");
+    if (ctx->multi) {
+      multi_get_ensemble_api(*ctx->multi, theta, false, log_weights, iteration);
+      return;
+    }
     Ctx& c = ctx->c;
     if (!c.has_ensemble) throw InvalidArg("no ensemble");
     CK(cudaSetDevice(c.device));
@@ -776,6 +820,10 @@ int dasmc_gpu_get_ensemble(dasmc_ctx* ctx, double* theta, double* log_weights, i
 int dasmc_gpu_get_ensemble_f32(dasmc_ctx* ctx, float* theta, double* log_weights, int* iteration) {
   return guarded([&] {
     if (!ctx) throw InvalidArg("null ctx");
+    if (ctx->multi) {
+      multi_get_ensemble_api(*ctx->multi, theta, true, log_weights, iteration);
+      return;
+    }
     Ctx& c = ctx->c;
     if (!c.has_ensemble) throw InvalidArg("no ensemble");
     CK(cudaSetDevice(c.device));
@@ -806,9 +854,13 @@ int dasmc_gpu_smc_step(dasmc_ctx* ctx, const dasmc_kernel_cfg* cfg, uint64_t see
                        double fraction, int resample_always, dasmc_iter_record* record) {
   return guarded([&] {
     if (!ctx || !cfg) throw InvalidArg("null argument");
+    if (!(fraction >= 0.0 && fraction <= 1.0)) throw InvalidArg("resample_fraction: must be in [0, 1]");
+    if (ctx->multi) {
+      multi_smc_step_api(*ctx->multi, *cfg, seed, resample_kind, fraction, resample_always, record);
+      return;
+    }
     Ctx& c = ctx->c;
     CK(cudaSetDevice(c.device));
-    if (!(fraction >= 0.0 && fraction <= 1.0)) throw InvalidArg("resample_fraction: must be in [0, 1]");
     const int slot = c.rec_head % kRecRing;
     CK(cudaEventRecord(c.ev0, c.stream));
     smc_step_async(c, *cfg, seed, resample_kind, fraction, resample_always, slot);
@@ -830,6 +882,10 @@ int dasmc_gpu_smc_step(dasmc_ctx* ctx, const dasmc_kernel_cfg* cfg, uint64_t see
 int dasmc_gpu_sync_records(dasmc_ctx* ctx, dasmc_iter_record* records, int count) {
   return guarded([&] {
     if (!ctx) throw InvalidArg("null ctx");
+    if (ctx->multi) {
+      multi_sync_records_api(*ctx->multi, records, count);
+      return;
+    }
     Ctx& c = ctx->c;
     CK(cudaSetDevice(c.device));
     if (count < 0 || count > c.rec_head || count > kRecRing) throw InvalidArg("record count out of range");
@@ -868,6 +924,10 @@ int dasmc_gpu_last_proposals(dasmc_ctx* ctx, double* p_final, double* log_target
 int dasmc_gpu_sda_moments(dasmc_ctx* ctx, int64_t prefix_end, int64_t block_end, double* out6) {
   return guarded([&] {
     if (!ctx || !out6) throw InvalidArg("null argument");
+    if (ctx->multi) {
+      multi_sda_moments_api(*ctx->multi, prefix_end, block_end, out6);
+      return;
+    }
     if (!ctx->c.has_ensemble) throw InvalidArg("no ensemble");
     CK(cudaSetDevice(ctx->c.device));
     sda_moments_dev(ctx->c, prefix_end, block_end, out6);
@@ -1092,6 +1152,13 @@ int dasmc_gpu_unpack_rows(dasmc_ctx* ctx, const float* src_dev, const int32_t* s
 }
 
 int dasmc_gpu_reserve_rows(dasmc_ctx* ctx, int64_t M) {
+  if (ctx && ctx->multi) {
+    for (int r = 0; r < dasmc_gpu_multi_shards(ctx); ++r) {
+      const int rc = dasmc_gpu_reserve_rows(multi_shard_handle(ctx->multi, r), M);
+      if (rc != DASMC_OK) return rc;
+    }
+    return DASMC_OK;
+  }
   return guarded([&] {
     if (!ctx || M < 1 || M > ctx->c.n) throw InvalidArg("reserve_rows: M out of range");
     CK(cudaSetDevice(ctx->c.device));
@@ -1099,14 +1166,17 @@ int dasmc_gpu_reserve_rows(dasmc_ctx* ctx, int64_t M) {
   });
 }
 
-void* dasmc_gpu_stream(dasmc_ctx* ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
+void* dasmc_gpu_stream(dasmc_ctx* ctx) {
+  if (ctx && ctx->multi) return (void*)multi_lead(*ctx->multi).stream;
+  return ctx ? (void*)ctx->c.stream : nullptr;
+}
 
 int64_t dasmc_launch_count(void) { return (int64_t)g_launch_count.load(); }
 
 int dasmc_gpu_set_timing(dasmc_ctx* ctx, int enable) {
   return guarded([&] {
     if (!ctx) throw InvalidArg("null ctx");
-    Ctx& c = ctx->c;
+    Ctx& c = ctx->multi ? multi_lead(*ctx->multi) : ctx->c;  // a group times its lead shard
     CK(cudaSetDevice(c.device));
     harvest_timers(c);
     for (int k = 0; k < kTimerKinds; ++k) {
@@ -1120,7 +1190,7 @@ int dasmc_gpu_set_timing(dasmc_ctx* ctx, int enable) {
 int dasmc_gpu_kernel_times(dasmc_ctx* ctx, double* ms3, int64_t* count3) {
   return guarded([&] {
     if (!ctx || !ms3 || !count3) throw InvalidArg("null argument");
-    Ctx& c = ctx->c;
+    Ctx& c = ctx->multi ? multi_lead(*ctx->multi) : ctx->c;
     CK(cudaSetDevice(c.device));
     harvest_timers(c);
     for (int k = 0; k < kTimerKinds; ++k) {
@@ -1432,3 +1502,447 @@ int dasmc_gpu_bench_memory(dasmc_ctx* ctx, int64_t J, const int32_t* idx, int re
 }
 
 }  // extern "C"
+
+// =====================================================================================
+// Single-process multi-GPU group: one ensemble of J particles sharded over
+// G shard contexts, shard r on devices[r] owning the contiguous global slots [lo_r, hi_r)
+// (parallel.hpp:30-31).  The C++ driver owns the whole iteration (smc.hpp:109-158):
+//   1. every shard proposes / reweights its own slots (RNG streams keyed by the GLOBAL slot);
+//   2. all-gather of the (log_w, log_target_new) vectors: peer copies over NVLink into every
+//      shard's full-J vectors (reference order);
+//   3. every shard runs the same normalise / ESS / decision / CDF / search on the full
+//      vectors (identical indices, no broadcast) and finalises its own rows (divergent
+//      particles keep theta, smc.hpp:129-131);
+//   4. migration: each shard's gather kernel pulls its new rows theta_new[j] =
+//      fin[owner(idx[j])][idx[j] - lo_owner] straight from the owners' memory (peer loads
+//      over NVLink; no host plan, no staging copies).
+// Cross-shard ordering is stream / event based; the only host read per iteration is the
+// record the caller asks for.  Shards may share a device (devices = {0, 0, 0}): the same
+// code then runs as an in-process emulation, bit-identical to one context.
+// SDA moments (annealing.hpp:153-174) come from an all-gather of the per-particle final
+// (prefix, block) log-likelihood pairs, reduced on the host in reference order.
+namespace dasmc_b200 {
+
+constexpr int kMaxShards = 16;
+
+struct PeerRows {
+  const float4* p[kMaxShards];
+  int64_t lo[kMaxShards + 1];
+  int G;
+};
+
+namespace {
+
+__global__ void __launch_bounds__(256) peer_gather_kernel(PeerRows src, float4* __restrict__ dst, int64_t Dp4,
+                                                          const int32_t* __restrict__ idx) {
+  const int64_t j = blockIdx.y;
+  const int64_t g = idx[j];
+  int r = 0;
+  while (r + 1 < src.G && g >= src.lo[r + 1]) ++r;
+  const float4* s = src.p[r] + (g - src.lo[r]) * Dp4;
+  float4* d = dst + j * Dp4;
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < Dp4; i += (int64_t)gridDim.x * 256) d[i] = s[i];
+}
+
+__global__ void pick_pairs_kernel(int64_t J, const int32_t* __restrict__ idx, const double* __restrict__ pre,
+                                  const double* __restrict__ blk, double* __restrict__ out_pre,
+                                  double* __restrict__ out_blk) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= J) return;
+  out_pre[j] = pre[idx[j]];
+  out_blk[j] = blk[idx[j]];
+}
+
+}  // namespace
+
+struct MultiState {
+  int G = 0;
+  std::vector<dasmc_ctx*> sh;
+  std::vector<int> dev;
+  std::vector<int64_t> lo;  // G + 1 slot boundaries
+  int64_t J = 0, Jcap = 0;
+  bool has = false;
+  int rec_head = 0;
+  // per shard, on its device: full-J vectors (log_w, log_target_new, w, cdf, uniforms,
+  // final prefix / block ll, post-resample prefix / block ll) and indices; local vectors
+  std::vector<double*> full;   // [9][Jcap]
+  std::vector<int32_t*> idx;   // [Jcap]
+  std::vector<double*> loc;    // [4][Jcap / G + 1]: log_w, log_target_new, final prefix, final block
+  std::vector<cudaEvent_t> ev_w, ev_f, ev_g;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  bool parts_valid = false;
+  int64_t parts_P = -1, parts_M = -1;
+};
+
+namespace {
+
+enum { kLw = 0, kLt, kW, kCdf, kUni, kFp, kFb, kSp, kSb, kNumFull };
+
+Ctx& shard(MultiState& m, int r) { return m.sh[(size_t)r]->c; }
+
+void multi_free(MultiState* m) {
+  if (!m) return;
+  for (int r = 0; r < m->G; ++r) {
+    if (r < (int)m->dev.size()) cudaSetDevice(m->dev[(size_t)r]);
+    if (r < (int)m->full.size() && m->full[(size_t)r]) cudaFree(m->full[(size_t)r]);
+    if (r < (int)m->idx.size() && m->idx[(size_t)r]) cudaFree(m->idx[(size_t)r]);
+    if (r < (int)m->loc.size() && m->loc[(size_t)r]) cudaFree(m->loc[(size_t)r]);
+    for (auto* v : {&m->ev_w, &m->ev_f, &m->ev_g})
+      if (r < (int)v->size() && (*v)[(size_t)r]) cudaEventDestroy((*v)[(size_t)r]);
+    if (r < (int)m->sh.size() && m->sh[(size_t)r]) dasmc_gpu_destroy(m->sh[(size_t)r]);
+  }
+  if (m->e0) cudaEventDestroy(m->e0);
+  if (m->e1) cudaEventDestroy(m->e1);
+  delete m;
+}
+
+// (re)size the full-J vectors for an ensemble of J particles
+void multi_reserve(MultiState& m, int64_t J) {
+  if (J <= m.Jcap) return;
+  for (int r = 0; r < m.G; ++r) {
+    CK(cudaSetDevice(m.dev[(size_t)r]));
+    CK(cudaStreamSynchronize(shard(m, r).stream));
+    if (m.full[(size_t)r]) CK(cudaFree(m.full[(size_t)r]));
+    if (m.idx[(size_t)r]) CK(cudaFree(m.idx[(size_t)r]));
+    if (m.loc[(size_t)r]) CK(cudaFree(m.loc[(size_t)r]));
+    m.full[(size_t)r] = nullptr;
+    m.idx[(size_t)r] = nullptr;
+    m.loc[(size_t)r] = nullptr;
+    dmalloc(m.full[(size_t)r], (size_t)kNumFull * J);
+    dmalloc(m.idx[(size_t)r], (size_t)J);
+    dmalloc(m.loc[(size_t)r], (size_t)4 * (J / m.G + 1));
+    Ctx& c = shard(m, r);
+    // the resampling uniforms of J_total slots need jump polynomials for J_total draws
+    const int64_t need = (J + 2 * c.rng_chunk - 1) / (2 * c.rng_chunk) + 1;
+    if (need > c.jump_chunks) {
+      CK(cudaFree(c.jump_tab));
+      c.jump_tab = nullptr;
+      const auto tab = jump_table(2 * (uint64_t)c.rng_chunk, need);
+      dmalloc(c.jump_tab, (size_t)need * 4);
+      CK(cudaMemcpy(c.jump_tab, tab.data(), sizeof(uint64_t) * 4 * tab.size(), cudaMemcpyHostToDevice));
+      c.jump_chunks = need;
+    }
+  }
+  m.Jcap = J;
+}
+
+void multi_ranges(MultiState& m, int64_t J) {
+  m.lo.assign((size_t)m.G + 1, 0);
+  for (int r = 0; r <= m.G; ++r) m.lo[(size_t)r] = J * r / m.G;  // parallel.hpp:30-31
+  for (int r = 0; r < m.G; ++r)
+    if (m.lo[(size_t)r + 1] - m.lo[(size_t)r] < 2) throw InvalidArg("multi-GPU group: need >= 2 particles per shard");
+}
+
+void multi_peer_copy(MultiState& m, int d, double* dst, int r, const double* src, int64_t count) {
+  if (count <= 0) return;
+  CK(cudaMemcpyPeerAsync(dst, m.dev[(size_t)d], src, m.dev[(size_t)r], sizeof(double) * count, shard(m, d).stream));
+}
+
+// One SMC iteration of the whole sharded ensemble.  Asynchronous; the record lands in shard
+// 0's record ring at `slot`.
+void multi_step(MultiState& m, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind, double fraction, int always,
+                int slot) {
+  if (rkind != DASMC_MULTINOMIAL && rkind != DASMC_SYSTEMATIC) throw InvalidArg("bad resample kind");
+  const int G = m.G;
+  const int64_t J = m.J;
+  const int k = shard(m, 0).iteration;
+  const bool parts = shard(m, 0).mode == DASMC_SDA;
+  std::vector<float*> fin((size_t)G);
+  // 1. propose + local weights (+ final ll pairs for the SDA moments) on every shard
+  for (int r = 0; r < G; ++r) {
+    Ctx& c = shard(m, r);
+    CK(cudaSetDevice(c.device));
+    for (int q = 0; q < G; ++q) CK(cudaStreamWaitEvent(c.stream, m.ev_g[(size_t)q], 0));  // peers done reading
+    const int t1 = (c.start + 1) % 3, t2 = (c.start + 2) % 3;
+    float* bufs[3] = {c.theta[c.start], c.theta[t1], c.theta[t2]};
+    const int end_idx = propose_async(c, kc, seed, m.lo[(size_t)r]);
+    const int64_t Jr = c.J;
+    const int64_t stride = m.Jcap / G + 1;
+    double* loc = m.loc[(size_t)r];
+    launch_local_weights(c, Jr, loc, loc + stride);
+    if (parts) launch_select_parts(c, Jr, c.iota, loc + 2 * stride, loc + 3 * stride);
+    // finalised rows: divergent particles keep theta (smc.hpp:129-131), into the free buffer
+    const int dst_idx = end_idx == 1 ? 2 : 1;
+    launch_gather(c, bufs[0], bufs[end_idx], bufs[dst_idx], Jr, c.iota);
+    fin[(size_t)r] = bufs[dst_idx];
+    CK(cudaEventRecord(m.ev_w[(size_t)r], c.stream));
+  }
+  // 2. all-gather into every shard's full vectors (reference slot order)
+  for (int d = 0; d < G; ++d) {
+    Ctx& c = shard(m, d);
+    CK(cudaSetDevice(c.device));
+    double* full = m.full[(size_t)d];
+    for (int r = 0; r < G; ++r) {
+      CK(cudaStreamWaitEvent(c.stream, m.ev_w[(size_t)r], 0));
+      const int64_t lo = m.lo[(size_t)r], n = m.lo[(size_t)r + 1] - lo, stride = m.Jcap / G + 1;
+      const double* loc = m.loc[(size_t)r];
+      multi_peer_copy(m, d, full + kLw * m.Jcap + lo, r, loc, n);
+      multi_peer_copy(m, d, full + kLt * m.Jcap + lo, r, loc + stride, n);
+      if (parts && d == 0) {
+        multi_peer_copy(m, d, full + kFp * m.Jcap + lo, r, loc + 2 * stride, n);
+        multi_peer_copy(m, d, full + kFb * m.Jcap + lo, r, loc + 3 * stride, n);
+      }
+    }
+    // 3. redundant normalise / ESS / decision / resampling indices (smc.hpp:127-156)
+    double* lw = full + kLw * m.Jcap;
+    launch_uniforms(c, fork_key(seed, tag::kResample, (uint64_t)k, 0), rkind == DASMC_MULTINOMIAL ? J : 1,
+                    full + kUni * m.Jcap);
+    launch_normalize_resample(c, J, lw, full + kLt * m.Jcap, full + kW * m.Jcap, full + kCdf * m.Jcap,
+                              full + kUni * m.Jcap, m.idx[(size_t)d], fraction, always, rkind, slot, k);
+    CK(cudaMemcpyAsync(c.logw, lw + m.lo[(size_t)d], sizeof(double) * c.J, cudaMemcpyDeviceToDevice, c.stream));
+    if (parts && d == 0)
+      pick_pairs_kernel<<<(unsigned)((J + 255) / 256), 256, 0, c.stream>>>(
+          J, m.idx[0], full + kFp * m.Jcap, full + kFb * m.Jcap, full + kSp * m.Jcap, full + kSb * m.Jcap);
+    if (parts && d == 0) LAUNCHED();
+  }
+  // 4. migration: every shard pulls its new rows from the owners' finalised buffers
+  PeerRows src{};
+  src.G = G;
+  for (int r = 0; r < G; ++r) src.p[r] = reinterpret_cast<const float4*>(fin[(size_t)r]);
+  for (int r = 0; r <= G; ++r) src.lo[r] = m.lo[(size_t)r];
+  for (int d = 0; d < G; ++d) {
+    Ctx& c = shard(m, d);
+    CK(cudaSetDevice(c.device));
+    for (int r = 0; r < G; ++r) CK(cudaStreamWaitEvent(c.stream, m.ev_w[(size_t)r], 0));  // rows finalised
+    const int64_t Dp4 = c.net.Dp / 4;
+    const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>((Dp4 + 255) / 256, 64));
+    peer_gather_kernel<<<dim3((unsigned)chunks, (unsigned)c.J), 256, 0, c.stream>>>(
+        src, reinterpret_cast<float4*>(c.theta[c.start]), Dp4, m.idx[(size_t)d] + m.lo[(size_t)d]);
+    LAUNCHED();
+    CK(cudaEventRecord(m.ev_g[(size_t)d], c.stream));
+    c.iteration = k + 1;  // smc.hpp:150, 154
+    c.step_parts_valid = false;
+    c.cache_valid = false;
+  }
+  // shard 0's stream marks the end of the whole iteration (records, timing)
+  CK(cudaSetDevice(shard(m, 0).device));
+  for (int r = 1; r < G; ++r) CK(cudaStreamWaitEvent(shard(m, 0).stream, m.ev_g[(size_t)r], 0));
+  m.parts_valid = parts;
+  m.parts_P = shard(m, 0).prefix_end;
+  m.parts_M = shard(m, 0).block_end;
+}
+
+MultiState* multi_of(dasmc_ctx* ctx) { return ctx ? ctx->multi : nullptr; }
+
+}  // namespace
+}  // namespace dasmc_b200
+
+extern "C" {
+
+int dasmc_gpu_create_multi(const dasmc_net_desc* net, const float* X, const int32_t* y, int64_t n,
+                           int max_particles, const int* devices, int ndev, int precision, dasmc_ctx** out) {
+  if (out == nullptr) {
+    g_err = "null out";
+    return DASMC_EINVAL;
+  }
+  *out = nullptr;
+  auto* m = new MultiState();
+  const int rc = guarded([&] {
+    if (!devices || ndev < 1 || ndev > kMaxShards) throw InvalidArg("multi-GPU group: 1..16 devices");
+    if (max_particles < 2 * ndev) throw InvalidArg("multi-GPU group: max_particles must be >= 2 per shard");
+    m->G = ndev;
+    m->dev.assign(devices, devices + ndev);
+    m->sh.assign((size_t)ndev, nullptr);
+    m->full.assign((size_t)ndev, nullptr);
+    m->idx.assign((size_t)ndev, nullptr);
+    m->loc.assign((size_t)ndev, nullptr);
+    m->ev_w.assign((size_t)ndev, nullptr);
+    m->ev_f.assign((size_t)ndev, nullptr);
+    m->ev_g.assign((size_t)ndev, nullptr);
+    const int per = (max_particles + ndev - 1) / ndev + 1;
+    for (int r = 0; r < ndev; ++r) {
+      const int rc2 = dasmc_gpu_create(net, X, y, n, per, devices[r], precision, &m->sh[(size_t)r]);
+      if (rc2 != DASMC_OK) throw std::runtime_error(g_err);
+      CK(cudaSetDevice(devices[r]));
+      for (auto* v : {&m->ev_w, &m->ev_f, &m->ev_g})
+        CK(cudaEventCreateWithFlags(&(*v)[(size_t)r], cudaEventDisableTiming));
+      // peer access to every other shard's device (NVLink loads / copies)
+      for (int q = 0; q < ndev; ++q) {
+        if (devices[q] == devices[r]) continue;
+        int can = 0;
+        CK(cudaDeviceCanAccessPeer(&can, devices[r], devices[q]));
+        if (!can) throw InvalidArg("multi-GPU group: devices without peer access");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(devices[q], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+        cudaGetLastError();
+      }
+    }
+    CK(cudaSetDevice(devices[0]));
+    CK(cudaEventCreate(&m->e0));
+    CK(cudaEventCreate(&m->e1));
+    multi_reserve(*m, max_particles);
+  });
+  if (rc != DASMC_OK) {
+    multi_free(m);
+    return rc;
+  }
+  auto* h = new dasmc_ctx();
+  h->multi = m;
+  h->c.net = m->sh[0]->c.net;  // param_count, layouts
+  h->c.device = devices[0];
+  *out = h;
+  return DASMC_OK;
+}
+
+int dasmc_gpu_multi_shards(const dasmc_ctx* ctx) { return ctx && ctx->multi ? ctx->multi->G : 1; }
+
+}  // extern "C"
+
+namespace dasmc_b200 {
+namespace {
+
+// ---- group versions of the hot-path entry points (dispatched from the C-ABI) ----------------
+void multi_set_target(MultiState& m, int64_t P, int64_t M, int64_t N, int mode, double beta, double sigma) {
+  for (int r = 0; r < m.G; ++r) {
+    const int rc = dasmc_gpu_set_target(m.sh[(size_t)r], P, M, N, mode, beta, sigma);
+    if (rc != DASMC_OK) throw InvalidArg(g_err);
+  }
+  m.parts_valid = false;
+}
+
+void multi_init(MultiState& m, int64_t J, uint64_t seed) {
+  multi_ranges(m, J);
+  multi_reserve(m, J);
+  for (int r = 0; r < m.G; ++r) {
+    Ctx& c = shard(m, r);
+    CK(cudaSetDevice(c.device));
+    init_ensemble_dev(c, m.lo[(size_t)r + 1] - m.lo[(size_t)r], seed, m.lo[(size_t)r]);
+  }
+  m.J = J;
+  m.has = true;
+  m.parts_valid = false;
+}
+
+template <typename T>
+void multi_set_ensemble(MultiState& m, const T* theta, const double* lw, int64_t J, int iteration) {
+  multi_ranges(m, J);
+  multi_reserve(m, J);
+  const int64_t D = shard(m, 0).net.D;
+  for (int r = 0; r < m.G; ++r) {
+    const int64_t lo = m.lo[(size_t)r], n = m.lo[(size_t)r + 1] - lo;
+    int rc;
+    if constexpr (std::is_same<T, float>::value)
+      rc = dasmc_gpu_set_ensemble_f32(m.sh[(size_t)r], theta + lo * D, lw + lo, n, iteration);
+    else
+      rc = dasmc_gpu_set_ensemble(m.sh[(size_t)r], theta + lo * D, lw + lo, n, iteration);
+    if (rc != DASMC_OK) throw InvalidArg(g_err);
+  }
+  m.J = J;
+  m.has = true;
+  m.parts_valid = false;
+}
+
+template <typename T>
+void multi_get_ensemble(MultiState& m, T* theta, double* lw, int* iteration) {
+  if (!m.has) throw InvalidArg("no ensemble");
+  const int64_t D = shard(m, 0).net.D;
+  for (int r = 0; r < m.G; ++r) {
+    const int64_t lo = m.lo[(size_t)r];
+    int rc;
+    if constexpr (std::is_same<T, float>::value)
+      rc = dasmc_gpu_get_ensemble_f32(m.sh[(size_t)r], theta ? theta + lo * D : nullptr, lw ? lw + lo : nullptr,
+                                      nullptr);
+    else
+      rc = dasmc_gpu_get_ensemble(m.sh[(size_t)r], theta ? theta + lo * D : nullptr, lw ? lw + lo : nullptr, nullptr);
+    if (rc != DASMC_OK) throw std::runtime_error(g_err);
+  }
+  if (iteration) *iteration = shard(m, 0).iteration;
+}
+
+void multi_sda_moments(MultiState& m, int64_t P, int64_t M, double* out6) {
+  if (!m.has) throw InvalidArg("no ensemble");
+  if (P < 0 || P > M || M > shard(m, 0).n) throw InvalidArg("SubsetWindow: need 0 <= prefix_end <= block_end <= total_n");
+  if (M <= P) throw InvalidArg("sda_moments: window has no new block");
+  const int64_t J = m.J;
+  std::vector<double> pre((size_t)J), blk((size_t)J), lw((size_t)J);
+  Ctx& c0 = shard(m, 0);
+  CK(cudaSetDevice(c0.device));
+  if (m.parts_valid && m.parts_P == P && m.parts_M == M && !c0.force_moment_pass) {
+    // the all-gathered (prefix, block) pairs of the step's own evaluations, resampled
+    download(c0, pre.data(), m.full[0] + kSp * m.Jcap, sizeof(double) * J);
+    download(c0, blk.data(), m.full[0] + kSb * m.Jcap, sizeof(double) * J);
+  } else {
+    for (int r = 0; r < m.G; ++r) {
+      Ctx& c = shard(m, r);
+      CK(cudaSetDevice(c.device));
+      loglik_parts_dev(c, c.theta[c.start], c.J, P, M);
+      download(c, pre.data() + m.lo[(size_t)r], c.ll_pre, sizeof(double) * c.J);
+      download(c, blk.data() + m.lo[(size_t)r], c.ll_blk, sizeof(double) * c.J);
+    }
+  }
+  for (int r = 0; r < m.G; ++r) {
+    Ctx& c = shard(m, r);
+    CK(cudaSetDevice(c.device));
+    download(c, lw.data() + m.lo[(size_t)r], c.logw, sizeof(double) * c.J);
+  }
+  for (int64_t j = 0; j < J; ++j) {
+    pre[(size_t)j] = -pre[(size_t)j];
+    blk[(size_t)j] = -blk[(size_t)j];
+  }
+  sda_moments_from(pre.data(), blk.data(), lw.data(), J, out6);
+}
+
+}  // namespace
+}  // namespace dasmc_b200
+
+namespace dasmc_b200 {
+void multi_destroy(MultiState* m) { multi_free(m); }
+dasmc_ctx* multi_shard_handle(MultiState* m, int r) { return m->sh[(size_t)r]; }
+Ctx& multi_lead(MultiState& m) { return shard(m, 0); }
+void multi_set_target_api(MultiState& m, int64_t P, int64_t M, int64_t N, int mode, double beta, double sigma) {
+  multi_set_target(m, P, M, N, mode, beta, sigma);
+}
+void multi_init_api(MultiState& m, int64_t J, uint64_t seed) { multi_init(m, J, seed); }
+void multi_set_ensemble_api(MultiState& m, const void* theta, bool f32, const double* lw, int64_t J, int it) {
+  if (f32)
+    multi_set_ensemble(m, static_cast<const float*>(theta), lw, J, it);
+  else
+    multi_set_ensemble(m, static_cast<const double*>(theta), lw, J, it);
+}
+void multi_get_ensemble_api(MultiState& m, void* theta, bool f32, double* lw, int* it) {
+  if (f32)
+    multi_get_ensemble(m, static_cast<float*>(theta), lw, it);
+  else
+    multi_get_ensemble(m, static_cast<double*>(theta), lw, it);
+}
+void multi_smc_step_api(MultiState& m, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind, double fraction,
+                        int always, dasmc_iter_record* record) {
+  if (!m.has) throw InvalidArg("smc_step: no ensemble (call init_ensemble or set_ensemble)");
+  Ctx& c0 = shard(m, 0);
+  CK(cudaSetDevice(c0.device));
+  const int slot = m.rec_head % kRecRing;
+  CK(cudaEventRecord(m.e0, c0.stream));
+  multi_step(m, kc, seed, rkind, fraction, always, slot);
+  CK(cudaSetDevice(c0.device));
+  CK(cudaEventRecord(m.e1, c0.stream));
+  ++m.rec_head;
+  if (record) {
+    fetch_records(c0, slot, 1);
+    *record = read_record(c0, slot);
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, m.e0, m.e1));
+    record->sampler_ms = ms;
+    record->batch = c0.block_end;
+    record->beta = c0.mode == DASMC_SDA ? c0.beta : 1.0;
+  }
+}
+void multi_sync_records_api(MultiState& m, dasmc_iter_record* records, int count) {
+  Ctx& c0 = shard(m, 0);
+  CK(cudaSetDevice(c0.device));
+  if (count < 0 || count > m.rec_head || count > kRecRing) throw InvalidArg("record count out of range");
+  for (int r = 0; r < m.G; ++r) {
+    CK(cudaSetDevice(shard(m, r).device));
+    CK(cudaStreamSynchronize(shard(m, r).stream));
+  }
+  CK(cudaSetDevice(c0.device));
+  if (count == 0 || records == nullptr) return;
+  CK(cudaMemcpy(c0.h_records, c0.records, sizeof(double) * 8 * kRecRing, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < count; ++i) {
+    const int slot = (m.rec_head - count + i) % kRecRing;
+    records[i] = read_record(c0, slot);
+    records[i].batch = c0.block_end;
+    records[i].beta = c0.mode == DASMC_SDA ? c0.beta : 1.0;
+  }
+}
+void multi_sda_moments_api(MultiState& m, int64_t P, int64_t M, double* out6) { multi_sda_moments(m, P, M, out6); }
+}  // namespace dasmc_b200

@@ -558,10 +558,11 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
   auto go = [&](auto act_c) {
     constexpr int A_ = decltype(act_c)::value;
     auto kern = conv_tc_kernel<EPI, A_>;
-    static bool attr = false;  // one flag per (EPI, ACT) instantiation
-    if (!attr) {
+    static bool attr[kMaxDevices] = {};  // one flag per (EPI, ACT) instantiation and device
+    const int dv = current_device();
+    if (!attr[dv]) {
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      attr = true;
+      attr[dv] = true;
     }
     const int per_sm = std::max(1, std::min(2, (int)((228 * 1024) / (smem + 1024))));
     const int grid = std::max(1, std::min(units, c.ctc->num_sms * per_sm));

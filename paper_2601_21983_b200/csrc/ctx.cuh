@@ -46,6 +46,14 @@ extern std::atomic<long long> g_launch_count;
 constexpr int kTimerKinds = 3;
 
 constexpr int kMaxLayers = 8;
+// Function attributes (dynamic shared memory opt-in) are per device: kernels keep one
+// "already set" flag per device ordinal (multi-GPU groups drive several devices).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < kMaxDevices ? d : kMaxDevices - 1;
+}
 constexpr int kMaxConv = 6;
 
 struct LayerDev {
@@ -283,6 +291,8 @@ void launch_gather(Ctx& c, const float* start, const float* end, float* dst, int
                    const int32_t* idx = nullptr);
 // post-step (prefix, block) ll: (flags[s] ? first-evaluation : last-evaluation)[s], s = idx[j]
 void launch_gather_parts(Ctx& c, int64_t J);
+// out[j] = (flags[s] ? first-evaluation : last-evaluation) (prefix, block) ll, s = idx[j]
+void launch_select_parts(Ctx& c, int64_t J, const int32_t* idx, double* out_pre, double* out_blk);
 // start-gradient cache: p += h/2 g_cached, theta_out = theta + h p (kernels.hpp:89-91), flags
 void launch_start_from_cache(Ctx& c, const EpiParams& e, int64_t J);
 // rows dst[j] = src[idx[j]] of Dp floats, and lt_cache[j] = lt_new[idx[j]]

@@ -687,12 +687,13 @@ int grid_for(int64_t total, int threads = 256) {
 
 // dynamic shared memory of the weights / resampling kernels (the opt-in above 48 KB, once)
 size_t cdf_smem(int64_t J) {
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kMaxDevices] = {};
+  const int dv = current_device();
+  if (!attr[dv]) {
     const int b = (int)(kCdfSmemMax * sizeof(double));
     CK(cudaFuncSetAttribute(weights_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     CK(cudaFuncSetAttribute(resample_hook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    attr = true;
+    attr[dv] = true;
   }
   return cdf_smem_bytes(J);
 }
@@ -1653,6 +1654,12 @@ void launch_gather_cache(Ctx& c, const float* src, float* dst, int64_t J) {
   const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>((Dp4 + 255) / 256, 64));
   gather_cache_kernel<<<dim3((unsigned)chunks, (unsigned)J), 256, 0, c.stream>>>(
       reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), Dp4, c.idx, c.lt_new, c.lt_cache);
+  LAUNCHED();
+}
+
+void launch_select_parts(Ctx& c, int64_t J, const int32_t* idx, double* out_pre, double* out_blk) {
+  gather_parts_kernel<<<(unsigned)((J + 255) / 256), 256, 0, c.stream>>>(J, idx, c.flags, c.ll_pre0, c.ll_blk0, c.ll_pre,
+                                                                        c.ll_blk, out_pre, out_blk);
   LAUNCHED();
 }
 

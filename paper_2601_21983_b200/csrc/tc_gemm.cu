@@ -1232,8 +1232,11 @@ void launch_tc(Ctx& c, const CUtensorMap& A, const CUtensorMap& Alo, const CUten
   }
   const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16 + epi_smem_bytes + 64;
   auto kern = tc_kernel<EPI, SPLIT, AM, CP, ACT, CL, PREC>;
-  static bool attr_set = false;
-  static int max_clusters = 0;
+  static bool attr_set_dev[kMaxDevices] = {};
+  static int max_clusters_dev[kMaxDevices] = {};
+  const int dv = current_device();
+  bool& attr_set = attr_set_dev[dv];
+  int& max_clusters = max_clusters_dev[dv];
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   cfg.blockDim = dim3(kThreads);
@@ -1511,10 +1514,11 @@ void tc_eval_deep(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P
       constexpr int CPv = decltype(cp)::value;
       const size_t sm = sizeof(float) * ((size_t)nin * CPv + CPv);
       auto kern = head_kernel<CPv>;
-      static bool attr = false;
-      if (!attr) {
+      static bool attr[kMaxDevices] = {};
+      const int dv = current_device();
+      if (!attr[dv]) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-        attr = true;
+        attr[dv] = true;
       }
       kern<<<grid, 128, sm, c.stream>>>(s->aT[L - 1], nin, C, nba, theta_in, net.Dp, ly.woff, ly.boff, net.act, c.y,
                                         M, P, (float)beta_rows, need_grad ? 1 : 0, c.ll_part, c.ll_slots, s->dTl[L],
