@@ -38,6 +38,9 @@ namespace dasmc_b200 {
 
 namespace {
 
+#ifndef DASMC_CONV_MINB
+#define DASMC_CONV_MINB 2  // CTAs per SM the register budget is sized for (2: 8 producer warps per SM)
+#endif
 constexpr int kCBM = 128;              // UMMA M
 constexpr int kCBK = 32;               // tf32 elements per 128-byte swizzle row (one k-block)
 constexpr int kProdWarps = 4;          // gather producers
@@ -101,42 +104,63 @@ __device__ __forceinline__ int row_off(const GOperand& o, int i) {
 }
 __device__ __forceinline__ int col_off(const GOperand& o, int q) { return o.coloff ? o.coloff[q] : q; }
 
-// One operand tile (rows [r0, r0 + nrows_tile), k-block kb) into shared memory at `tile`.
-// Vector path: lane -> (row lane / 8, 16-byte chunk lane % 8), a warp stores 4 full rows.
-// Scalar path: lane -> (row lane / 4, element lane % 4 of a chunk), 8 rows x 16 bytes per
-// instruction; both are bank-conflict free under the 128B swizzle.
-template <int MAXP>
-__device__ __forceinline__ void gather_tile(const GOperand& o, const float* pbase, const float* ones, uint32_t tile,
-                                            const int* roff, int npass, int nrt, int kb, int pt, int lane) {
+// Column (k) offsets of k-block kb that this lane's copies use: the vector path needs one
+// (16-byte chunk lane % 8), the scalar path eight (element lane % 4 of chunks 0..7).
+// kZeroRow marks columns past K.
+__device__ __forceinline__ void load_cols(const GOperand& o, int kb, int lane, int* co) {
   const int q0 = kb * kCBK;
   if (o.vec) {
+    const int q = q0 + 4 * (lane & 7);
+    co[0] = q < o.K ? col_off(o, q) : kZeroRow;
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int q = q0 + 4 * c + (lane & 3);
+      co[c] = q < o.K ? col_off(o, q) : kZeroRow;
+    }
+  }
+}
+
+// Row offsets of the tile rows this lane copies (pass p: vector rows (p*4 + warp)*4 + lane/8,
+// scalar rows (p*4 + warp)*8 + lane/4); kZeroRow past the operand's rows or the tile.
+template <int MAXP>
+__device__ __forceinline__ void load_rows(const GOperand& o, int r0, int nrt, int pt, int lane, int* ro) {
+#pragma unroll
+  for (int p = 0; p < MAXP; ++p) {
+    const int rl = o.vec ? (p * kProdWarps + pt) * 4 + (lane >> 3) : (p * kProdWarps + pt) * 8 + (lane >> 2);
+    ro[p] = rl < nrt ? row_off(o, r0 + rl) : kZeroRow;
+  }
+}
+
+// One operand tile (k-block kb) into shared memory at `tile` from precomputed row / column
+// offsets.  Vector path: lane -> (row lane / 8, 16-byte chunk lane % 8), a warp stores 4 full
+// rows.  Scalar path: lane -> (row lane / 4, element lane % 4 of a chunk), 8 rows x 16 bytes
+// per instruction; both are bank-conflict free under the 128B swizzle.
+template <int MAXP>
+__device__ __forceinline__ void gather_tile(const GOperand& o, const float* pbase, const float* ones, uint32_t tile,
+                                            const int* roff, const int* coff, int nrt, int pt, int lane) {
+  if (o.vec) {
     const int c = lane & 7;
-    const int q = q0 + 4 * c;
-    const bool qv = q < o.K;
-    const int co = qv ? col_off(o, q) : 0;
+    const int co = coff[0];
 #pragma unroll
     for (int p = 0; p < MAXP; ++p) {
-      if (p >= npass) break;
       const int rl = (p * kProdWarps + pt) * 4 + (lane >> 3);  // row within the tile
       if (rl >= nrt) break;
       const int ro = roff[p];
-      const bool v = qv && ro != kZeroRow;
+      const bool v = co != kZeroRow && ro != kZeroRow;
       cp_async16(tile + swz(rl, 4 * c), v ? pbase + (int64_t)ro + co : pbase, v);
     }
   } else {
     const int e = lane & 3;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      const int q = q0 + 4 * c + e;
-      const bool qv = q < o.K;
-      const int co = qv ? col_off(o, q) : 0;
+      const int co = coff[c];
 #pragma unroll
       for (int p = 0; p < MAXP; ++p) {
-        if (p >= npass) break;
         const int rl = (p * kProdWarps + pt) * 8 + (lane >> 2);
         if (rl >= nrt) break;
         const int ro = roff[p];
-        const bool v = qv && ro != kZeroRow;
+        const bool v = co != kZeroRow && ro != kZeroRow;
         const float* src = ro == kOnesRow ? ones : (v ? pbase + (int64_t)ro + co : pbase);
         cp_async4(tile + swz(rl, 4 * c + e), src, v);
       }
@@ -144,8 +168,10 @@ __device__ __forceinline__ void gather_tile(const GOperand& o, const float* pbas
   }
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 template <int EPI, int ACT>
-__global__ void __launch_bounds__(kCThreads, 2) conv_tc_kernel(const __grid_constant__ GParams p) {
+__global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(const __grid_constant__ GParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -182,37 +208,58 @@ __global__ void __launch_bounds__(kCThreads, 2) conv_tc_kernel(const __grid_cons
 
   if (warp < kProdWarps) {
     // ===================== gather producers =====================
+    // Offsets are loaded one step ahead (next k-block's columns, next tile's rows) so the
+    // table lookups overlap the copies instead of stalling every k-block on an L2 round trip;
+    // the column tables are also L1-prefetched 8 k-blocks ahead.
     const uint32_t stages0 = smem_u32(smem);
-    const int pa = p.a.vec ? 8 : 4;                                   // A row passes per thread
-    const int pb = p.b.vec ? (p.nmma + 15) / 16 : (p.nmma + 31) / 32;  // B row passes per thread
     int s = 0;
     uint32_t ph = 0;
-    for (int t = blockIdx.x; t < units; t += gridDim.x) {
+    int t = blockIdx.x;
+    int ra[8], rb[4], ran[8], rbn[4], ca[8], cb[8], can[8], cbn[8];
+    if (t < units) {
+      load_rows<8>(p.a, (t % p.rtiles) * kCBM, kCBM, warp, lane, ra);
+      load_rows<4>(p.b, 0, p.nmma, warp, lane, rb);
+    }
+    load_cols(p.a, 0, lane, ca);
+    load_cols(p.b, 0, lane, cb);
+    while (t < units) {
       const int rt = t % p.rtiles, j = t / p.rtiles;
-      int ra[8], rb[16];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int rl = p.a.vec ? (q * kProdWarps + warp) * 4 + (lane >> 3) : (q * kProdWarps + warp) * 8 + (lane >> 2);
-        ra[q] = q < pa ? row_off(p.a, rt * kCBM + rl) : kZeroRow;
-      }
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int rl = p.b.vec ? (q * kProdWarps + warp) * 4 + (lane >> 3) : (q * kProdWarps + warp) * 8 + (lane >> 2);
-        rb[q] = (q < pb && rl < p.nmma) ? row_off(p.b, rl) : kZeroRow;
+      const int tn = t + gridDim.x;
+      if (tn < units) {
+        load_rows<8>(p.a, (tn % p.rtiles) * kCBM, kCBM, warp, lane, ran);
+        load_rows<4>(p.b, 0, p.nmma, warp, lane, rbn);
       }
       const float* abase = p.a.base + (int64_t)j * p.a.ps;
       const float* bbase = p.b.base + (int64_t)j * p.b.ps;
+      (void)rt;
       for (int kb = 0; kb < p.nkb; ++kb) {
+        const int kbn = kb + 1 < p.nkb ? kb + 1 : 0;  // the next tile starts again at k-block 0
+        load_cols(p.a, kbn, lane, can);
+        load_cols(p.b, kbn, lane, cbn);
+        if (lane == 0 && kb + 8 < p.nkb) {
+          if (p.a.coloff) prefetch_l1(p.a.coloff + (kb + 8) * kCBK);
+          if (p.b.coloff) prefetch_l1(p.b.coloff + (kb + 8) * kCBK);
+        }
         mbar_wait(&empty[s], ph ^ 1);
         const uint32_t st = stages0 + (uint32_t)s * stage_bytes;
-        gather_tile<8>(p.a, abase, p.ones, st, ra, pa, kCBM, kb, warp, lane);
-        gather_tile<16>(p.b, bbase, p.ones, st + a_bytes, rb, pb, p.nmma, kb, warp, lane);
+        gather_tile<8>(p.a, abase, p.ones, st, ra, ca, kCBM, warp, lane);
+        gather_tile<4>(p.b, bbase, p.ones, st + a_bytes, rb, cb, p.nmma, warp, lane);
         cp_async_arrive(&full[s]);
         if (++s == p.stages) {
           s = 0;
           ph ^= 1;
         }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          ca[q] = can[q];
+          cb[q] = cbn[q];
+        }
       }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ra[q] = ran[q];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) rb[q] = rbn[q];
+      t = tn;
     }
     // drain: the CTA may not exit with copies in flight
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -543,6 +590,7 @@ void build_tables(Ctx& c, int64_t mc) {
 
 template <int EPI>
 void launch_gemm(Ctx& c, GParams& p, int act) {
+  if (p.nmma > 64) throw std::invalid_argument("conv: MMA N > 64");
   const size_t stage_bytes = (size_t)kCBM * 128 + (size_t)p.nmma * 128;
   // up to 6 stages, two CTAs per SM when they fit (more producer warps in flight per SM)
   const size_t fixed = 1024 + 64 * 8 + 64;
@@ -564,7 +612,9 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       attr[dv] = true;
     }
-    const int per_sm = std::max(1, std::min(2, (int)((228 * 1024) / (smem + 1024))));
+    int per_sm = 1;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCThreads, smem));
+    per_sm = std::max(1, std::min(2, per_sm));
     const int grid = std::max(1, std::min(units, c.ctc->num_sms * per_sm));
     kern<<<grid, kCThreads, smem, c.stream>>>(p);
     LAUNCHED();
@@ -583,7 +633,7 @@ bool cnn_tc_eligible(const Ctx& c) {
   if (n.nconv < 1) return false;
   for (int i = 0; i < n.nconv; ++i) {
     const ConvDev& d = n.conv[i];
-    if (d.cout % 4 != 0 || d.cout > 256 || d.cin > 256) return false;
+    if (d.cout % 4 != 0 || d.cout > 64 || d.cin > 64) return false;  // MMA N <= 64 (producer row passes)
     if (i > 0 && d.cin % 4 != 0) return false;
   }
   return true;
