@@ -74,11 +74,14 @@ struct GParams {
   int mask_ld;
   const float* theta;  // forward: bias b[n] at theta[j * Dp + boff + n]
   int64_t Dp, boff;
-  // weights: row i < nrows_w is parameter woff + n * Kw + prow[i] (prow[i] < 0: bias boff + n)
+  // weights: row i < nrows_w, column n is parameter woff + prow[i] + pcol[n]; the bias row
+  // (prow[i] < 0) is boff + bcol[n] where bcol[n] >= 0 (other columns of that row are skipped)
   EpiParams e;
   int64_t woff;
-  int Kw, nrows_w;
+  int nrows_w;
   const int* prow;
+  const int* pcol;
+  const int* bcol;
 };
 
 constexpr int kEpiConvFwd = 0, kEpiConvDx = 1, kEpiConvDw = 2;
@@ -88,8 +91,10 @@ __device__ __forceinline__ uint32_t swz(int row, int k) {
   return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((((k >> 2) ^ row) & 7) << 4) + ((k & 3) << 2));
 }
 
+// .ca: allocate in L1 -- an input pixel is re-read by up to k*k rows of the implicit im2col
+// tile, which then hit L1 instead of crossing the L2 -> SM crossbar k*k times
 __device__ __forceinline__ void cp_async16(uint32_t dst, const float* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
 }
 __device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(valid ? 4 : 0) : "memory");
@@ -107,9 +112,10 @@ __device__ __forceinline__ int col_off(const GOperand& o, int q) { return o.colo
 // Column (k) offsets of k-block kb that this lane's copies use: the vector path needs one
 // (16-byte chunk lane % 8), the scalar path eight (element lane % 4 of chunks 0..7).
 // kZeroRow marks columns past K.
+template <bool VEC>
 __device__ __forceinline__ void load_cols(const GOperand& o, int kb, int lane, int* co) {
   const int q0 = kb * kCBK;
-  if (o.vec) {
+  if (VEC) {
     const int q = q0 + 4 * (lane & 7);
     co[0] = q < o.K ? col_off(o, q) : kZeroRow;
   } else {
@@ -128,7 +134,11 @@ __device__ __forceinline__ void load_rows(const GOperand& o, int r0, int nrt, in
 #pragma unroll
   for (int p = 0; p < MAXP; ++p) {
     const int rl = o.vec ? (p * kProdWarps + pt) * 4 + (lane >> 3) : (p * kProdWarps + pt) * 8 + (lane >> 2);
-    ro[p] = rl < nrt ? row_off(o, r0 + rl) : kZeroRow;
+    if (rl >= nrt) {  // past the tile: nothing to copy
+      ro[p] = kZeroRow;
+      continue;
+    }
+    ro[p] = row_off(o, r0 + rl);
   }
 }
 
@@ -136,10 +146,10 @@ __device__ __forceinline__ void load_rows(const GOperand& o, int r0, int nrt, in
 // offsets.  Vector path: lane -> (row lane / 8, 16-byte chunk lane % 8), a warp stores 4 full
 // rows.  Scalar path: lane -> (row lane / 4, element lane % 4 of a chunk), 8 rows x 16 bytes
 // per instruction; both are bank-conflict free under the 128B swizzle.
-template <int MAXP>
+template <int MAXP, bool VEC>
 __device__ __forceinline__ void gather_tile(const GOperand& o, const float* pbase, const float* ones, uint32_t tile,
                                             const int* roff, const int* coff, int nrt, int pt, int lane) {
-  if (o.vec) {
+  if (VEC) {
     const int c = lane & 7;
     const int co = coff[0];
 #pragma unroll
@@ -148,13 +158,14 @@ __device__ __forceinline__ void gather_tile(const GOperand& o, const float* pbas
       if (rl >= nrt) break;
       const int ro = roff[p];
       const bool v = co != kZeroRow && ro != kZeroRow;
-      cp_async16(tile + swz(rl, 4 * c), v ? pbase + (int64_t)ro + co : pbase, v);
+      const float* src = ro == kOnesRow ? ones : (v ? pbase + (int64_t)ro + co : pbase);
+      cp_async16(tile + swz(rl, 4 * c), src, v);
     }
   } else {
     const int e = lane & 3;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      const int co = coff[c];
+      const int co = coff[VEC ? 0 : c];
 #pragma unroll
       for (int p = 0; p < MAXP; ++p) {
         const int rl = (p * kProdWarps + pt) * 8 + (lane >> 2);
@@ -170,7 +181,7 @@ __device__ __forceinline__ void gather_tile(const GOperand& o, const float* pbas
 
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
-template <int EPI, int ACT>
+template <int EPI, int ACT, bool AV>
 __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(const __grid_constant__ GParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -215,50 +226,49 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
     int s = 0;
     uint32_t ph = 0;
     int t = blockIdx.x;
-    int ra[8], rb[4], ran[8], rbn[4], ca[8], cb[8], can[8], cbn[8];
+    constexpr int NCA = AV ? 1 : 8;  // column offsets per k-block this lane needs (A); B is vector
+    int ra[8], rb[16], ran[8], rbn[16], ca[NCA], cb[1], can[NCA], cbn[1];
     if (t < units) {
       load_rows<8>(p.a, (t % p.rtiles) * kCBM, kCBM, warp, lane, ra);
-      load_rows<4>(p.b, 0, p.nmma, warp, lane, rb);
+      load_rows<16>(p.b, 0, p.nmma, warp, lane, rb);
     }
-    load_cols(p.a, 0, lane, ca);
-    load_cols(p.b, 0, lane, cb);
+    load_cols<AV>(p.a, 0, lane, ca);
+    load_cols<true>(p.b, 0, lane, cb);
     while (t < units) {
       const int rt = t % p.rtiles, j = t / p.rtiles;
       const int tn = t + gridDim.x;
       if (tn < units) {
         load_rows<8>(p.a, (tn % p.rtiles) * kCBM, kCBM, warp, lane, ran);
-        load_rows<4>(p.b, 0, p.nmma, warp, lane, rbn);
+        load_rows<16>(p.b, 0, p.nmma, warp, lane, rbn);
       }
       const float* abase = p.a.base + (int64_t)j * p.a.ps;
       const float* bbase = p.b.base + (int64_t)j * p.b.ps;
       (void)rt;
       for (int kb = 0; kb < p.nkb; ++kb) {
         const int kbn = kb + 1 < p.nkb ? kb + 1 : 0;  // the next tile starts again at k-block 0
-        load_cols(p.a, kbn, lane, can);
-        load_cols(p.b, kbn, lane, cbn);
+        load_cols<AV>(p.a, kbn, lane, can);
+        load_cols<true>(p.b, kbn, lane, cbn);
         if (lane == 0 && kb + 8 < p.nkb) {
           if (p.a.coloff) prefetch_l1(p.a.coloff + (kb + 8) * kCBK);
           if (p.b.coloff) prefetch_l1(p.b.coloff + (kb + 8) * kCBK);
         }
         mbar_wait(&empty[s], ph ^ 1);
         const uint32_t st = stages0 + (uint32_t)s * stage_bytes;
-        gather_tile<8>(p.a, abase, p.ones, st, ra, ca, kCBM, warp, lane);
-        gather_tile<4>(p.b, bbase, p.ones, st + a_bytes, rb, cb, p.nmma, warp, lane);
+        gather_tile<8, AV>(p.a, abase, p.ones, st, ra, ca, kCBM, warp, lane);
+        gather_tile<16, true>(p.b, bbase, p.ones, st + a_bytes, rb, cb, p.nmma, warp, lane);
         cp_async_arrive(&full[s]);
         if (++s == p.stages) {
           s = 0;
           ph ^= 1;
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          ca[q] = can[q];
-          cb[q] = cbn[q];
-        }
+        for (int q = 0; q < NCA; ++q) ca[q] = can[q];
+        cb[0] = cbn[0];
       }
 #pragma unroll
       for (int q = 0; q < 8; ++q) ra[q] = ran[q];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) rb[q] = rbn[q];
+      for (int q = 0; q < 16; ++q) rb[q] = rbn[q];
       t = tn;
     }
     // drain: the CTA may not exit with copies in flight
@@ -348,11 +358,18 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
         } else {
           if (r >= p.nrows_w) continue;
           const int pr = p.prow[r];
-          int64_t idx[16];
+          const int64_t base = (int64_t)j * p.Dp;
+          if (pr >= 0) {
+            int64_t idx[16];
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
-            idx[q] = (int64_t)j * p.Dp + (pr >= 0 ? p.woff + (int64_t)(n0 + q) * p.Kw + pr : p.boff + n0 + q);
-          leapfrog_update_n<16>(p.e, j, idx, v, nq);
+            for (int q = 0; q < 16; ++q) idx[q] = base + p.woff + pr + (q < nq ? p.pcol[n0 + q] : 0);
+            leapfrog_update_n<16>(p.e, j, idx, v, nq);
+          } else {  // the bias row: one column per output channel
+            for (int q = 0; q < nq; ++q) {
+              const int b = p.bcol[n0 + q];
+              if (b >= 0) leapfrog_update(p.e, j, base + p.boff + b, v[q]);
+            }
+          }
         }
       }
       tc_fence_before();
@@ -483,24 +500,38 @@ int round_up(int v, int a) { return (v + a - 1) / a * a; }
 }  // namespace
 
 // ---- per-context state ------------------------------------------------------------------------
+// Weight-gradient layout (the "shifted rows" form): with K = (image, y, x') over the input
+// width x' in [0, win_p) (win_p = win rounded up to 4),
+//   dW[co, ci, ky, kx] = sum_K In[ci][y + ky][x'] * dZ[co][y][x' - kx],
+// A rows (ky, ci) read the stage input in a channel-major, width-padded copy (inT: x'
+// contiguous) and B rows (kx, co) read k copies of dZ shifted by kx (dZs), so both operands are
+// 16-byte chunks of 4 consecutive x' -- no scalar im2col gathers -- and N = k * cout.
 struct ConvTcState {
   float* Xr = nullptr;  // tf32-rounded copy of the active X rows (stage-0 operand)
   int64_t Xr_rows = 0;
   float* ones = nullptr;
   int64_t mcap = 0;  // images per chunk the buffers hold
-  int korder[kMaxConv] = {};   // 0: k = (ky, kx, ci) over NHWC input; 1: (ci, ky, kx) over X (NCHW)
-  int nmmaF[kMaxConv] = {}, KpF[kMaxConv] = {}, nmmaD[kMaxConv] = {}, KpD[kMaxConv] = {};
+  int korder[kMaxConv] = {};   // forward k order: 0 = (ky, kx, ci) over NHWC input; 1 = (ci, ky, kx) over X
+  int nmmaF[kMaxConv] = {}, KpF[kMaxConv] = {}, nmmaD[kMaxConv] = {}, KpD[kMaxConv] = {}, nmmaW[kMaxConv] = {};
+  int winp[kMaxConv] = {};     // stage input width padded to a multiple of 4
   float* Wf[kMaxConv] = {};
   float* Wd[kMaxConv] = {};
-  float* dP[kMaxConv] = {};  // delta of a pooled (non-last) stage output, NHWC
+  float* dP[kMaxConv] = {};    // delta of a pooled (non-last) stage output, NHWC
+  float* inT[kMaxConv] = {};   // stage input, [mcap][cin][hin][win_p] (stage 0: shared by all particles)
+  float* dZs[kMaxConv] = {};   // [k][mcap][cout][ho][win_p]: dZ shifted right by kx
   // tables (device, int32)
-  int* fa_row[kMaxConv] = {};  // output pixel -> input pixel base (forward A rows, weight-gradient A columns)
+  int* fa_row[kMaxConv] = {};  // output pixel -> input pixel base (forward A rows)
   int* fa_col[kMaxConv] = {};  // forward k -> offset
-  int* wa_row[kMaxConv] = {};  // weight-gradient A rows: (ky, kx, ci) offsets + the ones row
-  int* prow[kMaxConv] = {};    // weight-gradient row -> parameter offset within W (-1: bias)
   int* zpix[kMaxConv] = {};    // output pixel -> zero-bordered delta buffer position
   int* da_row[kMaxConv] = {};  // delta A rows: input pixel -> dZpad base
   int* da_col[kMaxConv] = {};  // delta k = (ky, kx, co) -> offset
+  int* wa_row[kMaxConv] = {};  // weight-gradient A rows (ky, ci) -> inT offset (+ the ones row)
+  int* wa_col[kMaxConv] = {};  // weight-gradient K (m, y, x') -> inT offset
+  int* wb_row[kMaxConv] = {};  // weight-gradient B rows (kx, co) -> dZs offset
+  int* wb_col[kMaxConv] = {};  // weight-gradient K (m, y, x') -> dZs offset
+  int* prow[kMaxConv] = {};    // weight-gradient row (ky, ci) -> ci*k*k + ky*k (-1: bias row)
+  int* pcol[kMaxConv] = {};    // weight-gradient column (kx, co) -> co*cin*k*k + kx
+  int* bcol[kMaxConv] = {};    // bias row column (kx, co) -> co if kx == 0 else -1
   int num_sms = 148;
 };
 
@@ -515,7 +546,8 @@ T* upload_vec(const std::vector<T>& v) {
 }
 
 void free_tables(ConvTcState* s) {
-  int** t[] = {s->fa_row, s->fa_col, s->wa_row, s->prow, s->zpix, s->da_row, s->da_col};
+  int** t[] = {s->fa_row, s->fa_col, s->zpix, s->da_row, s->da_col, s->wa_row,
+               s->wa_col, s->wb_row, s->wb_col, s->prow, s->pcol, s->bcol};
   for (int** a : t)
     for (int i = 0; i < kMaxConv; ++i)
       if (a[i]) {
@@ -524,18 +556,20 @@ void free_tables(ConvTcState* s) {
       }
 }
 
-// Tables of stage i for chunks of up to `mc` images (host-built, geometry only).
+// Tables of every stage for chunks of up to `mc` images (host-built, geometry only).
 void build_tables(Ctx& c, int64_t mc) {
   ConvTcState* s = c.ctc;
   free_tables(s);
   const NetDev& net = c.net;
   for (int i = 0; i < net.nconv; ++i) {
     const ConvDev& d = net.conv[i];
-    const int k = d.k, kk2 = k * k, pad = k - 1, H2 = d.ho + 2 * pad, W2 = d.wo + 2 * pad;
+    const int k = d.k, kk2 = k * k, pad = k - 1, H2 = d.ho + 2 * pad, W2 = d.wo + 2 * pad, wp = s->winp[i];
     const int64_t npix = (int64_t)d.ho * d.wo, nin = (int64_t)d.hin * d.win;
     const bool x_nchw = i == 0;  // stage 0 reads X [c][h][w]; later stages NHWC activations
     const int64_t limit = (int64_t)1 << 31;
-    if (mc * std::max<int64_t>(nin * d.cin, (int64_t)H2 * W2 * d.cout) >= limit)
+    const int64_t biggest = std::max({nin * d.cin, (int64_t)H2 * W2 * d.cout, (int64_t)d.cin * d.hin * wp,
+                                      (int64_t)k * mc * d.cout * d.ho * wp / std::max<int64_t>(mc, 1)});
+    if (mc * biggest >= limit || (int64_t)k * mc * d.cout * d.ho * wp >= limit)
       throw std::invalid_argument("conv: chunk too large for 32-bit operand tables");
     std::vector<int> fa_row((size_t)(mc * npix)), zpix((size_t)(mc * npix));
     for (int64_t m = 0; m < mc; ++m)
@@ -547,7 +581,7 @@ void build_tables(Ctx& c, int64_t mc) {
           zpix[(size_t)r] = (int)(m * (int64_t)H2 * W2 * d.cout + ((int64_t)(y + pad) * W2 + x + pad) * d.cout);
         }
     const int Kf = d.cin * kk2;
-    std::vector<int> fa_col((size_t)Kf), wa_row((size_t)Kf + 1), prow((size_t)Kf + 1);
+    std::vector<int> fa_col((size_t)Kf);
     for (int q = 0; q < Kf; ++q) {
       int ci, ky, kx;
       if (s->korder[i] == 0) {
@@ -559,18 +593,44 @@ void build_tables(Ctx& c, int64_t mc) {
         ky = (q % kk2) / k;
         kx = q % k;
       }
-      const int off = x_nchw ? (int)(ci * nin + (int64_t)ky * d.win + kx) : (int)(((int64_t)ky * d.win + kx) * d.cin + ci);
-      fa_col[(size_t)q] = off;
-      wa_row[(size_t)q] = off;
-      prow[(size_t)q] = ci * kk2 + ky * k + kx;
+      fa_col[(size_t)q] = x_nchw ? (int)(ci * nin + (int64_t)ky * d.win + kx) : (int)(((int64_t)ky * d.win + kx) * d.cin + ci);
     }
-    wa_row[(size_t)Kf] = kOnesRow;
-    prow[(size_t)Kf] = -1;
     s->fa_row[i] = upload_vec(fa_row);
     s->zpix[i] = upload_vec(zpix);
     s->fa_col[i] = upload_vec(fa_col);
+    // weight gradient (shifted-rows form)
+    const int64_t planeA = (int64_t)d.cin * d.hin * wp, planeB = (int64_t)d.cout * d.ho * wp;
+    std::vector<int> wa_row((size_t)k * d.cin + 1), prow((size_t)k * d.cin + 1);
+    for (int ky = 0; ky < k; ++ky)
+      for (int ci = 0; ci < d.cin; ++ci) {
+        wa_row[(size_t)ky * d.cin + ci] = (int)((int64_t)ci * d.hin * wp + (int64_t)ky * wp);
+        prow[(size_t)ky * d.cin + ci] = ci * kk2 + ky * k;
+      }
+    wa_row[(size_t)k * d.cin] = kOnesRow;
+    prow[(size_t)k * d.cin] = -1;
+    std::vector<int> wa_col((size_t)(mc * d.ho * wp)), wb_col((size_t)(mc * d.ho * wp));
+    for (int64_t m = 0; m < mc; ++m)
+      for (int y = 0; y < d.ho; ++y)
+        for (int x = 0; x < wp; ++x) {
+          const int64_t q = (m * d.ho + y) * wp + x;
+          wa_col[(size_t)q] = (int)(m * planeA + (int64_t)y * wp + x);
+          wb_col[(size_t)q] = (int)(m * planeB + (int64_t)y * wp + x);
+        }
+    std::vector<int> wb_row((size_t)k * d.cout), pcol((size_t)k * d.cout), bcol((size_t)k * d.cout);
+    for (int kx = 0; kx < k; ++kx)
+      for (int co = 0; co < d.cout; ++co) {
+        const size_t n = (size_t)kx * d.cout + co;
+        wb_row[n] = (int)((int64_t)kx * mc * planeB + (int64_t)co * d.ho * wp);
+        pcol[n] = co * Kf + kx;
+        bcol[n] = kx == 0 ? co : -1;
+      }
     s->wa_row[i] = upload_vec(wa_row);
+    s->wa_col[i] = upload_vec(wa_col);
+    s->wb_row[i] = upload_vec(wb_row);
+    s->wb_col[i] = upload_vec(wb_col);
     s->prow[i] = upload_vec(prow);
+    s->pcol[i] = upload_vec(pcol);
+    s->bcol[i] = upload_vec(bcol);
     if (i > 0) {  // delta GEMM of stage i: rows = input pixels of stage i (= stage i-1 output or pool)
       std::vector<int> da_row((size_t)(mc * nin)), da_col((size_t)d.cout * kk2);
       for (int64_t m = 0; m < mc; ++m)
@@ -590,12 +650,13 @@ void build_tables(Ctx& c, int64_t mc) {
 
 template <int EPI>
 void launch_gemm(Ctx& c, GParams& p, int act) {
-  if (p.nmma > 64) throw std::invalid_argument("conv: MMA N > 64");
+  if (p.nmma > 256) throw std::invalid_argument("conv: MMA N > 256");
+  if (!p.b.vec) throw std::invalid_argument("conv: B operands are 16-byte gathers");
   const size_t stage_bytes = (size_t)kCBM * 128 + (size_t)p.nmma * 128;
   // up to 6 stages, two CTAs per SM when they fit (more producer warps in flight per SM)
   const size_t fixed = 1024 + 64 * 8 + 64;
   int stages = (int)std::min<size_t>(6, (110 * 1024 - fixed) / stage_bytes);
-  if (stages < 2) stages = (int)std::min<size_t>(4, (227 * 1024 - fixed) / stage_bytes);
+  if (stages < 3) stages = (int)std::min<size_t>(6, (227 * 1024 - fixed) / stage_bytes);
   if (stages < 2) throw std::invalid_argument("conv: GEMM tile does not fit in shared memory");
   p.stages = stages;
   const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16;
@@ -603,10 +664,11 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
   while (tc < p.nmma) tc <<= 1;
   p.tcols_half = tc;
   const int units = p.rtiles * p.J;
-  auto go = [&](auto act_c) {
+  auto go = [&](auto act_c, auto av_c) {
     constexpr int A_ = decltype(act_c)::value;
-    auto kern = conv_tc_kernel<EPI, A_>;
-    static bool attr[kMaxDevices] = {};  // one flag per (EPI, ACT) instantiation and device
+    constexpr bool AV = decltype(av_c)::value;
+    auto kern = conv_tc_kernel<EPI, A_, AV>;
+    static bool attr[kMaxDevices] = {};  // one flag per instantiation and device
     const int dv = current_device();
     if (!attr[dv]) {
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -615,14 +677,53 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
     int per_sm = 1;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCThreads, smem));
     per_sm = std::max(1, std::min(2, per_sm));
+    if (2 * tc * per_sm > 512) per_sm = 1;  // TMEM: 512 columns per SM
     const int grid = std::max(1, std::min(units, c.ctc->num_sms * per_sm));
     kern<<<grid, kCThreads, smem, c.stream>>>(p);
     LAUNCHED();
   };
+  auto go_av = [&](auto act_c) {
+    if (p.a.vec)
+      go(act_c, std::true_type{});
+    else
+      go(act_c, std::false_type{});
+  };
   if (act == DASMC_RELU)
-    go(std::integral_constant<int, DASMC_RELU>{});
+    go_av(std::integral_constant<int, DASMC_RELU>{});
   else
-    go(std::integral_constant<int, DASMC_TANH>{});
+    go_av(std::integral_constant<int, DASMC_TANH>{});
+}
+
+// [m][c][h][w] (stage 0: X) or NHWC [m][h][w][c] -> [m][c][h][w_p] (x' >= w stays zero)
+__global__ void to_chw_pad_kernel(const float* __restrict__ src, int64_t src_ps, int nhwc, int C, int H, int W, int Wp,
+                                  float* __restrict__ dst, int64_t dst_ps, int64_t M, int64_t J) {
+  const int64_t per = (int64_t)C * H * W, total = J * M * per;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / (M * per), rem = g - j * M * per, m = rem / per;
+    const int o = (int)(rem - m * per);  // (c, y, x) order of the destination
+    const int c = o / (H * W), yx = o - c * H * W, y = yx / W, x = yx - y * W;
+    const float v = src[j * src_ps + m * per + (nhwc ? ((int64_t)yx * C + c) : (int64_t)o)];
+    dst[j * dst_ps + m * (int64_t)C * H * Wp + ((int64_t)c * H + y) * Wp + x] = v;
+  }
+}
+
+// dZs[kx][m][co][y][x'] = dZ(m, y, x' - kx, co) (0 outside [0, wo)), from the zero-bordered
+// NHWC delta buffer; every x' in [0, w_p) is written
+__global__ void dz_shift_kernel(ConvDev d, const float* __restrict__ dZ, int64_t dz_ps, int Wp, float* __restrict__ out,
+                                int64_t out_ps, int64_t kx_stride, int64_t M, int64_t J) {
+  const int pad = d.k - 1, W2 = d.wo + 2 * pad, H2 = d.ho + 2 * pad, C = d.cout;
+  const int64_t per = (int64_t)C * d.ho * Wp, total = J * M * per;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / (M * per), rem = g - j * M * per, m = rem / per;
+    const int o = (int)(rem - m * per);
+    const int co = o / (d.ho * Wp), yx = o - co * d.ho * Wp, y = yx / Wp, x = yx - y * Wp;
+    const float* z = dZ + j * dz_ps + m * (int64_t)H2 * W2 * C + (int64_t)(y + pad) * W2 * C + co;
+    float* w = out + j * out_ps + m * per + o;
+    for (int kx = 0; kx < d.k; ++kx) {
+      const int xs = x - kx + pad;  // padded column of dZ(x - kx)
+      w[kx * kx_stride] = (xs >= 0 && xs < W2) ? z[(int64_t)xs * C] : 0.f;
+    }
+  }
 }
 
 }  // namespace
@@ -633,7 +734,7 @@ bool cnn_tc_eligible(const Ctx& c) {
   if (n.nconv < 1) return false;
   for (int i = 0; i < n.nconv; ++i) {
     const ConvDev& d = n.conv[i];
-    if (d.cout % 4 != 0 || d.cout > 64 || d.cin > 64) return false;  // MMA N <= 64 (producer row passes)
+    if (d.cout % 4 != 0 || d.cout > 64 || d.cin > 64 || d.k * d.cout > 256) return false;  // MMA N <= 256
     if (i > 0 && d.cin % 4 != 0) return false;
   }
   return true;
@@ -653,6 +754,8 @@ void cnn_tc_init(Ctx& c) {
     s->KpF[i] = round_up(d.cin * d.k * d.k, kCBK);
     s->nmmaD[i] = round_up(d.cin, 16);
     s->KpD[i] = round_up(d.cout * d.k * d.k, kCBK);
+    s->nmmaW[i] = round_up(d.k * d.cout, 16);
+    s->winp[i] = round_up(d.win, 4);
     CK(cudaMalloc(&s->Wf[i], sizeof(float) * (size_t)c.Jmax * s->nmmaF[i] * s->KpF[i]));
     if (i > 0) CK(cudaMalloc(&s->Wd[i], sizeof(float) * (size_t)c.Jmax * s->nmmaD[i] * s->KpD[i]));
   }
@@ -682,7 +785,7 @@ void cnn_tc_free(Ctx& c) {
   if (!s) return;
   free_tables(s);
   for (int i = 0; i < kMaxConv; ++i) {
-    float* p[] = {s->Wf[i], s->Wd[i], s->dP[i]};
+    float* p[] = {s->Wf[i], s->Wd[i], s->dP[i], s->inT[i], s->dZs[i]};
     for (float* q : p)
       if (q) cudaFree(q);
   }
@@ -697,8 +800,11 @@ int64_t cnn_tc_image_floats(const Ctx& c) {
   int64_t f = 0;
   for (int i = 0; i < net.nconv; ++i) {
     const ConvDev& d = net.conv[i];
-    f += act_plane(d) + pad_plane(d);
-    if (d.pool || i == net.nconv - 1) f += pool_plane(d) > 0 ? std::max(pool_plane(d), act_plane(d)) : 0;
+    const int64_t wp = round_up(d.win, 4);
+    f += act_plane(d) + pad_plane(d) + (int64_t)d.k * d.cout * d.ho * wp;  // output, delta, shifted deltas
+    if (i > 0) f += (int64_t)d.cin * d.hin * wp;                        // channel-major input copy
+    if (d.pool) f += pool_plane(d);
+    else if (i == net.nconv - 1) f += act_plane(d);  // the flatten copy
     if (d.pool && i + 1 < net.nconv) f += pool_plane(d);
   }
   return f;
@@ -706,25 +812,30 @@ int64_t cnn_tc_image_floats(const Ctx& c) {
 
 // Stage buffers for chunks of mc images: cact = NHWC stage output, cpool = pooled NHWC (or the
 // head's flatten order for the last stage), cdel = zero-bordered NHWC delta, dP = delta of a
-// pooled non-last stage output.
+// pooled non-last stage output, inT / dZs = the weight-gradient operands.
 void cnn_tc_alloc(Ctx& c, int64_t mc) {
   ConvTcState* s = c.ctc;
   const NetDev& net = c.net;
   const size_t J = (size_t)c.Jmax;
   for (int i = 0; i < net.nconv; ++i) {
-    float** bufs[] = {&c.cact[i], &c.cpool[i], &c.cdel[i], &s->dP[i]};
+    float** bufs[] = {&c.cact[i], &c.cpool[i], &c.cdel[i], &s->dP[i], &s->inT[i], &s->dZs[i]};
     for (float** b : bufs)
       if (*b) {
         CK(cudaFree(*b));
         *b = nullptr;
       }
     const ConvDev& d = net.conv[i];
+    const int64_t wp = s->winp[i];
     CK(cudaMalloc(&c.cact[i], sizeof(float) * J * mc * act_plane(d)));
     CK(cudaMalloc(&c.cdel[i], sizeof(float) * J * mc * pad_plane(d)));
     CK(cudaMemsetAsync(c.cdel[i], 0, sizeof(float) * J * mc * pad_plane(d), c.stream));
     const bool last = i == net.nconv - 1;
     if (d.pool || last) CK(cudaMalloc(&c.cpool[i], sizeof(float) * J * mc * (d.pool ? pool_plane(d) : act_plane(d))));
     if (d.pool && !last) CK(cudaMalloc(&s->dP[i], sizeof(float) * J * mc * pool_plane(d)));
+    const size_t in_t = (size_t)mc * d.cin * d.hin * wp * (i == 0 ? 1 : J);  // stage 0: shared
+    CK(cudaMalloc(&s->inT[i], sizeof(float) * in_t));
+    CK(cudaMemsetAsync(s->inT[i], 0, sizeof(float) * in_t, c.stream));  // padding columns stay zero
+    CK(cudaMalloc(&s->dZs[i], sizeof(float) * J * d.k * mc * d.cout * d.ho * wp));
   }
   build_tables(c, mc);
   s->mcap = mc;
@@ -758,9 +869,14 @@ void cnn_tc_forward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t m
     const ConvDev& d = net.conv[i];
     const int64_t R = mc * d.ho * d.wo;
     GParams p{};
-    p.a.base = i == 0 ? s->Xr + m0 * img : c.cpool[i - 1] ? c.cpool[i - 1] : c.cact[i - 1];
-    if (i > 0 && !net.conv[i - 1].pool) p.a.base = c.cact[i - 1];
-    p.a.ps = i == 0 ? 0 : cap * (net.conv[i - 1].pool ? pool_plane(net.conv[i - 1]) : act_plane(net.conv[i - 1]));
+    if (i == 0) {
+      p.a.base = s->Xr + m0 * img;
+      p.a.ps = 0;
+    } else {
+      const ConvDev& dp = net.conv[i - 1];
+      p.a.base = dp.pool ? c.cpool[i - 1] : c.cact[i - 1];
+      p.a.ps = cap * (dp.pool ? pool_plane(dp) : act_plane(dp));
+    }
     p.a.rowoff = s->fa_row[i];
     p.a.nrows = (int)R;
     p.a.coloff = s->fa_col[i];
@@ -821,38 +937,55 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
   }
   for (int i = L; i >= 0; --i) {
     const ConvDev& d = net.conv[i];
-    const int64_t R = mc * d.ho * d.wo;
-    // ---- weight gradient + fused leapfrog: dW[(ky,kx,ci) | bias, co] = sum_r In[., r] dZ[co, r]
+    const int wp = s->winp[i];
+    // ---- weight gradient + fused leapfrog (shifted-rows form, see ConvTcState):
+    //      D[(ky, ci) | ones, (kx, co)] = sum_(m, y, x') inT[ci][y + ky][x'] dZs[kx][co][y][x']
     {
+      const int64_t JA = i == 0 ? 1 : J;
+      const int64_t planeA = (int64_t)d.cin * d.hin * wp;
+      if (i == 0) {
+        to_chw_pad_kernel<<<grid_of(mc * img), 256, 0, c.stream>>>(s->Xr + m0 * img, 0, 0, d.cin, d.hin, d.win, wp,
+                                                                   s->inT[0], 0, mc, 1);
+      } else {
+        const ConvDev& dp = net.conv[i - 1];
+        to_chw_pad_kernel<<<grid_of(JA * mc * d.cin * d.hin * d.win), 256, 0, c.stream>>>(
+            dp.pool ? c.cpool[i - 1] : c.cact[i - 1], cap * (dp.pool ? pool_plane(dp) : act_plane(dp)), 1, d.cin, d.hin,
+            d.win, wp, s->inT[i], cap * planeA, mc, JA);
+      }
+      LAUNCHED();
+      const int64_t planeB = (int64_t)d.cout * d.ho * wp;
+      dz_shift_kernel<<<grid_of(J * mc * planeB), 256, 0, c.stream>>>(d, c.cdel[i], cap * pad_plane(d), wp, s->dZs[i],
+                                                                       (int64_t)d.k * cap * planeB, cap * planeB, mc, J);
+      LAUNCHED();
       GParams p{};
-      const bool x_in = i == 0;
-      p.a.base = x_in ? s->Xr + m0 * img : (net.conv[i - 1].pool ? c.cpool[i - 1] : c.cact[i - 1]);
-      p.a.ps = x_in ? 0 : cap * (net.conv[i - 1].pool ? pool_plane(net.conv[i - 1]) : act_plane(net.conv[i - 1]));
+      p.a.base = s->inT[i];
+      p.a.ps = i == 0 ? 0 : cap * planeA;
       p.a.rowoff = s->wa_row[i];
-      p.a.nrows = d.cin * d.k * d.k + 1;
-      p.a.coloff = s->fa_row[i];
-      p.a.K = (int)R;
-      p.a.vec = 0;
-      p.b.base = c.cdel[i];
-      p.b.ps = cap * pad_plane(d);
-      p.b.ld = 1;
-      p.b.nrows = d.cout;
-      p.b.coloff = s->zpix[i];
-      p.b.K = (int)R;
-      p.b.vec = 0;
+      p.a.nrows = d.k * d.cin + 1;
+      p.a.coloff = s->wa_col[i];
+      p.a.K = (int)(mc * d.ho * wp);
+      p.a.vec = 1;
+      p.b.base = s->dZs[i];
+      p.b.ps = (int64_t)d.k * cap * planeB;
+      p.b.rowoff = s->wb_row[i];
+      p.b.nrows = d.k * d.cout;
+      p.b.coloff = s->wb_col[i];
+      p.b.K = p.a.K;
+      p.b.vec = 1;
       p.ones = s->ones;
       p.J = (int)J;
       p.rtiles = (p.a.nrows + kCBM - 1) / kCBM;
-      p.nkb = (int)((R + kCBK - 1) / kCBK);
-      p.nmma = s->nmmaF[i];
-      p.nvalid = d.cout;
+      p.nkb = (p.a.K + kCBK - 1) / kCBK;
+      p.nmma = s->nmmaW[i];
+      p.nvalid = d.k * d.cout;
       p.Dp = net.Dp;
       p.boff = d.boff;
       p.e = e;
       p.woff = d.woff;
-      p.Kw = d.cin * d.k * d.k;
       p.nrows_w = p.a.nrows;
       p.prow = s->prow[i];
+      p.pcol = s->pcol[i];
+      p.bcol = s->bcol[i];
       launch_gemm<kEpiConvDw>(c, p, net.act);
     }
     if (i == 0) break;
