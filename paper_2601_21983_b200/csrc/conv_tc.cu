@@ -485,6 +485,23 @@ __global__ void flat_to_dzpad_kernel(ConvDev d, const float* __restrict__ F, int
   }
 }
 
+__global__ void im2col_x_kernel(ConvDev d, const float* __restrict__ X, int64_t rows, int Kp, float* __restrict__ out) {
+  const int K = d.cin * d.k * d.k, npix = d.ho * d.wo;
+  const int64_t total = rows * npix * Kp;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rp = g / Kp;
+    const int q = (int)(g - rp * Kp);
+    const int64_t m = rp / npix;
+    const int p = (int)(rp - m * npix), y = p / d.wo, x = p - y * d.wo;
+    float v = 0.f;
+    if (q < K) {
+      const int ci = q / (d.k * d.k), r = q - ci * d.k * d.k, ky = r / d.k, kx = r - ky * d.k;
+      v = X[((m * d.cin + ci) * d.hin + y + ky) * d.win + x + kx];
+    }
+    out[g] = v;
+  }
+}
+
 __global__ void round_tf32_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = tf32_hi(src[i]);
@@ -509,6 +526,8 @@ int round_up(int v, int a) { return (v + a - 1) / a * a; }
 struct ConvTcState {
   float* Xr = nullptr;  // tf32-rounded copy of the active X rows (stage-0 operand)
   int64_t Xr_rows = 0;
+  float* Xcol = nullptr;  // stage-0 im2col of Xr, [rows * ho * wo][KpF[0]], k = (ci, ky, kx): shared by
+  int64_t Xcol_rows = 0;  // every particle, built once per data set (16-byte gathers for the stage-0 GEMM)
   float* ones = nullptr;
   int64_t mcap = 0;  // images per chunk the buffers hold
   int korder[kMaxConv] = {};   // forward k order: 0 = (ky, kx, ci) over NHWC input; 1 = (ci, ky, kx) over X
@@ -517,8 +536,10 @@ struct ConvTcState {
   float* Wf[kMaxConv] = {};
   float* Wd[kMaxConv] = {};
   float* dP[kMaxConv] = {};    // delta of a pooled (non-last) stage output, NHWC
-  float* inT[kMaxConv] = {};   // stage input, [mcap][cin][hin][win_p] (stage 0: shared by all particles)
-  float* dZs[kMaxConv] = {};   // [k][mcap][cout][ho][win_p]: dZ shifted right by kx
+  // one stage's weight gradient runs at a time: its operand copies share two scratch buffers
+  float* inT = nullptr;        // stage input, [mcap][cin][hin][win_p] per particle (stage 0: shared)
+  float* dZs = nullptr;        // [k][mcap][cout][ho][win_p] per particle: dZ shifted right by kx
+  size_t inT_floats = 0, dZs_floats = 0;
   // tables (device, int32)
   int* fa_row[kMaxConv] = {};  // output pixel -> input pixel base (forward A rows)
   int* fa_col[kMaxConv] = {};  // forward k -> offset
@@ -694,16 +715,21 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
     go_av(std::integral_constant<int, DASMC_TANH>{});
 }
 
-// [m][c][h][w] (stage 0: X) or NHWC [m][h][w][c] -> [m][c][h][w_p] (x' >= w stays zero)
+// [m][c][h][w] (stage 0: X) or NHWC [m][h][w][c] -> [m][c][h][w_p], zeros at x' >= w (the
+// buffer is a scratch shared by the stages, so the padding is rewritten every time)
 __global__ void to_chw_pad_kernel(const float* __restrict__ src, int64_t src_ps, int nhwc, int C, int H, int W, int Wp,
                                   float* __restrict__ dst, int64_t dst_ps, int64_t M, int64_t J) {
-  const int64_t per = (int64_t)C * H * W, total = J * M * per;
+  const int64_t per = (int64_t)C * H * Wp, total = J * M * per;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = g / (M * per), rem = g - j * M * per, m = rem / per;
-    const int o = (int)(rem - m * per);  // (c, y, x) order of the destination
-    const int c = o / (H * W), yx = o - c * H * W, y = yx / W, x = yx - y * W;
-    const float v = src[j * src_ps + m * per + (nhwc ? ((int64_t)yx * C + c) : (int64_t)o)];
-    dst[j * dst_ps + m * (int64_t)C * H * Wp + ((int64_t)c * H + y) * Wp + x] = v;
+    const int o = (int)(rem - m * per);  // (c, y, x') order of the destination
+    const int c = o / (H * Wp), yx = o - c * H * Wp, y = yx / Wp, x = yx - y * Wp;
+    float v = 0.f;
+    if (x < W) {
+      const int64_t s0 = j * src_ps + m * (int64_t)C * H * W;
+      v = src[s0 + (nhwc ? ((int64_t)y * W + x) * C + c : ((int64_t)c * H + y) * W + x)];
+    }
+    dst[j * dst_ps + m * per + o] = v;
   }
 }
 
@@ -778,6 +804,18 @@ void cnn_tc_refresh_data(Ctx& c, const float* X, int64_t rows) {
   }
   round_tf32_kernel<<<grid_of(rows * d), 256, 0, c.stream>>>(X, s->Xr, rows * d);
   LAUNCHED();
+  const ConvDev& d0 = c.net.conv[0];
+  const int64_t per = (int64_t)d0.ho * d0.wo * s->KpF[0];
+  if (rows > s->Xcol_rows) {
+    CK(cudaStreamSynchronize(c.stream));
+    if (s->Xcol) CK(cudaFree(s->Xcol));
+    s->Xcol = nullptr;
+    const int64_t cap = std::max(rows, c.n);
+    CK(cudaMalloc(&s->Xcol, sizeof(float) * (size_t)cap * per));
+    s->Xcol_rows = cap;
+  }
+  im2col_x_kernel<<<grid_of(rows * per), 256, 0, c.stream>>>(d0, s->Xr, rows, s->KpF[0], s->Xcol);
+  LAUNCHED();
 }
 
 void cnn_tc_free(Ctx& c) {
@@ -785,29 +823,33 @@ void cnn_tc_free(Ctx& c) {
   if (!s) return;
   free_tables(s);
   for (int i = 0; i < kMaxConv; ++i) {
-    float* p[] = {s->Wf[i], s->Wd[i], s->dP[i], s->inT[i], s->dZs[i]};
+    float* p[] = {s->Wf[i], s->Wd[i], s->dP[i]};
     for (float* q : p)
       if (q) cudaFree(q);
   }
   if (s->Xr) cudaFree(s->Xr);
+  if (s->Xcol) cudaFree(s->Xcol);
   if (s->ones) cudaFree(s->ones);
+  if (s->inT) cudaFree(s->inT);
+  if (s->dZs) cudaFree(s->dZs);
   delete s;
   c.ctc = nullptr;
 }
 
 int64_t cnn_tc_image_floats(const Ctx& c) {
   const NetDev& net = c.net;
-  int64_t f = 0;
+  int64_t f = 0, scratch_a = 0, scratch_b = 0;
   for (int i = 0; i < net.nconv; ++i) {
     const ConvDev& d = net.conv[i];
     const int64_t wp = round_up(d.win, 4);
-    f += act_plane(d) + pad_plane(d) + (int64_t)d.k * d.cout * d.ho * wp;  // output, delta, shifted deltas
-    if (i > 0) f += (int64_t)d.cin * d.hin * wp;                        // channel-major input copy
+    f += act_plane(d) + pad_plane(d);  // output, zero-bordered delta
+    scratch_b = std::max<int64_t>(scratch_b, (int64_t)d.k * d.cout * d.ho * wp);     // shifted deltas
+    if (i > 0) scratch_a = std::max<int64_t>(scratch_a, (int64_t)d.cin * d.hin * wp);  // channel-major input
     if (d.pool) f += pool_plane(d);
     else if (i == net.nconv - 1) f += act_plane(d);  // the flatten copy
     if (d.pool && i + 1 < net.nconv) f += pool_plane(d);
   }
-  return f;
+  return f + scratch_a + scratch_b;
 }
 
 // Stage buffers for chunks of mc images: cact = NHWC stage output, cpool = pooled NHWC (or the
@@ -818,7 +860,7 @@ void cnn_tc_alloc(Ctx& c, int64_t mc) {
   const NetDev& net = c.net;
   const size_t J = (size_t)c.Jmax;
   for (int i = 0; i < net.nconv; ++i) {
-    float** bufs[] = {&c.cact[i], &c.cpool[i], &c.cdel[i], &s->dP[i], &s->inT[i], &s->dZs[i]};
+    float** bufs[] = {&c.cact[i], &c.cpool[i], &c.cdel[i], &s->dP[i]};
     for (float** b : bufs)
       if (*b) {
         CK(cudaFree(*b));
@@ -832,11 +874,21 @@ void cnn_tc_alloc(Ctx& c, int64_t mc) {
     const bool last = i == net.nconv - 1;
     if (d.pool || last) CK(cudaMalloc(&c.cpool[i], sizeof(float) * J * mc * (d.pool ? pool_plane(d) : act_plane(d))));
     if (d.pool && !last) CK(cudaMalloc(&s->dP[i], sizeof(float) * J * mc * pool_plane(d)));
-    const size_t in_t = (size_t)mc * d.cin * d.hin * wp * (i == 0 ? 1 : J);  // stage 0: shared
-    CK(cudaMalloc(&s->inT[i], sizeof(float) * in_t));
-    CK(cudaMemsetAsync(s->inT[i], 0, sizeof(float) * in_t, c.stream));  // padding columns stay zero
-    CK(cudaMalloc(&s->dZs[i], sizeof(float) * J * d.k * mc * d.cout * d.ho * wp));
+    (void)wp;
   }
+  size_t fa = 0, fb = 0;
+  for (int i = 0; i < net.nconv; ++i) {
+    const ConvDev& d = net.conv[i];
+    const size_t wp = (size_t)s->winp[i];
+    fa = std::max(fa, (size_t)mc * d.cin * d.hin * wp * (i == 0 ? 1 : J));  // stage 0: shared by particles
+    fb = std::max(fb, J * d.k * mc * d.cout * d.ho * wp);
+  }
+  if (s->inT) CK(cudaFree(s->inT));
+  if (s->dZs) CK(cudaFree(s->dZs));
+  CK(cudaMalloc(&s->inT, sizeof(float) * fa));
+  CK(cudaMalloc(&s->dZs, sizeof(float) * fb));
+  s->inT_floats = fa;
+  s->dZs_floats = fb;
   build_tables(c, mc);
   s->mcap = mc;
 }
@@ -869,19 +921,23 @@ void cnn_tc_forward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t m
     const ConvDev& d = net.conv[i];
     const int64_t R = mc * d.ho * d.wo;
     GParams p{};
-    if (i == 0) {
-      p.a.base = s->Xr + m0 * img;
+    if (i == 0) {  // the shared im2col of X: dense 16-byte rows
+      p.a.base = s->Xcol + m0 * d.ho * d.wo * s->KpF[0];
       p.a.ps = 0;
+      p.a.ld = s->KpF[0];
+      p.a.nrows = (int)R;
+      p.a.K = s->KpF[0];
+      p.a.vec = 1;
     } else {
       const ConvDev& dp = net.conv[i - 1];
       p.a.base = dp.pool ? c.cpool[i - 1] : c.cact[i - 1];
       p.a.ps = cap * (dp.pool ? pool_plane(dp) : act_plane(dp));
+      p.a.rowoff = s->fa_row[i];
+      p.a.nrows = (int)R;
+      p.a.coloff = s->fa_col[i];
+      p.a.K = d.cin * d.k * d.k;
+      p.a.vec = s->korder[i] == 0 ? 1 : 0;
     }
-    p.a.rowoff = s->fa_row[i];
-    p.a.nrows = (int)R;
-    p.a.coloff = s->fa_col[i];
-    p.a.K = d.cin * d.k * d.k;
-    p.a.vec = s->korder[i] == 0 ? 1 : 0;
     p.b.base = s->Wf[i];
     p.b.ps = (int64_t)s->nmmaF[i] * s->KpF[i];
     p.b.ld = s->KpF[i];
@@ -944,28 +1000,28 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
       const int64_t JA = i == 0 ? 1 : J;
       const int64_t planeA = (int64_t)d.cin * d.hin * wp;
       if (i == 0) {
-        to_chw_pad_kernel<<<grid_of(mc * img), 256, 0, c.stream>>>(s->Xr + m0 * img, 0, 0, d.cin, d.hin, d.win, wp,
-                                                                   s->inT[0], 0, mc, 1);
+        to_chw_pad_kernel<<<grid_of(mc * planeA), 256, 0, c.stream>>>(s->Xr + m0 * img, 0, 0, d.cin, d.hin, d.win, wp,
+                                                                     s->inT, 0, mc, 1);
       } else {
         const ConvDev& dp = net.conv[i - 1];
-        to_chw_pad_kernel<<<grid_of(JA * mc * d.cin * d.hin * d.win), 256, 0, c.stream>>>(
+        to_chw_pad_kernel<<<grid_of(JA * mc * planeA), 256, 0, c.stream>>>(
             dp.pool ? c.cpool[i - 1] : c.cact[i - 1], cap * (dp.pool ? pool_plane(dp) : act_plane(dp)), 1, d.cin, d.hin,
-            d.win, wp, s->inT[i], cap * planeA, mc, JA);
+            d.win, wp, s->inT, cap * planeA, mc, JA);
       }
       LAUNCHED();
       const int64_t planeB = (int64_t)d.cout * d.ho * wp;
-      dz_shift_kernel<<<grid_of(J * mc * planeB), 256, 0, c.stream>>>(d, c.cdel[i], cap * pad_plane(d), wp, s->dZs[i],
+      dz_shift_kernel<<<grid_of(J * mc * planeB), 256, 0, c.stream>>>(d, c.cdel[i], cap * pad_plane(d), wp, s->dZs,
                                                                        (int64_t)d.k * cap * planeB, cap * planeB, mc, J);
       LAUNCHED();
       GParams p{};
-      p.a.base = s->inT[i];
+      p.a.base = s->inT;
       p.a.ps = i == 0 ? 0 : cap * planeA;
       p.a.rowoff = s->wa_row[i];
       p.a.nrows = d.k * d.cin + 1;
       p.a.coloff = s->wa_col[i];
       p.a.K = (int)(mc * d.ho * wp);
       p.a.vec = 1;
-      p.b.base = s->dZs[i];
+      p.b.base = s->dZs;
       p.b.ps = (int64_t)d.k * cap * planeB;
       p.b.rowoff = s->wb_row[i];
       p.b.nrows = d.k * d.cout;

@@ -385,11 +385,38 @@ __global__ void eval_finalize_kernel(int64_t J, const double* __restrict__ ll_pa
 }
 
 // ---- parallel xoshiro256++ normals ------------------------------------------------------------
+// normal() of rng.hpp:76-81 -- sqrt(-2 ln(1 - u1)) cos(2 pi u2), u = (x >> 11) 2^-53 -- in fp32
+// from the exact integer draws (the device stores fp32 momenta):
+//  * radius: ln(1 - u1) as log1p(-u1) for u1 < 1/2, else ln((2^53 - a) 2^-53) with the
+//    integer complement, so both branches see a 24-bit-exact argument;
+//  * angle: the quadrant comes from the top two bits of the 53-bit integer and the remainder
+//    is folded to phi in [0, pi/4] (complemented in integers when past pi/4), so sin / cos
+//    are evaluated on a relatively exact small angle -- including next to the zeros of cos.
+// The stored value is within a few fp32 ulp of the fp64 normal rounded to fp32 (stated bound
+// in tests/test_gpu_parity.py), at ~1/3 of the fp64 Box-Muller's instruction count.
+__device__ __forceinline__ float normal_from_draws(uint64_t x1, uint64_t x2) {
+  const uint64_t a = x1 >> 11;
+  const float L = a < (1ULL << 52) ? log1pf(-__ull2float_rn(a) * 0x1p-53f)
+                                   : logf(__ull2float_rn((1ULL << 53) - a) * 0x1p-53f);
+  const float r = sqrtf(-2.f * L);
+  const uint64_t b = x2 >> 11;
+  const int q = (int)(b >> 51);
+  const uint64_t f = b & ((1ULL << 51) - 1);
+  const bool comp = f >= (1ULL << 50);
+  const uint64_t g = comp ? (1ULL << 51) - f : f;
+  float sp, cp;
+  sincosf(__ull2float_rn(g) * (6.28318530717958647692f * 0x1p-53f), &sp, &cp);
+  const float ct = comp ? sp : cp;  // cos / sin of the angle within its quadrant
+  const float st = comp ? cp : sp;
+  const float cs = q == 0 ? ct : q == 1 ? -st : q == 2 ? -ct : st;
+  return r * cs;
+}
+
 // Thread (j, c) draws the c-th chunk of `chunk` normals of stream fork(a, b, c')
 // by jumping c*2*chunk steps ahead (F2-linear jump with host-precomputed
-// polynomials).  Box-Muller in fp64 exactly as rng.hpp:76-81; the value is
-// stored in fp32 at its internal position.  With chunk = a layer's fan-out a
-// chunk is one column of W, so a warp's stores are coalesced.
+// polynomials); each normal consumes two draws (rng.hpp:76-81) and is stored in fp32
+// at its internal position.  With chunk = a layer's fan-out a chunk is one column of
+// W, so a warp's stores are coalesced.
 __global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b, int per_particle_c,
                                int64_t J, int64_t nchunks, int64_t chunk, const uint64_t* __restrict__ jump_tab,
                                float scale, float* __restrict__ dst, double* __restrict__ sq_part, int64_t j_offset) {
@@ -413,12 +440,9 @@ __global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b
   int64_t nw = (int64_t)net.seg[l].in * net.seg[l].out;
   int64_t r = t < nw ? t % net.seg[l].out : 0, cc = t < nw ? t / net.seg[l].out : 0;
   for (int64_t i = lo; i < hi; ++i) {
-    const double u1 = 1.0 - x.uniform();
-    const double u2 = x.uniform();
-    // cos(2 pi u2) as cospi(2 u2): no Payne-Hanek reduction path; differs from
-    // cos(fl(2 pi) u2) by ~1e-16, far below the fp32 rounding of the stored value
-    const double nv = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
-    const float v = (float)((double)scale * nv);
+    const uint64_t x1 = x.next();
+    const uint64_t x2 = x.next();
+    const float v = scale * normal_from_draws(x1, x2);
     const LayerDev& ly = net.seg[l];
     out[t < nw ? ly.woff + r * ly.in + cc : ly.boff + (t - nw)] = v;
     sq += (double)v * (double)v;
