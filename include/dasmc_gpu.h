@@ -344,6 +344,14 @@ int dasmc_gpu_create_multi(const dasmc_net_desc* net, const float* X, const int3
                            int max_particles, const int* devices, int ndev, int precision, dasmc_ctx** out);
 int dasmc_gpu_multi_shards(const dasmc_ctx* ctx); /* G (1 for a single context) */
 
+/* CUDA-graph replay of smc_step (single contexts; SURVEY.md §7 hard part 7: small configs are
+ * launch-bound).  The step's kernels read the iteration / record slot / resampling key from
+ * device memory, so one instantiated graph per step signature (buffer rotation, target,
+ * kernel configuration, resampling options, allocations) replays every iteration with only
+ * its first node's argument updated.  Results are bit-identical to eager launches.  Off by
+ * default; ignored while the start-gradient cache is on. */
+int dasmc_gpu_set_graphs(dasmc_ctx* ctx, int enable);
+
 /* ---- instrumentation (bench.py) ------------------------------------------------------ */
 /* The context's CUDA stream (cudaStream_t) -- every kernel of the context runs on it. */
 void* dasmc_gpu_stream(dasmc_ctx* ctx);

@@ -108,6 +108,7 @@ SIGNATURES = {
     "dasmc_gpu_create_multi": (C.c_int, [C.POINTER(NetDesc), _F, _I32, C.c_int64, C.c_int, C.POINTER(C.c_int), C.c_int,
                                           C.c_int, C.POINTER(_P)]),
     "dasmc_gpu_multi_shards": (C.c_int, [_P]),
+    "dasmc_gpu_set_graphs": (C.c_int, [_P, C.c_int]),
     "dasmc_gpu_init_ensemble": (C.c_int, [_P, C.c_int64, C.c_uint64]),
     "dasmc_gpu_set_ensemble": (C.c_int, [_P, _D, _D, C.c_int64, C.c_int]),
     "dasmc_gpu_get_ensemble": (C.c_int, [_P, _D, _D, C.POINTER(C.c_int)]),

@@ -341,6 +341,9 @@ class GpuEnsembleTarget:
         L.check(self.lib.dasmc_gpu_sda_moments(self.h, prefix_end, block_end, _dp(out)))
         return out
 
+    def set_graphs(self, enable: bool = True):  # CUDA-graph replay of smc_step (launch-bound configs)
+        L.check(self.lib.dasmc_gpu_set_graphs(self.h, 1 if enable else 0))
+
     def set_cache_start(self, enable: bool = True):  # SPEC.md:410 start-gradient cache (opt-in)
         L.check(self.lib.dasmc_gpu_set_cache_start(self.h, 1 if enable else 0))
 

@@ -138,16 +138,19 @@ NetDev make_net(const dasmc_net_desc* d) {
 // floats per input row: the MLP input or the CNN image
 int64_t input_floats(const NetDev& n) { return n.nconv > 0 ? (int64_t)n.in_c * n.in_h * n.in_w : n.sizes[0]; }
 
+void graphs_free(Ctx& c);
+
 void free_ctx(Ctx& c) {
   cudaSetDevice(c.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
+  graphs_free(c);
   tc_free(c);
   cnn_tc_free(c);
   if (c.gacc) cudaFree(c.gacc);
   void* ptrs[] = {c.X_full, c.Xt, c.y_full, c.Xg, c.yg, c.rows_dev, c.gcache[0], c.gcache[1], c.lt_cache, c.theta[0], c.theta[1], c.theta[2], c.p, c.grad, c.logw, c.dT, c.ll_part,
                   c.th_part, c.p_part, c.p0_part, c.p0_sum, c.pS_sum, c.flags, c.lt_old, c.lt_new, c.ll_pre, c.ll_blk, c.ll_pre0, c.ll_blk0,
                   c.sda_pre, c.sda_blk, c.wts, c.cdf,
-                  c.uni, c.idx, c.records, c.jump_tab, c.stage, c.sh_buf, c.sh_idx, c.sh_rows, c.iota};
+                  c.uni, c.idx, c.records, c.jump_tab, c.stage, c.sh_buf, c.sh_idx, c.sh_rows, c.iota, c.dstep};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int l = 0; l <= kMaxLayers; ++l)
@@ -260,7 +263,7 @@ void cache_signature_store(Ctx& c) {
 // (smc.hpp:118-122, kernels.hpp:75-99).  Global slot of local particle j is
 // j_offset + j (RNG streams).  Returns the buffer index (relative to c.start)
 // holding theta_S.
-int propose_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int64_t j_offset) {
+int propose_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int64_t j_offset, const DevStep* ds = nullptr) {
   check_kernel_cfg(kc);
   if (!c.has_ensemble) throw InvalidArg("smc_step: no ensemble (call init_ensemble or set_ensemble)");
   validate_target(c);
@@ -272,7 +275,7 @@ int propose_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int64_t j_o
   target_rows(c, M, P, br);
   launch_zero_ints(c, c.flags, J);
   // fresh momenta p0 ~ N(0, I) from root.fork(kProposal, k, j) (smc.hpp:119-120; kernels.hpp:131)
-  launch_normals(c, seed, tag::kProposal, (uint64_t)k, J, 1.0f, c.p, c.p0_part, j_offset);
+  launch_normals(c, seed, tag::kProposal, (uint64_t)k, J, 1.0f, c.p, c.p0_part, j_offset, ds);
   const int t0 = c.start, t1 = (c.start + 1) % 3, t2 = (c.start + 2) % 3;
   float* bufs[3] = {c.theta[t0], c.theta[t1], c.theta[t2]};
   int in_idx = 0;
@@ -308,10 +311,14 @@ void smc_step_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind
   const int k = c.iteration;
   const int t1 = (c.start + 1) % 3, t2 = (c.start + 2) % 3;
   float* bufs[3] = {c.theta[c.start], c.theta[t1], c.theta[t2]};
-  const int end_idx = propose_async(c, kc, seed, 0);  // theta_S
+  // the step's scalars (iteration, record slot, resampling stream key) go to device memory
+  // first, so a captured graph of this sequence replays with only that argument changed
+  const DevStep ds{k, slot, fork_key(seed, tag::kResample, (uint64_t)k, 0)};
+  launch_set_step(c, ds);
+  const int end_idx = propose_async(c, kc, seed, 0, c.dstep);  // theta_S
   // resampling uniforms from root.fork(kResample, k) (smc.hpp:152)
-  launch_uniforms(c, fork_key(seed, tag::kResample, (uint64_t)k, 0), rkind == DASMC_MULTINOMIAL ? J : 1, c.uni);
-  launch_weights_and_resample(c, J, fraction, always, rkind, slot, k, 0.0);
+  launch_uniforms(c, ds.ukey, rkind == DASMC_MULTINOMIAL ? J : 1, c.uni, c.dstep);
+  launch_weights_and_resample(c, J, fraction, always, rkind, slot, k, 0.0, c.dstep);
   const int dst_idx = end_idx == 1 ? 2 : 1;  // the free trajectory buffer
   launch_gather(c, bufs[0], bufs[end_idx], bufs[dst_idx], J);
   launch_gather_parts(c, J);  // the post-step ensemble's (prefix, block) ll, for sda_advance
@@ -325,6 +332,130 @@ void smc_step_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind
   c.step_M = c.block_end;
   c.start = dst_idx == 1 ? t1 : t2;
   c.iteration = k + 1;  // smc.hpp:150, 154
+}
+
+// ---- CUDA-graph replay of smc_step (launch-bound configs, SURVEY.md §7 hard part 7) --------------
+// The step's launch sequence depends on the buffer rotation, the target, the kernel
+// configuration and the allocations, never on the iteration (DevStep carries that), so one
+// instantiated graph per signature replays every iteration with that signature.  The first
+// occurrence of a signature runs eagerly (warming lazily created state), the second captures.
+constexpr int kMaxGraphs = 16;
+
+void graphs_free(Ctx& c) {
+  for (int i = 0; i < c.n_graphs; ++i) cudaGraphExecDestroy(c.graphs[i].exec);
+  delete[] c.graphs;
+  c.graphs = nullptr;
+  c.n_graphs = 0;
+  c.seen_valid = false;
+}
+
+void step_signature(const Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind, double fraction, int always,
+                    int64_t* sig) {
+  auto bits = [](double v) {
+    int64_t b;
+    std::memcpy(&b, &v, sizeof b);
+    return b;
+  };
+  const int64_t v[kSigLen] = {c.start, c.J, c.mode, c.prefix_end, c.block_end, c.total_n, bits(c.beta), bits(c.sigma),
+                              bits(kc.step_size), kc.leapfrog_steps, kc.kind, (int64_t)seed, rkind, bits(fraction),
+                              always, (int64_t)(uintptr_t)c.X, c.alloc_epoch, c.Mcap, c.ll_slots,
+                              c.tc ? 1 : 0, c.n_active, c.cache_start ? 1 : 0, 0, 0};
+  std::memcpy(sig, v, sizeof v);
+}
+
+GraphEntry* find_graph(Ctx& c, const int64_t* sig) {
+  for (int i = 0; i < c.n_graphs; ++i)
+    if (std::memcmp(c.graphs[i].sig, sig, sizeof(int64_t) * kSigLen) == 0) return &c.graphs[i];
+  return nullptr;
+}
+
+void smc_step_async(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind, double fraction, int always,
+                    int slot);
+
+// One smc_step through the graph cache (falls back to eager launches while a signature is new).
+void smc_step_graphed(Ctx& c, const dasmc_kernel_cfg& kc, uint64_t seed, int rkind, double fraction, int always,
+                      int slot) {
+  check_kernel_cfg(kc);
+  if (!c.has_ensemble) throw InvalidArg("smc_step: no ensemble (call init_ensemble or set_ensemble)");
+  validate_target(c);
+  ensure_activation_capacity(c, c.block_end);  // never inside a capture
+  int64_t sig[kSigLen];
+  step_signature(c, kc, seed, rkind, fraction, always, sig);
+  GraphEntry* e = find_graph(c, sig);
+  const int k = c.iteration;
+  if (!e) {
+    const bool seen = c.seen_valid && std::memcmp(c.seen_sig, sig, sizeof sig) == 0;
+    if (!seen || c.n_graphs >= kMaxGraphs) {
+      std::memcpy(c.seen_sig, sig, sizeof sig);
+      c.seen_valid = true;
+      smc_step_async(c, kc, seed, rkind, fraction, always, slot);
+      return;
+    }
+    if (!c.graphs) c.graphs = new GraphEntry[kMaxGraphs];
+    const int start0 = c.start;
+    const long long n0 = g_launch_count.load();
+    cudaGraph_t g = nullptr;
+    c.capturing = true;
+    CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      smc_step_async(c, kc, seed, rkind, fraction, always, slot);
+    } catch (...) {
+      cudaStreamEndCapture(c.stream, &g);
+      if (g) cudaGraphDestroy(g);
+      c.capturing = false;
+      throw;
+    }
+    CK(cudaStreamEndCapture(c.stream, &g));
+    c.capturing = false;
+    GraphEntry& ne = c.graphs[c.n_graphs];
+    std::memcpy(ne.sig, sig, sizeof sig);
+    ne.start_after = c.start;
+    ne.launches = g_launch_count.load() - n0;
+    g_launch_count.fetch_sub(ne.launches);  // captured, not launched
+    ne.node = nullptr;
+    size_t nn = 0;
+    CK(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+    for (cudaGraphNode_t n : nodes) {
+      cudaGraphNodeType t;
+      CK(cudaGraphNodeGetType(n, &t));
+      if (t != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp{};
+      CK(cudaGraphKernelNodeGetParams(n, &kp));
+      if (kp.func == set_step_kernel_fn()) {
+        ne.node = n;
+        ne.params = kp;
+        break;
+      }
+    }
+    if (!ne.node) {
+      cudaGraphDestroy(g);
+      throw CudaError{"graph capture: step-parameter node not found"};
+    }
+    CK(cudaGraphInstantiate(&ne.exec, g, 0));
+    CK(cudaGraphDestroy(g));  // the exec keeps its own copy; node handles stay valid for updates
+    ++c.n_graphs;
+    e = &ne;
+    c.start = start0;  // nothing ran yet: replay below
+  }
+  DevStep v{k, slot, fork_key(seed, tag::kResample, (uint64_t)k, 0)};
+  DevStep* dptr = c.dstep;
+  void* args[2] = {&v, &dptr};
+  cudaKernelNodeParams kp = e->params;
+  kp.kernelParams = args;
+  kp.extra = nullptr;
+  CK(cudaGraphExecKernelNodeSetParams(e->exec, e->node, &kp));
+  CK(cudaGraphLaunch(e->exec, c.stream));
+  g_launch_count.fetch_add(e->launches);
+  // the host-side effects smc_step_async has on the context
+  c.last_step_cached = false;
+  c.cache_valid = false;
+  c.step_parts_valid = true;
+  c.step_P = c.mode == DASMC_SDA ? c.prefix_end : c.block_end;
+  c.step_M = c.block_end;
+  c.start = e->start_after;
+  c.iteration = k + 1;
 }
 
 dasmc_iter_record read_record(Ctx& c, int slot) {
@@ -448,7 +579,9 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
   {
     int64_t widest = 0;
     for (int l = 1; l <= c.net.L; ++l) widest = std::max<int64_t>(widest, c.net.sizes[l]);
-    c.rng_chunk = widest >= 128 ? widest : kRngChunkNormals;
+    // a few whole columns per thread: the 256-step F2 jump-ahead is paid once per ~1024 normals
+    // (warp stores stay within a few 32-byte sectors per row)
+    c.rng_chunk = widest >= 128 ? widest * std::max<int64_t>(1, kRngChunkNormals / widest) : kRngChunkNormals;
   }
   const int64_t nch_rng = (c.net.D + c.rng_chunk - 1) / c.rng_chunk;
   c.rng_slots = (int)nch_rng;
@@ -472,6 +605,7 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
   dmalloc(c.uni, (size_t)Jmax);
   dmalloc(c.idx, (size_t)Jmax);
   dmalloc(c.records, (size_t)kRecRing * 8);
+  dmalloc(c.dstep, 1);
   {
     std::vector<int32_t> io((size_t)Jmax);
     for (int i = 0; i < Jmax; ++i) io[(size_t)i] = i;
@@ -863,7 +997,10 @@ int dasmc_gpu_smc_step(dasmc_ctx* ctx, const dasmc_kernel_cfg* cfg, uint64_t see
     CK(cudaSetDevice(c.device));
     const int slot = c.rec_head % kRecRing;
     CK(cudaEventRecord(c.ev0, c.stream));
-    smc_step_async(c, *cfg, seed, resample_kind, fraction, resample_always, slot);
+    if (c.use_graphs && !c.cache_start)
+      smc_step_graphed(c, *cfg, seed, resample_kind, fraction, resample_always, slot);
+    else
+      smc_step_async(c, *cfg, seed, resample_kind, fraction, resample_always, slot);
     CK(cudaEventRecord(c.ev1, c.stream));
     ++c.rec_head;
     if (record) {
@@ -1785,6 +1922,18 @@ int dasmc_gpu_create_multi(const dasmc_net_desc* net, const float* X, const int3
 }
 
 int dasmc_gpu_multi_shards(const dasmc_ctx* ctx) { return ctx && ctx->multi ? ctx->multi->G : 1; }
+
+int dasmc_gpu_set_graphs(dasmc_ctx* ctx, int enable) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg("null ctx");
+    if (ctx->multi) throw InvalidArg("set_graphs: single contexts only");
+    Ctx& c = ctx->c;
+    CK(cudaSetDevice(c.device));
+    CK(cudaStreamSynchronize(c.stream));
+    graphs_free(c);
+    c.use_graphs = enable != 0;
+  });
+}
 
 }  // extern "C"
 

@@ -69,6 +69,13 @@ struct GParams {
   int64_t out_ps;
   const int* outoff;
   int out_ld;
+  // second, channel-major copy of the output (the weight-gradient operands): value (r, n) also
+  // goes to out2[j * out2_ps + out2off[r] + n * out2_cs + kx * (out2_ks + 1)] for kx < out2_k
+  // (out2_k = 1: the next stage's input copy; k: the kx-shifted delta copies)
+  float* out2;
+  int64_t out2_ps, out2_cs, out2_ks;
+  const int* out2off;
+  int out2_k;
   const float* mask;  // delta: act'(mask[j * mask_ps + maskoff[r] + n]) (nullptr: identity)
   int64_t mask_ps;
   int mask_ld;
@@ -355,6 +362,15 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
             for (int q = 0; q < 16; ++q)
               if (q < nq) dst[q] = v[q];
           }
+          if (p.out2) {  // lanes are consecutive pixels: each (channel, kx) store is coalesced
+            float* d2 = p.out2 + (int64_t)j * p.out2_ps + p.out2off[r] + (int64_t)n0 * p.out2_cs;
+            for (int kx = 0; kx < p.out2_k; ++kx) {
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                if (q < nq) d2[(int64_t)q * p.out2_cs] = v[q];
+              d2 += p.out2_ks + 1;
+            }
+          }
         } else {
           if (r >= p.nrows_w) continue;
           const int pr = p.prow[r];
@@ -416,7 +432,8 @@ __global__ void conv_wcopy_kernel(const float* __restrict__ theta, int64_t Dp, i
 // 2x2/2 max-pool forward of an NHWC stage output; flat != 0 writes the flatten order (c, y, x)
 // of the head input instead of NHWC.
 __global__ void pool_fwd_nhwc_kernel(ConvDev d, const float* __restrict__ A, int64_t a_ps, float* __restrict__ P,
-                                     int64_t p_ps, int64_t M, int64_t J, int flat) {
+                                     int64_t p_ps, int64_t M, int64_t J, int flat, float* __restrict__ T, int64_t t_ps,
+                                     int t_wp) {
   const int C = d.cout;
   const int64_t per = (int64_t)d.sh * d.sw * C, total = J * M * per;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
@@ -427,6 +444,8 @@ __global__ void pool_fwd_nhwc_kernel(ConvDev d, const float* __restrict__ A, int
     const int64_t rowC = (int64_t)d.wo * C;
     const float v = fmaxf(fmaxf(a[0], a[C]), fmaxf(a[rowC], a[rowC + C]));
     P[j * p_ps + m * per + (flat ? (int64_t)c * d.sh * d.sw + pyx : o)] = v;
+    // the next stage's channel-major, width-padded input copy (its weight-gradient operand)
+    if (T) T[j * t_ps + m * (int64_t)C * d.sh * t_wp + ((int64_t)c * d.sh + py) * t_wp + px] = v;
   }
 }
 
@@ -436,7 +455,8 @@ __global__ void pool_fwd_nhwc_kernel(ConvDev d, const float* __restrict__ A, int
 // post-activation value, network.hpp:211-214).  Pad = k - 1 on every side.
 __global__ void pool_bwd_nhwc_kernel(ConvDev d, int act, const float* __restrict__ A, int64_t a_ps,
                                      const float* __restrict__ dP, int64_t dp_ps, int flat, float* __restrict__ dZ,
-                                     int64_t dz_ps, int64_t M, int64_t J) {
+                                     int64_t dz_ps, int64_t M, int64_t J, float* __restrict__ S, int64_t s_ps,
+                                     int64_t s_kx, int s_wp) {
   const int C = d.cout, pad = d.k - 1, W2 = d.wo + 2 * pad, H2 = d.ho + 2 * pad;
   const int64_t per = (int64_t)d.sh * d.sw * C, total = J * M * per;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
@@ -459,6 +479,14 @@ __global__ void pool_bwd_nhwc_kernel(ConvDev d, int act, const float* __restrict
     z[C] = best == 1 ? v : 0.f;
     z[zrow] = best == 2 ? v : 0.f;
     z[zrow + C] = best == 3 ? v : 0.f;
+    // kx-shifted channel-major copies (the weight-gradient B operand): dZs[kx][c][y][x + kx]
+    float* s0 = S + j * s_ps + m * (int64_t)C * d.ho * s_wp + ((int64_t)c * d.ho + 2 * py) * s_wp + 2 * px;
+    for (int kx = 0; kx < d.k; ++kx, s0 += s_kx + 1) {
+      s0[0] = best == 0 ? v : 0.f;
+      s0[1] = best == 1 ? v : 0.f;
+      s0[s_wp] = best == 2 ? v : 0.f;
+      s0[s_wp + 1] = best == 3 ? v : 0.f;
+    }
   }
 }
 
@@ -474,14 +502,17 @@ __global__ void nhwc_to_flat_kernel(ConvDev d, const float* __restrict__ A, int6
   }
 }
 __global__ void flat_to_dzpad_kernel(ConvDev d, const float* __restrict__ F, int64_t f_ps, float* __restrict__ dZ,
-                                     int64_t dz_ps, int64_t M, int64_t J) {
+                                     int64_t dz_ps, int64_t M, int64_t J, float* __restrict__ S, int64_t s_ps,
+                                     int64_t s_kx, int s_wp) {
   const int C = d.cout, pad = d.k - 1, W2 = d.wo + 2 * pad, H2 = d.ho + 2 * pad;
   const int64_t per = (int64_t)d.ho * d.wo * C, total = J * M * per;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = g / (M * per), rem = g - j * M * per, m = rem / per;
     const int o = (int)(rem - m * per), c = o % C, yx = o / C, y = yx / d.wo, x = yx - y * d.wo;
-    dZ[j * dz_ps + m * (int64_t)H2 * W2 * C + ((int64_t)(y + pad) * W2 + x + pad) * C + c] =
-        tf32_hi(F[j * f_ps + m * per + (int64_t)c * d.ho * d.wo + yx]);
+    const float v = tf32_hi(F[j * f_ps + m * per + (int64_t)c * d.ho * d.wo + yx]);
+    dZ[j * dz_ps + m * (int64_t)H2 * W2 * C + ((int64_t)(y + pad) * W2 + x + pad) * C + c] = v;
+    float* s0 = S + j * s_ps + m * (int64_t)C * d.ho * s_wp + ((int64_t)c * d.ho + y) * s_wp + x;
+    for (int kx = 0; kx < d.k; ++kx, s0 += s_kx + 1) *s0 = v;
   }
 }
 
@@ -536,10 +567,12 @@ struct ConvTcState {
   float* Wf[kMaxConv] = {};
   float* Wd[kMaxConv] = {};
   float* dP[kMaxConv] = {};    // delta of a pooled (non-last) stage output, NHWC
-  // one stage's weight gradient runs at a time: its operand copies share two scratch buffers
-  float* inT = nullptr;        // stage input, [mcap][cin][hin][win_p] per particle (stage 0: shared)
-  float* dZs = nullptr;        // [k][mcap][cout][ho][win_p] per particle: dZ shifted right by kx
-  size_t inT_floats = 0, dZs_floats = 0;
+  // weight-gradient operands, written by the producers of the stage input / delta (epilogue
+  // second outputs, pool kernels): zero-initialised, so padding columns stay zero
+  float* inT[kMaxConv] = {};   // stage input [mcap][cin][hin][win_p] per particle (stage 0: shared X copy)
+  float* dZs[kMaxConv] = {};   // [k][mcap][cout][ho][win_p] per particle: dZ shifted right by kx
+  int* c2o[kMaxConv] = {};     // input pixel of stage i -> its inT[i] offset (channel 0)
+  int* dzo[kMaxConv] = {};     // output pixel of stage i -> its dZs[i] offset (channel 0, kx 0)
   // tables (device, int32)
   int* fa_row[kMaxConv] = {};  // output pixel -> input pixel base (forward A rows)
   int* fa_col[kMaxConv] = {};  // forward k -> offset
@@ -567,8 +600,8 @@ T* upload_vec(const std::vector<T>& v) {
 }
 
 void free_tables(ConvTcState* s) {
-  int** t[] = {s->fa_row, s->fa_col, s->zpix, s->da_row, s->da_col, s->wa_row,
-               s->wa_col, s->wb_row, s->wb_col, s->prow, s->pcol, s->bcol};
+  int** t[] = {s->fa_row, s->fa_col, s->zpix, s->da_row, s->da_col, s->wa_row, s->wa_col,
+               s->wb_row, s->wb_col, s->prow, s->pcol, s->bcol, s->c2o, s->dzo};
   for (int** a : t)
     for (int i = 0; i < kMaxConv; ++i)
       if (a[i]) {
@@ -645,6 +678,15 @@ void build_tables(Ctx& c, int64_t mc) {
         pcol[n] = co * Kf + kx;
         bcol[n] = kx == 0 ? co : -1;
       }
+    std::vector<int> c2o((size_t)(mc * nin)), dzo((size_t)(mc * npix));
+    for (int64_t m = 0; m < mc; ++m) {
+      for (int y = 0; y < d.hin; ++y)
+        for (int x = 0; x < d.win; ++x) c2o[(size_t)(m * nin + (int64_t)y * d.win + x)] = (int)(m * planeA + (int64_t)y * wp + x);
+      for (int y = 0; y < d.ho; ++y)
+        for (int x = 0; x < d.wo; ++x) dzo[(size_t)(m * npix + (int64_t)y * d.wo + x)] = (int)(m * planeB + (int64_t)y * wp + x);
+    }
+    s->c2o[i] = upload_vec(c2o);
+    s->dzo[i] = upload_vec(dzo);
     s->wa_row[i] = upload_vec(wa_row);
     s->wa_col[i] = upload_vec(wa_col);
     s->wb_row[i] = upload_vec(wb_row);
@@ -733,25 +775,6 @@ __global__ void to_chw_pad_kernel(const float* __restrict__ src, int64_t src_ps,
   }
 }
 
-// dZs[kx][m][co][y][x'] = dZ(m, y, x' - kx, co) (0 outside [0, wo)), from the zero-bordered
-// NHWC delta buffer; every x' in [0, w_p) is written
-__global__ void dz_shift_kernel(ConvDev d, const float* __restrict__ dZ, int64_t dz_ps, int Wp, float* __restrict__ out,
-                                int64_t out_ps, int64_t kx_stride, int64_t M, int64_t J) {
-  const int pad = d.k - 1, W2 = d.wo + 2 * pad, H2 = d.ho + 2 * pad, C = d.cout;
-  const int64_t per = (int64_t)C * d.ho * Wp, total = J * M * per;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = g / (M * per), rem = g - j * M * per, m = rem / per;
-    const int o = (int)(rem - m * per);
-    const int co = o / (d.ho * Wp), yx = o - co * d.ho * Wp, y = yx / Wp, x = yx - y * Wp;
-    const float* z = dZ + j * dz_ps + m * (int64_t)H2 * W2 * C + (int64_t)(y + pad) * W2 * C + co;
-    float* w = out + j * out_ps + m * per + o;
-    for (int kx = 0; kx < d.k; ++kx) {
-      const int xs = x - kx + pad;  // padded column of dZ(x - kx)
-      w[kx * kx_stride] = (xs >= 0 && xs < W2) ? z[(int64_t)xs * C] : 0.f;
-    }
-  }
-}
-
 }  // namespace
 
 // ---- public entry points (conv_tc.cuh) ----------------------------------------------------------
@@ -823,33 +846,31 @@ void cnn_tc_free(Ctx& c) {
   if (!s) return;
   free_tables(s);
   for (int i = 0; i < kMaxConv; ++i) {
-    float* p[] = {s->Wf[i], s->Wd[i], s->dP[i]};
+    float* p[] = {s->Wf[i], s->Wd[i], s->dP[i], s->inT[i], s->dZs[i]};
     for (float* q : p)
       if (q) cudaFree(q);
   }
   if (s->Xr) cudaFree(s->Xr);
   if (s->Xcol) cudaFree(s->Xcol);
   if (s->ones) cudaFree(s->ones);
-  if (s->inT) cudaFree(s->inT);
-  if (s->dZs) cudaFree(s->dZs);
   delete s;
   c.ctc = nullptr;
 }
 
 int64_t cnn_tc_image_floats(const Ctx& c) {
   const NetDev& net = c.net;
-  int64_t f = 0, scratch_a = 0, scratch_b = 0;
+  int64_t f = 0;
   for (int i = 0; i < net.nconv; ++i) {
     const ConvDev& d = net.conv[i];
     const int64_t wp = round_up(d.win, 4);
-    f += act_plane(d) + pad_plane(d);  // output, zero-bordered delta
-    scratch_b = std::max<int64_t>(scratch_b, (int64_t)d.k * d.cout * d.ho * wp);     // shifted deltas
-    if (i > 0) scratch_a = std::max<int64_t>(scratch_a, (int64_t)d.cin * d.hin * wp);  // channel-major input
+    f += act_plane(d) + pad_plane(d);               // output, zero-bordered delta
+    f += (int64_t)d.k * d.cout * d.ho * wp;          // kx-shifted deltas
+    if (i > 0) f += (int64_t)d.cin * d.hin * wp;     // channel-major input copy
     if (d.pool) f += pool_plane(d);
     else if (i == net.nconv - 1) f += act_plane(d);  // the flatten copy
     if (d.pool && i + 1 < net.nconv) f += pool_plane(d);
   }
-  return f + scratch_a + scratch_b;
+  return f;
 }
 
 // Stage buffers for chunks of mc images: cact = NHWC stage output, cpool = pooled NHWC (or the
@@ -860,35 +881,27 @@ void cnn_tc_alloc(Ctx& c, int64_t mc) {
   const NetDev& net = c.net;
   const size_t J = (size_t)c.Jmax;
   for (int i = 0; i < net.nconv; ++i) {
-    float** bufs[] = {&c.cact[i], &c.cpool[i], &c.cdel[i], &s->dP[i]};
+    float** bufs[] = {&c.cact[i], &c.cpool[i], &c.cdel[i], &s->dP[i], &s->inT[i], &s->dZs[i]};
     for (float** b : bufs)
       if (*b) {
         CK(cudaFree(*b));
         *b = nullptr;
       }
     const ConvDev& d = net.conv[i];
-    const int64_t wp = s->winp[i];
+    const size_t wp = (size_t)s->winp[i];
     CK(cudaMalloc(&c.cact[i], sizeof(float) * J * mc * act_plane(d)));
     CK(cudaMalloc(&c.cdel[i], sizeof(float) * J * mc * pad_plane(d)));
     CK(cudaMemsetAsync(c.cdel[i], 0, sizeof(float) * J * mc * pad_plane(d), c.stream));
     const bool last = i == net.nconv - 1;
     if (d.pool || last) CK(cudaMalloc(&c.cpool[i], sizeof(float) * J * mc * (d.pool ? pool_plane(d) : act_plane(d))));
     if (d.pool && !last) CK(cudaMalloc(&s->dP[i], sizeof(float) * J * mc * pool_plane(d)));
-    (void)wp;
+    const size_t fa = (size_t)mc * d.cin * d.hin * wp * (i == 0 ? 1 : J);  // stage 0: shared by particles
+    const size_t fb = J * d.k * mc * d.cout * d.ho * wp;
+    CK(cudaMalloc(&s->inT[i], sizeof(float) * fa));
+    CK(cudaMemsetAsync(s->inT[i], 0, sizeof(float) * fa, c.stream));
+    CK(cudaMalloc(&s->dZs[i], sizeof(float) * fb));
+    CK(cudaMemsetAsync(s->dZs[i], 0, sizeof(float) * fb, c.stream));
   }
-  size_t fa = 0, fb = 0;
-  for (int i = 0; i < net.nconv; ++i) {
-    const ConvDev& d = net.conv[i];
-    const size_t wp = (size_t)s->winp[i];
-    fa = std::max(fa, (size_t)mc * d.cin * d.hin * wp * (i == 0 ? 1 : J));  // stage 0: shared by particles
-    fb = std::max(fb, J * d.k * mc * d.cout * d.ho * wp);
-  }
-  if (s->inT) CK(cudaFree(s->inT));
-  if (s->dZs) CK(cudaFree(s->dZs));
-  CK(cudaMalloc(&s->inT, sizeof(float) * fa));
-  CK(cudaMalloc(&s->dZs, sizeof(float) * fb));
-  s->inT_floats = fa;
-  s->dZs_floats = fb;
   build_tables(c, mc);
   s->mcap = mc;
 }
@@ -957,11 +970,24 @@ void cnn_tc_forward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t m
     p.theta = theta;
     p.Dp = net.Dp;
     p.boff = d.boff;
-    launch_gemm<kEpiConvFwd>(c, p, net.act);
     const bool last = i == net.nconv - 1;
+    int64_t nxt_ps = 0;  // per-particle floats of the next stage's channel-major input copy
+    if (!last) {
+      const ConvDev& dn = net.conv[i + 1];
+      nxt_ps = cap * (int64_t)dn.cin * dn.hin * s->winp[i + 1];
+      if (!d.pool) {  // the epilogue writes it (no pool in between)
+        p.out2 = s->inT[i + 1];
+        p.out2_ps = nxt_ps;
+        p.out2off = s->c2o[i + 1];
+        p.out2_cs = (int64_t)dn.hin * s->winp[i + 1];
+        p.out2_k = 1;
+      }
+    }
+    launch_gemm<kEpiConvFwd>(c, p, net.act);
     if (d.pool) {
       pool_fwd_nhwc_kernel<<<grid_of(J * mc * pool_plane(d)), 256, 0, c.stream>>>(
-          d, c.cact[i], cap * act_plane(d), c.cpool[i], cap * pool_plane(d), mc, J, last ? 1 : 0);
+          d, c.cact[i], cap * act_plane(d), c.cpool[i], cap * pool_plane(d), mc, J, last ? 1 : 0,
+          last ? nullptr : s->inT[i + 1], nxt_ps, last ? 0 : s->winp[i + 1]);
       LAUNCHED();
     } else if (last) {
       nhwc_to_flat_kernel<<<grid_of(J * mc * act_plane(d)), 256, 0, c.stream>>>(d, c.cact[i], cap * act_plane(d),
@@ -979,15 +1005,17 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
   const int64_t img = (int64_t)net.in_c * net.in_h * net.in_w;
   const int64_t cap = s->mcap;
   const int L = net.nconv - 1;
+  auto planeB_of = [&](int i) { return (int64_t)net.conv[i].cout * net.conv[i].ho * s->winp[i]; };
   {
     const ConvDev& d = net.conv[L];
+    const int64_t pb = cap * planeB_of(L);
     if (d.pool) {
       pool_bwd_nhwc_kernel<<<grid_of(J * mc * pool_plane(d)), 256, 0, c.stream>>>(
           d, net.act, c.cact[L], cap * act_plane(d), c.cpool[L], cap * pool_plane(d), 1, c.cdel[L], cap * pad_plane(d),
-          mc, J);
+          mc, J, s->dZs[L], d.k * pb, pb, s->winp[L]);
     } else {
-      flat_to_dzpad_kernel<<<grid_of(J * mc * act_plane(d)), 256, 0, c.stream>>>(d, c.cpool[L], cap * act_plane(d),
-                                                                                   c.cdel[L], cap * pad_plane(d), mc, J);
+      flat_to_dzpad_kernel<<<grid_of(J * mc * act_plane(d)), 256, 0, c.stream>>>(
+          d, c.cpool[L], cap * act_plane(d), c.cdel[L], cap * pad_plane(d), mc, J, s->dZs[L], d.k * pb, pb, s->winp[L]);
     }
     LAUNCHED();
   }
@@ -997,31 +1025,22 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
     // ---- weight gradient + fused leapfrog (shifted-rows form, see ConvTcState):
     //      D[(ky, ci) | ones, (kx, co)] = sum_(m, y, x') inT[ci][y + ky][x'] dZs[kx][co][y][x']
     {
-      const int64_t JA = i == 0 ? 1 : J;
       const int64_t planeA = (int64_t)d.cin * d.hin * wp;
-      if (i == 0) {
+      const int64_t planeB = planeB_of(i);
+      if (i == 0) {  // stage 0's input is X: its channel-major padded copy, shared by the particles
         to_chw_pad_kernel<<<grid_of(mc * planeA), 256, 0, c.stream>>>(s->Xr + m0 * img, 0, 0, d.cin, d.hin, d.win, wp,
-                                                                     s->inT, 0, mc, 1);
-      } else {
-        const ConvDev& dp = net.conv[i - 1];
-        to_chw_pad_kernel<<<grid_of(JA * mc * planeA), 256, 0, c.stream>>>(
-            dp.pool ? c.cpool[i - 1] : c.cact[i - 1], cap * (dp.pool ? pool_plane(dp) : act_plane(dp)), 1, d.cin, d.hin,
-            d.win, wp, s->inT, cap * planeA, mc, JA);
+                                                                     s->inT[0], 0, mc, 1);
+        LAUNCHED();
       }
-      LAUNCHED();
-      const int64_t planeB = (int64_t)d.cout * d.ho * wp;
-      dz_shift_kernel<<<grid_of(J * mc * planeB), 256, 0, c.stream>>>(d, c.cdel[i], cap * pad_plane(d), wp, s->dZs,
-                                                                       (int64_t)d.k * cap * planeB, cap * planeB, mc, J);
-      LAUNCHED();
       GParams p{};
-      p.a.base = s->inT;
+      p.a.base = s->inT[i];
       p.a.ps = i == 0 ? 0 : cap * planeA;
       p.a.rowoff = s->wa_row[i];
       p.a.nrows = d.k * d.cin + 1;
       p.a.coloff = s->wa_col[i];
       p.a.K = (int)(mc * d.ho * wp);
       p.a.vec = 1;
-      p.b.base = s->dZs;
+      p.b.base = s->dZs[i];
       p.b.ps = (int64_t)d.k * cap * planeB;
       p.b.rowoff = s->wb_row[i];
       p.b.nrows = d.k * d.cout;
@@ -1080,12 +1099,20 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
       p.mask = c.cact[i - 1];
       p.mask_ps = cap * act_plane(dp);
       p.mask_ld = dp.cout;
+      // and its kx-shifted channel-major copies (stage i-1's weight-gradient B operand)
+      p.out2 = s->dZs[i - 1];
+      p.out2_ps = (int64_t)dp.k * cap * planeB_of(i - 1);
+      p.out2off = s->dzo[i - 1];
+      p.out2_cs = (int64_t)dp.ho * s->winp[i - 1];
+      p.out2_ks = cap * planeB_of(i - 1);
+      p.out2_k = dp.k;
     }
     launch_gemm<kEpiConvDx>(c, p, net.act);
     if (dp.pool) {
+      const int64_t pb = cap * planeB_of(i - 1);
       pool_bwd_nhwc_kernel<<<grid_of(J * mc * pool_plane(dp)), 256, 0, c.stream>>>(
           dp, net.act, c.cact[i - 1], cap * act_plane(dp), s->dP[i - 1], cap * pool_plane(dp), 0, c.cdel[i - 1],
-          cap * pad_plane(dp), mc, J);
+          cap * pad_plane(dp), mc, J, s->dZs[i - 1], dp.k * pb, pb, s->winp[i - 1]);
       LAUNCHED();
     }
   }

@@ -97,6 +97,25 @@ enum EpiMode : int {
   kEpiFirstLast = 4,  // S = 0 never happens; reserved
 };
 
+// Per-step scalars the step's kernels read from device memory (written by the step's first
+// kernel), so a captured CUDA graph of smc_step replays unchanged across iterations: only that
+// first node's by-value argument is updated per launch.
+struct DevStep {
+  int k;          // ensemble iteration (RNG forks, the record)
+  int slot;       // record ring slot
+  uint64_t ukey;  // root.fork(kResample, k) (smc.hpp:152)
+};
+
+constexpr int kSigLen = 24;
+struct GraphEntry {  // one instantiated smc_step graph (capi.cu smc_step_graphed)
+  int64_t sig[kSigLen];
+  cudaGraphExec_t exec;
+  cudaGraphNode_t node;  // the set_step kernel node (its by-value DevStep is updated per launch)
+  cudaKernelNodeParams params;
+  int start_after;
+  long long launches;
+};
+
 struct EpiParams {
   int mode;
   float h, hh;     // step size, half step
@@ -240,6 +259,16 @@ struct Ctx {
   float* gacc = nullptr;  // [Jmax][Dp] data-gradient sums across window chunks (EpiParams::acc_mode)
   int64_t cnn_ll_slots = 0;
 
+  // CUDA-graph replay of smc_step (dasmc_gpu_set_graphs): one instantiated graph per step
+  // signature (buffer rotation, target, kernel config, allocations)
+  DevStep* dstep = nullptr;
+  bool use_graphs = false, capturing = false;
+  long long alloc_epoch = 0;  // bumped by every reallocation a captured graph could reference
+  struct GraphEntry* graphs = nullptr;
+  int n_graphs = 0;
+  int64_t seen_sig[kSigLen] = {};
+  bool seen_valid = false;
+
   // kernel-range timers
   bool ktime = false;
   std::vector<cudaEvent_t> kev[kTimerKinds];
@@ -277,16 +306,18 @@ void launch_eval(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t P,
 void launch_eval_finalize(Ctx& c, int64_t J, double* values_out, double* pre_out, double* blk_out, int64_t M,
                           bool with_theta_norm);
 void launch_normals(Ctx& c, uint64_t key_root, uint64_t tag_a, uint64_t a2, int64_t J, float scale, float* dst,
-                    double* sq_part, int64_t j_offset = 0);
+                    double* sq_part, int64_t j_offset = 0, const DevStep* ds = nullptr);
+void launch_set_step(Ctx& c, const DevStep& v);
+const void* set_step_kernel_fn();  // the set_step kernel (graph node lookup)
 void launch_ref_to_internal_f64(Ctx& c, const double* src, float* dst, int64_t J);
 void launch_ref_to_internal_f32(Ctx& c, const float* src, float* dst, int64_t J);
 void launch_internal_to_ref_f64(Ctx& c, const float* src, double* dst, int64_t J);
 void launch_internal_to_ref_f32(Ctx& c, const float* src, float* dst, int64_t J);
 void launch_zero_ints(Ctx& c, int* p, int64_t n);
 void launch_p_sumsq(Ctx& c, int64_t J);
-void launch_uniforms(Ctx& c, uint64_t key, int64_t count, double* dst);
+void launch_uniforms(Ctx& c, uint64_t key, int64_t count, double* dst, const DevStep* ds = nullptr);
 void launch_weights_and_resample(Ctx& c, int64_t J, double fraction, int always, int kind, int rec_slot,
-                                 int k, double log_target_const);
+                                 int k, double log_target_const, const DevStep* ds = nullptr);
 void launch_gather(Ctx& c, const float* start, const float* end, float* dst, int64_t J,
                    const int32_t* idx = nullptr);
 // post-step (prefix, block) ll: (flags[s] ? first-evaluation : last-evaluation)[s], s = idx[j]

@@ -23,7 +23,7 @@ namespace dasmc_b200 {
 
 std::atomic<long long> g_launch_count{0};
 
-KTimer::KTimer(Ctx& cc, int k) : c(cc), kind(k) {
+KTimer::KTimer(Ctx& cc, int k) : c(cc), kind(cc.capturing ? -1 : k) {
   if (!c.ktime || kind < 0) return;
   auto& v = c.kev[kind];
   while ((int)v.size() < 2 * (c.kev_used[kind] + 1)) {
@@ -419,10 +419,12 @@ __device__ __forceinline__ float normal_from_draws(uint64_t x1, uint64_t x2) {
 // W, so a warp's stores are coalesced.
 __global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b, int per_particle_c,
                                int64_t J, int64_t nchunks, int64_t chunk, const uint64_t* __restrict__ jump_tab,
-                               float scale, float* __restrict__ dst, double* __restrict__ sq_part, int64_t j_offset) {
+                               float scale, float* __restrict__ dst, double* __restrict__ sq_part, int64_t j_offset,
+                               const DevStep* __restrict__ ds) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= J * nchunks) return;
   const int64_t j = g / nchunks, c = g - j * nchunks;
+  if (ds) b = (uint64_t)ds->k;  // the step's iteration, from device memory (graph replay)
   // fork(kProposal, k, j) -> (a, b, j); fork(kInit, j) -> (a, j, 0); j is the GLOBAL slot
   const uint64_t jg = (uint64_t)(j + j_offset);
   const uint64_t key = per_particle_c ? fork_key(root, a, b, jg) : fork_key(root, a, jg, 0);
@@ -465,7 +467,8 @@ __global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b
 // `count` uniforms of one stream (resampling), chunked with the same jumps
 // (a chunk of `chunk` normals = 2*chunk draws).
 __global__ void uniforms_kernel(uint64_t key, int64_t count, int64_t chunk, const uint64_t* __restrict__ jump_tab,
-                                double* __restrict__ dst) {
+                                double* __restrict__ dst, const DevStep* __restrict__ ds) {
+  if (ds) key = ds->ukey;
   const int64_t per = 2 * chunk;
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c * per >= count) return;
@@ -560,8 +563,13 @@ __global__ void __launch_bounds__(kWT) weights_kernel(int64_t J, double* __restr
                                                       const int* __restrict__ flags, double* __restrict__ w,
                                                       double* __restrict__ cdf, const double* __restrict__ uni,
                                                       int32_t* __restrict__ idx, double fraction, int always,
-                                                      int kind, double* __restrict__ rec, int k, int compute_lw) {
+                                                      int kind, double* __restrict__ rec, int k, int compute_lw,
+                                                      const DevStep* __restrict__ ds) {
   __shared__ double sh[kWT / 32 + 1];
+  if (ds) {  // record slot and iteration from device memory (graph replay); rec = the ring base
+    rec += (size_t)ds->slot * 8;
+    k = ds->k;
+  }
   __shared__ int s_res;
   // 1) new log-weights (kernels.hpp:153-163, smc.hpp:127-138); with compute_lw = 0
   //    logw already holds them (the gathered vector of a sharded ensemble)
@@ -700,6 +708,8 @@ __global__ void gather_parts_kernel(int64_t J, const int32_t* __restrict__ idx, 
   out_blk[j] = flags[s] ? blk0[s] : blk[s];
 }
 
+__global__ void set_step_kernel(DevStep v, DevStep* d) { *d = v; }
+
 __global__ void zero_ints_kernel(int* p, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = 0;
@@ -727,6 +737,7 @@ size_t cdf_smem(int64_t J) {
 // ---- host launchers ----------------------------------------------------------------------------
 void ensure_stage(Ctx& c, size_t bytes) {
   if (bytes <= c.stage_bytes) return;
+  ++c.alloc_epoch;
   if (c.stage) CK(cudaFree(c.stage));
   c.stage = nullptr;
   CK(cudaMalloc(&c.stage, bytes));
@@ -1260,7 +1271,7 @@ void cnn_chunk_simt(Ctx& c, const float* theta_in, int64_t J, int64_t m0, int64_
 // fit kCnnBudget, else the largest multiple of 128 that does.  A pure function of (M, net,
 // Jmax, precision): the chunk split -- and with it the fp32 order of the cross-chunk gradient
 // sums -- never depends on earlier calls.  DASMC_CNN_CHUNK (tests) caps it.
-constexpr double kCnnBudget = 48e9;
+constexpr double kCnnBudget = 100e9;  // of the 180 GB of HBM
 int64_t cnn_image_floats(const Ctx& c) {
   const NetDev& net = c.net;
   int64_t f = 0;
@@ -1420,10 +1431,13 @@ void launch_predictive_mix(Ctx& c, const float* logits, int64_t R, int64_t J, co
 
 void ensure_activation_capacity(Ctx& c, int64_t M) {
   if (c.net.nconv > 0) {
+    const int64_t before = c.Mcap, slots = c.ll_slots;
     cnn_ensure(c, M);
+    if (c.Mcap != before || c.ll_slots != slots) ++c.alloc_epoch;
     return;
   }
   if (M <= c.Mcap) return;
+  ++c.alloc_epoch;
   CK(cudaStreamSynchronize(c.stream));
   const int64_t Mnew = ((M + 127) / 128) * 128;
   if (c.tc) {
@@ -1527,21 +1541,27 @@ void launch_eval_finalize(Ctx& c, int64_t J, double* values_out, double* pre_out
   LAUNCHED();
 }
 
+void launch_set_step(Ctx& c, const DevStep& v) {
+  set_step_kernel<<<1, 1, 0, c.stream>>>(v, c.dstep);
+  LAUNCHED();
+}
+const void* set_step_kernel_fn() { return reinterpret_cast<const void*>(&set_step_kernel); }
+
 void launch_normals(Ctx& c, uint64_t root, uint64_t a, uint64_t b, int64_t J, float scale, float* dst,
-                    double* sq_part, int64_t j_offset) {
+                    double* sq_part, int64_t j_offset, const DevStep* ds) {
   const int64_t nch = (c.net.D + c.rng_chunk - 1) / c.rng_chunk;
   const int per_particle_c = a == tag::kProposal ? 1 : 0;
   const int64_t total = J * nch;
   normals_kernel<<<(unsigned)((total + 127) / 128), 128, 0, c.stream>>>(
-      c.net, root, a, b, per_particle_c, J, nch, c.rng_chunk, c.jump_tab, scale, dst, sq_part, j_offset);
+      c.net, root, a, b, per_particle_c, J, nch, c.rng_chunk, c.jump_tab, scale, dst, sq_part, j_offset, ds);
   LAUNCHED();
 }
 
-void launch_uniforms(Ctx& c, uint64_t key, int64_t count, double* dst) {
+void launch_uniforms(Ctx& c, uint64_t key, int64_t count, double* dst, const DevStep* ds) {
   const int64_t per = 2 * c.rng_chunk;
   const int64_t nch = (count + per - 1) / per;
   if (nch > c.jump_chunks) throw std::invalid_argument("uniforms: jump table too small");
-  uniforms_kernel<<<(unsigned)((nch + 63) / 64), 64, 0, c.stream>>>(key, count, c.rng_chunk, c.jump_tab, dst);
+  uniforms_kernel<<<(unsigned)((nch + 63) / 64), 64, 0, c.stream>>>(key, count, c.rng_chunk, c.jump_tab, dst, ds);
   LAUNCHED();
 }
 
@@ -1576,13 +1596,13 @@ void launch_slot_sums(Ctx& c, int64_t J, int p0_slots, int pS_slots) {
 }
 
 void launch_weights_and_resample(Ctx& c, int64_t J, double fraction, int always, int kind, int rec_slot, int k,
-                                 double) {
+                                 double, const DevStep* ds) {
   const int p0_slots = c.rng_slots;
   const int pS_slots = (int)((c.net.Dp + kSqChunk - 1) / kSqChunk);
   launch_slot_sums(c, J, p0_slots, pS_slots);
   weights_kernel<<<1, kWT, cdf_smem(J), c.stream>>>(J, c.logw, c.lt_old, c.lt_new, c.p0_sum, 1, c.pS_sum, 1,
                                           c.flags, c.wts, c.cdf, c.uni, c.idx, fraction, always, kind,
-                                          c.records + (size_t)rec_slot * 8, k, 1);
+                                          ds ? c.records : c.records + (size_t)rec_slot * 8, k, 1, ds);
   LAUNCHED();
 }
 
@@ -1598,7 +1618,7 @@ void launch_normalize_resample(Ctx& c, int64_t Jtot, double* lw_full, const doub
                                const double* uni, int32_t* idx, double fraction, int always, int kind, int rec_slot,
                                int k) {
   weights_kernel<<<1, kWT, cdf_smem(Jtot), c.stream>>>(Jtot, lw_full, nullptr, lt_full, nullptr, 0, nullptr, 0, nullptr, w, cdf,
-                                          uni, idx, fraction, always, kind, c.records + (size_t)rec_slot * 8, k, 0);
+                                          uni, idx, fraction, always, kind, c.records + (size_t)rec_slot * 8, k, 0, nullptr);
   LAUNCHED();
 }
 
