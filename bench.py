@@ -187,8 +187,9 @@ def cpu_model():
 
 def config_of(args, w, ks, Ms, world):
     """The workload description both arms print (same dict: the driver compares them)."""
-    J = w["J"]
-    return {"workload": w["desc"], "particles_per_gpu": J, "iterations": [ks[0], ks[-1]],
+    J = w["J"] if not getattr(args, "J_total", None) else -(-args.J_total // world)
+    return {"workload": w["desc"], "particles_per_gpu": J, "particles_total": J * world if not getattr(args, "J_total", None)
+            else args.J_total, "iterations": [ks[0], ks[-1]],
             "window_rows": [Ms[0], Ms[-1]], "precision": args.precision, "resample": args.resample,
             "l2": "inputs larger than L2 (activations >= 24 GB per step)" if w.get("big", True)
             else "inputs smaller than L2 (launch-bound config)",
@@ -275,6 +276,8 @@ def run_ours(args, w):
     spec, X, y = make_data(w)
     J, S, N = w["J"], w["S"], w["n"]
     D = p.param_count(spec)
+    if args.J_total:
+        J = (args.J_total + world - 1) // world
     t = p.GpuEnsembleTarget(spec, X, y, J, device=local, precision=args.precision)
     k0 = w["k0"]
     ks_warm = [k0 + i for i in range(args.warmup)]
@@ -301,15 +304,27 @@ def run_ours(args, w):
 
     P0, M0, mode0, beta0 = target_of(k0)
     t.set_target(P0, M0, N, mode0, beta0, 1.0)
-    # world > 1: one particle-sharded ensemble of J_total = J * world (weak scaling,
-    # paper_2601_21983_b200/dist.py); this rank owns global slots [j0, j0 + J)
-    J_total = J * world
-    j0 = J * rank
+    # world > 1: one particle-sharded ensemble (paper_2601_21983_b200/dist.py) of J_total = J * world
+    # (weak scaling) or, with --J-total, a fixed J_total split over the ranks (strong scaling,
+    # BASELINE configs[4]'s fixed-J sweep); this rank owns global slots [j0, j0 + J)
+    if args.J_total:
+        from paper_2601_21983_b200.dist import shard_range
+        J_total = args.J_total
+        j0, j1 = shard_range(J_total, world, rank)
+        J = j1 - j0
+    else:
+        J_total = J * world
+        j0 = J * rank
     L.check(lib.dasmc_gpu_init_ensemble_at(t.h, J, 0, j0))
     th0, lw0, _ = t.get_ensemble(J, dtype=np.float32)
     t.set_ensemble(th0, lw0, k0)
     kc = p.KernelConfig.hmc(w["h"], S)
     rk = args.resample
+    if world == 1 and not w.get("big", True) and not args.no_graphs:
+        # launch-bound config (C1): CUDA-graph replay of each smc_step (bit-identical,
+        # tests/test_gpu_graphs.py).  Not for the big configs: their kernel-range timers (the
+        # live roofline) run on eager launches, and launch overhead is < 1 % of their step
+        t.set_graphs(True)
     sharded_recs = []
     Ms = []
     if world > 1:
@@ -450,7 +465,8 @@ def run_ours(args, w):
     if rank == 0:
         line = {"metric": "particle-sample grad evals/sec", "value": value, "unit": "particle-sample grad evals/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPES.get(args.precision, args.precision),
+                "higher_is_better": True, "scaling": "strong" if args.J_total else "weak", "vs_baseline": None,
+                "dtype": DTYPES.get(args.precision, args.precision),
                 "data": DATA_DESC,
                 "config": config_of(args, w, ks, Ms, world),
                 "iterations_per_sec": args.steps / (ms_max / 1e3),
@@ -480,7 +496,10 @@ def main():
     ap.add_argument("--resample", default="systematic", choices=["systematic", "multinomial"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of CUDA-graph replay")
     ap.add_argument("--J", type=int, default=None, help="particles per GPU (default: the config's)")
+    ap.add_argument("--J-total", type=int, default=None,
+                    help="fixed ensemble size split over the GPUs (strong scaling; C5's J sweep)")
     args = ap.parse_args()
     w = dict(WORKLOADS[args.config])
     if args.J:

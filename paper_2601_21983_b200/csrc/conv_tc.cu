@@ -452,42 +452,71 @@ __global__ void pool_fwd_nhwc_kernel(ConvDev d, const float* __restrict__ A, int
 // Max-pool backward into the stage's zero-bordered delta buffer: the pooled delta (NHWC, or the
 // head's flatten order) times act'(max) goes to the first maximum of the window in (dy, dx)
 // order, zeros to the other three positions (network activation derivative from the
-// post-activation value, network.hpp:211-214).  Pad = k - 1 on every side.
-__global__ void pool_bwd_nhwc_kernel(ConvDev d, int act, const float* __restrict__ A, int64_t a_ps,
-                                     const float* __restrict__ dP, int64_t dp_ps, int flat, float* __restrict__ dZ,
-                                     int64_t dz_ps, int64_t M, int64_t J, float* __restrict__ S, int64_t s_ps,
-                                     int64_t s_kx, int s_wp) {
-  const int C = d.cout, pad = d.k - 1, W2 = d.wo + 2 * pad, H2 = d.ho + 2 * pad;
-  const int64_t per = (int64_t)d.sh * d.sw * C, total = J * M * per;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = g / (M * per), rem = g - j * M * per, m = rem / per;
-    const int o = (int)(rem - m * per);
-    const int c = o % C, pyx = o / C, py = pyx / d.sw, px = pyx - py * d.sw;
+// post-activation value, network.hpp:211-214).  Pad = k - 1 on every side.  One block per
+// (particle, image, pooled row): the two pre-pool rows are staged in shared memory, so both
+// outputs -- the NHWC zero-bordered delta (the delta GEMM's operand) and the k kx-shifted
+// channel-major copies (the weight-gradient operand) -- are written with coalesced rows.
+// Rows / columns no window covers (odd sizes, floor pooling) are never written (zero from
+// allocation).
+__global__ void __launch_bounds__(256) pool_bwd_rows_kernel(ConvDev d, int act, const float* __restrict__ A,
+                                                            int64_t a_ps, const float* __restrict__ dP, int64_t dp_ps,
+                                                            int flat, float* __restrict__ dZ, int64_t dz_ps, int64_t M,
+                                                            float* __restrict__ S, int64_t s_ps, int64_t s_kx, int s_wp) {
+  extern __shared__ float pz[];  // [2][wo][C + 1]: the window deltas of the two pre-pool rows
+  const int C = d.cout, pad = d.k - 1, W2 = d.wo + 2 * pad, H2 = d.ho + 2 * pad, CP = C + 1;
+  const int64_t row = blockIdx.x;  // (j, m, py)
+  const int py = (int)(row % d.sh);
+  const int64_t jm = row / d.sh, m = jm % M, j = jm / M;
+  const int wo2 = 2 * d.sw;  // pre-pool columns covered by windows
+  for (int i = threadIdx.x; i < 2 * d.wo * CP; i += blockDim.x) pz[i] = 0.f;
+  __syncthreads();
+  const float* arow = A + j * a_ps + m * (int64_t)d.ho * d.wo * C + (int64_t)(2 * py) * d.wo * C;
+  const int64_t per = (int64_t)d.sh * d.sw * C;
+  for (int i = threadIdx.x; i < d.sw * C; i += blockDim.x) {  // (px, c), c fastest: coalesced NHWC reads
+    const int c = i % C, px = i / C;
+    const float* a = arow + (int64_t)(2 * px) * C + c;
     const int64_t rowC = (int64_t)d.wo * C;
-    const float* a = A + j * a_ps + m * (int64_t)d.ho * d.wo * C + ((int64_t)(2 * py) * d.wo + 2 * px) * C + c;
     const float a0 = a[0], a1 = a[C], a2 = a[rowC], a3 = a[rowC + C];
     int best = 0;
     float mx = a0;
     if (a1 > mx) { mx = a1; best = 1; }
     if (a2 > mx) { mx = a2; best = 2; }
     if (a3 > mx) { mx = a3; best = 3; }
-    const float gp = dP[j * dp_ps + m * per + (flat ? (int64_t)c * d.sh * d.sw + pyx : o)];
+    const float gp = dP[j * dp_ps + m * per + (flat ? (int64_t)c * d.sh * d.sw + py * d.sw + px
+                                                        : ((int64_t)py * d.sw + px) * C + c)];
     const float v = tf32_hi(gp * (act == DASMC_RELU ? (mx > 0.f ? 1.f : 0.f) : 1.f - mx * mx));
-    float* z = dZ + j * dz_ps + m * (int64_t)H2 * W2 * C + ((int64_t)(2 * py + pad) * W2 + 2 * px + pad) * C + c;
-    const int64_t zrow = (int64_t)W2 * C;
-    z[0] = best == 0 ? v : 0.f;
-    z[C] = best == 1 ? v : 0.f;
-    z[zrow] = best == 2 ? v : 0.f;
-    z[zrow + C] = best == 3 ? v : 0.f;
-    // kx-shifted channel-major copies (the weight-gradient B operand): dZs[kx][c][y][x + kx]
-    float* s0 = S + j * s_ps + m * (int64_t)C * d.ho * s_wp + ((int64_t)c * d.ho + 2 * py) * s_wp + 2 * px;
-    for (int kx = 0; kx < d.k; ++kx, s0 += s_kx + 1) {
-      s0[0] = best == 0 ? v : 0.f;
-      s0[1] = best == 1 ? v : 0.f;
-      s0[s_wp] = best == 2 ? v : 0.f;
-      s0[s_wp + 1] = best == 3 ? v : 0.f;
+    pz[((best >> 1) * d.wo + 2 * px + (best & 1)) * CP + c] = v;
+  }
+  __syncthreads();
+  // NHWC zero-bordered rows: (dy, x, c) contiguous per row
+  float* z = dZ + j * dz_ps + m * (int64_t)H2 * W2 * C;
+  for (int i = threadIdx.x; i < 2 * wo2 * C; i += blockDim.x) {
+    const int c = i % C, xy = i / C, x = xy % wo2, dy = xy / wo2;
+    z[((int64_t)(2 * py + dy + pad) * W2 + x + pad) * C + c] = pz[(dy * d.wo + x) * CP + c];
+  }
+  // channel-major kx-shifted copies: for each (kx, c, dy) a contiguous run over x
+  float* sb = S + j * s_ps + m * (int64_t)C * d.ho * s_wp;
+  for (int i = threadIdx.x; i < d.k * C * 2 * wo2; i += blockDim.x) {
+    const int x = i % wo2, r = i / wo2, dy = r % 2, kc = r / 2, c = kc % C, kx = kc / C;
+    sb[kx * s_kx + ((int64_t)c * d.ho + 2 * py + dy) * s_wp + x + kx] = pz[(dy * d.wo + x) * CP + c];
+  }
+}
+
+void launch_pool_bwd(Ctx& c, const ConvDev& d, int act, const float* A, int64_t a_ps, const float* dP, int64_t dp_ps,
+                     int flat, float* dZ, int64_t dz_ps, int64_t M, int64_t J, float* S, int64_t s_ps, int64_t s_kx,
+                     int s_wp) {
+  const size_t sm = sizeof(float) * 2 * (size_t)d.wo * (d.cout + 1);
+  if (sm > 48 * 1024) {
+    static bool attr[kMaxDevices] = {};
+    const int dv = current_device();
+    if (!attr[dv]) {
+      CK(cudaFuncSetAttribute(pool_bwd_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr[dv] = true;
     }
   }
+  pool_bwd_rows_kernel<<<(unsigned)(J * M * d.sh), 256, sm, c.stream>>>(d, act, A, a_ps, dP, dp_ps, flat, dZ, dz_ps, M,
+                                                                        S, s_ps, s_kx, s_wp);
+  LAUNCHED();
 }
 
 // Last stage without a pool: NHWC output <-> the head's flatten order (c, y, x).
@@ -716,10 +745,13 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
   if (p.nmma > 256) throw std::invalid_argument("conv: MMA N > 256");
   if (!p.b.vec) throw std::invalid_argument("conv: B operands are 16-byte gathers");
   const size_t stage_bytes = (size_t)kCBM * 128 + (size_t)p.nmma * 128;
-  // up to 6 stages, two CTAs per SM when they fit (more producer warps in flight per SM)
+  // Stage ring: the implicit-im2col GEMMs (forward, delta) re-read each input pixel up to k*k
+  // times from L1, so they keep a short ring (3 stages) and leave most of the SM's unified
+  // L1 / shared memory to L1; the weight-gradient GEMM streams (no reuse) with 6 stages.
   const size_t fixed = 1024 + 64 * 8 + 64;
-  int stages = (int)std::min<size_t>(6, (110 * 1024 - fixed) / stage_bytes);
-  if (stages < 3) stages = (int)std::min<size_t>(6, (227 * 1024 - fixed) / stage_bytes);
+  const int want = EPI == kEpiConvDw ? 6 : 3;
+  int stages = (int)std::min<size_t>(want, (110 * 1024 - fixed) / stage_bytes);
+  if (stages < 2) stages = (int)std::min<size_t>(want, (227 * 1024 - fixed) / stage_bytes);
   if (stages < 2) throw std::invalid_argument("conv: GEMM tile does not fit in shared memory");
   p.stages = stages;
   const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16;
@@ -737,6 +769,9 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       attr[dv] = true;
     }
+    // unified L1 / shared split: just the shared memory two CTAs need, the rest stays L1
+    const int carve = (int)std::min<size_t>(100, (2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     int per_sm = 1;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCThreads, smem));
     per_sm = std::max(1, std::min(2, per_sm));
@@ -1010,14 +1045,13 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
     const ConvDev& d = net.conv[L];
     const int64_t pb = cap * planeB_of(L);
     if (d.pool) {
-      pool_bwd_nhwc_kernel<<<grid_of(J * mc * pool_plane(d)), 256, 0, c.stream>>>(
-          d, net.act, c.cact[L], cap * act_plane(d), c.cpool[L], cap * pool_plane(d), 1, c.cdel[L], cap * pad_plane(d),
-          mc, J, s->dZs[L], d.k * pb, pb, s->winp[L]);
+      launch_pool_bwd(c, d, net.act, c.cact[L], cap * act_plane(d), c.cpool[L], cap * pool_plane(d), 1, c.cdel[L],
+                      cap * pad_plane(d), mc, J, s->dZs[L], d.k * pb, pb, s->winp[L]);
     } else {
       flat_to_dzpad_kernel<<<grid_of(J * mc * act_plane(d)), 256, 0, c.stream>>>(
           d, c.cpool[L], cap * act_plane(d), c.cdel[L], cap * pad_plane(d), mc, J, s->dZs[L], d.k * pb, pb, s->winp[L]);
+      LAUNCHED();
     }
-    LAUNCHED();
   }
   for (int i = L; i >= 0; --i) {
     const ConvDev& d = net.conv[i];
@@ -1110,10 +1144,8 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
     launch_gemm<kEpiConvDx>(c, p, net.act);
     if (dp.pool) {
       const int64_t pb = cap * planeB_of(i - 1);
-      pool_bwd_nhwc_kernel<<<grid_of(J * mc * pool_plane(dp)), 256, 0, c.stream>>>(
-          dp, net.act, c.cact[i - 1], cap * act_plane(dp), s->dP[i - 1], cap * pool_plane(dp), 0, c.cdel[i - 1],
-          cap * pad_plane(dp), mc, J, s->dZs[i - 1], dp.k * pb, pb, s->winp[i - 1]);
-      LAUNCHED();
+      launch_pool_bwd(c, dp, net.act, c.cact[i - 1], cap * act_plane(dp), s->dP[i - 1], cap * pool_plane(dp), 0,
+                      c.cdel[i - 1], cap * pad_plane(dp), mc, J, s->dZs[i - 1], dp.k * pb, pb, s->winp[i - 1]);
     }
   }
 }

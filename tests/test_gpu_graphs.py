@@ -9,8 +9,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _run(product, spec, X, y, prec, graphs, windows, mode="scaled", kind="systematic", always=False):
-    J = 64
+def _run(product, spec, X, y, prec, graphs, windows, mode="scaled", kind="systematic", always=False, J=64):
     t = product.GpuEnsembleTarget(spec, X, y, J, precision=prec)
     if graphs:
         t.set_graphs(True)
@@ -48,3 +47,16 @@ def test_graph_replay_bit_identical(product, prec, mode, kind, always):
     for ra, rb in zip(a[0], b[0]):
         assert {k: v for k, v in ra.items() if k != "sampler_ms"} == {k: v for k, v in rb.items() if k != "sampler_ms"}
     assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and a[3] == b[3] == len(windows)
+
+
+def test_graph_replay_c2_shape(product):
+    """The one-hidden-layer tensor-core path at the C2 shape (CTA-pair cluster launches of the
+    fused forward, TMA descriptors as kernel parameters) replays bit-identically too."""
+    spec = product.NetSpec([784, 200, 10], "relu")
+    X, y = product.make_teacher_data(spec, 1200, 1, 0, 2, threads=8)
+    windows = [(0, 512)] * 5 + [(0, 1024)] * 4
+    a = _run(product, spec, X, y, "f16x2", False, windows, J=96)
+    b = _run(product, spec, X, y, "f16x2", True, windows, J=96)
+    for ra, rb in zip(a[0], b[0]):
+        assert {k: v for k, v in ra.items() if k != "sampler_ms"} == {k: v for k, v in rb.items() if k != "sampler_ms"}
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
