@@ -458,53 +458,62 @@ __global__ void pool_fwd_nhwc_kernel(ConvDev d, const float* __restrict__ A, int
 // channel-major copies (the weight-gradient operand) -- are written with coalesced rows.
 // Rows / columns no window covers (odd sizes, floor pooling) are never written (zero from
 // allocation).
+// Layout of a stage's weight-gradient delta copies (ConvTcState::DzLayout): value (m, c, y, x)
+// goes to S[kx * s_kx + c * s_c + m * s_m + y * s_y + x + kx] for kx < kc.
+struct DzL {
+  int kc, s_y;
+  int64_t s_kx, s_m, s_c;
+};
+
 __global__ void __launch_bounds__(256) pool_bwd_rows_kernel(ConvDev d, int act, const float* __restrict__ A,
                                                             int64_t a_ps, const float* __restrict__ dP, int64_t dp_ps,
                                                             int flat, float* __restrict__ dZ, int64_t dz_ps, int64_t M,
-                                                            float* __restrict__ S, int64_t s_ps, int64_t s_kx, int s_wp) {
-  extern __shared__ float pz[];  // [2][wo][C + 1]: the window deltas of the two pre-pool rows
+                                                            float* __restrict__ S, int64_t s_ps, DzL L) {
+  extern __shared__ float pz[];  // [2][wo][C + 1]: the window deltas of two pre-pool rows
   const int C = d.cout, pad = d.k - 1, W2 = d.wo + 2 * pad, H2 = d.ho + 2 * pad, CP = C + 1;
-  const int64_t row = blockIdx.x;  // (j, m, py)
-  const int py = (int)(row % d.sh);
-  const int64_t jm = row / d.sh, m = jm % M, j = jm / M;
+  const int64_t img = blockIdx.x;  // (j, m): one image of one particle per block
+  const int64_t m = img % M, j = img / M;
   const int wo2 = 2 * d.sw;  // pre-pool columns covered by windows
-  for (int i = threadIdx.x; i < 2 * d.wo * CP; i += blockDim.x) pz[i] = 0.f;
-  __syncthreads();
-  const float* arow = A + j * a_ps + m * (int64_t)d.ho * d.wo * C + (int64_t)(2 * py) * d.wo * C;
   const int64_t per = (int64_t)d.sh * d.sw * C;
-  for (int i = threadIdx.x; i < d.sw * C; i += blockDim.x) {  // (px, c), c fastest: coalesced NHWC reads
-    const int c = i % C, px = i / C;
-    const float* a = arow + (int64_t)(2 * px) * C + c;
-    const int64_t rowC = (int64_t)d.wo * C;
-    const float a0 = a[0], a1 = a[C], a2 = a[rowC], a3 = a[rowC + C];
-    int best = 0;
-    float mx = a0;
-    if (a1 > mx) { mx = a1; best = 1; }
-    if (a2 > mx) { mx = a2; best = 2; }
-    if (a3 > mx) { mx = a3; best = 3; }
-    const float gp = dP[j * dp_ps + m * per + (flat ? (int64_t)c * d.sh * d.sw + py * d.sw + px
-                                                        : ((int64_t)py * d.sw + px) * C + c)];
-    const float v = tf32_hi(gp * (act == DASMC_RELU ? (mx > 0.f ? 1.f : 0.f) : 1.f - mx * mx));
-    pz[((best >> 1) * d.wo + 2 * px + (best & 1)) * CP + c] = v;
-  }
-  __syncthreads();
-  // NHWC zero-bordered rows: (dy, x, c) contiguous per row
+  const float* aimg = A + j * a_ps + m * (int64_t)d.ho * d.wo * C;
   float* z = dZ + j * dz_ps + m * (int64_t)H2 * W2 * C;
-  for (int i = threadIdx.x; i < 2 * wo2 * C; i += blockDim.x) {
-    const int c = i % C, xy = i / C, x = xy % wo2, dy = xy / wo2;
-    z[((int64_t)(2 * py + dy + pad) * W2 + x + pad) * C + c] = pz[(dy * d.wo + x) * CP + c];
-  }
-  // channel-major kx-shifted copies: for each (kx, c, dy) a contiguous run over x
-  float* sb = S + j * s_ps + m * (int64_t)C * d.ho * s_wp;
-  for (int i = threadIdx.x; i < d.k * C * 2 * wo2; i += blockDim.x) {
-    const int x = i % wo2, r = i / wo2, dy = r % 2, kc = r / 2, c = kc % C, kx = kc / C;
-    sb[kx * s_kx + ((int64_t)c * d.ho + 2 * py + dy) * s_wp + x + kx] = pz[(dy * d.wo + x) * CP + c];
+  float* sb = S + j * s_ps + m * L.s_m;
+  for (int py = 0; py < d.sh; ++py) {
+    __syncthreads();  // the previous row pair's reads of pz are done
+    for (int i = threadIdx.x; i < 2 * d.wo * CP; i += blockDim.x) pz[i] = 0.f;
+    __syncthreads();
+    const float* arow = aimg + (int64_t)(2 * py) * d.wo * C;
+    for (int i = threadIdx.x; i < d.sw * C; i += blockDim.x) {  // (px, c), c fastest: coalesced NHWC reads
+      const int c = i % C, px = i / C;
+      const float* a = arow + (int64_t)(2 * px) * C + c;
+      const int64_t rowC = (int64_t)d.wo * C;
+      const float a0 = a[0], a1 = a[C], a2 = a[rowC], a3 = a[rowC + C];
+      int best = 0;
+      float mx = a0;
+      if (a1 > mx) { mx = a1; best = 1; }
+      if (a2 > mx) { mx = a2; best = 2; }
+      if (a3 > mx) { mx = a3; best = 3; }
+      const float gp = dP[j * dp_ps + m * per + (flat ? (int64_t)c * d.sh * d.sw + py * d.sw + px
+                                                          : ((int64_t)py * d.sw + px) * C + c)];
+      const float v = tf32_hi(gp * (act == DASMC_RELU ? (mx > 0.f ? 1.f : 0.f) : 1.f - mx * mx));
+      pz[((best >> 1) * d.wo + 2 * px + (best & 1)) * CP + c] = v;
+    }
+    __syncthreads();
+    // NHWC zero-bordered rows: (dy, x, c) contiguous per row
+    for (int i = threadIdx.x; i < 2 * wo2 * C; i += blockDim.x) {
+      const int c = i % C, xy = i / C, x = xy % wo2, dy = xy / wo2;
+      z[((int64_t)(2 * py + dy + pad) * W2 + x + pad) * C + c] = pz[(dy * d.wo + x) * CP + c];
+    }
+    // channel-major (kx-shifted) copies: for each (kx, c, dy) a contiguous run over x
+    for (int i = threadIdx.x; i < L.kc * C * 2 * wo2; i += blockDim.x) {
+      const int x = i % wo2, r = i / wo2, dy = r % 2, kc = r / 2, c = kc % C, kx = kc / C;
+      sb[kx * L.s_kx + c * L.s_c + (int64_t)(2 * py + dy) * L.s_y + x + kx] = pz[(dy * d.wo + x) * CP + c];
+    }
   }
 }
 
 void launch_pool_bwd(Ctx& c, const ConvDev& d, int act, const float* A, int64_t a_ps, const float* dP, int64_t dp_ps,
-                     int flat, float* dZ, int64_t dz_ps, int64_t M, int64_t J, float* S, int64_t s_ps, int64_t s_kx,
-                     int s_wp) {
+                     int flat, float* dZ, int64_t dz_ps, int64_t M, int64_t J, float* S, int64_t s_ps, const DzL& L) {
   const size_t sm = sizeof(float) * 2 * (size_t)d.wo * (d.cout + 1);
   if (sm > 48 * 1024) {
     static bool attr[kMaxDevices] = {};
@@ -514,8 +523,8 @@ void launch_pool_bwd(Ctx& c, const ConvDev& d, int act, const float* A, int64_t 
       attr[dv] = true;
     }
   }
-  pool_bwd_rows_kernel<<<(unsigned)(J * M * d.sh), 256, sm, c.stream>>>(d, act, A, a_ps, dP, dp_ps, flat, dZ, dz_ps, M,
-                                                                        S, s_ps, s_kx, s_wp);
+  pool_bwd_rows_kernel<<<(unsigned)(J * M), 256, sm, c.stream>>>(d, act, A, a_ps, dP, dp_ps, flat, dZ, dz_ps, M, S,
+                                                                 s_ps, L);
   LAUNCHED();
 }
 
@@ -531,8 +540,7 @@ __global__ void nhwc_to_flat_kernel(ConvDev d, const float* __restrict__ A, int6
   }
 }
 __global__ void flat_to_dzpad_kernel(ConvDev d, const float* __restrict__ F, int64_t f_ps, float* __restrict__ dZ,
-                                     int64_t dz_ps, int64_t M, int64_t J, float* __restrict__ S, int64_t s_ps,
-                                     int64_t s_kx, int s_wp) {
+                                     int64_t dz_ps, int64_t M, int64_t J, float* __restrict__ S, int64_t s_ps, DzL L) {
   const int C = d.cout, pad = d.k - 1, W2 = d.wo + 2 * pad, H2 = d.ho + 2 * pad;
   const int64_t per = (int64_t)d.ho * d.wo * C, total = J * M * per;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
@@ -540,8 +548,8 @@ __global__ void flat_to_dzpad_kernel(ConvDev d, const float* __restrict__ F, int
     const int o = (int)(rem - m * per), c = o % C, yx = o / C, y = yx / d.wo, x = yx - y * d.wo;
     const float v = tf32_hi(F[j * f_ps + m * per + (int64_t)c * d.ho * d.wo + yx]);
     dZ[j * dz_ps + m * (int64_t)H2 * W2 * C + ((int64_t)(y + pad) * W2 + x + pad) * C + c] = v;
-    float* s0 = S + j * s_ps + m * (int64_t)C * d.ho * s_wp + ((int64_t)c * d.ho + y) * s_wp + x;
-    for (int kx = 0; kx < d.k; ++kx, s0 += s_kx + 1) *s0 = v;
+    float* s0 = S + j * s_ps + m * L.s_m + c * L.s_c + (int64_t)y * L.s_y + x;
+    for (int kx = 0; kx < L.kc; ++kx, s0 += L.s_kx + 1) *s0 = v;
   }
 }
 
@@ -559,6 +567,17 @@ __global__ void im2col_x_kernel(ConvDev d, const float* __restrict__ X, int64_t 
       v = X[((m * d.cin + ci) * d.hin + y + ky) * d.win + x + kx];
     }
     out[g] = v;
+  }
+}
+
+// XcolT[q][r] = Xcol[r][q] (q < K) and XcolT[K][r] = 1 (the bias row): the stage-0
+// weight-gradient A operand, pixel-contiguous rows
+__global__ void xcolT_kernel(const float* __restrict__ Xcol, int64_t R, int Kp, int K, int64_t ld,
+                             float* __restrict__ XcolT) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < R * (K + 1);
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = g / R, r = g - q * R;
+    XcolT[q * ld + r] = q < K ? Xcol[r * Kp + q] : 1.f;
   }
 }
 
@@ -600,6 +619,13 @@ struct ConvTcState {
   // second outputs, pool kernels): zero-initialised, so padding columns stay zero
   float* inT[kMaxConv] = {};   // stage input [mcap][cin][hin][win_p] per particle (stage 0: shared X copy)
   float* dZs[kMaxConv] = {};   // [k][mcap][cout][ho][win_p] per particle: dZ shifted right by kx
+  DzL dzl[kMaxConv] = {};      // layout of dZs[i] (set with the chunk capacity)
+  // stage 0 with pixels-per-image % 4 == 0: its weight gradient contracts the shared im2col of X
+  // (transposed, XcolT[q][image * npix + p]) with the unshifted channel-major delta, instead of
+  // k kx-shifted delta copies of the (largest) stage-0 plane
+  bool xcol0 = false;
+  float* XcolT = nullptr;
+  int64_t XcolT_rows = 0;
   int* c2o[kMaxConv] = {};     // input pixel of stage i -> its inT[i] offset (channel 0)
   int* dzo[kMaxConv] = {};     // output pixel of stage i -> its dZs[i] offset (channel 0, kx 0)
   // tables (device, int32)
@@ -681,29 +707,38 @@ void build_tables(Ctx& c, int64_t mc) {
     s->fa_row[i] = upload_vec(fa_row);
     s->zpix[i] = upload_vec(zpix);
     s->fa_col[i] = upload_vec(fa_col);
-    // weight gradient (shifted-rows form)
-    const int64_t planeA = (int64_t)d.cin * d.hin * wp, planeB = (int64_t)d.cout * d.ho * wp;
-    std::vector<int> wa_row((size_t)k * d.cin + 1), prow((size_t)k * d.cin + 1);
-    for (int ky = 0; ky < k; ++ky)
-      for (int ci = 0; ci < d.cin; ++ci) {
-        wa_row[(size_t)ky * d.cin + ci] = (int)((int64_t)ci * d.hin * wp + (int64_t)ky * wp);
-        prow[(size_t)ky * d.cin + ci] = ci * kk2 + ky * k;
-      }
-    wa_row[(size_t)k * d.cin] = kOnesRow;
-    prow[(size_t)k * d.cin] = -1;
-    std::vector<int> wa_col((size_t)(mc * d.ho * wp)), wb_col((size_t)(mc * d.ho * wp));
-    for (int64_t m = 0; m < mc; ++m)
-      for (int y = 0; y < d.ho; ++y)
-        for (int x = 0; x < wp; ++x) {
-          const int64_t q = (m * d.ho + y) * wp + x;
-          wa_col[(size_t)q] = (int)(m * planeA + (int64_t)y * wp + x);
-          wb_col[(size_t)q] = (int)(m * planeB + (int64_t)y * wp + x);
+    // weight gradient: shifted-rows form, or (stage 0, xcol0) the shared im2col of X
+    const int64_t planeA = (int64_t)d.cin * d.hin * wp;
+    const DzL& L = s->dzl[i];
+    const bool xc = i == 0 && s->xcol0;
+    const int nA = xc ? Kf + 1 : k * d.cin + 1, nB = xc ? d.cout : k * d.cout;
+    std::vector<int> wa_row((size_t)nA), prow((size_t)nA);
+    if (xc) {
+      for (int q = 0; q < Kf; ++q) prow[(size_t)q] = q;  // (ci, ky, kx): the internal W order
+    } else {
+      for (int ky = 0; ky < k; ++ky)
+        for (int ci = 0; ci < d.cin; ++ci) {
+          wa_row[(size_t)ky * d.cin + ci] = (int)((int64_t)ci * d.hin * wp + (int64_t)ky * wp);
+          prow[(size_t)ky * d.cin + ci] = ci * kk2 + ky * k;
         }
-    std::vector<int> wb_row((size_t)k * d.cout), pcol((size_t)k * d.cout), bcol((size_t)k * d.cout);
-    for (int kx = 0; kx < k; ++kx)
+      wa_row[(size_t)k * d.cin] = kOnesRow;
+    }
+    prow[(size_t)nA - 1] = -1;
+    const int64_t kw = xc ? mc * npix : mc * d.ho * wp;  // K of the weight-gradient GEMM
+    std::vector<int> wa_col(xc ? 0 : (size_t)kw), wb_col(xc ? 0 : (size_t)kw);
+    if (!xc)
+      for (int64_t m = 0; m < mc; ++m)
+        for (int y = 0; y < d.ho; ++y)
+          for (int x = 0; x < wp; ++x) {
+            const int64_t q = (m * d.ho + y) * wp + x;
+            wa_col[(size_t)q] = (int)(m * planeA + (int64_t)y * wp + x);
+            wb_col[(size_t)q] = (int)(m * L.s_m + (int64_t)y * L.s_y + x);
+          }
+    std::vector<int> wb_row((size_t)nB), pcol((size_t)nB), bcol((size_t)nB);
+    for (int kx = 0; kx < nB / d.cout; ++kx)
       for (int co = 0; co < d.cout; ++co) {
         const size_t n = (size_t)kx * d.cout + co;
-        wb_row[n] = (int)((int64_t)kx * mc * planeB + (int64_t)co * d.ho * wp);
+        wb_row[n] = (int)(kx * L.s_kx + co * L.s_c);
         pcol[n] = co * Kf + kx;
         bcol[n] = kx == 0 ? co : -1;
       }
@@ -712,14 +747,14 @@ void build_tables(Ctx& c, int64_t mc) {
       for (int y = 0; y < d.hin; ++y)
         for (int x = 0; x < d.win; ++x) c2o[(size_t)(m * nin + (int64_t)y * d.win + x)] = (int)(m * planeA + (int64_t)y * wp + x);
       for (int y = 0; y < d.ho; ++y)
-        for (int x = 0; x < d.wo; ++x) dzo[(size_t)(m * npix + (int64_t)y * d.wo + x)] = (int)(m * planeB + (int64_t)y * wp + x);
+        for (int x = 0; x < d.wo; ++x) dzo[(size_t)(m * npix + (int64_t)y * d.wo + x)] = (int)(m * L.s_m + (int64_t)y * L.s_y + x);
     }
     s->c2o[i] = upload_vec(c2o);
     s->dzo[i] = upload_vec(dzo);
-    s->wa_row[i] = upload_vec(wa_row);
-    s->wa_col[i] = upload_vec(wa_col);
+    s->wa_row[i] = xc ? nullptr : upload_vec(wa_row);
+    s->wa_col[i] = xc ? nullptr : upload_vec(wa_col);
     s->wb_row[i] = upload_vec(wb_row);
-    s->wb_col[i] = upload_vec(wb_col);
+    s->wb_col[i] = xc ? nullptr : upload_vec(wb_col);
     s->prow[i] = upload_vec(prow);
     s->pcol[i] = upload_vec(pcol);
     s->bcol[i] = upload_vec(bcol);
@@ -839,6 +874,10 @@ void cnn_tc_init(Ctx& c) {
     s->nmmaD[i] = round_up(d.cin, 16);
     s->KpD[i] = round_up(d.cout * d.k * d.k, kCBK);
     s->nmmaW[i] = round_up(d.k * d.cout, 16);
+    if (i == 0 && (d.ho * d.wo) % 4 == 0) {
+      s->xcol0 = true;
+      s->nmmaW[0] = round_up(d.cout, 16);
+    }
     s->winp[i] = round_up(d.win, 4);
     CK(cudaMalloc(&s->Wf[i], sizeof(float) * (size_t)c.Jmax * s->nmmaF[i] * s->KpF[i]));
     if (i > 0) CK(cudaMalloc(&s->Wd[i], sizeof(float) * (size_t)c.Jmax * s->nmmaD[i] * s->KpD[i]));
@@ -874,6 +913,22 @@ void cnn_tc_refresh_data(Ctx& c, const float* X, int64_t rows) {
   }
   im2col_x_kernel<<<grid_of(rows * per), 256, 0, c.stream>>>(d0, s->Xr, rows, s->KpF[0], s->Xcol);
   LAUNCHED();
+  if (s->xcol0) {
+    const int K0 = d0.cin * d0.k * d0.k;
+    const int64_t npix = (int64_t)d0.ho * d0.wo;
+    if (rows > s->XcolT_rows) {
+      CK(cudaStreamSynchronize(c.stream));
+      if (s->XcolT) CK(cudaFree(s->XcolT));
+      s->XcolT = nullptr;
+      const int64_t cap = std::max(rows, c.n);
+      if ((int64_t)(K0 + 1) * cap * npix >= ((int64_t)1 << 31)) throw std::invalid_argument("conv: X im2col too large");
+      CK(cudaMalloc(&s->XcolT, sizeof(float) * (size_t)(K0 + 1) * cap * npix));
+      s->XcolT_rows = cap;
+    }
+    xcolT_kernel<<<grid_of(rows * npix * (K0 + 1)), 256, 0, c.stream>>>(s->Xcol, rows * npix, s->KpF[0], K0,
+                                                                  s->XcolT_rows * npix, s->XcolT);
+    LAUNCHED();
+  }
 }
 
 void cnn_tc_free(Ctx& c) {
@@ -887,6 +942,7 @@ void cnn_tc_free(Ctx& c) {
   }
   if (s->Xr) cudaFree(s->Xr);
   if (s->Xcol) cudaFree(s->Xcol);
+  if (s->XcolT) cudaFree(s->XcolT);
   if (s->ones) cudaFree(s->ones);
   delete s;
   c.ctc = nullptr;
@@ -931,7 +987,21 @@ void cnn_tc_alloc(Ctx& c, int64_t mc) {
     if (d.pool || last) CK(cudaMalloc(&c.cpool[i], sizeof(float) * J * mc * (d.pool ? pool_plane(d) : act_plane(d))));
     if (d.pool && !last) CK(cudaMalloc(&s->dP[i], sizeof(float) * J * mc * pool_plane(d)));
     const size_t fa = (size_t)mc * d.cin * d.hin * wp * (i == 0 ? 1 : J);  // stage 0: shared by particles
-    const size_t fb = J * d.k * mc * d.cout * d.ho * wp;
+    DzL& L = s->dzl[i];
+    if (i == 0 && s->xcol0) {  // unshifted, channel-major [c][m][y*wo + x]
+      L.kc = 1;
+      L.s_y = d.wo;
+      L.s_m = (int64_t)d.ho * d.wo;
+      L.s_c = mc * L.s_m;
+      L.s_kx = 0;
+    } else {  // k copies [kx][m][c][y][x'], x' < win_p
+      L.kc = d.k;
+      L.s_y = (int)wp;
+      L.s_c = (int64_t)d.ho * wp;
+      L.s_m = d.cout * L.s_c;
+      L.s_kx = mc * L.s_m;
+    }
+    const size_t fb = J * (size_t)L.kc * (L.kc > 1 ? (size_t)L.s_kx : (size_t)d.cout * L.s_c);
     CK(cudaMalloc(&s->inT[i], sizeof(float) * fa));
     CK(cudaMemsetAsync(s->inT[i], 0, sizeof(float) * fa, c.stream));
     CK(cudaMalloc(&s->dZs[i], sizeof(float) * fb));
@@ -1040,44 +1110,57 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
   const int64_t img = (int64_t)net.in_c * net.in_h * net.in_w;
   const int64_t cap = s->mcap;
   const int L = net.nconv - 1;
-  auto planeB_of = [&](int i) { return (int64_t)net.conv[i].cout * net.conv[i].ho * s->winp[i]; };
+  // per-particle floats of dZs[i]
+  auto dzs_ps = [&](int i) {
+    const DzL& Lz = s->dzl[i];
+    return Lz.kc > 1 ? (int64_t)Lz.kc * Lz.s_kx : (int64_t)net.conv[i].cout * Lz.s_c;
+  };
   {
     const ConvDev& d = net.conv[L];
-    const int64_t pb = cap * planeB_of(L);
     if (d.pool) {
       launch_pool_bwd(c, d, net.act, c.cact[L], cap * act_plane(d), c.cpool[L], cap * pool_plane(d), 1, c.cdel[L],
-                      cap * pad_plane(d), mc, J, s->dZs[L], d.k * pb, pb, s->winp[L]);
+                      cap * pad_plane(d), mc, J, s->dZs[L], dzs_ps(L), s->dzl[L]);
     } else {
       flat_to_dzpad_kernel<<<grid_of(J * mc * act_plane(d)), 256, 0, c.stream>>>(
-          d, c.cpool[L], cap * act_plane(d), c.cdel[L], cap * pad_plane(d), mc, J, s->dZs[L], d.k * pb, pb, s->winp[L]);
+          d, c.cpool[L], cap * act_plane(d), c.cdel[L], cap * pad_plane(d), mc, J, s->dZs[L], dzs_ps(L), s->dzl[L]);
       LAUNCHED();
     }
   }
   for (int i = L; i >= 0; --i) {
     const ConvDev& d = net.conv[i];
     const int wp = s->winp[i];
-    // ---- weight gradient + fused leapfrog (shifted-rows form, see ConvTcState):
-    //      D[(ky, ci) | ones, (kx, co)] = sum_(m, y, x') inT[ci][y + ky][x'] dZs[kx][co][y][x']
+    // ---- weight gradient + fused leapfrog:
+    //   shifted-rows form  D[(ky, ci) | ones, (kx, co)] = sum_(m, y, x') inT[ci][y + ky][x'] dZs[kx][co][y][x']
+    //   stage 0 (xcol0)    D[(ci, ky, kx) | ones, co]  = sum_(m, p) XcolT[(ci, ky, kx)][m, p] dZ[co][m, p]
     {
+      const bool xc = i == 0 && s->xcol0;
       const int64_t planeA = (int64_t)d.cin * d.hin * wp;
-      const int64_t planeB = planeB_of(i);
-      if (i == 0) {  // stage 0's input is X: its channel-major padded copy, shared by the particles
-        to_chw_pad_kernel<<<grid_of(mc * planeA), 256, 0, c.stream>>>(s->Xr + m0 * img, 0, 0, d.cin, d.hin, d.win, wp,
-                                                                     s->inT[0], 0, mc, 1);
-        LAUNCHED();
-      }
       GParams p{};
-      p.a.base = s->inT[i];
-      p.a.ps = i == 0 ? 0 : cap * planeA;
-      p.a.rowoff = s->wa_row[i];
-      p.a.nrows = d.k * d.cin + 1;
-      p.a.coloff = s->wa_col[i];
-      p.a.K = (int)(mc * d.ho * wp);
+      if (xc) {
+        const int64_t npix = (int64_t)d.ho * d.wo;
+        p.a.base = s->XcolT + m0 * npix;
+        p.a.ps = 0;
+        p.a.ld = (int)(s->XcolT_rows * npix);
+        p.a.nrows = d.cin * d.k * d.k + 1;
+        p.a.K = (int)(mc * npix);
+      } else {
+        if (i == 0) {  // stage 0's input is X: its channel-major padded copy, shared by the particles
+          to_chw_pad_kernel<<<grid_of(mc * planeA), 256, 0, c.stream>>>(s->Xr + m0 * img, 0, 0, d.cin, d.hin, d.win,
+                                                                       wp, s->inT[0], 0, mc, 1);
+          LAUNCHED();
+        }
+        p.a.base = s->inT[i];
+        p.a.ps = i == 0 ? 0 : cap * planeA;
+        p.a.rowoff = s->wa_row[i];
+        p.a.nrows = d.k * d.cin + 1;
+        p.a.coloff = s->wa_col[i];
+        p.a.K = (int)(mc * d.ho * wp);
+      }
       p.a.vec = 1;
       p.b.base = s->dZs[i];
-      p.b.ps = (int64_t)d.k * cap * planeB;
+      p.b.ps = dzs_ps(i);
       p.b.rowoff = s->wb_row[i];
-      p.b.nrows = d.k * d.cout;
+      p.b.nrows = s->dzl[i].kc * d.cout;
       p.b.coloff = s->wb_col[i];
       p.b.K = p.a.K;
       p.b.vec = 1;
@@ -1086,7 +1169,7 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
       p.rtiles = (p.a.nrows + kCBM - 1) / kCBM;
       p.nkb = (p.a.K + kCBK - 1) / kCBK;
       p.nmma = s->nmmaW[i];
-      p.nvalid = d.k * d.cout;
+      p.nvalid = p.b.nrows;
       p.Dp = net.Dp;
       p.boff = d.boff;
       p.e = e;
@@ -1133,20 +1216,18 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
       p.mask = c.cact[i - 1];
       p.mask_ps = cap * act_plane(dp);
       p.mask_ld = dp.cout;
-      // and its kx-shifted channel-major copies (stage i-1's weight-gradient B operand)
+      // and its channel-major (kx-shifted) copies (stage i-1's weight-gradient B operand)
       p.out2 = s->dZs[i - 1];
-      p.out2_ps = (int64_t)dp.k * cap * planeB_of(i - 1);
+      p.out2_ps = dzs_ps(i - 1);
       p.out2off = s->dzo[i - 1];
-      p.out2_cs = (int64_t)dp.ho * s->winp[i - 1];
-      p.out2_ks = cap * planeB_of(i - 1);
-      p.out2_k = dp.k;
+      p.out2_cs = s->dzl[i - 1].s_c;
+      p.out2_ks = s->dzl[i - 1].s_kx;
+      p.out2_k = s->dzl[i - 1].kc;
     }
     launch_gemm<kEpiConvDx>(c, p, net.act);
-    if (dp.pool) {
-      const int64_t pb = cap * planeB_of(i - 1);
+    if (dp.pool)
       launch_pool_bwd(c, dp, net.act, c.cact[i - 1], cap * act_plane(dp), s->dP[i - 1], cap * pool_plane(dp), 0,
-                      c.cdel[i - 1], cap * pad_plane(dp), mc, J, s->dZs[i - 1], dp.k * pb, pb, s->winp[i - 1]);
-    }
+                      c.cdel[i - 1], cap * pad_plane(dp), mc, J, s->dZs[i - 1], dzs_ps(i - 1), s->dzl[i - 1]);
   }
 }
 
