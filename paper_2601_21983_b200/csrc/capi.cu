@@ -582,6 +582,10 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
     // a few whole columns per thread: the 256-step F2 jump-ahead is paid once per ~1024 normals
     // (warp stores stay within a few 32-byte sectors per row)
     c.rng_chunk = widest >= 128 ? widest * std::max<int64_t>(1, kRngChunkNormals / widest) : kRngChunkNormals;
+    // small nets (e.g. C1, D = 2410): at least ~64 chunks per particle, so there are enough
+    // independent streams to fill the GPU (per-thread work is a serial chain).  A function of D
+    // only: the fixed-order sums of the chunk partials do not depend on J or on the sharding
+    c.rng_chunk = std::min<int64_t>(c.rng_chunk, std::max<int64_t>(16, c.net.D / 64));
   }
   const int64_t nch_rng = (c.net.D + c.rng_chunk - 1) / c.rng_chunk;
   c.rng_slots = (int)nch_rng;
