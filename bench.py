@@ -77,7 +77,7 @@ DTYPES = {"fp32": "f32", "tf32": "tf32", "3xtf32": "3xtf32", "f16": "f16",
 
 
 def window(w, k):
-    if w.get("const_window"):
+    if w.get("const_window") or w.get("sda"):  # SDA: the initial window (the schedule is adaptive)
         return w["mb"]
     if "ctr" in w:
         c0, sw = w["ctr"]
