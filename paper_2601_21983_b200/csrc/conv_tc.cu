@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <type_traits>
 #include <vector>
@@ -63,6 +64,7 @@ struct GParams {
   GOperand a, b;
   const float* ones;  // 16 bytes of 1.0f (the source of kOnesRow elements)
   int J, rtiles, nkb, nmma, tcols_half, stages;
+  int dbg;  // DASMC_CONV_DBG ablations (profiling only): 1 no operand copies, 2 no epilogue stores, 4 no MMAs
   // epilogue (forward / delta): out[j * out_ps + outoff[r] + n] for r < Rvalid, n < nvalid
   int Rvalid, nvalid;
   float* out;
@@ -261,8 +263,10 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
         }
         mbar_wait(&empty[s], ph ^ 1);
         const uint32_t st = stages0 + (uint32_t)s * stage_bytes;
-        gather_tile<8, AV>(p.a, abase, p.ones, st, ra, ca, kCBM, warp, lane);
-        gather_tile<16, true>(p.b, bbase, p.ones, st + a_bytes, rb, cb, p.nmma, warp, lane);
+        if (!(p.dbg & 1)) {
+          gather_tile<8, AV>(p.a, abase, p.ones, st, ra, ca, kCBM, warp, lane);
+          gather_tile<16, true>(p.b, bbase, p.ones, st + a_bytes, rb, cb, p.nmma, warp, lane);
+        }
         cp_async_arrive(&full[s]);
         if (++s == p.stages) {
           s = 0;
@@ -298,8 +302,9 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
           tc_fence_after();
           uint8_t* st = smem + (size_t)s * stage_bytes;
           const uint64_t ad = smem_desc(st), bd = smem_desc(st + a_bytes);
+          if (!(p.dbg & 4))
 #pragma unroll
-          for (int k = 0; k < 4; ++k) tc_mma<0>(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < 4; ++k) tc_mma<0>(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
           tc_commit(&empty[s]);
           if (++s == p.stages) {
             s = 0;
@@ -329,6 +334,7 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
         const int n0 = ch * 16;
         const int nq = min(16, p.nvalid - n0);  // warp-uniform
         if (nq <= 0) continue;
+        if (p.dbg & 2) continue;
         if (EPI == kEpiConvFwd || EPI == kEpiConvDx) {
           if (r >= p.Rvalid) continue;
           float* dst = p.out + (int64_t)j * p.out_ps + (p.outoff ? (int64_t)p.outoff[r] : (int64_t)r * p.out_ld) + n0;
@@ -793,6 +799,11 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
   int tc = 32;
   while (tc < p.nmma) tc <<= 1;
   p.tcols_half = tc;
+  static const int dbg = [] {
+    const char* e = std::getenv("DASMC_CONV_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.dbg = dbg;
   const int units = p.rtiles * p.J;
   auto go = [&](auto act_c, auto av_c) {
     constexpr int A_ = decltype(act_c)::value;
