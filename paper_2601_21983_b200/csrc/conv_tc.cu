@@ -64,6 +64,7 @@ struct GParams {
   GOperand a, b;
   const float* ones;  // 16 bytes of 1.0f (the source of kOnesRow elements)
   int J, rtiles, nkb, nmma, tcols_half, stages;
+  int nsub;  // 128B-swizzle k atoms (32 tf32 each) per pipeline stage: nkb stages cover nkb * nsub atoms
   int dbg;  // DASMC_CONV_DBG ablations (profiling only): 1 no operand copies, 2 no epilogue stores, 4 no MMAs
   // epilogue (forward / delta): out[j * out_ps + outoff[r] + n] for r < Rvalid, n < nvalid
   int Rvalid, nvalid;
@@ -190,13 +191,41 @@ __device__ __forceinline__ void gather_tile(const GOperand& o, const float* pbas
 
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
+// mbarrier wait without a suspend-time hint: the convolution tiles are short (a few k-blocks),
+// so the pipeline hand-offs are frequent and a parked warp's wake-up latency would dominate
+// (DASMC_CONV_SPIN=0 restores the suspending wait for A/B)
+#ifndef DASMC_CONV_SPIN
+#define DASMC_CONV_SPIN 1
+#endif
+__device__ __forceinline__ void cwait(uint64_t* bar, uint32_t parity) {
+#if DASMC_CONV_SPIN
+  uint32_t ok = 0;
+  const long long t0 = clock64();
+  for (uint32_t i = 0;; ++i) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.b32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if ((i & 0xFFFFu) == 0xFFFFu && clock64() - t0 > 20000000000LL) __trap();  // watchdog (~10 s)
+  }
+#else
+  mbar_wait(bar, parity);
+#endif
+}
+
 template <int EPI, int ACT, bool AV>
 __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(const __grid_constant__ GParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t a_bytes = kCBM * 128, b_bytes = (uint32_t)p.nmma * 128;
-  const uint32_t stage_bytes = a_bytes + b_bytes;
+  const uint32_t stage_bytes = (uint32_t)p.nsub * (a_bytes + b_bytes);  // [A atoms][B atoms]
   uint64_t* full = (uint64_t*)(smem + (size_t)p.stages * stage_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
@@ -235,16 +264,21 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
     int s = 0;
     uint32_t ph = 0;
     int t = blockIdx.x;
-    constexpr int NCA = AV ? 1 : 8;  // column offsets per k-block this lane needs (A); B is vector
-    int ra[8], rb[16], ran[8], rbn[16], ca[NCA], cb[1], can[NCA], cbn[1];
+    static_assert(AV, "the gather producers copy 16-byte chunks");
+    constexpr int MAXS = 4;  // atoms per stage
+    int ra[8], rb[16], ran[8], rbn[16], ca[MAXS], cb[MAXS], can[MAXS], cbn[MAXS];
     if (t < units) {
       load_rows<8>(p.a, (t % p.rtiles) * kCBM, kCBM, warp, lane, ra);
       load_rows<16>(p.b, 0, p.nmma, warp, lane, rb);
     }
-    load_cols<AV>(p.a, 0, lane, ca);
-    load_cols<true>(p.b, 0, lane, cb);
+#pragma unroll
+    for (int u = 0; u < MAXS; ++u)
+      if (u < p.nsub) {
+        load_cols<true>(p.a, u, lane, ca + u);
+        load_cols<true>(p.b, u, lane, cb + u);
+      }
     while (t < units) {
-      const int rt = t % p.rtiles, j = t / p.rtiles;
+      const int j = t / p.rtiles;
       const int tn = t + gridDim.x;
       if (tn < units) {
         load_rows<8>(p.a, (tn % p.rtiles) * kCBM, kCBM, warp, lane, ran);
@@ -252,20 +286,28 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
       }
       const float* abase = p.a.base + (int64_t)j * p.a.ps;
       const float* bbase = p.b.base + (int64_t)j * p.b.ps;
-      (void)rt;
       for (int kb = 0; kb < p.nkb; ++kb) {
-        const int kbn = kb + 1 < p.nkb ? kb + 1 : 0;  // the next tile starts again at k-block 0
-        load_cols<AV>(p.a, kbn, lane, can);
-        load_cols<true>(p.b, kbn, lane, cbn);
-        if (lane == 0 && kb + 8 < p.nkb) {
-          if (p.a.coloff) prefetch_l1(p.a.coloff + (kb + 8) * kCBK);
-          if (p.b.coloff) prefetch_l1(p.b.coloff + (kb + 8) * kCBK);
+        const int kbn = kb + 1 < p.nkb ? kb + 1 : 0;  // the next tile starts again at stage 0
+#pragma unroll
+        for (int u = 0; u < MAXS; ++u)
+          if (u < p.nsub) {
+            load_cols<true>(p.a, kbn * p.nsub + u, lane, can + u);
+            load_cols<true>(p.b, kbn * p.nsub + u, lane, cbn + u);
+          }
+        if (lane == 0 && kb + 4 < p.nkb) {
+          if (p.a.coloff) prefetch_l1(p.a.coloff + (kb + 4) * p.nsub * kCBK);
+          if (p.b.coloff) prefetch_l1(p.b.coloff + (kb + 4) * p.nsub * kCBK);
         }
-        mbar_wait(&empty[s], ph ^ 1);
+        cwait(&empty[s], ph ^ 1);
         const uint32_t st = stages0 + (uint32_t)s * stage_bytes;
         if (!(p.dbg & 1)) {
-          gather_tile<8, AV>(p.a, abase, p.ones, st, ra, ca, kCBM, warp, lane);
-          gather_tile<16, true>(p.b, bbase, p.ones, st + a_bytes, rb, cb, p.nmma, warp, lane);
+#pragma unroll
+          for (int u = 0; u < MAXS; ++u)
+            if (u < p.nsub) {
+              gather_tile<8, true>(p.a, abase, p.ones, st + u * a_bytes, ra, ca + u, kCBM, warp, lane);
+              gather_tile<16, true>(p.b, bbase, p.ones, st + p.nsub * a_bytes + u * b_bytes, rb, cb + u, p.nmma, warp,
+                                    lane);
+            }
         }
         cp_async_arrive(&full[s]);
         if (++s == p.stages) {
@@ -273,8 +315,10 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
           ph ^= 1;
         }
 #pragma unroll
-        for (int q = 0; q < NCA; ++q) ca[q] = can[q];
-        cb[0] = cbn[0];
+        for (int u = 0; u < MAXS; ++u) {
+          ca[u] = can[u];
+          cb[u] = cbn[u];
+        }
       }
 #pragma unroll
       for (int q = 0; q < 8; ++q) ra[q] = ran[q];
@@ -291,20 +335,22 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
       for (int t = blockIdx.x; t < units; t += gridDim.x) {
-        mbar_wait(&tempty[acc], aph ^ 1);
+        cwait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * p.tcols_half);
         for (int kb = 0; kb < p.nkb; ++kb) {
-          mbar_wait(&full[s], ph);
+          cwait(&full[s], ph);
           // the stage was written through the generic proxy (cp.async); order it before the
           // tensor core's async-proxy reads
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           tc_fence_after();
           uint8_t* st = smem + (size_t)s * stage_bytes;
-          const uint64_t ad = smem_desc(st), bd = smem_desc(st + a_bytes);
           if (!(p.dbg & 4))
+            for (int u = 0; u < p.nsub; ++u) {
+              const uint64_t ad = smem_desc(st + u * a_bytes), bd = smem_desc(st + p.nsub * a_bytes + u * b_bytes);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) tc_mma<0>(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+              for (int k = 0; k < 4; ++k) tc_mma<0>(d, ad + 2 * k, bd + 2 * k, idesc, (kb | u | k) != 0);
+            }
           tc_commit(&empty[s]);
           if (++s == p.stages) {
             s = 0;
@@ -324,7 +370,7 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < units; t += gridDim.x) {
       const int rt = t % p.rtiles, j = t / p.rtiles;
-      mbar_wait(&tfull[acc], aph);
+      cwait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t)(acc * p.tcols_half) + ((uint32_t)(lg * 32) << 16);
       const int r = rt * kCBM + row_in_tile;
@@ -785,14 +831,24 @@ template <int EPI>
 void launch_gemm(Ctx& c, GParams& p, int act) {
   if (p.nmma > 256) throw std::invalid_argument("conv: MMA N > 256");
   if (!p.b.vec) throw std::invalid_argument("conv: B operands are 16-byte gathers");
-  const size_t stage_bytes = (size_t)kCBM * 128 + (size_t)p.nmma * 128;
-  // Stage ring: the implicit-im2col GEMMs (forward, delta) re-read each input pixel up to k*k
-  // times from L1, so they keep a short ring (3 stages) and leave most of the SM's unified
-  // L1 / shared memory to L1; the weight-gradient GEMM streams (no reuse) with 6 stages.
+  // Atoms per stage: several 32-wide k atoms per pipeline hand-off (the producer -> MMA -> producer
+  // round trip costs hundreds of cycles; conv tiles have few k atoms, so one atom per stage was
+  // hand-off bound), a divisor of the atom count when one exists
+  const int natoms = p.nkb;  // callers pass the atom count
+  int nsub = 1;
+  for (int cand : {4, 3, 2})
+    if (natoms % cand == 0) {
+      nsub = cand;
+      break;
+    }
+  if (nsub == 1 && natoms > 8) nsub = 4;  // padded last stage (zero-filled atoms)
+  p.nsub = nsub;
+  p.nkb = (natoms + nsub - 1) / nsub;
+  const size_t stage_bytes = (size_t)nsub * ((size_t)kCBM * 128 + (size_t)p.nmma * 128);
+  // two CTAs per SM when each gets >= 3 stages in ~110 KB, else one CTA with up to 6 stages
   const size_t fixed = 1024 + 64 * 8 + 64;
-  const int want = EPI == kEpiConvDw ? 6 : 3;
-  int stages = (int)std::min<size_t>(want, (110 * 1024 - fixed) / stage_bytes);
-  if (stages < 2) stages = (int)std::min<size_t>(want, (227 * 1024 - fixed) / stage_bytes);
+  int stages = (int)std::min<size_t>(6, (110 * 1024 - fixed) / stage_bytes);
+  if (stages < 3) stages = (int)std::min<size_t>(6, (227 * 1024 - fixed) / stage_bytes);
   if (stages < 2) throw std::invalid_argument("conv: GEMM tile does not fit in shared memory");
   p.stages = stages;
   const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16;
@@ -826,12 +882,8 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
     kern<<<grid, kCThreads, smem, c.stream>>>(p);
     LAUNCHED();
   };
-  auto go_av = [&](auto act_c) {
-    if (p.a.vec)
-      go(act_c, std::true_type{});
-    else
-      go(act_c, std::false_type{});
-  };
+  if (!p.a.vec) throw std::invalid_argument("conv: A operands are 16-byte gathers");
+  auto go_av = [&](auto act_c) { go(act_c, std::true_type{}); };
   if (act == DASMC_RELU)
     go_av(std::integral_constant<int, DASMC_RELU>{});
   else
