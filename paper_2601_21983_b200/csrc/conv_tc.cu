@@ -835,18 +835,25 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
   // round trip costs hundreds of cycles; conv tiles have few k atoms, so one atom per stage was
   // hand-off bound), a divisor of the atom count when one exists
   const int natoms = p.nkb;  // callers pass the atom count
+  const size_t atom_bytes = (size_t)kCBM * 128 + (size_t)p.nmma * 128;
+  const size_t fixed = 1024 + 64 * 8 + 64;
+  auto fits = [&](int ns) { return 2 * ns * atom_bytes + fixed <= 227 * 1024; };  // >= 2 stages
   int nsub = 1;
   for (int cand : {4, 3, 2})
-    if (natoms % cand == 0) {
+    if (natoms % cand == 0 && fits(cand)) {
       nsub = cand;
       break;
     }
-  if (nsub == 1 && natoms > 8) nsub = 4;  // padded last stage (zero-filled atoms)
+  if (nsub == 1 && natoms > 8)
+    for (int cand : {4, 3, 2})
+      if (fits(cand)) {  // padded last stage (zero-filled atoms)
+        nsub = cand;
+        break;
+      }
   p.nsub = nsub;
   p.nkb = (natoms + nsub - 1) / nsub;
   const size_t stage_bytes = (size_t)nsub * ((size_t)kCBM * 128 + (size_t)p.nmma * 128);
   // two CTAs per SM when each gets >= 3 stages in ~110 KB, else one CTA with up to 6 stages
-  const size_t fixed = 1024 + 64 * 8 + 64;
   int stages = (int)std::min<size_t>(6, (110 * 1024 - fixed) / stage_bytes);
   if (stages < 3) stages = (int)std::min<size_t>(6, (227 * 1024 - fixed) / stage_bytes);
   if (stages < 2) throw std::invalid_argument("conv: GEMM tile does not fit in shared memory");
