@@ -39,12 +39,15 @@ namespace dasmc_b200 {
 
 namespace {
 
+#ifndef DASMC_CONV_PW
+#define DASMC_CONV_PW 8  // gather producer warps per CTA
+#endif
 #ifndef DASMC_CONV_MINB
-#define DASMC_CONV_MINB 2  // CTAs per SM the register budget is sized for (2: 8 producer warps per SM)
+#define DASMC_CONV_MINB 1  // CTAs per SM the register budget is sized for
 #endif
 constexpr int kCBM = 128;              // UMMA M
 constexpr int kCBK = 32;               // tf32 elements per 128-byte swizzle row (one k-block)
-constexpr int kProdWarps = 4;          // gather producers
+constexpr int kProdWarps = DASMC_CONV_PW;  // gather producers
 constexpr int kCThreads = 32 * (kProdWarps + 1 + 4);  // + MMA warp + 4 epilogue warps
 constexpr int kOnesRow = -2147483647;  // row table entry: a row of ones (the bias row of dW)
 constexpr int kZeroRow = -2147483647 - 1;
