@@ -29,6 +29,7 @@
 #include <cstdlib>
 #include <stdexcept>
 #include <type_traits>
+#include <string>
 #include <vector>
 
 #include "conv_tc.cuh"
@@ -68,6 +69,15 @@ struct GParams {
   const float* ones;  // 16 bytes of 1.0f (the source of kOnesRow elements)
   int J, rtiles, nkb, nmma, tcols_half, stages;
   int nsub;  // 128B-swizzle k atoms (32 tf32 each) per pipeline stage: nkb stages cover nkb * nsub atoms
+  // direct convolution (DIRECT kernels, forward / delta with 32-channel blocks): each stage is one
+  // TMA slab of bh + k - 1 input rows x win_w pixels x 32 channels plus the k*k weight atoms of
+  // that channel block; the k*k shifted A operands are the same slab read through descriptors
+  // offset by (ky * win_w + kx) rows -- every input pixel crosses L2 -> SM once per tile
+  CUtensorMap mapA;  // 4-D {C, W, H, images}: the NHWC input (box {32, win_w, bh + k - 1, 1})
+  CUtensorMap mapB;  // 3-D {Kp, nmma, J}: the weight copy (box {32, nmma, 1})
+  int kk, cbn, flipB;        // kernel size, 32-channel blocks, weight atoms in flipped (ky, kx) order
+  int win_w, bh, ybl;        // slab width (pixels), output rows per tile, tiles per image
+  int out_h, out_w, slab_rows, imgs_pp, mimg;
   int dbg;  // DASMC_CONV_DBG ablations (profiling only): 1 no operand copies, 2 no epilogue stores, 4 no MMAs
   // epilogue (forward / delta): out[j * out_ps + outoff[r] + n] for r < Rvalid, n < nvalid
   int Rvalid, nvalid;
@@ -98,6 +108,16 @@ struct GParams {
 };
 
 constexpr int kEpiConvFwd = 0, kEpiConvDx = 1, kEpiConvDw = 2;
+#ifndef DASMC_CONV_BASEOFF
+#define DASMC_CONV_BASEOFF 1  // descriptor base-offset field for slab starts off the 1024-B swizzle atom
+#endif
+// K-major SW128 descriptor of a matrix starting at any 128-B row of a swizzled slab
+__device__ __forceinline__ uint64_t smem_desc_row(uint32_t addr) {
+  const uint64_t a = (addr >> 4) & 0x3FFFULL;
+  uint64_t d = a | (1ULL << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ULL << 46) | (2ULL << 61);
+  if (DASMC_CONV_BASEOFF) d |= (uint64_t)((addr >> 7) & 7) << 49;
+  return d;
+}
 
 // byte offset of element (row, k) of a 128B-swizzled K-major tile (8-row atoms of 1024 B)
 __device__ __forceinline__ uint32_t swz(int row, int k) {
@@ -222,23 +242,25 @@ __device__ __forceinline__ void cwait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
-template <int EPI, int ACT, bool AV>
+template <int EPI, int ACT, bool AV, bool DIRECT>
 __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(const __grid_constant__ GParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t a_bytes = kCBM * 128, b_bytes = (uint32_t)p.nmma * 128;
-  const uint32_t stage_bytes = (uint32_t)p.nsub * (a_bytes + b_bytes);  // [A atoms][B atoms]
+  const uint32_t slab_bytes = DIRECT ? (uint32_t)p.slab_rows * 128 : 0u;
+  const uint32_t stage_bytes = DIRECT ? slab_bytes + (uint32_t)(p.kk * p.kk) * b_bytes  // [slab][k*k B atoms]
+                                      : (uint32_t)p.nsub * (a_bytes + b_bytes);       // [A atoms][B atoms]
   uint64_t* full = (uint64_t*)(smem + (size_t)p.stages * stage_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = (uint32_t*)(tempty + 2);
-  const int units = p.rtiles * p.J;
+  const int units = DIRECT ? p.J * p.mimg * p.ybl : p.rtiles * p.J;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(&full[s], 32 * kProdWarps);  // one cp.async arrival per producer thread
+      mbar_init(&full[s], DIRECT ? 1 : 32 * kProdWarps);  // TMA expect_tx / one cp.async arrival per producer
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -258,7 +280,33 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  if (warp < kProdWarps) {
+  if (DIRECT && warp < kProdWarps) {
+    // ===================== TMA producer (direct convolution) =====================
+    if (warp == 0 && lane == 0) {
+      prefetch_map(&p.mapA);
+      prefetch_map(&p.mapB);
+      const uint32_t tx = (uint32_t)(p.bh + p.kk - 1) * p.win_w * 128 + (uint32_t)(p.kk * p.kk) * b_bytes;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < units; t += gridDim.x) {
+        const int yb = t % p.ybl, m = (t / p.ybl) % p.mimg, j = t / (p.ybl * p.mimg);
+        for (int cb = 0; cb < p.cbn; ++cb) {
+          cwait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + (size_t)s * stage_bytes;
+          mbar_expect_tx(&full[s], tx);
+          tma_4d(st, &p.mapA, &full[s], cb * kCBK, 0, yb * p.bh, j * p.imgs_pp + m);
+          for (int a = 0; a < p.kk * p.kk; ++a) {
+            const int src = p.flipB ? p.kk * p.kk - 1 - a : a;  // delta: W'[ky'][kx'] = W[k-1-ky'][k-1-kx']
+            tma_3d(st + slab_bytes + a * b_bytes, &p.mapB, &full[s], (src * p.cbn + cb) * kCBK, 0, j);
+          }
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp < kProdWarps) {
     // ===================== gather producers =====================
     // Offsets are loaded one step ahead (next k-block's columns, next tile's rows) so the
     // table lookups overlap the copies instead of stalling every k-block on an L2 round trip;
@@ -341,6 +389,30 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
         cwait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * p.tcols_half);
+        if (DIRECT) {
+          for (int cb = 0; cb < p.cbn; ++cb) {
+            cwait(&full[s], ph);
+            tc_fence_after();
+            const uint32_t st = smem_u32(smem + (size_t)s * stage_bytes);
+            if (!(p.dbg & 4))
+              for (int a = 0; a < p.kk * p.kk; ++a) {
+                const int ky = a / p.kk, kx = a - ky * p.kk;
+                const uint64_t ad = smem_desc_row(st + (uint32_t)(ky * p.win_w + kx) * 128);
+                const uint64_t bd = smem_desc_row(st + slab_bytes + (uint32_t)a * b_bytes);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) tc_mma<0>(d, ad + 2 * k, bd + 2 * k, idesc, (cb | a | k) != 0);
+              }
+            tc_commit(&empty[s]);
+            if (++s == p.stages) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+          tc_commit(&tfull[acc]);
+          acc ^= 1;
+          if (acc == 0) aph ^= 1;
+          continue;
+        }
         for (int kb = 0; kb < p.nkb; ++kb) {
           cwait(&full[s], ph);
           // the stage was written through the generic proxy (cp.async); order it before the
@@ -372,11 +444,22 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
     int acc = 0;
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < units; t += gridDim.x) {
-      const int rt = t % p.rtiles, j = t / p.rtiles;
+      int j, r;
+      bool rv = true;  // the row is an output of this tile
+      if (DIRECT) {    // slab row -> output pixel (y, x) of image m; wide rows (x >= out_w) are dropped
+        const int yb = t % p.ybl, m = (t / p.ybl) % p.mimg;
+        j = t / (p.ybl * p.mimg);
+        const int yl = row_in_tile / p.win_w, x = row_in_tile - yl * p.win_w, y = yb * p.bh + yl;
+        rv = yl < p.bh && y < p.out_h && x < p.out_w;
+        r = (m * p.out_h + y) * p.out_w + x;
+      } else {
+        const int rt = t % p.rtiles;
+        j = t / p.rtiles;
+        r = rt * kCBM + row_in_tile;
+      }
       cwait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t)(acc * p.tcols_half) + ((uint32_t)(lg * 32) << 16);
-      const int r = rt * kCBM + row_in_tile;
       for (int ch = 0; ch < p.nmma / 16; ++ch) {
         float v[16];
         tmem_ld16(taddr + ch * 16, v);
@@ -385,7 +468,7 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
         if (nq <= 0) continue;
         if (p.dbg & 2) continue;
         if (EPI == kEpiConvFwd || EPI == kEpiConvDx) {
-          if (r >= p.Rvalid) continue;
+          if (!rv || r >= p.Rvalid) continue;
           float* dst = p.out + (int64_t)j * p.out_ps + (p.outoff ? (int64_t)p.outoff[r] : (int64_t)r * p.out_ld) + n0;
           if (EPI == kEpiConvFwd) {
             const float* b = p.theta + (int64_t)j * p.Dp + p.boff + n0;
@@ -535,8 +618,6 @@ __global__ void __launch_bounds__(256) pool_bwd_rows_kernel(ConvDev d, int act, 
   float* sb = S + j * s_ps + m * L.s_m;
   for (int py = 0; py < d.sh; ++py) {
     __syncthreads();  // the previous row pair's reads of pz are done
-    for (int i = threadIdx.x; i < 2 * d.wo * CP; i += blockDim.x) pz[i] = 0.f;
-    __syncthreads();
     const float* arow = aimg + (int64_t)(2 * py) * d.wo * C;
     for (int i = threadIdx.x; i < d.sw * C; i += blockDim.x) {  // (px, c), c fastest: coalesced NHWC reads
       const int c = i % C, px = i / C;
@@ -551,7 +632,12 @@ __global__ void __launch_bounds__(256) pool_bwd_rows_kernel(ConvDev d, int act, 
       const float gp = dP[j * dp_ps + m * per + (flat ? (int64_t)c * d.sh * d.sw + py * d.sw + px
                                                           : ((int64_t)py * d.sw + px) * C + c)];
       const float v = tf32_hi(gp * (act == DASMC_RELU ? (mx > 0.f ? 1.f : 0.f) : 1.f - mx * mx));
-      pz[((best >> 1) * d.wo + 2 * px + (best & 1)) * CP + c] = v;
+      // all four window positions (the three non-maxima get 0): no separate zeroing pass
+      float* w = pz + (2 * px) * CP + c;
+      w[0] = best == 0 ? v : 0.f;
+      w[CP] = best == 1 ? v : 0.f;
+      w[d.wo * CP] = best == 2 ? v : 0.f;
+      w[(d.wo + 1) * CP] = best == 3 ? v : 0.f;
     }
     __syncthreads();
     // NHWC zero-bordered rows: (dy, x, c) contiguous per row
@@ -681,6 +767,7 @@ struct ConvTcState {
   bool xcol0 = false;
   float* XcolT = nullptr;
   int64_t XcolT_rows = 0;
+  bool direct_ok = true;       // DASMC_CONV_DIRECT=0 forces the gather path (A/B, tests)
   int* c2o[kMaxConv] = {};     // input pixel of stage i -> its inT[i] offset (channel 0)
   int* dzo[kMaxConv] = {};     // output pixel of stage i -> its dZs[i] offset (channel 0, kx 0)
   // tables (device, int32)
@@ -830,35 +917,98 @@ void build_tables(Ctx& c, int64_t mc) {
   }
 }
 
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn conv_encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult r;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &r));
+    if (!q) throw CudaError{"cuTensorMapEncodeTiled unavailable"};
+    return (EncodeTiledFn)q;
+  }();
+  return fn;
+}
+// fp32 tensor, innermost dim first; strides in bytes for dims >= 1; 128B-swizzled boxes
+CUtensorMap conv_map(const float* base, int rank, const uint64_t* dims, const uint64_t* strides, const uint32_t* box) {
+  CUtensorMap m;
+  const uint32_t es[5] = {1, 1, 1, 1, 1};
+  const CUresult r = conv_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<float*>(base),
+                                      dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError{"cuTensorMapEncodeTiled (conv) failed (" + std::to_string((int)r) + ")"};
+  return m;
+}
+
+// Direct-convolution stage parameters (GParams::mapA ...) for an NHWC input [J][cap][H][W][C]
+// convolved with k x k weights into out_h x out_w outputs; false when the slab ring does not fit.
+bool setup_direct(GParams& p, const float* in, int64_t cap, int H, int W, int C, int k, int out_h, int out_w,
+                  int64_t mc, const float* wcopy, int Kp, int J, bool flip) {
+  if (C % kCBK != 0 || W > 128) return false;
+  p.kk = k;
+  p.cbn = C / kCBK;
+  p.flipB = flip ? 1 : 0;
+  p.win_w = W;
+  p.bh = std::max(1, kCBM / W);
+  p.ybl = (out_h + p.bh - 1) / p.bh;
+  p.out_h = out_h;
+  p.out_w = out_w;
+  const int rows = std::max((p.bh + k - 1) * W, (k - 1) * (W + 1) + kCBM);
+  p.slab_rows = (rows + 7) / 8 * 8;
+  p.imgs_pp = (int)cap;
+  p.mimg = (int)mc;
+  const size_t stage = (size_t)p.slab_rows * 128 + (size_t)k * k * p.nmma * 128;
+  if (2 * stage + 2048 > 227 * 1024) return false;
+  const uint64_t da[4] = {(uint64_t)C, (uint64_t)W, (uint64_t)H, (uint64_t)J * cap};
+  const uint64_t sa[3] = {(uint64_t)C * 4, (uint64_t)W * C * 4, (uint64_t)H * W * C * 4};
+  const uint32_t ba[4] = {(uint32_t)kCBK, (uint32_t)W, (uint32_t)(p.bh + k - 1), 1};
+  p.mapA = conv_map(in, 4, da, sa, ba);
+  const uint64_t db[3] = {(uint64_t)Kp, (uint64_t)p.nmma, (uint64_t)J};
+  const uint64_t sb[2] = {(uint64_t)Kp * 4, (uint64_t)p.nmma * Kp * 4};
+  const uint32_t bb[3] = {(uint32_t)kCBK, (uint32_t)p.nmma, 1};
+  p.mapB = conv_map(wcopy, 3, db, sb, bb);
+  return true;
+}
+
 template <int EPI>
-void launch_gemm(Ctx& c, GParams& p, int act) {
+void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
   if (p.nmma > 256) throw std::invalid_argument("conv: MMA N > 256");
-  if (!p.b.vec) throw std::invalid_argument("conv: B operands are 16-byte gathers");
-  // Atoms per stage: several 32-wide k atoms per pipeline hand-off (the producer -> MMA -> producer
-  // round trip costs hundreds of cycles; conv tiles have few k atoms, so one atom per stage was
-  // hand-off bound), a divisor of the atom count when one exists
-  const int natoms = p.nkb;  // callers pass the atom count
-  const size_t atom_bytes = (size_t)kCBM * 128 + (size_t)p.nmma * 128;
+  if (!p.b.vec && !direct) throw std::invalid_argument("conv: B operands are 16-byte gathers");
   const size_t fixed = 1024 + 64 * 8 + 64;
-  auto fits = [&](int ns) { return 2 * ns * atom_bytes + fixed <= 227 * 1024; };  // >= 2 stages
-  int nsub = 1;
-  for (int cand : {4, 3, 2})
-    if (natoms % cand == 0 && fits(cand)) {
-      nsub = cand;
-      break;
-    }
-  if (nsub == 1 && natoms > 8)
+  size_t stage_bytes;
+  int stages;
+  if (direct) {
+    p.nsub = 1;
+    stage_bytes = (size_t)p.slab_rows * 128 + (size_t)p.kk * p.kk * p.nmma * 128;
+    stages = (int)std::min<size_t>(4, (227 * 1024 - fixed) / stage_bytes);
+  } else {
+    // Atoms per stage: several 32-wide k atoms per pipeline hand-off (the producer -> MMA ->
+    // producer round trip costs hundreds of cycles; conv tiles have few k atoms), a divisor of
+    // the atom count when one exists
+    const int natoms = p.nkb;  // callers pass the atom count
+    const size_t atom_bytes = (size_t)kCBM * 128 + (size_t)p.nmma * 128;
+    auto fits = [&](int ns) { return 2 * ns * atom_bytes + fixed <= 227 * 1024; };  // >= 2 stages
+    int nsub = 1;
     for (int cand : {4, 3, 2})
-      if (fits(cand)) {  // padded last stage (zero-filled atoms)
+      if (natoms % cand == 0 && fits(cand)) {
         nsub = cand;
         break;
       }
-  p.nsub = nsub;
-  p.nkb = (natoms + nsub - 1) / nsub;
-  const size_t stage_bytes = (size_t)nsub * ((size_t)kCBM * 128 + (size_t)p.nmma * 128);
-  // two CTAs per SM when each gets >= 3 stages in ~110 KB, else one CTA with up to 6 stages
-  int stages = (int)std::min<size_t>(6, (110 * 1024 - fixed) / stage_bytes);
-  if (stages < 3) stages = (int)std::min<size_t>(6, (227 * 1024 - fixed) / stage_bytes);
+    if (nsub == 1 && natoms > 8)
+      for (int cand : {4, 3, 2})
+        if (fits(cand)) {  // padded last stage (zero-filled atoms)
+          nsub = cand;
+          break;
+        }
+    p.nsub = nsub;
+    p.nkb = (natoms + nsub - 1) / nsub;
+    stage_bytes = (size_t)nsub * atom_bytes;
+    // two CTAs per SM when each gets >= 3 stages in ~110 KB, else one CTA with up to 6 stages
+    stages = (int)std::min<size_t>(6, (110 * 1024 - fixed) / stage_bytes);
+    if (stages < 3) stages = (int)std::min<size_t>(6, (227 * 1024 - fixed) / stage_bytes);
+  }
   if (stages < 2) throw std::invalid_argument("conv: GEMM tile does not fit in shared memory");
   p.stages = stages;
   const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16;
@@ -870,11 +1020,11 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
     return e ? std::atoi(e) : 0;
   }();
   p.dbg = dbg;
-  const int units = p.rtiles * p.J;
-  auto go = [&](auto act_c, auto av_c) {
+  const int units = direct ? p.J * p.mimg * p.ybl : p.rtiles * p.J;
+  auto go = [&](auto act_c, auto dir_c) {
     constexpr int A_ = decltype(act_c)::value;
-    constexpr bool AV = decltype(av_c)::value;
-    auto kern = conv_tc_kernel<EPI, A_, AV>;
+    constexpr bool DI = decltype(dir_c)::value;
+    auto kern = conv_tc_kernel<EPI, A_, true, DI>;
     static bool attr[kMaxDevices] = {};  // one flag per instantiation and device
     const int dv = current_device();
     if (!attr[dv]) {
@@ -892,8 +1042,16 @@ void launch_gemm(Ctx& c, GParams& p, int act) {
     kern<<<grid, kCThreads, smem, c.stream>>>(p);
     LAUNCHED();
   };
-  if (!p.a.vec) throw std::invalid_argument("conv: A operands are 16-byte gathers");
-  auto go_av = [&](auto act_c) { go(act_c, std::true_type{}); };
+  if (!p.a.vec && !direct) throw std::invalid_argument("conv: A operands are 16-byte gathers");
+  auto go_av = [&](auto act_c) {
+    if constexpr (EPI != kEpiConvDw) {
+      if (direct) {
+        go(act_c, std::true_type{});
+        return;
+      }
+    }
+    go(act_c, std::false_type{});
+  };
   if (act == DASMC_RELU)
     go_av(std::integral_constant<int, DASMC_RELU>{});
   else
@@ -955,6 +1113,7 @@ void cnn_tc_init(Ctx& c) {
     CK(cudaMalloc(&s->Wf[i], sizeof(float) * (size_t)c.Jmax * s->nmmaF[i] * s->KpF[i]));
     if (i > 0) CK(cudaMalloc(&s->Wd[i], sizeof(float) * (size_t)c.Jmax * s->nmmaD[i] * s->KpD[i]));
   }
+  if (const char* e = std::getenv("DASMC_CONV_DIRECT")) s->direct_ok = e[0] != '0';
   const float ones[4] = {1.f, 1.f, 1.f, 1.f};
   CK(cudaMalloc(&s->ones, sizeof(ones)));
   CK(cudaMemcpy(s->ones, ones, sizeof(ones), cudaMemcpyHostToDevice));
@@ -1161,7 +1320,15 @@ void cnn_tc_forward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t m
         p.out2_k = 1;
       }
     }
-    launch_gemm<kEpiConvFwd>(c, p, net.act);
+    // direct convolution from TMA slabs when the input has 32-channel blocks (DASMC_CONV_DIRECT=0: gathers)
+    bool direct = false;
+    if (i > 0 && s->direct_ok) {
+      const ConvDev& dp = net.conv[i - 1];
+      direct = setup_direct(p, p.a.base, cap, d.hin, d.win, d.cin, d.k, d.ho, d.wo, mc, s->Wf[i], s->KpF[i], (int)J,
+                            false);
+      (void)dp;
+    }
+    launch_gemm<kEpiConvFwd>(c, p, net.act, direct);
     if (d.pool) {
       pool_fwd_nhwc_kernel<<<grid_of(J * mc * pool_plane(d)), 256, 0, c.stream>>>(
           d, c.cact[i], cap * act_plane(d), c.cpool[i], cap * pool_plane(d), mc, J, last ? 1 : 0,
@@ -1297,7 +1464,10 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
       p.out2_ks = s->dzl[i - 1].s_kx;
       p.out2_k = s->dzl[i - 1].kc;
     }
-    launch_gemm<kEpiConvDx>(c, p, net.act);
+    const int H2 = d.ho + 2 * (d.k - 1), W2 = d.wo + 2 * (d.k - 1);
+    const bool direct = s->direct_ok && setup_direct(p, c.cdel[i], cap, H2, W2, d.cout, d.k, d.hin, d.win, mc,
+                                                     s->Wd[i], s->KpD[i], (int)J, true);
+    launch_gemm<kEpiConvDx>(c, p, net.act, direct);
     if (dp.pool)
       launch_pool_bwd(c, dp, net.act, c.cact[i - 1], cap * act_plane(dp), s->dP[i - 1], cap * pool_plane(dp), 0,
                       c.cdel[i - 1], cap * pad_plane(dp), mc, J, s->dZs[i - 1], dzs_ps(i - 1), s->dzl[i - 1]);
