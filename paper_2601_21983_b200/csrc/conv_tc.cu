@@ -49,7 +49,13 @@ namespace {
 constexpr int kCBM = 128;              // UMMA M
 constexpr int kCBK = 32;               // tf32 elements per 128-byte swizzle row (one k-block)
 constexpr int kProdWarps = DASMC_CONV_PW;  // gather producers
-constexpr int kCThreads = 32 * (kProdWarps + 1 + 4);  // + MMA warp + 4 epilogue warps
+// warps per CTA: gather mode = kProdWarps producers + MMA warp + 4 epilogue warps; direct mode =
+// one TMA warp + MMA warp + 8 epilogue warps (two per TMEM lane group, splitting the columns:
+// the direct tiles are epilogue-heavy)
+template <bool DIRECT>
+struct ConvWarps {
+  static constexpr int P = DIRECT ? 1 : kProdWarps, E = DIRECT ? 8 : 4, T = 32 * (P + 1 + E);
+};
 constexpr int kOnesRow = -2147483647;  // row table entry: a row of ones (the bias row of dW)
 constexpr int kZeroRow = -2147483647 - 1;
 
@@ -109,7 +115,8 @@ struct GParams {
 
 constexpr int kEpiConvFwd = 0, kEpiConvDx = 1, kEpiConvDw = 2;
 #ifndef DASMC_CONV_BASEOFF
-#define DASMC_CONV_BASEOFF 1  // descriptor base-offset field for slab starts off the 1024-B swizzle atom
+#define DASMC_CONV_BASEOFF 0  // 1: set the descriptor base-offset field for slab starts off the 1024-B atom
+                              // (measured wrong on B200: the swizzle follows the absolute address)
 #endif
 // K-major SW128 descriptor of a matrix starting at any 128-B row of a swizzled slab
 __device__ __forceinline__ uint64_t smem_desc_row(uint32_t addr) {
@@ -243,7 +250,8 @@ __device__ __forceinline__ void cwait(uint64_t* bar, uint32_t parity) {
 }
 
 template <int EPI, int ACT, bool AV, bool DIRECT>
-__global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(const __grid_constant__ GParams p) {
+__global__ void __launch_bounds__(ConvWarps<DIRECT>::T, DASMC_CONV_MINB) conv_tc_kernel(const __grid_constant__ GParams p) {
+  constexpr int PW = ConvWarps<DIRECT>::P, EW = ConvWarps<DIRECT>::E;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -265,11 +273,11 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], EW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kProdWarps) {
+  if (warp == PW) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "r"(2 * p.tcols_half)
                  : "memory");
@@ -280,7 +288,7 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  if (DIRECT && warp < kProdWarps) {
+  if (DIRECT && warp < PW) {
     // ===================== TMA producer (direct convolution) =====================
     if (warp == 0 && lane == 0) {
       prefetch_map(&p.mapA);
@@ -306,7 +314,7 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
         }
       }
     }
-  } else if (warp < kProdWarps) {
+  } else if (warp < PW) {
     // ===================== gather producers =====================
     // Offsets are loaded one step ahead (next k-block's columns, next tile's rows) so the
     // table lookups overlap the copies instead of stalling every k-block on an L2 round trip;
@@ -379,7 +387,7 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
     }
     // drain: the CTA may not exit with copies in flight
     asm volatile("cp.async.wait_all;" ::: "memory");
-  } else if (warp == kProdWarps) {
+  } else if (warp == PW) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
       const uint32_t idesc = idesc_tf32(p.nmma, kCBM);
@@ -440,6 +448,9 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
   } else {
     // ===================== epilogue (4 warps, one TMEM lane group each) =====================
     const int lg = warp & 3;
+    const int part = (warp - PW - 1) >> 2;  // column half (direct mode: two warps per lane group)
+    const int nch = p.nmma / 16;
+    const int ch_lo = EW == 8 ? (part * nch) / 2 : 0, ch_hi = EW == 8 ? ((part + 1) * nch) / 2 : nch;
     const int row_in_tile = lg * 32 + lane;
     int acc = 0;
     uint32_t aph = 0;
@@ -460,7 +471,7 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
       cwait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t)(acc * p.tcols_half) + ((uint32_t)(lg * 32) << 16);
-      for (int ch = 0; ch < p.nmma / 16; ++ch) {
+      for (int ch = ch_lo; ch < ch_hi; ++ch) {
         float v[16];
         tmem_ld16(taddr + ch * 16, v);
         const int n0 = ch * 16;
@@ -534,7 +545,7 @@ __global__ void __launch_bounds__(kCThreads, DASMC_CONV_MINB) conv_tc_kernel(con
     }
   }
   __syncthreads();
-  if (warp == kProdWarps) {
+  if (warp == PW) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * p.tcols_half)
                  : "memory");
@@ -1035,11 +1046,12 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
     const int carve = (int)std::min<size_t>(100, (2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     int per_sm = 1;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCThreads, smem));
+    constexpr int NT = ConvWarps<DI>::T;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     per_sm = std::max(1, std::min(2, per_sm));
     if (2 * tc * per_sm > 512) per_sm = 1;  // TMEM: 512 columns per SM
     const int grid = std::max(1, std::min(units, c.ctc->num_sms * per_sm));
-    kern<<<grid, kCThreads, smem, c.stream>>>(p);
+    kern<<<grid, NT, smem, c.stream>>>(p);
     LAUNCHED();
   };
   if (!p.a.vec && !direct) throw std::invalid_argument("conv: A operands are 16-byte gathers");
