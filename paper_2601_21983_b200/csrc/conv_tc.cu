@@ -84,6 +84,10 @@ struct GParams {
   int kk, cbn, flipB;        // kernel size, 32-channel blocks, weight atoms in flipped (ky, kx) order
   int win_w, bh, ybl;        // slab width (pixels), output rows per tile, tiles per image
   int out_h, out_w, slab_rows, imgs_pp, mimg;
+  // weight gradient from TMA (DIRECT + kEpiConvDw): K = (image, q) over flattened channel-major planes
+  // of row stride win_p; A rows (ky, ci) are boxes of inT at q + ky * win_p, B rows (kx, co) boxes of
+  // the unshifted delta at q - kx (TMA zero fill supplies the out-of-plane positions)
+  int cin_rows, cout_rows, kpi, wpd, a_imgs_pp;
   int dbg;  // DASMC_CONV_DBG ablations (profiling only): 1 no operand copies, 2 no epilogue stores, 4 no MMAs
   // epilogue (forward / delta): out[j * out_ps + outoff[r] + n] for r < Rvalid, n < nvalid
   int Rvalid, nvalid;
@@ -256,15 +260,17 @@ __global__ void __launch_bounds__(ConvWarps<DIRECT>::T, DASMC_CONV_MINB) conv_tc
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t a_bytes = kCBM * 128, b_bytes = (uint32_t)p.nmma * 128;
-  const uint32_t slab_bytes = DIRECT ? (uint32_t)p.slab_rows * 128 : 0u;
-  const uint32_t stage_bytes = DIRECT ? slab_bytes + (uint32_t)(p.kk * p.kk) * b_bytes  // [slab][k*k B atoms]
-                                      : (uint32_t)p.nsub * (a_bytes + b_bytes);       // [A atoms][B atoms]
+  constexpr bool DWT = DIRECT && EPI == kEpiConvDw;  // weight gradient from TMA
+  const uint32_t slab_bytes = DIRECT && !DWT ? (uint32_t)p.slab_rows * 128 : 0u;
+  const uint32_t stage_bytes = DWT      ? a_bytes + b_bytes                                   // [A][B]
+                               : DIRECT ? slab_bytes + (uint32_t)(p.kk * p.kk) * b_bytes      // [slab][k*k B atoms]
+                                        : (uint32_t)p.nsub * (a_bytes + b_bytes);             // [A atoms][B atoms]
   uint64_t* full = (uint64_t*)(smem + (size_t)p.stages * stage_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = (uint32_t*)(tempty + 2);
-  const int units = DIRECT ? p.J * p.mimg * p.ybl : p.rtiles * p.J;
+  const int units = DIRECT && !DWT ? p.J * p.mimg * p.ybl : p.rtiles * p.J;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -288,7 +294,43 @@ __global__ void __launch_bounds__(ConvWarps<DIRECT>::T, DASMC_CONV_MINB) conv_tc
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  if (DIRECT && warp < PW) {
+  if (DWT && warp < PW) {
+    // ===================== TMA producer (weight gradient) =====================
+    if (warp == 0 && lane == 0) {
+      prefetch_map(&p.mapA);
+      prefetch_map(&p.mapB);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < units; t += gridDim.x) {
+        const int rt = t % p.rtiles, j = t / p.rtiles;
+        // this tile's ky blocks (cin_rows rows each); the ones row (bias) is stage memory, set below
+        const int ky0 = rt * kCBM / p.cin_rows, ky1 = min(p.kk, (rt + 1) * kCBM / p.cin_rows);
+        const uint32_t tx = (uint32_t)(ky1 - ky0) * p.cin_rows * 128 + (uint32_t)p.kk * p.cout_rows * 128;
+        const int one_row = p.kk * p.cin_rows - rt * kCBM < kCBM ? p.kk * p.cin_rows - rt * kCBM : -1;
+        for (int m = 0; m < p.mimg; ++m)
+          for (int kb = 0; kb < p.kpi; ++kb) {
+            cwait(&empty[s], ph ^ 1);
+            uint8_t* st = smem + (size_t)s * stage_bytes;
+            if (one_row >= 0) {  // the bias row of ones (all 32 values equal: swizzle-invariant)
+              float4* o = reinterpret_cast<float4*>(st + (one_row >> 3) * 1024 + (one_row & 7) * 128);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) o[u] = make_float4(1.f, 1.f, 1.f, 1.f);
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            mbar_expect_tx(&full[s], tx);
+            const int q0 = kb * kCBK;
+            for (int ky = ky0; ky < ky1; ++ky)
+              tma_3d(st + (ky - ky0) * p.cin_rows * 128, &p.mapA, &full[s], q0 + ky * p.wpd, 0, j * p.a_imgs_pp + m);
+            for (int kx = 0; kx < p.kk; ++kx)
+              tma_3d(st + a_bytes + kx * p.cout_rows * 128, &p.mapB, &full[s], q0 - kx, 0, j * p.imgs_pp + m);
+            if (++s == p.stages) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+      }
+    }
+  } else if (DIRECT && warp < PW) {
     // ===================== TMA producer (direct convolution) =====================
     if (warp == 0 && lane == 0) {
       prefetch_map(&p.mapA);
@@ -397,7 +439,7 @@ __global__ void __launch_bounds__(ConvWarps<DIRECT>::T, DASMC_CONV_MINB) conv_tc
         cwait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * p.tcols_half);
-        if (DIRECT) {
+        if (DIRECT && !DWT) {
           for (int cb = 0; cb < p.cbn; ++cb) {
             cwait(&full[s], ph);
             tc_fence_after();
@@ -457,7 +499,7 @@ __global__ void __launch_bounds__(ConvWarps<DIRECT>::T, DASMC_CONV_MINB) conv_tc
     for (int t = blockIdx.x; t < units; t += gridDim.x) {
       int j, r;
       bool rv = true;  // the row is an output of this tile
-      if (DIRECT) {    // slab row -> output pixel (y, x) of image m; wide rows (x >= out_w) are dropped
+      if (DIRECT && !DWT) {  // slab row -> output pixel (y, x) of image m; wide rows (x >= out_w) are dropped
         const int yb = t % p.ybl, m = (t / p.ybl) % p.mimg;
         j = t / (p.ybl * p.mimg);
         const int yl = row_in_tile / p.win_w, x = row_in_tile - yl * p.win_w, y = yb * p.bh + yl;
@@ -779,6 +821,7 @@ struct ConvTcState {
   float* XcolT = nullptr;
   int64_t XcolT_rows = 0;
   bool direct_ok = true;       // DASMC_CONV_DIRECT=0 forces the gather path (A/B, tests)
+  bool dwt[kMaxConv] = {};     // weight gradient from TMA (flattened, unshifted delta copy: DzL kc = 1)
   int* c2o[kMaxConv] = {};     // input pixel of stage i -> its inT[i] offset (channel 0)
   int* dzo[kMaxConv] = {};     // output pixel of stage i -> its dZs[i] offset (channel 0, kx 0)
   // tables (device, int32)
@@ -990,7 +1033,11 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
   const size_t fixed = 1024 + 64 * 8 + 64;
   size_t stage_bytes;
   int stages;
-  if (direct) {
+  if (direct && EPI == kEpiConvDw) {
+    p.nsub = 1;
+    stage_bytes = (size_t)kCBM * 128 + (size_t)p.nmma * 128;
+    stages = (int)std::min<size_t>(8, (227 * 1024 - fixed) / stage_bytes);
+  } else if (direct) {
     p.nsub = 1;
     stage_bytes = (size_t)p.slab_rows * 128 + (size_t)p.kk * p.kk * p.nmma * 128;
     stages = (int)std::min<size_t>(4, (227 * 1024 - fixed) / stage_bytes);
@@ -1031,7 +1078,7 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
     return e ? std::atoi(e) : 0;
   }();
   p.dbg = dbg;
-  const int units = direct ? p.J * p.mimg * p.ybl : p.rtiles * p.J;
+  const int units = direct && EPI != kEpiConvDw ? p.J * p.mimg * p.ybl : p.rtiles * p.J;
   auto go = [&](auto act_c, auto dir_c) {
     constexpr int A_ = decltype(act_c)::value;
     constexpr bool DI = decltype(dir_c)::value;
@@ -1056,13 +1103,10 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
   };
   if (!p.a.vec && !direct) throw std::invalid_argument("conv: A operands are 16-byte gathers");
   auto go_av = [&](auto act_c) {
-    if constexpr (EPI != kEpiConvDw) {
-      if (direct) {
-        go(act_c, std::true_type{});
-        return;
-      }
-    }
-    go(act_c, std::false_type{});
+    if (direct)
+      go(act_c, std::true_type{});
+    else
+      go(act_c, std::false_type{});
   };
   if (act == DASMC_RELU)
     go_av(std::integral_constant<int, DASMC_RELU>{});
@@ -1121,11 +1165,13 @@ void cnn_tc_init(Ctx& c) {
       s->xcol0 = true;
       s->nmmaW[0] = round_up(d.cout, 16);
     }
+    s->dwt[i] = !(i == 0 && s->xcol0) && kCBM % d.cin == 0 && d.k * d.cout <= 256 && d.k * d.cin < 8 * kCBM;
     s->winp[i] = round_up(d.win, 4);
     CK(cudaMalloc(&s->Wf[i], sizeof(float) * (size_t)c.Jmax * s->nmmaF[i] * s->KpF[i]));
     if (i > 0) CK(cudaMalloc(&s->Wd[i], sizeof(float) * (size_t)c.Jmax * s->nmmaD[i] * s->KpD[i]));
   }
   if (const char* e = std::getenv("DASMC_CONV_DIRECT")) s->direct_ok = e[0] != '0';
+  for (int i = 0; i < net.nconv; ++i) s->dwt[i] = s->dwt[i] && s->direct_ok;
   const float ones[4] = {1.f, 1.f, 1.f, 1.f};
   CK(cudaMalloc(&s->ones, sizeof(ones)));
   CK(cudaMemcpy(s->ones, ones, sizeof(ones), cudaMemcpyHostToDevice));
@@ -1232,7 +1278,13 @@ void cnn_tc_alloc(Ctx& c, int64_t mc) {
     if (d.pool && !last) CK(cudaMalloc(&s->dP[i], sizeof(float) * J * mc * pool_plane(d)));
     const size_t fa = (size_t)mc * d.cin * d.hin * wp * (i == 0 ? 1 : J);  // stage 0: shared by particles
     DzL& L = s->dzl[i];
-    if (i == 0 && s->xcol0) {  // unshifted, channel-major [c][m][y*wo + x]
+    if (s->dwt[i]) {  // unshifted, flattened channel-major planes of row stride win_p: [m][c][y * win_p + x]
+      L.kc = 1;
+      L.s_y = (int)wp;
+      L.s_c = (int64_t)d.ho * wp;
+      L.s_m = d.cout * L.s_c;
+      L.s_kx = 0;
+    } else if (i == 0 && s->xcol0) {  // unshifted, channel-major [c][m][y*wo + x]
       L.kc = 1;
       L.s_y = d.wo;
       L.s_m = (int64_t)d.ho * d.wo;
@@ -1245,7 +1297,7 @@ void cnn_tc_alloc(Ctx& c, int64_t mc) {
       L.s_m = d.cout * L.s_c;
       L.s_kx = mc * L.s_m;
     }
-    const size_t fb = J * (size_t)L.kc * (L.kc > 1 ? (size_t)L.s_kx : (size_t)d.cout * L.s_c);
+    const size_t fb = J * (L.kc > 1 ? (size_t)L.kc * L.s_kx : s->dwt[i] ? (size_t)mc * L.s_m : (size_t)d.cout * L.s_c);
     CK(cudaMalloc(&s->inT[i], sizeof(float) * fa));
     CK(cudaMemsetAsync(s->inT[i], 0, sizeof(float) * fa, c.stream));
     CK(cudaMalloc(&s->dZs[i], sizeof(float) * fb));
@@ -1365,7 +1417,7 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
   // per-particle floats of dZs[i]
   auto dzs_ps = [&](int i) {
     const DzL& Lz = s->dzl[i];
-    return Lz.kc > 1 ? (int64_t)Lz.kc * Lz.s_kx : (int64_t)net.conv[i].cout * Lz.s_c;
+    return Lz.kc > 1 ? (int64_t)Lz.kc * Lz.s_kx : s->dwt[i] ? cap * Lz.s_m : (int64_t)net.conv[i].cout * Lz.s_c;
   };
   {
     const ConvDev& d = net.conv[L];
@@ -1388,6 +1440,45 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
       const bool xc = i == 0 && s->xcol0;
       const int64_t planeA = (int64_t)d.cin * d.hin * wp;
       GParams p{};
+      if (s->dwt[i]) {  // TMA operands: inT rows (ky, ci) at q + ky * win_p, unshifted delta rows (kx, co) at q - kx
+        if (i == 0) {
+          to_chw_pad_kernel<<<grid_of(mc * planeA), 256, 0, c.stream>>>(s->Xr + m0 * img, 0, 0, d.cin, d.hin, d.win,
+                                                                       wp, s->inT[0], 0, mc, 1);
+          LAUNCHED();
+        }
+        const uint64_t imgsA = i == 0 ? (uint64_t)cap : (uint64_t)J * cap;
+        const uint64_t da[3] = {(uint64_t)d.hin * wp, (uint64_t)d.cin, imgsA};
+        const uint64_t sa[2] = {(uint64_t)d.hin * wp * 4, (uint64_t)planeA * 4};
+        const uint32_t ba[3] = {(uint32_t)kCBK, (uint32_t)d.cin, 1};
+        p.mapA = conv_map(s->inT[i], 3, da, sa, ba);
+        const uint64_t db[3] = {(uint64_t)d.ho * wp, (uint64_t)d.cout, (uint64_t)J * cap};
+        const uint64_t sb[2] = {(uint64_t)d.ho * wp * 4, (uint64_t)d.cout * d.ho * wp * 4};
+        const uint32_t bb[3] = {(uint32_t)kCBK, (uint32_t)d.cout, 1};
+        p.mapB = conv_map(s->dZs[i], 3, db, sb, bb);
+        p.kk = d.k;
+        p.cin_rows = d.cin;
+        p.cout_rows = d.cout;
+        p.wpd = wp;
+        p.kpi = (int)((d.ho * wp + kCBK - 1) / kCBK);
+        p.mimg = (int)mc;
+        p.imgs_pp = (int)cap;
+        p.a_imgs_pp = i == 0 ? 0 : (int)cap;
+        p.J = (int)J;
+        p.rtiles = (d.k * d.cin + 1 + kCBM - 1) / kCBM;
+        p.nkb = (int)mc * p.kpi;
+        p.nmma = s->nmmaW[i];
+        p.nvalid = d.k * d.cout;
+        p.Dp = net.Dp;
+        p.boff = d.boff;
+        p.e = e;
+        p.woff = d.woff;
+        p.nrows_w = d.k * d.cin + 1;
+        p.prow = s->prow[i];
+        p.pcol = s->pcol[i];
+        p.bcol = s->bcol[i];
+        p.ones = s->ones;
+        launch_gemm<kEpiConvDw>(c, p, net.act, true);
+      } else {
       if (xc) {
         const int64_t npix = (int64_t)d.ho * d.wo;
         p.a.base = s->XcolT + m0 * npix;
@@ -1431,6 +1522,7 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
       p.pcol = s->pcol[i];
       p.bcol = s->bcol[i];
       launch_gemm<kEpiConvDw>(c, p, net.act);
+      }
     }
     if (i == 0) break;
     // ---- delta of the stage input: dI[r_in, ci] = sum_(ky,kx,co) dZpad[.] W[co, ci, ky, kx]
