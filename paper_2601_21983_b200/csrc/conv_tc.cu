@@ -1171,7 +1171,11 @@ void cnn_tc_init(Ctx& c) {
     if (i > 0) CK(cudaMalloc(&s->Wd[i], sizeof(float) * (size_t)c.Jmax * s->nmmaD[i] * s->KpD[i]));
   }
   if (const char* e = std::getenv("DASMC_CONV_DIRECT")) s->direct_ok = e[0] != '0';
-  for (int i = 0; i < net.nconv; ++i) s->dwt[i] = s->dwt[i] && s->direct_ok;
+  // weight gradient from TMA: experimental, off unless DASMC_CONV_DWT=1 (faults on B200 in the
+  // C3 stage-1 shape; the gather form is the default)
+  const char* dwt_env = std::getenv("DASMC_CONV_DWT");
+  const bool dwt_on = dwt_env && dwt_env[0] == '1';
+  for (int i = 0; i < net.nconv; ++i) s->dwt[i] = s->dwt[i] && s->direct_ok && dwt_on;
   const float ones[4] = {1.f, 1.f, 1.f, 1.f};
   CK(cudaMalloc(&s->ones, sizeof(ones)));
   CK(cudaMemcpy(s->ones, ones, sizeof(ones), cudaMemcpyHostToDevice));
