@@ -311,18 +311,21 @@ __global__ void __launch_bounds__(ConvWarps<DIRECT>::T, DASMC_CONV_MINB) conv_tc
           for (int kb = 0; kb < p.kpi; ++kb) {
             cwait(&empty[s], ph ^ 1);
             uint8_t* st = smem + (size_t)s * stage_bytes;
-            if (one_row >= 0) {  // the bias row of ones (all 32 values equal: swizzle-invariant)
+            if (one_row >= 0 && !(p.dbg & 32)) {  // the bias row of ones (all 32 values equal: swizzle-invariant)
               float4* o = reinterpret_cast<float4*>(st + (one_row >> 3) * 1024 + (one_row & 7) * 128);
 #pragma unroll
               for (int u = 0; u < 8; ++u) o[u] = make_float4(1.f, 1.f, 1.f, 1.f);
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             }
-            mbar_expect_tx(&full[s], tx);
+            const uint32_t txa = (uint32_t)(ky1 - ky0) * p.cin_rows * 128, txb = tx - txa;
+            mbar_expect_tx(&full[s], ((p.dbg & 8) ? 0u : txa) + ((p.dbg & 16) ? 0u : txb));
             const int q0 = kb * kCBK;
+            if (!(p.dbg & 8))
             for (int ky = ky0; ky < ky1; ++ky)
               tma_3d(st + (ky - ky0) * p.cin_rows * 128, &p.mapA, &full[s], q0 + ky * p.wpd, 0, j * p.a_imgs_pp + m);
+            if (!(p.dbg & 16))
             for (int kx = 0; kx < p.kk; ++kx)
-              tma_3d(st + a_bytes + kx * p.cout_rows * 128, &p.mapB, &full[s], q0 - kx, 0, j * p.imgs_pp + m);
+              tma_3d(st + a_bytes + kx * p.cout_rows * 128, &p.mapB, &full[s], (p.dbg & 64) ? q0 : (p.dbg & 128) ? q0 + 4 - kx : q0 - kx, 0, j * p.imgs_pp + m);
             if (++s == p.stages) {
               s = 0;
               ph ^= 1;
@@ -544,7 +547,8 @@ __global__ void __launch_bounds__(ConvWarps<DIRECT>::T, DASMC_CONV_MINB) conv_tc
 #pragma unroll
             for (int q = 0; q < 16; ++q) v[q] = tf32_hi(v[q]);
           }
-          if (nq == 16 && (((uintptr_t)dst) & 15) == 0) {
+          if (!p.out) {  // delta into stage 0: only the channel-major copy below is read
+          } else if (nq == 16 && (((uintptr_t)dst) & 15) == 0) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
               reinterpret_cast<float4*>(dst)[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
@@ -622,9 +626,12 @@ __global__ void conv_wcopy_kernel(const float* __restrict__ theta, int64_t Dp, i
 
 // 2x2/2 max-pool forward of an NHWC stage output; flat != 0 writes the flatten order (c, y, x)
 // of the head input instead of NHWC.
+// code[j][m][py][px][c] (one byte per pooled element) = position 0..3 of the window's first maximum in
+// (dy, dx) order, bit 2 = max > 0: the max-pool backward routes through it and (ReLU) never re-reads
+// the pre-pool plane.
 __global__ void pool_fwd_nhwc_kernel(ConvDev d, const float* __restrict__ A, int64_t a_ps, float* __restrict__ P,
                                      int64_t p_ps, int64_t M, int64_t J, int flat, float* __restrict__ T, int64_t t_ps,
-                                     int t_wp) {
+                                     int t_wp, uint8_t* __restrict__ code) {
   const int C = d.cout;
   const int64_t per = (int64_t)d.sh * d.sw * C, total = J * M * per;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
@@ -633,8 +640,14 @@ __global__ void pool_fwd_nhwc_kernel(ConvDev d, const float* __restrict__ A, int
     const int c = o % C, pyx = o / C, py = pyx / d.sw, px = pyx - py * d.sw;
     const float* a = A + j * a_ps + m * (int64_t)d.ho * d.wo * C + ((int64_t)(2 * py) * d.wo + 2 * px) * C + c;
     const int64_t rowC = (int64_t)d.wo * C;
-    const float v = fmaxf(fmaxf(a[0], a[C]), fmaxf(a[rowC], a[rowC + C]));
+    const float a0 = a[0], a1 = a[C], a2 = a[rowC], a3 = a[rowC + C];
+    int best = 0;
+    float v = a0;
+    if (a1 > v) { v = a1; best = 1; }
+    if (a2 > v) { v = a2; best = 2; }
+    if (a3 > v) { v = a3; best = 3; }
     P[j * p_ps + m * per + (flat ? (int64_t)c * d.sh * d.sw + pyx : o)] = v;
+    if (code) code[(j * M + m) * per + o] = (uint8_t)(best | (v > 0.f ? 4 : 0));  // bit 2: relu'(max)
     // the next stage's channel-major, width-padded input copy (its weight-gradient operand)
     if (T) T[j * t_ps + m * (int64_t)C * d.sh * t_wp + ((int64_t)c * d.sh + py) * t_wp + px] = v;
   }
@@ -656,8 +669,12 @@ struct DzL {
   int64_t s_kx, s_m, s_c;
 };
 
+// code = pool_fwd_nhwc_kernel's argmax codes (ReLU: act' from the code; tanh: the maximum is read back from
+// the pre-pool plane A at the coded position); dZ == nullptr (stage 0: no delta GEMM reads it) skips the
+// NHWC output.
 __global__ void __launch_bounds__(256) pool_bwd_rows_kernel(ConvDev d, int act, const float* __restrict__ A,
-                                                            int64_t a_ps, const float* __restrict__ dP, int64_t dp_ps,
+                                                            int64_t a_ps, const uint8_t* __restrict__ code,
+                                                            const float* __restrict__ dP, int64_t dp_ps,
                                                             int flat, float* __restrict__ dZ, int64_t dz_ps, int64_t M,
                                                             float* __restrict__ S, int64_t s_ps, DzL L) {
   extern __shared__ float pz[];  // [2][wo][C + 1]: the window deltas of two pre-pool rows
@@ -666,25 +683,26 @@ __global__ void __launch_bounds__(256) pool_bwd_rows_kernel(ConvDev d, int act, 
   const int64_t m = img % M, j = img / M;
   const int wo2 = 2 * d.sw;  // pre-pool columns covered by windows
   const int64_t per = (int64_t)d.sh * d.sw * C;
+  const uint8_t* cimg = code + (j * M + m) * per;
   const float* aimg = A + j * a_ps + m * (int64_t)d.ho * d.wo * C;
-  float* z = dZ + j * dz_ps + m * (int64_t)H2 * W2 * C;
+  float* z = dZ ? dZ + j * dz_ps + m * (int64_t)H2 * W2 * C : nullptr;
   float* sb = S + j * s_ps + m * L.s_m;
   for (int py = 0; py < d.sh; ++py) {
     __syncthreads();  // the previous row pair's reads of pz are done
-    const float* arow = aimg + (int64_t)(2 * py) * d.wo * C;
     for (int i = threadIdx.x; i < d.sw * C; i += blockDim.x) {  // (px, c), c fastest: coalesced NHWC reads
       const int c = i % C, px = i / C;
-      const float* a = arow + (int64_t)(2 * px) * C + c;
-      const int64_t rowC = (int64_t)d.wo * C;
-      const float a0 = a[0], a1 = a[C], a2 = a[rowC], a3 = a[rowC + C];
-      int best = 0;
-      float mx = a0;
-      if (a1 > mx) { mx = a1; best = 1; }
-      if (a2 > mx) { mx = a2; best = 2; }
-      if (a3 > mx) { mx = a3; best = 3; }
-      const float gp = dP[j * dp_ps + m * per + (flat ? (int64_t)c * d.sh * d.sw + py * d.sw + px
-                                                          : ((int64_t)py * d.sw + px) * C + c)];
-      const float v = tf32_hi(gp * (act == DASMC_RELU ? (mx > 0.f ? 1.f : 0.f) : 1.f - mx * mx));
+      const int64_t o = ((int64_t)py * d.sw + px) * C + c;
+      const int64_t po = flat ? (int64_t)c * d.sh * d.sw + py * d.sw + px : o;  // pooled-output layout
+      const int cd = cimg[o], best = cd & 3;
+      const float gp = dP[j * dp_ps + m * per + po];
+      float dact;
+      if (act == DASMC_RELU) {
+        dact = (cd & 4) ? 1.f : 0.f;
+      } else {
+        const float mx = aimg[((int64_t)(2 * py + (best >> 1)) * d.wo + 2 * px + (best & 1)) * C + c];
+        dact = 1.f - mx * mx;
+      }
+      const float v = tf32_hi(gp * dact);
       // all four window positions (the three non-maxima get 0): no separate zeroing pass
       float* w = pz + (2 * px) * CP + c;
       w[0] = best == 0 ? v : 0.f;
@@ -694,6 +712,7 @@ __global__ void __launch_bounds__(256) pool_bwd_rows_kernel(ConvDev d, int act, 
     }
     __syncthreads();
     // NHWC zero-bordered rows: (dy, x, c) contiguous per row
+    if (z)
     for (int i = threadIdx.x; i < 2 * wo2 * C; i += blockDim.x) {
       const int c = i % C, xy = i / C, x = xy % wo2, dy = xy / wo2;
       z[((int64_t)(2 * py + dy + pad) * W2 + x + pad) * C + c] = pz[(dy * d.wo + x) * CP + c];
@@ -706,8 +725,9 @@ __global__ void __launch_bounds__(256) pool_bwd_rows_kernel(ConvDev d, int act, 
   }
 }
 
-void launch_pool_bwd(Ctx& c, const ConvDev& d, int act, const float* A, int64_t a_ps, const float* dP, int64_t dp_ps,
-                     int flat, float* dZ, int64_t dz_ps, int64_t M, int64_t J, float* S, int64_t s_ps, const DzL& L) {
+void launch_pool_bwd(Ctx& c, const ConvDev& d, int act, const float* A, int64_t a_ps, const uint8_t* code,
+                     const float* dP, int64_t dp_ps, int flat, float* dZ, int64_t dz_ps, int64_t M, int64_t J, float* S,
+                     int64_t s_ps, const DzL& L) {
   const size_t sm = sizeof(float) * 2 * (size_t)d.wo * (d.cout + 1);
   if (sm > 48 * 1024) {
     static bool attr[kMaxDevices] = {};
@@ -717,8 +737,8 @@ void launch_pool_bwd(Ctx& c, const ConvDev& d, int act, const float* A, int64_t 
       attr[dv] = true;
     }
   }
-  pool_bwd_rows_kernel<<<(unsigned)(J * M), 256, sm, c.stream>>>(d, act, A, a_ps, dP, dp_ps, flat, dZ, dz_ps, M, S,
-                                                                 s_ps, L);
+  pool_bwd_rows_kernel<<<(unsigned)(J * M), 256, sm, c.stream>>>(d, act, A, a_ps, code, dP, dp_ps, flat, dZ, dz_ps, M,
+                                                                 S, s_ps, L);
   LAUNCHED();
 }
 
@@ -741,7 +761,7 @@ __global__ void flat_to_dzpad_kernel(ConvDev d, const float* __restrict__ F, int
     const int64_t j = g / (M * per), rem = g - j * M * per, m = rem / per;
     const int o = (int)(rem - m * per), c = o % C, yx = o / C, y = yx / d.wo, x = yx - y * d.wo;
     const float v = tf32_hi(F[j * f_ps + m * per + (int64_t)c * d.ho * d.wo + yx]);
-    dZ[j * dz_ps + m * (int64_t)H2 * W2 * C + ((int64_t)(y + pad) * W2 + x + pad) * C + c] = v;
+    if (dZ) dZ[j * dz_ps + m * (int64_t)H2 * W2 * C + ((int64_t)(y + pad) * W2 + x + pad) * C + c] = v;
     float* s0 = S + j * s_ps + m * L.s_m + c * L.s_c + (int64_t)y * L.s_y + x;
     for (int kx = 0; kx < L.kc; ++kx, s0 += L.s_kx + 1) *s0 = v;
   }
@@ -809,6 +829,7 @@ struct ConvTcState {
   float* Wf[kMaxConv] = {};
   float* Wd[kMaxConv] = {};
   float* dP[kMaxConv] = {};    // delta of a pooled (non-last) stage output, NHWC
+  uint8_t* pcode[kMaxConv] = {};  // pooled stages: argmax code of every window, [Jmax][mcap][sh][sw][cout]
   // weight-gradient operands, written by the producers of the stage input / delta (epilogue
   // second outputs, pool kernels): zero-initialised, so padding columns stay zero
   float* inT[kMaxConv] = {};   // stage input [mcap][cin][hin][win_p] per particle (stage 0: shared X copy)
@@ -1233,6 +1254,7 @@ void cnn_tc_free(Ctx& c) {
     float* p[] = {s->Wf[i], s->Wd[i], s->dP[i], s->inT[i], s->dZs[i]};
     for (float* q : p)
       if (q) cudaFree(q);
+    if (s->pcode[i]) cudaFree(s->pcode[i]);
   }
   if (s->Xr) cudaFree(s->Xr);
   if (s->Xcol) cudaFree(s->Xcol);
@@ -1248,7 +1270,8 @@ int64_t cnn_tc_image_floats(const Ctx& c) {
   for (int i = 0; i < net.nconv; ++i) {
     const ConvDev& d = net.conv[i];
     const int64_t wp = round_up(d.win, 4);
-    f += act_plane(d) + pad_plane(d);               // output, zero-bordered delta
+    f += act_plane(d) + (i > 0 ? pad_plane(d) : 0);  // output, zero-bordered delta (stages > 0)
+    if (d.pool) f += (pool_plane(d) + 3) / 4;        // argmax codes (bytes)
     f += (int64_t)d.k * d.cout * d.ho * wp;          // kx-shifted deltas
     if (i > 0) f += (int64_t)d.cin * d.hin * wp;     // channel-major input copy
     if (d.pool) f += pool_plane(d);
@@ -1272,11 +1295,18 @@ void cnn_tc_alloc(Ctx& c, int64_t mc) {
         CK(cudaFree(*b));
         *b = nullptr;
       }
+    if (s->pcode[i]) {
+      CK(cudaFree(s->pcode[i]));
+      s->pcode[i] = nullptr;
+    }
     const ConvDev& d = net.conv[i];
     const size_t wp = (size_t)s->winp[i];
     CK(cudaMalloc(&c.cact[i], sizeof(float) * J * mc * act_plane(d)));
-    CK(cudaMalloc(&c.cdel[i], sizeof(float) * J * mc * pad_plane(d)));
-    CK(cudaMemsetAsync(c.cdel[i], 0, sizeof(float) * J * mc * pad_plane(d), c.stream));
+    if (i > 0) {  // stage 0 has no delta GEMM: its zero-bordered NHWC delta is never read, so never written
+      CK(cudaMalloc(&c.cdel[i], sizeof(float) * J * mc * pad_plane(d)));
+      CK(cudaMemsetAsync(c.cdel[i], 0, sizeof(float) * J * mc * pad_plane(d), c.stream));
+    }
+    if (d.pool) CK(cudaMalloc(&s->pcode[i], J * mc * pool_plane(d)));
     const bool last = i == net.nconv - 1;
     if (d.pool || last) CK(cudaMalloc(&c.cpool[i], sizeof(float) * J * mc * (d.pool ? pool_plane(d) : act_plane(d))));
     if (d.pool && !last) CK(cudaMalloc(&s->dP[i], sizeof(float) * J * mc * pool_plane(d)));
@@ -1400,7 +1430,7 @@ void cnn_tc_forward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t m
     if (d.pool) {
       pool_fwd_nhwc_kernel<<<grid_of(J * mc * pool_plane(d)), 256, 0, c.stream>>>(
           d, c.cact[i], cap * act_plane(d), c.cpool[i], cap * pool_plane(d), mc, J, last ? 1 : 0,
-          last ? nullptr : s->inT[i + 1], nxt_ps, last ? 0 : s->winp[i + 1]);
+          last ? nullptr : s->inT[i + 1], nxt_ps, last ? 0 : s->winp[i + 1], s->pcode[i]);
       LAUNCHED();
     } else if (last) {
       nhwc_to_flat_kernel<<<grid_of(J * mc * act_plane(d)), 256, 0, c.stream>>>(d, c.cact[i], cap * act_plane(d),
@@ -1426,8 +1456,8 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
   {
     const ConvDev& d = net.conv[L];
     if (d.pool) {
-      launch_pool_bwd(c, d, net.act, c.cact[L], cap * act_plane(d), c.cpool[L], cap * pool_plane(d), 1, c.cdel[L],
-                      cap * pad_plane(d), mc, J, s->dZs[L], dzs_ps(L), s->dzl[L]);
+      launch_pool_bwd(c, d, net.act, c.cact[L], cap * act_plane(d), s->pcode[L], c.cpool[L], cap * pool_plane(d), 1,
+                      L > 0 ? c.cdel[L] : nullptr, cap * pad_plane(d), mc, J, s->dZs[L], dzs_ps(L), s->dzl[L]);
     } else {
       flat_to_dzpad_kernel<<<grid_of(J * mc * act_plane(d)), 256, 0, c.stream>>>(
           d, c.cpool[L], cap * act_plane(d), c.cdel[L], cap * pad_plane(d), mc, J, s->dZs[L], dzs_ps(L), s->dzl[L]);
@@ -1558,7 +1588,7 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
       p.out_ps = cap * pool_plane(dp);
       p.out_ld = dp.cout;
     } else {  // pre-activation delta of stage i-1: act'(a_{i-1}), into its zero-bordered buffer
-      p.out = c.cdel[i - 1];
+      p.out = c.cdel[i - 1];  // nullptr for stage 0 (no delta GEMM reads it)
       p.out_ps = cap * pad_plane(dp);
       p.outoff = s->zpix[i - 1];
       p.mask = c.cact[i - 1];
@@ -1577,8 +1607,9 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
                                                      s->Wd[i], s->KpD[i], (int)J, true);
     launch_gemm<kEpiConvDx>(c, p, net.act, direct);
     if (dp.pool)
-      launch_pool_bwd(c, dp, net.act, c.cact[i - 1], cap * act_plane(dp), s->dP[i - 1], cap * pool_plane(dp), 0,
-                      c.cdel[i - 1], cap * pad_plane(dp), mc, J, s->dZs[i - 1], dzs_ps(i - 1), s->dzl[i - 1]);
+      launch_pool_bwd(c, dp, net.act, c.cact[i - 1], cap * act_plane(dp), s->pcode[i - 1], s->dP[i - 1],
+                      cap * pool_plane(dp), 0, i - 1 > 0 ? c.cdel[i - 1] : nullptr, cap * pad_plane(dp), mc, J,
+                      s->dZs[i - 1], dzs_ps(i - 1), s->dzl[i - 1]);
   }
 }
 

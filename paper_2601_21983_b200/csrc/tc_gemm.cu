@@ -121,6 +121,8 @@ struct TileParams {
   int J;
   int rg;      // row tiles per scheduling group
   int nkb;     // k blocks of BK
+  int klast;   // MMA k-steps (a quarter k block each) the last k block needs (0 = all 4): K tails skip the
+               // all-zero quarters
   int nmma;    // MMA N (multiple of 16, <= 256)
   int brows;   // TMA box rows of B (valid rows)
   int stages;
@@ -391,13 +393,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * 256);
-        for (int kb = 0; kb < tp.nkb; ++kb) {
+        // one k block: NKS MMA k-steps (32 bytes of K each) per operand part, straight-line code (the
+        // issuing thread's instruction count is on the critical path of the MMA-bound GEMMs)
+        auto kblock = [&](int kb, auto nks_c) {
+          constexpr int NKS = decltype(nks_c)::value;
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint64_t ad = smem_desc(A_of(s, 0)), bd = smem_desc(B_of(s, 0));
           const uint64_t adl = smem_desc(A_of(s, 1)), bdl = smem_desc(B_of(s, 1));
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {  // 32 bytes of K per instruction
+          for (int k = 0; k < NKS; ++k) {
             const uint64_t off = (uint64_t)(k * 32) >> 4;  // 32 bytes per K=8 step inside the swizzle row
             if (PAIR) {
               tc_mma2<KP>(d, ad + off, bd + off, idesc, (kb | k) != 0);
@@ -417,6 +422,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             s = 0;
             ph ^= 1;
           }
+        };
+        for (int kb = 0; kb < tp.nkb - 1; ++kb) kblock(kb, std::integral_constant<int, 4>{});
+        // the last k block: a K tail skips its all-zero quarters (tp.klast k-steps)
+        switch (tp.klast) {
+          case 1: kblock(tp.nkb - 1, std::integral_constant<int, 1>{}); break;
+          case 2: kblock(tp.nkb - 1, std::integral_constant<int, 2>{}); break;
+          case 3: kblock(tp.nkb - 1, std::integral_constant<int, 3>{}); break;
+          default: kblock(tp.nkb - 1, std::integral_constant<int, 4>{}); break;
         }
         if (PAIR)
           tc_commit2(&tfull[acc], pair_mask);
@@ -523,7 +536,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         // 16-column TMEM loads, except in the fp16 mode whose (epilogue-bound) forward
         // runs 9 % faster with 8 (B200 in-process A/B; tf32 / tf32h 4 % slower with 8)
         constexpr int CW = DASMC_CW > 0 ? DASMC_CW : (PREC == 1 ? 8 : 16);
+        // whole 16-column chunks per part (C2: 64 / 64 / 72 of 200 columns); DASMC_V_EVENSPLIT: columns
+        // split evenly over the lane group's kParts warps (67 / 67 / 66)
+#ifdef DASMC_V_EVENSPLIT  // measured slower on B200 (26.1 vs 25.6 ms per C2 launch): unaligned tails
+        const int col_per = (n1 + kParts - 1) / kParts;
+        const int col_lo = min(n1, part * col_per), col_hi = min(n1, col_lo + col_per);
+        c_lo = 0;
+        c_hi = (col_hi - col_lo + CW - 1) / CW;
+#else
         chunk_range((n1 + CW - 1) / CW, c_lo, c_hi);
+        const int col_lo = 0, col_hi = n1;
+#endif
         if (dbg == 3) c_hi = c_lo;
         // transposed buffers are row-blocked [J][nblk][rows][128]: a tile's rows are one
         // contiguous region; consecutive rows of a block are 128 floats apart
@@ -576,8 +599,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto act = [](float z) { return ACT == DASMC_RELU ? fmaxf(z, 0.f) : tanhf(z); };
         // pass 1: a1 = act(z1); partial z2 = W2 a1 over this warp's columns
         auto chunk1 = [&](auto store, int ch, const float* v) {
-          const int o0 = ch * CW;
-          const int nq = min(CW, n1 - o0);  // warp-uniform
+          const int o0 = col_lo + ch * CW;
+          const int nq = min(CW, col_hi - o0);  // warp-uniform
           TS* pa = a1T + (int64_t)o0 * kRow;
           float* pal = SPLIT ? a1Tlo + (int64_t)o0 * kRow : nullptr;
           auto one = [&](int q, const float2* w) {
@@ -600,14 +623,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto run_chunks = [&](auto body) {
           float va[CW] = {}, vb[CW] = {};
           int ch = c_lo;
-          if (ch < c_hi) tmem_ldw_async<CW>(taddr + ch * CW, va);
+          const uint32_t tcol = taddr + (uint32_t)col_lo;
+          if (ch < c_hi) tmem_ldw_async<CW>(tcol + ch * CW, va);
           tmem_waitw<CW>(va);
           while (ch < c_hi) {
-            if (ch + 1 < c_hi) tmem_ldw_async<CW>(taddr + (ch + 1) * CW, vb);
+            if (ch + 1 < c_hi) tmem_ldw_async<CW>(tcol + (ch + 1) * CW, vb);
             body(ch, va);
             tmem_waitw<CW>(vb);
             if (++ch >= c_hi) break;
-            if (ch + 1 < c_hi) tmem_ldw_async<CW>(taddr + (ch + 1) * CW, va);
+            if (ch + 1 < c_hi) tmem_ldw_async<CW>(tcol + (ch + 1) * CW, va);
             body(ch, vb);
             tmem_waitw<CW>(va);
             ++ch;
@@ -695,8 +719,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int c = 0; c < CP / 2; ++c) d2p[c] = make_float2(d2[2 * c], d2[2 * c + 1]);
           auto chunk2 = [&](int ch, const float* v) {
-            const int o0 = ch * CW;
-            const int nq = min(CW, n1 - o0);  // warp-uniform
+            const int o0 = col_lo + ch * CW;
+            const int nq = min(CW, col_hi - o0);  // warp-uniform
             TS* pd = d1T + (int64_t)o0 * kRow;
             float* pdl = SPLIT ? d1Tlo + (int64_t)o0 * kRow : nullptr;
             auto one = [&](int q, const float2* w) {
@@ -1624,7 +1648,11 @@ void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t 
     // cluster shape (see ClusterShape): CTA pairs stream half of W1's rows each (box
     // nmma / 2, rows >= n1 zero fill); QA = 2 multicasts X rows (box 64 rows per CTA),
     // QB = 2 multicasts W1 rows (two pieces of bbox rows, multiples of 8)
+#ifdef DASMC_V_F16X2_MC
+    const int cl = (s->split || (PREC != 0 && !s->f16x2)) ? std::min(s->cluster, 1) : s->cluster;
+#else
     const int cl = (s->split || PREC != 0) ? std::min(s->cluster, 1) : s->cluster;
+#endif
     const bool pair = cl > 0;
     const int QA = (cl == 2 || cl == 4) ? 2 : 1, QB = (cl == 3 || cl == 4) ? 2 : 1;
     const int half = round16(n1) / 2;
@@ -1647,6 +1675,8 @@ void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t 
     if (const char* e = std::getenv("DASMC_TC_HINTB")) tp.hint_b = std::atoi(e);        // tuning only
     if (const char* e = std::getenv("DASMC_TC_PREFETCH")) tp.prefetch = std::atoi(e);   // tuning only
     tp.nkb = (n0 + 1 + BKE - 1) / BKE;
+    tp.klast = (n0 + 1 - (tp.nkb - 1) * BKE + BKE / 4 - 1) / (BKE / 4);  // C2: 785 = 12 x 64 + 17 -> 2 of 4 k-steps
+    if (const char* e = std::getenv("DASMC_TC_KLAST")) tp.klast = std::atoi(e);         // tuning only
     tp.nmma = round16(n1);
     tp.brows = n1;
     FwdParams fp{};
@@ -1682,6 +1712,15 @@ void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t 
       constexpr int K = decltype(cp)::value, A_ = decltype(act)::value;
       if constexpr (PREC == 1) {
         if (s->f16x2) {
+#ifdef DASMC_V_F16X2_MC  // multicast cluster shapes for the f16x2 forward (tuning builds)
+          if (cl == 3)
+            launch_tc<kEpiKindFwd, false, kAShared, K, A_, 3, 3>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+          else if (cl == 4)
+            launch_tc<kEpiKindFwd, false, kAShared, K, A_, 4, 3>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+          else if (cl == 2)
+            launch_tc<kEpiKindFwd, false, kAShared, K, A_, 2, 3>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
+          else
+#endif
           if (pair)
             launch_tc<kEpiKindFwd, false, kAShared, K, A_, 1, 3>(c, A, Alo, B, Blo, tp, fp, dp, epi_bytes);
           else
