@@ -52,9 +52,14 @@ constexpr int kProdWarps = DASMC_CONV_PW;  // gather producers
 // warps per CTA: gather mode = kProdWarps producers + MMA warp + 4 epilogue warps; direct mode =
 // one TMA warp + MMA warp + 8 epilogue warps (two per TMEM lane group, splitting the columns:
 // the direct tiles are epilogue-heavy)
-template <bool DIRECT>
+// TMA weight gradient (direct + weights): one TMA warp + kShiftWarps shifter warps (they build the k
+// kx-shifted B tiles of a k block from one unshifted staging tile in shared memory) + MMA warp + 8
+// epilogue warps
+constexpr int kShiftWarps = 8;
+template <bool DIRECT, bool DWT = false>
 struct ConvWarps {
-  static constexpr int P = DIRECT ? 1 : kProdWarps, E = DIRECT ? 8 : 4, T = 32 * (P + 1 + E);
+  static constexpr int P = DWT ? 1 + kShiftWarps : DIRECT ? 1 : kProdWarps, E = DIRECT && !DWT ? 8 : 4,
+                       T = 32 * (P + 1 + E);
 };
 constexpr int kOnesRow = -2147483647;  // row table entry: a row of ones (the bias row of dW)
 constexpr int kZeroRow = -2147483647 - 1;
@@ -85,9 +90,12 @@ struct GParams {
   int win_w, bh, ybl;        // slab width (pixels), output rows per tile, tiles per image
   int out_h, out_w, slab_rows, imgs_pp, mimg;
   // weight gradient from TMA (DIRECT + kEpiConvDw): K = (image, q) over flattened channel-major planes
-  // of row stride win_p; A rows (ky, ci) are boxes of inT at q + ky * win_p, B rows (kx, co) boxes of
-  // the unshifted delta at q - kx (TMA zero fill supplies the out-of-plane positions)
-  int cin_rows, cout_rows, kpi, wpd, a_imgs_pp;
+  // of row stride win_p; A rows (ky, ci) are boxes of inT at q + ky * win_p (16-byte aligned: win_p is a
+  // multiple of 4).  B rows (kx, co) are the unshifted delta at q - kx: a TMA box must start 16-byte
+  // aligned, so one unswizzled staging tile [cout][halo + 32] starting at q - halo is loaded per k block
+  // (TMA zero fill supplies the out-of-plane positions) and shifter warps copy its k shifted windows
+  // into the swizzled B tile (shared memory to shared memory: no kx-shifted copies in HBM)
+  int cin_rows, cout_rows, kpi, wpd, a_imgs_pp, halo, stg_bytes;
   int dbg;  // DASMC_CONV_DBG ablations (profiling only): 1 no operand copies, 2 no epilogue stores, 4 no MMAs
   // epilogue (forward / delta): out[j * out_ps + outoff[r] + n] for r < Rvalid, n < nvalid
   int Rvalid, nvalid;
@@ -254,28 +262,33 @@ __device__ __forceinline__ void cwait(uint64_t* bar, uint32_t parity) {
 }
 
 template <int EPI, int ACT, bool AV, bool DIRECT>
-__global__ void __launch_bounds__(ConvWarps<DIRECT>::T, DASMC_CONV_MINB) conv_tc_kernel(const __grid_constant__ GParams p) {
-  constexpr int PW = ConvWarps<DIRECT>::P, EW = ConvWarps<DIRECT>::E;
+__global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DASMC_CONV_MINB)
+    conv_tc_kernel(const __grid_constant__ GParams p) {
+  using CW_ = ConvWarps<DIRECT, DIRECT && EPI == 2>;
+  constexpr int PW = CW_::P, EW = CW_::E;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t a_bytes = kCBM * 128, b_bytes = (uint32_t)p.nmma * 128;
   constexpr bool DWT = DIRECT && EPI == kEpiConvDw;  // weight gradient from TMA
   const uint32_t slab_bytes = DIRECT && !DWT ? (uint32_t)p.slab_rows * 128 : 0u;
-  const uint32_t stage_bytes = DWT      ? a_bytes + b_bytes                                   // [A][B]
+  const uint32_t stage_bytes = DWT      ? a_bytes + b_bytes + (uint32_t)p.stg_bytes           // [A][B][staging]
                                : DIRECT ? slab_bytes + (uint32_t)(p.kk * p.kk) * b_bytes      // [slab][k*k B atoms]
                                         : (uint32_t)p.nsub * (a_bytes + b_bytes);             // [A atoms][B atoms]
   uint64_t* full = (uint64_t*)(smem + (size_t)p.stages * stage_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = (uint32_t*)(tempty + 2);
+  uint64_t* sfull = tempty + 2;  // DWT: the staging tile of a stage has landed
+  uint32_t* tmem_holder = (uint32_t*)(sfull + p.stages);
   const int units = DIRECT && !DWT ? p.J * p.mimg * p.ybl : p.rtiles * p.J;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(&full[s], DIRECT ? 1 : 32 * kProdWarps);  // TMA expect_tx / one cp.async arrival per producer
+      // TMA expect_tx (+ one arrival per shifter warp) / one cp.async arrival per producer thread
+      mbar_init(&full[s], DWT ? 1 + kShiftWarps : DIRECT ? 1 : 32 * kProdWarps);
       mbar_init(&empty[s], 1);
+      mbar_init(&sfull[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -295,43 +308,81 @@ __global__ void __launch_bounds__(ConvWarps<DIRECT>::T, DASMC_CONV_MINB) conv_tc
   const uint32_t tmem_base = *tmem_holder;
 
   if (DWT && warp < PW) {
-    // ===================== TMA producer (weight gradient) =====================
-    if (warp == 0 && lane == 0) {
-      prefetch_map(&p.mapA);
-      prefetch_map(&p.mapB);
+    // ===================== TMA producer + shifter warps (weight gradient) =====================
+    if (warp == 0) {
+      if (lane == 0) {
+        prefetch_map(&p.mapA);
+        prefetch_map(&p.mapB);
+        int s = 0;
+        uint32_t ph = 0;
+        for (int t = blockIdx.x; t < units; t += gridDim.x) {
+          const int rt = t % p.rtiles, j = t / p.rtiles;
+          // this tile's ky blocks (cin_rows rows each); the ones row (bias) is stage memory, set below
+          const int ky0 = rt * kCBM / p.cin_rows, ky1 = min(p.kk, (rt + 1) * kCBM / p.cin_rows);
+          const uint32_t txa = (uint32_t)(ky1 - ky0) * p.cin_rows * 128;
+          const uint32_t txs = (uint32_t)p.cout_rows * (uint32_t)(p.halo + kCBK) * 4;
+          const int one_row = p.kk * p.cin_rows - rt * kCBM < kCBM ? p.kk * p.cin_rows - rt * kCBM : -1;
+          for (int m = 0; m < p.mimg; ++m)
+            for (int kb = 0; kb < p.kpi; ++kb) {
+              cwait(&empty[s], ph ^ 1);
+              uint8_t* st = smem + (size_t)s * stage_bytes;
+              if (one_row >= 0) {  // the bias row of ones (all 32 values equal: swizzle-invariant)
+                float4* o = reinterpret_cast<float4*>(st + (one_row >> 3) * 1024 + (one_row & 7) * 128);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) o[u] = make_float4(1.f, 1.f, 1.f, 1.f);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              }
+              const int q0 = kb * kCBK;
+              mbar_expect_tx(&sfull[s], txs);
+              tma_3d(st + a_bytes + b_bytes, &p.mapB, &sfull[s], q0 - p.halo, 0, j * p.imgs_pp + m);
+              mbar_expect_tx(&full[s], txa);
+              for (int ky = ky0; ky < ky1; ++ky)
+                tma_3d(st + (ky - ky0) * p.cin_rows * 128, &p.mapA, &full[s], q0 + ky * p.wpd, 0, j * p.a_imgs_pp + m);
+              if (++s == p.stages) {
+                s = 0;
+                ph ^= 1;
+              }
+            }
+        }
+      }
+    } else {
+      // shifter warp: B tile row (kx, co) = staging row co shifted by kx; one row per instruction pair
+      // (lane = k element: consecutive staging words, and a conflict-free swizzled row of the tile)
+      // Warp sw takes rows co = sw, sw + 8, ... of every kx block (cout is a multiple of 8, so those
+      // rows sit at the same position of consecutive 8-row swizzle atoms: 1024 bytes apart); four rows
+      // are in flight per step
+      const int sw = warp - 1;
+      const int ldst = p.halo + kCBK, nco = p.cout_rows / kShiftWarps;
       int s = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < units; t += gridDim.x) {
-        const int rt = t % p.rtiles, j = t / p.rtiles;
-        // this tile's ky blocks (cin_rows rows each); the ones row (bias) is stage memory, set below
-        const int ky0 = rt * kCBM / p.cin_rows, ky1 = min(p.kk, (rt + 1) * kCBM / p.cin_rows);
-        const uint32_t tx = (uint32_t)(ky1 - ky0) * p.cin_rows * 128 + (uint32_t)p.kk * p.cout_rows * 128;
-        const int one_row = p.kk * p.cin_rows - rt * kCBM < kCBM ? p.kk * p.cin_rows - rt * kCBM : -1;
-        for (int m = 0; m < p.mimg; ++m)
-          for (int kb = 0; kb < p.kpi; ++kb) {
-            cwait(&empty[s], ph ^ 1);
-            uint8_t* st = smem + (size_t)s * stage_bytes;
-            if (one_row >= 0 && !(p.dbg & 32)) {  // the bias row of ones (all 32 values equal: swizzle-invariant)
-              float4* o = reinterpret_cast<float4*>(st + (one_row >> 3) * 1024 + (one_row & 7) * 128);
+      for (int t = blockIdx.x; t < units; t += gridDim.x)
+        for (int mk = 0; mk < p.mimg * p.kpi; ++mk) {
+          cwait(&sfull[s], ph);
+          uint8_t* st = smem + (size_t)s * stage_bytes;
+          const float* stg = reinterpret_cast<const float*>(st + a_bytes + b_bytes) + sw * ldst + p.halo + lane;
+          const uint32_t tile = smem_u32(st + a_bytes);
+          for (int kx = 0; kx < p.kk; ++kx) {
+            const int r0 = kx * p.cout_rows + sw;
+            const uint32_t dst = tile + swz(r0, lane);
+            const float* src = stg - kx;
+            for (int u = 0; u < nco; u += 4) {
+              float v[4];
 #pragma unroll
-              for (int u = 0; u < 8; ++u) o[u] = make_float4(1.f, 1.f, 1.f, 1.f);
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            }
-            const uint32_t txa = (uint32_t)(ky1 - ky0) * p.cin_rows * 128, txb = tx - txa;
-            mbar_expect_tx(&full[s], ((p.dbg & 8) ? 0u : txa) + ((p.dbg & 16) ? 0u : txb));
-            const int q0 = kb * kCBK;
-            if (!(p.dbg & 8))
-            for (int ky = ky0; ky < ky1; ++ky)
-              tma_3d(st + (ky - ky0) * p.cin_rows * 128, &p.mapA, &full[s], q0 + ky * p.wpd, 0, j * p.a_imgs_pp + m);
-            if (!(p.dbg & 16))
-            for (int kx = 0; kx < p.kk; ++kx)
-              tma_3d(st + a_bytes + kx * p.cout_rows * 128, &p.mapB, &full[s], (p.dbg & 64) ? q0 : (p.dbg & 128) ? q0 + 4 - kx : q0 - kx, 0, j * p.imgs_pp + m);
-            if (++s == p.stages) {
-              s = 0;
-              ph ^= 1;
+              for (int w = 0; w < 4; ++w) v[w] = u + w < nco ? src[(u + w) * kShiftWarps * ldst] : 0.f;
+#pragma unroll
+              for (int w = 0; w < 4; ++w)
+                if (u + w < nco)
+                  asm volatile("st.shared.f32 [%0], %1;" ::"r"(dst + (uint32_t)(u + w) * 1024u), "f"(v[w]) : "memory");
             }
           }
-      }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(smem_u32(&full[s]));
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
     }
   } else if (DIRECT && warp < PW) {
     // ===================== TMA producer (direct convolution) =====================
@@ -1006,13 +1057,14 @@ EncodeTiledFn conv_encode_fn() {
   return fn;
 }
 // fp32 tensor, innermost dim first; strides in bytes for dims >= 1; 128B-swizzled boxes
-CUtensorMap conv_map(const float* base, int rank, const uint64_t* dims, const uint64_t* strides, const uint32_t* box) {
+CUtensorMap conv_map(const float* base, int rank, const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
+                     bool swizzle = true) {
   CUtensorMap m;
   const uint32_t es[5] = {1, 1, 1, 1, 1};
   const CUresult r = conv_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<float*>(base),
                                       dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                      swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError{"cuTensorMapEncodeTiled (conv) failed (" + std::to_string((int)r) + ")"};
   return m;
 }
@@ -1056,7 +1108,7 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
   int stages;
   if (direct && EPI == kEpiConvDw) {
     p.nsub = 1;
-    stage_bytes = (size_t)kCBM * 128 + (size_t)p.nmma * 128;
+    stage_bytes = (size_t)kCBM * 128 + (size_t)p.nmma * 128 + (size_t)p.stg_bytes;
     stages = (int)std::min<size_t>(8, (227 * 1024 - fixed) / stage_bytes);
   } else if (direct) {
     p.nsub = 1;
@@ -1090,7 +1142,7 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
   }
   if (stages < 2) throw std::invalid_argument("conv: GEMM tile does not fit in shared memory");
   p.stages = stages;
-  const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+  const size_t smem = 1024 + stages * stage_bytes + (3 * stages + 4) * 8 + 16;
   int tc = 32;
   while (tc < p.nmma) tc <<= 1;
   p.tcols_half = tc;
@@ -1114,7 +1166,7 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
     const int carve = (int)std::min<size_t>(100, (2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     int per_sm = 1;
-    constexpr int NT = ConvWarps<DI>::T;
+    constexpr int NT = ConvWarps<DI, DI && EPI == kEpiConvDw>::T;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     per_sm = std::max(1, std::min(2, per_sm));
     if (2 * tc * per_sm > 512) per_sm = 1;  // TMEM: 512 columns per SM
@@ -1186,16 +1238,17 @@ void cnn_tc_init(Ctx& c) {
       s->xcol0 = true;
       s->nmmaW[0] = round_up(d.cout, 16);
     }
-    s->dwt[i] = !(i == 0 && s->xcol0) && kCBM % d.cin == 0 && d.k * d.cout <= 256 && d.k * d.cin < 8 * kCBM;
+    s->dwt[i] = !(i == 0 && s->xcol0) && kCBM % d.cin == 0 && d.k * d.cout <= 256 && d.k * d.cin < 8 * kCBM &&
+                d.cout % 8 == 0;
     s->winp[i] = round_up(d.win, 4);
     CK(cudaMalloc(&s->Wf[i], sizeof(float) * (size_t)c.Jmax * s->nmmaF[i] * s->KpF[i]));
     if (i > 0) CK(cudaMalloc(&s->Wd[i], sizeof(float) * (size_t)c.Jmax * s->nmmaD[i] * s->KpD[i]));
   }
   if (const char* e = std::getenv("DASMC_CONV_DIRECT")) s->direct_ok = e[0] != '0';
-  // weight gradient from TMA: experimental, off unless DASMC_CONV_DWT=1 (faults on B200 in the
-  // C3 stage-1 shape; the gather form is the default)
+  // weight gradient from TMA + shared-memory shifts (DASMC_CONV_DWT=0: the gather form with k kx-shifted
+  // delta copies in HBM)
   const char* dwt_env = std::getenv("DASMC_CONV_DWT");
-  const bool dwt_on = dwt_env && dwt_env[0] == '1';
+  const bool dwt_on = !(dwt_env && dwt_env[0] == '0');
   for (int i = 0; i < net.nconv; ++i) s->dwt[i] = s->dwt[i] && s->direct_ok && dwt_on;
   const float ones[4] = {1.f, 1.f, 1.f, 1.f};
   CK(cudaMalloc(&s->ones, sizeof(ones)));
@@ -1485,10 +1538,13 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
         const uint64_t sa[2] = {(uint64_t)d.hin * wp * 4, (uint64_t)planeA * 4};
         const uint32_t ba[3] = {(uint32_t)kCBK, (uint32_t)d.cin, 1};
         p.mapA = conv_map(s->inT[i], 3, da, sa, ba);
+        // the unshifted delta: unswizzled staging boxes [cout][halo + 32] starting at q - halo
+        p.halo = round_up(d.k - 1, 4);
+        p.stg_bytes = round_up(d.cout * (p.halo + kCBK) * 4, 1024);
         const uint64_t db[3] = {(uint64_t)d.ho * wp, (uint64_t)d.cout, (uint64_t)J * cap};
         const uint64_t sb[2] = {(uint64_t)d.ho * wp * 4, (uint64_t)d.cout * d.ho * wp * 4};
-        const uint32_t bb[3] = {(uint32_t)kCBK, (uint32_t)d.cout, 1};
-        p.mapB = conv_map(s->dZs[i], 3, db, sb, bb);
+        const uint32_t bb[3] = {(uint32_t)(p.halo + kCBK), (uint32_t)d.cout, 1};
+        p.mapB = conv_map(s->dZs[i], 3, db, sb, bb, false);
         p.kk = d.k;
         p.cin_rows = d.cin;
         p.cout_rows = d.cout;
