@@ -43,6 +43,9 @@ namespace {
 #ifndef DASMC_CONV_PW
 #define DASMC_CONV_PW 8  // gather producer warps per CTA
 #endif
+#ifndef DASMC_CONV_GEW
+#define DASMC_CONV_GEW 4  // epilogue warps of the gather kernels (4 or 8)
+#endif
 #ifndef DASMC_CONV_MINB
 #define DASMC_CONV_MINB 1  // CTAs per SM the register budget is sized for
 #endif
@@ -58,8 +61,8 @@ constexpr int kProdWarps = DASMC_CONV_PW;  // gather producers
 constexpr int kShiftWarps = 8;
 template <bool DIRECT, bool DWT = false>
 struct ConvWarps {
-  static constexpr int P = DWT ? 1 + kShiftWarps : DIRECT ? 1 : kProdWarps, E = DIRECT && !DWT ? 8 : 4,
-                       T = 32 * (P + 1 + E);
+  static constexpr int P = DWT ? 1 + kShiftWarps : DIRECT ? 1 : kProdWarps,
+                       E = DIRECT && !DWT ? 8 : DIRECT ? 4 : DASMC_CONV_GEW, T = 32 * (P + 1 + E);
 };
 constexpr int kOnesRow = -2147483647;  // row table entry: a row of ones (the bias row of dW)
 constexpr int kZeroRow = -2147483647 - 1;
@@ -80,6 +83,11 @@ struct GParams {
   const float* ones;  // 16 bytes of 1.0f (the source of kOnesRow elements)
   int J, rtiles, nkb, nmma, tcols_half, stages;
   int nsub;  // 128B-swizzle k atoms (32 tf32 each) per pipeline stage: nkb stages cover nkb * nsub atoms
+  // particle batching (gather kernels whose A operand is shared by every particle: the stage-0 forward
+  // over the im2col of X and the stage-0 weight gradient over its transpose): a unit covers nb
+  // consecutive particles, MMA N = nb * nmma_p, column n belongs to particle j0 + n / nmma_p.  The B rows
+  // of consecutive particles are contiguous (b.ps = nmma_p rows), so the producers see one tall matrix.
+  int nb, nmma_p;
   // direct convolution (DIRECT kernels, forward / delta with 32-channel blocks): each stage is one
   // TMA slab of bh + k - 1 input rows x win_w pixels x 32 channels plus the k*k weight atoms of
   // that channel block; the k*k shifted A operands are the same slab read through descriptors
@@ -182,10 +190,15 @@ __device__ __forceinline__ void load_cols(const GOperand& o, int kb, int lane, i
 // Row offsets of the tile rows this lane copies (pass p: vector rows (p*4 + warp)*4 + lane/8,
 // scalar rows (p*4 + warp)*8 + lane/4); kZeroRow past the operand's rows or the tile.
 template <int MAXP>
-__device__ __forceinline__ void load_rows(const GOperand& o, int r0, int nrt, int pt, int lane, int* ro) {
+__device__ __forceinline__ void load_rows(const GOperand& o, int r0, int nrt, int pt, int lane, int* ro,
+                                          int nlim = 0x7fffffff) {
 #pragma unroll
   for (int p = 0; p < MAXP; ++p) {
     const int rl = o.vec ? (p * kProdWarps + pt) * 4 + (lane >> 3) : (p * kProdWarps + pt) * 8 + (lane >> 2);
+    if (rl >= nlim) {  // rows of particles past the ensemble (a batched unit's tail): zeros
+      ro[p] = kZeroRow;
+      continue;
+    }
     if (rl >= nrt) {  // past the tile: nothing to copy
       ro[p] = kZeroRow;
       continue;
@@ -281,7 +294,8 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
   uint64_t* tempty = tfull + 2;
   uint64_t* sfull = tempty + 2;  // DWT: the staging tile of a stage has landed
   uint32_t* tmem_holder = (uint32_t*)(sfull + p.stages);
-  const int units = DIRECT && !DWT ? p.J * p.mimg * p.ybl : p.rtiles * p.J;
+  const int nb = DIRECT ? 1 : p.nb;  // particles per unit
+  const int units = DIRECT && !DWT ? p.J * p.mimg * p.ybl : p.rtiles * ((p.J + nb - 1) / nb);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -422,9 +436,11 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
     static_assert(AV, "the gather producers copy 16-byte chunks");
     constexpr int MAXS = 4;  // atoms per stage
     int ra[8], rb[16], ran[8], rbn[16], ca[MAXS], cb[MAXS], can[MAXS], cbn[MAXS];
+    // B rows a unit may read: its particles that exist (batched units; all rows otherwise)
+    auto blim = [&](int tt) { return nb > 1 ? min(nb, p.J - (tt / p.rtiles) * nb) * p.nmma_p : 0x7fffffff; };
     if (t < units) {
       load_rows<8>(p.a, (t % p.rtiles) * kCBM, kCBM, warp, lane, ra);
-      load_rows<16>(p.b, 0, p.nmma, warp, lane, rb);
+      load_rows<16>(p.b, 0, p.nmma, warp, lane, rb, blim(t));
     }
 #pragma unroll
     for (int u = 0; u < MAXS; ++u)
@@ -433,11 +449,11 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
         load_cols<true>(p.b, u, lane, cb + u);
       }
     while (t < units) {
-      const int j = t / p.rtiles;
+      const int j = (t / p.rtiles) * nb;  // first particle of the unit
       const int tn = t + gridDim.x;
       if (tn < units) {
         load_rows<8>(p.a, (tn % p.rtiles) * kCBM, kCBM, warp, lane, ran);
-        load_rows<16>(p.b, 0, p.nmma, warp, lane, rbn);
+        load_rows<16>(p.b, 0, p.nmma, warp, lane, rbn, blim(tn));
       }
       const float* abase = p.a.base + (int64_t)j * p.a.ps;
       const float* bbase = p.b.base + (int64_t)j * p.b.ps;
@@ -561,16 +577,23 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
         r = (m * p.out_h + y) * p.out_w + x;
       } else {
         const int rt = t % p.rtiles;
-        j = t / p.rtiles;
+        j = (t / p.rtiles) * nb;  // first particle of the unit
         r = rt * kCBM + row_in_tile;
       }
+      const int j_unit = j;
       cwait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t)(acc * p.tcols_half) + ((uint32_t)(lg * 32) << 16);
       for (int ch = ch_lo; ch < ch_hi; ++ch) {
         float v[16];
         tmem_ld16(taddr + ch * 16, v);
-        const int n0 = ch * 16;
+        int n0 = ch * 16;
+        if (!DIRECT && nb > 1) {  // batched unit: this chunk's particle and its column within the particle
+          const int jb = n0 / p.nmma_p;
+          j = j_unit + jb;
+          n0 -= jb * p.nmma_p;
+          if (j >= p.J) continue;
+        }
         const int nq = min(16, p.nvalid - n0);  // warp-uniform
         if (nq <= 0) continue;
         if (p.dbg & 2) continue;
@@ -893,6 +916,7 @@ struct ConvTcState {
   float* XcolT = nullptr;
   int64_t XcolT_rows = 0;
   bool direct_ok = true;       // DASMC_CONV_DIRECT=0 forces the gather path (A/B, tests)
+  bool batch0 = true;          // DASMC_CONV_BATCH0=0: one particle per unit in the stage-0 GEMMs (A/B)
   bool dwt[kMaxConv] = {};     // weight gradient from TMA (flattened, unshifted delta copy: DzL kc = 1)
   int* c2o[kMaxConv] = {};     // input pixel of stage i -> its inT[i] offset (channel 0)
   int* dzo[kMaxConv] = {};     // output pixel of stage i -> its dZs[i] offset (channel 0, kx 0)
@@ -1101,6 +1125,10 @@ bool setup_direct(GParams& p, const float* in, int64_t cap, int H, int W, int C,
 
 template <int EPI>
 void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
+  if (p.nb < 1) {
+    p.nb = 1;
+    p.nmma_p = p.nmma;
+  }
   if (p.nmma > 256) throw std::invalid_argument("conv: MMA N > 256");
   if (!p.b.vec && !direct) throw std::invalid_argument("conv: B operands are 16-byte gathers");
   const size_t fixed = 1024 + 64 * 8 + 64;
@@ -1151,7 +1179,7 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
     return e ? std::atoi(e) : 0;
   }();
   p.dbg = dbg;
-  const int units = direct && EPI != kEpiConvDw ? p.J * p.mimg * p.ybl : p.rtiles * p.J;
+  const int units = direct && EPI != kEpiConvDw ? p.J * p.mimg * p.ybl : p.rtiles * ((p.J + p.nb - 1) / p.nb);
   auto go = [&](auto act_c, auto dir_c) {
     constexpr int A_ = decltype(act_c)::value;
     constexpr bool DI = decltype(dir_c)::value;
@@ -1245,6 +1273,7 @@ void cnn_tc_init(Ctx& c) {
     if (i > 0) CK(cudaMalloc(&s->Wd[i], sizeof(float) * (size_t)c.Jmax * s->nmmaD[i] * s->KpD[i]));
   }
   if (const char* e = std::getenv("DASMC_CONV_DIRECT")) s->direct_ok = e[0] != '0';
+  if (const char* e = std::getenv("DASMC_CONV_BATCH0")) s->batch0 = e[0] != '0';
   // weight gradient from TMA + shared-memory shifts (DASMC_CONV_DWT=0: the gather form with k kx-shifted
   // delta copies in HBM)
   const char* dwt_env = std::getenv("DASMC_CONV_DWT");
@@ -1450,6 +1479,14 @@ void cnn_tc_forward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t m
     p.rtiles = (int)((R + kCBM - 1) / kCBM);
     p.nkb = s->KpF[i] / kCBK;
     p.nmma = s->nmmaF[i];
+    if (i == 0 && s->batch0 && d.cout == s->nmmaF[0]) {
+      // X's im2col is shared by every particle: nb particles per unit (MMA N = nb * cout, one A tile
+      // read for nb particles); their weight copies are consecutive rows of Wf
+      p.nb = std::max(1, std::min<int>(256 / s->nmmaF[0], (int)J));
+      p.nmma_p = s->nmmaF[0];
+      p.nmma = round_up(p.nb * p.nmma_p, 16);
+      p.b.nrows = p.nb * p.nmma_p;
+    }
     p.Rvalid = (int)R;
     p.nvalid = d.cout;
     p.out = c.cact[i];
@@ -1603,6 +1640,24 @@ void cnn_tc_backward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t 
       p.nkb = (p.a.K + kCBK - 1) / kCBK;
       p.nmma = s->nmmaW[i];
       p.nvalid = p.b.nrows;
+      if (xc && s->batch0 && d.cout == s->nmmaW[0]) {
+        // the transposed im2col of X is shared by every particle: nb particles per unit; the unshifted
+        // channel-major deltas [c][m][pixel] of consecutive particles are consecutive rows of s_c floats
+        // K is the whole chunk, so the grid is only rtiles * J / nb units: batch while ~80 % of the SMs keep
+        // one (measured on B200: C3 J = 512 nb 1 / 2 / 4 / 16 = 6.4 / 3.5 / 2.1 / 4.7 ms, C4 J = 256
+        // nb 1 / 2 / 4 / 8 = 2.8 / 1.6 / 2.3 / 3.7 ms per launch)
+        int nbw = 1;
+        while (2 * nbw * d.cout <= 256 && 5 * p.rtiles * (J / (2 * nbw)) >= 4 * s->num_sms) nbw *= 2;
+        if (const char* e = std::getenv("DASMC_CONV_NBW")) nbw = std::max(1, std::min(256 / d.cout, std::atoi(e)));
+        if ((int64_t)nbw * d.cout * s->dzl[0].s_c < ((int64_t)1 << 31)) {
+          p.nb = nbw;
+          p.nmma_p = d.cout;
+          p.nmma = round_up(nbw * d.cout, 16);
+          p.b.rowoff = nullptr;
+          p.b.ld = (int)s->dzl[0].s_c;
+          p.b.nrows = nbw * d.cout;
+        }
+      }
       p.Dp = net.Dp;
       p.boff = d.boff;
       p.e = e;
