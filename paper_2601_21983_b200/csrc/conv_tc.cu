@@ -703,28 +703,51 @@ __global__ void conv_wcopy_kernel(const float* __restrict__ theta, int64_t Dp, i
 // code[j][m][py][px][c] (one byte per pooled element) = position 0..3 of the window's first maximum in
 // (dy, dx) order, bit 2 = max > 0: the max-pool backward routes through it and (ReLU) never re-reads
 // the pre-pool plane.
-__global__ void pool_fwd_nhwc_kernel(ConvDev d, const float* __restrict__ A, int64_t a_ps, float* __restrict__ P,
-                                     int64_t p_ps, int64_t M, int64_t J, int flat, float* __restrict__ T, int64_t t_ps,
-                                     int t_wp, uint8_t* __restrict__ code) {
-  const int C = d.cout;
-  const int64_t per = (int64_t)d.sh * d.sw * C, total = J * M * per;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = g / (M * per), rem = g - j * M * per, m = rem / per;
-    const int o = (int)(rem - m * per);
-    const int c = o % C, pyx = o / C, py = pyx / d.sw, px = pyx - py * d.sw;
-    const float* a = A + j * a_ps + m * (int64_t)d.ho * d.wo * C + ((int64_t)(2 * py) * d.wo + 2 * px) * C + c;
-    const int64_t rowC = (int64_t)d.wo * C;
-    const float a0 = a[0], a1 = a[C], a2 = a[rowC], a3 = a[rowC + C];
-    int best = 0;
-    float v = a0;
-    if (a1 > v) { v = a1; best = 1; }
-    if (a2 > v) { v = a2; best = 2; }
-    if (a3 > v) { v = a3; best = 3; }
-    P[j * p_ps + m * per + (flat ? (int64_t)c * d.sh * d.sw + pyx : o)] = v;
-    if (code) code[(j * M + m) * per + o] = (uint8_t)(best | (v > 0.f ? 4 : 0));  // bit 2: relu'(max)
-    // the next stage's channel-major, width-padded input copy (its weight-gradient operand)
-    if (T) T[j * t_ps + m * (int64_t)C * d.sh * t_wp + ((int64_t)c * d.sh + py) * t_wp + px] = v;
+template <bool P2>
+__global__ void __launch_bounds__(256) pool_fwd_nhwc_kernel(ConvDev d, const float* __restrict__ A, int64_t a_ps,
+                                                            float* __restrict__ P, int64_t p_ps, int M, int flat,
+                                                            float* __restrict__ T, int64_t t_ps, int t_wp,
+                                                            uint8_t* __restrict__ code, int logC) {
+  const int C = d.cout, per = d.sh * d.sw * C, shsw = d.sh * d.sw;
+  const int m = (int)(blockIdx.x % (unsigned)M);  // one image of one particle per block: 32-bit index math inside
+  const int64_t j = blockIdx.x / (unsigned)M;
+  const float* aimg = A + j * a_ps + (int64_t)m * d.ho * d.wo * C;
+  float* pimg = P + j * p_ps + (int64_t)m * per;
+  uint8_t* cimg = code ? code + (j * M + m) * per : nullptr;
+  float* timg = T ? T + j * t_ps + (int64_t)m * C * d.sh * t_wp : nullptr;
+  const int rowC = d.wo * C;
+  for (int py = 0; py < d.sh; ++py) {
+    const float* arow = aimg + 2 * py * rowC;
+    for (int i = threadIdx.x; i < d.sw * C; i += 256) {  // (px, c), c fastest
+      const int px = P2 ? i >> logC : i / C, c = P2 ? i & (C - 1) : i - px * C;
+      const float* a = arow + 2 * px * C + c;
+      const float a0 = a[0], a1 = a[C], a2 = a[rowC], a3 = a[rowC + C];
+      int best = 0;
+      float v = a0;
+      if (a1 > v) { v = a1; best = 1; }
+      if (a2 > v) { v = a2; best = 2; }
+      if (a3 > v) { v = a3; best = 3; }
+      const int o = py * d.sw * C + i;
+      pimg[flat ? c * shsw + py * d.sw + px : o] = v;
+      if (cimg) cimg[o] = (uint8_t)(best | (v > 0.f ? 4 : 0));  // bit 2: relu'(max)
+      // the next stage's channel-major, width-padded input copy (its weight-gradient operand)
+      if (timg) timg[(c * d.sh + py) * t_wp + px] = v;
+    }
   }
+}
+
+void launch_pool_fwd(Ctx& c, const ConvDev& d, const float* A, int64_t a_ps, float* P, int64_t p_ps, int64_t M,
+                     int64_t J, int flat, float* T, int64_t t_ps, int t_wp, uint8_t* code) {
+  const bool p2 = (d.cout & (d.cout - 1)) == 0;
+  int logC = 0;
+  while ((1 << logC) < d.cout) ++logC;
+  if (p2)
+    pool_fwd_nhwc_kernel<true><<<(unsigned)(J * M), 256, 0, c.stream>>>(d, A, a_ps, P, p_ps, (int)M, flat, T, t_ps, t_wp,
+                                                                        code, logC);
+  else
+    pool_fwd_nhwc_kernel<false><<<(unsigned)(J * M), 256, 0, c.stream>>>(d, A, a_ps, P, p_ps, (int)M, flat, T, t_ps,
+                                                                         t_wp, code, logC);
+  LAUNCHED();
 }
 
 // Max-pool backward into the stage's zero-bordered delta buffer: the pooled delta (NHWC, or the
@@ -746,55 +769,73 @@ struct DzL {
 // code = pool_fwd_nhwc_kernel's argmax codes (ReLU: act' from the code; tanh: the maximum is read back from
 // the pre-pool plane A at the coded position); dZ == nullptr (stage 0: no delta GEMM reads it) skips the
 // NHWC output.
+// The index arithmetic is shifts and masks when C is a power of two (P2; logC = log2 C): the kernel is
+// issue-bound, and per-element integer divisions were most of its instructions.
+template <bool P2>
 __global__ void __launch_bounds__(256) pool_bwd_rows_kernel(ConvDev d, int act, const float* __restrict__ A,
                                                             int64_t a_ps, const uint8_t* __restrict__ code,
                                                             const float* __restrict__ dP, int64_t dp_ps,
-                                                            int flat, float* __restrict__ dZ, int64_t dz_ps, int64_t M,
-                                                            float* __restrict__ S, int64_t s_ps, DzL L) {
-  extern __shared__ float pz[];  // [2][wo][C + 1]: the window deltas of two pre-pool rows
+                                                            int flat, float* __restrict__ dZ, int64_t dz_ps, int M,
+                                                            float* __restrict__ S, int64_t s_ps, DzL L, int logC,
+                                                            int PR) {
+  extern __shared__ float pz[];  // [2 PR][wo][C + 1]: the window deltas of PR pooled rows (2 PR pre-pool rows)
   const int C = d.cout, pad = d.k - 1, W2 = d.wo + 2 * pad, H2 = d.ho + 2 * pad, CP = C + 1;
-  const int64_t img = blockIdx.x;  // (j, m): one image of one particle per block
-  const int64_t m = img % M, j = img / M;
+  const int m = (int)(blockIdx.x % (unsigned)M);  // (j, m): one image of one particle per block
+  const int64_t j = blockIdx.x / (unsigned)M;
   const int wo2 = 2 * d.sw;  // pre-pool columns covered by windows
-  const int64_t per = (int64_t)d.sh * d.sw * C;
+  const int per = d.sh * d.sw * C, shsw = d.sh * d.sw;
   const uint8_t* cimg = code + (j * M + m) * per;
-  const float* aimg = A + j * a_ps + m * (int64_t)d.ho * d.wo * C;
-  float* z = dZ ? dZ + j * dz_ps + m * (int64_t)H2 * W2 * C : nullptr;
+  const float* dpimg = dP + j * dp_ps + (int64_t)m * per;
+  const float* aimg = A + j * a_ps + (int64_t)m * d.ho * d.wo * C;
+  float* z = dZ ? dZ + j * dz_ps + (int64_t)m * H2 * W2 * C : nullptr;
   float* sb = S + j * s_ps + m * L.s_m;
-  for (int py = 0; py < d.sh; ++py) {
-    __syncthreads();  // the previous row pair's reads of pz are done
-    for (int i = threadIdx.x; i < d.sw * C; i += blockDim.x) {  // (px, c), c fastest: coalesced NHWC reads
-      const int c = i % C, px = i / C;
-      const int64_t o = ((int64_t)py * d.sw + px) * C + c;
-      const int64_t po = flat ? (int64_t)c * d.sh * d.sw + py * d.sw + px : o;  // pooled-output layout
-      const int cd = cimg[o], best = cd & 3;
-      const float gp = dP[j * dp_ps + m * per + po];
-      float dact;
-      if (act == DASMC_RELU) {
-        dact = (cd & 4) ? 1.f : 0.f;
-      } else {
-        const float mx = aimg[((int64_t)(2 * py + (best >> 1)) * d.wo + 2 * px + (best & 1)) * C + c];
-        dact = 1.f - mx * mx;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int py0 = 0; py0 < d.sh; py0 += PR) {
+    const int npr = min(PR, d.sh - py0);  // pooled rows of this pass
+    __syncthreads();  // the previous pass's reads of pz are done
+    for (int pyl = 0; pyl < npr; ++pyl) {
+      const int py = py0 + pyl;
+      float* prow = pz + 2 * pyl * d.wo * CP;
+      for (int i = threadIdx.x; i < d.sw * C; i += 256) {  // (px, c), c fastest: coalesced NHWC reads
+        const int px = P2 ? i >> logC : i / C, c = P2 ? i & (C - 1) : i - px * C;
+        const int o = py * d.sw * C + i;
+        const int po = flat ? c * shsw + py * d.sw + px : o;  // pooled-output layout
+        const int cd = cimg[o], best = cd & 3;
+        const float gp = dpimg[po];
+        float dact;
+        if (act == DASMC_RELU) {
+          dact = (cd & 4) ? 1.f : 0.f;
+        } else {
+          const float mx = aimg[((2 * py + (best >> 1)) * d.wo + 2 * px + (best & 1)) * C + c];
+          dact = 1.f - mx * mx;
+        }
+        const float v = tf32_hi(gp * dact);
+        // all four window positions (the three non-maxima get 0): no separate zeroing pass
+        float* w = prow + (2 * px) * CP + c;
+        w[0] = best == 0 ? v : 0.f;
+        w[CP] = best == 1 ? v : 0.f;
+        w[d.wo * CP] = best == 2 ? v : 0.f;
+        w[(d.wo + 1) * CP] = best == 3 ? v : 0.f;
       }
-      const float v = tf32_hi(gp * dact);
-      // all four window positions (the three non-maxima get 0): no separate zeroing pass
-      float* w = pz + (2 * px) * CP + c;
-      w[0] = best == 0 ? v : 0.f;
-      w[CP] = best == 1 ? v : 0.f;
-      w[d.wo * CP] = best == 2 ? v : 0.f;
-      w[(d.wo + 1) * CP] = best == 3 ? v : 0.f;
     }
     __syncthreads();
-    // NHWC zero-bordered rows: (dy, x, c) contiguous per row
+    // NHWC zero-bordered rows: (x, c) contiguous per row
     if (z)
-    for (int i = threadIdx.x; i < 2 * wo2 * C; i += blockDim.x) {
-      const int c = i % C, xy = i / C, x = xy % wo2, dy = xy / wo2;
-      z[((int64_t)(2 * py + dy + pad) * W2 + x + pad) * C + c] = pz[(dy * d.wo + x) * CP + c];
-    }
-    // channel-major (kx-shifted) copies: for each (kx, c, dy) a contiguous run over x
-    for (int i = threadIdx.x; i < L.kc * C * 2 * wo2; i += blockDim.x) {
-      const int x = i % wo2, r = i / wo2, dy = r % 2, kc = r / 2, c = kc % C, kx = kc / C;
-      sb[kx * L.s_kx + c * L.s_c + (int64_t)(2 * py + dy) * L.s_y + x + kx] = pz[(dy * d.wo + x) * CP + c];
+      for (int yl = 0; yl < 2 * npr; ++yl) {
+        float* zr = z + ((int64_t)(2 * py0 + yl + pad) * W2 + pad) * C;
+        const float* src = pz + yl * d.wo * CP;
+        for (int i = threadIdx.x; i < wo2 * C; i += 256) {
+          const int x = P2 ? i >> logC : i / C, c = P2 ? i & (C - 1) : i - x * C;
+          zr[i] = src[x * CP + c];
+        }
+      }
+    // channel-major (kx-shifted) copies: one warp per (kx, c) pair, a run over x per pre-pool row
+    for (int kcc = warp; kcc < L.kc * C; kcc += 8) {
+      const int kx = P2 ? kcc >> logC : kcc / C, c = P2 ? kcc & (C - 1) : kcc - kx * C;
+      float* dst = sb + kx * L.s_kx + c * L.s_c + (int64_t)(2 * py0) * L.s_y + kx;
+      const float* src = pz + c;
+      for (int yl = 0; yl < 2 * npr; ++yl, dst += L.s_y, src += d.wo * CP)
+        for (int x = lane; x < wo2; x += 32) dst[x] = src[x * CP];
     }
   }
 }
@@ -802,17 +843,26 @@ __global__ void __launch_bounds__(256) pool_bwd_rows_kernel(ConvDev d, int act, 
 void launch_pool_bwd(Ctx& c, const ConvDev& d, int act, const float* A, int64_t a_ps, const uint8_t* code,
                      const float* dP, int64_t dp_ps, int flat, float* dZ, int64_t dz_ps, int64_t M, int64_t J, float* S,
                      int64_t s_ps, const DzL& L) {
-  const size_t sm = sizeof(float) * 2 * (size_t)d.wo * (d.cout + 1);
-  if (sm > 48 * 1024) {
-    static bool attr[kMaxDevices] = {};
-    const int dv = current_device();
-    if (!attr[dv]) {
-      CK(cudaFuncSetAttribute(pool_bwd_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr[dv] = true;
-    }
-  }
-  pool_bwd_rows_kernel<<<(unsigned)(J * M), 256, sm, c.stream>>>(d, act, A, a_ps, code, dP, dp_ps, flat, dZ, dz_ps, M,
-                                                                 S, s_ps, L);
+  // pooled rows per pass (fewer block-wide barriers per image): what ~kb KB of shared memory hold
+  const size_t row_bytes = sizeof(float) * 2 * (size_t)d.wo * (d.cout + 1);
+  static const int kb = [] {
+    const char* e = std::getenv("DASMC_POOL_KB");
+    return e ? std::atoi(e) : 24;
+  }();
+  const int PR = (int)std::max<size_t>(1, std::min<size_t>((size_t)d.sh, (size_t)kb * 1024 / row_bytes));
+  const size_t sm = row_bytes * PR;
+  const bool p2 = (d.cout & (d.cout - 1)) == 0;
+  int logC = 0;
+  while ((1 << logC) < d.cout) ++logC;
+  auto go = [&](auto kern) {
+    if (sm > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    kern<<<(unsigned)(J * M), 256, sm, c.stream>>>(d, act, A, a_ps, code, dP, dp_ps, flat, dZ, dz_ps, (int)M, S, s_ps, L,
+                                                   logC, PR);
+  };
+  if (p2)
+    go(pool_bwd_rows_kernel<true>);
+  else
+    go(pool_bwd_rows_kernel<false>);
   LAUNCHED();
 }
 
@@ -1518,10 +1568,8 @@ void cnn_tc_forward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t m
     }
     launch_gemm<kEpiConvFwd>(c, p, net.act, direct);
     if (d.pool) {
-      pool_fwd_nhwc_kernel<<<grid_of(J * mc * pool_plane(d)), 256, 0, c.stream>>>(
-          d, c.cact[i], cap * act_plane(d), c.cpool[i], cap * pool_plane(d), mc, J, last ? 1 : 0,
-          last ? nullptr : s->inT[i + 1], nxt_ps, last ? 0 : s->winp[i + 1], s->pcode[i]);
-      LAUNCHED();
+      launch_pool_fwd(c, d, c.cact[i], cap * act_plane(d), c.cpool[i], cap * pool_plane(d), mc, J, last ? 1 : 0,
+                      last ? nullptr : s->inT[i + 1], nxt_ps, last ? 0 : s->winp[i + 1], s->pcode[i]);
     } else if (last) {
       nhwc_to_flat_kernel<<<grid_of(J * mc * act_plane(d)), 256, 0, c.stream>>>(d, c.cact[i], cap * act_plane(d),
                                                                                  c.cpool[i], cap * act_plane(d), mc, J);
