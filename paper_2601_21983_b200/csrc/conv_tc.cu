@@ -340,7 +340,7 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
             for (int kb = 0; kb < p.kpi; ++kb) {
               cwait(&empty[s], ph ^ 1);
               uint8_t* st = smem + (size_t)s * stage_bytes;
-              if (one_row >= 0) {  // the bias row of ones (all 32 values equal: swizzle-invariant)
+              if (one_row >= 0 && !(p.dbg & 16)) {  // the bias row of ones (all 32 values equal: swizzle-invariant)
                 float4* o = reinterpret_cast<float4*>(st + (one_row >> 3) * 1024 + (one_row & 7) * 128);
 #pragma unroll
                 for (int u = 0; u < 8; ++u) o[u] = make_float4(1.f, 1.f, 1.f, 1.f);
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
           uint8_t* st = smem + (size_t)s * stage_bytes;
           const float* stg = reinterpret_cast<const float*>(st + a_bytes + b_bytes) + sw * ldst + p.halo + lane;
           const uint32_t tile = smem_u32(st + a_bytes);
-          for (int kx = 0; kx < p.kk; ++kx) {
+          for (int kx = 0; kx < ((p.dbg & 8) ? 0 : p.kk); ++kx) {
             const int r0 = kx * p.cout_rows + sw;
             const uint32_t dst = tile + swz(r0, lane);
             const float* src = stg - kx;
@@ -1404,7 +1404,8 @@ int64_t cnn_tc_image_floats(const Ctx& c) {
     const int64_t wp = round_up(d.win, 4);
     f += act_plane(d) + (i > 0 ? pad_plane(d) : 0);  // output, zero-bordered delta (stages > 0)
     if (d.pool) f += (pool_plane(d) + 3) / 4;        // argmax codes (bytes)
-    f += (int64_t)d.k * d.cout * d.ho * wp;          // kx-shifted deltas
+    const bool one_copy = c.ctc && (c.ctc->dwt[i] || (i == 0 && c.ctc->xcol0));
+    f += (int64_t)(one_copy ? 1 : d.k) * d.cout * d.ho * wp;  // channel-major delta copy (k kx-shifted ones: gather form)
     if (i > 0) f += (int64_t)d.cin * d.hin * wp;     // channel-major input copy
     if (d.pool) f += pool_plane(d);
     else if (i == net.nconv - 1) f += act_plane(d);  // the flatten copy
