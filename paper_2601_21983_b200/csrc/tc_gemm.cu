@@ -98,6 +98,18 @@ constexpr int kAShared = 0, kABlocked = 1, kARowMajor = 2;
 #ifndef DASMC_W2_AHEAD
 #define DASMC_W2_AHEAD 0
 #endif
+// Pass 2 of the fused-forward epilogue, delta1 = (delta2 W2) . act'(z1), as one small tensor-core MMA
+// per tile (ReLU nets, CTA pairs, fp16-stored operands): delta2 (fp16, [128][16]) and W2 (fp16,
+// [nmma / 2][16] per CTA) are written to shared memory in the unswizzled K-major core-matrix layout,
+// one epilogue thread of the pair leader issues a cta_group::2 kind::f16 MMA (M = 256, N = nmma, K = 16)
+// that overwrites the tile's z1 accumulator once every warp has read it, and the CUDA cores only mask
+// (ReLU' bits kept in registers from pass 1), round and store.
+// Opt-in (-DDASMC_L2TC=1): parity-green, but measured on B200 it does not move the default mode
+// (C2 forward, interleaved A/B: f16x2 26.4 vs 26.3 ms, tf32h 25.8 vs 26.9 ms, f16 20.7 vs 19.8 ms per launch):
+// the forward is bound by its operand loads and activation stores, not by the epilogue's instruction count.
+#ifndef DASMC_L2TC
+#define DASMC_L2TC 0
+#endif
 // Epilogue activation stores (a1^T, delta1^T: streamed once, re-read by the
 // weight-gradient GEMMs after ~25 GB of other traffic)
 #ifndef DASMC_ST_POLICY
@@ -236,6 +248,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = (uint32_t*)(tempty + 2);
   float* epi_smem = (float*)(tmem_holder + 4);  // 16-byte aligned
+  // tensor-core pass 2 (see DASMC_L2TC): two mbarriers and the two small operand tiles behind the
+  // CUDA-core epilogue's buffers
+  constexpr bool L2TC = DASMC_L2TC && EPI == kEpiKindFwd && CL == 1 && ACT == DASMC_RELU && !SPLIT && PREC >= 1;
+  uint64_t* l2bar = nullptr;  // [0] ready (every epilogue warp of the pair, on the leader), [1] done (MMA commit)
+  uint8_t* d2tile = nullptr;  // delta2 [128][16] fp16
+  uint8_t* w2h = nullptr;     // W2 rows o = prank * b_rows ..: [b_rows][16] fp16
+  if constexpr (L2TC) {
+    constexpr int CS0 = (CP + 3) & ~3;
+    uint8_t* q = reinterpret_cast<uint8_t*>(epi_smem + 2 * ((size_t)fp.n1 * CS0 + CS0) + (size_t)kParts * 128 * CP) +
+                 8 * sizeof(double);
+    l2bar = reinterpret_cast<uint64_t*>(q);
+    uint8_t* t0 = q + 16;
+    t0 += (128u - (smem_u32(t0) & 127u)) & 127u;
+    d2tile = t0;
+    w2h = t0 + 4096;
+  }
 
   auto A_of = [&](int s, int lo) { return stages + (size_t)s * stage_bytes + (lo ? a_bytes : 0); };
   auto B_of = [&](int s, int lo) { return stages + (size_t)s * stage_bytes + sub * a_bytes + (lo ? b_bytes : 0); };
@@ -259,6 +287,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[b], 1);
       // one arrival per epilogue warp (of both CTAs of a pair: the leader's barrier)
       mbar_init(&tempty[b], (PAIR ? 2 : 1) * kEpiWarps);
+    }
+    if constexpr (L2TC) {
+      mbar_init(&l2bar[0], 2 * kEpiWarps);
+      mbar_init(&l2bar[1], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -462,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t aph = 0;
     const uint64_t st_pol = l2_policy(2);  // activation stores: evict first (DASMC_ST_POLICY 3)
     int it = 0;                     // forward tiles processed (W2^T buffer parity)
+    uint32_t l2ph = 0;              // parity of the pass-2 MMA barriers (L2TC)
     double* ll_pending = nullptr;   // forward: ll slot of the previous tile, written by thread 0
     double* red = (double*)(epi_smem + 2 * ((size_t)fp.n1 * ((CP + 3) & ~3) + ((CP + 3) & ~3)) +
                             (size_t)kParts * 128 * CP);  // [4][2] lane-group partials
@@ -482,6 +515,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         // a tile of the cluster wholly past the window (or a padding particle): nothing to store
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
+        if constexpr (L2TC) {
+          if (fp.need_grad && (fp.dbg == 0 || fp.dbg >= 5)) {
+            // the peer's pass-2 MMA still reads this CTA's half of W2 and writes this CTA's accumulator
+            const float* thp = fp.theta + (int64_t)j * fp.Dp;
+            for (int i = et; i < (int)b_rows * 16; i += kEpiThreads) {
+              const int r = i >> 4, k = i & 15, o = (int)(prank * b_rows) + r;
+              const float x = (o < fp.n1 && k < fp.C) ? thp[fp.woff2 + (int64_t)k * fp.n1 + o] : 0.f;
+              *reinterpret_cast<__half*>(w2h + (r >> 3) * 256 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2) =
+                  __float2half_rn(x);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&l2bar[0]), crank & ~1u));
+            mbar_wait(&l2bar[1], l2ph);
+            tc_fence_after();
+            l2ph ^= 1;
+          }
+        }
         release_acc(acc);
         acc ^= 1;
         if (acc == 0) aph ^= 1;
@@ -526,6 +578,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (et < CS) b2s[et] = b2v;
         named_bar(1, kEpiThreads);
         if (et == 0 && ll_pending) flush_ll();
+        const bool l2go = L2TC && fp.need_grad && (dbg == 0 || dbg >= 5);  // pass 2 on the tensor core
+        if constexpr (L2TC) {
+          if (l2go) {
+            // this CTA's half of W2 as the MMA's B operand: rows o, k = class (zero past C)
+            for (int i = et; i < (int)b_rows * 8; i += kEpiThreads) {
+              const int r = i >> 3, kp = i & 7, o = (int)(prank * b_rows) + r;
+              const float x0 = (o < n1 && 2 * kp < C) ? W2T[o * CS + 2 * kp] : 0.f;
+              const float x1 = (o < n1 && 2 * kp + 1 < C) ? W2T[o * CS + 2 * kp + 1] : 0.f;
+              *reinterpret_cast<__half2*>(w2h + (r >> 3) * 256 + (kp >> 2) * 128 + (r & 7) * 16 + (kp & 3) * 4) =
+                  __floats2half2_rn(x0, x1);
+            }
+          }
+        }
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(lg * 32) << 16);
@@ -558,6 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float2 z2p[CP / 2];
 #pragma unroll
         for (int c = 0; c < CP / 2; ++c) z2p[c] = make_float2(0.f, 0.f);
+        uint32_t mk0 = 0, mk1 = 0, mk2 = 0;  // L2TC: ReLU' bits of this thread's columns (a 96-bit stack)
         // DASMC_DEBUG_EPI=4 (profiling only): every tile stores into one L2-resident block
         const int64_t sblk = dbg == 4 ? (int64_t)(blockIdx.x & 1) : (int64_t)j * nblk + rt;
         TS* a1T = reinterpret_cast<TS*>(fp.a1T) + sblk * (n1 + 1) * kRow + row_in_tile;
@@ -603,9 +669,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int nq = min(CW, col_hi - o0);  // warp-uniform
           TS* pa = a1T + (int64_t)o0 * kRow;
           float* pal = SPLIT ? a1Tlo + (int64_t)o0 * kRow : nullptr;
+          uint32_t mcur = 0;  // L2TC: ReLU' bits of this chunk's columns
           auto one = [&](int q, const float2* w) {
             const float a = act(v[q]);
             const float2 aa = make_float2(a, a);
+            if constexpr (L2TC) mcur |= a > 0.f ? (1u << q) : 0u;
 #pragma unroll
             for (int c = 0; c < CP / 2; ++c) z2p[c] = __ffma2_rn(aa, w[c], z2p[c]);
             if (decltype(store)::value) {
@@ -618,6 +686,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             w2_pipeline(o0, CW, one);
           else  // tail chunk: still unrolled so v[] stays in registers
             w2_pipeline(o0, nq, one);
+          if constexpr (L2TC) {  // push the chunk's bits (pass 2 pops them in reverse chunk order)
+            mk2 = (mk2 << CW) | (mk1 >> (32 - CW));
+            mk1 = (mk1 << CW) | (mk0 >> (32 - CW));
+            mk0 = (mk0 << CW) | mcur;
+          }
         };
         // TMEM loads double-buffered: chunk ch+1 is in flight while ch is processed
         auto run_chunks = [&](auto body) {
@@ -711,7 +784,74 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        if (fp.need_grad && (dbg == 0 || dbg >= 5)) {  // 6: no delta1^T stores
+        if (l2go) {
+          if constexpr (L2TC) {
+            // pass 2 on the tensor core: delta1 = (delta2 W2) . relu'(z1)  (network.hpp:209-215)
+            if (part == 0) {  // this row's delta2 as the MMA's A operand (zeros past the window / past C)
+              __half2 h[8];
+#pragma unroll
+              for (int c = 0; c < 8; ++c)
+                h[c] = __floats2half2_rn(2 * c < CP ? d2[2 * c] : 0.f, 2 * c + 1 < CP ? d2[2 * c + 1] : 0.f);
+              uint4* dst = reinterpret_cast<uint4*>(d2tile + (row_in_tile >> 3) * 256 + (row_in_tile & 7) * 16);
+              dst[0] = *reinterpret_cast<const uint4*>(&h[0]);
+              dst[8] = *reinterpret_cast<const uint4*>(&h[4]);  // + 128 bytes: k = 8..15
+            }
+            // operand tiles (generic-proxy writes) -> the MMA's async-proxy reads; this warp's z1 loads are
+            // complete (tcgen05.wait::ld in run_chunks) before the MMA overwrites the accumulator
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&l2bar[0]), crank & ~1u));
+            if (et == 0 && prank == 0) {
+              mbar_wait(&l2bar[0], l2ph);
+              tc_fence_after();
+              // unswizzled K-major core matrices (8 rows x 16 bytes): LBO (k) = 128 B, SBO (rows) = 256 B
+              auto desc0 = [](const void* p) {
+                return (uint64_t)((smem_u32(p) >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) |
+                       ((uint64_t)(256 >> 4) << 32) | (1ULL << 46);
+              };
+              tc_mma2<1>(tmem_base + (uint32_t)(acc * 256), desc0(d2tile), desc0(w2h), idesc_f16(tp.nmma, 2 * BM), 0);
+              tc_commit2(&l2bar[1], (uint16_t)(3u << (2 * pr)));
+            }
+            mbar_wait(&l2bar[1], l2ph);
+            tc_fence_after();
+            l2ph ^= 1;
+            TS* d1T = reinterpret_cast<TS*>(fp.d1T) + sblk * n1 * kRow + row_in_tile;
+            // chunks in reverse order (the bit stack), TMEM loads double-buffered
+            auto chunk2t = [&](int ch, const float* v) {
+              const int o0 = col_lo + ch * CW;
+              const int nq = min(CW, col_hi - o0);  // warp-uniform
+              TS* pd = d1T + (int64_t)o0 * kRow;
+              const uint32_t mcur = mk0;
+              mk0 = (mk0 >> CW) | (mk1 << (32 - CW));
+              mk1 = (mk1 >> CW) | (mk2 << (32 - CW));
+              mk2 >>= CW;
+#pragma unroll
+              for (int q = 0; q < CW; ++q)
+                if (q < nq) {
+                  const TS hi = to_op<SP>((mcur >> q) & 1u ? v[q] : 0.f);
+                  if (dbg != 6) pd[q * kRow] = hi;
+                }
+            };
+            {
+              float va[CW] = {}, vb[CW] = {};
+              const uint32_t tcol = taddr + (uint32_t)col_lo;
+              int ch = c_hi - 1;
+              if (ch >= c_lo) tmem_ldw_async<CW>(tcol + ch * CW, va);
+              tmem_waitw<CW>(va);
+              while (ch >= c_lo) {
+                if (ch - 1 >= c_lo) tmem_ldw_async<CW>(tcol + (ch - 1) * CW, vb);
+                chunk2t(ch, va);
+                tmem_waitw<CW>(vb);
+                if (--ch < c_lo) break;
+                if (ch - 1 >= c_lo) tmem_ldw_async<CW>(tcol + (ch - 1) * CW, va);
+                chunk2t(ch, vb);
+                tmem_waitw<CW>(va);
+                --ch;
+              }
+            }
+          }
+        } else if (fp.need_grad && (dbg == 0 || dbg >= 5)) {  // 6: no delta1^T stores
           // pass 2: delta1 = (W2^T delta2) . act'(z1)  (network.hpp:209-215); zero past the window
           TS* d1T = reinterpret_cast<TS*>(fp.d1T) + sblk * n1 * kRow + row_in_tile;
           float* d1Tlo = SPLIT ? fp.d1Tlo + ((int64_t)j * nblk + rt) * n1 * kRow + row_in_tile : nullptr;
@@ -1706,7 +1846,9 @@ void tc_eval_fused(Ctx& c, const float* theta_in, int64_t J, int64_t M, int64_t 
     // classes padded to 4, 10 or 16 (W2^T rows float4-aligned in shared memory)
     const int CP = C <= 4 ? 4 : C <= 10 ? 10 : 16;
     const int CS = (CP + 3) & ~3;
-    const size_t epi_bytes = sizeof(float) * (2 * ((size_t)n1 * CS + CS) + kParts * 128 * CP) + 8 * sizeof(double) + 16;
+    // + the tensor-core pass 2's barriers and operand tiles (DASMC_L2TC): 16 + alignment + 4096 + 128 rows x 32 B
+    const size_t epi_bytes = sizeof(float) * (2 * ((size_t)n1 * CS + CS) + kParts * 128 * CP) + 8 * sizeof(double) + 16 +
+                             (16 + 128 + 4096 + 128 * 32);
     DwParams dp{};
     auto go = [&](auto cp, auto act) {
       constexpr int K = decltype(cp)::value, A_ = decltype(act)::value;
