@@ -152,6 +152,37 @@ def test_c3_many_particles_long_window(product, oracle, prec):
     assert norm_err(g[0], go[0]) < tol and norm_err(g1[0], go[0]) < tol
 
 
+@pytest.mark.parametrize("arch,J", [(C3, 251), (C4, 189)])
+def test_stage0_particle_batching_tail(product, oracle, arch, J, monkeypatch):
+    """The stage-0 GEMMs put several particles on the MMA's N dimension (the im2col of X and its transpose
+    are shared by every particle).  J is not a multiple of the batch, so the last unit's missing particles
+    are zero rows; the weight-gradient batch is forced to 4 (the heuristic keeps one particle per unit at
+    this small J).  Particles at the start, across a batch boundary and in the tail match the oracle, and
+    equal the unbatched evaluation (values bit-identical, gradients to fp32 reassociation)."""
+    M, n = 24, 32
+    spec, X, y = problem(product, arch, n)
+    D = product.param_count(spec)
+    th = (0.2 * np.random.default_rng(8).standard_normal((J, D))).astype(np.float32).astype(np.float64)
+    monkeypatch.setenv("DASMC_CONV_NBW", "4")
+    t = product.GpuEnsembleTarget(spec, X, y, J, precision="tf32")
+    t.set_target(0, M, n, "scaled", 1.0, 1.0)
+    v, g = t.log_target_with_grad(th)
+    t.close()
+    monkeypatch.delenv("DASMC_CONV_NBW")
+    monkeypatch.setenv("DASMC_CONV_BATCH0", "0")
+    t = product.GpuEnsembleTarget(spec, X, y, J, precision="tf32")
+    t.set_target(0, M, n, "scaled", 1.0, 1.0)
+    v0, g0 = t.log_target_with_grad(th)
+    t.close()
+    assert np.all(np.isfinite(v)) and np.all(np.isfinite(g))
+    np.testing.assert_array_equal(v, v0)
+    assert max(norm_err(g[j], g0[j]) for j in range(J)) < 1e-5
+    pick = [0, 3, 4, 15, 16, J - 2, J - 1]
+    vo, go = oracle.value_and_grad(spec.oracle_layers(), 0, X.astype(np.float64), y, (0, M, n), 0, 1.0, 1.0, th[pick])
+    assert rel(v[pick], vo) < VAL_TC
+    assert max(norm_err(g[j], go[i]) for i, j in enumerate(pick)) < GRAD_TC
+
+
 def test_c4_full_batch_window(product):
     """BASELINE configs[3]'s full-batch phase: a window of all n = 50000 images (tensor-core
     stages, chunked).  Size-independent checks: finite values and gradients, and additivity of
