@@ -446,7 +446,8 @@ def run_ours(args, w):
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(args.precision)
+            # per workload and precision: ncu dram bytes (read + write) per launch of the dominant kernel
+            traffic = json.load(open(tf)).get(args.config, {}).get(args.precision)
         except Exception:
             traffic = None
     roof = {"bound": "tensor" if args.precision != "fp32" else "compute", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

@@ -157,7 +157,8 @@ const char* dasmc_last_error(void);
  * Replaces: Dataset + TargetContext ownership (dataset.hpp:46-56,
  * target.hpp:95-102).  X is n x input row-major fp32 in the run's fixed
  * (already shuffled) order, y the int32 labels.  The data is copied once to
- * HBM and stays resident.  max_particles bounds J for buffer sizing. */
+ * HBM and stays resident.  max_particles bounds J for buffer sizing (2 .. 65535 per context; larger
+ * ensembles shard over dasmc_gpu_create_multi). */
 int dasmc_gpu_create(const dasmc_net_desc* net, const float* X, const int32_t* y, int64_t n,
                      int max_particles, int device, int precision, dasmc_ctx** out);
 int dasmc_gpu_destroy(dasmc_ctx* ctx);

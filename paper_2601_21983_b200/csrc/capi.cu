@@ -539,6 +539,9 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
   if (n < 1) throw InvalidArg("dataset: n must be >= 1");
   if (X == nullptr || y == nullptr) throw InvalidArg("dataset: null X or y");
   if (Jmax < 2) throw InvalidArg("max_particles must be >= 2");
+  // per context: the gather / row kernels index particles by gridDim.y and the single-block weights
+  // kernel walks J in shared-memory batches; larger ensembles shard over a multi-GPU group
+  if (Jmax > 65535) throw InvalidArg("max_particles must be <= 65535 per context");
   if (precision != DASMC_PREC_FP32 && precision != DASMC_PREC_TF32 && precision != DASMC_PREC_3XTF32 &&
       precision != DASMC_PREC_F16 && precision != DASMC_PREC_TF32H && precision != DASMC_PREC_F16X2)
     throw InvalidArg("bad precision");

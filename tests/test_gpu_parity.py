@@ -336,3 +336,12 @@ def test_bench_memory_hook(product):
                                              ms.ctypes.data_as(C.POINTER(C.c_double)),
                                              by.ctypes.data_as(C.POINTER(C.c_double))))
     t.close()
+
+
+def test_particle_count_bounds(product):
+    """max_particles is bounded per context (2 .. 65535: the gather kernels index particles by gridDim.y,
+    ADVICE r1); out-of-range values are invalid arguments, not launch failures."""
+    spec, X, y = make_problem(product, [6, 4, 3], "tanh", 16)
+    for bad in (1, 65536, 100000):
+        with pytest.raises(ValueError):
+            product.GpuEnsembleTarget(spec, X, y, bad)

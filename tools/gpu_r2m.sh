@@ -9,6 +9,7 @@ timeout 600 python bench.py > $O/bench_c2.log 2>&1; echo c2=$?
 timeout 600 python bench.py --config c1 --steps 20 --warmup 5 > $O/bench_c1.log 2>&1; echo c1=$?
 timeout 600 python bench.py --config c3 --steps 5 --warmup 3 > $O/bench_c3.log 2>&1; echo c3=$?
 timeout 600 python bench.py --config c4 --steps 3 --warmup 3 > $O/bench_c4.log 2>&1; echo c4=$?
+timeout 1500 python bench.py --config c4fb --steps 1 --warmup 1 --e2e-steps 1 --no-cpu > $O/bench_c4fb.log 2>&1; echo c4fb=$?; tail -1 $O/bench_c4fb.log | cut -c1-300
 timeout 600 python bench.py --config c5 --steps 5 --warmup 3 > $O/bench_c5.log 2>&1; echo c5=$?
 for f in bench_c2 bench_c1 bench_c3 bench_c4 bench_c5; do tail -1 $O/$f.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$f', round(d['ms_per_step'],3), '%.4g'%d['value'], 'e2e %.4g'%d['e2e']['value'], 'frac', round(d['roofline']['frac'],4), d['config'].get('window_rows'), 'cpu', d.get('cpu_baseline',{}).get('value'))"; done
 for a in "--config c2" "--config c5"; do python tools/membench.py $a; done > $O/membench.jsonl 2>/dev/null; cat $O/membench.jsonl | cut -c1-300
