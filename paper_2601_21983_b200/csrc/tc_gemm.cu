@@ -601,17 +601,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // 16-column TMEM loads, except in the fp16 mode whose (epilogue-bound) forward
         // runs 9 % faster with 8 (B200 in-process A/B; tf32 / tf32h 4 % slower with 8)
         constexpr int CW = DASMC_CW > 0 ? DASMC_CW : (PREC == 1 ? 8 : 16);
-        // whole 16-column chunks per part (C2: 64 / 64 / 72 of 200 columns); DASMC_V_EVENSPLIT: columns
-        // split evenly over the lane group's kParts warps (67 / 67 / 66)
-#ifdef DASMC_V_EVENSPLIT  // measured slower on B200 (26.1 vs 25.6 ms per C2 launch): unaligned tails
-        const int col_per = (n1 + kParts - 1) / kParts;
-        const int col_lo = min(n1, part * col_per), col_hi = min(n1, col_lo + col_per);
-        c_lo = 0;
-        c_hi = (col_hi - col_lo + CW - 1) / CW;
-#else
+        // whole CW-column chunks per part (C2: 64 / 64 / 72 of 200 columns).  An even 67 / 67 / 66 split was
+        // measured slower on B200 (26.1 vs 25.6 ms per C2 launch: unaligned TMEM chunks and 2-3 column tails)
         chunk_range((n1 + CW - 1) / CW, c_lo, c_hi);
-        const int col_lo = 0, col_hi = n1;
-#endif
+        constexpr int col_lo = 0;
+        const int col_hi = n1;
         if (dbg == 3) c_hi = c_lo;
         // transposed buffers are row-blocked [J][nblk][rows][128]: a tile's rows are one
         // contiguous region; consecutive rows of a block are 128 floats apart
