@@ -95,6 +95,12 @@ struct GParams {
   CUtensorMap mapA;  // 4-D {C, W, H, images}: the NHWC input (box {32, win_w, bh + k - 1, 1})
   CUtensorMap mapB;  // 3-D {Kp, nmma, J}: the weight copy (box {32, nmma, 1})
   int kk, cbn, flipB;        // kernel size, 32-channel blocks, weight atoms in flipped (ky, kx) order
+  // kx fold (slab width divides 32, k * nmma <= 256): the k weight atoms of a kernel row are one B tile of
+  // k * nmma rows, so a tile issues k instead of k * k MMA groups, D2[r][(kx, n)] = sum_(ky, c) slab[r + ky W][c]
+  // B[(ky, kx)][n][c], and the epilogue forms out[r][n] = sum_kx D2[r + kx][(kx, n)] with warp shuffles (a
+  // slab line never straddles a warp, and valid outputs have x + kx inside the line).  The MMAs at small N
+  // are bound by their 128-row A reads, so this is k times fewer of them.
+  int fold;
   int win_w, bh, ybl;        // slab width (pixels), output rows per tile, tiles per image
   int out_h, out_w, slab_rows, imgs_pp, mimg;
   // weight gradient from TMA (DIRECT + kEpiConvDw): K = (image, q) over flattened channel-major planes
@@ -514,7 +520,16 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
             cwait(&full[s], ph);
             tc_fence_after();
             const uint32_t st = smem_u32(smem + (size_t)s * stage_bytes);
-            if (!(p.dbg & 4))
+            if (p.dbg & 4) {
+            } else if (p.fold) {
+              const uint32_t idf = idesc_tf32(p.kk * p.nmma, kCBM);
+              for (int ky = 0; ky < p.kk; ++ky) {
+                const uint64_t ad = smem_desc_row(st + (uint32_t)(ky * p.win_w) * 128);
+                const uint64_t bd = smem_desc_row(st + slab_bytes + (uint32_t)(ky * p.kk) * b_bytes);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) tc_mma<0>(d, ad + 2 * k, bd + 2 * k, idf, (cb | ky | k) != 0);
+              }
+            } else
               for (int a = 0; a < p.kk * p.kk; ++a) {
                 const int ky = a / p.kk, kx = a - ky * p.kk;
                 const uint64_t ad = smem_desc_row(st + (uint32_t)(ky * p.win_w + kx) * 128);
@@ -587,6 +602,14 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
       for (int ch = ch_lo; ch < ch_hi; ++ch) {
         float v[16];
         tmem_ld16(taddr + ch * 16, v);
+        if (DIRECT && !DWT && p.fold) {  // out[r] = sum_kx D2[r + kx][(kx, .)]: every lane takes part in the shuffles
+          for (int kx = 1; kx < p.kk; ++kx) {
+            float u[16];
+            tmem_ld16(taddr + (kx * nch + ch) * 16, u);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] += __shfl_down_sync(0xffffffffu, u[q], kx);
+          }
+        }
         int n0 = ch * 16;
         if (!DIRECT && nb > 1) {  // batched unit: this chunk's particle and its column within the particle
           const int jb = n0 / p.nmma_p;
@@ -1162,6 +1185,11 @@ bool setup_direct(GParams& p, const float* in, int64_t cap, int H, int W, int C,
   p.mimg = (int)mc;
   const size_t stage = (size_t)p.slab_rows * 128 + (size_t)k * k * p.nmma * 128;
   if (2 * stage + 2048 > 227 * 1024) return false;
+  static const bool fold_ok = [] {
+    const char* e = std::getenv("DASMC_CONV_FOLD");  // 0: one MMA group per tap (A/B, tests)
+    return !(e && e[0] == '0');
+  }();
+  p.fold = fold_ok && k > 1 && 32 % W == 0 && k * p.nmma <= 256 ? 1 : 0;
   const uint64_t da[4] = {(uint64_t)C, (uint64_t)W, (uint64_t)H, (uint64_t)J * cap};
   const uint64_t sa[3] = {(uint64_t)C * 4, (uint64_t)W * C * 4, (uint64_t)H * W * C * 4};
   const uint32_t ba[4] = {(uint32_t)kCBK, (uint32_t)W, (uint32_t)(p.bh + k - 1), 1};
@@ -1222,7 +1250,7 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
   p.stages = stages;
   const size_t smem = 1024 + stages * stage_bytes + (3 * stages + 4) * 8 + 16;
   int tc = 32;
-  while (tc < p.nmma) tc <<= 1;
+  while (tc < (direct && EPI != kEpiConvDw && p.fold ? p.kk * p.nmma : p.nmma)) tc <<= 1;
   p.tcols_half = tc;
   static const int dbg = [] {
     const char* e = std::getenv("DASMC_CONV_DBG");
