@@ -101,6 +101,10 @@ struct GParams {
   // slab line never straddles a warp, and valid outputs have x + kx inside the line).  The MMAs at small N
   // are bound by their 128-row A reads, so this is k times fewer of them.
   int fold;
+  // resident weights (direct forward / delta): the k * k * cbn weight atoms of a particle stay in shared
+  // memory while the CTA works through a contiguous range of that particle's tiles (they were re-loaded per
+  // tile, most of the L2 -> SM bytes); the pipeline stages then hold input slabs only
+  int persist;
   int win_w, bh, ybl;        // slab width (pixels), output rows per tile, tiles per image
   int out_h, out_w, slab_rows, imgs_pp, mimg;
   // weight gradient from TMA (DIRECT + kEpiConvDw): K = (image, q) over flattened channel-major planes
@@ -292,15 +296,22 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
   constexpr bool DWT = DIRECT && EPI == kEpiConvDw;  // weight gradient from TMA
   const uint32_t slab_bytes = DIRECT && !DWT ? (uint32_t)p.slab_rows * 128 : 0u;
   const uint32_t stage_bytes = DWT      ? a_bytes + b_bytes + (uint32_t)p.stg_bytes           // [A][B][staging]
-                               : DIRECT ? slab_bytes + (uint32_t)(p.kk * p.kk) * b_bytes      // [slab][k*k B atoms]
+                               : DIRECT ? slab_bytes + (p.persist ? 0u : (uint32_t)(p.kk * p.kk) * b_bytes)  // [slab][k*k B atoms]
                                         : (uint32_t)p.nsub * (a_bytes + b_bytes);             // [A atoms][B atoms]
-  uint64_t* full = (uint64_t*)(smem + (size_t)p.stages * stage_bytes);
+  const bool PERS = DIRECT && !DWT && p.persist;
+  uint8_t* wres = smem + (size_t)p.stages * stage_bytes;  // resident weight atoms [cb][ky * k + kx]
+  const uint32_t wres_bytes = PERS ? (uint32_t)(p.cbn * p.kk * p.kk) * b_bytes : 0u;
+  uint64_t* full = (uint64_t*)(wres + wres_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
   uint64_t* sfull = tempty + 2;  // DWT: the staging tile of a stage has landed
   uint32_t* tmem_holder = (uint32_t*)(sfull + p.stages);
   const int nb = DIRECT ? 1 : p.nb;  // particles per unit
+  // resident weights: CTA b takes the contiguous tiles [u0, u1) (a particle's tiles are consecutive)
+  const int pu = PERS ? p.J * p.mimg * p.ybl : 0;
+  const int u0 = PERS ? (int)((int64_t)pu * blockIdx.x / gridDim.x) : 0;
+  const int u1 = PERS ? (int)((int64_t)pu * (blockIdx.x + 1) / gridDim.x) : 0;
   const int units = DIRECT && !DWT ? p.J * p.mimg * p.ybl : p.rtiles * ((p.J + nb - 1) / nb);
 
   if (threadIdx.x == 0) {
@@ -409,20 +420,44 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
     if (warp == 0 && lane == 0) {
       prefetch_map(&p.mapA);
       prefetch_map(&p.mapB);
-      const uint32_t tx = (uint32_t)(p.bh + p.kk - 1) * p.win_w * 128 + (uint32_t)(p.kk * p.kk) * b_bytes;
-      int s = 0;
+      const uint32_t txs = (uint32_t)(p.bh + p.kk - 1) * p.win_w * 128;
+      const uint32_t tx = txs + (PERS ? 0u : (uint32_t)(p.kk * p.kk) * b_bytes);
+      int s = 0, jres = -1;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < units; t += gridDim.x) {
+      for (int t = PERS ? u0 : (int)blockIdx.x; t < (PERS ? u1 : units); t += PERS ? 1 : (int)gridDim.x) {
         const int yb = t % p.ybl, m = (t / p.ybl) % p.mimg, j = t / (p.ybl * p.mimg);
+        if (PERS && j != jres) {
+          // a new particle: every MMA issued so far has completed once each stage is free again; then its
+          // weight atoms replace the previous particle's (sfull[0] completes when they have landed)
+          if (jres >= 0) {
+            int s2 = s;
+            uint32_t ph2 = ph;
+            for (int i = 0; i < p.stages; ++i) {
+              cwait(&empty[s2], ph2 ^ 1);
+              if (++s2 == p.stages) {
+                s2 = 0;
+                ph2 ^= 1;
+              }
+            }
+          }
+          jres = j;
+          mbar_expect_tx(&sfull[0], wres_bytes);
+          for (int cb = 0; cb < p.cbn; ++cb)
+            for (int a = 0; a < p.kk * p.kk; ++a) {
+              const int src = p.flipB ? p.kk * p.kk - 1 - a : a;
+              tma_3d(wres + (size_t)(cb * p.kk * p.kk + a) * b_bytes, &p.mapB, &sfull[0], (src * p.cbn + cb) * kCBK, 0, j);
+            }
+        }
         for (int cb = 0; cb < p.cbn; ++cb) {
           cwait(&empty[s], ph ^ 1);
           uint8_t* st = smem + (size_t)s * stage_bytes;
           mbar_expect_tx(&full[s], tx);
           tma_4d(st, &p.mapA, &full[s], cb * kCBK, 0, yb * p.bh, j * p.imgs_pp + m);
-          for (int a = 0; a < p.kk * p.kk; ++a) {
-            const int src = p.flipB ? p.kk * p.kk - 1 - a : a;  // delta: W'[ky'][kx'] = W[k-1-ky'][k-1-kx']
-            tma_3d(st + slab_bytes + a * b_bytes, &p.mapB, &full[s], (src * p.cbn + cb) * kCBK, 0, j);
-          }
+          if (!PERS)
+            for (int a = 0; a < p.kk * p.kk; ++a) {
+              const int src = p.flipB ? p.kk * p.kk - 1 - a : a;  // delta: W'[ky'][kx'] = W[k-1-ky'][k-1-kx']
+              tma_3d(st + slab_bytes + a * b_bytes, &p.mapB, &full[s], (src * p.cbn + cb) * kCBK, 0, j);
+            }
           if (++s == p.stages) {
             s = 0;
             ph ^= 1;
@@ -511,21 +546,33 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
       const uint32_t idesc = idesc_tf32(p.nmma, kCBM);
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
-      for (int t = blockIdx.x; t < units; t += gridDim.x) {
+      int jres = -1;
+      uint32_t wph = 0;
+      for (int t = PERS ? u0 : (int)blockIdx.x; t < (PERS ? u1 : units); t += PERS ? 1 : (int)gridDim.x) {
         cwait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * p.tcols_half);
         if (DIRECT && !DWT) {
+          if (PERS) {
+            const int j = t / (p.ybl * p.mimg);
+            if (j != jres) {  // this particle's weight atoms have landed
+              jres = j;
+              cwait(&sfull[0], wph);
+              wph ^= 1;
+            }
+          }
           for (int cb = 0; cb < p.cbn; ++cb) {
             cwait(&full[s], ph);
             tc_fence_after();
             const uint32_t st = smem_u32(smem + (size_t)s * stage_bytes);
+            // weight atoms of this channel block: resident, or behind the stage's slab
+            const uint32_t wat = PERS ? smem_u32(wres) + (uint32_t)(cb * p.kk * p.kk) * b_bytes : st + slab_bytes;
             if (p.dbg & 4) {
             } else if (p.fold) {
               const uint32_t idf = idesc_tf32(p.kk * p.nmma, kCBM);
               for (int ky = 0; ky < p.kk; ++ky) {
                 const uint64_t ad = smem_desc_row(st + (uint32_t)(ky * p.win_w) * 128);
-                const uint64_t bd = smem_desc_row(st + slab_bytes + (uint32_t)(ky * p.kk) * b_bytes);
+                const uint64_t bd = smem_desc_row(wat + (uint32_t)(ky * p.kk) * b_bytes);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) tc_mma<0>(d, ad + 2 * k, bd + 2 * k, idf, (cb | ky | k) != 0);
               }
@@ -533,7 +580,7 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
               for (int a = 0; a < p.kk * p.kk; ++a) {
                 const int ky = a / p.kk, kx = a - ky * p.kk;
                 const uint64_t ad = smem_desc_row(st + (uint32_t)(ky * p.win_w + kx) * 128);
-                const uint64_t bd = smem_desc_row(st + slab_bytes + (uint32_t)a * b_bytes);
+                const uint64_t bd = smem_desc_row(wat + (uint32_t)a * b_bytes);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) tc_mma<0>(d, ad + 2 * k, bd + 2 * k, idesc, (cb | a | k) != 0);
               }
@@ -581,7 +628,7 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
     const int row_in_tile = lg * 32 + lane;
     int acc = 0;
     uint32_t aph = 0;
-    for (int t = blockIdx.x; t < units; t += gridDim.x) {
+    for (int t = PERS ? u0 : (int)blockIdx.x; t < (PERS ? u1 : units); t += PERS ? 1 : (int)gridDim.x) {
       int j, r;
       bool rv = true;  // the row is an output of this tile
       if (DIRECT && !DWT) {  // slab row -> output pixel (y, x) of image m; wide rows (x >= out_w) are dropped
@@ -1210,7 +1257,7 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
   if (p.nmma > 256) throw std::invalid_argument("conv: MMA N > 256");
   if (!p.b.vec && !direct) throw std::invalid_argument("conv: B operands are 16-byte gathers");
   const size_t fixed = 1024 + 64 * 8 + 64;
-  size_t stage_bytes;
+  size_t stage_bytes, wres = 0;  // wres: resident weight atoms (direct kernels)
   int stages;
   if (direct && EPI == kEpiConvDw) {
     p.nsub = 1;
@@ -1218,8 +1265,15 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
     stages = (int)std::min<size_t>(8, (227 * 1024 - fixed) / stage_bytes);
   } else if (direct) {
     p.nsub = 1;
-    stage_bytes = (size_t)p.slab_rows * 128 + (size_t)p.kk * p.kk * p.nmma * 128;
-    stages = (int)std::min<size_t>(4, (227 * 1024 - fixed) / stage_bytes);
+    const size_t slab = (size_t)p.slab_rows * 128, watoms = (size_t)p.kk * p.kk * p.nmma * 128;
+    static const bool persist_ok = [] {
+      const char* e = std::getenv("DASMC_CONV_PERSIST");  // 0: weight atoms re-loaded with every tile (A/B, tests)
+      return !(e && e[0] == '0');
+    }();
+    wres = persist_ok && (size_t)p.cbn * watoms + 3 * slab + fixed <= 227 * 1024 ? (size_t)p.cbn * watoms : 0;
+    p.persist = wres ? 1 : 0;
+    stage_bytes = wres ? slab : slab + watoms;
+    stages = (int)std::min<size_t>(wres ? 6 : 4, (227 * 1024 - fixed - wres) / stage_bytes);
   } else {
     // Atoms per stage: several 32-wide k atoms per pipeline hand-off (the producer -> MMA ->
     // producer round trip costs hundreds of cycles; conv tiles have few k atoms), a divisor of
@@ -1248,7 +1302,7 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
   }
   if (stages < 2) throw std::invalid_argument("conv: GEMM tile does not fit in shared memory");
   p.stages = stages;
-  const size_t smem = 1024 + stages * stage_bytes + (3 * stages + 4) * 8 + 16;
+  const size_t smem = 1024 + stages * stage_bytes + wres + (3 * stages + 4) * 8 + 16;
   int tc = 32;
   while (tc < (direct && EPI != kEpiConvDw && p.fold ? p.kk * p.nmma : p.nmma)) tc <<= 1;
   p.tcols_half = tc;
