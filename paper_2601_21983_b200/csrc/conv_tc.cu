@@ -643,6 +643,26 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
         r = rt * kCBM + row_in_tile;
       }
       const int j_unit = j;
+      // Row offsets (table lookups) and the first chunk's act' mask are loaded BEFORE the accumulator wait:
+      // their global-memory latency then overlaps the tile's MMAs instead of sitting between the TMEM load
+      // and the stores (the delta epilogue was the longer half of its kernel, ncu / DASMC_CONV_DBG=2)
+      int64_t off1 = 0;
+      int off2 = 0;
+      float4 mk[4];
+      bool mk_ok = false;
+      if ((EPI == kEpiConvFwd || EPI == kEpiConvDx) && rv && r < p.Rvalid) {
+        off1 = p.outoff ? (int64_t)p.outoff[r] : (int64_t)r * p.out_ld;
+        if (p.out2) off2 = p.out2off[r];
+        if (EPI == kEpiConvDx && p.mask && ch_lo < ch_hi && (p.mask_ld & 3) == 0 && p.nvalid - ch_lo * 16 >= 16) {
+          const float4* m4 =
+              reinterpret_cast<const float4*>(p.mask + (int64_t)j * p.mask_ps + (int64_t)r * p.mask_ld + ch_lo * 16);
+          if ((reinterpret_cast<uintptr_t>(m4) & 15) == 0) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) mk[u] = __ldg(m4 + u);
+            mk_ok = true;
+          }
+        }
+      }
       cwait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t)(acc * p.tcols_half) + ((uint32_t)(lg * 32) << 16);
@@ -669,7 +689,7 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
         if (p.dbg & 2) continue;
         if (EPI == kEpiConvFwd || EPI == kEpiConvDx) {
           if (!rv || r >= p.Rvalid) continue;
-          float* dst = p.out + (int64_t)j * p.out_ps + (p.outoff ? (int64_t)p.outoff[r] : (int64_t)r * p.out_ld) + n0;
+          float* dst = p.out + (int64_t)j * p.out_ps + off1 + n0;
           if (EPI == kEpiConvFwd) {
             const float* b = p.theta + (int64_t)j * p.Dp + p.boff + n0;
 #pragma unroll
@@ -679,7 +699,14 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
                 v[q] = tf32_hi(ACT == DASMC_RELU ? fmaxf(z, 0.f) : tanhf(z));
               }
           } else {
-            if (p.mask) {
+            if (p.mask && mk_ok && ch == ch_lo) {
+              const float* a16 = reinterpret_cast<const float*>(mk);
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                const float a = a16[q];
+                v[q] *= ACT == DASMC_RELU ? (a > 0.f ? 1.f : 0.f) : 1.f - a * a;
+              }
+            } else if (p.mask) {
               const float* m = p.mask + (int64_t)j * p.mask_ps + (int64_t)r * p.mask_ld + n0;
 #pragma unroll
               for (int q = 0; q < 16; ++q)
@@ -702,7 +729,7 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
               if (q < nq) dst[q] = v[q];
           }
           if (p.out2) {  // lanes are consecutive pixels: each (channel, kx) store is coalesced
-            float* d2 = p.out2 + (int64_t)j * p.out2_ps + p.out2off[r] + (int64_t)n0 * p.out2_cs;
+            float* d2 = p.out2 + (int64_t)j * p.out2_ps + off2 + (int64_t)n0 * p.out2_cs;
             for (int kx = 0; kx < p.out2_k; ++kx) {
 #pragma unroll
               for (int q = 0; q < 16; ++q)
