@@ -82,6 +82,11 @@ struct GParams {
   GOperand a, b;
   const float* ones;  // 16 bytes of 1.0f (the source of kOnesRow elements)
   int J, rtiles, nkb, nmma, tcols_half, stages;
+  // TMEM accumulators in flight (2, 4 or 8; nacc * tcols_half <= 512 / CTAs per SM).  A tile's hand-offs
+  // (commit -> epilogue wake-up -> tcgen05.ld -> stores -> arrive -> issuer wake-up) take a few thousand
+  // cycles, and these short-K tiles spend less than that in their MMAs: with two accumulators the round trip,
+  // not the work, set the time per tile
+  int nacc;
   int nsub;  // 128B-swizzle k atoms (32 tf32 each) per pipeline stage: nkb stages cover nkb * nsub atoms
   // particle batching (gather kernels whose A operand is shared by every particle: the stage-0 forward
   // over the im2col of X and the stage-0 weight gradient over its transpose): a unit covers nb
@@ -101,6 +106,7 @@ struct GParams {
   // slab line never straddles a warp, and valid outputs have x + kx inside the line).  The MMAs at small N
   // are bound by their 128-row A reads, so this is k times fewer of them.
   int fold;
+  int ksteps;  // MMA k-steps (8 channels each) per tap and channel block: < 4 when the block's upper channels are padding
   // resident weights (direct forward / delta): the k * k * cbn weight atoms of a particle stay in shared
   // memory while the CTA works through a contiguous range of that particle's tiles (they were re-loaded per
   // tile, most of the L2 -> SM bytes); the pipeline stages then hold input slabs only
@@ -262,6 +268,31 @@ __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefe
 #ifndef DASMC_CONV_SPIN
 #define DASMC_CONV_SPIN 1
 #endif
+// epilogue warps back off between polls (8 spinning warps otherwise take issue slots from the lone
+// MMA-issuing thread on their scheduler; DASMC_CONV_BACKOFF=0 for A/B)
+#ifndef DASMC_CONV_BACKOFF
+#define DASMC_CONV_BACKOFF 1
+#endif
+__device__ __forceinline__ void cwait_epi(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  const long long t0 = clock64();
+  for (uint32_t i = 0;; ++i) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.b32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+#if DASMC_CONV_BACKOFF
+    __nanosleep(64);
+#endif
+    if ((i & 0xFFFFu) == 0xFFFFu && clock64() - t0 > 20000000000LL) __trap();  // watchdog (~10 s)
+  }
+}
 __device__ __forceinline__ void cwait(uint64_t* bar, uint32_t parity) {
 #if DASMC_CONV_SPIN
   uint32_t ok = 0;
@@ -304,8 +335,9 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
   uint64_t* full = (uint64_t*)(wres + wres_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* sfull = tempty + 2;  // DWT: the staging tile of a stage has landed
+  constexpr int kMaxAcc = 8;
+  uint64_t* tempty = tfull + kMaxAcc;
+  uint64_t* sfull = tempty + kMaxAcc;  // DWT: the staging tile of a stage has landed
   uint32_t* tmem_holder = (uint32_t*)(sfull + p.stages);
   const int nb = DIRECT ? 1 : p.nb;  // particles per unit
   // resident weights: CTA b takes the contiguous tiles [u0, u1) (a particle's tiles are consecutive)
@@ -321,7 +353,7 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
       mbar_init(&empty[s], 1);
       mbar_init(&sfull[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kMaxAcc; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], EW);
     }
@@ -329,7 +361,7 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
   }
   if (warp == PW) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(2 * p.tcols_half)
+                 "r"(p.nacc * p.tcols_half)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -567,23 +599,40 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
             const uint32_t st = smem_u32(smem + (size_t)s * stage_bytes);
             // weight atoms of this channel block: resident, or behind the stage's slab
             const uint32_t wat = PERS ? smem_u32(wres) + (uint32_t)(cb * p.kk * p.kk) * b_bytes : st + slab_bytes;
-            if (p.dbg & 4) {
-            } else if (p.fold) {
-              const uint32_t idf = idesc_tf32(p.kk * p.nmma, kCBM);
-              for (int ky = 0; ky < p.kk; ++ky) {
-                const uint64_t ad = smem_desc_row(st + (uint32_t)(ky * p.win_w) * 128);
-                const uint64_t bd = smem_desc_row(wat + (uint32_t)(ky * p.kk) * b_bytes);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) tc_mma<0>(d, ad + 2 * k, bd + 2 * k, idf, (cb | ky | k) != 0);
+            // The issuing thread's instruction count bounds these short-K tiles (25 taps x 4 MMAs per 128
+            // pixels at C3), so the per-tap descriptors advance by precomputed increments (descriptor
+            // address fields count 16-byte units; no divisions, no per-MMA predicates past the first)
+            if (!(p.dbg & 4)) {
+              uint64_t ad = smem_desc_row(st), bd = smem_desc_row(wat);
+              const uint32_t idf = p.fold ? idesc_tf32(p.kk * p.nmma, kCBM) : idesc;
+              const uint64_t bstep = (uint64_t)(b_bytes >> 4) * (p.fold ? (uint32_t)p.kk : 1u);
+              const uint64_t ax = p.fold ? (uint64_t)p.win_w * 8 : 8, ay = (uint64_t)(p.win_w - p.kk + 1) * 8;
+              auto group = [&](bool acc0) {
+                tc_mma<0>(d, ad, bd, idf, acc0);
+                if (p.ksteps == 4) {
+                  tc_mma<0>(d, ad + 2, bd + 2, idf, 1);
+                  tc_mma<0>(d, ad + 4, bd + 4, idf, 1);
+                  tc_mma<0>(d, ad + 6, bd + 6, idf, 1);
+                } else {
+                  for (int k = 1; k < p.ksteps; ++k) tc_mma<0>(d, ad + 2 * k, bd + 2 * k, idf, 1);
+                }
+                bd += bstep;
+              };
+              if (p.fold) {
+                for (int ky = 0; ky < p.kk; ++ky) {
+                  group((cb | ky) != 0);
+                  ad += ax;
+                }
+              } else {
+                for (int ky = 0; ky < p.kk; ++ky) {
+                  for (int kx = 0; kx < p.kk; ++kx) {
+                    group((cb | ky | kx) != 0);
+                    ad += ax;
+                  }
+                  ad += ay - ax;
+                }
               }
-            } else
-              for (int a = 0; a < p.kk * p.kk; ++a) {
-                const int ky = a / p.kk, kx = a - ky * p.kk;
-                const uint64_t ad = smem_desc_row(st + (uint32_t)(ky * p.win_w + kx) * 128);
-                const uint64_t bd = smem_desc_row(wat + (uint32_t)a * b_bytes);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) tc_mma<0>(d, ad + 2 * k, bd + 2 * k, idesc, (cb | a | k) != 0);
-              }
+            }
             tc_commit(&empty[s]);
             if (++s == p.stages) {
               s = 0;
@@ -591,8 +640,10 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
             }
           }
           tc_commit(&tfull[acc]);
-          acc ^= 1;
-          if (acc == 0) aph ^= 1;
+          if (++acc == p.nacc) {
+            acc = 0;
+            aph ^= 1;
+          }
           continue;
         }
         for (int kb = 0; kb < p.nkb; ++kb) {
@@ -615,8 +666,10 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
           }
         }
         tc_commit(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) aph ^= 1;
+        if (++acc == p.nacc) {
+          acc = 0;
+          aph ^= 1;
+        }
       }
     }
   } else {
@@ -663,7 +716,7 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
           }
         }
       }
-      cwait(&tfull[acc], aph);
+      cwait_epi(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t)(acc * p.tcols_half) + ((uint32_t)(lg * 32) << 16);
       for (int ch = ch_lo; ch < ch_hi; ++ch) {
@@ -757,14 +810,16 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[acc]));
-      acc ^= 1;
-      if (acc == 0) aph ^= 1;
+      if (++acc == p.nacc) {
+        acc = 0;
+        aph ^= 1;
+      }
     }
   }
   __syncthreads();
   if (warp == PW) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * p.tcols_half)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.nacc * p.tcols_half)
                  : "memory");
   }
 }
@@ -773,7 +828,8 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
 // W copies for the forward (Wf[j][n][kk], kk in the stage's k-order) and delta (Wd[j][ci][kk],
 // kk = (ky, kx, co)) GEMMs, tf32-rounded, zero padded to [nrows][Kp].
 __global__ void conv_wcopy_kernel(const float* __restrict__ theta, int64_t Dp, int64_t woff, int cin, int k, int cout,
-                                  int mode, int korder, int nrows, int Kp, int64_t J, float* __restrict__ out) {
+                                  int mode, int korder, int nrows, int Kp, int64_t J, float* __restrict__ out,
+                                  int cin_p) {
   const int kk2 = k * k;
   const int64_t per = (int64_t)nrows * Kp, total = J * per;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
@@ -781,8 +837,10 @@ __global__ void conv_wcopy_kernel(const float* __restrict__ theta, int64_t Dp, i
     const int rem = (int)(g - j * per), n = rem / Kp, q = rem - n * Kp;
     float v = 0.f;
     if (mode == 0) {  // forward: row co, column q over (ky, kx, ci) [korder 0] or (ci, ky, kx) [korder 1]
-      if (n < cout && q < cin * kk2) {
-        const int src = korder == 0 ? (q % cin) * kk2 + q / cin : q;
+      // korder 0: q = (ky, kx, ci) with ci < cin_p (the input's channel pitch; zero columns past cin)
+      const int ci = korder == 0 ? q % cin_p : 0, tap = korder == 0 ? q / cin_p : 0;
+      if (n < cout && (korder == 0 ? (tap < kk2 && ci < cin) : q < cin * kk2)) {
+        const int src = korder == 0 ? ci * kk2 + tap : q;
         v = theta[j * Dp + woff + (int64_t)n * cin * kk2 + src];
       }
     } else {  // delta: row ci, column q over (ky, kx, co)
@@ -804,12 +862,13 @@ template <bool P2>
 __global__ void __launch_bounds__(256) pool_fwd_nhwc_kernel(ConvDev d, const float* __restrict__ A, int64_t a_ps,
                                                             float* __restrict__ P, int64_t p_ps, int M, int flat,
                                                             float* __restrict__ T, int64_t t_ps, int t_wp,
-                                                            uint8_t* __restrict__ code, int logC) {
+                                                            uint8_t* __restrict__ code, int logC, int cp) {
+  // cp: channel pitch of the pooled NHWC plane (>= C; padding channels are never written and stay zero)
   const int C = d.cout, per = d.sh * d.sw * C, shsw = d.sh * d.sw;
   const int m = (int)(blockIdx.x % (unsigned)M);  // one image of one particle per block: 32-bit index math inside
   const int64_t j = blockIdx.x / (unsigned)M;
   const float* aimg = A + j * a_ps + (int64_t)m * d.ho * d.wo * C;
-  float* pimg = P + j * p_ps + (int64_t)m * per;
+  float* pimg = P + j * p_ps + (int64_t)m * (flat ? per : shsw * cp);
   uint8_t* cimg = code ? code + (j * M + m) * per : nullptr;
   float* timg = T ? T + j * t_ps + (int64_t)m * C * d.sh * t_wp : nullptr;
   const int rowC = d.wo * C;
@@ -825,7 +884,7 @@ __global__ void __launch_bounds__(256) pool_fwd_nhwc_kernel(ConvDev d, const flo
       if (a2 > v) { v = a2; best = 2; }
       if (a3 > v) { v = a3; best = 3; }
       const int o = py * d.sw * C + i;
-      pimg[flat ? c * shsw + py * d.sw + px : o] = v;
+      pimg[flat ? c * shsw + py * d.sw + px : (py * d.sw + px) * cp + c] = v;
       if (cimg) cimg[o] = (uint8_t)(best | (v > 0.f ? 4 : 0));  // bit 2: relu'(max)
       // the next stage's channel-major, width-padded input copy (its weight-gradient operand)
       if (timg) timg[(c * d.sh + py) * t_wp + px] = v;
@@ -834,16 +893,16 @@ __global__ void __launch_bounds__(256) pool_fwd_nhwc_kernel(ConvDev d, const flo
 }
 
 void launch_pool_fwd(Ctx& c, const ConvDev& d, const float* A, int64_t a_ps, float* P, int64_t p_ps, int64_t M,
-                     int64_t J, int flat, float* T, int64_t t_ps, int t_wp, uint8_t* code) {
+                     int64_t J, int flat, float* T, int64_t t_ps, int t_wp, uint8_t* code, int cp) {
   const bool p2 = (d.cout & (d.cout - 1)) == 0;
   int logC = 0;
   while ((1 << logC) < d.cout) ++logC;
   if (p2)
     pool_fwd_nhwc_kernel<true><<<(unsigned)(J * M), 256, 0, c.stream>>>(d, A, a_ps, P, p_ps, (int)M, flat, T, t_ps, t_wp,
-                                                                        code, logC);
+                                                                        code, logC, cp);
   else
     pool_fwd_nhwc_kernel<false><<<(unsigned)(J * M), 256, 0, c.stream>>>(d, A, a_ps, P, p_ps, (int)M, flat, T, t_ps,
-                                                                         t_wp, code, logC);
+                                                                         t_wp, code, logC, cp);
   LAUNCHED();
 }
 
@@ -1064,6 +1123,11 @@ struct ConvTcState {
   int64_t XcolT_rows = 0;
   bool direct_ok = true;       // DASMC_CONV_DIRECT=0 forces the gather path (A/B, tests)
   bool batch0 = true;          // DASMC_CONV_BATCH0=0: one particle per unit in the stage-0 GEMMs (A/B)
+  // channel pitch of stage i's pooled NHWC output: cout, or 32 when the next stage then qualifies for the
+  // direct convolution (its input needs 32-channel blocks; the padding channels stay zero and the next
+  // stage's weight copy has zero columns for them).  C3: the 16-channel 12x12 input of stage 1 -- gathered
+  // as an implicit im2col, that forward was bound by the L1 gather rate (7.3 ms per launch)
+  int cpd[kMaxConv] = {};
   bool dwt[kMaxConv] = {};     // weight gradient from TMA (flattened, unshifted delta copy: DzL kc = 1)
   int* c2o[kMaxConv] = {};     // input pixel of stage i -> its inT[i] offset (channel 0)
   int* dzo[kMaxConv] = {};     // output pixel of stage i -> its dZs[i] offset (channel 0, kx 0)
@@ -1243,8 +1307,10 @@ CUtensorMap conv_map(const float* base, int rank, const uint64_t* dims, const ui
 // Direct-convolution stage parameters (GParams::mapA ...) for an NHWC input [J][cap][H][W][C]
 // convolved with k x k weights into out_h x out_w outputs; false when the slab ring does not fit.
 bool setup_direct(GParams& p, const float* in, int64_t cap, int H, int W, int C, int k, int out_h, int out_w,
-                  int64_t mc, const float* wcopy, int Kp, int J, bool flip) {
+                  int64_t mc, const float* wcopy, int Kp, int J, bool flip, int c_real = 0) {
   if (C % kCBK != 0 || W > 128) return false;
+  // channels that carry data (c_real < C: a channel-padded input of one block)
+  p.ksteps = c_real > 0 && c_real < C && C == kCBK ? (c_real + 7) / 8 : 4;
   p.kk = k;
   p.cbn = C / kCBK;
   p.flipB = flip ? 1 : 0;
@@ -1257,8 +1323,9 @@ bool setup_direct(GParams& p, const float* in, int64_t cap, int H, int W, int C,
   p.slab_rows = (rows + 7) / 8 * 8;
   p.imgs_pp = (int)cap;
   p.mimg = (int)mc;
-  const size_t stage = (size_t)p.slab_rows * 128 + (size_t)k * k * p.nmma * 128;
-  if (2 * stage + 2048 > 227 * 1024) return false;
+  const size_t slabb = (size_t)p.slab_rows * 128, watoms = (size_t)k * k * p.nmma * 128;
+  // two [slab | atoms] stages, or resident atoms + three slabs (launch_gemm picks the same way)
+  if (2 * (slabb + watoms) + 2048 > 227 * 1024 && (size_t)p.cbn * watoms + 3 * slabb + 4096 > 227 * 1024) return false;
   static const bool fold_ok = [] {
     const char* e = std::getenv("DASMC_CONV_FOLD");  // 0: one MMA group per tap (A/B, tests)
     return !(e && e[0] == '0');
@@ -1297,7 +1364,9 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
       const char* e = std::getenv("DASMC_CONV_PERSIST");  // 0: weight atoms re-loaded with every tile (A/B, tests)
       return !(e && e[0] == '0');
     }();
-    wres = persist_ok && (size_t)p.cbn * watoms + 3 * slab + fixed <= 227 * 1024 ? (size_t)p.cbn * watoms : 0;
+    wres = (persist_ok || 2 * (slab + watoms) + 2048 > 227 * 1024) && (size_t)p.cbn * watoms + 3 * slab + 4096 <= 227 * 1024
+               ? (size_t)p.cbn * watoms
+               : 0;
     p.persist = wres ? 1 : 0;
     stage_bytes = wres ? slab : slab + watoms;
     stages = (int)std::min<size_t>(wres ? 6 : 4, (227 * 1024 - fixed - wres) / stage_bytes);
@@ -1329,7 +1398,7 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
   }
   if (stages < 2) throw std::invalid_argument("conv: GEMM tile does not fit in shared memory");
   p.stages = stages;
-  const size_t smem = 1024 + stages * stage_bytes + wres + (3 * stages + 4) * 8 + 16;
+  const size_t smem = 1024 + stages * stage_bytes + wres + (3 * stages + 16) * 8 + 16;
   int tc = 32;
   while (tc < (direct && EPI != kEpiConvDw && p.fold ? p.kk * p.nmma : p.nmma)) tc <<= 1;
   p.tcols_half = tc;
@@ -1357,6 +1426,9 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     per_sm = std::max(1, std::min(2, per_sm));
     if (2 * tc * per_sm > 512) per_sm = 1;  // TMEM: 512 columns per SM
+    p.nacc = 2;
+    while (p.nacc < 8 && 2 * p.nacc * tc * per_sm <= 512) p.nacc *= 2;
+    if (const char* e = std::getenv("DASMC_CONV_NACC")) p.nacc = std::max(2, std::min(p.nacc, std::atoi(e)));  // A/B
     const int grid = std::max(1, std::min(units, c.ctc->num_sms * per_sm));
     kern<<<grid, NT, smem, c.stream>>>(p);
     LAUNCHED();
@@ -1418,6 +1490,19 @@ void cnn_tc_init(Ctx& c) {
     s->korder[i] = (i > 0 && d.cin % 4 == 0) ? 0 : 1;
     s->nmmaF[i] = round_up(d.cout, 16);
     s->KpF[i] = round_up(d.cin * d.k * d.k, kCBK);
+    s->cpd[i] = d.cout;
+    if (i > 0 && net.conv[i - 1].pool && d.cin < kCBK && d.cin % 4 == 0 && s->korder[i] == 0 && d.win <= 32 &&
+        !(std::getenv("DASMC_CONV_CPAD") && std::getenv("DASMC_CONV_CPAD")[0] == '0') &&
+        !(std::getenv("DASMC_CONV_DIRECT") && std::getenv("DASMC_CONV_DIRECT")[0] == '0')) {
+      // pad the pooled input of this stage to one 32-channel block if its direct convolution then fits
+      const int bh = std::max(1, kCBM / d.win);
+      const size_t slabb = (size_t)round_up(std::max((bh + d.k - 1) * d.win, (d.k - 1) * (d.win + 1) + kCBM), 8) * 128;
+      const size_t watoms = (size_t)d.k * d.k * s->nmmaF[i] * 128;
+      if (2 * (slabb + watoms) + 2048 <= 227 * 1024 || watoms + 3 * slabb + 4096 <= 227 * 1024) {
+        s->cpd[i - 1] = kCBK;
+        s->KpF[i] = d.k * d.k * kCBK;
+      }
+    }
     s->nmmaD[i] = round_up(d.cin, 16);
     s->KpD[i] = round_up(d.cout * d.k * d.k, kCBK);
     s->nmmaW[i] = round_up(d.k * d.cout, 16);
@@ -1516,7 +1601,7 @@ int64_t cnn_tc_image_floats(const Ctx& c) {
     const bool one_copy = c.ctc && (c.ctc->dwt[i] || (i == 0 && c.ctc->xcol0));
     f += (int64_t)(one_copy ? 1 : d.k) * d.cout * d.ho * wp;  // channel-major delta copy (k kx-shifted ones: gather form)
     if (i > 0) f += (int64_t)d.cin * d.hin * wp;     // channel-major input copy
-    if (d.pool) f += pool_plane(d);
+    if (d.pool) f += (int64_t)d.sh * d.sw * (c.ctc ? c.ctc->cpd[i] : d.cout);
     else if (i == net.nconv - 1) f += act_plane(d);  // the flatten copy
     if (d.pool && i + 1 < net.nconv) f += pool_plane(d);
   }
@@ -1550,7 +1635,11 @@ void cnn_tc_alloc(Ctx& c, int64_t mc) {
     }
     if (d.pool) CK(cudaMalloc(&s->pcode[i], J * mc * pool_plane(d)));
     const bool last = i == net.nconv - 1;
-    if (d.pool || last) CK(cudaMalloc(&c.cpool[i], sizeof(float) * J * mc * (d.pool ? pool_plane(d) : act_plane(d))));
+    if (d.pool || last) {
+      const size_t pf = J * mc * (size_t)(d.pool ? (int64_t)d.sh * d.sw * s->cpd[i] : act_plane(d));
+      CK(cudaMalloc(&c.cpool[i], sizeof(float) * pf));
+      if (d.pool && s->cpd[i] != d.cout) CK(cudaMemsetAsync(c.cpool[i], 0, sizeof(float) * pf, c.stream));  // padding channels
+    }
     if (d.pool && !last) CK(cudaMalloc(&s->dP[i], sizeof(float) * J * mc * pool_plane(d)));
     const size_t fa = (size_t)mc * d.cin * d.hin * wp * (i == 0 ? 1 : J);  // stage 0: shared by particles
     DzL& L = s->dzl[i];
@@ -1592,11 +1681,12 @@ void cnn_tc_weights(Ctx& c, const float* theta, int64_t J, bool need_grad) {
   for (int i = 0; i < net.nconv; ++i) {
     const ConvDev& d = net.conv[i];
     conv_wcopy_kernel<<<grid_of(J * s->nmmaF[i] * s->KpF[i]), 256, 0, c.stream>>>(
-        theta, net.Dp, d.woff, d.cin, d.k, d.cout, 0, s->korder[i], s->nmmaF[i], s->KpF[i], J, s->Wf[i]);
+        theta, net.Dp, d.woff, d.cin, d.k, d.cout, 0, s->korder[i], s->nmmaF[i], s->KpF[i], J, s->Wf[i],
+        i > 0 && net.conv[i - 1].pool ? s->cpd[i - 1] : d.cin);
     LAUNCHED();
     if (need_grad && i > 0) {
       conv_wcopy_kernel<<<grid_of(J * s->nmmaD[i] * s->KpD[i]), 256, 0, c.stream>>>(
-          theta, net.Dp, d.woff, d.cin, d.k, d.cout, 1, 0, s->nmmaD[i], s->KpD[i], J, s->Wd[i]);
+          theta, net.Dp, d.woff, d.cin, d.k, d.cout, 1, 0, s->nmmaD[i], s->KpD[i], J, s->Wd[i], d.cin);
       LAUNCHED();
     }
   }
@@ -1621,7 +1711,7 @@ void cnn_tc_forward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t m
     } else {
       const ConvDev& dp = net.conv[i - 1];
       p.a.base = dp.pool ? c.cpool[i - 1] : c.cact[i - 1];
-      p.a.ps = cap * (dp.pool ? pool_plane(dp) : act_plane(dp));
+      p.a.ps = cap * (dp.pool ? (int64_t)dp.sh * dp.sw * s->cpd[i - 1] : act_plane(dp));
       p.a.rowoff = s->fa_row[i];
       p.a.nrows = (int)R;
       p.a.coloff = s->fa_col[i];
@@ -1672,14 +1762,17 @@ void cnn_tc_forward(Ctx& c, const float* theta, int64_t J, int64_t m0, int64_t m
     bool direct = false;
     if (i > 0 && s->direct_ok) {
       const ConvDev& dp = net.conv[i - 1];
-      direct = setup_direct(p, p.a.base, cap, d.hin, d.win, d.cin, d.k, d.ho, d.wo, mc, s->Wf[i], s->KpF[i], (int)J,
-                            false);
+      direct = setup_direct(p, p.a.base, cap, d.hin, d.win, dp.pool ? s->cpd[i - 1] : d.cin, d.k, d.ho, d.wo, mc,
+                            s->Wf[i], s->KpF[i], (int)J, false, d.cin);
+      if (!direct && dp.pool && s->cpd[i - 1] != dp.cout)
+        throw std::invalid_argument("conv: channel-padded input without a direct convolution");
       (void)dp;
     }
     launch_gemm<kEpiConvFwd>(c, p, net.act, direct);
     if (d.pool) {
-      launch_pool_fwd(c, d, c.cact[i], cap * act_plane(d), c.cpool[i], cap * pool_plane(d), mc, J, last ? 1 : 0,
-                      last ? nullptr : s->inT[i + 1], nxt_ps, last ? 0 : s->winp[i + 1], s->pcode[i]);
+      launch_pool_fwd(c, d, c.cact[i], cap * act_plane(d), c.cpool[i],
+                      cap * (last ? pool_plane(d) : (int64_t)d.sh * d.sw * s->cpd[i]), mc, J, last ? 1 : 0,
+                      last ? nullptr : s->inT[i + 1], nxt_ps, last ? 0 : s->winp[i + 1], s->pcode[i], last ? d.cout : s->cpd[i]);
     } else if (last) {
       nhwc_to_flat_kernel<<<grid_of(J * mc * act_plane(d)), 256, 0, c.stream>>>(d, c.cact[i], cap * act_plane(d),
                                                                                  c.cpool[i], cap * act_plane(d), mc, J);
