@@ -111,7 +111,13 @@ struct GParams {
   // memory while the CTA works through a contiguous range of that particle's tiles (they were re-loaded per
   // tile, most of the L2 -> SM bytes); the pipeline stages then hold input slabs only
   int persist;
-  int win_w, bh, ybl;        // slab width (pixels), output rows per tile, tiles per image
+  int win_w, bh, ybl;        // slab line pitch (pixels), output rows per tile, tiles per image
+  // tma_w < win_w: the input is tma_w pixels wide and each slab line is loaded by its own TMA box into a
+  // line pitch of win_w = 16 or 32 pixels (the pad pixels are never written and only feed dropped outputs).
+  // A pitch that divides 32 makes the kx fold possible and keeps every A matrix start on an 8-row boundary:
+  // at unaligned starts (row offset ky * W + kx) the same MMAs measured ~3x slower (C3 stage-1 forward,
+  // N = 32: ~100 cycles per MMA against ~34 for the aligned N = 80 ones of the folded delta GEMM)
+  int tma_w;
   int out_h, out_w, slab_rows, imgs_pp, mimg;
   // weight gradient from TMA (DIRECT + kEpiConvDw): K = (image, q) over flattened channel-major planes
   // of row stride win_p; A rows (ky, ci) are boxes of inT at q + ky * win_p (16-byte aligned: win_p is a
@@ -452,7 +458,7 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
     if (warp == 0 && lane == 0) {
       prefetch_map(&p.mapA);
       prefetch_map(&p.mapB);
-      const uint32_t txs = (uint32_t)(p.bh + p.kk - 1) * p.win_w * 128;
+      const uint32_t txs = (uint32_t)(p.bh + p.kk - 1) * p.tma_w * 128;
       const uint32_t tx = txs + (PERS ? 0u : (uint32_t)(p.kk * p.kk) * b_bytes);
       int s = 0, jres = -1;
       uint32_t ph = 0;
@@ -484,7 +490,12 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
           cwait(&empty[s], ph ^ 1);
           uint8_t* st = smem + (size_t)s * stage_bytes;
           mbar_expect_tx(&full[s], tx);
-          tma_4d(st, &p.mapA, &full[s], cb * kCBK, 0, yb * p.bh, j * p.imgs_pp + m);
+          if (p.tma_w == p.win_w) {
+            tma_4d(st, &p.mapA, &full[s], cb * kCBK, 0, yb * p.bh, j * p.imgs_pp + m);
+          } else {  // one box per slab line, into the padded line pitch
+            for (int ln = 0; ln < p.bh + p.kk - 1; ++ln)
+              tma_4d(st + (size_t)ln * p.win_w * 128, &p.mapA, &full[s], cb * kCBK, 0, yb * p.bh + ln, j * p.imgs_pp + m);
+          }
           if (!PERS)
             for (int a = 0; a < p.kk * p.kk; ++a) {
               const int src = p.flipB ? p.kk * p.kk - 1 - a : a;  // delta: W'[ky'][kx'] = W[k-1-ky'][k-1-kx']
@@ -1314,7 +1325,16 @@ bool setup_direct(GParams& p, const float* in, int64_t cap, int H, int W, int C,
   p.kk = k;
   p.cbn = C / kCBK;
   p.flipB = flip ? 1 : 0;
-  p.win_w = W;
+  static const bool fold_ok = [] {
+    const char* e = std::getenv("DASMC_CONV_FOLD");  // 0: one MMA group per tap, unpadded slab lines (A/B, tests)
+    return !(e && e[0] == '0');
+  }();
+  // line pitch: the next of 16 / 32 when the fold applies (then also every A start is 8-row aligned)
+  int Wp = W;
+  if (fold_ok && k > 1 && W <= 32 && k * p.nmma <= 256 && 32 % W != 0) Wp = W <= 16 ? 16 : 32;
+  p.tma_w = W;
+  p.win_w = Wp;
+  W = Wp;
   p.bh = std::max(1, kCBM / W);
   p.ybl = (out_h + p.bh - 1) / p.bh;
   p.out_h = out_h;
@@ -1326,14 +1346,11 @@ bool setup_direct(GParams& p, const float* in, int64_t cap, int H, int W, int C,
   const size_t slabb = (size_t)p.slab_rows * 128, watoms = (size_t)k * k * p.nmma * 128;
   // two [slab | atoms] stages, or resident atoms + three slabs (launch_gemm picks the same way)
   if (2 * (slabb + watoms) + 2048 > 227 * 1024 && (size_t)p.cbn * watoms + 3 * slabb + 4096 > 227 * 1024) return false;
-  static const bool fold_ok = [] {
-    const char* e = std::getenv("DASMC_CONV_FOLD");  // 0: one MMA group per tap (A/B, tests)
-    return !(e && e[0] == '0');
-  }();
   p.fold = fold_ok && k > 1 && 32 % W == 0 && k * p.nmma <= 256 ? 1 : 0;
-  const uint64_t da[4] = {(uint64_t)C, (uint64_t)W, (uint64_t)H, (uint64_t)J * cap};
-  const uint64_t sa[3] = {(uint64_t)C * 4, (uint64_t)W * C * 4, (uint64_t)H * W * C * 4};
-  const uint32_t ba[4] = {(uint32_t)kCBK, (uint32_t)W, (uint32_t)(p.bh + k - 1), 1};
+  const uint64_t Wr = (uint64_t)p.tma_w;  // the input's real width
+  const uint64_t da[4] = {(uint64_t)C, Wr, (uint64_t)H, (uint64_t)J * cap};
+  const uint64_t sa[3] = {(uint64_t)C * 4, Wr * C * 4, (uint64_t)H * Wr * C * 4};
+  const uint32_t ba[4] = {(uint32_t)kCBK, (uint32_t)Wr, p.tma_w == p.win_w ? (uint32_t)(p.bh + k - 1) : 1u, 1};
   p.mapA = conv_map(in, 4, da, sa, ba);
   const uint64_t db[3] = {(uint64_t)Kp, (uint64_t)p.nmma, (uint64_t)J};
   const uint64_t sb[2] = {(uint64_t)Kp * 4, (uint64_t)p.nmma * Kp * 4};
