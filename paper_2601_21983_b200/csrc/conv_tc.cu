@@ -1007,9 +1007,84 @@ __global__ void __launch_bounds__(256) pool_bwd_rows_kernel(ConvDev d, int act, 
   }
 }
 
+// Max-pool backward with one channel-major delta copy S (the TMA weight-gradient form / stage 0) and, for
+// stages >= 1, the zero-bordered NHWC delta: two passes over the pooled elements instead of a transposition
+// through shared memory.  One block per (particle, image).  NHWC pass: channel fastest.  Channel-major pass:
+// thread -> (channel c, pooled column px) with px fastest, so a warp's stores per pooled row are contiguous runs
+// of one channel-major row, and the strided code / delta reads of neighbouring channels share cache lines
+// within the block.  ~4x fewer instructions than the staged kernel, which was issue-bound (ncu: 89-92 %).
+__global__ void __launch_bounds__(256) pool_bwd_cm_kernel(ConvDev d, int act, const float* __restrict__ A, int64_t a_ps,
+                                                          const uint8_t* __restrict__ code,
+                                                          const float* __restrict__ dP, int64_t dp_ps, int flat, int M,
+                                                          float* __restrict__ dZ, int64_t dz_ps,
+                                                          float* __restrict__ S, int64_t s_ps, DzL L) {
+  const int C = d.cout, per = d.sh * d.sw * C, shsw = d.sh * d.sw;
+  const int m = (int)(blockIdx.x % (unsigned)M);
+  const int64_t j = blockIdx.x / (unsigned)M;
+  const uint8_t* cimg = code + (j * M + m) * per;
+  const float* dpimg = dP + j * dp_ps + (int64_t)m * per;
+  const float* aimg = A + j * a_ps + (int64_t)m * d.ho * d.wo * C;
+  float* sb = S + j * s_ps + m * L.s_m;
+  if (dZ) {
+    // the zero-bordered NHWC delta (stages >= 1), channel fastest: every store of a warp is one run of
+    // channels of a pixel row.  The codes and pooled deltas are read again below (cache hits).
+    const int pad = d.k - 1, W2 = d.wo + 2 * pad, H2 = d.ho + 2 * pad;
+    float* z = dZ + j * dz_ps + (int64_t)m * H2 * W2 * C;
+    for (int o = threadIdx.x; o < per; o += 256) {
+      const int pp = o / C, c = o - pp * C, py = pp / d.sw, px = pp - py * d.sw;
+      const int po = flat ? c * shsw + pp : o;
+      const int cd = cimg[o], best = cd & 3;
+      const float gp = dpimg[po];
+      float dact;
+      if (act == DASMC_RELU) {
+        dact = (cd & 4) ? 1.f : 0.f;
+      } else {
+        const float mx = aimg[((2 * py + (best >> 1)) * d.wo + 2 * px + (best & 1)) * C + c];
+        dact = 1.f - mx * mx;
+      }
+      const float v = tf32_hi(gp * dact);
+      float* z0 = z + ((int64_t)(2 * py + pad) * W2 + 2 * px + pad) * C + c;
+      z0[0] = best == 0 ? v : 0.f;
+      z0[C] = best == 1 ? v : 0.f;
+      z0[(int64_t)W2 * C] = best == 2 ? v : 0.f;
+      z0[(int64_t)W2 * C + C] = best == 3 ? v : 0.f;
+    }
+  }
+  for (int i = threadIdx.x; i < C * d.sw; i += 256) {
+    const int c = i / d.sw, px = i - c * d.sw;
+    float* srow = sb + c * L.s_c + 2 * px;
+    for (int py = 0; py < d.sh; ++py) {
+      const int o = (py * d.sw + px) * C + c;
+      const int po = flat ? c * shsw + py * d.sw + px : o;
+      const int cd = cimg[o], best = cd & 3;
+      const float gp = dpimg[po];
+      float dact;
+      if (act == DASMC_RELU) {
+        dact = (cd & 4) ? 1.f : 0.f;
+      } else {
+        const float mx = aimg[((2 * py + (best >> 1)) * d.wo + 2 * px + (best & 1)) * C + c];
+        dact = 1.f - mx * mx;
+      }
+      const float v = tf32_hi(gp * dact);
+      float* r0 = srow + (int64_t)(2 * py) * L.s_y;
+      float* r1 = r0 + L.s_y;
+      r0[0] = best == 0 ? v : 0.f;
+      r0[1] = best == 1 ? v : 0.f;
+      r1[0] = best == 2 ? v : 0.f;
+      r1[1] = best == 3 ? v : 0.f;
+    }
+  }
+}
+
 void launch_pool_bwd(Ctx& c, const ConvDev& d, int act, const float* A, int64_t a_ps, const uint8_t* code,
                      const float* dP, int64_t dp_ps, int flat, float* dZ, int64_t dz_ps, int64_t M, int64_t J, float* S,
                      int64_t s_ps, const DzL& L) {
+  if (L.kc == 1) {  // one channel-major copy (+ the NHWC delta): no staging through shared memory needed
+    pool_bwd_cm_kernel<<<(unsigned)(J * M), 256, 0, c.stream>>>(d, act, A, a_ps, code, dP, dp_ps, flat, (int)M, dZ, dz_ps, S,
+                                                                s_ps, L);
+    LAUNCHED();
+    return;
+  }
   // pooled rows per pass (fewer block-wide barriers per image): what ~kb KB of shared memory hold
   const size_t row_bytes = sizeof(float) * 2 * (size_t)d.wo * (d.cout + 1);
   static const int kb = [] {
