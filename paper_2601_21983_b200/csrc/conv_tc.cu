@@ -1400,7 +1400,7 @@ bool setup_direct(GParams& p, const float* in, int64_t cap, int H, int W, int C,
   p.kk = k;
   p.cbn = C / kCBK;
   p.flipB = flip ? 1 : 0;
-  static const bool fold_ok = [] {
+  const bool fold_ok = [] {  // read per call: the tests toggle it within one process
     const char* e = std::getenv("DASMC_CONV_FOLD");  // 0: one MMA group per tap, unpadded slab lines (A/B, tests)
     return !(e && e[0] == '0');
   }();
@@ -1452,7 +1452,7 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
   } else if (direct) {
     p.nsub = 1;
     const size_t slab = (size_t)p.slab_rows * 128, watoms = (size_t)p.kk * p.kk * p.nmma * 128;
-    static const bool persist_ok = [] {
+    const bool persist_ok = [] {  // read per call: the tests toggle it within one process
       const char* e = std::getenv("DASMC_CONV_PERSIST");  // 0: weight atoms re-loaded with every tile (A/B, tests)
       return !(e && e[0] == '0');
     }();

@@ -183,6 +183,39 @@ def test_stage0_particle_batching_tail(product, oracle, arch, J, monkeypatch):
     assert max(norm_err(g[j], go[i]) for i, j in enumerate(pick)) < GRAD_TC
 
 
+@pytest.mark.parametrize("arch", [C3, C4])
+@pytest.mark.parametrize("switch", ["DASMC_CONV_FOLD", "DASMC_CONV_PERSIST", "DASMC_CONV_CPAD", "DASMC_CONV_DWT",
+                                    "DASMC_CONV_DIRECT"])
+def test_conv_path_switches_agree(product, oracle, arch, switch, monkeypatch):
+    """The tensor-core stages choose among operand-feed forms (conv_tc.cu: kx fold + padded slab lines,
+    resident weights, channel-padded pooled outputs, TMA weight gradients with shared-memory shifts, direct
+    convolutions vs gathers).  Each form switched off must give the same log target (bit-identical: the
+    forward operands and accumulation order per pixel do not change... except where the fold reassociates the
+    sum over kx, so values are compared to 1e-6 relative) and the same gradient to fp32 reassociation, and
+    both must meet the oracle bound."""
+    M, n, J = 24, 32, 3
+    spec, X, y = problem(product, arch, n)
+    D = product.param_count(spec)
+    th = (0.2 * np.random.default_rng(9).standard_normal((J, D))).astype(np.float32).astype(np.float64)
+
+    def run():
+        t = product.GpuEnsembleTarget(spec, X, y, J, precision="tf32")
+        t.set_target(0, M, n, "scaled", 1.0, 1.0)
+        out = t.log_target_with_grad(th)
+        t.close()
+        return out
+
+    v, g = run()
+    monkeypatch.setenv(switch, "0")
+    v0, g0 = run()
+    assert rel(v, v0) < 1e-6
+    assert max(norm_err(g[j], g0[j]) for j in range(J)) < 2e-3
+    vo, go = oracle.value_and_grad(spec.oracle_layers(), 0, X.astype(np.float64), y, (0, M, n), 0, 1.0, 1.0, th)
+    for vv, gg in ((v, g), (v0, g0)):
+        assert rel(vv, vo) < VAL_TC
+        assert max(norm_err(gg[j], go[j]) for j in range(J)) < GRAD_TC
+
+
 def test_c4_full_batch_window(product):
     """BASELINE configs[3]'s full-batch phase: a window of all n = 50000 images (tensor-core
     stages, chunked).  Size-independent checks: finite values and gradients, and additivity of
