@@ -24,6 +24,12 @@ C3 = (((1, 28, 28), [(5, 16, True), (5, 32, True)]), [512, 10], "relu")
 C4 = (((3, 32, 32), [(3, 32, False), (3, 32, True), (3, 64, False), (3, 64, True)]), [1600, 256, 10], "relu")
 # odd sizes (floor pooling), tanh, a last stage without a pool (NHWC <-> flatten permutes)
 ODD = (((2, 11, 11), [(3, 4, True), (2, 8, False)]), [8 * 3 * 3, 6, 3], "tanh")
+# wider input (slab lines padded from 18 / 16 to a pitch of 32 / 16), three stages, a pooled last stage
+WIDE = (((3, 40, 40), [(5, 32, True), (3, 64, False), (3, 32, True)]), [32 * 7 * 7, 10], "relu")
+# narrow channel counts: 8-channel pooled outputs padded to a 32-channel block (one data-carrying k-step),
+# k = 2 kernels, a 12-channel stage (not a multiple of 8: the gather-form weight gradient with kx-shifted
+# copies and the staged pool backward), tanh
+NARROW = (((1, 20, 20), [(3, 8, True), (2, 16, True), (3, 12, False)]), [12 * 2 * 2, 5], "tanh")
 VAL_TC, GRAD_TC = 2e-4, 3e-2
 
 
@@ -46,7 +52,7 @@ def problem(product, arch, n, kind=1):
     return spec, X, y
 
 
-@pytest.mark.parametrize("arch,M,J", [(C3, 40, 3), (C4, 12, 2), (ODD, 50, 4)])
+@pytest.mark.parametrize("arch,M,J", [(C3, 40, 3), (C4, 12, 2), (ODD, 50, 4), (WIDE, 10, 2), (NARROW, 40, 3)])
 def test_cnn_tc_value_and_grad(product, oracle, arch, M, J):
     n = 64
     spec, X, y = problem(product, arch, n)
