@@ -352,6 +352,11 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
   const int u1 = PERS ? (int)((int64_t)pu * (blockIdx.x + 1) / gridDim.x) : 0;
   const int units = DIRECT && !DWT ? p.J * p.mimg * p.ybl : p.rtiles * ((p.J + nb - 1) / nb);
 
+  if (!DIRECT && p.rtiles == 1 && p.a.nrows < kCBM) {  // see the gather producers: A rows past the operand stay zero
+    const uint32_t words = (uint32_t)p.stages * stage_bytes / 16;
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
       // TMA expect_tx (+ one arrival per shifter warp) / one cp.async arrival per producer thread
@@ -518,6 +523,9 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
     uint32_t ph = 0;
     int t = blockIdx.x;
     static_assert(AV, "the gather producers copy 16-byte chunks");
+    // a single row tile with few rows (the stage-0 weight gradient: 26-28 of 128): the rows past the operand
+    // are zeroed once (below, before the first barrier) and never copied again
+    const int a_rows = p.rtiles == 1 ? min(kCBM, (p.a.nrows + 7) & ~7) : kCBM;
     constexpr int MAXS = 4;  // atoms per stage
     int ra[8], rb[16], ran[8], rbn[16], ca[MAXS], cb[MAXS], can[MAXS], cbn[MAXS];
     // B rows a unit may read: its particles that exist (batched units; all rows otherwise)
@@ -559,7 +567,7 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
 #pragma unroll
           for (int u = 0; u < MAXS; ++u)
             if (u < p.nsub) {
-              gather_tile<8, true>(p.a, abase, p.ones, st + u * a_bytes, ra, ca + u, kCBM, warp, lane);
+              gather_tile<8, true>(p.a, abase, p.ones, st + u * a_bytes, ra, ca + u, a_rows, warp, lane);
               gather_tile<16, true>(p.b, bbase, p.ones, st + p.nsub * a_bytes + u * b_bytes, rb, cb + u, p.nmma, warp,
                                     lane);
             }
