@@ -59,10 +59,15 @@ constexpr int kProdWarps = DASMC_CONV_PW;  // gather producers
 // kx-shifted B tiles of a k block from one unshifted staging tile in shared memory) + MMA warp + 8
 // epilogue warps
 constexpr int kShiftWarps = 8;
-template <bool DIRECT, bool DWT = false>
+// FWDG (the gather-mode forward): 4 producers + 8 epilogue warps instead of 8 + 4 -- its tiles are one or a
+// few k blocks feeding up to 256 output columns, and one epilogue warp per scheduler ran its long dependent
+// instruction stream (TMEM load, bias, activation, rounding, 4 + 16 stores per 16 columns) at a fraction of
+// the issue rate; the thread count and so the register budget stay the same
+template <bool DIRECT, bool DWT = false, bool FWDG = false>
 struct ConvWarps {
-  static constexpr int P = DWT ? 1 + kShiftWarps : DIRECT ? 1 : kProdWarps,
-                       E = DIRECT && !DWT ? 8 : DIRECT ? 4 : DASMC_CONV_GEW, T = 32 * (P + 1 + E);
+  static constexpr int P = DWT ? 1 + kShiftWarps : DIRECT ? 1 : FWDG ? kProdWarps / 2 : kProdWarps,
+                       E = DIRECT && !DWT ? 8 : DIRECT ? 4 : FWDG ? 2 * DASMC_CONV_GEW : DASMC_CONV_GEW,
+                       T = 32 * (P + 1 + E);
 };
 constexpr int kOnesRow = -2147483647;  // row table entry: a row of ones (the bias row of dW)
 constexpr int kZeroRow = -2147483647 - 1;
@@ -211,12 +216,12 @@ __device__ __forceinline__ void load_cols(const GOperand& o, int kb, int lane, i
 
 // Row offsets of the tile rows this lane copies (pass p: vector rows (p*4 + warp)*4 + lane/8,
 // scalar rows (p*4 + warp)*8 + lane/4); kZeroRow past the operand's rows or the tile.
-template <int MAXP>
+template <int MAXP, int NPW = kProdWarps>
 __device__ __forceinline__ void load_rows(const GOperand& o, int r0, int nrt, int pt, int lane, int* ro,
                                           int nlim = 0x7fffffff) {
 #pragma unroll
   for (int p = 0; p < MAXP; ++p) {
-    const int rl = o.vec ? (p * kProdWarps + pt) * 4 + (lane >> 3) : (p * kProdWarps + pt) * 8 + (lane >> 2);
+    const int rl = o.vec ? (p * NPW + pt) * 4 + (lane >> 3) : (p * NPW + pt) * 8 + (lane >> 2);
     if (rl >= nlim) {  // rows of particles past the ensemble (a batched unit's tail): zeros
       ro[p] = kZeroRow;
       continue;
@@ -233,7 +238,7 @@ __device__ __forceinline__ void load_rows(const GOperand& o, int r0, int nrt, in
 // offsets.  Vector path: lane -> (row lane / 8, 16-byte chunk lane % 8), a warp stores 4 full
 // rows.  Scalar path: lane -> (row lane / 4, element lane % 4 of a chunk), 8 rows x 16 bytes
 // per instruction; both are bank-conflict free under the 128B swizzle.
-template <int MAXP, bool VEC>
+template <int MAXP, bool VEC, int NPW = kProdWarps>
 __device__ __forceinline__ void gather_tile(const GOperand& o, const float* pbase, const float* ones, uint32_t tile,
                                             const int* roff, const int* coff, int nrt, int pt, int lane) {
   if (VEC) {
@@ -241,7 +246,7 @@ __device__ __forceinline__ void gather_tile(const GOperand& o, const float* pbas
     const int co = coff[0];
 #pragma unroll
     for (int p = 0; p < MAXP; ++p) {
-      const int rl = (p * kProdWarps + pt) * 4 + (lane >> 3);  // row within the tile
+      const int rl = (p * NPW + pt) * 4 + (lane >> 3);  // row within the tile
       if (rl >= nrt) break;
       const int ro = roff[p];
       const bool v = co != kZeroRow && ro != kZeroRow;
@@ -255,7 +260,7 @@ __device__ __forceinline__ void gather_tile(const GOperand& o, const float* pbas
       const int co = coff[VEC ? 0 : c];
 #pragma unroll
       for (int p = 0; p < MAXP; ++p) {
-        const int rl = (p * kProdWarps + pt) * 8 + (lane >> 2);
+        const int rl = (p * NPW + pt) * 8 + (lane >> 2);
         if (rl >= nrt) break;
         const int ro = roff[p];
         const bool v = co != kZeroRow && ro != kZeroRow;
@@ -321,10 +326,11 @@ __device__ __forceinline__ void cwait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
-template <int EPI, int ACT, bool AV, bool DIRECT>
-__global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DASMC_CONV_MINB)
+// EW8: the gather-mode forward with 4 producer + 8 epilogue warps (ConvWarps FWDG)
+template <int EPI, int ACT, bool EW8, bool DIRECT>
+__global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2, EW8 && !DIRECT && EPI == 0>::T), DASMC_CONV_MINB)
     conv_tc_kernel(const __grid_constant__ GParams p) {
-  using CW_ = ConvWarps<DIRECT, DIRECT && EPI == 2>;
+  using CW_ = ConvWarps<DIRECT, DIRECT && EPI == 2, EW8 && !DIRECT && EPI == 0>;
   constexpr int PW = CW_::P, EW = CW_::E;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -360,7 +366,7 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
       // TMA expect_tx (+ one arrival per shifter warp) / one cp.async arrival per producer thread
-      mbar_init(&full[s], DWT ? 1 + kShiftWarps : DIRECT ? 1 : 32 * kProdWarps);
+      mbar_init(&full[s], DWT ? 1 + kShiftWarps : DIRECT ? 1 : 32 * PW);
       mbar_init(&empty[s], 1);
       mbar_init(&sfull[s], 1);
     }
@@ -522,7 +528,6 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
     int s = 0;
     uint32_t ph = 0;
     int t = blockIdx.x;
-    static_assert(AV, "the gather producers copy 16-byte chunks");
     // a single row tile with few rows (the stage-0 weight gradient: 26-28 of 128): the rows past the operand
     // are zeroed once (below, before the first barrier) and never copied again
     const int a_rows = p.rtiles == 1 ? min(kCBM, (p.a.nrows + 7) & ~7) : kCBM;
@@ -531,8 +536,8 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
     // B rows a unit may read: its particles that exist (batched units; all rows otherwise)
     auto blim = [&](int tt) { return nb > 1 ? min(nb, p.J - (tt / p.rtiles) * nb) * p.nmma_p : 0x7fffffff; };
     if (t < units) {
-      load_rows<8>(p.a, (t % p.rtiles) * kCBM, kCBM, warp, lane, ra);
-      load_rows<16>(p.b, 0, p.nmma, warp, lane, rb, blim(t));
+      load_rows<8, PW>(p.a, (t % p.rtiles) * kCBM, kCBM, warp, lane, ra);
+      load_rows<16, PW>(p.b, 0, p.nmma, warp, lane, rb, blim(t));
     }
 #pragma unroll
     for (int u = 0; u < MAXS; ++u)
@@ -544,8 +549,8 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
       const int j = (t / p.rtiles) * nb;  // first particle of the unit
       const int tn = t + gridDim.x;
       if (tn < units) {
-        load_rows<8>(p.a, (tn % p.rtiles) * kCBM, kCBM, warp, lane, ran);
-        load_rows<16>(p.b, 0, p.nmma, warp, lane, rbn, blim(tn));
+        load_rows<8, PW>(p.a, (tn % p.rtiles) * kCBM, kCBM, warp, lane, ran);
+        load_rows<16, PW>(p.b, 0, p.nmma, warp, lane, rbn, blim(tn));
       }
       const float* abase = p.a.base + (int64_t)j * p.a.ps;
       const float* bbase = p.b.base + (int64_t)j * p.b.ps;
@@ -567,8 +572,8 @@ __global__ void __launch_bounds__((ConvWarps<DIRECT, DIRECT && EPI == 2>::T), DA
 #pragma unroll
           for (int u = 0; u < MAXS; ++u)
             if (u < p.nsub) {
-              gather_tile<8, true>(p.a, abase, p.ones, st + u * a_bytes, ra, ca + u, a_rows, warp, lane);
-              gather_tile<16, true>(p.b, bbase, p.ones, st + p.nsub * a_bytes + u * b_bytes, rb, cb + u, p.nmma, warp,
+              gather_tile<8, true, PW>(p.a, abase, p.ones, st + u * a_bytes, ra, ca + u, a_rows, warp, lane);
+              gather_tile<16, true, PW>(p.b, bbase, p.ones, st + p.nsub * a_bytes + u * b_bytes, rb, cb + u, p.nmma, warp,
                                     lane);
             }
         }
@@ -1508,10 +1513,14 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
   }();
   p.dbg = dbg;
   const int units = direct && EPI != kEpiConvDw ? p.J * p.mimg * p.ybl : p.rtiles * ((p.J + p.nb - 1) / p.nb);
-  auto go = [&](auto act_c, auto dir_c) {
+  // gather-mode forward without a second (channel-major) output: 4 producer + 8 epilogue warps (measured on
+  // B200: C3 stage 0, pooled, 5.1 -> 3.5 ms; with the second output, C4 stage 0, 6.7 -> 8.0 ms, so 8 + 4 stays)
+  const bool ew8 = EPI == kEpiConvFwd && !direct && !p.out2;
+  auto go = [&](auto act_c, auto dir_c, auto ew_c) {
     constexpr int A_ = decltype(act_c)::value;
     constexpr bool DI = decltype(dir_c)::value;
-    auto kern = conv_tc_kernel<EPI, A_, true, DI>;
+    constexpr bool E8 = decltype(ew_c)::value && EPI == kEpiConvFwd && !DI;
+    auto kern = conv_tc_kernel<EPI, A_, E8, DI>;
     static bool attr[kMaxDevices] = {};  // one flag per instantiation and device
     const int dv = current_device();
     if (!attr[dv]) {
@@ -1522,7 +1531,7 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
     const int carve = (int)std::min<size_t>(100, (2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     int per_sm = 1;
-    constexpr int NT = ConvWarps<DI, DI && EPI == kEpiConvDw>::T;
+    constexpr int NT = ConvWarps<DI, DI && EPI == kEpiConvDw, E8>::T;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     per_sm = std::max(1, std::min(2, per_sm));
     if (2 * tc * per_sm > 512) per_sm = 1;  // TMEM: 512 columns per SM
@@ -1536,9 +1545,11 @@ void launch_gemm(Ctx& c, GParams& p, int act, bool direct = false) {
   if (!p.a.vec && !direct) throw std::invalid_argument("conv: A operands are 16-byte gathers");
   auto go_av = [&](auto act_c) {
     if (direct)
-      go(act_c, std::true_type{});
+      go(act_c, std::true_type{}, std::false_type{});
+    else if (ew8)
+      go(act_c, std::false_type{}, std::true_type{});
     else
-      go(act_c, std::false_type{});
+      go(act_c, std::false_type{}, std::false_type{});
   };
   if (act == DASMC_RELU)
     go_av(std::integral_constant<int, DASMC_RELU>{});
