@@ -436,29 +436,56 @@ __global__ void normals_kernel(NetDev net, uint64_t root, uint64_t a, uint64_t b
   float* out = dst + j * net.Dp;
   // reference index i -> internal offset, walked incrementally (one division per chunk):
   // layer l, W(r, c) at ref_off + r + c*out -> woff + r*in + c; then the bias block.
+  // The destination is walked as a pointer: + `in` per row of a column, back to the next column's top at
+  // the end of one, then the bias run (no multiplication or 64-bit index arithmetic per normal; the loop is
+  // integer-issue bound).
   int l = 0;
   while (l < net.nseg - 1 && lo >= net.seg[l + 1].ref_off) ++l;
   int64_t t = lo - net.seg[l].ref_off;
   int64_t nw = (int64_t)net.seg[l].in * net.seg[l].out;
-  int64_t r = t < nw ? t % net.seg[l].out : 0, cc = t < nw ? t / net.seg[l].out : 0;
+  int r = t < nw ? (int)(t % net.seg[l].out) : 0;
+  {
+    const int64_t cc = t < nw ? t / net.seg[l].out : 0;
+    out += t < nw ? net.seg[l].woff + (int64_t)r * net.seg[l].in + cc : net.seg[l].boff + (t - nw);
+  }
+  int rem = (int)min((int64_t)0x7fffffff, (t < nw ? nw : nw + net.seg[l].nb) - t);  // elements left in this run
+  bool in_w = t < nw;
   for (int64_t i = lo; i < hi; ++i) {
     const uint64_t x1 = x.next();
     const uint64_t x2 = x.next();
     const float v = scale * normal_from_draws(x1, x2);
-    const LayerDev& ly = net.seg[l];
-    out[t < nw ? ly.woff + r * ly.in + cc : ly.boff + (t - nw)] = v;
+    *out = v;
     sq += (double)v * (double)v;
     // advance to i + 1
-    if (++t < nw) {
-      if (++r == ly.out) {
-        r = 0;
-        ++cc;
+    const LayerDev& ly = net.seg[l];
+    if (--rem > 0) {
+      if (in_w) {
+        if (++r == ly.out) {  // top of the next column
+          r = 0;
+          out -= (int64_t)(ly.out - 1) * ly.in - 1;
+        } else {
+          out += ly.in;
+        }
+      } else {
+        ++out;
       }
-    } else if (t == nw + ly.nb && l + 1 < net.nseg) {
+    } else if (in_w) {  // the weights are done: this layer's bias run
+      in_w = false;
+      rem = ly.nb;
+      out = dst + j * net.Dp + ly.boff;
+      if (rem == 0 && l + 1 < net.nseg) {
+        ++l;
+        in_w = true;
+        r = 0;
+        rem = (int)min((int64_t)0x7fffffff, (int64_t)net.seg[l].in * net.seg[l].out);
+        out = dst + j * net.Dp + net.seg[l].woff;
+      }
+    } else if (l + 1 < net.nseg) {  // next layer's weights
       ++l;
-      t = 0;
-      r = cc = 0;
-      nw = (int64_t)net.seg[l].in * net.seg[l].out;
+      in_w = true;
+      r = 0;
+      rem = (int)min((int64_t)0x7fffffff, (int64_t)net.seg[l].in * net.seg[l].out);
+      out = dst + j * net.Dp + net.seg[l].woff;
     }
   }
   if (sq_part) sq_part[j * nchunks + c] = sq;
