@@ -630,7 +630,9 @@ void create_ctx(Ctx& c, const dasmc_net_desc* net, const float* X, const int32_t
     if (precision != DASMC_PREC_TF32 && precision != DASMC_PREC_TF32H)
       throw InvalidArg("CNN contexts: precision fp32 (CUDA cores) or tf32 (tensor-core convolutions)");
     if (!cnn_tc_eligible(c))
-      throw InvalidArg("tensor-core CNN stages need cout % 4 == 0 (and cin % 4 == 0 after stage 0), <= 256 channels");
+      throw InvalidArg(
+          "tensor-core CNN stages need cout % 4 == 0 (and cin % 4 == 0 after stage 0), cin, cout <= 64 and "
+          "k * cout <= 256 (the weight-gradient GEMM's N); use precision fp32 for other stages");
     cnn_tc_init(c);
   } else if (precision != DASMC_PREC_FP32) {
     if (!tc_layer1_eligible(c))

@@ -1,0 +1,58 @@
+"""Validation aid (not product): random small CNN architectures on the tensor-core path against the fp64
+oracle (value 2e-4 relative, gradient normwise 3e-2: the bounds of tests/test_gpu_cnn_tc.py).
+  python tools/cnn_fuzz.py [n_archs] [seed]"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+import paper_2601_21983_b200 as p  # noqa: E402
+import pyoracle as O  # noqa: E402
+
+n_archs = int(sys.argv[1]) if len(sys.argv) > 1 else 12
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+bad = 0
+for a in range(n_archs):
+    while True:
+        cin, h = int(rng.choice([1, 2, 3])), int(rng.integers(10, 41))
+        w = h if rng.random() < 0.6 else int(rng.integers(10, 41))
+        stages, hh, ww = [], h, w
+        for s in range(int(rng.integers(1, 4))):
+            k = int(rng.choice([2, 3, 5]))
+            co = int(rng.choice([4, 8, 12, 16, 24, 32, 48, 64]))
+            pool = bool(rng.random() < 0.5)
+            hh, ww = hh - k + 1, ww - k + 1
+            if pool:
+                hh, ww = hh // 2, ww // 2
+            stages.append((k, co, pool))
+            if hh < 1 or ww < 1:
+                break
+        if hh >= 1 and ww >= 1 and stages[-1][1] * hh * ww <= 4096:
+            break
+    act = "relu" if rng.random() < 0.7 else "tanh"
+    F = stages[-1][1] * hh * ww
+    head = [F, int(rng.choice([6, 10, 33])), int(rng.choice([3, 10]))] if rng.random() < 0.5 else [F, int(rng.choice([3, 10]))]
+    spec = p.NetSpec(head, act, ((cin, h, w), stages))
+    n, M, J = 24, int(rng.integers(5, 20)), int(rng.integers(1, 4)) + 1
+    X, y = p.make_teacher_data(spec, n, 1, 0, 3 + a, threads=4)
+    D = p.param_count(spec)
+    th = (0.3 * rng.standard_normal((J, D))).astype(np.float32).astype(np.float64)
+    try:
+        t = p.GpuEnsembleTarget(spec, X, y, J, precision="tf32")
+        t.set_target(0, M, n, "scaled", 1.0, 1.0)
+        v, g = t.log_target_with_grad(th)
+        t.close()
+    except ValueError as e:  # outside the tensor-core path's stage limits (k * cout <= 256 ...): not a parity failure
+        print("ARCH", a, (cin, h, w), stages, head, act, "unsupported:", str(e)[:80])
+        continue
+    vo, go = O.value_and_grad(spec.oracle_layers(), 0 if act == "relu" else 1, X.astype(np.float64), y, (0, M, n), 0, 1.0, 1.0, th)
+    rv = float(np.max(np.abs(v - vo) / np.abs(vo)))
+    rg = max(float(np.linalg.norm(g[j] - go[j]) / np.linalg.norm(go[j])) for j in range(J))
+    ok = rv < 2e-4 and rg < 3e-2
+    bad += 0 if ok else 1
+    print("ARCH", a, (cin, h, w), stages, head, act, f"M={M} J={J} value {rv:.1e} grad {rg:.1e}", "ok" if ok else "FAIL")
+print("failures:", bad)
+sys.exit(1 if bad else 0)
